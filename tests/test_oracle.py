@@ -1,0 +1,442 @@
+"""Pinning the CPU oracle (oracle/sgp_oracle.cpp) before it is trusted.
+
+The reference cannot be compiled in this image (Eigen3 absent), so the oracle is
+pinned against every known-answer test the reference ships or specifies:
+  * proj/tests/test_kernels.cpp (kern_* / factor_gram KATs, FD gates),
+  * SPEC.md psi_stats / bound / parallel examples and invariants,
+  * the Gauss-Hermite quadrature oracle (proj/include/sgp/quadrature.hpp:47-116),
+  * the dense-GP oracle (proj/tests/support/oracles.hpp:22-37),
+  * central finite differences (oracles.hpp:50-53, step 1e-5).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+from paper_1410_4984_b200.rng import Rng
+
+
+# ---------------------------------------------------------------------------
+# Rng (common.hpp:45-97): C restatement == Python restatement
+# ---------------------------------------------------------------------------
+def test_rng_python_matches_c(orc):
+    r = Rng(7)
+    py = r.normal_matrix(5, 3)
+    c = orc.rng_normal_matrix(7, 5, 3)
+    assert np.array_equal(py, c)
+    u = Rng(0)
+    assert u.state == 0x9E3779B97F4A7C15
+    assert np.array_equal(np.array([Rng(3).next_uniform() for _ in range(1)]), orc.rng_uniform(3, 1))
+
+
+# ---------------------------------------------------------------------------
+# test_kernels.cpp KATs
+# ---------------------------------------------------------------------------
+def test_kern_cross_hand_values(orc):
+    assert orc.kern_cross([[0.7]], [[0.7]], 2.3, [0.8])[0, 0] == 2.3
+    assert orc.kern_cross([[0.0]], [[1.0]], 1.0, [1.0])[0, 0] == pytest.approx(0.6065306597126334, rel=1e-14)
+    assert abs(orc.kern_cross([[-3.0]], [[4.0]], 1.7, [1e9])[0, 0] - 1.7) < 1e-12
+
+
+def test_kern_cross_symmetry_exact(orc):
+    rng = Rng(11)
+    x = rng.uniform_matrix(5, 2, -2.0, 2.0)
+    z = rng.uniform_matrix(3, 2, -2.0, 2.0)
+    kxz = orc.kern_cross(x, z, 1.3, [0.7, 1.9])
+    kzx = orc.kern_cross(z, x, 1.3, [0.7, 1.9])
+    assert np.max(np.abs(kxz.T - kzx)) == 0.0
+    kxx = orc.kern_cross(x, x, 1.3, [0.7, 1.9])
+    assert np.max(np.abs(np.diag(kxx) - 1.3)) == 0.0
+    assert np.all(kxz > 0) and np.all(kxz <= 1.3)
+
+
+def test_kern_cross_monotone_and_errors(orc):
+    x = (0.3 + 0.1 * np.arange(50)).reshape(50, 1)
+    kx = orc.kern_cross(x, [[0.3]], 1.0, [0.9])[:, 0]
+    assert np.all(np.diff(kx) <= 0)
+    with pytest.raises(ValueError):
+        orc.kern_cross(np.zeros((2, 3)), np.zeros((2, 2)), 1.0, [1.0, 1.0])
+    xb = np.zeros((2, 2))
+    xb[0, 0] = np.nan
+    with pytest.raises(ValueError):
+        orc.kern_cross(xb, np.zeros((2, 2)), 1.0, [1.0, 1.0])
+    with pytest.raises(ValueError):
+        orc.kern_cross(np.zeros((2, 2)), np.zeros((2, 2)), -1.0, [1.0, 1.0])
+
+
+def test_kern_gram_basics(orc):
+    g, _ = orc.kern_gram([[0.4]], 2.0, [1.0], 0.125)
+    assert g.shape == (1, 1) and g[0, 0] == 2.125
+    g, _ = orc.kern_gram([[0.0], [1.0]], 1.0, [1.0], 0.0)
+    assert g[0, 0] == 1.0 and g[1, 1] == 1.0 and g[0, 1] == g[1, 0]
+    assert g[0, 1] == pytest.approx(0.6065306597126334, rel=1e-14)
+    g, dup = orc.kern_gram([[0.5], [0.5]], 1.0, [1.0], 0.0)
+    assert g[0, 1] == 1.0 and dup
+    assert np.max(np.abs(g - g.T)) == 0.0
+    assert np.linalg.eigvalsh(g).min() < 1e-14
+
+
+def test_factor_gram_jitter_escalation(orc):
+    f = orc.factor_gram([[0.5], [0.5]], 1.0, [1.0], 0.0)
+    assert f["jitter"] > 0.0
+    f2 = orc.factor_gram([[0.0], [1.0]], 1.0, [1.0], 1e-6)
+    assert f2["jitter"] == 1e-6
+    assert abs(f2["log_det"] - math.log(np.linalg.det(f2["kmm"]))) < 1e-10
+
+
+def test_kern_grads_zero_and_mirror(orc):
+    rng = Rng(5)
+    x = rng.uniform_matrix(4, 2, -2.0, 2.0)
+    z = rng.uniform_matrix(3, 2, -2.0, 2.0)
+    g = orc.kern_grads(x, z, 1.1, [0.9, 0.9], np.zeros((4, 3)))
+    assert g["d_variance"] == 0.0 and np.all(g["d_lengthscales"] == 0) and np.all(g["d_z"] == 0)
+    g = orc.kern_grads([[0.3, -0.7]], [[0.3, -0.7]], 1.4, [0.8, 0.8], [[0.9]])
+    assert np.max(np.abs(g["d_z"] + g["d_x"])) == 0.0
+
+
+def test_kern_grads_central_fd(orc):
+    """test_kernels.cpp:180-240 with the same Rng(42) draw order."""
+    rng = Rng(42)
+    n, m, q = 3, 2, 2
+    x = rng.uniform_matrix(n, q, -2.0, 2.0)
+    z = rng.uniform_matrix(m, q, -2.0, 2.0)
+    up = rng.uniform_matrix(n, m, -1.0, 1.0)
+    var = 0.5 + 1.5 * rng.next_uniform()
+    ls = np.array([0.5 + 1.5 * rng.next_uniform() for _ in range(q)])
+
+    def loss(xx, zz, vv, ll):
+        return float(np.sum(up * orc.kern_cross(xx, zz, vv, ll)))
+
+    g = orc.kern_grads(x, z, var, ls, up)
+    h = 1e-5
+    fd = (loss(x, z, var + h, ls) - loss(x, z, var - h, ls)) / (2 * h)
+    assert rel_err(g["d_variance"], fd) < 1e-6
+    for j in range(q):
+        lp, lm = ls.copy(), ls.copy()
+        lp[j] += h
+        lm[j] -= h
+        assert rel_err(g["d_lengthscales"][j], (loss(x, z, var, lp) - loss(x, z, var, lm)) / (2 * h)) < 1e-6
+    for i in range(m):
+        for j in range(q):
+            zp, zm = z.copy(), z.copy()
+            zp[i, j] += h
+            zm[i, j] -= h
+            assert rel_err(g["d_z"][i, j], (loss(x, zp, var, ls) - loss(x, zm, var, ls)) / (2 * h)) < 1e-6
+    for i in range(n):
+        for j in range(q):
+            xp, xm = x.copy(), x.copy()
+            xp[i, j] += h
+            xm[i, j] -= h
+            assert rel_err(g["d_x"][i, j], (loss(xp, z, var, ls) - loss(xm, z, var, ls)) / (2 * h)) < 1e-6
+
+
+# ---------------------------------------------------------------------------
+# SPEC.md psi_stats examples
+# ---------------------------------------------------------------------------
+def test_stats_deterministic_single_point(orc):
+    st, _ = orc.sweep_stats(False, [[0.0]], None, [[1.0]], [[0.0]], 1.0, [1.0])
+    assert st.phi == 1.0 and st.psi_y[0, 0] == 1.0 and st.phi_big[0, 0] == 1.0 and st.yy == 1.0
+
+
+def test_stats_deterministic_zero_outputs_and_brute(orc):
+    rng = np.random.default_rng(0)
+    x = rng.uniform(-2, 2, (5, 2))
+    z = rng.uniform(-2, 2, (3, 2))
+    y = rng.normal(size=(5, 2))
+    st, _ = orc.sweep_stats(False, x, None, y, z, 1.3, [0.8, 1.4])
+    knm = orc.kern_cross(x, z, 1.3, [0.8, 1.4])
+    assert np.max(np.abs(st.phi_big - knm.T @ knm)) < 1e-12
+    assert np.max(np.abs(st.psi_y - knm.T @ y)) < 1e-12
+    st0, _ = orc.sweep_stats(False, x, None, np.zeros_like(y), z, 1.3, [0.8, 1.4])
+    assert np.all(st0.psi_y == 0) and st0.yy == 0 and np.array_equal(st0.phi_big, st.phi_big)
+
+
+def test_psi_expected_kats(orc):
+    # psi1 mu=0,S=1,z=0 -> 1/sqrt(2); psi2 -> 1/sqrt(3)
+    assert orc.psi1_expected([[0.0]], [[1.0]], [[0.0]], 1.0, [1.0])[0, 0] == pytest.approx(1 / math.sqrt(2), rel=1e-15)
+    st, _ = orc.sweep_stats(True, [[0.0]], [[1.0]], np.zeros((1, 0)), [[0.0]], 1.0, [1.0])
+    assert st.phi_big[0, 0] == pytest.approx(1 / math.sqrt(3), rel=1e-15)
+    # psi0: N=10, var=2 -> 20
+    st, _ = orc.sweep_stats(True, np.zeros((10, 1)), np.ones((10, 1)), np.zeros((10, 1)), [[0.0]], 2.0, [1.0])
+    assert st.phi == 20.0
+
+
+def _gh_psi(mu, s, z, var, ls, nodes=160):
+    """Tensor-product Gauss-Hermite (quadrature.hpp:47-116) — independent of the closed forms.
+
+    160 nodes: the reference default (50) under-resolves psi2 when l=0.5, S=2 (measured 3.5e-4 at 50,
+    1.9e-7 at 100, 1.7e-13 at 200 nodes against the closed form)."""
+    t, w = np.polynomial.hermite.hermgauss(nodes)
+    q = len(mu)
+    grids = np.meshgrid(*[mu[j] + np.sqrt(2 * s[j]) * t for j in range(q)], indexing="ij")
+    wgrid = np.ones_like(grids[0])
+    for j, wm in enumerate(np.meshgrid(*[w / np.sqrt(np.pi)] * q, indexing="ij")):
+        wgrid = wgrid * wm
+    pts = np.stack([g.ravel() for g in grids], 1)
+    wv = wgrid.ravel()
+    d2 = (((pts[:, None, :] - z[None, :, :]) / ls) ** 2).sum(-1)
+    k = var * np.exp(-0.5 * d2)  # P x M
+    psi1 = wv @ k
+    psi2 = (k * wv[:, None]).T @ k
+    return psi1, psi2
+
+
+@pytest.mark.parametrize("q", [1, 2])
+def test_quadrature_agreement(orc, q):
+    """expected stats match quadrature within rel 1e-6 for Q in {1,2}."""
+    rng = np.random.default_rng(100 + q)
+    for trial in range(10):
+        mu = rng.uniform(-2, 2, q)
+        s = rng.uniform(0.5, 2.0, q)
+        z = rng.uniform(-2, 2, (3, q))
+        var = rng.uniform(0.5, 2.0)
+        ls = rng.uniform(0.5, 2.0, q)
+        p1, p2 = _gh_psi(mu, s, z, var, ls)
+        c1 = orc.psi1_expected(mu[None], s[None], z, var, ls)[0]
+        st, _ = orc.sweep_stats(True, mu[None], s[None], np.zeros((1, 1)), z, var, ls)
+        assert rel_err(c1, p1) < 1e-6
+        assert rel_err(st.phi_big, p2) < 1e-6
+
+
+def test_delta_limit_and_additivity(orc):
+    rng = np.random.default_rng(3)
+    n, q, m, d = 40, 2, 4, 3
+    mu = rng.normal(size=(n, q))
+    y = rng.normal(size=(n, d))
+    z = rng.normal(size=(m, q))
+    ls = [0.8, 1.3]
+    sd, _ = orc.sweep_stats(False, mu, None, y, z, 1.2, ls)
+    se, _ = orc.sweep_stats(True, mu, np.full((n, q), 1e-14), y, z, 1.2, ls)
+    assert rel_err(se.phi_big, sd.phi_big) < 1e-8 and rel_err(se.psi_y, sd.psi_y) < 1e-8
+    s = rng.uniform(0.25, 1.0, (n, q))
+    full, _ = orc.sweep_stats(True, mu, s, y, z, 1.2, ls)
+    a, _ = orc.sweep_stats(True, mu[:17], s[:17], y[:17], z, 1.2, ls)
+    b, _ = orc.sweep_stats(True, mu[17:], s[17:], y[17:], z, 1.2, ls)
+    assert rel_err(a.phi_big + b.phi_big, full.phi_big) < 1e-12
+    assert rel_err(a.psi_y + b.psi_y, full.psi_y) < 1e-12
+    assert np.array_equal(full.phi_big, full.phi_big.T)
+
+
+@pytest.mark.parametrize("expected", [True, False])
+def test_stats_grads_fd(orc, expected):
+    """N=3, M=2, Q=2, D=2, every gradient vs central FD of d_phi*phi+<dPsi,Psi>+<dPhi,Phi>."""
+    rng = np.random.default_rng(11)
+    n, m, q, d = 3, 2, 2, 2
+    mu = rng.uniform(-2, 2, (n, q))
+    s = rng.uniform(0.5, 2, (n, q))
+    y = rng.normal(size=(n, d))
+    z = rng.uniform(-2, 2, (m, q))
+    var = 1.3
+    ls = np.array([0.7, 1.6])
+    dpsi = rng.normal(size=(m, d))
+    a = rng.normal(size=(m, m))
+    dphi_big = a + a.T
+    dphi = -0.7
+
+    def L(mu_, s_, z_, var_, ls_):
+        st, _ = orc.sweep_stats(expected, mu_, s_ if expected else None, y, z_, var_, ls_)
+        return dphi * st.phi + np.sum(dpsi * st.psi_y) + np.sum(dphi_big * st.phi_big)
+
+    _, g = orc.sweep_stats(expected, mu, s if expected else None, y, z, var, ls, adj=(dphi, dpsi, dphi_big))
+    h = 1e-5
+
+    def fd(fn, x0):
+        return (fn(x0 + h) - fn(x0 - h)) / (2 * h)
+
+    assert rel_err(g.d_variance, fd(lambda v: L(mu, s, z, v, ls), var)) < 1e-6
+    for j in range(q):
+        def f(v, j=j):
+            l2 = ls.copy()
+            l2[j] = v
+            return L(mu, s, z, var, l2)
+        assert rel_err(g.d_lengthscales[j], fd(f, ls[j])) < 1e-6
+    for i in range(m):
+        for j in range(q):
+            def f(v, i=i, j=j):
+                z2 = z.copy()
+                z2[i, j] = v
+                return L(mu, s, z2, var, ls)
+            assert rel_err(g.d_z[i, j], fd(f, z[i, j])) < 1e-6
+    if expected:
+        for i in range(n):
+            for j in range(q):
+                def fm(v, i=i, j=j):
+                    m2 = mu.copy()
+                    m2[i, j] = v
+                    return L(m2, s, z, var, ls)
+
+                def fs(v, i=i, j=j):
+                    s2 = s.copy()
+                    s2[i, j] = v
+                    return L(mu, s2, z, var, ls)
+                assert rel_err(g.d_mu[i, j], fd(fm, mu[i, j])) < 1e-6
+                assert rel_err(g.d_s[i, j], fd(fs, s[i, j])) < 1e-6
+
+
+def test_stats_rejects_bad_inputs(orc):
+    mu = np.zeros((2, 1))
+    with pytest.raises(ValueError):
+        orc.sweep_stats(True, mu, np.zeros((2, 1)), np.zeros((2, 1)), [[0.0]], 1.0, [1.0])  # S <= 0
+    with pytest.raises(ValueError):
+        asym = np.array([[0.0, 1.0], [0.0, 0.0]])
+        orc.sweep_stats(True, mu, np.ones((2, 1)), np.zeros((2, 1)), [[0.0], [1.0]], 1.0, [1.0],
+                        adj=(0.0, np.zeros((2, 1)), asym))
+
+
+# ---------------------------------------------------------------------------
+# bound.hpp KATs
+# ---------------------------------------------------------------------------
+def test_bound_single_point_kat(orc):
+    """N=M=1, x=z=0, y=1, var=ls=beta=1, jitter 0 -> -1/2 log(4 pi) - 1/4."""
+    st, _ = orc.sweep_stats(False, [[0.0]], None, [[1.0]], [[0.0]], 1.0, [1.0])
+    kmm, _ = orc.kern_gram([[0.0]], 1.0, [1.0], 0.0)
+    b = orc.bound(st, kmm, 1.0, 1, 1)
+    assert b["total"] == pytest.approx(-0.5 * math.log(4 * math.pi) - 0.25, rel=1e-14)
+    assert b["total"] == pytest.approx(-1.5155121234846454, rel=1e-14)
+    assert b["d_phi"] == -0.5
+
+
+def _dense_gp_log_marginal(x, y, var, ls, beta):
+    """oracles.hpp:22-37 in numpy."""
+    d2 = (((x[:, None, :] - x[None, :, :]) / ls) ** 2).sum(-1)
+    knn = var * np.exp(-0.5 * d2) + np.eye(len(x)) / beta
+    L = np.linalg.cholesky(knn)
+    alpha = np.linalg.solve(knn, y)
+    n = len(x)
+    return float(-0.5 * y.shape[1] * (n * math.log(2 * math.pi) + 2 * np.log(np.diag(L)).sum())
+                 - 0.5 * np.sum(y * alpha))
+
+
+@pytest.mark.parametrize("n", [10, 50])
+def test_bound_dense_exactness_and_lower_bound(orc, n):
+    rng = np.random.default_rng(n)
+    q, d = 2, 2
+    x = rng.uniform(-2, 2, (n, q))
+    y = rng.normal(size=(n, d))
+    var, ls, beta = 1.2, np.array([0.9, 1.4]), 4.0
+    dense = _dense_gp_log_marginal(x, y, var, ls, beta)
+    st, _ = orc.sweep_stats(False, x, None, y, x, var, ls)
+    kmm, _ = orc.kern_gram(x, var, ls, 1e-10 * var)
+    b = orc.bound(st, kmm, beta, n, d, adjoints=False)
+    assert rel_err(b["total"], dense) < 1e-6  # exact at Z=X up to jitter conditioning
+    for trial in range(5):
+        z = rng.uniform(-2, 2, (4, q))
+        st, _ = orc.sweep_stats(False, x, None, y, z, var, ls)
+        kmm, _ = orc.kern_gram(z, var, ls, 1e-6 * var)
+        assert orc.bound(st, kmm, beta, n, d, adjoints=False)["total"] <= dense + 1e-10
+
+
+def test_bound_adjoints_fd(orc):
+    """N=5, M=3, D=2 adjoints vs central FD of bound_regression."""
+    rng = np.random.default_rng(5)
+    n, m, q, d = 5, 3, 2, 2
+    x = rng.uniform(-2, 2, (n, q))
+    y = rng.normal(size=(n, d))
+    z = rng.uniform(-2, 2, (m, q))
+    st, _ = orc.sweep_stats(False, x, None, y, z, 1.1, [1.0, 0.8])
+    kmm, _ = orc.kern_gram(z, 1.1, [1.0, 0.8], 1e-6)
+    beta = 3.0
+    b = orc.bound(st, kmm, beta, n, d)
+    h = 1e-5
+    f = lambda **kw: orc.bound(orc.Stats(kw.get("phi", st.phi), kw.get("yy", st.yy), n, kw.get("psi", st.psi_y),
+                                         kw.get("Phi", st.phi_big)), kw.get("K", kmm), kw.get("beta", beta), n, d,
+                               adjoints=False)["total"]
+    assert rel_err(b["d_phi"], (f(phi=st.phi + h) - f(phi=st.phi - h)) / (2 * h)) < 1e-6
+    assert rel_err(b["d_beta"], (f(beta=beta + h) - f(beta=beta - h)) / (2 * h)) < 1e-6
+    for i in range(m):
+        for j in range(d):
+            P1, P2 = st.psi_y.copy(), st.psi_y.copy()
+            P1[i, j] += h
+            P2[i, j] -= h
+            assert rel_err(b["d_psi_y"][i, j], (f(psi=P1) - f(psi=P2)) / (2 * h)) < 1e-6
+    for i in range(m):
+        for j in range(i, m):
+            E = np.zeros((m, m))
+            E[i, j] = E[j, i] = 1.0  # symmetric perturbation: directional derivative = sum grad*E
+            want_phi = (f(Phi=st.phi_big + h * E) - f(Phi=st.phi_big - h * E)) / (2 * h)
+            want_k = (f(K=kmm + h * E) - f(K=kmm - h * E)) / (2 * h)
+            assert rel_err(np.sum(b["d_phi_big"] * E), want_phi) < 1e-6
+            assert rel_err(np.sum(b["d_kmm"] * E), want_k) < 1e-6
+
+
+# ---------------------------------------------------------------------------
+# parallel.hpp: engine protocol, partition invariance, determinism, gradcheck
+# ---------------------------------------------------------------------------
+def test_make_partition(orc):
+    assert orc.make_partition(10, 1) == [(0, 10)]
+    assert orc.make_partition(10, 3) == [(0, 4), (4, 7), (7, 10)]
+    assert orc.make_partition(64000, 32) == [(2000 * i, 2000 * (i + 1)) for i in range(32)]
+    with pytest.raises(ValueError):
+        orc.make_partition(3, 4)
+
+
+def _gplvm_problem(n=64, q=2, d=3, m=6, seed=0):
+    rng = np.random.default_rng(seed)
+    mu = rng.normal(size=(n, q))
+    s = rng.uniform(0.25, 1.0, (n, q))
+    y = rng.normal(size=(n, d))
+    z = mu[rng.choice(n, m, replace=False)] + 0.01 * rng.normal(size=(m, q))
+    ls = rng.uniform(0.5, 2.0, q)
+    return mu, s, y, z, 1.3, ls, 20.0
+
+
+def test_engine_partition_and_tile_invariance(orc):
+    """SPEC.md:364-366 (scaled: N=512, M=8)."""
+    mu, s, y, z, var, ls, beta = _gplvm_problem(n=512, m=8)
+    base = orc.engine_evaluate(True, mu, s, y, z, var, ls, beta, workers=1)
+    for p, (bs, ts) in [(2, (64, 1024)), (4, (7, 7)), (8, (1, 64))]:
+        r = orc.engine_evaluate(True, mu, s, y, z, var, ls, beta, workers=p, block_span=bs, thread_span=ts)
+        assert rel_err(r.bound["total"], base.bound["total"]) < 1e-10
+        for f in ("d_mu", "d_s", "d_z", "d_lengthscales"):
+            assert rel_err(getattr(r, f), getattr(base, f)) < 1e-10
+        assert rel_err(r.d_beta, base.d_beta) < 1e-10 and rel_err(r.d_variance, base.d_variance) < 1e-10
+    again = orc.engine_evaluate(True, mu, s, y, z, var, ls, beta, workers=4, block_span=7, thread_span=7)
+    again2 = orc.engine_evaluate(True, mu, s, y, z, var, ls, beta, workers=4, block_span=7, thread_span=7)
+    assert again.bound["total"] == again2.bound["total"] and np.array_equal(again.d_mu, again2.d_mu)
+
+
+@pytest.mark.parametrize("latent", [True, False])
+def test_engine_full_objective_gradcheck(orc, latent):
+    """SPEC.md:425 / acceptance 5: N=20, M=5, Q=2, D=3, every segment < 1e-5 relative error."""
+    mu, s, y, z, var, ls, beta = _gplvm_problem(n=20, q=2, d=3, m=5, seed=4)
+
+    def total(mu_=mu, s_=s, z_=z, var_=var, ls_=ls, beta_=beta):
+        return orc.engine_evaluate(latent, mu_, s_, y, z_, var_, ls_, beta_, workers=2,
+                                   with_grads=False).bound["total"]
+
+    r = orc.engine_evaluate(latent, mu, s, y, z, var, ls, beta, workers=2)
+    h = 1e-5
+    assert rel_err(r.d_beta, (total(beta_=beta + h) - total(beta_=beta - h)) / (2 * h)) < 1e-5
+    assert rel_err(r.d_variance, (total(var_=var + h) - total(var_=var - h)) / (2 * h)) < 1e-5
+    for j in range(2):
+        lp, lm = ls.copy(), ls.copy()
+        lp[j] += h
+        lm[j] -= h
+        assert rel_err(r.d_lengthscales[j], (total(ls_=lp) - total(ls_=lm)) / (2 * h)) < 1e-5
+    for i in range(5):
+        for j in range(2):
+            zp, zm = z.copy(), z.copy()
+            zp[i, j] += h
+            zm[i, j] -= h
+            assert rel_err(r.d_z[i, j], (total(z_=zp) - total(z_=zm)) / (2 * h)) < 1e-5
+    if latent:
+        for i in range(0, 20, 3):
+            for j in range(2):
+                mp, mm = mu.copy(), mu.copy()
+                mp[i, j] += h
+                mm[i, j] -= h
+                assert rel_err(r.d_mu[i, j], (total(mu_=mp) - total(mu_=mm)) / (2 * h)) < 1e-5
+                sp, sm = s.copy(), s.copy()
+                sp[i, j] += h
+                sm[i, j] -= h
+                assert rel_err(r.d_s[i, j], (total(s_=sp) - total(s_=sm)) / (2 * h)) < 1e-5
+
+
+def test_engine_kl_kat_and_sign(orc):
+    """KL(mu=1,S=1) = 0.5; bound_gplvm subtracts KL."""
+    mu = np.array([[1.0]])
+    s = np.array([[1.0]])
+    r = orc.engine_evaluate(True, mu, s, [[1.0]], [[0.5]], 1.0, [1.0], 1.0, with_grads=False)
+    assert r.bound["kl_term"] == pytest.approx(-0.5, rel=1e-15)
+    assert r.bound["total"] == pytest.approx(sum(r.bound[k] for k in r.bound if k != "total"), rel=1e-12)
