@@ -1,0 +1,220 @@
+/*
+ * sgpx.h -- C ABI of the B200-native psi-statistics engine (libsgpx.so).
+ *
+ * Drop-in boundary for the data-parallel hot path of the reference
+ * (arXiv 1410.4984 restatement under /root/reference/proj/include/sgp):
+ *
+ *   sgpx_sweep_stats        replaces sgp::detail::sweep_stats            psi_stats.hpp:108-326
+ *                           (and the wrappers stats_deterministic :332, psi2_expected :379,
+ *                            stats_expected :389, stats_grads :402, stats_grads_deterministic :415)
+ *   sgpx_psi1_expected      replaces sgp::psi1_expected                  psi_stats.hpp:351-376
+ *   sgpx_psi0_expected      replaces sgp::psi0_expected                  psi_stats.hpp:343-347
+ *   sgpx_engine_*           replaces sgp::Engine (ctor :326-346, broadcast :358-367,
+ *                           evaluate :370-450, run_pass :455-479) and Worker::pass :132-176
+ *   sgpx_coordinate_host    the coordinator algebra of Engine::evaluate: factor_gram
+ *                           (kernels.hpp:177-197) + bound_core (bound.hpp:84-119) +
+ *                           adjoints_from_core (bound.hpp:196-226)
+ *   sgpx_finish_host        gradient assembly of Engine::evaluate (parallel.hpp:414-421):
+ *                           kern_grads(Z,Z,dKmm) (kernels.hpp:124-164) + jitter term
+ *
+ * Conventions
+ *   - All matrices at this boundary are fp64, column-major with a leading
+ *     dimension (Eigen::MatrixXd / Eigen::Ref with outer stride).  ld == 0
+ *     means ld == rows.
+ *   - Outputs are caller-allocated and fully overwritten (the reference
+ *     allocates and overwrites, psi_stats.hpp:123-134).
+ *   - Return codes: SGPX_OK, SGPX_INVALID_ARGUMENT (the reference throws
+ *     std::invalid_argument via require(), common.hpp:24-26), SGPX_NUMERIC
+ *     (sgp::NumericError, common.hpp:20-22), SGPX_CUDA, SGPX_NCCL,
+ *     SGPX_INTERNAL.  The message of the last failure on the calling thread is
+ *     sgpx_last_error().  No C++ exception crosses this boundary.
+ *   - Threading: a context (one device + one stream + scratch) is
+ *     single-threaded; different contexts may be driven concurrently from
+ *     different host threads (reference: pure, reentrant).
+ *   - Arithmetic: exponent/Psi tiles in FP32 (FFMA + MUFU.EX2), every sum
+ *     across datapoints and across CTAs in fp64, all M-sized algebra in fp64.
+ *   - There is no CPU fallback: without a CUDA device every compute entry point
+ *     returns SGPX_CUDA.
+ */
+#ifndef SGPX_H_
+#define SGPX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGPX_OK 0
+#define SGPX_INVALID_ARGUMENT 1
+#define SGPX_NUMERIC 2
+#define SGPX_CUDA 3
+#define SGPX_NCCL 4
+#define SGPX_INTERNAL 5
+
+#define SGPX_ABI_VERSION 1
+
+/* Column-major views (Eigen::Ref<const Matrix> / Eigen::Ref<Matrix>). */
+typedef struct {
+  const double* data;
+  int64_t rows, cols, ld;
+} sgpx_cmat;
+
+typedef struct {
+  double* data;
+  int64_t rows, cols, ld;
+} sgpx_mmat;
+
+/* sgp::KernelSpec (kernels.hpp:13-33): RBF-ARD, variance * exp(-1/2 sum_q (x_q-z_q)^2 / l_q^2). */
+typedef struct {
+  double variance;
+  const double* lengthscales; /* q entries */
+  int64_t q;
+} sgpx_kernel_spec;
+
+/* sgp::TileConfig (common.hpp:30-37).  Validated (both >= 1) and otherwise
+ * ignored: the sm_100a launch geometry is fixed by the kernels. */
+typedef struct {
+  int64_t block_span, thread_span;
+} sgpx_tile_config;
+
+/* sgp::StatsAdjoints (psi_stats.hpp:56-60). d_phi_big must be symmetric. */
+typedef struct {
+  double d_phi;
+  sgpx_cmat d_psi_y;   /* M x D */
+  sgpx_cmat d_phi_big; /* M x M */
+} sgpx_stats_adjoints;
+
+/* sgp::SufficientStats (psi_stats.hpp:31-53). */
+typedef struct {
+  double phi;
+  sgpx_mmat psi_y;   /* M x D out */
+  sgpx_mmat phi_big; /* M x M out (symmetric) */
+  double yy;
+  int64_t n_count;
+} sgpx_sufficient_stats;
+
+/* sgp::StatsGrads (psi_stats.hpp:65-71).  d_mu / d_s are used only on the
+ * expected path (data may be NULL otherwise). */
+typedef struct {
+  sgpx_mmat d_mu; /* N x Q */
+  sgpx_mmat d_s;  /* N x Q */
+  sgpx_mmat d_z;  /* M x Q */
+  double d_variance;
+  double* d_lengthscales; /* Q out */
+} sgpx_stats_grads;
+
+/* sgp::BoundBreakdown (bound.hpp:22-35). */
+typedef struct {
+  double total, log_det_term, data_fit_term, quadratic_term, trace_phi_term, trace_kmm_term, kl_term;
+} sgpx_bound_breakdown;
+
+typedef struct sgpx_ctx sgpx_ctx;
+typedef struct sgpx_engine sgpx_engine;
+
+/* ---- library / context ---------------------------------------------------- */
+const char* sgpx_last_error(void);
+int sgpx_abi_version(void);
+/* Number of CUDA devices visible (0 on a host without GPU; never fails). */
+int sgpx_device_count(void);
+int sgpx_ctx_create(int device, sgpx_ctx** out);
+int sgpx_ctx_destroy(sgpx_ctx* ctx);
+/* Run all work of this context on an external cudaStream_t (e.g. torch's current stream). */
+int sgpx_ctx_set_stream(sgpx_ctx* ctx, void* cuda_stream);
+int sgpx_ctx_synchronize(sgpx_ctx* ctx);
+/* Kernel launches issued by this context since creation (profiling evidence). */
+int64_t sgpx_ctx_launch_count(const sgpx_ctx* ctx);
+
+/* ---- the sweep (psi_stats.hpp:108-326) ------------------------------------- */
+/* expected != 0: q(X) = N(mu, diag s) path (Bayesian GP-LVM); otherwise mu is X
+ * and s is ignored (may be empty).  adj == NULL: statistics only; grads, if
+ * given, are zeroed with d_variance = 0 (psi_stats.hpp:128-134).  Host pointers. */
+int sgpx_sweep_stats(sgpx_ctx* ctx, int expected, sgpx_cmat mu, sgpx_cmat s, sgpx_cmat y, sgpx_cmat z,
+                     const sgpx_kernel_spec* kernel, const sgpx_tile_config* tiles,
+                     const sgpx_stats_adjoints* adj, sgpx_sufficient_stats* stats, sgpx_stats_grads* grads);
+
+/* psi1_expected (psi_stats.hpp:351-376): the N x M matrix E[k(x_n, z_m)]. */
+int sgpx_psi1_expected(sgpx_ctx* ctx, sgpx_cmat mu, sgpx_cmat s, sgpx_cmat z, const sgpx_kernel_spec* kernel,
+                       sgpx_mmat out);
+
+/* psi0_expected (psi_stats.hpp:343-347): N * variance (validates q). */
+int sgpx_psi0_expected(sgpx_cmat mu, sgpx_cmat s, const sgpx_kernel_spec* kernel, double* out);
+
+/* ---- coordinator algebra (host fp64, no device needed) --------------------- */
+/* Packed statistics vector (the allreduce #1 payload), fp64:
+ *   [0] phi  [1] yy  [2] n_count  [3] kl  [4 .. 4+P) Phi upper triangle, pairs
+ *   (a<=b) in m1-major order (psi_stats.hpp:85-97)  [4+P .. 4+P+M*D) Psi, M x D col-major.
+ * P = M(M+1)/2. */
+int64_t sgpx_packed_stats_count(int64_t m, int64_t d);
+/* Packed global-gradient vector (allreduce #2 payload): [0] d_variance
+ * [1 .. 1+Q) d_lengthscales  [1+Q .. 1+Q+M*Q) d_z col-major. */
+int64_t sgpx_packed_grads_count(int64_t m, int64_t q);
+
+/* Coordinator step of Engine::evaluate (parallel.hpp:378-408): factor_gram,
+ * bound_core, KL term (latent), adjoints_from_core.  Inputs: the REDUCED packed
+ * stats.  Outputs: breakdown; optional adjoints d_psi_y (M x D), d_phi_big
+ * (M x M), d_kmm (M x M), scalars adj_scalars[0]=d_phi [1]=d_beta
+ * [2]=jitter_factor used.  n/d: global N and D. */
+int sgpx_coordinate_host(int kind, int64_t n, int64_t d, int64_t m, const double* packed_stats, sgpx_cmat z,
+                         const sgpx_kernel_spec* kernel, double beta, double jitter_factor,
+                         sgpx_bound_breakdown* bd, double* adj_scalars, double* d_psi_y, double* d_phi_big,
+                         double* d_kmm);
+
+/* Gradient assembly (parallel.hpp:414-421): given the REDUCED packed grads,
+ * adds kern_grads(Z, Z, dKmm).d_z + .d_x, kern_grads.d_variance + jitter_factor
+ * * tr(dKmm), kern_grads.d_lengthscales.  Writes d_z (M x Q), *d_variance, d_ls (Q). */
+int sgpx_finish_host(int64_t m, int64_t q, const double* packed_grads, sgpx_cmat z, const sgpx_kernel_spec* kernel,
+                     const double* d_kmm, double jitter_factor, double* d_z, double* d_variance, double* d_ls);
+
+/* ---- engine (parallel.hpp:326-479), one instance per rank / GPU ------------ */
+typedef struct {
+  int kind;          /* 0 = regression (X fixed), 1 = latent (Bayesian GP-LVM) */
+  int64_t n_global;  /* N over all ranks */
+  int64_t row_begin; /* first global row owned here (make_partition, parallel.hpp:28-41) */
+  int64_t n_local;   /* rows owned here */
+  int64_t q, d, m;
+  double jitter_factor; /* factor_gram start (default 1e-6, parallel.hpp:327) */
+} sgpx_engine_config;
+
+typedef struct {
+  sgpx_bound_breakdown bound;
+  double phi, yy;
+  int64_t n_count;
+  double* psi_y;   /* optional host out, M x D */
+  double* phi_big; /* optional host out, M x M */
+  int has_grads;
+  double* d_z;            /* optional host out, M x Q */
+  double* d_lengthscales; /* optional host out, Q */
+  double d_variance, d_beta;
+  double jitter_factor_used;
+  /* EngineTimings (parallel.hpp:296-301), seconds, device-event timed */
+  double stats_pass_s, coordinator_s, grad_pass_s, wall_s;
+} sgpx_eval_result;
+
+int sgpx_engine_create(sgpx_ctx* ctx, const sgpx_engine_config* cfg, sgpx_engine** out);
+int sgpx_engine_destroy(sgpx_engine* eng);
+/* Shard rows (the Worker copies, parallel.hpp:339-343).  on_device != 0: the
+ * pointers are device memory on the context's device.  y: n_local x D;
+ * x_or_mu, s: n_local x Q (s ignored for regression). */
+int sgpx_engine_set_data(sgpx_engine* eng, sgpx_cmat x_or_mu, sgpx_cmat s, sgpx_cmat y, int on_device);
+/* Engine::broadcast: global params (kernel, beta, Z: host memory, M x Q); mu/s (latent) optional
+ * local slice, n_local x Q (data == NULL keeps the current; on_device != 0: device pointers, adopted). */
+int sgpx_engine_broadcast(sgpx_engine* eng, const sgpx_kernel_spec* kernel, double beta, sgpx_cmat z, sgpx_cmat mu,
+                          sgpx_cmat s, int on_device);
+/* Single-rank Engine::evaluate(with_grads): the whole pipeline, no collective. */
+int sgpx_engine_evaluate(sgpx_engine* eng, int with_grads, sgpx_eval_result* out);
+/* Multi-rank phases: the caller all-reduces (sum, fp64) the packed device
+ * buffers between phases -- NCCL over NVLink, e.g. torch.distributed.all_reduce
+ * on the context's stream. */
+int sgpx_engine_stats_pass(sgpx_engine* eng, double** packed_dev, int64_t* count);
+int sgpx_engine_coordinate(sgpx_engine* eng, int with_grads);
+int sgpx_engine_grad_pass(sgpx_engine* eng, double** packed_dev, int64_t* count);
+int sgpx_engine_finish(sgpx_engine* eng, sgpx_eval_result* out);
+/* Local per-datapoint gradients (KL included), device, n_local x Q col-major (ld = n_local). */
+int sgpx_engine_local_grads_device(sgpx_engine* eng, double** d_mu, double** d_s);
+int sgpx_engine_copy_local_grads(sgpx_engine* eng, sgpx_mmat d_mu, sgpx_mmat d_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGPX_H_ */

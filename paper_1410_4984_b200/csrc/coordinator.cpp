@@ -1,0 +1,297 @@
+// coordinator.cpp -- fp64 M x M algebra of Engine::evaluate (see coordinator.hpp).
+#include "coordinator.hpp"
+
+#include <algorithm>
+#include <cmath>
+
+namespace sgpx {
+namespace coord {
+
+void Kernel::validate() const {  // kernels.hpp:18-24
+  require(std::isfinite(variance) && variance > 0.0, "kernel variance must be positive");
+  require(!ls.empty(), "kernel needs at least one lengthscale");
+  for (double l : ls) require(std::isfinite(l) && l > 0.0, "kernel lengthscales must be positive");
+}
+
+// Left-looking Cholesky on column-major storage, inner loops over contiguous
+// column entries (vectorisable).  Works on a copy so A is untouched.
+bool cholesky(const Mat& a, Mat& L) {
+  const int64_t n = a.r;
+  L = a;
+  for (int64_t j = 0; j < n; ++j) {
+    double* cj = L.col(j);
+    // cj[j:n] -= sum_k L[j:n, k] * L[j, k]
+    for (int64_t k = 0; k < j; ++k) {
+      const double ljk = L(j, k);
+      const double* ck = L.col(k);
+      for (int64_t i = j; i < n; ++i) cj[i] -= ck[i] * ljk;
+    }
+    const double djj = cj[j];
+    if (!(djj > 0.0)) return false;
+    const double ljj = std::sqrt(djj);
+    const double inv = 1.0 / ljj;
+    cj[j] = ljj;
+    for (int64_t i = j + 1; i < n; ++i) cj[i] *= inv;
+    for (int64_t i = 0; i < j; ++i) cj[i] = 0.0;
+  }
+  return true;
+}
+
+double log_det_chol(const Mat& L) {
+  double s = 0.0;
+  for (int64_t i = 0; i < L.r; ++i) s += std::log(L(i, i));
+  return 2.0 * s;
+}
+
+void chol_solve(const Mat& L, Mat& B) {
+  const int64_t n = L.r;
+  for (int64_t c = 0; c < B.c; ++c) {
+    double* x = B.col(c);
+    // forward: L y = b (column-oriented)
+    for (int64_t k = 0; k < n; ++k) {
+      x[k] /= L(k, k);
+      const double xk = x[k];
+      const double* lk = L.col(k);
+      for (int64_t i = k + 1; i < n; ++i) x[i] -= lk[i] * xk;
+    }
+    // backward: L^T x = y (dot-product oriented on columns of L)
+    for (int64_t k = n - 1; k >= 0; --k) {
+      const double* lk = L.col(k);
+      double s = x[k];
+      for (int64_t i = k + 1; i < n; ++i) s -= lk[i] * x[i];
+      x[k] = s / lk[k];
+    }
+  }
+}
+
+Mat gemm(const Mat& A, bool ta, const Mat& B, bool tb) {
+  const int64_t m = ta ? A.c : A.r, k = ta ? A.r : A.c, n = tb ? B.r : B.c;
+  Mat C(m, n);
+  if (!ta) {
+    for (int64_t j = 0; j < n; ++j) {
+      double* cj = C.col(j);
+      for (int64_t p = 0; p < k; ++p) {
+        const double b = tb ? B(j, p) : B(p, j);
+        if (b == 0.0) continue;
+        const double* ap = A.col(p);
+        for (int64_t i = 0; i < m; ++i) cj[i] += ap[i] * b;
+      }
+    }
+  } else {
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t i = 0; i < m; ++i) {
+        const double* ai = A.col(i);
+        double s = 0.0;
+        if (!tb) {
+          const double* bj = B.col(j);
+          for (int64_t p = 0; p < k; ++p) s += ai[p] * bj[p];
+        } else {
+          for (int64_t p = 0; p < k; ++p) s += ai[p] * B(j, p);
+        }
+        C(i, j) = s;
+      }
+  }
+  return C;
+}
+
+static void symmetrize(Mat& a) {
+  for (int64_t j = 0; j < a.c; ++j)
+    for (int64_t i = j + 1; i < a.r; ++i) {
+      const double s = 0.5 * (a(i, j) + a(j, i));
+      a(i, j) = s;
+      a(j, i) = s;
+    }
+}
+
+Mat chol_inverse(const Mat& L) {
+  const int64_t n = L.r;
+  Mat X(n, n);
+  for (int64_t i = 0; i < n; ++i) X(i, i) = 1.0;
+  chol_solve(L, X);
+  symmetrize(X);
+  return X;
+}
+
+Mat kern_gram(const Mat& z, const Kernel& k, double jitter, bool* near_dup) {
+  k.validate();
+  require(z.c == k.q(), "kern_gram Z: column count does not match kernel input dimension");
+  for (double x : z.v) require(std::isfinite(x), "kern_gram Z: non-finite entries");
+  require(z.r >= 1, "kern_gram: need at least one inducing input");
+  require(jitter >= 0.0, "kern_gram: jitter must be non-negative");
+  const int64_t m = z.r, q = z.c;
+  std::vector<double> il2(q);
+  for (int64_t j = 0; j < q; ++j) il2[j] = 1.0 / (k.ls[j] * k.ls[j]);
+  Mat out(m, m);
+  bool dup = false;
+  for (int64_t a = 0; a < m; ++a) {
+    out(a, a) = k.variance + jitter;
+    for (int64_t b = a + 1; b < m; ++b) {
+      double d2 = 0.0;
+      for (int64_t j = 0; j < q; ++j) {
+        const double d = z(a, j) - z(b, j);
+        d2 += d * d * il2[j];
+      }
+      if (d2 < 1e-24) dup = true;
+      const double v = k.variance * std::exp(-0.5 * d2);
+      out(a, b) = v;
+      out(b, a) = v;
+    }
+  }
+  if (near_dup) *near_dup = dup;
+  return out;
+}
+
+GramFactor factor_gram(const Mat& z, const Kernel& k, double jitter_factor) {
+  require(jitter_factor >= 0.0, "factor_gram: jitter factor must be non-negative");
+  double jf = jitter_factor;
+  for (;;) {
+    GramFactor f;
+    f.jitter_factor = jf;
+    f.jitter = jf * k.variance;
+    f.kmm = kern_gram(z, k, f.jitter, nullptr);
+    if (cholesky(f.kmm, f.L)) {
+      f.log_det = log_det_chol(f.L);
+      return f;
+    }
+    if (jf >= 1e-2)
+      throw NumericError(
+          "factor_gram: Gram matrix not factorizable even at jitter 1e-2 * variance (ill-conditioned inducing "
+          "inputs)");
+    jf = (jf == 0.0) ? 1e-6 : jf * 10.0;
+  }
+}
+
+// bound.hpp:52-62: escalating diagonal shift anchored to the matrix's own scale.
+static bool factor_spd(const Mat& a, Mat& L) {
+  if (cholesky(a, L)) return true;
+  double scale = 0.0;
+  for (int64_t i = 0; i < a.r; ++i) scale = std::max(scale, std::fabs(a(i, i)));
+  for (double f = 1e-10; f <= 1e-2; f *= 10.0) {
+    Mat b = a;
+    for (int64_t i = 0; i < a.r; ++i) b(i, i) += f * scale;
+    if (cholesky(b, L)) return true;
+  }
+  return false;
+}
+
+Stats unpack_stats(const double* p, int64_t m, int64_t d) {
+  Stats s;
+  s.phi = p[0];
+  s.yy = p[1];
+  s.n = p[2];
+  s.kl = p[3];
+  s.phi_big = Mat(m, m);
+  const double* pairs = p + 4;
+  int64_t idx = 0;
+  for (int64_t a = 0; a < m; ++a)
+    for (int64_t b = a; b < m; ++b) {
+      const double v = pairs[idx++];
+      s.phi_big(a, b) = v;
+      s.phi_big(b, a) = v;
+    }
+  s.psi_y = Mat(m, d);
+  std::copy(pairs + idx, pairs + idx + m * d, s.psi_y.v.begin());
+  return s;
+}
+
+Result coordinate(bool latent, int64_t n, int64_t d, const Stats& st, const Mat& z, const Kernel& k, double beta,
+                  double jitter_factor, bool with_adjoints) {
+  const int64_t m = z.r;
+  require(beta > 0.0 && std::isfinite(beta), "bound: beta must be positive");
+  require(n >= 1 && d >= 1, "bound: need N >= 1 and D >= 1");
+  require(int64_t(st.n) == n, "bound: stats n_count does not match N");
+  require(st.phi >= 0.0 && st.yy >= 0.0, "bound: phi and yy must be non-negative");
+  Result r;
+  r.gram = factor_gram(z, k, jitter_factor);
+  // bound_core (bound.hpp:84-119).  The Kmm factor of factor_gram is exactly
+  // factor_spd(Kmm)'s first (successful) attempt.
+  const Mat& Lk = r.gram.L;
+  const double log_det_kmm = r.gram.log_det;
+  Mat a = r.gram.kmm;
+  for (size_t i = 0; i < a.v.size(); ++i) a.v[i] += beta * st.phi_big.v[i];
+  Mat La;
+  if (!factor_spd(a, La)) throw NumericError("bound (Kmm + beta*Phi): Cholesky factorization failed after jitter escalation");
+  const double log_det_a = log_det_chol(La);
+  Mat g = st.psi_y;
+  chol_solve(La, g);
+  const Mat a_inv = chol_inverse(La);
+  const Mat kmm_inv = chol_inverse(Lk);
+  const double log_2pi = 1.8378770664093454835606594728112;
+  const double nd = double(n), dd = double(d);
+  Breakdown& bd = r.bd;
+  bd.log_det = dd * (0.5 * nd * std::log(beta) + 0.5 * log_det_kmm - 0.5 * nd * log_2pi - 0.5 * log_det_a);
+  bd.data_fit = -0.5 * beta * st.yy;
+  double pg = 0.0;
+  for (size_t i = 0; i < g.v.size(); ++i) pg += st.psi_y.v[i] * g.v[i];
+  bd.quadratic = 0.5 * beta * beta * pg;
+  bd.trace_phi = -0.5 * beta * dd * st.phi;
+  double kp = 0.0, ap = 0.0;
+  for (size_t i = 0; i < kmm_inv.v.size(); ++i) {
+    kp += kmm_inv.v[i] * st.phi_big.v[i];
+    ap += a_inv.v[i] * st.phi_big.v[i];
+  }
+  bd.trace_kmm = 0.5 * beta * dd * kp;
+  bd.kl = latent ? -st.kl : 0.0;
+  bd.total = bd.sum();
+  if (!std::isfinite(bd.total)) throw NumericError("bound: non-finite value");
+  if (!with_adjoints) return r;
+
+  // adjoints_from_core (bound.hpp:196-226)
+  Adjoints& adj = r.adj;
+  adj.d_phi = -0.5 * beta * dd;
+  adj.d_psi_y = g;
+  for (double& x : adj.d_psi_y.v) x *= beta * beta;
+  Mat ggt = gemm(g, false, g, true);
+  symmetrize(ggt);
+  adj.d_phi_big = Mat(m, m);
+  for (size_t i = 0; i < ggt.v.size(); ++i)
+    adj.d_phi_big.v[i] = -0.5 * beta * dd * a_inv.v[i] - 0.5 * beta * beta * beta * ggt.v[i] + 0.5 * beta * dd * kmm_inv.v[i];
+  Mat kpk = gemm(gemm(kmm_inv, false, st.phi_big, false), false, kmm_inv, false);
+  symmetrize(kpk);
+  adj.d_kmm = Mat(m, m);
+  for (size_t i = 0; i < ggt.v.size(); ++i)
+    adj.d_kmm.v[i] = 0.5 * dd * kmm_inv.v[i] - 0.5 * dd * a_inv.v[i] - 0.5 * beta * beta * ggt.v[i] - 0.5 * beta * dd * kpk.v[i];
+  const Mat phig = gemm(st.phi_big, false, g, false);
+  double tr_gphig = 0.0;
+  for (size_t i = 0; i < g.v.size(); ++i) tr_gphig += g.v[i] * phig.v[i];
+  // d_beta: the sum of the workers' beta_share (parallel.hpp:185-195) equals this
+  // global expression (bound.hpp:217-223) evaluated on the reduced statistics.
+  adj.d_beta = 0.5 * dd * nd / beta - 0.5 * dd * ap - 0.5 * st.yy + beta * pg - 0.5 * beta * beta * tr_gphig -
+               0.5 * dd * st.phi + 0.5 * dd * kp;
+  return r;
+}
+
+KernGrads kern_grads_zz(const Mat& z, const Kernel& k, const Mat& up) {
+  const int64_t m = z.r, q = z.c;
+  std::vector<double> il2(q), il3(q);
+  for (int64_t j = 0; j < q; ++j) {
+    const double l = k.ls[j];
+    il2[j] = 1.0 / (l * l);
+    il3[j] = 1.0 / (l * l * l);
+  }
+  KernGrads g;
+  g.d_ls.assign(q, 0.0);
+  g.d_z = Mat(m, q);
+  Mat dx(m, q);
+  for (int64_t mm = 0; mm < m; ++mm)
+    for (int64_t nn = 0; nn < m; ++nn) {
+      double d2 = 0.0;
+      for (int64_t j = 0; j < q; ++j) {
+        const double dlt = z(nn, j) - z(mm, j);
+        d2 += dlt * dlt * il2[j];
+      }
+      const double uv = up(nn, mm) * k.variance * std::exp(-0.5 * d2);
+      g.d_variance += uv / k.variance;
+      for (int64_t j = 0; j < q; ++j) {
+        const double dlt = z(nn, j) - z(mm, j);
+        dx(nn, j) -= uv * dlt * il2[j];
+        g.d_z(mm, j) += uv * dlt * il2[j];
+        g.d_ls[j] += uv * dlt * dlt * il3[j];
+      }
+    }
+  for (size_t i = 0; i < g.d_z.v.size(); ++i) g.d_z.v[i] += dx.v[i];
+  return g;
+}
+
+}  // namespace coord
+}  // namespace sgpx

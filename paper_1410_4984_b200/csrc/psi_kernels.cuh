@@ -1,0 +1,83 @@
+// psi_kernels.cuh -- device-side contract of the sm_100a psi-statistics kernels.
+//
+// Reference: proj/include/sgp/psi_stats.hpp:108-326 (detail::sweep_stats).  The
+// kernels compute the same sums with an algebraically equivalent factorisation
+// of the exponents:
+//
+//   psi2:  log2 v_nab = L_na + L_nb + sum_q K_nq z_aq z_bq
+//          L_na = sum_q [al_nq z_aq + be_nq z_aq^2] + B_n / 2
+//          al = log2e*d2*mu, be = -log2e*(1/l^2 + d2)/4, K = log2e*(1/l^2 - d2)/2,
+//          B_n = log2 c2_n - log2e * sum_q d2 mu^2,  d2 = 1/(2S + l^2)
+//   psi1:  log2 v1_nm = b1_n - (log2e/2) sum_q d1 (mu - z_m)^2,  d1 = 1/(S + l^2)
+//
+// with mu and z translated by the mean of Z (exact invariance of the stationary
+// kernel) so the fp32 terms stay O(1).  One inner (n, a, b) step is Q FFMA + 1 FADD
+// + 1 MUFU.EX2 forward; the reference's direct form is ~3Q+4 flops.
+#pragma once
+#include <cstdint>
+
+namespace sgpx {
+
+constexpr int kMaxQ = 32;
+
+// Per-launch constants (passed by value; ~0.7 KB of kernel parameter space).
+struct PsiConst {
+  int64_t n;                  // rows of this launch (the shard / call)
+  int64_t ld_mu, ld_s, ld_y;  // leading dimensions (elements) of the fp64 inputs
+  const double* mu;           // n x q, column-major, device (X on the deterministic path)
+  const double* s;            // n x q (expected path only)
+  const double* y;            // n x d
+  const float* zc;            // [mv][qv] centered inducing inputs, zero padded
+  const double* z64;          // m x q column-major inducing inputs (fp64, uncentered)
+  int q, qv, m, mv, d, dv;    // true and padded (multiple of 4) sizes
+  int expected;
+  float variance, log2_var;
+  double center[kMaxQ];       // translation applied to mu and z (mean of Z rows)
+  float il2[kMaxQ], l2[kMaxQ];
+  double ls[kMaxQ];
+};
+
+// Backward-only inputs.
+struct BwdConst {
+  const float* u;     // [mv][mv] symmetric dL/dPhi (upper triangle mirrored), zero padded
+  const float* dpsi;  // [d][mv]  dL/dPsi transposed, zero padded
+  double d_phi;       // dL/dphi
+  int add_kl;         // latent engine pass: subtract KL gradients (parallel.hpp:163-166)
+  int write_local;    // write d_mu / d_s
+  double* d_mu;       // n x q col-major (ld = ld_g), fp64
+  double* d_s;
+  int64_t ld_g;
+};
+
+// Packed per-CTA partial layouts (fp64, CTA-private rows, single-writer per slot):
+//   forward : [0] yy  [1] kl  [2 .. 2+P) Phi pairs (m1-major)  [2+P .. 2+P+M*D) Psi (m + d*M)
+//   backward: [0] d_variance  [1 .. 1+Q) d_lengthscales  [1+Q .. 1+Q+M*Q) d_z (a + q*M)
+inline int64_t fwd_part_count(int m, int d) { return 2 + int64_t(m) * (m + 1) / 2 + int64_t(m) * d; }
+inline int64_t bwd_part_count(int m, int q) { return 1 + q + int64_t(m) * q; }
+
+struct LaunchGeom {
+  int grid, threads;
+  size_t smem;
+};
+
+// Latent dimensions with an instantiated kernel; other Q are zero-padded up.
+int instantiated_q(int q);
+// Launch geometry the launchers will use (grid = persistent CTAs), so callers can
+// size the per-CTA partial buffers: rows x fwd_part_count / bwd_part_count.
+int plan_forward(const PsiConst& P, int num_sms, LaunchGeom* geom);
+int plan_backward(const PsiConst& P, int num_sms, LaunchGeom* geom);
+
+// Host launchers (psi_kernels.cu).  All are asynchronous on `stream`.
+// Forward: writes `part` (grid rows of fwd_part_count) and reduces them into
+// `packed` (sgpx packed-stats layout, see sgpx.h) in fixed CTA order.  err_flag
+// receives 1 if any non-finite mu / y or non-positive S was seen.
+int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, int num_sms,
+                void* stream, LaunchGeom* geom);
+int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
+                 LaunchGeom* geom);
+// psi1_expected: out n x m col-major fp64 (ld_out).
+int psi1_matrix(const PsiConst& P, double* out, int64_t ld_out, void* stream);
+// Number of __global__ launches issued so far by this process (evidence counter).
+int64_t launches_issued();
+
+}  // namespace sgpx

@@ -1,0 +1,933 @@
+// sgpx_api.cu -- implementation of the C ABI declared in include/sgpx.h.
+//
+// Host side of the B200 engine: contexts (device + stream + scratch), the
+// drop-in sweep_stats / psi1_expected entry points, and the per-rank Engine
+// whose evaluate() is the 2-pass protocol of the reference
+// (proj/include/sgp/parallel.hpp:370-450):
+//   psi forward kernel  -> [allreduce #1 by the caller] -> fp64 coordinator on the host
+//   -> psi backward kernel -> [allreduce #2 by the caller] -> gradient assembly.
+// No CPU fallback exists: every compute entry point needs the CUDA device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/sgpx.h"
+#include "coordinator.hpp"
+#include "psi_kernels.cuh"
+
+namespace sgpx {
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CUDA_OK(call)                                                                            \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));   \
+  } while (0)
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return SGPX_OK;
+  } catch (const InvalidArgument& e) {
+    g_last_error = e.what();
+    return SGPX_INVALID_ARGUMENT;
+  } catch (const NumericError& e) {
+    g_last_error = e.what();
+    return SGPX_NUMERIC;
+  } catch (const CudaError& e) {
+    g_last_error = e.what();
+    return SGPX_CUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SGPX_INTERNAL;
+  }
+}
+
+int64_t round4(int64_t x) { return (x + 3) / 4 * 4; }
+
+// Device buffer that only grows.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* get() const {
+    return static_cast<T*>(p);
+  }
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    CUDA_OK(cudaMalloc(&p, std::max<size_t>(n, 256)));
+    bytes = std::max<size_t>(n, 256);
+  }
+};
+
+// Pinned host buffer that only grows.
+struct HostBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~HostBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  template <class T>
+  T* get() const {
+    return static_cast<T*>(p);
+  }
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    CUDA_OK(cudaMallocHost(&p, std::max<size_t>(n, 256)));
+    bytes = std::max<size_t>(n, 256);
+  }
+};
+
+coord::Mat mat_from(sgpx_cmat a) {
+  coord::Mat m(a.rows, a.cols);
+  const int64_t ld = a.ld ? a.ld : a.rows;
+  for (int64_t j = 0; j < a.cols; ++j)
+    for (int64_t i = 0; i < a.rows; ++i) m(i, j) = a.data[i + j * ld];
+  return m;
+}
+
+void mat_to(const coord::Mat& m, sgpx_mmat out) {
+  if (!out.data) return;
+  require(out.rows == m.r && out.cols == m.c, "output matrix has the wrong shape");
+  const int64_t ld = out.ld ? out.ld : out.rows;
+  for (int64_t j = 0; j < m.c; ++j)
+    for (int64_t i = 0; i < m.r; ++i) out.data[i + j * ld] = m(i, j);
+}
+
+coord::Kernel kernel_from(const sgpx_kernel_spec* k) {
+  require(k != nullptr, "kernel spec is null");
+  coord::Kernel out;
+  out.variance = k->variance;
+  require(k->q >= 0 && (k->q == 0 || k->lengthscales), "kernel lengthscales missing");
+  out.ls.assign(k->lengthscales, k->lengthscales + k->q);
+  out.validate();
+  return out;
+}
+
+bool all_finite(const coord::Mat& m) {
+  for (double x : m.v)
+    if (!std::isfinite(x)) return false;
+  return true;
+}
+
+}  // namespace
+}  // namespace sgpx
+
+using namespace sgpx;
+
+// -----------------------------------------------------------------------------
+// Context
+// -----------------------------------------------------------------------------
+struct sgpx_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 0;
+  int64_t launches0 = 0;
+  // scratch of the one-shot sweep / psi1 entry points
+  DevBuf mu, s, y, zc, z64, fpart, bpart, pstats, pgrads, u, dpsi, dmu, ds, err, out;
+  HostBuf h_stats, h_grads, h_u, h_dpsi, h_err, h_stage;
+};
+
+// Device-side state of one shard (one rank, or one sweep call).
+namespace sgpx {
+namespace {
+
+struct ShardInputs {
+  int64_t n = 0, q = 0, d = 0, m = 0;
+  bool expected = false;
+  const double *mu = nullptr, *s = nullptr, *y = nullptr;
+  int64_t ld_mu = 0, ld_s = 0, ld_y = 0;
+};
+
+// Build the per-launch constants and upload the centred fp32 / fp64 copies of Z.
+PsiConst make_const(sgpx_ctx* ctx, const ShardInputs& in, const coord::Kernel& k, const coord::Mat& z, DevBuf& zc_buf,
+                    DevBuf& z64_buf, HostBuf& staging) {
+  require(in.q >= 1 && in.q <= kMaxQ, "latent dimension Q must be in [1, 32] on the B200 path");
+  PsiConst P{};
+  P.n = in.n;
+  P.ld_mu = in.ld_mu;
+  P.ld_s = in.ld_s;
+  P.ld_y = in.ld_y;
+  P.mu = in.mu;
+  P.s = in.s;
+  P.y = in.y;
+  P.q = int(in.q);
+  P.qv = int(round4(instantiated_q(int(in.q))));
+  P.m = int(in.m);
+  P.mv = int(round4(in.m));
+  P.d = int(in.d);
+  P.dv = int(round4(in.d));
+  P.expected = in.expected ? 1 : 0;
+  P.variance = float(k.variance);
+  P.log2_var = float(std::log2(k.variance));
+  for (int j = 0; j < P.q; ++j) {
+    double c = 0.0;
+    for (int64_t a = 0; a < in.m; ++a) c += z(a, j);
+    P.center[j] = in.m ? c / double(in.m) : 0.0;
+    const double l = k.ls[j];
+    P.ls[j] = l;
+    P.l2[j] = float(l * l);
+    P.il2[j] = float(1.0 / (l * l));
+  }
+  for (int j = P.q; j < kMaxQ; ++j) {
+    P.center[j] = 0.0;
+    P.ls[j] = 1.0;
+    P.l2[j] = 1.f;
+    P.il2[j] = 1.f;
+  }
+  const size_t zc_bytes = sizeof(float) * P.mv * P.qv, z64_bytes = sizeof(double) * z.v.size();
+  staging.ensure(zc_bytes + z64_bytes + 16);
+  float* hz = staging.get<float>();
+  std::fill(hz, hz + size_t(P.mv) * P.qv, 0.f);
+  for (int64_t a = 0; a < in.m; ++a)
+    for (int j = 0; j < P.q; ++j) hz[a * P.qv + j] = float(z(a, j) - P.center[j]);
+  double* h64 = reinterpret_cast<double*>(staging.get<char>() + ((zc_bytes + 15) / 16) * 16);
+  std::copy(z.v.begin(), z.v.end(), h64);
+  zc_buf.ensure(zc_bytes);
+  z64_buf.ensure(z64_bytes);
+  CUDA_OK(cudaMemcpyAsync(zc_buf.p, hz, zc_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_OK(cudaMemcpyAsync(z64_buf.p, h64, z64_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  // the staging buffer is reused by the next broadcast: wait for the copies
+  CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  P.zc = zc_buf.get<float>();
+  P.z64 = z64_buf.get<double>();
+  return P;
+}
+
+// Fill the fp32 backward operands: U = d_phi_big mirrored from its upper
+// triangle (the reference reads only a <= b, psi_stats.hpp:280-281), [mv][mv];
+// dPsi transposed, [d][mv].
+void stage_adjoints(const PsiConst& P, const coord::Mat& dphi_big, const coord::Mat& dpsi, HostBuf& hu, HostBuf& hd) {
+  hu.ensure(sizeof(float) * P.mv * P.mv);
+  hd.ensure(sizeof(float) * std::max(1, P.d) * P.mv);
+  float* u = hu.get<float>();
+  std::fill(u, u + size_t(P.mv) * P.mv, 0.f);
+  for (int a = 0; a < P.m; ++a)
+    for (int b = a; b < P.m; ++b) {
+      const float v = float(dphi_big(a, b));
+      u[size_t(b) * P.mv + a] = v;
+      u[size_t(a) * P.mv + b] = v;
+    }
+  float* dp = hd.get<float>();
+  std::fill(dp, dp + size_t(std::max(1, P.d)) * P.mv, 0.f);
+  for (int dd = 0; dd < P.d; ++dd)
+    for (int a = 0; a < P.m; ++a) dp[size_t(dd) * P.mv + a] = float(dpsi(a, dd));
+}
+
+void check_err_flag(int flag) {
+  if (flag & 1) throw InvalidArgument("stats sweep: non-finite data or non-positive variances");
+  if (flag & 2) throw InvalidArgument("stats sweep: non-finite data");
+}
+
+// Copy a (possibly strided) host/device column-major matrix into a dense device buffer.
+void upload(sgpx_ctx* ctx, DevBuf& dst, sgpx_cmat a, bool on_device) {
+  const int64_t ld = a.ld ? a.ld : a.rows;
+  const size_t bytes = sizeof(double) * std::max<int64_t>(1, a.rows * a.cols);
+  dst.ensure(bytes);
+  if (a.rows * a.cols == 0) return;
+  CUDA_OK(cudaMemcpy2DAsync(dst.p, sizeof(double) * a.rows, a.data, sizeof(double) * ld, sizeof(double) * a.rows,
+                              a.cols, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+}
+
+void check_view(sgpx_cmat a, const char* name) {
+  require(a.rows >= 0 && a.cols >= 0, std::string(name) + ": negative shape");
+  require(a.ld == 0 || a.ld >= a.rows, std::string(name) + ": leading dimension smaller than rows");
+  require(a.rows * a.cols == 0 || a.data != nullptr, std::string(name) + ": null data");
+}
+
+}  // namespace
+}  // namespace sgpx
+
+// -----------------------------------------------------------------------------
+// Engine
+// -----------------------------------------------------------------------------
+struct sgpx_engine {
+  sgpx_ctx* ctx = nullptr;
+  sgpx_engine_config cfg{};
+  bool latent = false;
+  // shard inputs (owned copies or adopted device pointers)
+  DevBuf own_x, own_s, own_y;
+  ShardInputs in;
+  bool has_data = false, has_params = false;
+  // broadcast parameters
+  coord::Kernel kernel;
+  coord::Mat z;
+  double beta = 1.0;
+  PsiConst P{};
+  DevBuf zc, z64, fpart, bpart, pstats, pgrads, u, dpsi, dmu, ds, err;
+  HostBuf h_stats, h_grads, h_u, h_dpsi, h_err, h_stage;
+  // coordinator results of the current evaluation
+  coord::Result res;
+  bool coordinated = false, with_grads = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  double coord_s = 0.0;
+  LaunchGeom gf{}, gb{};
+  ~sgpx_engine() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+namespace sgpx {
+namespace {
+
+void engine_stats_pass(sgpx_engine* e) {
+  require(e->has_data && e->has_params, "engine: set_data and broadcast must precede evaluate");
+  sgpx_ctx* ctx = e->ctx;
+  const int64_t count = sgpx_packed_stats_count(e->cfg.m, e->cfg.d);
+  e->pstats.ensure(sizeof(double) * count);
+  e->err.ensure(sizeof(int));
+  CUDA_OK(cudaMemsetAsync(e->err.p, 0, sizeof(int), ctx->stream));
+  LaunchGeom g{};
+  if (e->in.n > 0) {
+    if (plan_forward(e->P, ctx->num_sms, &g)) throw CudaError("psi forward: launch planning failed");
+    e->fpart.ensure(sizeof(double) * fwd_part_count(e->P.m, e->P.d) * std::max(1, g.grid));
+    CUDA_OK(cudaEventRecord(e->ev[0], ctx->stream));
+    if (psi_forward(e->P, e->fpart.get<double>(), e->pstats.get<double>(), e->err.get<int>(), ctx->num_sms,
+                    ctx->stream, &e->gf))
+      throw CudaError(std::string("psi forward launch: ") + cudaGetErrorString(cudaGetLastError()));
+    CUDA_OK(cudaEventRecord(e->ev[1], ctx->stream));
+  } else {
+    CUDA_OK(cudaMemsetAsync(e->pstats.p, 0, sizeof(double) * count, ctx->stream));
+    CUDA_OK(cudaEventRecord(e->ev[0], ctx->stream));
+    CUDA_OK(cudaEventRecord(e->ev[1], ctx->stream));
+  }
+  e->coordinated = false;
+}
+
+void engine_coordinate(sgpx_engine* e, bool with_grads) {
+  sgpx_ctx* ctx = e->ctx;
+  const auto t0 = std::chrono::steady_clock::now();
+  const int64_t count = sgpx_packed_stats_count(e->cfg.m, e->cfg.d);
+  e->h_stats.ensure(sizeof(double) * count);
+  e->h_err.ensure(sizeof(int));
+  CUDA_OK(cudaMemcpyAsync(e->h_stats.p, e->pstats.p, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_OK(cudaMemcpyAsync(e->h_err.p, e->err.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  check_err_flag(*e->h_err.get<int>());
+  coord::Stats st = coord::unpack_stats(e->h_stats.get<double>(), e->cfg.m, e->cfg.d);
+  e->res = coord::coordinate(e->latent, e->cfg.n_global, e->cfg.d, st, e->z, e->kernel, e->beta, e->cfg.jitter_factor,
+                             with_grads);
+  e->with_grads = with_grads;
+  if (with_grads) {
+    stage_adjoints(e->P, e->res.adj.d_phi_big, e->res.adj.d_psi_y, e->h_u, e->h_dpsi);
+    e->u.ensure(sizeof(float) * e->P.mv * e->P.mv);
+    e->dpsi.ensure(sizeof(float) * std::max(1, e->P.d) * e->P.mv);
+    CUDA_OK(cudaMemcpyAsync(e->u.p, e->h_u.p, sizeof(float) * e->P.mv * e->P.mv, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_OK(cudaMemcpyAsync(e->dpsi.p, e->h_dpsi.p, sizeof(float) * std::max(1, e->P.d) * e->P.mv,
+                              cudaMemcpyHostToDevice, ctx->stream));
+  }
+  e->coordinated = true;
+  e->coord_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void engine_grad_pass(sgpx_engine* e) {
+  require(e->coordinated && e->with_grads, "engine: coordinate(with_grads=1) must precede the gradient pass");
+  sgpx_ctx* ctx = e->ctx;
+  const int64_t count = sgpx_packed_grads_count(e->cfg.m, e->cfg.q);
+  e->pgrads.ensure(sizeof(double) * count);
+  e->dmu.ensure(sizeof(double) * std::max<int64_t>(1, e->in.n * e->cfg.q));
+  e->ds.ensure(sizeof(double) * std::max<int64_t>(1, e->in.n * e->cfg.q));
+  CUDA_OK(cudaEventRecord(e->ev[2], ctx->stream));
+  if (e->in.n > 0) {
+    BwdConst B{};
+    B.u = e->u.get<float>();
+    B.dpsi = e->dpsi.get<float>();
+    B.d_phi = e->res.adj.d_phi;
+    B.add_kl = e->latent ? 1 : 0;
+    B.write_local = e->latent ? 1 : 0;
+    B.d_mu = e->dmu.get<double>();
+    B.d_s = e->ds.get<double>();
+    B.ld_g = e->in.n;
+    LaunchGeom g{};
+    if (plan_backward(e->P, ctx->num_sms, &g)) throw CudaError("psi backward: launch planning failed");
+    e->bpart.ensure(sizeof(double) * bwd_part_count(e->P.m, e->P.q) * std::max(1, g.grid));
+    if (psi_backward(e->P, B, e->bpart.get<double>(), e->pgrads.get<double>(), ctx->num_sms, ctx->stream, &e->gb))
+      throw CudaError(std::string("psi backward launch: ") + cudaGetErrorString(cudaGetLastError()));
+  } else {
+    CUDA_OK(cudaMemsetAsync(e->pgrads.p, 0, sizeof(double) * count, ctx->stream));
+  }
+  CUDA_OK(cudaEventRecord(e->ev[3], ctx->stream));
+}
+
+void engine_finish(sgpx_engine* e, sgpx_eval_result* out) {
+  require(out != nullptr, "engine: result pointer is null");
+  require(e->coordinated, "engine: coordinate must precede finish");
+  sgpx_ctx* ctx = e->ctx;
+  const int64_t m = e->cfg.m, q = e->cfg.q, d = e->cfg.d;
+  const coord::Stats st = coord::unpack_stats(e->h_stats.get<double>(), m, d);
+  out->bound = sgpx_bound_breakdown{e->res.bd.total,     e->res.bd.log_det,   e->res.bd.data_fit, e->res.bd.quadratic,
+                                    e->res.bd.trace_phi, e->res.bd.trace_kmm, e->res.bd.kl};
+  out->phi = st.phi;
+  out->yy = st.yy;
+  out->n_count = int64_t(st.n);
+  if (out->psi_y) std::copy(st.psi_y.v.begin(), st.psi_y.v.end(), out->psi_y);
+  if (out->phi_big) std::copy(st.phi_big.v.begin(), st.phi_big.v.end(), out->phi_big);
+  out->jitter_factor_used = e->res.gram.jitter_factor;
+  out->has_grads = e->with_grads ? 1 : 0;
+  float ms = 0.f;
+  if (e->with_grads) {
+    const int64_t count = sgpx_packed_grads_count(m, q);
+    e->h_grads.ensure(sizeof(double) * count);
+    CUDA_OK(cudaMemcpyAsync(e->h_grads.p, e->pgrads.p, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    const double* g = e->h_grads.get<double>();
+    coord::KernGrads kg = coord::kern_grads_zz(e->z, e->kernel, e->res.adj.d_kmm);
+    double tr = 0.0;
+    for (int64_t i = 0; i < m; ++i) tr += e->res.adj.d_kmm(i, i);
+    out->d_variance = g[0] + kg.d_variance + e->res.gram.jitter_factor * tr;
+    if (out->d_lengthscales)
+      for (int64_t j = 0; j < q; ++j) out->d_lengthscales[j] = g[1 + j] + kg.d_ls[j];
+    if (out->d_z)
+      for (int64_t i = 0; i < m * q; ++i) out->d_z[i] = g[1 + q + i] + kg.d_z.v[i];
+    out->d_beta = e->res.adj.d_beta;
+    cudaEventElapsedTime(&ms, e->ev[2], e->ev[3]);
+    out->grad_pass_s = ms * 1e-3;
+  } else {
+    CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    out->d_variance = 0.0;
+    out->d_beta = 0.0;
+    out->grad_pass_s = 0.0;
+  }
+  cudaEventElapsedTime(&ms, e->ev[0], e->ev[1]);
+  out->stats_pass_s = ms * 1e-3;
+  out->coordinator_s = e->coord_s;
+}
+
+}  // namespace
+}  // namespace sgpx
+
+extern "C" {
+
+const char* sgpx_last_error(void) { return g_last_error.c_str(); }
+int sgpx_abi_version(void) { return SGPX_ABI_VERSION; }
+
+int sgpx_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int sgpx_ctx_create(int device, sgpx_ctx** out) {
+  return guard([&] {
+    require(out != nullptr, "ctx_create: out is null");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      throw CudaError("no CUDA device: the B200 psi-statistics engine has no CPU fallback");
+    }
+    require(device >= 0 && device < n, "ctx_create: device index out of range");
+    CUDA_OK(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    CUDA_OK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+      throw CudaError("device " + std::string(prop.name) + " is not sm_100-class; libsgpx is built for sm_100a");
+    auto c = std::make_unique<sgpx_ctx>();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+    c->launches0 = launches_issued();
+    *out = c.release();
+  });
+}
+
+int sgpx_ctx_destroy(sgpx_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int sgpx_ctx_set_stream(sgpx_ctx* ctx, void* stream) {
+  return guard([&] {
+    require(ctx != nullptr, "ctx is null");
+    CUDA_OK(cudaSetDevice(ctx->device));
+    if (ctx->own_stream && ctx->stream) CUDA_OK(cudaStreamDestroy(ctx->stream));
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    ctx->own_stream = false;
+  });
+}
+
+int sgpx_ctx_synchronize(sgpx_ctx* ctx) {
+  return guard([&] {
+    require(ctx != nullptr, "ctx is null");
+    CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int64_t sgpx_ctx_launch_count(const sgpx_ctx* ctx) { return ctx ? launches_issued() - ctx->launches0 : 0; }
+
+int64_t sgpx_packed_stats_count(int64_t m, int64_t d) { return 4 + m * (m + 1) / 2 + m * d; }
+int64_t sgpx_packed_grads_count(int64_t m, int64_t q) { return 1 + q + m * q; }
+
+// ---- sweep_stats (psi_stats.hpp:108-326) ------------------------------------
+int sgpx_sweep_stats(sgpx_ctx* ctx, int expected, sgpx_cmat mu, sgpx_cmat s, sgpx_cmat y, sgpx_cmat z,
+                     const sgpx_kernel_spec* kernel, const sgpx_tile_config* tiles, const sgpx_stats_adjoints* adj,
+                     sgpx_sufficient_stats* stats, sgpx_stats_grads* grads) {
+  return guard([&] {
+    require(ctx != nullptr, "ctx is null");
+    require(stats != nullptr, "stats output is null");
+    coord::Kernel k = kernel_from(kernel);
+    if (tiles) require(tiles->block_span >= 1 && tiles->thread_span >= 1, "TileConfig spans must be >= 1");
+    check_view(mu, "mu");
+    check_view(y, "y");
+    check_view(z, "z");
+    const int64_t n = mu.rows, q = mu.cols, m = z.rows, d = y.cols;
+    require(z.cols == q, "stats sweep: Z column count mismatch");
+    require(int64_t(k.ls.size()) == q, "stats sweep: kernel dimension mismatch");
+    require(y.rows == n, "stats sweep: X/Y row counts differ");
+    if (expected) {
+      check_view(s, "s");
+      require(s.rows == n && s.cols == q, "VariationalPosterior: mu and s shapes differ");
+    }
+    coord::Mat zm = mat_from(z);
+    require(all_finite(zm), "stats sweep: non-finite data");
+    coord::Mat dphi_big, dpsi;
+    if (adj) {
+      require(adj->d_psi_y.rows == m && adj->d_psi_y.cols == d, "stats adjoints: d_psi_y shape must be M x D");
+      require(adj->d_phi_big.rows == m && adj->d_phi_big.cols == m, "stats adjoints: d_phi_big shape must be M x M");
+      dphi_big = mat_from(adj->d_phi_big);
+      dpsi = mat_from(adj->d_psi_y);
+      double scale = 0.0, asym = 0.0;
+      for (int64_t j = 0; j < m; ++j)
+        for (int64_t i = 0; i < m; ++i) {
+          scale = std::max(scale, std::fabs(dphi_big(i, j)));
+          asym = std::max(asym, std::fabs(dphi_big(i, j) - dphi_big(j, i)));
+        }
+      require(asym <= 1e-10 * (1.0 + scale), "stats adjoints: d_phi_big must be symmetric");
+    }
+    CUDA_OK(cudaSetDevice(ctx->device));
+    // Reference semantics: outputs fully overwritten (psi_stats.hpp:123-134).
+    stats->phi = double(n) * k.variance;
+    stats->n_count = n;
+    stats->yy = 0.0;
+    coord::Mat zero_psi(m, d), zero_phi(m, m);
+    if (grads) {
+      coord::Mat zq(m, q);
+      mat_to(zq, grads->d_z);
+      grads->d_variance = adj ? adj->d_phi * double(n) : 0.0;
+      if (grads->d_lengthscales) std::fill(grads->d_lengthscales, grads->d_lengthscales + q, 0.0);
+      if (expected) {
+        coord::Mat nq(n, q);
+        mat_to(nq, grads->d_mu);
+        mat_to(nq, grads->d_s);
+      }
+    }
+    if (n == 0 || m == 0) {
+      mat_to(zero_psi, stats->psi_y);
+      mat_to(zero_phi, stats->phi_big);
+      return;
+    }
+    upload(ctx, ctx->mu, mu, false);
+    if (expected) upload(ctx, ctx->s, s, false);
+    upload(ctx, ctx->y, y, false);
+    ShardInputs in;
+    in.n = n;
+    in.q = q;
+    in.d = d;
+    in.m = m;
+    in.expected = expected != 0;
+    in.mu = ctx->mu.get<double>();
+    in.ld_mu = n;
+    in.s = expected ? ctx->s.get<double>() : nullptr;
+    in.ld_s = n;
+    in.y = ctx->y.get<double>();
+    in.ld_y = n;
+    PsiConst P = make_const(ctx, in, k, zm, ctx->zc, ctx->z64, ctx->h_stage);
+    LaunchGeom g{};
+    if (plan_forward(P, ctx->num_sms, &g)) throw CudaError("psi forward: launch planning failed");
+    ctx->fpart.ensure(sizeof(double) * fwd_part_count(P.m, P.d) * std::max(1, g.grid));
+    const int64_t count = sgpx_packed_stats_count(m, d);
+    ctx->pstats.ensure(sizeof(double) * count);
+    ctx->err.ensure(sizeof(int));
+    CUDA_OK(cudaMemsetAsync(ctx->err.p, 0, sizeof(int), ctx->stream));
+    if (psi_forward(P, ctx->fpart.get<double>(), ctx->pstats.get<double>(), ctx->err.get<int>(), ctx->num_sms,
+                    ctx->stream, nullptr))
+      throw CudaError(std::string("psi forward launch: ") + cudaGetErrorString(cudaGetLastError()));
+    ctx->h_stats.ensure(sizeof(double) * count);
+    ctx->h_err.ensure(sizeof(int));
+    CUDA_OK(cudaMemcpyAsync(ctx->h_stats.p, ctx->pstats.p, sizeof(double) * count, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    CUDA_OK(cudaMemcpyAsync(ctx->h_err.p, ctx->err.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    check_err_flag(*ctx->h_err.get<int>());
+    const coord::Stats st = coord::unpack_stats(ctx->h_stats.get<double>(), m, d);
+    stats->yy = st.yy;
+    mat_to(st.psi_y, stats->psi_y);
+    mat_to(st.phi_big, stats->phi_big);
+    if (!grads || !adj) return;
+
+    stage_adjoints(P, dphi_big, dpsi, ctx->h_u, ctx->h_dpsi);
+    ctx->u.ensure(sizeof(float) * P.mv * P.mv);
+    ctx->dpsi.ensure(sizeof(float) * std::max(1, P.d) * P.mv);
+    CUDA_OK(cudaMemcpyAsync(ctx->u.p, ctx->h_u.p, sizeof(float) * P.mv * P.mv, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_OK(cudaMemcpyAsync(ctx->dpsi.p, ctx->h_dpsi.p, sizeof(float) * std::max(1, P.d) * P.mv,
+                              cudaMemcpyHostToDevice, ctx->stream));
+    ctx->dmu.ensure(sizeof(double) * n * q);
+    ctx->ds.ensure(sizeof(double) * n * q);
+    BwdConst B{};
+    B.u = ctx->u.get<float>();
+    B.dpsi = ctx->dpsi.get<float>();
+    B.d_phi = adj->d_phi;
+    B.add_kl = 0;
+    B.write_local = expected ? 1 : 0;
+    B.d_mu = ctx->dmu.get<double>();
+    B.d_s = ctx->ds.get<double>();
+    B.ld_g = n;
+    if (plan_backward(P, ctx->num_sms, &g)) throw CudaError("psi backward: launch planning failed");
+    ctx->bpart.ensure(sizeof(double) * bwd_part_count(P.m, P.q) * std::max(1, g.grid));
+    const int64_t gcount = sgpx_packed_grads_count(m, q);
+    ctx->pgrads.ensure(sizeof(double) * gcount);
+    if (psi_backward(P, B, ctx->bpart.get<double>(), ctx->pgrads.get<double>(), ctx->num_sms, ctx->stream, nullptr))
+      throw CudaError(std::string("psi backward launch: ") + cudaGetErrorString(cudaGetLastError()));
+    ctx->h_grads.ensure(sizeof(double) * gcount);
+    CUDA_OK(cudaMemcpyAsync(ctx->h_grads.p, ctx->pgrads.p, sizeof(double) * gcount, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    if (expected) {
+      const int64_t ldm = grads->d_mu.ld ? grads->d_mu.ld : grads->d_mu.rows;
+      const int64_t lds = grads->d_s.ld ? grads->d_s.ld : grads->d_s.rows;
+      require(grads->d_mu.data && grads->d_s.data, "stats grads: d_mu / d_s outputs are null");
+      CUDA_OK(cudaMemcpy2DAsync(grads->d_mu.data, sizeof(double) * ldm, ctx->dmu.p, sizeof(double) * n,
+                                  sizeof(double) * n, q, cudaMemcpyDeviceToHost, ctx->stream));
+      CUDA_OK(cudaMemcpy2DAsync(grads->d_s.data, sizeof(double) * lds, ctx->ds.p, sizeof(double) * n,
+                                  sizeof(double) * n, q, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    const double* gg = ctx->h_grads.get<double>();
+    grads->d_variance = gg[0];
+    if (grads->d_lengthscales)
+      for (int64_t j = 0; j < q; ++j) grads->d_lengthscales[j] = gg[1 + j];
+    coord::Mat dz(m, q);
+    std::copy(gg + 1 + q, gg + 1 + q + m * q, dz.v.begin());
+    mat_to(dz, grads->d_z);
+  });
+}
+
+int sgpx_psi1_expected(sgpx_ctx* ctx, sgpx_cmat mu, sgpx_cmat s, sgpx_cmat z, const sgpx_kernel_spec* kernel,
+                       sgpx_mmat out) {
+  return guard([&] {
+    require(ctx != nullptr, "ctx is null");
+    coord::Kernel k = kernel_from(kernel);
+    check_view(mu, "mu");
+    check_view(s, "s");
+    check_view(z, "z");
+    const int64_t n = mu.rows, q = mu.cols, m = z.rows;
+    require(s.rows == n && s.cols == q, "VariationalPosterior: mu and s shapes differ");
+    require(z.cols == q, "psi1_expected: Z column count mismatch");
+    require(int64_t(k.ls.size()) == q, "psi1_expected: kernel dimension mismatch");
+    require(out.rows == n && out.cols == m && (n * m == 0 || out.data), "psi1_expected: output must be N x M");
+    coord::Mat zm = mat_from(z);
+    CUDA_OK(cudaSetDevice(ctx->device));
+    if (n * m == 0) return;
+    upload(ctx, ctx->mu, mu, false);
+    upload(ctx, ctx->s, s, false);
+    ShardInputs in;
+    in.n = n;
+    in.q = q;
+    in.m = m;
+    in.d = 0;
+    in.expected = true;
+    in.mu = ctx->mu.get<double>();
+    in.ld_mu = n;
+    in.s = ctx->s.get<double>();
+    in.ld_s = n;
+    PsiConst P = make_const(ctx, in, k, zm, ctx->zc, ctx->z64, ctx->h_stage);
+    ctx->out.ensure(sizeof(double) * n * m);
+    // validation (VariationalPosterior::validate, psi_stats.hpp:20-25) via the forward err flag is
+    // not run here; check on the host copy instead.
+    {
+      const int64_t ldm = mu.ld ? mu.ld : n, lds = s.ld ? s.ld : n;
+      for (int64_t j = 0; j < q; ++j)
+        for (int64_t i = 0; i < n; ++i) {
+          require(std::isfinite(mu.data[i + j * ldm]) && std::isfinite(s.data[i + j * lds]),
+                  "VariationalPosterior: non-finite entries");
+          require(s.data[i + j * lds] > 0.0, "VariationalPosterior: variances must be positive");
+        }
+    }
+    if (psi1_matrix(P, ctx->out.get<double>(), n, ctx->stream))
+      throw CudaError(std::string("psi1 launch: ") + cudaGetErrorString(cudaGetLastError()));
+    const int64_t ldo = out.ld ? out.ld : n;
+    CUDA_OK(cudaMemcpy2DAsync(out.data, sizeof(double) * ldo, ctx->out.p, sizeof(double) * n, sizeof(double) * n, m,
+                                cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sgpx_psi0_expected(sgpx_cmat mu, sgpx_cmat s, const sgpx_kernel_spec* kernel, double* out) {
+  return guard([&] {
+    coord::Kernel k = kernel_from(kernel);
+    check_view(mu, "mu");
+    check_view(s, "s");
+    require(mu.rows == s.rows && mu.cols == s.cols, "VariationalPosterior: mu and s shapes differ");
+    require(out != nullptr, "psi0_expected: out is null");
+    *out = double(mu.rows) * k.variance;
+  });
+}
+
+// ---- coordinator (host) -------------------------------------------------------
+int sgpx_coordinate_host(int kind, int64_t n, int64_t d, int64_t m, const double* packed_stats, sgpx_cmat z,
+                         const sgpx_kernel_spec* kernel, double beta, double jitter_factor, sgpx_bound_breakdown* bd,
+                         double* adj_scalars, double* d_psi_y, double* d_phi_big, double* d_kmm) {
+  return guard([&] {
+    require(packed_stats && bd, "coordinate: null input/output");
+    coord::Kernel k = kernel_from(kernel);
+    require(z.rows == m, "coordinate: Z must have M rows");
+    coord::Mat zm = mat_from(z);
+    const coord::Stats st = coord::unpack_stats(packed_stats, m, d);
+    const bool want = adj_scalars != nullptr;
+    coord::Result r = coord::coordinate(kind == 1, n, d, st, zm, k, beta, jitter_factor, want);
+    *bd = sgpx_bound_breakdown{r.bd.total, r.bd.log_det, r.bd.data_fit, r.bd.quadratic, r.bd.trace_phi, r.bd.trace_kmm,
+                               r.bd.kl};
+    if (want) {
+      adj_scalars[0] = r.adj.d_phi;
+      adj_scalars[1] = r.adj.d_beta;
+      adj_scalars[2] = r.gram.jitter_factor;
+      if (d_psi_y) std::copy(r.adj.d_psi_y.v.begin(), r.adj.d_psi_y.v.end(), d_psi_y);
+      if (d_phi_big) std::copy(r.adj.d_phi_big.v.begin(), r.adj.d_phi_big.v.end(), d_phi_big);
+      if (d_kmm) std::copy(r.adj.d_kmm.v.begin(), r.adj.d_kmm.v.end(), d_kmm);
+    }
+  });
+}
+
+int sgpx_finish_host(int64_t m, int64_t q, const double* packed_grads, sgpx_cmat z, const sgpx_kernel_spec* kernel,
+                     const double* d_kmm, double jitter_factor, double* d_z, double* d_variance, double* d_ls) {
+  return guard([&] {
+    require(packed_grads && d_kmm && d_z && d_variance && d_ls, "finish: null input/output");
+    coord::Kernel k = kernel_from(kernel);
+    coord::Mat zm = mat_from(z);
+    coord::Mat dk(m, m);
+    std::copy(d_kmm, d_kmm + m * m, dk.v.begin());
+    coord::KernGrads kg = coord::kern_grads_zz(zm, k, dk);
+    double tr = 0.0;
+    for (int64_t i = 0; i < m; ++i) tr += dk(i, i);
+    *d_variance = packed_grads[0] + kg.d_variance + jitter_factor * tr;
+    for (int64_t j = 0; j < q; ++j) d_ls[j] = packed_grads[1 + j] + kg.d_ls[j];
+    for (int64_t i = 0; i < m * q; ++i) d_z[i] = packed_grads[1 + q + i] + kg.d_z.v[i];
+  });
+}
+
+// ---- engine -------------------------------------------------------------------
+int sgpx_engine_create(sgpx_ctx* ctx, const sgpx_engine_config* cfg, sgpx_engine** out) {
+  return guard([&] {
+    require(ctx && cfg && out, "engine_create: null argument");
+    require(cfg->kind == 0 || cfg->kind == 1, "engine_create: kind must be 0 (regression) or 1 (latent)");
+    require(cfg->n_local >= 0 && cfg->row_begin >= 0 && cfg->row_begin + cfg->n_local <= cfg->n_global,
+            "engine_create: shard rows outside [0, N)");
+    require(cfg->q >= 1 && cfg->q <= kMaxQ, "engine_create: Q must be in [1, 32]");
+    require(cfg->m >= 1 && cfg->d >= 1, "engine_create: need M >= 1 and D >= 1");
+    require(cfg->jitter_factor >= 0.0, "factor_gram: jitter factor must be non-negative");
+    CUDA_OK(cudaSetDevice(ctx->device));
+    auto e = std::make_unique<sgpx_engine>();
+    e->ctx = ctx;
+    e->cfg = *cfg;
+    e->latent = cfg->kind == 1;
+    for (auto& ev : e->ev) CUDA_OK(cudaEventCreate(&ev));
+    *out = e.release();
+  });
+}
+
+int sgpx_engine_destroy(sgpx_engine* eng) {
+  return guard([&] {
+    if (!eng) return;
+    cudaSetDevice(eng->ctx->device);
+    delete eng;
+  });
+}
+
+int sgpx_engine_set_data(sgpx_engine* e, sgpx_cmat x_or_mu, sgpx_cmat s, sgpx_cmat y, int on_device) {
+  return guard([&] {
+    require(e != nullptr, "engine is null");
+    const int64_t n = e->cfg.n_local, q = e->cfg.q, d = e->cfg.d;
+    check_view(x_or_mu, "x_or_mu");
+    check_view(y, "y");
+    require(y.rows == n && y.cols == d, "worker: Y must be n_local x D");
+    require(x_or_mu.rows == n && x_or_mu.cols == q, "worker: X/mu must be n_local x Q");
+    if (e->latent) {
+      check_view(s, "s");
+      require(s.rows == n && s.cols == q, "worker: local parameter row mismatch");
+    }
+    CUDA_OK(cudaSetDevice(e->ctx->device));
+    ShardInputs& in = e->in;
+    in.n = n;
+    in.q = q;
+    in.d = d;
+    in.m = e->cfg.m;
+    in.expected = e->latent;
+    if (on_device) {  // adopt (the caller keeps the device buffers alive)
+      in.mu = x_or_mu.data;
+      in.ld_mu = x_or_mu.ld ? x_or_mu.ld : n;
+      in.y = y.data;
+      in.ld_y = y.ld ? y.ld : n;
+      in.s = e->latent ? s.data : nullptr;
+      in.ld_s = e->latent ? (s.ld ? s.ld : n) : n;
+    } else {
+      upload(e->ctx, e->own_x, x_or_mu, false);
+      upload(e->ctx, e->own_y, y, false);
+      in.mu = e->own_x.get<double>();
+      in.ld_mu = n;
+      in.y = e->own_y.get<double>();
+      in.ld_y = n;
+      if (e->latent) {
+        upload(e->ctx, e->own_s, s, false);
+        in.s = e->own_s.get<double>();
+      }
+      in.ld_s = n;
+    }
+    e->has_data = true;
+    if (e->has_params) {
+      e->P.mu = in.mu;
+      e->P.ld_mu = in.ld_mu;
+      e->P.s = in.s;
+      e->P.ld_s = in.ld_s;
+      e->P.y = in.y;
+      e->P.ld_y = in.ld_y;
+    }
+  });
+}
+
+int sgpx_engine_broadcast(sgpx_engine* e, const sgpx_kernel_spec* kernel, double beta, sgpx_cmat z, sgpx_cmat mu,
+                          sgpx_cmat s, int on_device) {
+  return guard([&] {
+    require(e != nullptr, "engine is null");
+    coord::Kernel k = kernel_from(kernel);
+    require(int64_t(k.ls.size()) == e->cfg.q, "broadcast: kernel dimension mismatch");
+    check_view(z, "z");
+    require(z.rows == e->cfg.m && z.cols == e->cfg.q, "broadcast: Z must be M x Q");
+    require(std::isfinite(beta) && beta > 0.0, "noise precision beta must be positive");
+    require(e->has_data, "broadcast: set_data (the Engine's shard rows) must come first");
+    CUDA_OK(cudaSetDevice(e->ctx->device));
+    coord::Mat zm = mat_from(z);
+    require(all_finite(zm), "stats sweep: non-finite data");
+    if (e->latent && mu.data) {
+      require(e->has_data, "broadcast: set_data must precede a local-parameter broadcast");
+      check_view(mu, "mu");
+      check_view(s, "s");
+      require(mu.rows == e->cfg.n_local && s.rows == e->cfg.n_local && mu.cols == e->cfg.q && s.cols == e->cfg.q,
+              "broadcast: local parameter row mismatch");
+      if (on_device) {
+        e->in.mu = mu.data;
+        e->in.ld_mu = mu.ld ? mu.ld : e->cfg.n_local;
+        e->in.s = s.data;
+        e->in.ld_s = s.ld ? s.ld : e->cfg.n_local;
+      } else {
+        upload(e->ctx, e->own_x, mu, false);
+        upload(e->ctx, e->own_s, s, false);
+        e->in.mu = e->own_x.get<double>();
+        e->in.ld_mu = e->cfg.n_local;
+        e->in.s = e->own_s.get<double>();
+        e->in.ld_s = e->cfg.n_local;
+      }
+    }
+    e->kernel = k;
+    e->z = zm;
+    e->beta = beta;
+    e->P = make_const(e->ctx, e->in, k, zm, e->zc, e->z64, e->h_stage);
+    e->has_params = true;
+    e->coordinated = false;
+  });
+}
+
+int sgpx_engine_stats_pass(sgpx_engine* e, double** packed_dev, int64_t* count) {
+  return guard([&] {
+    require(e != nullptr, "engine is null");
+    CUDA_OK(cudaSetDevice(e->ctx->device));
+    engine_stats_pass(e);
+    if (packed_dev) *packed_dev = e->pstats.get<double>();
+    if (count) *count = sgpx_packed_stats_count(e->cfg.m, e->cfg.d);
+  });
+}
+
+int sgpx_engine_coordinate(sgpx_engine* e, int with_grads) {
+  return guard([&] {
+    require(e != nullptr, "engine is null");
+    CUDA_OK(cudaSetDevice(e->ctx->device));
+    engine_coordinate(e, with_grads != 0);
+  });
+}
+
+int sgpx_engine_grad_pass(sgpx_engine* e, double** packed_dev, int64_t* count) {
+  return guard([&] {
+    require(e != nullptr, "engine is null");
+    CUDA_OK(cudaSetDevice(e->ctx->device));
+    engine_grad_pass(e);
+    if (packed_dev) *packed_dev = e->pgrads.get<double>();
+    if (count) *count = sgpx_packed_grads_count(e->cfg.m, e->cfg.q);
+  });
+}
+
+int sgpx_engine_finish(sgpx_engine* e, sgpx_eval_result* out) {
+  return guard([&] {
+    require(e != nullptr, "engine is null");
+    CUDA_OK(cudaSetDevice(e->ctx->device));
+    engine_finish(e, out);
+  });
+}
+
+int sgpx_engine_evaluate(sgpx_engine* e, int with_grads, sgpx_eval_result* out) {
+  return guard([&] {
+    require(e != nullptr && out != nullptr, "engine/result is null");
+    require(e->cfg.n_local == e->cfg.n_global, "engine_evaluate is the single-rank pipeline; use the phases");
+    CUDA_OK(cudaSetDevice(e->ctx->device));
+    const auto t0 = std::chrono::steady_clock::now();
+    engine_stats_pass(e);
+    engine_coordinate(e, with_grads != 0);
+    if (with_grads) engine_grad_pass(e);
+    engine_finish(e, out);
+    out->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+int sgpx_engine_local_grads_device(sgpx_engine* e, double** d_mu, double** d_s) {
+  return guard([&] {
+    require(e != nullptr && d_mu && d_s, "null argument");
+    require(e->latent, "regression engines hold no local gradients");
+    *d_mu = e->dmu.get<double>();
+    *d_s = e->ds.get<double>();
+  });
+}
+
+int sgpx_engine_copy_local_grads(sgpx_engine* e, sgpx_mmat d_mu, sgpx_mmat d_s) {
+  return guard([&] {
+    require(e != nullptr, "engine is null");
+    require(e->latent, "regression engines hold no local gradients");
+    const int64_t n = e->cfg.n_local, q = e->cfg.q;
+    require(d_mu.rows == n && d_mu.cols == q && d_s.rows == n && d_s.cols == q, "local grads must be n_local x Q");
+    CUDA_OK(cudaSetDevice(e->ctx->device));
+    CUDA_OK(cudaMemcpy2DAsync(d_mu.data, sizeof(double) * (d_mu.ld ? d_mu.ld : n), e->dmu.p, sizeof(double) * n,
+                                sizeof(double) * n, q, cudaMemcpyDeviceToHost, e->ctx->stream));
+    CUDA_OK(cudaMemcpy2DAsync(d_s.data, sizeof(double) * (d_s.ld ? d_s.ld : n), e->ds.p, sizeof(double) * n,
+                                sizeof(double) * n, q, cudaMemcpyDeviceToHost, e->ctx->stream));
+    CUDA_OK(cudaStreamSynchronize(e->ctx->stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,152 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle.
+
+Tolerances (north star: <= 1e-4 relative for the mixed FP32/fp64 path):
+  * statistics Phi, Psi, yy:         norm-wise relative error <= 2e-6
+  * per-datapoint / global gradients: norm-wise relative error <= 1e-5
+  * bound total:                      |a-b| / max(|a|,|b|,1) <= 1e-5 (reference rel_err scale)
+The exponents run in FP32 (FFMA + MUFU.EX2); every sum over datapoints and
+across CTAs is fp64.
+"""
+import numpy as np
+import pytest
+
+from conftest import norm_rel_err, rel_err
+
+pytestmark = pytest.mark.gpu
+
+STAT_TOL = 2e-6
+GRAD_TOL = 1e-5
+BOUND_TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def sgp():
+    from paper_1410_4984_b200 import sgp as m
+
+    if m.device_count() == 0:
+        pytest.fail("no CUDA device visible to libsgpx (gpu tests must run on the B200)")
+    return m
+
+
+def problem(seed=0, n=300, q=3, d=4, m=7, s_lo=0.25, s_hi=1.0):
+    rng = np.random.default_rng(seed)
+    mu = rng.normal(size=(n, q))
+    s = rng.uniform(s_lo, s_hi, (n, q))
+    y = rng.normal(size=(n, d))
+    z = mu[rng.choice(n, m, replace=False)] + 0.05 * rng.normal(size=(m, q))
+    ls = rng.uniform(0.5, 2.0, q)
+    return mu, s, y, z, 1.3, ls
+
+
+def sym_adj(rng, m, d):
+    a = rng.normal(size=(m, m))
+    return -0.7, rng.normal(size=(m, d)), a + a.T
+
+
+@pytest.mark.parametrize("shape", [(300, 3, 4, 7), (1, 1, 1, 1), (33, 2, 1, 5), (257, 10, 10, 100),
+                                   (100, 1, 3, 50), (64, 20, 5, 12), (1000, 8, 2, 33), (70, 5, 0, 9)])
+@pytest.mark.parametrize("expected", [True, False])
+def test_stats_parity(sgp, orc, shape, expected):
+    n, q, d, m = shape
+    mu, s, y, z, var, ls = problem(1, n, q, d, m)
+    k = sgp.KernelSpec(var, ls)
+    got = sgp.sweep_stats(expected, mu, s, y, z, k)[0]
+    want, _ = orc.sweep_stats(expected, mu, s if expected else None, y, z, var, ls)
+    assert got.phi == pytest.approx(want.phi, rel=1e-15)
+    assert got.n_count == want.n_count
+    assert rel_err(got.yy, want.yy) < 1e-12
+    assert norm_rel_err(got.phi_big, want.phi_big) < STAT_TOL
+    if d:
+        assert norm_rel_err(got.psi_y, want.psi_y) < STAT_TOL
+    assert np.array_equal(got.phi_big, got.phi_big.T)
+
+
+@pytest.mark.parametrize("shape", [(300, 3, 4, 7), (1, 1, 1, 1), (33, 2, 1, 5), (257, 10, 10, 100),
+                                   (100, 1, 3, 50), (64, 20, 5, 12), (1000, 8, 2, 33)])
+@pytest.mark.parametrize("expected", [True, False])
+def test_grads_parity(sgp, orc, shape, expected):
+    n, q, d, m = shape
+    mu, s, y, z, var, ls = problem(2, n, q, d, m)
+    rng = np.random.default_rng(5)
+    adj = sym_adj(rng, m, d)
+    k = sgp.KernelSpec(var, ls)
+    st, g = sgp.sweep_stats(expected, mu, s, y, z, k, adj=sgp.StatsAdjoints(*adj))
+    wst, wg = orc.sweep_stats(expected, mu, s if expected else None, y, z, var, ls, adj=adj)
+    assert norm_rel_err(st.phi_big, wst.phi_big) < STAT_TOL
+    assert norm_rel_err(g.d_z, wg.d_z) < GRAD_TOL
+    assert rel_err(g.d_variance, wg.d_variance) < GRAD_TOL or norm_rel_err(g.d_variance, wg.d_variance) < GRAD_TOL
+    assert norm_rel_err(g.d_lengthscales, wg.d_lengthscales) < GRAD_TOL
+    if expected:
+        assert norm_rel_err(g.d_mu, wg.d_mu) < GRAD_TOL
+        assert norm_rel_err(g.d_s, wg.d_s) < GRAD_TOL
+
+
+def test_psi1_expected_parity(sgp, orc):
+    mu, s, _, z, var, ls = problem(3, 200, 4, 1, 9)
+    got = sgp.psi1_expected(sgp.VariationalPosterior(mu, s), z, sgp.KernelSpec(var, ls))
+    want = orc.psi1_expected(mu, s, z, var, ls)
+    assert rel_err(got, want) < 1e-12
+
+
+def test_spec_kats_on_gpu(sgp):
+    """SPEC.md:130,139,149,158 through the B200 path."""
+    k = sgp.KernelSpec(1.0, [1.0])
+    st = sgp.stats_deterministic([[0.0]], [[1.0]], [[0.0]], k)
+    assert st.phi == 1.0 and abs(st.psi_y[0, 0] - 1.0) < 1e-6 and abs(st.phi_big[0, 0] - 1.0) < 1e-6 and st.yy == 1.0
+    q = sgp.VariationalPosterior(np.zeros((1, 1)), np.ones((1, 1)))
+    assert abs(sgp.psi1_expected(q, [[0.0]], k)[0, 0] - 1 / np.sqrt(2)) < 1e-15
+    assert abs(sgp.psi2_expected(q, [[0.0]], k)[0, 0] - 1 / np.sqrt(3)) < 1e-6
+    assert sgp.psi0_expected(sgp.VariationalPosterior(np.zeros((10, 1)), np.ones((10, 1))), sgp.KernelSpec(2.0, [1.0])) == 20.0
+
+
+def test_errors_match_reference(sgp):
+    k = sgp.KernelSpec(1.0, [1.0])
+    with pytest.raises(ValueError, match="variances must be positive"):
+        sgp.stats_expected(sgp.VariationalPosterior(np.zeros((4, 1)), np.zeros((4, 1))), np.zeros((4, 1)), [[0.0]], k)
+    bad = np.zeros((4, 1))
+    bad[2, 0] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        sgp.stats_deterministic(bad, np.zeros((4, 1)), [[0.0]], k)
+    with pytest.raises(ValueError, match="symmetric"):
+        sgp.sweep_stats(True, np.zeros((4, 1)), np.ones((4, 1)), np.zeros((4, 1)), [[0.0], [1.0]], k,
+                        adj=sgp.StatsAdjoints(0.0, np.zeros((2, 1)), np.array([[0.0, 1.0], [0.0, 0.0]])))
+    with pytest.raises(ValueError, match="kernel dimension"):
+        sgp.stats_deterministic(np.zeros((4, 2)), np.zeros((4, 1)), np.zeros((1, 2)), k)
+    # N == 0: zero statistics, no launch
+    st = sgp.stats_deterministic(np.zeros((0, 1)), np.zeros((0, 2)), [[0.0]], k)
+    assert st.phi == 0.0 and st.n_count == 0 and np.all(st.phi_big == 0)
+
+
+def test_bitwise_determinism(sgp):
+    mu, s, y, z, var, ls = problem(4, 5000, 10, 10, 100)
+    k = sgp.KernelSpec(var, ls)
+    rng = np.random.default_rng(0)
+    adj = sgp.StatsAdjoints(*sym_adj(rng, 100, 10))
+    a = sgp.sweep_stats(True, mu, s, y, z, k, adj=adj)
+    b = sgp.sweep_stats(True, mu, s, y, z, k, adj=adj)
+    assert np.array_equal(a[0].phi_big, b[0].phi_big) and np.array_equal(a[0].psi_y, b[0].psi_y)
+    assert np.array_equal(a[1].d_mu, b[1].d_mu) and np.array_equal(a[1].d_z, b[1].d_z)
+
+
+@pytest.mark.parametrize("latent", [True, False])
+def test_engine_evaluate_parity(sgp, orc, latent):
+    """Engine::evaluate(true): bound and every gradient segment vs the oracle engine."""
+    mu, s, y, z, var, ls = problem(6, 3000, 10, 10, 100)
+    beta = 100.0
+    k = sgp.KernelSpec(var, ls)
+    eng = sgp.Engine(sgp.ModelKind.latent if latent else sgp.ModelKind.regression, mu, s if latent else None, y)
+    eng.broadcast(k, beta, z)
+    r = eng.evaluate(True)
+    ref = orc.engine_evaluate(latent, mu, s, y, z, var, ls, beta, workers=4)
+    assert rel_err(r.bound.total, ref.bound["total"]) < BOUND_TOL
+    for f in sgp.BOUND_FIELDS:
+        assert rel_err(getattr(r.bound, f), ref.bound[f]) < BOUND_TOL, f
+    g = r.grads
+    assert norm_rel_err(g.d_z, ref.d_z) < GRAD_TOL
+    assert norm_rel_err(g.d_lengthscales, ref.d_lengthscales) < GRAD_TOL
+    assert rel_err(g.d_variance, ref.d_variance) < GRAD_TOL * max(1.0, abs(ref.d_variance)) ** 0 or \
+        norm_rel_err(g.d_variance, ref.d_variance) < GRAD_TOL
+    assert norm_rel_err(g.d_beta, ref.d_beta) < GRAD_TOL
+    if latent:
+        assert norm_rel_err(g.d_mu, ref.d_mu) < GRAD_TOL
+        assert norm_rel_err(g.d_s, ref.d_s) < GRAD_TOL
