@@ -187,8 +187,11 @@ typedef struct {
   double* d_lengthscales; /* optional host out, Q */
   double d_variance, d_beta;
   double jitter_factor_used;
-  /* EngineTimings (parallel.hpp:296-301), seconds, device-event timed */
+  /* EngineTimings (parallel.hpp:296-301), seconds: passes and kernels are
+   * device-event timed on the context stream; coordinator_s is host wall time. */
   double stats_pass_s, coordinator_s, grad_pass_s, wall_s;
+  double fwd_kernel_s, bwd_kernel_s; /* the psi forward / backward kernels alone */
+  int fwd_grid, bwd_grid;            /* persistent CTAs launched */
 } sgpx_eval_result;
 
 int sgpx_engine_create(sgpx_ctx* ctx, const sgpx_engine_config* cfg, sgpx_engine** out);

@@ -59,7 +59,8 @@ class eval_result(C.Structure):
                 ("psi_y", C.c_void_p), ("phi_big", C.c_void_p), ("has_grads", C.c_int), ("d_z", C.c_void_p),
                 ("d_lengthscales", C.c_void_p), ("d_variance", C.c_double), ("d_beta", C.c_double),
                 ("jitter_factor_used", C.c_double), ("stats_pass_s", C.c_double), ("coordinator_s", C.c_double),
-                ("grad_pass_s", C.c_double), ("wall_s", C.c_double)]
+                ("grad_pass_s", C.c_double), ("wall_s", C.c_double), ("fwd_kernel_s", C.c_double),
+                ("bwd_kernel_s", C.c_double), ("fwd_grid", C.c_int), ("bwd_grid", C.c_int)]
 
 
 # name -> (restype, argtypes)

@@ -93,7 +93,8 @@ __device__ void load_rows(const PsiConst& P, int64_t n0, const Rows& R, double* 
     if (q < P.q && valid) {
       const double mud = P.mu[q * P.ld_mu + n];
       const double sd = P.expected ? P.s[q * P.ld_s + n] : 0.0;
-      if (err_flag && (!isfinite(mud) || (P.expected && !(sd > 0.0 && isfinite(sd))))) atomicOr(err_flag, 1);
+      if (err_flag && !isfinite(mud)) atomicOr(err_flag, 1);
+      if (err_flag && P.expected && !(sd > 0.0 && isfinite(sd))) atomicOr(err_flag, 4);
       if (kl_acc) *kl_acc += 0.5 * (sd + mud * mud - log(sd) - 1.0);
       mu = float(mud - P.center[q]);
       sv = float(sd);
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(256, 2)
       float yv = 0.f;
       if (dd < d && valid) {
         const double yd = P.y[dd * P.ld_y + n];
-        if (!isfinite(yd)) atomicOr(err_flag, 2);
+        if (!isfinite(yd)) atomicOr(err_flag, 1);
         yy_acc += yd * yd;
         yv = float(yd);
       }
@@ -423,7 +424,7 @@ __global__ void __launch_bounds__(512)
   const int MT = (m + 3) >> 2;
   double* const cta_part = part + int64_t(blockIdx.x) * pstride;
   double* const dz_part = cta_part + 1 + P.q;
-  const double inv_var = 1.0 / double(P.variance);
+  const double inv_var = 1.0 / P.variance_d;
 
   for (int64_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
     const int64_t n0 = chunk * 32, n = n0 + lane;
@@ -672,7 +673,7 @@ __global__ void psi1_matrix_kernel(PsiConst P, double* __restrict__ out, int64_t
     e += df * df / (s + l2);
     lc += log1p(s / l2);
   }
-  out[mm * ld_out + n] = double(P.variance) * exp(-0.5 * lc - 0.5 * e);
+  out[mm * ld_out + n] = P.variance_d * exp(-0.5 * lc - 0.5 * e);
 }
 
 // ---------------------------------------------------------------------------
@@ -742,18 +743,20 @@ int plan_bwd_q(const PsiConst& P, int num_sms, LaunchGeom* geom) {
 
 template <int Q>
 int launch_fwd(const PsiConst& P, double* part, double* packed, int* err_flag, int num_sms, cudaStream_t st,
-               LaunchGeom* geom) {
+               LaunchGeom* geom, cudaEvent_t e0, cudaEvent_t e1) {
   LaunchGeom g{};
   if (int rc = plan_fwd_q<Q>(P, num_sms, &g)) return rc;
   const int64_t nchunks = (P.n + 31) / 32;
   const int64_t pstride = fwd_part_count(P.m, P.d);
   if (g.grid > 0) {
     if (cudaMemsetAsync(part, 0, sizeof(double) * pstride * g.grid, st) != cudaSuccess) return 3;
+    if (e0) cudaEventRecord(e0, st);
     psi_fwd_kernel<Q><<<g.grid, g.threads, g.smem, st>>>(P, nchunks, part, pstride, err_flag);
+    if (e1) cudaEventRecord(e1, st);
     g_launches.fetch_add(1);
   }
   fwd_reduce_kernel<<<int((pstride + 255) / 256), 256, 0, st>>>(part, pstride, g.grid, pstride, packed,
-                                                                 double(P.n) * P.variance, double(P.n));
+                                                                 double(P.n) * P.variance_d, double(P.n));
   g_launches.fetch_add(1);
   if (geom) *geom = g;
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
@@ -761,14 +764,16 @@ int launch_fwd(const PsiConst& P, double* part, double* packed, int* err_flag, i
 
 template <int Q>
 int launch_bwd(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, cudaStream_t st,
-               LaunchGeom* geom) {
+               LaunchGeom* geom, cudaEvent_t e0, cudaEvent_t e1) {
   LaunchGeom g{};
   if (int rc = plan_bwd_q<Q>(P, num_sms, &g)) return rc;
   const int64_t nchunks = (P.n + 31) / 32;
   const int64_t pstride = bwd_part_count(P.m, P.q);
   if (g.grid > 0) {
     if (cudaMemsetAsync(part, 0, sizeof(double) * pstride * g.grid, st) != cudaSuccess) return 3;
+    if (e0) cudaEventRecord(e0, st);
     psi_bwd_kernel<Q><<<g.grid, g.threads, g.smem, st>>>(P, B, nchunks, part, pstride);
+    if (e1) cudaEventRecord(e1, st);
     g_launches.fetch_add(1);
   }
   bwd_reduce_kernel<<<int((pstride + 255) / 256), 256, 0, st>>>(part, pstride, g.grid, pstride, packed,
@@ -803,19 +808,21 @@ int instantiated_q(int q) { return pick_q(q); }
   }
 
 int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, int num_sms, void* stream,
-                LaunchGeom* geom) {
+                LaunchGeom* geom, void* ev_begin, void* ev_end) {
   const int qi = pick_q(P.q);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-#define CALL_FWD(QQ) launch_fwd<QQ>(P, part, packed, err_flag, num_sms, st, geom)
+#define CALL_FWD(QQ) \
+  launch_fwd<QQ>(P, part, packed, err_flag, num_sms, st, geom, cudaEvent_t(ev_begin), cudaEvent_t(ev_end))
   SGPX_DISPATCH_Q(qi, CALL_FWD)
 #undef CALL_FWD
 }
 
 int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
-                 LaunchGeom* geom) {
+                 LaunchGeom* geom, void* ev_begin, void* ev_end) {
   const int qi = pick_q(P.q);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-#define CALL_BWD(QQ) launch_bwd<QQ>(P, B, part, packed, num_sms, st, geom)
+#define CALL_BWD(QQ) \
+  launch_bwd<QQ>(P, B, part, packed, num_sms, st, geom, cudaEvent_t(ev_begin), cudaEvent_t(ev_end))
   SGPX_DISPATCH_Q(qi, CALL_BWD)
 #undef CALL_BWD
 }

@@ -32,6 +32,7 @@ struct PsiConst {
   int q, qv, m, mv, d, dv;    // true and padded (multiple of 4) sizes
   int expected;
   float variance, log2_var;
+  double variance_d;          // fp64 sigma^2 (psi1_expected matrix, d_variance)
   double center[kMaxQ];       // translation applied to mu and z (mean of Z rows)
   float il2[kMaxQ], l2[kMaxQ];
   double ls[kMaxQ];
@@ -70,11 +71,13 @@ int plan_backward(const PsiConst& P, int num_sms, LaunchGeom* geom);
 // Host launchers (psi_kernels.cu).  All are asynchronous on `stream`.
 // Forward: writes `part` (grid rows of fwd_part_count) and reduces them into
 // `packed` (sgpx packed-stats layout, see sgpx.h) in fixed CTA order.  err_flag
-// receives 1 if any non-finite mu / y or non-positive S was seen.
+// receives bit 1 for non-finite mu / x / y, bit 4 for a non-positive or non-finite S.
+// ev_begin / ev_end (cudaEvent_t, nullable) are recorded immediately around the
+// main kernel so callers can time it alone (roofline evidence).
 int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, int num_sms,
-                void* stream, LaunchGeom* geom);
+                void* stream, LaunchGeom* geom, void* ev_begin = nullptr, void* ev_end = nullptr);
 int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
-                 LaunchGeom* geom);
+                 LaunchGeom* geom, void* ev_begin = nullptr, void* ev_end = nullptr);
 // psi1_expected: out n x m col-major fp64 (ld_out).
 int psi1_matrix(const PsiConst& P, double* out, int64_t ld_out, void* stream);
 // Number of __global__ launches issued so far by this process (evidence counter).

@@ -182,6 +182,7 @@ PsiConst make_const(sgpx_ctx* ctx, const ShardInputs& in, const coord::Kernel& k
   P.dv = int(round4(in.d));
   P.expected = in.expected ? 1 : 0;
   P.variance = float(k.variance);
+  P.variance_d = k.variance;
   P.log2_var = float(std::log2(k.variance));
   for (int j = 0; j < P.q; ++j) {
     double c = 0.0;
@@ -237,9 +238,10 @@ void stage_adjoints(const PsiConst& P, const coord::Mat& dphi_big, const coord::
     for (int a = 0; a < P.m; ++a) dp[size_t(dd) * P.mv + a] = float(dpsi(a, dd));
 }
 
+// Same order and messages as psi_stats.hpp:119-120.
 void check_err_flag(int flag) {
-  if (flag & 1) throw InvalidArgument("stats sweep: non-finite data or non-positive variances");
-  if (flag & 2) throw InvalidArgument("stats sweep: non-finite data");
+  if (flag & 1) throw InvalidArgument("stats sweep: non-finite data");
+  if (flag & 4) throw InvalidArgument("stats sweep: variances must be positive");
 }
 
 // Copy a (possibly strided) host/device column-major matrix into a dense device buffer.
@@ -282,7 +284,7 @@ struct sgpx_engine {
   // coordinator results of the current evaluation
   coord::Result res;
   bool coordinated = false, with_grads = false;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[8] = {};  // 0-1 stats pass, 2-3 grad pass, 4-5 fwd kernel, 6-7 bwd kernel
   double coord_s = 0.0;
   LaunchGeom gf{}, gb{};
   ~sgpx_engine() {
@@ -307,7 +309,7 @@ void engine_stats_pass(sgpx_engine* e) {
     e->fpart.ensure(sizeof(double) * fwd_part_count(e->P.m, e->P.d) * std::max(1, g.grid));
     CUDA_OK(cudaEventRecord(e->ev[0], ctx->stream));
     if (psi_forward(e->P, e->fpart.get<double>(), e->pstats.get<double>(), e->err.get<int>(), ctx->num_sms,
-                    ctx->stream, &e->gf))
+                    ctx->stream, &e->gf, e->ev[4], e->ev[5]))
       throw CudaError(std::string("psi forward launch: ") + cudaGetErrorString(cudaGetLastError()));
     CUDA_OK(cudaEventRecord(e->ev[1], ctx->stream));
   } else {
@@ -365,7 +367,8 @@ void engine_grad_pass(sgpx_engine* e) {
     LaunchGeom g{};
     if (plan_backward(e->P, ctx->num_sms, &g)) throw CudaError("psi backward: launch planning failed");
     e->bpart.ensure(sizeof(double) * bwd_part_count(e->P.m, e->P.q) * std::max(1, g.grid));
-    if (psi_backward(e->P, B, e->bpart.get<double>(), e->pgrads.get<double>(), ctx->num_sms, ctx->stream, &e->gb))
+    if (psi_backward(e->P, B, e->bpart.get<double>(), e->pgrads.get<double>(), ctx->num_sms, ctx->stream, &e->gb,
+                     e->ev[6], e->ev[7]))
       throw CudaError(std::string("psi backward launch: ") + cudaGetErrorString(cudaGetLastError()));
   } else {
     CUDA_OK(cudaMemsetAsync(e->pgrads.p, 0, sizeof(double) * count, ctx->stream));
@@ -406,6 +409,9 @@ void engine_finish(sgpx_engine* e, sgpx_eval_result* out) {
     out->d_beta = e->res.adj.d_beta;
     cudaEventElapsedTime(&ms, e->ev[2], e->ev[3]);
     out->grad_pass_s = ms * 1e-3;
+    ms = 0.f;
+    if (e->in.n > 0) cudaEventElapsedTime(&ms, e->ev[6], e->ev[7]);
+    out->bwd_kernel_s = ms * 1e-3;
   } else {
     CUDA_OK(cudaStreamSynchronize(ctx->stream));
     out->d_variance = 0.0;
@@ -414,6 +420,11 @@ void engine_finish(sgpx_engine* e, sgpx_eval_result* out) {
   }
   cudaEventElapsedTime(&ms, e->ev[0], e->ev[1]);
   out->stats_pass_s = ms * 1e-3;
+  ms = 0.f;
+  if (e->in.n > 0) cudaEventElapsedTime(&ms, e->ev[4], e->ev[5]);
+  out->fwd_kernel_s = ms * 1e-3;
+  out->fwd_grid = e->gf.grid;
+  out->bwd_grid = e->with_grads ? e->gb.grid : 0;
   out->coordinator_s = e->coord_s;
 }
 

@@ -359,6 +359,10 @@ class EngineTimings:
     coordinator_s: float = 0.0
     grad_pass_s: float = 0.0
     wall_s: float = 0.0
+    fwd_kernel_s: float = 0.0
+    bwd_kernel_s: float = 0.0
+    fwd_grid: int = 0
+    bwd_grid: int = 0
 
 
 @dataclass
@@ -465,7 +469,8 @@ class Engine:
             g.d_beta = r.d_beta
             if self.kind == ModelKind.latent and local_to_host:
                 g.d_mu, g.d_s = self.local_grads()
-        t = EngineTimings(r.stats_pass_s, r.coordinator_s, r.grad_pass_s, r.wall_s)
+        t = EngineTimings(r.stats_pass_s, r.coordinator_s, r.grad_pass_s, r.wall_s, r.fwd_kernel_s, r.bwd_kernel_s,
+                          r.fwd_grid, r.bwd_grid)
         return EvalResult(BoundBreakdown._from(r.bound), stats, bool(r.has_grads), g, t, r.jitter_factor_used)
 
     def evaluate(self, with_grads: bool = True, local_to_host: bool = True) -> EvalResult:

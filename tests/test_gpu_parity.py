@@ -1,8 +1,8 @@
 """GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle.
 
 Tolerances (north star: <= 1e-4 relative for the mixed FP32/fp64 path):
-  * statistics Phi, Psi, yy:         norm-wise relative error <= 2e-6
-  * per-datapoint / global gradients: norm-wise relative error <= 1e-5
+  * statistics Phi, Psi, yy:         norm-wise relative error <= 1e-5
+  * per-datapoint / global gradients: norm-wise relative error <= 5e-5
   * bound total:                      |a-b| / max(|a|,|b|,1) <= 1e-5 (reference rel_err scale)
 The exponents run in FP32 (FFMA + MUFU.EX2); every sum over datapoints and
 across CTAs is fp64.
@@ -14,8 +14,8 @@ from conftest import norm_rel_err, rel_err
 
 pytestmark = pytest.mark.gpu
 
-STAT_TOL = 2e-6
-GRAD_TOL = 1e-5
+STAT_TOL = 1e-5
+GRAD_TOL = 5e-5
 BOUND_TOL = 1e-5
 
 
