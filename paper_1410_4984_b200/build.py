@@ -28,7 +28,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, os.path.basename(src) + ".o")
-        cmd = [NVCC, "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-O3", "-x",
+        cmd = [NVCC, "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-O3,-march=x86-64-v3", "-x",
                "cu" if src.endswith(".cu") else "c++", "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")

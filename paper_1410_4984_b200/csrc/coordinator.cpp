@@ -68,11 +68,30 @@ Mat gemm(const Mat& A, bool ta, const Mat& B, bool tb) {
   const int64_t m = ta ? A.c : A.r, k = ta ? A.r : A.c, n = tb ? B.r : B.c;
   Mat C(m, n);
   if (!ta) {
-    for (int64_t j = 0; j < n; ++j) {
+    // C[:, j..j+3] += A[:, p] * B(p, j..j+3): each A column is streamed once per 4 output columns.
+    int64_t j = 0;
+    for (; j + 4 <= n; j += 4) {
+      double* __restrict__ c0 = C.col(j);
+      double* __restrict__ c1 = C.col(j + 1);
+      double* __restrict__ c2 = C.col(j + 2);
+      double* __restrict__ c3 = C.col(j + 3);
+      for (int64_t p = 0; p < k; ++p) {
+        const double b0 = tb ? B(j, p) : B(p, j), b1 = tb ? B(j + 1, p) : B(p, j + 1);
+        const double b2 = tb ? B(j + 2, p) : B(p, j + 2), b3 = tb ? B(j + 3, p) : B(p, j + 3);
+        const double* __restrict__ ap = A.col(p);
+        for (int64_t i = 0; i < m; ++i) {
+          const double a = ap[i];
+          c0[i] += a * b0;
+          c1[i] += a * b1;
+          c2[i] += a * b2;
+          c3[i] += a * b3;
+        }
+      }
+    }
+    for (; j < n; ++j) {
       double* cj = C.col(j);
       for (int64_t p = 0; p < k; ++p) {
         const double b = tb ? B(j, p) : B(p, j);
-        if (b == 0.0) continue;
         const double* ap = A.col(p);
         for (int64_t i = 0; i < m; ++i) cj[i] += ap[i] * b;
       }
@@ -104,11 +123,31 @@ static void symmetrize(Mat& a) {
 }
 
 Mat chol_inverse(const Mat& L) {
+  // W = L^{-1} (lower triangular, column-oriented forward substitution), then
+  // (L L^T)^{-1} = W^T W computed as dot products of W's columns (exactly symmetric).
   const int64_t n = L.r;
+  Mat W(n, n);
+  for (int64_t j = 0; j < n; ++j) {
+    double* x = W.col(j);
+    x[j] = 1.0;
+    for (int64_t k = j; k < n; ++k) {
+      x[k] /= L(k, k);
+      const double xk = x[k];
+      const double* lk = L.col(k);
+      for (int64_t i = k + 1; i < n; ++i) x[i] -= lk[i] * xk;
+    }
+  }
   Mat X(n, n);
-  for (int64_t i = 0; i < n; ++i) X(i, i) = 1.0;
-  chol_solve(L, X);
-  symmetrize(X);
+  for (int64_t j = 0; j < n; ++j) {
+    const double* wj = W.col(j);
+    for (int64_t i = j; i < n; ++i) {
+      const double* wi = W.col(i);
+      double s = 0.0;
+      for (int64_t k = i; k < n; ++k) s += wi[k] * wj[k];  // rows k >= max(i, j) = i
+      X(i, j) = s;
+      X(j, i) = s;
+    }
+  }
   return X;
 }
 
@@ -212,9 +251,8 @@ Result coordinate(bool latent, int64_t n, int64_t d, const Stats& st, const Mat&
   Mat La;
   if (!factor_spd(a, La)) throw NumericError("bound (Kmm + beta*Phi): Cholesky factorization failed after jitter escalation");
   const double log_det_a = log_det_chol(La);
-  Mat g = st.psi_y;
-  chol_solve(La, g);
   const Mat a_inv = chol_inverse(La);
+  const Mat g = gemm(a_inv, false, st.psi_y, false);
   const Mat kmm_inv = chol_inverse(Lk);
   const double log_2pi = 1.8378770664093454835606594728112;
   const double nd = double(n), dd = double(d);
@@ -262,34 +300,50 @@ Result coordinate(bool latent, int64_t n, int64_t d, const Stats& st, const Mat&
 }
 
 KernGrads kern_grads_zz(const Mat& z, const Kernel& k, const Mat& up) {
+  // kern_grads(Z, Z, k, U) (kernels.hpp:124-164) with d_z + d_x summed, for a symmetric
+  // upstream U = dL/dKmm.  With W = U o K (Hadamard), sum over both slots:
+  //   d_z + d_x = 2 (W Z - diag(W 1) Z) / l^2,   d_l_q = sum_nm W_nm (z_nq - z_mq)^2 / l_q^3,
+  //   d_variance = sum W / variance.
   const int64_t m = z.r, q = z.c;
-  std::vector<double> il2(q), il3(q);
-  for (int64_t j = 0; j < q; ++j) {
-    const double l = k.ls[j];
-    il2[j] = 1.0 / (l * l);
-    il3[j] = 1.0 / (l * l * l);
-  }
-  KernGrads g;
-  g.d_ls.assign(q, 0.0);
-  g.d_z = Mat(m, q);
-  Mat dx(m, q);
-  for (int64_t mm = 0; mm < m; ++mm)
-    for (int64_t nn = 0; nn < m; ++nn) {
+  std::vector<double> il2(q);
+  for (int64_t j = 0; j < q; ++j) il2[j] = 1.0 / (k.ls[j] * k.ls[j]);
+  Mat zs(m, q);  // z / l
+  for (int64_t j = 0; j < q; ++j)
+    for (int64_t a = 0; a < m; ++a) zs(a, j) = z(a, j) / k.ls[j];
+  Mat W(m, m);
+  for (int64_t b = 0; b < m; ++b)
+    for (int64_t a = b; a < m; ++a) {
       double d2 = 0.0;
       for (int64_t j = 0; j < q; ++j) {
-        const double dlt = z(nn, j) - z(mm, j);
-        d2 += dlt * dlt * il2[j];
+        const double d = zs(a, j) - zs(b, j);
+        d2 += d * d;
       }
-      const double uv = up(nn, mm) * k.variance * std::exp(-0.5 * d2);
-      g.d_variance += uv / k.variance;
-      for (int64_t j = 0; j < q; ++j) {
-        const double dlt = z(nn, j) - z(mm, j);
-        dx(nn, j) -= uv * dlt * il2[j];
-        g.d_z(mm, j) += uv * dlt * il2[j];
-        g.d_ls[j] += uv * dlt * dlt * il3[j];
-      }
+      const double kv = k.variance * std::exp(-0.5 * d2);
+      W(a, b) = up(a, b) * kv;
+      W(b, a) = up(b, a) * kv;
     }
-  for (size_t i = 0; i < g.d_z.v.size(); ++i) g.d_z.v[i] += dx.v[i];
+  KernGrads g;
+  g.d_ls.assign(q, 0.0);
+  std::vector<double> rs(m, 0.0);
+  double tot = 0.0;
+  for (int64_t b = 0; b < m; ++b)
+    for (int64_t a = 0; a < m; ++a) {
+      rs[a] += W(a, b);
+      tot += W(a, b);
+    }
+  g.d_variance = tot / k.variance;
+  const Mat WZ = gemm(W, false, z, false);  // M x Q
+  g.d_z = Mat(m, q);
+  for (int64_t j = 0; j < q; ++j) {
+    double s2 = 0.0, cross = 0.0;
+    for (int64_t a = 0; a < m; ++a) {
+      g.d_z(a, j) = 2.0 * (WZ(a, j) - rs[a] * z(a, j)) * il2[j];
+      s2 += rs[a] * z(a, j) * z(a, j);
+      cross += z(a, j) * WZ(a, j);
+    }
+    // sum_ab W_ab (z_a - z_b)^2 = 2 (sum_a rs_a z_a^2 - z^T W z) for symmetric W
+    g.d_ls[j] = 2.0 * (s2 - cross) * il2[j] / k.ls[j];
+  }
   return g;
 }
 
