@@ -75,7 +75,7 @@ class ClockSampler:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
                                          stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -203,8 +203,13 @@ def run_b200(args, world, rank, local_rank):
     kernel = sgp.KernelSpec(VARIANCE, np.full(q, LENGTHSCALE))
     stream = torch.cuda.current_stream(dev)
 
+    use_dist = world > 1 or args.force_dist
+    if use_dist and dist is None:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
     eng = DistributedEngine(sgp.ModelKind.latent, mu, s, y, n_global, row_begin,
-                            passes=None) if world > 1 else None
+                            passes=None) if use_dist else None
     if eng is None:
         ctx = sgp.Context(local_rank)
         ctx.set_stream(stream.cuda_stream)
@@ -287,7 +292,10 @@ def run_b200(args, world, rank, local_rank):
     mu_h.copy_(mu.t())
     s_h.copy_(s.t())
     mu_np, s_np = mu_h.numpy().T, s_h.numpy().T  # Fortran-ordered views of pinned memory
+    gmu_h = torch.empty(q, n_local, dtype=torch.float64, pin_memory=True)
+    gs_h = torch.empty(q, n_local, dtype=torch.float64, pin_memory=True)
     target = single if eng is None else eng
+    target.set_local_grads_out(gmu_h.numpy().T, gs_h.numpy().T)
     for _ in range(max(1, args.warmup // 2)):
         target.broadcast(kernel, BETA, z, mu_np, s_np)
         evaluate(True)
@@ -348,13 +356,14 @@ def run_b200(args, world, rank, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS))
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--cpu-sample", type=int, default=32768)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--force-dist", action="store_true", help="use DistributedEngine (NCCL) even at world size 1")
     args = ap.parse_args()
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)

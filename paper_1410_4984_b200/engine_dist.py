@@ -109,6 +109,9 @@ class DistributedEngine:
     def broadcast(self, kernel: sgp.KernelSpec, beta: float, z, mu=None, s=None):
         self.passes.broadcast(kernel, beta, z, mu, s)
 
+    def set_local_grads_out(self, dmu, ds):
+        self.passes.eng.set_local_grads_out(dmu, ds)
+
     def evaluate(self, with_grads: bool = True, local_to_host: bool = True) -> sgp.EvalResult:
         packed = self.passes.stats_pass()
         self.dist.all_reduce(packed, op=self.dist.ReduceOp.SUM, group=self.group)  # allreduce #1

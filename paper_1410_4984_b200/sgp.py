@@ -459,6 +459,10 @@ class Engine:
         r.d_lengthscales = bufs["d_ls"].ctypes.data_as(C.c_void_p)
         return r, bufs
 
+    def set_local_grads_out(self, dmu, ds):
+        """Preallocated host buffers (pinned for speed) that evaluate() fills with d_mu / d_s."""
+        self._grads_out = (dmu, ds)
+
     def _pack(self, r, bufs, with_grads, local_to_host=True) -> EvalResult:
         stats = SufficientStats(r.phi, bufs["psi_y"], bufs["phi_big"], r.yy, int(r.n_count))
         g = GradientParts()
@@ -468,7 +472,7 @@ class Engine:
             g.d_variance = r.d_variance
             g.d_beta = r.d_beta
             if self.kind == ModelKind.latent and local_to_host:
-                g.d_mu, g.d_s = self.local_grads()
+                g.d_mu, g.d_s = self.local_grads(getattr(self, "_grads_out", None))
         t = EngineTimings(r.stats_pass_s, r.coordinator_s, r.grad_pass_s, r.wall_s, r.fwd_kernel_s, r.bwd_kernel_s,
                           r.fwd_grid, r.bwd_grid)
         return EvalResult(BoundBreakdown._from(r.bound), stats, bool(r.has_grads), g, t, r.jitter_factor_used)
@@ -479,10 +483,17 @@ class Engine:
         check(self._lib.sgpx_engine_evaluate(self._h, 1 if with_grads else 0, C.byref(r)))
         return self._pack(r, bufs, with_grads, local_to_host)
 
-    def local_grads(self):
+    def local_grads(self, out=None):
+        """(d_mu, d_s) on the host, n_local x Q.  ``out``: optional preallocated Fortran-ordered
+        float64 pair (e.g. views of pinned memory) to avoid a pageable copy."""
         n, q = self.n, self.q
-        dmu = np.zeros((n, q), order="F")
-        ds = np.zeros((n, q), order="F")
+        if out is None:
+            dmu = np.zeros((n, q), order="F")
+            ds = np.zeros((n, q), order="F")
+        else:
+            dmu, ds = out
+            if not (dmu.flags.f_contiguous and ds.flags.f_contiguous and dmu.shape == (n, q) == ds.shape):
+                raise SgpxInvalidArgument("local_grads out= must be two Fortran-ordered n_local x Q arrays")
         check(self._lib.sgpx_engine_copy_local_grads(self._h, _cm(dmu), _cm(ds)))
         return dmu, ds
 
