@@ -78,6 +78,17 @@ int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, 
                 void* stream, LaunchGeom* geom, void* ev_begin = nullptr, void* ev_end = nullptr);
 int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
                  LaunchGeom* geom, void* ev_begin = nullptr, void* ev_end = nullptr);
+// Tensor-core (tcgen05) variants, psi_tc.cu.  tc_supported: shapes they handle (M <= 128, Q <= 32).
+bool tc_supported(const PsiConst& P);
+bool tc_backward_available();
+bool use_tc(const PsiConst& P, bool backward);
+int plan_forward_tc(const PsiConst& P, int num_sms, LaunchGeom* geom);
+int psi_forward_tc(const PsiConst& P, double* part, double* packed, int* err_flag, int num_sms, void* stream,
+                   LaunchGeom* geom, void* ev_begin, void* ev_end);
+int plan_backward_tc(const PsiConst& P, int num_sms, LaunchGeom* geom);
+int psi_backward_tc(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
+                    LaunchGeom* geom, void* ev_begin, void* ev_end);
+
 // psi1_expected: out n x m col-major fp64 (ld_out).
 int psi1_matrix(const PsiConst& P, double* out, int64_t ld_out, void* stream);
 // Number of __global__ launches issued so far by this process (evidence counter).
