@@ -622,7 +622,7 @@ bool use_tc(const PsiConst& P, bool backward) {
     return 0;
   }();
   if (forced == 1) return false;
-  if (backward && !tc_backward_available()) return false;
+  if (backward) return tc_backward_available() && tc_backward_fits(P);
   return tc_supported(P);
 }
 
@@ -659,6 +659,7 @@ int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, 
 
 int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
                  LaunchGeom* geom, void* ev_begin, void* ev_end) {
+  if (use_tc(P, true)) return psi_backward_tc(P, B, part, packed, num_sms, stream, geom, ev_begin, ev_end);
   const int qi = pick_q(P.q);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 #define CALL_BWD(QQ) \
@@ -676,6 +677,7 @@ int plan_forward(const PsiConst& P, int num_sms, LaunchGeom* geom) {
 }
 
 int plan_backward(const PsiConst& P, int num_sms, LaunchGeom* geom) {
+  if (use_tc(P, true)) return plan_backward_tc(P, num_sms, geom);
   const int qi = pick_q(P.q);
 #define CALL_PB(QQ) plan_bwd_q<QQ>(P, num_sms, geom)
   SGPX_DISPATCH_Q(qi, CALL_PB)

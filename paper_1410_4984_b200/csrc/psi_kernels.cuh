@@ -36,6 +36,7 @@ struct PsiConst {
   double center[kMaxQ];       // translation applied to mu and z (mean of Z rows)
   float il2[kMaxQ], l2[kMaxQ];
   double ls[kMaxQ];
+  unsigned long long* prof;   // optional per-phase cycle counters (SGPX_TC_PROFILE=1), else null
 };
 
 // Backward-only inputs.
@@ -81,6 +82,7 @@ int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* pac
 // Tensor-core (tcgen05) variants, psi_tc.cu.  tc_supported: shapes they handle (M <= 128, Q <= 32).
 bool tc_supported(const PsiConst& P);
 bool tc_backward_available();
+bool tc_backward_fits(const PsiConst& P);
 bool use_tc(const PsiConst& P, bool backward);
 int plan_forward_tc(const PsiConst& P, int num_sms, LaunchGeom* geom);
 int psi_forward_tc(const PsiConst& P, double* part, double* packed, int* err_flag, int num_sms, void* stream,

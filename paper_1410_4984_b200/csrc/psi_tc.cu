@@ -17,6 +17,8 @@
 #include <math_constants.h>
 
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 
 #include "psi_common.cuh"
 #include "psi_kernels.cuh"
@@ -30,6 +32,13 @@ namespace {
 using namespace dev;
 
 constexpr int kPipes = 2;
+
+// Per-phase cycle counters (only when P.prof != null): accumulated by lane 0 of each pipeline's
+// first warp.  Slots: 0 prologue, 1 A1 build + barrier, 2 MMA1 wait, 3 element loop, 4 MMA2 issue,
+// 5 MMA2 wait, 6 contraction, 7 epilogue, 8 tiles.
+#define TCP_MARK(var) long long var = P.prof ? clock64() : 0
+#define TCP_ADD(slot, from) \
+  do { if (P.prof && wq == 0 && lane == 0) atomicAdd(P.prof + (slot), (unsigned long long)(clock64() - (from))); } while (0)
 constexpr int kThreadsTC = 128 * kPipes;
 
 __host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
@@ -379,14 +388,454 @@ int launch_fwd_tc_q(const PsiConst& P, double* part, double* packed, int* err_fl
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
+
+// =============================================================================================
+// Backward (gradient pass) on tensor cores.
+// TMEM per pipeline (256 columns): [0, n1) D1 = s, then G_hi in place; [n1, n1+n1) G_lo;
+// [2 n1, 2 n1 + n2) D2 = [R | S].  Requires 2 n1 + n2 <= 256 (M <= 112 with Q <= 15).
+// =============================================================================================
+__device__ __forceinline__ void build_c2(const PsiConst& P, const TCLayout& L, const float* Zc, float* c2) {
+  const int tot = L.n2 * L.k2;
+  for (int i = threadIdx.x; i < tot; i += blockDim.x) {
+    const int j = i / L.k2, b = i - j * L.k2;
+    float x = 0.f;
+    if (b < P.m) x = (j == 0) ? 1.f : (j <= P.q ? Zc[b * P.qv + (j - 1)] : 0.f);
+    const float h = tc::tf32_hi(x);
+    c2[tc::canon(j, b, L.k2)] = h;
+    c2[L.n2 * L.k2 + tc::canon(j, b, L.k2)] = x - h;
+  }
+}
+
+// MMA2: D2 = G (TMEM, hi/lo) * C2^T (smem, hi/lo), 3xTF32.
+__device__ __forceinline__ void issue_mma2(const TCLayout& L, uint32_t base, const float* c2) {
+  const uint32_t idesc = tc::idesc_tf32(128, L.n2);
+  const uint32_t g_hi = base, g_lo = base + L.n1, d2 = base + 2 * L.n1;
+  const uint32_t c_hi = tc::smem_u32(c2), c_lo = c_hi + L.n2 * L.k2 * 4;
+  uint32_t acc = 0;
+  for (int t = 0; t < 3; ++t) {
+    const uint32_t a = (t == 2) ? g_lo : g_hi, c = (t == 1) ? c_lo : c_hi;
+    for (int ks = 0; ks < L.k2 / 8; ++ks) {
+      tc::mma_ts(d2, a + ks * 8, tc::desc(c + ks * 256, L.k2), idesc, acc);
+      acc = 1;
+    }
+  }
+}
+
+size_t bwd_tc_smem_bytes(const PsiConst& P, int Q) {
+  const TCLayout L = tc_layout(P.q, P.m);
+  size_t f = 2 * size_t(L.n1) * L.k1 + kPipes * 2 * 128 * size_t(L.k1) + 2 * size_t(L.n2) * L.k2 +
+             size_t(P.mv) * P.qv + rows_floats(P.qv) + size_t(P.mv) * 32 * 2 + size_t(P.dv) * 32 +
+             size_t(kThreadsTC / 32) * (2 + 5 * Q) * 32;
+  return f * 4 + (Q + 1) * 32 * sizeof(double) + 64;
+}
+
+template <int Q>
+__global__ void __launch_bounds__(kThreadsTC, 1)
+    psi_bwd_tc_kernel(PsiConst P, BwdConst B, int64_t nchunks, double* __restrict__ part, int64_t pstride) {
+  constexpr int NACC = 2 + 5 * Q;
+  constexpr int T0 = 0, Y1 = 1, Y2 = 1 + Q, XX = 1 + 2 * Q, P0 = 1 + 3 * Q, P1 = 2 + 3 * Q, P2 = 2 + 4 * Q;
+  extern __shared__ __align__(1024) float sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5, nthr = blockDim.x;
+  const int m = P.m, mv = P.mv, qv = P.qv, d = P.d;
+  const TCLayout L = tc_layout(P.q, m);
+  float* p = sm;
+  float* B1 = p;
+  p += 2 * L.n1 * L.k1;
+  float* A1 = p;
+  p += kPipes * 2 * 128 * L.k1;
+  float* C2 = p;
+  p += 2 * L.n2 * L.k2;
+  float* Zc = p;
+  p += mv * qv;
+  Rows R = carve_rows(p, qv);
+  float* Ls = p;
+  p += mv * 32;
+  float* Ys = p;
+  p += P.dv * 32;
+  float* G1s = p;
+  p += mv * 32;
+  float* acc = p;
+  p += nw * NACC * 32;
+  double* dacc = reinterpret_cast<double*>(p);  // [(Q+1)][32]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(dacc + (Q + 1) * 32);  // [pipe][2]: MMA1, MMA2 done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2 * kPipes);
+
+  for (int i = tid; i < mv * qv; i += nthr) Zc[i] = P.zc[i];
+  for (int i = tid; i < (Q + 1) * 32; i += nthr) dacc[i] = 0.0;
+  __syncthreads();
+  build_b1(P, L, Zc, B1);
+  build_c2(P, L, Zc, C2);
+  if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
+  if (tid == 0) {
+    for (int i = 0; i < 2 * kPipes; ++i) tc::mbar_init(&mbar[i], 1);
+    tc::mbar_fence_init();
+  }
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int pipe = warp >> 2, wq = warp & 3;
+  const uint32_t base = tmem + pipe * 256;
+  const uint32_t lane_off = uint32_t(32 * wq) << 16;
+  float* a1 = A1 + pipe * 2 * 128 * L.k1;
+  uint32_t ph1 = 0, ph2 = 0;
+  const int MT = (m + 3) >> 2;
+  double* const cta_part = part + int64_t(blockIdx.x) * pstride;
+  double* const dz_part = cta_part + 1 + P.q;
+  const double inv_var = 1.0 / P.variance_d;
+
+  for (int64_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
+    const int64_t n0 = chunk * 32, n = n0 + lane;
+    const bool valid = n < P.n;
+    TCP_MARK(tp0);
+    load_rows<Q>(P, n0, R, nullptr, nullptr);
+    build_L<Q>(P, R, Zc, Ls);
+    for (int dd = warp; dd < d; dd += nw) Ys[dd * 32 + lane] = valid ? float(P.y[dd * P.ld_y + n]) : 0.f;
+    __syncthreads();
+    {  // psi1 adjoint weights G1_nm = v1_nm <y_n, dPsi_m>
+      float mu[Q], d1[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        mu[q] = R.mu[q * 32 + lane];
+        d1[q] = R.d1[q * 32 + lane];
+      }
+      const float b1 = R.b1[lane];
+      for (int mt = warp; mt < (mv >> 2); mt += nw) {
+        float w4[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int dd = 0; dd < d; ++dd) {
+          const float yv = Ys[dd * 32 + lane];
+          const float4 dp = __ldg(reinterpret_cast<const float4*>(B.dpsi + int64_t(dd) * mv) + mt);
+          w4[0] = fmaf(yv, dp.x, w4[0]);
+          w4[1] = fmaf(yv, dp.y, w4[1]);
+          w4[2] = fmaf(yv, dp.z, w4[2]);
+          w4[3] = fmaf(yv, dp.w, w4[3]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int mm = 4 * mt + i;
+          float g = 0.f;
+          if (mm < m) {
+            float z[Q];
+            load_z<Q>(Zc + mm * qv, z);
+            float e = 0.f;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+              const float df = mu[q] - z[q];
+              e = fmaf(df * df, d1[q], e);
+            }
+            g = w4[i] * ex2(fmaf(-0.5f * kLog2e, e, b1));
+          }
+          G1s[mm * 32 + lane] = g;
+        }
+      }
+    }
+    __syncthreads();
+
+    // per-datapoint accumulators of this thread (row = (lane, a)), summed over its tiles
+    float t0 = 0.f, p0 = 0.f, y1[Q], y2[Q], xq[Q], p1[Q], p2[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) y1[q] = y2[q] = xq[q] = p1[q] = p2[q] = 0.f;
+    float kk[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) kk[q] = R.kk[q * 32 + lane];
+
+    TCP_ADD(0, tp0);
+    for (int t = pipe; t < MT; t += kPipes) {
+      const int a = 4 * t + wq;
+      const bool va = a < m;
+      const int ac = va ? a : 0;
+      TCP_MARK(tp1);
+      build_a1_row<Q>(L, kk, Zc + ac * qv, va, a1, 32 * wq + lane);
+      tc::fence_async_smem();
+      tc::fence_before();
+      tc::named_sync(1 + pipe, 128);
+      if (wq == 0 && lane == 0) {
+        tc::fence_after();
+        issue_mma1(L, base, a1, B1);
+        tc::commit(&mbar[2 * pipe]);
+      }
+      TCP_ADD(1, tp1);
+      TCP_MARK(tp2);
+      tc::mbar_wait(&mbar[2 * pipe], ph1);
+      ph1 ^= 1;
+      tc::fence_after();
+      TCP_ADD(2, tp2);
+      TCP_MARK(tp3);
+      const float La = Ls[ac * 32 + lane];
+      const float* urow = B.u + int64_t(ac) * mv;  // U symmetric: row a
+      // G = U_ab ex2(s) over all b, written back as G_hi (in place) and G_lo
+      int c = 0;
+      for (; c + 32 <= m; c += 32) {
+        uint32_t r[32], lo[32];
+        tc::ld32(base + lane_off + c, r);
+        tc::ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const float4 u4 = __ldg(reinterpret_cast<const float4*>(urow + c + j));
+          const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int b = c + j + u;
+            const float s = __uint_as_float(r[j + u]) + La + Ls[b * 32 + lane];
+            const float g = va ? uu[u] * ex2(s) : 0.f;
+            const float h = tc::tf32_hi(g);
+            r[j + u] = __float_as_uint(h);
+            lo[j + u] = __float_as_uint(g - h);
+          }
+        }
+        tc::st32(base + lane_off + c, r);
+        tc::st32(base + lane_off + L.n1 + c, lo);
+      }
+      for (; c < L.k2; c += 8) {
+        uint32_t r[8], lo[8];
+        tc::ld8(base + lane_off + c, r);
+        tc::ld_wait();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int b = c + j;
+          float g = 0.f;
+          if (va && b < m) {
+            const float s = __uint_as_float(r[j]) + La + Ls[b * 32 + lane];
+            g = urow[b] * ex2(s);
+          }
+          const float h = tc::tf32_hi(g);
+          r[j] = __float_as_uint(h);
+          lo[j] = __float_as_uint(g - h);
+        }
+        tc::st8(base + lane_off + c, r);
+        tc::st8(base + lane_off + L.n1 + c, lo);
+      }
+      tc::st_wait();
+      TCP_ADD(3, tp3);
+      TCP_MARK(tp4);
+      tc::fence_before();
+      tc::named_sync(1 + pipe, 128);
+      if (wq == 0 && lane == 0) {
+        tc::fence_after();
+        issue_mma2(L, base, C2);
+        tc::commit(&mbar[2 * pipe + 1]);
+      }
+      TCP_ADD(4, tp4);
+      TCP_MARK(tp5);
+      tc::mbar_wait(&mbar[2 * pipe + 1], ph2);
+      ph2 ^= 1;
+      tc::fence_after();
+      TCP_ADD(5, tp5);
+      TCP_MARK(tp6);
+      uint32_t rs[16];
+      tc::ld16(base + lane_off + 2 * L.n1, rs);
+      tc::ld_wait();
+      const float Ra = __uint_as_float(rs[0]);
+      float Sa[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) Sa[q] = (q + 1 < 16) ? __uint_as_float(rs[(q + 1) % 16]) : 0.f;
+      // contractions (natural-log units; G already carries U and v)
+      const float g1 = va ? G1s[a * 32 + lane] : 0.f;
+      t0 += Ra;
+      p0 += g1;
+      float vals[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const float z = Zc[ac * qv + q];
+        y1[q] = fmaf(z, Ra, y1[q]);
+        y2[q] = fmaf(z * z, Ra, y2[q]);
+        xq[q] = fmaf(z, Sa[q], xq[q]);
+        p1[q] = fmaf(z, g1, p1[q]);
+        p2[q] = fmaf(z * z, g1, p2[q]);
+        const float mu = R.mu[q * 32 + lane], d2 = R.d2[q * 32 + lane], d1 = R.d1[q * 32 + lane];
+        const float kn = R.sv[q * 32 + lane] * P.il2[q] * d2;
+        const float c2 = 0.5f * (P.il2[q] + d2);
+        vals[q] = 2.f * (fmaf(d2, mu, -c2 * z) * Ra + kn * Sa[q]) + g1 * d1 * (mu - z);
+      }
+      // reduce the Q d_z values of inducing point a over the 32 datapoints of the chunk
+      constexpr int QR = Q <= 8 ? 8 : (Q <= 16 ? 16 : 32);
+      float vr[QR];
+#pragma unroll
+      for (int i = 0; i < QR; ++i) vr[i] = (i < Q) ? vals[i % Q] : 0.f;
+      const float tot = reduce_scatter<QR>(vr, lane);
+      const int shift = QR == 8 ? 2 : (QR == 16 ? 1 : 0);
+      const int qi = lane >> shift;
+      if (va && qi < P.q && (lane & ((1 << shift) - 1)) == 0) atomicAdd(dz_part + a + int64_t(qi) * m, double(tot));
+      TCP_ADD(6, tp6);
+      if (P.prof && wq == 0 && lane == 0) atomicAdd(P.prof + 8, 1ull);
+    }
+    TCP_MARK(tp7);
+    // merge the per-datapoint accumulators of the 8 warps
+    {
+      float* accw = acc + warp * NACC * 32;
+      accw[T0 * 32 + lane] = t0;
+      accw[P0 * 32 + lane] = p0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        accw[(Y1 + q) * 32 + lane] = y1[q];
+        accw[(Y2 + q) * 32 + lane] = y2[q];
+        accw[(XX + q) * 32 + lane] = xq[q];
+        accw[(P1 + q) * 32 + lane] = p1[q];
+        accw[(P2 + q) * 32 + lane] = p2[q];
+      }
+    }
+    __syncthreads();
+    for (int q = warp; q < P.q; q += nw) {
+      if (!valid) continue;
+      double T = 0, A1s = 0, A2s = 0, X = 0, Q0 = 0, Q1 = 0, Q2 = 0;
+      for (int w2 = 0; w2 < nw; ++w2) {
+        const float* aw = acc + w2 * NACC * 32;
+        T += aw[T0 * 32 + lane];
+        A1s += aw[(Y1 + q) * 32 + lane];
+        A2s += aw[(Y2 + q) * 32 + lane];
+        X += aw[(XX + q) * 32 + lane];
+        Q0 += aw[P0 * 32 + lane];
+        Q1 += aw[(P1 + q) * 32 + lane];
+        Q2 += aw[(P2 + q) * 32 + lane];
+      }
+      const double mu = R.mu[q * 32 + lane], sv = R.sv[q * 32 + lane];
+      const double l = P.ls[q], l2 = l * l, il2 = 1.0 / l2, il3 = il2 / l;
+      const double d2 = 1.0 / (2.0 * sv + l2), d1 = 1.0 / (sv + l2);
+      const double q1 = mu * mu * Q0 - 2.0 * mu * Q1 + Q2;
+      const double dl = T * (2.0 * sv * d2 / l + 2.0 * l * d2 * d2 * mu * mu) - 4.0 * l * d2 * d2 * mu * A1s +
+                        A2s * (il3 + l * d2 * d2) - X * (il3 - l * d2 * d2) + sv * d1 * Q0 / l + l * d1 * d1 * q1;
+      dacc[q * 32 + lane] += dl;
+      if (q == 0) dacc[Q * 32 + lane] += (2.0 * T + Q0) * inv_var;
+      if (B.write_local) {
+        double dmu = -2.0 * d2 * mu * T + 2.0 * d2 * A1s - d1 * (mu * Q0 - Q1);
+        double ds = T * (-d2 + 2.0 * d2 * d2 * mu * mu) - 4.0 * d2 * d2 * mu * A1s + d2 * d2 * (A2s + X) -
+                    0.5 * d1 * Q0 + 0.5 * d1 * d1 * q1;
+        if (B.add_kl) {
+          const double mo = P.mu[q * P.ld_mu + n], so = P.s[q * P.ld_s + n];
+          dmu -= mo;
+          ds -= 0.5 * (1.0 - 1.0 / so);
+        }
+        B.d_mu[q * B.ld_g + n] = dmu;
+        B.d_s[q * B.ld_g + n] = ds;
+      }
+    }
+    __syncthreads();
+    TCP_ADD(7, tp7);
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, 512);
+  }
+  if (tid <= Q) {
+    double s = 0.0;
+    for (int l2i = 0; l2i < 32; ++l2i) s += dacc[tid * 32 + l2i];
+    if (tid < P.q)
+      cta_part[1 + tid] = s;
+    else if (tid == Q)
+      cta_part[0] = s;
+  }
+}
+
+__global__ void bwd_reduce_tc(const double* __restrict__ part, int64_t pstride, int nparts, int64_t count,
+                              double* __restrict__ packed, double dvar0) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < count; k += int64_t(gridDim.x) * blockDim.x) {
+    double s = (k == 0) ? dvar0 : 0.0;
+    for (int c = 0; c < nparts; ++c) s += part[c * pstride + k];
+    packed[k] = s;
+  }
+}
+
+template <int Q>
+int plan_bwd_tc_q(const PsiConst& P, int num_sms, LaunchGeom* geom) {
+  const size_t smem = bwd_tc_smem_bytes(P, Q);
+  if (smem > 227 * 1024) return 1;
+  auto kern = psi_bwd_tc_kernel<Q>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return 3;
+  const int64_t nchunks = (P.n + 31) / 32;
+  *geom = LaunchGeom{int(std::min<int64_t>(nchunks, num_sms)), kThreadsTC, smem};
+  return 0;
+}
+
+unsigned long long* tc_profile_buffer() {
+  static unsigned long long* buf = nullptr;
+  static const bool on = getenv("SGPX_TC_PROFILE") != nullptr;
+  if (on && !buf) {
+    cudaMalloc(&buf, 16 * sizeof(unsigned long long));
+    cudaMemset(buf, 0, 16 * sizeof(unsigned long long));
+  }
+  return on ? buf : nullptr;
+}
+
+void tc_profile_report(const char* what, cudaStream_t st) {
+  unsigned long long* buf = tc_profile_buffer();
+  if (!buf) return;
+  unsigned long long h[16];
+  cudaStreamSynchronize(st);
+  cudaMemcpy(h, buf, sizeof(h), cudaMemcpyDeviceToHost);
+  const char* names[] = {"prologue", "a1+bar", "mma1_wait", "elements", "mma2_issue", "mma2_wait", "contract",
+                         "epilogue"};
+  fprintf(stderr, "[tc-profile %s] tiles/pipe-sum=%llu:", what, h[8]);
+  unsigned long long tot = 0;
+  for (int i = 0; i < 8; ++i) tot += h[i];
+  for (int i = 0; i < 8; ++i) fprintf(stderr, " %s=%.1f%%", names[i], 100.0 * h[i] / (tot ? tot : 1));
+  fprintf(stderr, " (cycles/tile %.0f)\n", double(tot) / double(h[8] ? h[8] : 1));
+  cudaMemset(buf, 0, sizeof(h));
+}
+
+template <int Q>
+int launch_bwd_tc_q(const PsiConst& P0, const BwdConst& B, double* part, double* packed, int num_sms, cudaStream_t st,
+                    LaunchGeom* geom, cudaEvent_t e0, cudaEvent_t e1) {
+  PsiConst P = P0;
+  P.prof = tc_profile_buffer();
+  LaunchGeom g{};
+  if (int rc = plan_bwd_tc_q<Q>(P, num_sms, &g)) return rc;
+  const int64_t nchunks = (P.n + 31) / 32;
+  const int64_t pstride = bwd_part_count(P.m, P.q);
+  if (g.grid > 0) {
+    if (cudaMemsetAsync(part, 0, sizeof(double) * pstride * g.grid, st) != cudaSuccess) return 3;
+    if (e0) cudaEventRecord(e0, st);
+    psi_bwd_tc_kernel<Q><<<g.grid, g.threads, g.smem, st>>>(P, B, nchunks, part, pstride);
+    if (e1) cudaEventRecord(e1, st);
+    g_tc_launches.fetch_add(1);
+  }
+  bwd_reduce_tc<<<int((pstride + 255) / 256), 256, 0, st>>>(part, pstride, g.grid, pstride, packed,
+                                                            B.d_phi * double(P.n));
+  g_tc_launches.fetch_add(1);
+  tc_profile_report("bwd", st);
+  if (geom) *geom = g;
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
 }  // namespace
 
 bool tc_supported(const PsiConst& P) { return P.m >= 1 && P.m <= 128 && P.q >= 1 && P.q <= 32; }
-bool tc_backward_available() { return false; }
-int plan_backward_tc(const PsiConst&, int, LaunchGeom*) { return 1; }
-int psi_backward_tc(const PsiConst&, const BwdConst&, double*, double*, int, void*, LaunchGeom*, void*, void*) {
-  return 1;
+
+// Backward TMEM budget per pipeline: 2 n1 + n2 <= 256 columns.
+bool tc_backward_fits(const PsiConst& P) {
+  const TCLayout L = tc_layout(P.q, P.m);
+  return tc_supported(P) && 2 * L.n1 + L.n2 <= 256 && P.q <= 15;
 }
+bool tc_backward_available() { return true; }
+
+#define SGPX_TC_DISPATCH(FN, ...)                      \
+  switch (instantiated_q(P.q)) {                       \
+    case 1: return FN<1>(__VA_ARGS__);                 \
+    case 2: return FN<2>(__VA_ARGS__);                 \
+    case 3: return FN<3>(__VA_ARGS__);                 \
+    case 4: return FN<4>(__VA_ARGS__);                 \
+    case 5: return FN<5>(__VA_ARGS__);                 \
+    case 6: return FN<6>(__VA_ARGS__);                 \
+    case 8: return FN<8>(__VA_ARGS__);                 \
+    case 10: return FN<10>(__VA_ARGS__);               \
+    case 12: return FN<12>(__VA_ARGS__);               \
+    case 16: return FN<16>(__VA_ARGS__);               \
+    default: return 1;                                 \
+  }
+
+int plan_backward_tc(const PsiConst& P, int num_sms, LaunchGeom* geom) {
+  SGPX_TC_DISPATCH(plan_bwd_tc_q, P, num_sms, geom)
+}
+
+int psi_backward_tc(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
+                    LaunchGeom* geom, void* ev_begin, void* ev_end) {
+  SGPX_TC_DISPATCH(launch_bwd_tc_q, P, B, part, packed, num_sms, static_cast<cudaStream_t>(stream), geom,
+                   cudaEvent_t(ev_begin), cudaEvent_t(ev_end))
+}
+
 
 int plan_forward_tc(const PsiConst& P, int num_sms, LaunchGeom* geom) {
   switch (instantiated_q(P.q)) {

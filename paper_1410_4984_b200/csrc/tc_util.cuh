@@ -33,10 +33,10 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
 }
 
 // tf32 split helpers: hi = round-to-nearest tf32, lo = x - hi (the MMA reads lo's top bits).
+// Round to nearest (ties away) at the tf32 precision with two integer ops (cvt.rna.tf32.f32 is
+// emulated with ~4 instructions on sm_100a); inputs here are finite.
 __device__ __forceinline__ float tf32_hi(float x) {
-  uint32_t u;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
-  return __uint_as_float(u);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 // ---- TMEM ----------------------------------------------------------------------------------
