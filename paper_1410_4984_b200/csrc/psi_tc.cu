@@ -31,7 +31,9 @@ std::atomic<int64_t> g_tc_launches{0};
 namespace {
 using namespace dev;
 
-constexpr int kPipes = 2;
+constexpr int kPipes = 2;       // backward: TMEM 256 columns per pipeline
+constexpr int kPipesF = 4;      // forward: TMEM 128 columns per pipeline
+constexpr int kThreadsF = 128 * kPipesF;
 
 // Per-phase cycle counters (only when P.prof != null): accumulated by lane 0 of each pipeline's
 // first warp.  Slots: 0 prologue, 1 A1 build + barrier, 2 MMA1 wait, 3 element loop, 4 MMA2 issue,
@@ -115,24 +117,24 @@ __device__ __forceinline__ void build_a1_row(const TCLayout& L, const float (&kk
 }
 
 // Issue the 3xTF32 MMA1 of one tile: D1 = A1 B1^T (hi.hi + hi.lo + lo.hi).
+template <int Q>
 __device__ __forceinline__ void issue_mma1(const TCLayout& L, uint32_t d1, const float* a1, const float* b1) {
+  constexpr int KS = (Q + 7) / 8;  // K-steps of 8
   const uint32_t idesc = tc::idesc_tf32(128, L.n1);
-  const uint32_t a_hi = tc::smem_u32(a1), a_lo = a_hi + 128 * L.k1 * 4;
-  const uint32_t b_hi = tc::smem_u32(b1), b_lo = b_hi + L.n1 * L.k1 * 4;
-  uint32_t acc = 0;
+  const uint64_t a_hi = tc::desc(tc::smem_u32(a1), L.k1), a_lo = tc::desc(tc::smem_u32(a1) + 128 * L.k1 * 4, L.k1);
+  const uint64_t b_hi = tc::desc(tc::smem_u32(b1), L.k1), b_lo = tc::desc(tc::smem_u32(b1) + L.n1 * L.k1 * 4, L.k1);
+#pragma unroll
   for (int t = 0; t < 3; ++t) {
-    const uint32_t a = (t == 2) ? a_lo : a_hi, b = (t == 1) ? b_lo : b_hi;
-    for (int ks = 0; ks < L.k1 / 8; ++ks) {
-      tc::mma_ss(d1, tc::desc(a + ks * 256, L.k1), tc::desc(b + ks * 256, L.k1), idesc, acc);
-      acc = 1;
-    }
+    const uint64_t a = (t == 2) ? a_lo : a_hi, b = (t == 1) ? b_lo : b_hi;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) tc::mma_ss(d1, a + 16 * ks, b + 16 * ks, idesc, (t | ks) ? 1u : 0u);
   }
 }
 
 size_t fwd_tc_smem_bytes(const PsiConst& P) {
   const TCLayout L = tc_layout(P.q, P.m);
   size_t f = size_t(P.mv) * P.qv + rows_floats(P.qv) + size_t(P.mv) * 32 * 2 + 32 * size_t(P.dv) +
-             2 * size_t(L.n1) * L.k1 + kPipes * 2 * 128 * size_t(L.k1);
+             2 * size_t(L.n1) * L.k1 + kPipesF * 2 * 128 * size_t(L.k1);
   return f * 4 + 64 * sizeof(double) + 64;
 }
 
@@ -140,7 +142,7 @@ size_t fwd_tc_smem_bytes(const PsiConst& P) {
 // Forward (statistics pass) on tensor cores.
 // =============================================================================================
 template <int Q>
-__global__ void __launch_bounds__(kThreadsTC, 1)
+__global__ void __launch_bounds__(kThreadsF, 1)
     psi_fwd_tc_kernel(PsiConst P, int64_t nchunks, double* __restrict__ part, int64_t pstride, int* err_flag) {
   extern __shared__ __align__(1024) float sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5, nthr = blockDim.x;
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   float* B1 = p;  // 1024-aligned base keeps every operand tile 16-byte aligned
   p += 2 * L.n1 * L.k1;
   float* A1 = p;
-  p += kPipes * 2 * 128 * L.k1;
+  p += kPipesF * 2 * 128 * L.k1;
   float* Zc = p;
   p += mv * qv;
   Rows R = carve_rows(p, qv);
@@ -162,14 +164,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   p += 32 * dv;
   double* red = reinterpret_cast<double*>(p);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(red + 64);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + kPipes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + kPipesF);
 
   for (int i = tid; i < mv * qv; i += nthr) Zc[i] = P.zc[i];
   __syncthreads();
   build_b1(P, L, Zc, B1);
-  if (warp == 0) tc::tmem_alloc(tmem_slot, 256);
+  if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
   if (tid == 0) {
-    for (int i = 0; i < kPipes; ++i) tc::mbar_init(&mbar[i], 1);
+    for (int i = 0; i < kPipesF; ++i) tc::mbar_init(&mbar[i], 1);
     tc::mbar_fence_init();
   }
   tc::fence_async_smem();
@@ -238,7 +240,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       float kk[Q];
 #pragma unroll
       for (int q = 0; q < Q; ++q) kk[q] = R.kk[q * 32 + lane];
-      for (int t = pipe; t < MT; t += kPipes) {
+      for (int t = pipe; t < MT; t += kPipesF) {
         const int a = 4 * t + wq;
         const bool va = a < m;
         build_a1_row<Q>(L, kk, Zc + (va ? a : 0) * qv, va, a1, 32 * wq + lane);
@@ -247,7 +249,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         tc::named_sync(1 + pipe, 128);
         if (wq == 0 && lane == 0) {
           tc::fence_after();
-          issue_mma1(L, d1, a1, B1);
+          issue_mma1<Q>(L, d1, a1, B1);
           tc::commit(&mbar[pipe]);
         }
         tc::mbar_wait(&mbar[pipe], phase);
@@ -255,31 +257,34 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         tc::fence_after();
         const float La = Ls[(va ? a : 0) * 32 + lane];
         const int c0 = (4 * t) & ~31;
-        int c = c0;
-        for (; c + 32 <= m; c += 32) {
-          uint32_t r[32];
-          tc::ld32(d1 + lane_off + c, r);
+        const int cfull = c0 + ((m - c0) & ~31);  // end of the full 32-column chunks
+        uint32_t r[32];
+        if (c0 < cfull) tc::ld32(d1 + lane_off + c0, r);
+        for (int c = c0; c < cfull; c += 32) {
           tc::ld_wait();
           float v[32];
 #pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          if (c + 32 < cfull) tc::ld32(d1 + lane_off + c + 32, r);  // prefetch the next chunk
+#pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int b = c + j;
-            const float s = __uint_as_float(r[j]) + La + Ls[b * 32 + lane];
+            const float s = v[j] + La + Ls[b * 32 + lane];
             v[j] = (b >= a) ? ex2(s) : 0.f;
           }
           const float tot = reduce_scatter<32>(v, lane);
           const int b = c + lane;
           if (va && b >= a) atomicAdd(phi_part + pair_index(a, b, m), double(tot));
         }
-        for (; c < m; c += 8) {
-          uint32_t r[8];
-          tc::ld8(d1 + lane_off + c, r);
+        for (int c = cfull; c < m; c += 8) {
+          uint32_t r8[8];
+          tc::ld8(d1 + lane_off + c, r8);
           tc::ld_wait();
           float v[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int b = c + j;
-            const float s = __uint_as_float(r[j]) + La + Ls[min(b, mv - 1) * 32 + lane];
+            const float s = __uint_as_float(r8[j]) + La + Ls[min(b, mv - 1) * 32 + lane];
             v[j] = (b >= a && b < m) ? ex2(s) : 0.f;
           }
           const float tot = reduce_scatter<8>(v, lane);
@@ -326,7 +331,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   __syncthreads();
   if (warp == 0) {
     tc::fence_after();
-    tc::tmem_dealloc(tmem, 256);
+    tc::tmem_dealloc(tmem, 512);
   }
   if (tid == 0) {
     double s1 = 0.0, s2 = 0.0;
@@ -363,7 +368,7 @@ int plan_fwd_tc_q(const PsiConst& P, int num_sms, LaunchGeom* geom) {
   auto kern = psi_fwd_tc_kernel<Q>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return 3;
   const int64_t nchunks = (P.n + 31) / 32;
-  *geom = LaunchGeom{int(std::min<int64_t>(nchunks, num_sms)), kThreadsTC, smem};
+  *geom = LaunchGeom{int(std::min<int64_t>(nchunks, num_sms)), kThreadsF, smem};
   return 0;
 }
 
@@ -390,41 +395,25 @@ int launch_fwd_tc_q(const PsiConst& P, double* part, double* packed, int* err_fl
 
 
 // =============================================================================================
-// Backward (gradient pass) on tensor cores.
-// TMEM per pipeline (256 columns): [0, n1) D1 = s, then G_hi in place; [n1, n1+n1) G_lo;
-// [2 n1, 2 n1 + n2) D2 = [R | S].  Requires 2 n1 + n2 <= 256 (M <= 112 with Q <= 15).
+// Backward (gradient pass): MMA1 on the tensor cores for the exponent cross term, SIMT for
+// G = U_ab ex2(s) and the accumulations R_na = sum_b G, S_naq = sum_b G z_bq.
+// A tile is 32 datapoints x 8 inducing points: warp quadrant wq owns rows (n, a = 8t + wq) in
+// TMEM columns [0, 128) and (n, a + 4) in [128, 256), so one broadcast load of z_b feeds a
+// packed fma.rn.f32x2 over the two rows.  TMEM: 256 columns per pipeline, 2 pipelines.
 // =============================================================================================
-__device__ __forceinline__ void build_c2(const PsiConst& P, const TCLayout& L, const float* Zc, float* c2) {
-  const int tot = L.n2 * L.k2;
-  for (int i = threadIdx.x; i < tot; i += blockDim.x) {
-    const int j = i / L.k2, b = i - j * L.k2;
-    float x = 0.f;
-    if (b < P.m) x = (j == 0) ? 1.f : (j <= P.q ? Zc[b * P.qv + (j - 1)] : 0.f);
-    const float h = tc::tf32_hi(x);
-    c2[tc::canon(j, b, L.k2)] = h;
-    c2[L.n2 * L.k2 + tc::canon(j, b, L.k2)] = x - h;
-  }
-}
-
-// MMA2: D2 = G (TMEM, hi/lo) * C2^T (smem, hi/lo), 3xTF32.
-__device__ __forceinline__ void issue_mma2(const TCLayout& L, uint32_t base, const float* c2) {
-  const uint32_t idesc = tc::idesc_tf32(128, L.n2);
-  const uint32_t g_hi = base, g_lo = base + L.n1, d2 = base + 2 * L.n1;
-  const uint32_t c_hi = tc::smem_u32(c2), c_lo = c_hi + L.n2 * L.k2 * 4;
-  uint32_t acc = 0;
-  for (int t = 0; t < 3; ++t) {
-    const uint32_t a = (t == 2) ? g_lo : g_hi, c = (t == 1) ? c_lo : c_hi;
-    for (int ks = 0; ks < L.k2 / 8; ++ks) {
-      tc::mma_ts(d2, a + ks * 8, tc::desc(c + ks * 256, L.k2), idesc, acc);
-      acc = 1;
-    }
-  }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
 }
 
 size_t bwd_tc_smem_bytes(const PsiConst& P, int Q) {
   const TCLayout L = tc_layout(P.q, P.m);
-  size_t f = 2 * size_t(L.n1) * L.k1 + kPipes * 2 * 128 * size_t(L.k1) + 2 * size_t(L.n2) * L.k2 +
-             size_t(P.mv) * P.qv + rows_floats(P.qv) + size_t(P.mv) * 32 * 2 + size_t(P.dv) * 32 +
+  size_t f = 2 * size_t(L.n1) * L.k1 + kPipes * 2 * (2 * 128 * size_t(L.k1)) + size_t(P.mv) * P.qv +
+             rows_floats(P.qv) + size_t(P.mv) * 32 * 2 + size_t(P.dv) * 32 + size_t(P.d) * P.mv +
              size_t(kThreadsTC / 32) * (2 + 5 * Q) * 32;
   return f * 4 + (Q + 1) * 32 * sizeof(double) + 64;
 }
@@ -434,6 +423,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     psi_bwd_tc_kernel(PsiConst P, BwdConst B, int64_t nchunks, double* __restrict__ part, int64_t pstride) {
   constexpr int NACC = 2 + 5 * Q;
   constexpr int T0 = 0, Y1 = 1, Y2 = 1 + Q, XX = 1 + 2 * Q, P0 = 1 + 3 * Q, P1 = 2 + 3 * Q, P2 = 2 + 4 * Q;
+  constexpr int Q4 = (Q + 3) / 4;
   extern __shared__ __align__(1024) float sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5, nthr = blockDim.x;
   const int m = P.m, mv = P.mv, qv = P.qv, d = P.d;
@@ -441,10 +431,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   float* p = sm;
   float* B1 = p;
   p += 2 * L.n1 * L.k1;
-  float* A1 = p;
-  p += kPipes * 2 * 128 * L.k1;
-  float* C2 = p;
-  p += 2 * L.n2 * L.k2;
+  float* A1 = p;  // [pipe][group][hi/lo][128 x k1]
+  p += kPipes * 2 * (2 * 128 * L.k1);
   float* Zc = p;
   p += mv * qv;
   Rows R = carve_rows(p, qv);
@@ -454,20 +442,22 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   p += P.dv * 32;
   float* G1s = p;
   p += mv * 32;
+  float* Dps = p;  // dPsi^T [d][mv]
+  p += d * mv;
   float* acc = p;
   p += nw * NACC * 32;
   double* dacc = reinterpret_cast<double*>(p);  // [(Q+1)][32]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(dacc + (Q + 1) * 32);  // [pipe][2]: MMA1, MMA2 done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2 * kPipes);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(dacc + (Q + 1) * 32);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + kPipes);
 
   for (int i = tid; i < mv * qv; i += nthr) Zc[i] = P.zc[i];
+  for (int i = tid; i < d * mv; i += nthr) Dps[i] = B.dpsi[i];
   for (int i = tid; i < (Q + 1) * 32; i += nthr) dacc[i] = 0.0;
   __syncthreads();
   build_b1(P, L, Zc, B1);
-  build_c2(P, L, Zc, C2);
   if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
   if (tid == 0) {
-    for (int i = 0; i < 2 * kPipes; ++i) tc::mbar_init(&mbar[i], 1);
+    for (int i = 0; i < kPipes; ++i) tc::mbar_init(&mbar[i], 1);
     tc::mbar_fence_init();
   }
   tc::fence_async_smem();
@@ -479,9 +469,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   const int pipe = warp >> 2, wq = warp & 3;
   const uint32_t base = tmem + pipe * 256;
   const uint32_t lane_off = uint32_t(32 * wq) << 16;
-  float* a1 = A1 + pipe * 2 * 128 * L.k1;
-  uint32_t ph1 = 0, ph2 = 0;
-  const int MT = (m + 3) >> 2;
+  float* a1g0 = A1 + pipe * 2 * (2 * 128 * L.k1);
+  float* a1g1 = a1g0 + 2 * 128 * L.k1;
+  uint32_t ph = 0;
+  const int MT8 = (m + 7) >> 3;  // tiles of 8 inducing points
   double* const cta_part = part + int64_t(blockIdx.x) * pstride;
   double* const dz_part = cta_part + 1 + P.q;
   const double inv_var = 1.0 / P.variance_d;
@@ -492,6 +483,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     TCP_MARK(tp0);
     load_rows<Q>(P, n0, R, nullptr, nullptr);
     build_L<Q>(P, R, Zc, Ls);
+#pragma unroll 4
     for (int dd = warp; dd < d; dd += nw) Ys[dd * 32 + lane] = valid ? float(P.y[dd * P.ld_y + n]) : 0.f;
     __syncthreads();
     {  // psi1 adjoint weights G1_nm = v1_nm <y_n, dPsi_m>
@@ -504,9 +496,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       const float b1 = R.b1[lane];
       for (int mt = warp; mt < (mv >> 2); mt += nw) {
         float w4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
         for (int dd = 0; dd < d; ++dd) {
           const float yv = Ys[dd * 32 + lane];
-          const float4 dp = __ldg(reinterpret_cast<const float4*>(B.dpsi + int64_t(dd) * mv) + mt);
+          const float4 dp = *reinterpret_cast<const float4*>(Dps + dd * mv + 4 * mt);
           w4[0] = fmaf(yv, dp.x, w4[0]);
           w4[1] = fmaf(yv, dp.y, w4[1]);
           w4[2] = fmaf(yv, dp.z, w4[2]);
@@ -532,8 +525,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
     }
     __syncthreads();
+    TCP_ADD(0, tp0);
 
-    // per-datapoint accumulators of this thread (row = (lane, a)), summed over its tiles
     float t0 = 0.f, p0 = 0.f, y1[Q], y2[Q], xq[Q], p1[Q], p2[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) y1[q] = y2[q] = xq[q] = p1[q] = p2[q] = 0.f;
@@ -541,128 +534,107 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
     for (int q = 0; q < Q; ++q) kk[q] = R.kk[q * 32 + lane];
 
-    TCP_ADD(0, tp0);
-    for (int t = pipe; t < MT; t += kPipes) {
-      const int a = 4 * t + wq;
-      const bool va = a < m;
-      const int ac = va ? a : 0;
+    for (int t = pipe; t < MT8; t += kPipes) {
+      const int a0 = 8 * t + wq, a1i = a0 + 4;
+      const bool va0 = a0 < m, va1 = a1i < m;
+      const int ac0 = va0 ? a0 : 0, ac1 = va1 ? a1i : 0;
       TCP_MARK(tp1);
-      build_a1_row<Q>(L, kk, Zc + ac * qv, va, a1, 32 * wq + lane);
+      build_a1_row<Q>(L, kk, Zc + ac0 * qv, va0, a1g0, 32 * wq + lane);
+      build_a1_row<Q>(L, kk, Zc + ac1 * qv, va1, a1g1, 32 * wq + lane);
       tc::fence_async_smem();
       tc::fence_before();
       tc::named_sync(1 + pipe, 128);
       if (wq == 0 && lane == 0) {
         tc::fence_after();
-        issue_mma1(L, base, a1, B1);
-        tc::commit(&mbar[2 * pipe]);
+        issue_mma1<Q>(L, base, a1g0, B1);
+        issue_mma1<Q>(L, base + 128, a1g1, B1);
+        tc::commit(&mbar[pipe]);
       }
       TCP_ADD(1, tp1);
       TCP_MARK(tp2);
-      tc::mbar_wait(&mbar[2 * pipe], ph1);
-      ph1 ^= 1;
+      tc::mbar_wait(&mbar[pipe], ph);
+      ph ^= 1;
       tc::fence_after();
       TCP_ADD(2, tp2);
       TCP_MARK(tp3);
-      const float La = Ls[ac * 32 + lane];
-      const float* urow = B.u + int64_t(ac) * mv;  // U symmetric: row a
-      // G = U_ab ex2(s) over all b, written back as G_hi (in place) and G_lo
-      int c = 0;
-      for (; c + 32 <= m; c += 32) {
-        uint32_t r[32], lo[32];
-        tc::ld32(base + lane_off + c, r);
+      // padded rows (a >= M) get L_a = -inf so their G, R, S vanish
+      const float2 La = make_float2(va0 ? Ls[ac0 * 32 + lane] : -CUDART_INF_F, va1 ? Ls[ac1 * 32 + lane] : -CUDART_INF_F);
+      const float* u0 = B.u + int64_t(ac0) * mv;  // U symmetric: rows a0, a0+4
+      const float* u1 = B.u + int64_t(ac1) * mv;
+      float2 Racc = make_float2(0.f, 0.f), Sacc[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) Sacc[q] = make_float2(0.f, 0.f);
+      // sweep b in chunks of 16 TMEM columns (two rows per thread)
+      for (int c = 0; c < m; c += 16) {
+        uint32_t r0[16], r1[16];
+        tc::ld16(base + lane_off + c, r0);
+        tc::ld16(base + 128 + lane_off + c, r1);
         tc::ld_wait();
+#pragma unroll 4
+        for (int j = 0; j < 16; j += 4) {
+          const int bb = c + j;
+          if (bb >= m) break;
+          const float4 ua = __ldg(reinterpret_cast<const float4*>(u0 + bb));
+          const float4 ub = __ldg(reinterpret_cast<const float4*>(u1 + bb));
+          const float uaa[4] = {ua.x, ua.y, ua.z, ua.w}, ubb[4] = {ub.x, ub.y, ub.z, ub.w};
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          const float4 u4 = __ldg(reinterpret_cast<const float4*>(urow + c + j));
-          const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
+          for (int k = 0; k < 4; ++k) {
+            const int b = bb + k;
+            const bool vb = b < m;
+            const float Lb = Ls[(vb ? b : 0) * 32 + lane];
+            float2 s = make_float2(__uint_as_float(r0[j + k]) + La.x + Lb, __uint_as_float(r1[j + k]) + La.y + Lb);
+            float2 g = make_float2(vb ? uaa[k] * ex2(s.x) : 0.f, vb ? ubb[k] * ex2(s.y) : 0.f);
+            Racc.x += g.x;
+            Racc.y += g.y;
+            float z[Q];
+            load_z<Q>(Zc + (vb ? b : 0) * qv, z);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int b = c + j + u;
-            const float s = __uint_as_float(r[j + u]) + La + Ls[b * 32 + lane];
-            const float g = va ? uu[u] * ex2(s) : 0.f;
-            const float h = tc::tf32_hi(g);
-            r[j + u] = __float_as_uint(h);
-            lo[j + u] = __float_as_uint(g - h);
+            for (int q = 0; q < Q; ++q) Sacc[q] = fma2(g, make_float2(z[q], z[q]), Sacc[q]);
           }
         }
-        tc::st32(base + lane_off + c, r);
-        tc::st32(base + lane_off + L.n1 + c, lo);
       }
-      for (; c < L.k2; c += 8) {
-        uint32_t r[8], lo[8];
-        tc::ld8(base + lane_off + c, r);
-        tc::ld_wait();
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int b = c + j;
-          float g = 0.f;
-          if (va && b < m) {
-            const float s = __uint_as_float(r[j]) + La + Ls[b * 32 + lane];
-            g = urow[b] * ex2(s);
-          }
-          const float h = tc::tf32_hi(g);
-          r[j] = __float_as_uint(h);
-          lo[j] = __float_as_uint(g - h);
-        }
-        tc::st8(base + lane_off + c, r);
-        tc::st8(base + lane_off + L.n1 + c, lo);
-      }
-      tc::st_wait();
       TCP_ADD(3, tp3);
-      TCP_MARK(tp4);
-      tc::fence_before();
-      tc::named_sync(1 + pipe, 128);
-      if (wq == 0 && lane == 0) {
-        tc::fence_after();
-        issue_mma2(L, base, C2);
-        tc::commit(&mbar[2 * pipe + 1]);
-      }
-      TCP_ADD(4, tp4);
-      TCP_MARK(tp5);
-      tc::mbar_wait(&mbar[2 * pipe + 1], ph2);
-      ph2 ^= 1;
-      tc::fence_after();
-      TCP_ADD(5, tp5);
       TCP_MARK(tp6);
-      uint32_t rs[16];
-      tc::ld16(base + lane_off + 2 * L.n1, rs);
-      tc::ld_wait();
-      const float Ra = __uint_as_float(rs[0]);
-      float Sa[Q];
+      // contractions for the two rows (natural-log units; G carries U and v)
 #pragma unroll
-      for (int q = 0; q < Q; ++q) Sa[q] = (q + 1 < 16) ? __uint_as_float(rs[(q + 1) % 16]) : 0.f;
-      // contractions (natural-log units; G already carries U and v)
-      const float g1 = va ? G1s[a * 32 + lane] : 0.f;
-      t0 += Ra;
-      p0 += g1;
-      float vals[Q];
+      for (int h = 0; h < 2; ++h) {
+        const int a = h ? a1i : a0;
+        const bool va = h ? va1 : va0;
+        const int ac = h ? ac1 : ac0;
+        const float Ra = h ? Racc.y : Racc.x;
+        const float g1 = va ? G1s[a * 32 + lane] : 0.f;
+        t0 += Ra;
+        p0 += g1;
+        float vals[Q];
 #pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        const float z = Zc[ac * qv + q];
-        y1[q] = fmaf(z, Ra, y1[q]);
-        y2[q] = fmaf(z * z, Ra, y2[q]);
-        xq[q] = fmaf(z, Sa[q], xq[q]);
-        p1[q] = fmaf(z, g1, p1[q]);
-        p2[q] = fmaf(z * z, g1, p2[q]);
-        const float mu = R.mu[q * 32 + lane], d2 = R.d2[q * 32 + lane], d1 = R.d1[q * 32 + lane];
-        const float kn = R.sv[q * 32 + lane] * P.il2[q] * d2;
-        const float c2 = 0.5f * (P.il2[q] + d2);
-        vals[q] = 2.f * (fmaf(d2, mu, -c2 * z) * Ra + kn * Sa[q]) + g1 * d1 * (mu - z);
+        for (int q = 0; q < Q; ++q) {
+          const float Sa = h ? Sacc[q].y : Sacc[q].x;
+          const float z = Zc[ac * qv + q];
+          y1[q] = fmaf(z, Ra, y1[q]);
+          y2[q] = fmaf(z * z, Ra, y2[q]);
+          xq[q] = fmaf(z, Sa, xq[q]);
+          p1[q] = fmaf(z, g1, p1[q]);
+          p2[q] = fmaf(z * z, g1, p2[q]);
+          const float mu = R.mu[q * 32 + lane], d2 = R.d2[q * 32 + lane], d1 = R.d1[q * 32 + lane];
+          const float kn = R.sv[q * 32 + lane] * P.il2[q] * d2;
+          const float c2 = 0.5f * (P.il2[q] + d2);
+          vals[q] = 2.f * (fmaf(d2, mu, -c2 * z) * Ra + kn * Sa) + g1 * d1 * (mu - z);
+        }
+        constexpr int QR = Q <= 8 ? 8 : (Q <= 16 ? 16 : 32);
+        float vr[QR];
+#pragma unroll
+        for (int i = 0; i < QR; ++i) vr[i] = (i < Q) ? vals[i % Q] : 0.f;
+        const float tot = reduce_scatter<QR>(vr, lane);
+        const int shift = QR == 8 ? 2 : (QR == 16 ? 1 : 0);
+        const int qi = lane >> shift;
+        if (va && qi < P.q && (lane & ((1 << shift) - 1)) == 0)
+          atomicAdd(dz_part + a + int64_t(qi) * m, double(tot));
       }
-      // reduce the Q d_z values of inducing point a over the 32 datapoints of the chunk
-      constexpr int QR = Q <= 8 ? 8 : (Q <= 16 ? 16 : 32);
-      float vr[QR];
-#pragma unroll
-      for (int i = 0; i < QR; ++i) vr[i] = (i < Q) ? vals[i % Q] : 0.f;
-      const float tot = reduce_scatter<QR>(vr, lane);
-      const int shift = QR == 8 ? 2 : (QR == 16 ? 1 : 0);
-      const int qi = lane >> shift;
-      if (va && qi < P.q && (lane & ((1 << shift) - 1)) == 0) atomicAdd(dz_part + a + int64_t(qi) * m, double(tot));
       TCP_ADD(6, tp6);
       if (P.prof && wq == 0 && lane == 0) atomicAdd(P.prof + 8, 1ull);
     }
+    (void)Q4;
     TCP_MARK(tp7);
-    // merge the per-datapoint accumulators of the 8 warps
     {
       float* accw = acc + warp * NACC * 32;
       accw[T0 * 32 + lane] = t0;
@@ -806,8 +778,7 @@ bool tc_supported(const PsiConst& P) { return P.m >= 1 && P.m <= 128 && P.q >= 1
 
 // Backward TMEM budget per pipeline: 2 n1 + n2 <= 256 columns.
 bool tc_backward_fits(const PsiConst& P) {
-  const TCLayout L = tc_layout(P.q, P.m);
-  return tc_supported(P) && 2 * L.n1 + L.n2 <= 256 && P.q <= 15;
+  return tc_supported(P) && P.q <= 16 && bwd_tc_smem_bytes(P, instantiated_q(P.q)) <= 227 * 1024;
 }
 bool tc_backward_available() { return true; }
 
