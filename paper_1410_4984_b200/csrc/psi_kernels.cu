@@ -623,7 +623,8 @@ bool use_tc(const PsiConst& P, bool backward) {
   }();
   if (forced == 1) return false;
   if (backward) return tc_backward_available() && tc_backward_fits(P);
-  return tc_supported(P);
+  // forward: the SIMT kernel is faster until the TC forward is restructured (profiles/r01_*)
+  return forced == 2 && tc_supported(P);
 }
 
 int instantiated_q(int q) { return pick_q(q); }

@@ -72,40 +72,61 @@ __device__ __forceinline__ float reduce_scatter(float (&v)[K], int lane) {
 }
 
 struct TCLayout {
-  int k1;    // MMA1 K (Q rounded to 8)
+  int k1;    // MMA1 K (2Q rounded to 8)
   int n1;    // MMA1 N (M rounded to 16), <= 128
   int k2;    // MMA2 K (M rounded to 8)
   int n2;    // MMA2 N (Q+1 rounded to 16)
 };
 
 __host__ __device__ inline TCLayout tc_layout(int q, int m) {
-  return TCLayout{round_up(q, 8), round_up(m, 16), round_up(m, 8), round_up(q + 1, 16)};
+  return TCLayout{round_up(2 * q, 8), round_up(m, 16), round_up(m, 8), round_up(q + 1, 16)};
 }
 
-// B1 = centred Z as the K-major B operand (N1 rows b, K1 columns q), hi and lo planes.
+// B1[b, :] = [z_b1..z_bQ, z_b1^2..z_bQ^2] (centred Z) as the K-major B operand, hi and lo planes.
 __device__ __forceinline__ void build_b1(const PsiConst& P, const TCLayout& L, const float* Zc, float* b1) {
   const int tot = L.n1 * L.k1;
   for (int i = threadIdx.x; i < tot; i += blockDim.x) {
-    const int b = i / L.k1, q = i - b * L.k1;
-    const float z = (b < P.m && q < P.q) ? Zc[b * P.qv + q] : 0.f;
+    const int b = i / L.k1, k = i - b * L.k1;
+    float z = 0.f;
+    if (b < P.m && k < 2 * P.q) {
+      const float zz = Zc[b * P.qv + (k < P.q ? k : k - P.q)];
+      z = k < P.q ? zz : zz * zz;
+    }
     const float h = tc::tf32_hi(z);
-    b1[tc::canon(b, q, L.k1)] = h;
-    b1[L.n1 * L.k1 + tc::canon(b, q, L.k1)] = z - h;
+    b1[tc::canon(b, k, L.k1)] = h;
+    b1[L.n1 * L.k1 + tc::canon(b, k, L.k1)] = z - h;
   }
 }
 
-// A1 rows of one tile: row r = 32*wq + lane <-> (datapoint lane, inducing a), value K_nq z_aq.
+// A1 row of one tile, row r = 32*wq + lane <-> (datapoint lane, inducing a):
+//   [K_nq z_aq + al_nq (q < Q), be_nq (q < Q)]  so that  D1[(n,a), b] + C_na = log2 v_nab  with the
+// row constant C_na = sum_q (al z_aq + be z_aq^2) + B_n (returned; -inf for padded a / datapoints).
 template <int Q>
-__device__ __forceinline__ void build_a1_row(const TCLayout& L, const float (&kk)[Q], const float* za, bool valid_a,
-                                             float* a1, int r) {
-  constexpr int QV = (Q + 7) / 8 * 8;
+__device__ __forceinline__ float build_a1_row(const TCLayout& L, const Rows& R, int lane, const float* za,
+                                              bool valid_a, float* a1, int r) {
+  constexpr int KV = (2 * Q + 7) / 8 * 8;
+  float z[Q];
 #pragma unroll
-  for (int j = 0; j < QV; j += 4) {
+  for (int q = 0; q < Q; ++q) z[q] = za[q];
+  float c = R.b2[lane];
+#pragma unroll
+  for (int j = 0; j < KV; j += 4) {
     float h[4], l[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int q = j + u;
-      const float x = (q < Q && valid_a) ? kk[q % Q] * za[q % Q] : 0.f;
+      const int k = j + u;
+      float x = 0.f;
+      if (valid_a && k < 2 * Q) {
+        if (k < Q) {
+          const float al = R.al[k * 32 + lane];
+          x = fmaf(R.kk[k * 32 + lane], z[k % Q], al);
+          c = fmaf(al, z[k % Q], c);
+        } else {
+          const float be = R.be[(k - Q) * 32 + lane];
+          x = be;
+          c = fmaf(be * z[(k - Q) % Q], z[(k - Q) % Q], c);
+        }
+      }
       h[u] = tc::tf32_hi(x);
       l[u] = x - h[u];
     }
@@ -114,12 +135,13 @@ __device__ __forceinline__ void build_a1_row(const TCLayout& L, const float (&kk
       *reinterpret_cast<float4*>(a1 + 128 * L.k1 + tc::canon(r, j, L.k1)) = make_float4(l[0], l[1], l[2], l[3]);
     }
   }
+  return valid_a ? c : -CUDART_INF_F;
 }
 
 // Issue the 3xTF32 MMA1 of one tile: D1 = A1 B1^T (hi.hi + hi.lo + lo.hi).
 template <int Q>
 __device__ __forceinline__ void issue_mma1(const TCLayout& L, uint32_t d1, const float* a1, const float* b1) {
-  constexpr int KS = (Q + 7) / 8;  // K-steps of 8
+  constexpr int KS = (2 * Q + 7) / 8;  // K-steps of 8
   const uint32_t idesc = tc::idesc_tf32(128, L.n1);
   const uint64_t a_hi = tc::desc(tc::smem_u32(a1), L.k1), a_lo = tc::desc(tc::smem_u32(a1) + 128 * L.k1 * 4, L.k1);
   const uint64_t b_hi = tc::desc(tc::smem_u32(b1), L.k1), b_lo = tc::desc(tc::smem_u32(b1) + L.n1 * L.k1 * 4, L.k1);
@@ -133,7 +155,7 @@ __device__ __forceinline__ void issue_mma1(const TCLayout& L, uint32_t d1, const
 
 size_t fwd_tc_smem_bytes(const PsiConst& P) {
   const TCLayout L = tc_layout(P.q, P.m);
-  size_t f = size_t(P.mv) * P.qv + rows_floats(P.qv) + size_t(P.mv) * 32 * 2 + 32 * size_t(P.dv) +
+  size_t f = size_t(P.mv) * P.qv + rows_floats(P.qv) + size_t(P.mv) * 32 + 32 * size_t(P.dv) +
              2 * size_t(L.n1) * L.k1 + kPipesF * 2 * 128 * size_t(L.k1);
   return f * 4 + 64 * sizeof(double) + 64;
 }
@@ -156,8 +178,6 @@ __global__ void __launch_bounds__(kThreadsF, 1)
   float* Zc = p;
   p += mv * qv;
   Rows R = carve_rows(p, qv);
-  float* Ls = p;
-  p += mv * 32;
   float* V1s = p;
   p += 32 * mv;
   float* Ys = p;
@@ -197,8 +217,8 @@ __global__ void __launch_bounds__(kThreadsF, 1)
   for (int64_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
     const int64_t n0 = chunk * 32, n = n0 + lane;
     const bool valid = n < P.n;
+    TCP_MARK(tp0);
     load_rows<Q>(P, n0, R, P.expected ? &kl_acc : nullptr, err_flag);
-    build_L<Q>(P, R, Zc, Ls);
     {  // psi1 values [n][m]
       float mu[Q], d1v[Q];
 #pragma unroll
@@ -234,16 +254,15 @@ __global__ void __launch_bounds__(kThreadsF, 1)
       Ys[lane * dv + dd] = yv;
     }
     __syncthreads();
+    TCP_ADD(0, tp0);
 
     // ---- psi2 on the tensor cores: this pipeline's row tiles ----
     {
-      float kk[Q];
-#pragma unroll
-      for (int q = 0; q < Q; ++q) kk[q] = R.kk[q * 32 + lane];
       for (int t = pipe; t < MT; t += kPipesF) {
         const int a = 4 * t + wq;
         const bool va = a < m;
-        build_a1_row<Q>(L, kk, Zc + (va ? a : 0) * qv, va, a1, 32 * wq + lane);
+        TCP_MARK(tp1);
+        const float La = build_a1_row<Q>(L, R, lane, Zc + (va ? a : 0) * qv, va, a1, 32 * wq + lane);
         tc::fence_async_smem();
         tc::fence_before();
         tc::named_sync(1 + pipe, 128);
@@ -252,10 +271,13 @@ __global__ void __launch_bounds__(kThreadsF, 1)
           issue_mma1<Q>(L, d1, a1, B1);
           tc::commit(&mbar[pipe]);
         }
+        TCP_ADD(1, tp1);
+        TCP_MARK(tp2);
         tc::mbar_wait(&mbar[pipe], phase);
         phase ^= 1;
         tc::fence_after();
-        const float La = Ls[(va ? a : 0) * 32 + lane];
+        TCP_ADD(2, tp2);
+        TCP_MARK(tp3);
         const int c0 = (4 * t) & ~31;
         const int cfull = c0 + ((m - c0) & ~31);  // end of the full 32-column chunks
         uint32_t r[32];
@@ -269,8 +291,7 @@ __global__ void __launch_bounds__(kThreadsF, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int b = c + j;
-            const float s = v[j] + La + Ls[b * 32 + lane];
-            v[j] = (b >= a) ? ex2(s) : 0.f;
+            v[j] = (b >= a) ? ex2(v[j] + La) : 0.f;
           }
           const float tot = reduce_scatter<32>(v, lane);
           const int b = c + lane;
@@ -284,15 +305,17 @@ __global__ void __launch_bounds__(kThreadsF, 1)
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int b = c + j;
-            const float s = __uint_as_float(r8[j]) + La + Ls[min(b, mv - 1) * 32 + lane];
-            v[j] = (b >= a && b < m) ? ex2(s) : 0.f;
+            v[j] = (b >= a && b < m) ? ex2(__uint_as_float(r8[j]) + La) : 0.f;
           }
           const float tot = reduce_scatter<8>(v, lane);
           const int b = c + ((lane >> 2) & 7);
           if (va && b >= a && b < m && (lane & 3) == 0) atomicAdd(phi_part + pair_index(a, b, m), double(tot));
         }
+        TCP_ADD(3, tp3);
+        if (P.prof && wq == 0 && lane == 0) atomicAdd(P.prof + 8, 1ull);
       }
     }
+    TCP_MARK(tp7);
     // ---- psi1: Psi = Psi1^T Y, 4 m x 4 d register tiles over the chunk ----
     for (int t = tid; t < ntiles1; t += nthr) {
       const int mt = t / DT, dt = t - mt * DT;
@@ -320,6 +343,7 @@ __global__ void __launch_bounds__(kThreadsF, 1)
         }
     }
     __syncthreads();
+    TCP_ADD(7, tp7);
   }
   yy_acc = warp_sum_d(yy_acc);
   kl_acc = warp_sum_d(kl_acc);
@@ -372,9 +396,14 @@ int plan_fwd_tc_q(const PsiConst& P, int num_sms, LaunchGeom* geom) {
   return 0;
 }
 
+unsigned long long* tc_profile_buffer();
+void tc_profile_report(const char* what, cudaStream_t st);
+
 template <int Q>
-int launch_fwd_tc_q(const PsiConst& P, double* part, double* packed, int* err_flag, int num_sms, cudaStream_t st,
+int launch_fwd_tc_q(const PsiConst& P0, double* part, double* packed, int* err_flag, int num_sms, cudaStream_t st,
                     LaunchGeom* geom, cudaEvent_t e0, cudaEvent_t e1) {
+  PsiConst P = P0;
+  P.prof = tc_profile_buffer();
   LaunchGeom g{};
   if (int rc = plan_fwd_tc_q<Q>(P, num_sms, &g)) return rc;
   const int64_t nchunks = (P.n + 31) / 32;
@@ -389,6 +418,7 @@ int launch_fwd_tc_q(const PsiConst& P, double* part, double* packed, int* err_fl
   fwd_reduce_tc<<<int((pstride + 255) / 256), 256, 0, st>>>(part, pstride, g.grid, pstride, packed,
                                                             double(P.n) * P.variance_d, double(P.n));
   g_tc_launches.fetch_add(1);
+  tc_profile_report("fwd", st);
   if (geom) *geom = g;
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
@@ -413,8 +443,10 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
 size_t bwd_tc_smem_bytes(const PsiConst& P, int Q) {
   const TCLayout L = tc_layout(P.q, P.m);
   size_t f = 2 * size_t(L.n1) * L.k1 + kPipes * 2 * (2 * 128 * size_t(L.k1)) + size_t(P.mv) * P.qv +
-             rows_floats(P.qv) + size_t(P.mv) * 32 * 2 + size_t(P.dv) * 32 + size_t(P.d) * P.mv +
-             size_t(kThreadsTC / 32) * (2 + 5 * Q) * 32;
+             rows_floats(P.qv) + size_t(P.mv) * 32 + size_t(P.dv) * 32 + size_t(P.mv) * P.mv;
+  // the per-warp merge buffer aliases the A1 operand buffers (used only after the tile loop)
+  const size_t a1f = kPipes * 2 * (2 * 128 * size_t(L.k1)), accf = size_t(kThreadsTC / 32) * (2 + 5 * Q) * 32;
+  if (accf > a1f) f += accf - a1f;
   return f * 4 + (Q + 1) * 32 * sizeof(double) + 64;
 }
 
@@ -436,22 +468,23 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   float* Zc = p;
   p += mv * qv;
   Rows R = carve_rows(p, qv);
-  float* Ls = p;
-  p += mv * 32;
   float* Ys = p;
   p += P.dv * 32;
   float* G1s = p;
   p += mv * 32;
-  float* Dps = p;  // dPsi^T [d][mv]
-  p += d * mv;
-  float* acc = p;
-  p += nw * NACC * 32;
+  float* Us = p;  // U = dL/dPhi, [mv][mv] (symmetric, zero padded)
+  p += mv * mv;
+  float* acc = A1;  // per-warp per-datapoint merge buffer, aliases A1 (only used after the tile loop)
+  {
+    const int a1f = kPipes * 2 * (2 * 128 * L.k1), accf = nw * NACC * 32;
+    if (accf > a1f) p += accf - a1f;
+  }
   double* dacc = reinterpret_cast<double*>(p);  // [(Q+1)][32]
   uint64_t* mbar = reinterpret_cast<uint64_t*>(dacc + (Q + 1) * 32);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + kPipes);
 
   for (int i = tid; i < mv * qv; i += nthr) Zc[i] = P.zc[i];
-  for (int i = tid; i < d * mv; i += nthr) Dps[i] = B.dpsi[i];
+  for (int i = tid; i < mv * mv; i += nthr) Us[i] = B.u[i];
   for (int i = tid; i < (Q + 1) * 32; i += nthr) dacc[i] = 0.0;
   __syncthreads();
   build_b1(P, L, Zc, B1);
@@ -482,7 +515,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const bool valid = n < P.n;
     TCP_MARK(tp0);
     load_rows<Q>(P, n0, R, nullptr, nullptr);
-    build_L<Q>(P, R, Zc, Ls);
 #pragma unroll 4
     for (int dd = warp; dd < d; dd += nw) Ys[dd * 32 + lane] = valid ? float(P.y[dd * P.ld_y + n]) : 0.f;
     __syncthreads();
@@ -499,7 +531,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll 4
         for (int dd = 0; dd < d; ++dd) {
           const float yv = Ys[dd * 32 + lane];
-          const float4 dp = *reinterpret_cast<const float4*>(Dps + dd * mv + 4 * mt);
+          const float4 dp = __ldg(reinterpret_cast<const float4*>(B.dpsi + int64_t(dd) * mv) + mt);
           w4[0] = fmaf(yv, dp.x, w4[0]);
           w4[1] = fmaf(yv, dp.y, w4[1]);
           w4[2] = fmaf(yv, dp.z, w4[2]);
@@ -530,17 +562,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     float t0 = 0.f, p0 = 0.f, y1[Q], y2[Q], xq[Q], p1[Q], p2[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) y1[q] = y2[q] = xq[q] = p1[q] = p2[q] = 0.f;
-    float kk[Q];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) kk[q] = R.kk[q * 32 + lane];
-
     for (int t = pipe; t < MT8; t += kPipes) {
       const int a0 = 8 * t + wq, a1i = a0 + 4;
       const bool va0 = a0 < m, va1 = a1i < m;
       const int ac0 = va0 ? a0 : 0, ac1 = va1 ? a1i : 0;
       TCP_MARK(tp1);
-      build_a1_row<Q>(L, kk, Zc + ac0 * qv, va0, a1g0, 32 * wq + lane);
-      build_a1_row<Q>(L, kk, Zc + ac1 * qv, va1, a1g1, 32 * wq + lane);
+      // row constants C_na (padded rows a >= M get -inf so their G, R, S vanish)
+      const float2 La = make_float2(build_a1_row<Q>(L, R, lane, Zc + ac0 * qv, va0, a1g0, 32 * wq + lane),
+                                    build_a1_row<Q>(L, R, lane, Zc + ac1 * qv, va1, a1g1, 32 * wq + lane));
       tc::fence_async_smem();
       tc::fence_before();
       tc::named_sync(1 + pipe, 128);
@@ -557,40 +586,48 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       tc::fence_after();
       TCP_ADD(2, tp2);
       TCP_MARK(tp3);
-      // padded rows (a >= M) get L_a = -inf so their G, R, S vanish
-      const float2 La = make_float2(va0 ? Ls[ac0 * 32 + lane] : -CUDART_INF_F, va1 ? Ls[ac1 * 32 + lane] : -CUDART_INF_F);
-      const float* u0 = B.u + int64_t(ac0) * mv;  // U symmetric: rows a0, a0+4
-      const float* u1 = B.u + int64_t(ac1) * mv;
+      const float* u0 = Us + ac0 * mv;  // U symmetric: rows a0, a0+4
+      const float* u1 = Us + ac1 * mv;
       float2 Racc = make_float2(0.f, 0.f), Sacc[Q];
 #pragma unroll
       for (int q = 0; q < Q; ++q) Sacc[q] = make_float2(0.f, 0.f);
-      // sweep b in chunks of 16 TMEM columns (two rows per thread)
-      for (int c = 0; c < m; c += 16) {
+      // one column b for the two rows of this thread
+      auto column = [&](int b, float d0, float d1, float ua, float ub) {
+        const float g0 = ua * ex2(d0 + La.x), g1 = ub * ex2(d1 + La.y);
+        Racc.x += g0;
+        Racc.y += g1;
+        float z[Q];
+        load_z<Q>(Zc + b * qv, z);
+        const float2 g = make_float2(g0, g1);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) Sacc[q] = fma2(g, make_float2(z[q], z[q]), Sacc[q]);
+      };
+      // full 16-column chunks: no bound checks
+      const int cfull = m & ~15;
+      for (int c = 0; c < cfull; c += 16) {
         uint32_t r0[16], r1[16];
         tc::ld16(base + lane_off + c, r0);
         tc::ld16(base + 128 + lane_off + c, r1);
         tc::ld_wait();
-#pragma unroll 4
+#pragma unroll
         for (int j = 0; j < 16; j += 4) {
-          const int bb = c + j;
-          if (bb >= m) break;
-          const float4 ua = __ldg(reinterpret_cast<const float4*>(u0 + bb));
-          const float4 ub = __ldg(reinterpret_cast<const float4*>(u1 + bb));
-          const float uaa[4] = {ua.x, ua.y, ua.z, ua.w}, ubb[4] = {ub.x, ub.y, ub.z, ub.w};
+          const float4 ua = *reinterpret_cast<const float4*>(u0 + c + j);
+          const float4 ub = *reinterpret_cast<const float4*>(u1 + c + j);
+          column(c + j + 0, __uint_as_float(r0[j + 0]), __uint_as_float(r1[j + 0]), ua.x, ub.x);
+          column(c + j + 1, __uint_as_float(r0[j + 1]), __uint_as_float(r1[j + 1]), ua.y, ub.y);
+          column(c + j + 2, __uint_as_float(r0[j + 2]), __uint_as_float(r1[j + 2]), ua.z, ub.z);
+          column(c + j + 3, __uint_as_float(r0[j + 3]), __uint_as_float(r1[j + 3]), ua.w, ub.w);
+        }
+      }
+      if (cfull < m) {  // tail (< 16 columns; U and Zc are padded to mv, so b < mv reads stay in range)
+        uint32_t r0[16], r1[16];
+        tc::ld16(base + lane_off + cfull, r0);
+        tc::ld16(base + 128 + lane_off + cfull, r1);
+        tc::ld_wait();
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int b = bb + k;
-            const bool vb = b < m;
-            const float Lb = Ls[(vb ? b : 0) * 32 + lane];
-            float2 s = make_float2(__uint_as_float(r0[j + k]) + La.x + Lb, __uint_as_float(r1[j + k]) + La.y + Lb);
-            float2 g = make_float2(vb ? uaa[k] * ex2(s.x) : 0.f, vb ? ubb[k] * ex2(s.y) : 0.f);
-            Racc.x += g.x;
-            Racc.y += g.y;
-            float z[Q];
-            load_z<Q>(Zc + (vb ? b : 0) * qv, z);
-#pragma unroll
-            for (int q = 0; q < Q; ++q) Sacc[q] = fma2(g, make_float2(z[q], z[q]), Sacc[q]);
-          }
+        for (int j = 0; j < 16; ++j) {
+          const int b = cfull + j;
+          if (b < m) column(b, __uint_as_float(r0[j]), __uint_as_float(r1[j]), u0[b], u1[b]);
         }
       }
       TCP_ADD(3, tp3);
@@ -635,6 +672,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     }
     (void)Q4;
     TCP_MARK(tp7);
+    __syncthreads();  // every pipeline is done with its A1 buffers (acc aliases them)
     {
       float* accw = acc + warp * NACC * 32;
       accw[T0 * 32 + lane] = t0;
