@@ -185,6 +185,32 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
   return v[0];
 }
 
+// Sum of v[i] over the warp for K values per lane (K in {8, 16, 32}): lane ends up holding
+// the total of index lane >> (5 - log2 K).
+template <int K>
+__device__ __forceinline__ float reduce_scatter(float (&v)[K], int lane) {
+  int n = K;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    if (n > 1) {
+      const int h = n >> 1;
+      const bool hi = lane & off;
+#pragma unroll
+      for (int i = 0; i < K / 2; ++i) {
+        if (i < h) {
+          const float send = hi ? v[i] : v[i + h];
+          const float keep = hi ? v[i + h] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      n = h;
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+    }
+  }
+  return v[0];
+}
+
 __device__ __forceinline__ double warp_sum_d(double x) {
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);

@@ -91,6 +91,12 @@ int plan_backward_tc(const PsiConst& P, int num_sms, LaunchGeom* geom);
 int psi_backward_tc(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
                     LaunchGeom* geom, void* ev_begin, void* ev_end);
 
+// Standalone psi1 passes (psi1_kernels.cu), paired with the TC psi2 kernels.
+int psi1_fwd_rows(const PsiConst& P, int num_sms);
+int psi1_bwd_ctas(const PsiConst& P, int num_sms);  // each CTA writes 8 per-warp partial rows
+int psi1_forward(const PsiConst& P, double* part_rows, int64_t pstride, int rows, int* err_flag, void* stream);
+int psi1_backward(const PsiConst& P, const BwdConst& B, double* part_rows, int64_t pstride, int ctas, void* stream);
+
 // psi1_expected: out n x m col-major fp64 (ld_out).
 int psi1_matrix(const PsiConst& P, double* out, int64_t ld_out, void* stream);
 // Number of __global__ launches issued so far by this process (evidence counter).

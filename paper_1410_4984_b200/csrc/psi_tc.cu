@@ -45,32 +45,6 @@ constexpr int kThreadsTC = 128 * kPipes;
 
 __host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
-// Sum of v[i] over the warp for K values per lane (K in {8, 16, 32}): lane ends up holding
-// the total of index lane >> (5 - log2 K).
-template <int K>
-__device__ __forceinline__ float reduce_scatter(float (&v)[K], int lane) {
-  int n = K;
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-    if (n > 1) {
-      const int h = n >> 1;
-      const bool hi = lane & off;
-#pragma unroll
-      for (int i = 0; i < K / 2; ++i) {
-        if (i < h) {
-          const float send = hi ? v[i] : v[i + h];
-          const float keep = hi ? v[i + h] : v[i];
-          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-        }
-      }
-      n = h;
-    } else {
-      v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
-    }
-  }
-  return v[0];
-}
-
 struct TCLayout {
   int k1;    // MMA1 K (2Q rounded to 8)
   int n1;    // MMA1 N (M rounded to 16), <= 128
@@ -155,8 +129,7 @@ __device__ __forceinline__ void issue_mma1(const TCLayout& L, uint32_t d1, const
 
 size_t fwd_tc_smem_bytes(const PsiConst& P) {
   const TCLayout L = tc_layout(P.q, P.m);
-  size_t f = size_t(P.mv) * P.qv + rows_floats(P.qv) + size_t(P.mv) * 32 + 32 * size_t(P.dv) +
-             2 * size_t(L.n1) * L.k1 + kPipesF * 2 * 128 * size_t(L.k1);
+  size_t f = size_t(P.mv) * P.qv + rows_floats(P.qv) + 2 * size_t(L.n1) * L.k1 + kPipesF * 2 * 128 * size_t(L.k1);
   return f * 4 + 64 * sizeof(double) + 64;
 }
 
@@ -178,10 +151,6 @@ __global__ void __launch_bounds__(kThreadsF, 1)
   float* Zc = p;
   p += mv * qv;
   Rows R = carve_rows(p, qv);
-  float* V1s = p;
-  p += 32 * mv;
-  float* Ys = p;
-  p += 32 * dv;
   double* red = reinterpret_cast<double*>(p);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(red + 64);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + kPipesF);
@@ -209,50 +178,15 @@ __global__ void __launch_bounds__(kThreadsF, 1)
   const int64_t npairs = int64_t(m) * (m + 1) / 2;
   double* const cta_part = part + int64_t(blockIdx.x) * pstride;
   double* const phi_part = cta_part + 2;
-  double* const psi_part = phi_part + npairs;
-  const int DT = dv >> 2;
-  const int ntiles1 = (mv >> 2) * DT;
+  (void)npairs;
+  (void)d;
+  (void)dv;
 
-  double yy_acc = 0.0, kl_acc = 0.0;
+  double kl_acc = 0.0;
   for (int64_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
-    const int64_t n0 = chunk * 32, n = n0 + lane;
-    const bool valid = n < P.n;
+    const int64_t n0 = chunk * 32;
     TCP_MARK(tp0);
     load_rows<Q>(P, n0, R, P.expected ? &kl_acc : nullptr, err_flag);
-    {  // psi1 values [n][m]
-      float mu[Q], d1v[Q];
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        mu[q] = R.mu[q * 32 + lane];
-        d1v[q] = R.d1[q * 32 + lane];
-      }
-      const float b1 = R.b1[lane];
-      for (int mm = warp; mm < mv; mm += nw) {
-        float v = 0.f;
-        if (mm < m) {
-          float z[Q];
-          load_z<Q>(Zc + mm * qv, z);
-          float e = 0.f;
-#pragma unroll
-          for (int q = 0; q < Q; ++q) {
-            const float df = mu[q] - z[q];
-            e = fmaf(df * df, d1v[q], e);
-          }
-          v = ex2(fmaf(-0.5f * kLog2e, e, b1));
-        }
-        V1s[lane * mv + mm] = v;
-      }
-    }
-    for (int dd = warp; dd < dv; dd += nw) {
-      float yv = 0.f;
-      if (dd < d && valid) {
-        const double yd = P.y[dd * P.ld_y + n];
-        if (!isfinite(yd)) atomicOr(err_flag, 1);
-        yy_acc += yd * yd;
-        yv = float(yd);
-      }
-      Ys[lane * dv + dd] = yv;
-    }
     __syncthreads();
     TCP_ADD(0, tp0);
 
@@ -316,41 +250,11 @@ __global__ void __launch_bounds__(kThreadsF, 1)
       }
     }
     TCP_MARK(tp7);
-    // ---- psi1: Psi = Psi1^T Y, 4 m x 4 d register tiles over the chunk ----
-    for (int t = tid; t < ntiles1; t += nthr) {
-      const int mt = t / DT, dt = t - mt * DT;
-      float acc[4][4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-#pragma unroll 8
-      for (int k = 0; k < 32; ++k) {
-        const float4 vv = *reinterpret_cast<const float4*>(V1s + k * mv + 4 * mt);
-        const float4 yv = *reinterpret_cast<const float4*>(Ys + k * dv + 4 * dt);
-        const float va4[4] = {vv.x, vv.y, vv.z, vv.w}, ya[4] = {yv.x, yv.y, yv.z, yv.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(va4[i], ya[j], acc[i][j]);
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int mm = 4 * mt + i, dd = 4 * dt + j;
-          if (mm < m && dd < d) atomicAdd(psi_part + mm + int64_t(dd) * m, double(acc[i][j]));
-        }
-    }
     __syncthreads();
     TCP_ADD(7, tp7);
   }
-  yy_acc = warp_sum_d(yy_acc);
   kl_acc = warp_sum_d(kl_acc);
-  if (lane == 0) {
-    red[warp] = yy_acc;
-    red[32 + warp] = kl_acc;
-  }
+  if (lane == 0) red[32 + warp] = kl_acc;
   tc::fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -358,13 +262,9 @@ __global__ void __launch_bounds__(kThreadsF, 1)
     tc::tmem_dealloc(tmem, 512);
   }
   if (tid == 0) {
-    double s1 = 0.0, s2 = 0.0;
-    for (int i = 0; i < nw; ++i) {
-      s1 += red[i];
-      s2 += red[32 + i];
-    }
-    cta_part[0] = s1;
-    cta_part[1] = s2;
+    double s2 = 0.0;
+    for (int i = 0; i < nw; ++i) s2 += red[32 + i];
+    cta_part[1] = s2;  // yy and Psi come from psi1_fwd_kernel rows
   }
 }
 
@@ -386,13 +286,15 @@ __global__ void fwd_reduce_tc(const double* __restrict__ part, int64_t pstride, 
   }
 }
 
+// LaunchGeom.grid of the TC passes = partial rows (psi2 CTAs + psi1 rows), for buffer sizing.
 template <int Q>
 int plan_fwd_tc_q(const PsiConst& P, int num_sms, LaunchGeom* geom) {
   const size_t smem = fwd_tc_smem_bytes(P);
   auto kern = psi_fwd_tc_kernel<Q>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return 3;
   const int64_t nchunks = (P.n + 31) / 32;
-  *geom = LaunchGeom{int(std::min<int64_t>(nchunks, num_sms)), kThreadsF, smem};
+  const int g2 = int(std::min<int64_t>(nchunks, num_sms));
+  *geom = LaunchGeom{g2 + psi1_fwd_rows(P, num_sms), kThreadsF, smem};
   return 0;
 }
 
@@ -408,15 +310,17 @@ int launch_fwd_tc_q(const PsiConst& P0, double* part, double* packed, int* err_f
   if (int rc = plan_fwd_tc_q<Q>(P, num_sms, &g)) return rc;
   const int64_t nchunks = (P.n + 31) / 32;
   const int64_t pstride = fwd_part_count(P.m, P.d);
-  if (g.grid > 0) {
+  const int g2 = int(std::min<int64_t>(nchunks, num_sms)), g1 = g.grid - g2;
+  if (nchunks > 0) {
     if (cudaMemsetAsync(part, 0, sizeof(double) * pstride * g.grid, st) != cudaSuccess) return 3;
     if (e0) cudaEventRecord(e0, st);
-    psi_fwd_tc_kernel<Q><<<g.grid, g.threads, g.smem, st>>>(P, nchunks, part, pstride, err_flag);
-    if (e1) cudaEventRecord(e1, st);
+    psi_fwd_tc_kernel<Q><<<g2, g.threads, g.smem, st>>>(P, nchunks, part, pstride, err_flag);
     g_tc_launches.fetch_add(1);
+    if (int rc = psi1_forward(P, part + int64_t(g2) * pstride, pstride, g1, err_flag, st)) return rc;
+    if (e1) cudaEventRecord(e1, st);
   }
-  fwd_reduce_tc<<<int((pstride + 255) / 256), 256, 0, st>>>(part, pstride, g.grid, pstride, packed,
-                                                            double(P.n) * P.variance_d, double(P.n));
+  fwd_reduce_tc<<<int((pstride + 255) / 256), 256, 0, st>>>(part, pstride, nchunks > 0 ? g.grid : 0, pstride,
+                                                            packed, double(P.n) * P.variance_d, double(P.n));
   g_tc_launches.fetch_add(1);
   tc_profile_report("fwd", st);
   if (geom) *geom = g;
@@ -443,9 +347,9 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
 size_t bwd_tc_smem_bytes(const PsiConst& P, int Q) {
   const TCLayout L = tc_layout(P.q, P.m);
   size_t f = 2 * size_t(L.n1) * L.k1 + kPipes * 2 * (2 * 128 * size_t(L.k1)) + size_t(P.mv) * P.qv +
-             rows_floats(P.qv) + size_t(P.mv) * 32 + size_t(P.dv) * 32 + size_t(P.mv) * P.mv;
+             rows_floats(P.qv) + size_t(P.mv) * P.mv;
   // the per-warp merge buffer aliases the A1 operand buffers (used only after the tile loop)
-  const size_t a1f = kPipes * 2 * (2 * 128 * size_t(L.k1)), accf = size_t(kThreadsTC / 32) * (2 + 5 * Q) * 32;
+  const size_t a1f = kPipes * 2 * (2 * 128 * size_t(L.k1)), accf = size_t(kThreadsTC / 32) * (1 + 3 * Q) * 32;
   if (accf > a1f) f += accf - a1f;
   return f * 4 + (Q + 1) * 32 * sizeof(double) + 64;
 }
@@ -453,8 +357,8 @@ size_t bwd_tc_smem_bytes(const PsiConst& P, int Q) {
 template <int Q>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     psi_bwd_tc_kernel(PsiConst P, BwdConst B, int64_t nchunks, double* __restrict__ part, int64_t pstride) {
-  constexpr int NACC = 2 + 5 * Q;
-  constexpr int T0 = 0, Y1 = 1, Y2 = 1 + Q, XX = 1 + 2 * Q, P0 = 1 + 3 * Q, P1 = 2 + 3 * Q, P2 = 2 + 4 * Q;
+  constexpr int NACC = 1 + 3 * Q;
+  constexpr int T0 = 0, Y1 = 1, Y2 = 1 + Q, XX = 1 + 2 * Q;
   constexpr int Q4 = (Q + 3) / 4;
   extern __shared__ __align__(1024) float sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5, nthr = blockDim.x;
@@ -468,10 +372,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   float* Zc = p;
   p += mv * qv;
   Rows R = carve_rows(p, qv);
-  float* Ys = p;
-  p += P.dv * 32;
-  float* G1s = p;
-  p += mv * 32;
   float* Us = p;  // U = dL/dPhi, [mv][mv] (symmetric, zero padded)
   p += mv * mv;
   float* acc = A1;  // per-warp per-datapoint merge buffer, aliases A1 (only used after the tile loop)
@@ -515,53 +415,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const bool valid = n < P.n;
     TCP_MARK(tp0);
     load_rows<Q>(P, n0, R, nullptr, nullptr);
-#pragma unroll 4
-    for (int dd = warp; dd < d; dd += nw) Ys[dd * 32 + lane] = valid ? float(P.y[dd * P.ld_y + n]) : 0.f;
-    __syncthreads();
-    {  // psi1 adjoint weights G1_nm = v1_nm <y_n, dPsi_m>
-      float mu[Q], d1[Q];
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        mu[q] = R.mu[q * 32 + lane];
-        d1[q] = R.d1[q * 32 + lane];
-      }
-      const float b1 = R.b1[lane];
-      for (int mt = warp; mt < (mv >> 2); mt += nw) {
-        float w4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
-        for (int dd = 0; dd < d; ++dd) {
-          const float yv = Ys[dd * 32 + lane];
-          const float4 dp = __ldg(reinterpret_cast<const float4*>(B.dpsi + int64_t(dd) * mv) + mt);
-          w4[0] = fmaf(yv, dp.x, w4[0]);
-          w4[1] = fmaf(yv, dp.y, w4[1]);
-          w4[2] = fmaf(yv, dp.z, w4[2]);
-          w4[3] = fmaf(yv, dp.w, w4[3]);
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int mm = 4 * mt + i;
-          float g = 0.f;
-          if (mm < m) {
-            float z[Q];
-            load_z<Q>(Zc + mm * qv, z);
-            float e = 0.f;
-#pragma unroll
-            for (int q = 0; q < Q; ++q) {
-              const float df = mu[q] - z[q];
-              e = fmaf(df * df, d1[q], e);
-            }
-            g = w4[i] * ex2(fmaf(-0.5f * kLog2e, e, b1));
-          }
-          G1s[mm * 32 + lane] = g;
-        }
-      }
-    }
     __syncthreads();
     TCP_ADD(0, tp0);
 
-    float t0 = 0.f, p0 = 0.f, y1[Q], y2[Q], xq[Q], p1[Q], p2[Q];
+    float t0 = 0.f, y1[Q], y2[Q], xq[Q];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) y1[q] = y2[q] = xq[q] = p1[q] = p2[q] = 0.f;
+    for (int q = 0; q < Q; ++q) y1[q] = y2[q] = xq[q] = 0.f;
     for (int t = pipe; t < MT8; t += kPipes) {
       const int a0 = 8 * t + wq, a1i = a0 + 4;
       const bool va0 = a0 < m, va1 = a1i < m;
@@ -639,9 +498,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const bool va = h ? va1 : va0;
         const int ac = h ? ac1 : ac0;
         const float Ra = h ? Racc.y : Racc.x;
-        const float g1 = va ? G1s[a * 32 + lane] : 0.f;
         t0 += Ra;
-        p0 += g1;
         float vals[Q];
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
@@ -650,12 +507,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           y1[q] = fmaf(z, Ra, y1[q]);
           y2[q] = fmaf(z * z, Ra, y2[q]);
           xq[q] = fmaf(z, Sa, xq[q]);
-          p1[q] = fmaf(z, g1, p1[q]);
-          p2[q] = fmaf(z * z, g1, p2[q]);
-          const float mu = R.mu[q * 32 + lane], d2 = R.d2[q * 32 + lane], d1 = R.d1[q * 32 + lane];
+          const float mu = R.mu[q * 32 + lane], d2 = R.d2[q * 32 + lane];
           const float kn = R.sv[q * 32 + lane] * P.il2[q] * d2;
           const float c2 = 0.5f * (P.il2[q] + d2);
-          vals[q] = 2.f * (fmaf(d2, mu, -c2 * z) * Ra + kn * Sa) + g1 * d1 * (mu - z);
+          vals[q] = 2.f * (fmaf(d2, mu, -c2 * z) * Ra + kn * Sa);
         }
         constexpr int QR = Q <= 8 ? 8 : (Q <= 16 ? 16 : 32);
         float vr[QR];
@@ -676,49 +531,34 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     {
       float* accw = acc + warp * NACC * 32;
       accw[T0 * 32 + lane] = t0;
-      accw[P0 * 32 + lane] = p0;
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
         accw[(Y1 + q) * 32 + lane] = y1[q];
         accw[(Y2 + q) * 32 + lane] = y2[q];
         accw[(XX + q) * 32 + lane] = xq[q];
-        accw[(P1 + q) * 32 + lane] = p1[q];
-        accw[(P2 + q) * 32 + lane] = p2[q];
       }
     }
     __syncthreads();
     for (int q = warp; q < P.q; q += nw) {
       if (!valid) continue;
-      double T = 0, A1s = 0, A2s = 0, X = 0, Q0 = 0, Q1 = 0, Q2 = 0;
+      double T = 0, A1s = 0, A2s = 0, X = 0;
       for (int w2 = 0; w2 < nw; ++w2) {
         const float* aw = acc + w2 * NACC * 32;
         T += aw[T0 * 32 + lane];
         A1s += aw[(Y1 + q) * 32 + lane];
         A2s += aw[(Y2 + q) * 32 + lane];
         X += aw[(XX + q) * 32 + lane];
-        Q0 += aw[P0 * 32 + lane];
-        Q1 += aw[(P1 + q) * 32 + lane];
-        Q2 += aw[(P2 + q) * 32 + lane];
       }
       const double mu = R.mu[q * 32 + lane], sv = R.sv[q * 32 + lane];
       const double l = P.ls[q], l2 = l * l, il2 = 1.0 / l2, il3 = il2 / l;
-      const double d2 = 1.0 / (2.0 * sv + l2), d1 = 1.0 / (sv + l2);
-      const double q1 = mu * mu * Q0 - 2.0 * mu * Q1 + Q2;
+      const double d2 = 1.0 / (2.0 * sv + l2);
       const double dl = T * (2.0 * sv * d2 / l + 2.0 * l * d2 * d2 * mu * mu) - 4.0 * l * d2 * d2 * mu * A1s +
-                        A2s * (il3 + l * d2 * d2) - X * (il3 - l * d2 * d2) + sv * d1 * Q0 / l + l * d1 * d1 * q1;
+                        A2s * (il3 + l * d2 * d2) - X * (il3 - l * d2 * d2);
       dacc[q * 32 + lane] += dl;
-      if (q == 0) dacc[Q * 32 + lane] += (2.0 * T + Q0) * inv_var;
-      if (B.write_local) {
-        double dmu = -2.0 * d2 * mu * T + 2.0 * d2 * A1s - d1 * (mu * Q0 - Q1);
-        double ds = T * (-d2 + 2.0 * d2 * d2 * mu * mu) - 4.0 * d2 * d2 * mu * A1s + d2 * d2 * (A2s + X) -
-                    0.5 * d1 * Q0 + 0.5 * d1 * d1 * q1;
-        if (B.add_kl) {
-          const double mo = P.mu[q * P.ld_mu + n], so = P.s[q * P.ld_s + n];
-          dmu -= mo;
-          ds -= 0.5 * (1.0 - 1.0 / so);
-        }
-        B.d_mu[q * B.ld_g + n] = dmu;
-        B.d_s[q * B.ld_g + n] = ds;
+      if (q == 0) dacc[Q * 32 + lane] += 2.0 * T * inv_var;
+      if (B.write_local) {  // psi1_bwd_kernel wrote the psi1 and KL parts first
+        B.d_mu[q * B.ld_g + n] += -2.0 * d2 * mu * T + 2.0 * d2 * A1s;
+        B.d_s[q * B.ld_g + n] += T * (-d2 + 2.0 * d2 * d2 * mu * mu) - 4.0 * d2 * d2 * mu * A1s + d2 * d2 * (A2s + X);
       }
     }
     __syncthreads();
@@ -756,7 +596,8 @@ int plan_bwd_tc_q(const PsiConst& P, int num_sms, LaunchGeom* geom) {
   auto kern = psi_bwd_tc_kernel<Q>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return 3;
   const int64_t nchunks = (P.n + 31) / 32;
-  *geom = LaunchGeom{int(std::min<int64_t>(nchunks, num_sms)), kThreadsTC, smem};
+  const int g2 = int(std::min<int64_t>(nchunks, num_sms));
+  *geom = LaunchGeom{g2 + 8 * psi1_bwd_ctas(P, num_sms), kThreadsTC, smem};
   return 0;
 }
 
@@ -795,15 +636,18 @@ int launch_bwd_tc_q(const PsiConst& P0, const BwdConst& B, double* part, double*
   if (int rc = plan_bwd_tc_q<Q>(P, num_sms, &g)) return rc;
   const int64_t nchunks = (P.n + 31) / 32;
   const int64_t pstride = bwd_part_count(P.m, P.q);
-  if (g.grid > 0) {
+  const int g2 = int(std::min<int64_t>(nchunks, num_sms)), c1 = (g.grid - g2) / 8;
+  if (nchunks > 0) {
     if (cudaMemsetAsync(part, 0, sizeof(double) * pstride * g.grid, st) != cudaSuccess) return 3;
     if (e0) cudaEventRecord(e0, st);
-    psi_bwd_tc_kernel<Q><<<g.grid, g.threads, g.smem, st>>>(P, B, nchunks, part, pstride);
-    if (e1) cudaEventRecord(e1, st);
+    // psi1 first: it writes d_mu / d_s (psi1 + KL parts); the psi2 kernel accumulates into them
+    if (int rc = psi1_backward(P, B, part + int64_t(g2) * pstride, pstride, c1, st)) return rc;
+    psi_bwd_tc_kernel<Q><<<g2, g.threads, g.smem, st>>>(P, B, nchunks, part, pstride);
     g_tc_launches.fetch_add(1);
+    if (e1) cudaEventRecord(e1, st);
   }
-  bwd_reduce_tc<<<int((pstride + 255) / 256), 256, 0, st>>>(part, pstride, g.grid, pstride, packed,
-                                                            B.d_phi * double(P.n));
+  bwd_reduce_tc<<<int((pstride + 255) / 256), 256, 0, st>>>(part, pstride, nchunks > 0 ? g.grid : 0, pstride,
+                                                            packed, B.d_phi * double(P.n));
   g_tc_launches.fetch_add(1);
   tc_profile_report("bwd", st);
   if (geom) *geom = g;
