@@ -10,6 +10,8 @@
 //                     G1_nm = v1_nm <y_n, dPsi_m>; writes d_mu / d_s = psi1 part (+ KL) as the
 //                     first writer, and per-warp partial rows [d_variance, d_l, d_z].
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <math_constants.h>
 
 #include <atomic>
@@ -25,14 +27,15 @@ using namespace dev;
 
 template <int Q>
 __global__ void __launch_bounds__(256, 2)
-    psi1_fwd_kernel(PsiConst P, int64_t nchunks, double* __restrict__ part, int64_t pstride, int* err_flag) {
+    psi1_fwd_kernel(PsiConst P, int64_t nchunks, double* __restrict__ part, int64_t pstride, int* err_flag,
+                    int with_kl, int n_sacc) {
   extern __shared__ __align__(16) float sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5, nthr = blockDim.x;
   const int m = P.m, mv = P.mv, qv = P.qv, d = P.d, dv = P.dv;
   float* Zc = sm;
   float* V1s = Zc + mv * qv;   // [32][mv]
   float* Ys = V1s + 32 * mv;   // [32][dv]
-  double* red = reinterpret_cast<double*>(Ys + 32 * dv);
+  double* red = reinterpret_cast<double*>(Ys + 32 * dv);  // [2][32]
   for (int i = tid; i < mv * qv; i += nthr) Zc[i] = P.zc[i];
   __syncthreads();
   const int64_t npairs = int64_t(m) * (m + 1) / 2;
@@ -40,10 +43,24 @@ __global__ void __launch_bounds__(256, 2)
   double* const psi_part = cta_part + 2 + npairs;
   const int DT = dv >> 2;
   const int ntiles1 = (mv >> 2) * DT;
-  double yy_acc = 0.0;
+  double yy_acc = 0.0, kl_acc = 0.0;
+  // Psi tiles t < n_sacc accumulate in fp64 in shared memory across all chunks of this CTA (each
+  // tile has one owning thread; layout [16][n_sacc] so a warp's accesses are conflict-free); the
+  // CTA is the single writer of its partial row.  Tiles beyond n_sacc fall back to RED.ADD.F64.
+  double* sacc = red + 64;
+  for (int i = tid; i < 16 * n_sacc; i += nthr) sacc[i] = 0.0;
   for (int64_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
     const int64_t n = chunk * 32 + lane;
     const bool valid = n < P.n;
+    const int64_t nn = valid ? n : 0;
+    // all raw loads first (one memory latency per chunk)
+    double md[Q], sd[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int qq = q < P.q ? q : 0;
+      md[q] = __ldg(P.mu + qq * P.ld_mu + nn);
+      sd[q] = P.expected ? __ldg(P.s + qq * P.ld_s + nn) : 0.0;
+    }
     // per-lane psi1 constants (psi_stats.hpp:144-159): centred mu, 1/(S+l^2), log2 c1
     float mu[Q], d1[Q], b1 = P.log2_var;
 #pragma unroll
@@ -51,9 +68,13 @@ __global__ void __launch_bounds__(256, 2)
       mu[q] = 0.f;
       d1[q] = 0.f;
       if (q < P.q && valid) {
-        const double md = P.mu[q * P.ld_mu + n];
-        const float sv = P.expected ? float(P.s[q * P.ld_s + n]) : 0.f;
-        mu[q] = float(md - P.center[q]);
+        const float sv = float(sd[q]);
+        if (with_kl && (q % nw) == warp) {  // validation (psi_stats.hpp:119-120) + KL (parallel.hpp:148-149)
+          if (!isfinite(md[q])) atomicOr(err_flag, 1);
+          if (P.expected && !(sd[q] > 0.0 && isfinite(sd[q]))) atomicOr(err_flag, 4);
+          if (P.expected) kl_acc += 0.5 * (sd[q] + md[q] * md[q] - log(sd[q]) - 1.0);
+        }
+        mu[q] = float(md[q] - P.center[q]);
         d1[q] = 1.f / (sv + P.l2[q]);
         b1 += -0.5f * log2f(1.f + sv * P.il2[q]);
       }
@@ -74,52 +95,73 @@ __global__ void __launch_bounds__(256, 2)
       }
       V1s[lane * mv + mm] = v;
     }
-#pragma unroll 2
+#pragma unroll 4
     for (int dd = warp; dd < dv; dd += nw) {
-      float yv = 0.f;
-      if (dd < d && valid) {
-        const double yd = P.y[dd * P.ld_y + n];
-        if (!isfinite(yd)) atomicOr(err_flag, 1);
-        yy_acc += yd * yd;
-        yv = float(yd);
-      }
-      Ys[lane * dv + dd] = yv;
+      const double y0 = (dd < d && valid) ? __ldg(P.y + dd * P.ld_y + n) : 0.0;
+      if (!isfinite(y0)) atomicOr(err_flag, 1);
+      yy_acc += y0 * y0;
+      Ys[lane * dv + dd] = float(y0);
     }
     __syncthreads();
     for (int t = tid; t < ntiles1; t += nthr) {
       const int mt = t / DT, dt = t - mt * DT;
       float acc[4][4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+        for (int j = 0; j < 4; ++j) acc[r][j] = 0.f;
 #pragma unroll 8
       for (int k = 0; k < 32; ++k) {
         const float4 vv = *reinterpret_cast<const float4*>(V1s + k * mv + 4 * mt);
         const float4 yv = *reinterpret_cast<const float4*>(Ys + k * dv + 4 * dt);
         const float va[4] = {vv.x, vv.y, vv.z, vv.w}, ya[4] = {yv.x, yv.y, yv.z, yv.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(va[i], ya[j], acc[i][j]);
+          for (int j = 0; j < 4; ++j) acc[r][j] = fmaf(va[r], ya[j], acc[r][j]);
       }
+      if (t < n_sacc) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int mm = 4 * mt + i, dd = 4 * dt + j;
-          if (mm < m && dd < d) atomicAdd(psi_part + mm + int64_t(dd) * m, double(acc[i][j]));
-        }
+          for (int j = 0; j < 4; ++j) sacc[(4 * r + j) * n_sacc + t] += double(acc[r][j]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int mm = 4 * mt + r, dd = 4 * dt + j;
+            if (mm < m && dd < d) atomicAdd(psi_part + mm + int64_t(dd) * m, double(acc[r][j]));
+          }
+      }
     }
     __syncthreads();
   }
+  for (int t = tid; t < n_sacc; t += nthr) {
+    const int mt = t / DT, dt = t - mt * DT;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int mm = 4 * mt + r, dd = 4 * dt + j;
+        if (mm < m && dd < d) psi_part[mm + int64_t(dd) * m] = sacc[(4 * r + j) * n_sacc + t];
+      }
+  }
   yy_acc = warp_sum_d(yy_acc);
-  if (lane == 0) red[warp] = yy_acc;
+  kl_acc = warp_sum_d(kl_acc);
+  if (lane == 0) {
+    red[warp] = yy_acc;
+    red[32 + warp] = kl_acc;
+  }
   __syncthreads();
   if (tid == 0) {
-    double s = 0.0;
-    for (int i = 0; i < nw; ++i) s += red[i];
+    double s = 0.0, k = 0.0;
+    for (int i = 0; i < nw; ++i) {
+      s += red[i];
+      k += red[32 + i];
+    }
     cta_part[0] = s;
+    if (with_kl) cta_part[1] = k;
   }
 }
 
@@ -244,14 +286,19 @@ __global__ void __launch_bounds__(256, 2)
 
 template <int Q>
 int launch_psi1_fwd_q(const PsiConst& P, double* part_rows, int64_t pstride, int rows, int* err_flag,
-                      cudaStream_t st) {
+                      cudaStream_t st, int with_kl) {
   const int64_t nchunks = (P.n + 31) / 32;
-  const size_t smem = sizeof(float) * (size_t(P.mv) * P.qv + 32 * size_t(P.mv) + 32 * size_t(P.dv)) +
+  const size_t base = sizeof(float) * (size_t(P.mv) * P.qv + 32 * size_t(P.mv) + 32 * size_t(P.dv)) +
                       64 * sizeof(double);
+  // shared fp64 Psi accumulators: as many tiles as fit next to two resident CTAs per SM
+  const int ntiles1 = (P.mv / 4) * (P.dv / 4);
+  const size_t budget = 110 * 1024;
+  const int n_sacc = base >= budget ? 0 : int(std::min<size_t>(ntiles1, (budget - base) / (16 * sizeof(double))));
+  const size_t smem = base + size_t(n_sacc) * 16 * sizeof(double);
   auto kern = psi1_fwd_kernel<Q>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return 3;
   if (rows > 0) {
-    kern<<<rows, 256, smem, st>>>(P, nchunks, part_rows, pstride, err_flag);
+    kern<<<rows, 256, smem, st>>>(P, nchunks, part_rows, pstride, err_flag, with_kl, n_sacc);
     g_tc_launches.fetch_add(1);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
@@ -301,8 +348,9 @@ int psi1_bwd_ctas(const PsiConst& P, int num_sms) {
     default: return 1;                   \
   }
 
-int psi1_forward(const PsiConst& P, double* part_rows, int64_t pstride, int rows, int* err_flag, void* stream) {
-  SGPX_P1_DISPATCH(launch_psi1_fwd_q, P, part_rows, pstride, rows, err_flag, static_cast<cudaStream_t>(stream))
+int psi1_forward(const PsiConst& P, double* part_rows, int64_t pstride, int rows, int* err_flag, void* stream,
+                 int with_kl) {
+  SGPX_P1_DISPATCH(launch_psi1_fwd_q, P, part_rows, pstride, rows, err_flag, static_cast<cudaStream_t>(stream), with_kl)
 }
 
 int psi1_backward(const PsiConst& P, const BwdConst& B, double* part_rows, int64_t pstride, int ctas,

@@ -613,7 +613,7 @@ int64_t launches_issued() { return g_launches.load() + g_tc_launches.load(); }
 
 // Kernel family: tensor-core (tcgen05) psi2 when the shape fits (M <= 128), else SIMT.
 // SGPX_PSI_IMPL=simt forces the SIMT kernels (A/B comparisons, profiling).
-bool use_tc(const PsiConst& P, bool backward) {
+int impl_forced() {
   static const int forced = [] {
     const char* e = getenv("SGPX_PSI_IMPL");
     if (!e) return 0;
@@ -621,6 +621,14 @@ bool use_tc(const PsiConst& P, bool backward) {
     if (!strcmp(e, "tc")) return 2;
     return 0;
   }();
+  return forced;
+}
+
+// Forward on the pair-row tensor-core kernel (default when it fits); SGPX_PSI_IMPL=simt|tc overrides.
+bool use_pairs(const PsiConst& P) { return impl_forced() == 0 && pairs_supported(P); }
+
+bool use_tc(const PsiConst& P, bool backward) {
+  const int forced = impl_forced();
   if (forced == 1) return false;
   if (backward) return tc_backward_available() && tc_backward_fits(P);
   // forward: the SIMT kernel is faster until the TC forward is restructured (profiles/r01_*)
@@ -649,6 +657,27 @@ int instantiated_q(int q) { return pick_q(q); }
 
 int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, int num_sms, void* stream,
                 LaunchGeom* geom, void* ev_begin, void* ev_end) {
+  if (use_pairs(P)) {
+    LaunchGeom g{};
+    if (int rc = plan_forward(P, num_sms, &g)) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t pstride = fwd_part_count(P.m, P.d);
+    const int g1 = psi1_fwd_rows(P, num_sms);
+    if (cudaMemsetAsync(part, 0, sizeof(double) * pstride * g1, st) != cudaSuccess) return 3;
+    if (ev_begin) cudaEventRecord(cudaEvent_t(ev_begin), st);
+    if (g1 > 0) {
+      if (int rc = psi1_forward(P, part, pstride, g1, err_flag, stream, 1)) return rc;
+    }
+    fwd_reduce_kernel<<<int((pstride + 255) / 256), 256, 0, st>>>(part, pstride, g1, pstride, packed,
+                                                                   double(P.n) * P.variance_d, double(P.n));
+    g_launches.fetch_add(1);
+    if (P.n > 0) {
+      if (int rc = psi2_forward_pairs(P, part + int64_t(g1) * pstride, packed, num_sms, stream)) return rc;
+    }
+    if (ev_end) cudaEventRecord(cudaEvent_t(ev_end), st);
+    if (geom) *geom = g;
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  }
   if (use_tc(P, false)) return psi_forward_tc(P, part, packed, err_flag, num_sms, stream, geom, ev_begin, ev_end);
   const int qi = pick_q(P.q);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -670,6 +699,12 @@ int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* pac
 }
 
 int plan_forward(const PsiConst& P, int num_sms, LaunchGeom* geom) {
+  if (use_pairs(P)) {  // partial rows: psi1 rows + the Phi split partials
+    const int64_t pstride = fwd_part_count(P.m, P.d);
+    const int64_t extra = (pairs_part_doubles(P, num_sms) + pstride - 1) / pstride;
+    *geom = LaunchGeom{int(psi1_fwd_rows(P, num_sms) + extra), 256, 0};
+    return 0;
+  }
   if (use_tc(P, false)) return plan_forward_tc(P, num_sms, geom);
   const int qi = pick_q(P.q);
 #define CALL_PF(QQ) plan_fwd_q<QQ>(P, num_sms, geom)

@@ -94,7 +94,12 @@ int psi_backward_tc(const PsiConst& P, const BwdConst& B, double* part, double* 
 // Standalone psi1 passes (psi1_kernels.cu), paired with the TC psi2 kernels.
 int psi1_fwd_rows(const PsiConst& P, int num_sms);
 int psi1_bwd_ctas(const PsiConst& P, int num_sms);  // each CTA writes 8 per-warp partial rows
-int psi1_forward(const PsiConst& P, double* part_rows, int64_t pstride, int rows, int* err_flag, void* stream);
+int psi1_forward(const PsiConst& P, double* part_rows, int64_t pstride, int rows, int* err_flag, void* stream,
+                 int with_kl);
+// Pair-row tensor-core forward (psi_pairs.cu): Phi into packed[4 + p] (after the psi1 reduce).
+bool pairs_supported(const PsiConst& P);
+int64_t pairs_part_doubles(const PsiConst& P, int num_sms);
+int psi2_forward_pairs(const PsiConst& P, double* phi_part, double* packed, int num_sms, void* stream);
 int psi1_backward(const PsiConst& P, const BwdConst& B, double* part_rows, int64_t pstride, int ctas, void* stream);
 
 // psi1_expected: out n x m col-major fp64 (ld_out).

@@ -316,7 +316,7 @@ int launch_fwd_tc_q(const PsiConst& P0, double* part, double* packed, int* err_f
     if (e0) cudaEventRecord(e0, st);
     psi_fwd_tc_kernel<Q><<<g2, g.threads, g.smem, st>>>(P, nchunks, part, pstride, err_flag);
     g_tc_launches.fetch_add(1);
-    if (int rc = psi1_forward(P, part + int64_t(g2) * pstride, pstride, g1, err_flag, st)) return rc;
+    if (int rc = psi1_forward(P, part + int64_t(g2) * pstride, pstride, g1, err_flag, st, 0)) return rc;
     if (e1) cudaEventRecord(e1, st);
   }
   fwd_reduce_tc<<<int((pstride + 255) / 256), 256, 0, st>>>(part, pstride, nchunks > 0 ? g.grid : 0, pstride,

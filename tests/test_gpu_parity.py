@@ -150,3 +150,23 @@ def test_engine_evaluate_parity(sgp, orc, latent):
     if latent:
         assert norm_rel_err(g.d_mu, ref.d_mu) < GRAD_TOL
         assert norm_rel_err(g.d_s, ref.d_s) < GRAD_TOL
+
+
+@pytest.mark.parametrize("shape", [(100000, 8, 50, 48), (30000, 10, 50, 100)])
+def test_multi_chunk_parity(sgp, orc, shape):
+    """Shards large enough that every CTA of every kernel walks many chunks (pipelined producer /
+    consumer rings wrap several times; psi1 tiles exceed one per thread)."""
+    n, q, d, m = shape
+    mu, s, y, z, var, ls = problem(7, n, q, d, m)
+    rng = np.random.default_rng(8)
+    adj = sym_adj(rng, m, d)
+    k = sgp.KernelSpec(var, ls)
+    st, g = sgp.sweep_stats(True, mu, s, y, z, k, adj=sgp.StatsAdjoints(*adj))
+    wst, wg = orc.sweep_stats(True, mu, s, y, z, var, ls, adj=adj)
+    assert rel_err(st.yy, wst.yy) < 1e-12
+    assert norm_rel_err(st.phi_big, wst.phi_big) < STAT_TOL
+    assert norm_rel_err(st.psi_y, wst.psi_y) < STAT_TOL
+    assert norm_rel_err(g.d_z, wg.d_z) < GRAD_TOL
+    assert norm_rel_err(g.d_lengthscales, wg.d_lengthscales) < GRAD_TOL
+    assert norm_rel_err(g.d_mu, wg.d_mu) < GRAD_TOL
+    assert norm_rel_err(g.d_s, wg.d_s) < GRAD_TOL
