@@ -17,6 +17,22 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (offloads MUFU.EX2, which is 16/clk/SM): round-to-nearest split x = j + f,
+// f in [-1/2, 1/2], degree-5 relative-minimax polynomial (max rel. error 2.0e-7 in fp32 Horner,
+// on par with ex2.approx), exponent added with one integer op.  x is clamped at -125 (returns
+// ~2^-125 instead of 0 for -inf; harmless in sums).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: round(x) lands in the low mantissa bits
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(0.001328189391642809f, f, 0.009675598703324795f);
+  p = fmaf(p, f, 0.05550696700811386f);
+  p = fmaf(p, f, 0.24022118747234344f);
+  p = fmaf(p, f, 0.6931470036506653f);
+  p = fmaf(p, f, 1.0000001192092896f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 __device__ __forceinline__ int64_t pair_index(int a, int b, int m) {
   // upper triangle, m1-major order (psi_stats.hpp:85-97)
   return int64_t(a) * (2 * m - a + 1) / 2 + (b - a);

@@ -624,8 +624,12 @@ int impl_forced() {
   return forced;
 }
 
-// Forward on the pair-row tensor-core kernel (default when it fits); SGPX_PSI_IMPL=simt|tc overrides.
-bool use_pairs(const PsiConst& P) { return impl_forced() == 0 && pairs_supported(P); }
+// Row-tile tensor-core psi2 (default when it fits); SGPX_PSI_IMPL=simt|tc selects the older kernels.
+bool use_rt(const PsiConst& P) { return impl_forced() == 0 && rt_supported(P); }
+
+const double* rt_fwd_region(const PsiConst& P, const double* fwd_part, int num_sms) {
+  return fwd_part + int64_t(psi1_fwd_rows(P, num_sms)) * fwd_part_count(P.m, P.d);
+}
 
 bool use_tc(const PsiConst& P, bool backward) {
   const int forced = impl_forced();
@@ -657,13 +661,13 @@ int instantiated_q(int q) { return pick_q(q); }
 
 int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, int num_sms, void* stream,
                 LaunchGeom* geom, void* ev_begin, void* ev_end) {
-  if (use_pairs(P)) {
+  if (use_rt(P)) {
     LaunchGeom g{};
     if (int rc = plan_forward(P, num_sms, &g)) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t pstride = fwd_part_count(P.m, P.d);
     const int g1 = psi1_fwd_rows(P, num_sms);
-    if (cudaMemsetAsync(part, 0, sizeof(double) * pstride * g1, st) != cudaSuccess) return 3;
+    if (g1 > 0 && cudaMemsetAsync(part, 0, sizeof(double) * pstride * g1, st) != cudaSuccess) return 3;
     if (ev_begin) cudaEventRecord(cudaEvent_t(ev_begin), st);
     if (g1 > 0) {
       if (int rc = psi1_forward(P, part, pstride, g1, err_flag, stream, 1)) return rc;
@@ -671,9 +675,7 @@ int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, 
     fwd_reduce_kernel<<<int((pstride + 255) / 256), 256, 0, st>>>(part, pstride, g1, pstride, packed,
                                                                    double(P.n) * P.variance_d, double(P.n));
     g_launches.fetch_add(1);
-    if (P.n > 0) {
-      if (int rc = psi2_forward_pairs(P, part + int64_t(g1) * pstride, packed, num_sms, stream)) return rc;
-    }
+    if (int rc = rt_forward(P, part + int64_t(g1) * pstride, packed, num_sms, stream)) return rc;
     if (ev_end) cudaEventRecord(cudaEvent_t(ev_end), st);
     if (geom) *geom = g;
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
@@ -689,6 +691,26 @@ int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, 
 
 int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
                  LaunchGeom* geom, void* ev_begin, void* ev_end) {
+  if (use_rt(P)) {
+    if (!B.fwd_rt) return 1;
+    LaunchGeom g{};
+    if (int rc = plan_backward(P, num_sms, &g)) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t pstride = bwd_part_count(P.m, P.q);
+    const int c1 = P.n > 0 ? psi1_bwd_ctas(P, num_sms) : 0, rows = 8 * c1 + 1;
+    if (cudaMemsetAsync(part, 0, sizeof(double) * pstride * rows, st) != cudaSuccess) return 3;
+    if (ev_begin) cudaEventRecord(cudaEvent_t(ev_begin), st);
+    // psi1 first: it writes d_mu / d_s (psi1 + KL parts); the psi2 kernel accumulates into them
+    if (c1 > 0) {
+      if (int rc = psi1_backward(P, B, part, pstride, c1, stream)) return rc;
+    }
+    if (int rc = rt_backward(P, B, part + int64_t(rows) * pstride, part + int64_t(8 * c1) * pstride, num_sms, stream))
+      return rc;
+    if (ev_end) cudaEventRecord(cudaEvent_t(ev_end), st);
+    if (int rc = bwd_reduce_rows(part, pstride, rows, packed, B.d_phi * double(P.n), stream)) return rc;
+    if (geom) *geom = g;
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  }
   if (use_tc(P, true)) return psi_backward_tc(P, B, part, packed, num_sms, stream, geom, ev_begin, ev_end);
   const int qi = pick_q(P.q);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -699,10 +721,10 @@ int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* pac
 }
 
 int plan_forward(const PsiConst& P, int num_sms, LaunchGeom* geom) {
-  if (use_pairs(P)) {  // partial rows: psi1 rows + the Phi split partials
+  if (use_rt(P)) {  // partial rows: psi1 rows + the row-tile region
     const int64_t pstride = fwd_part_count(P.m, P.d);
-    const int64_t extra = (pairs_part_doubles(P, num_sms) + pstride - 1) / pstride;
-    *geom = LaunchGeom{int(psi1_fwd_rows(P, num_sms) + extra), 256, 0};
+    const int64_t extra = (rt_fwd_doubles(P, num_sms) + pstride - 1) / pstride;
+    *geom = LaunchGeom{int(psi1_fwd_rows(P, num_sms) + extra), 448, 0};
     return 0;
   }
   if (use_tc(P, false)) return plan_forward_tc(P, num_sms, geom);
@@ -713,6 +735,13 @@ int plan_forward(const PsiConst& P, int num_sms, LaunchGeom* geom) {
 }
 
 int plan_backward(const PsiConst& P, int num_sms, LaunchGeom* geom) {
+  if (use_rt(P)) {  // psi1 rows (8 per CTA) + 1 psi2 row + the row-tile scratch
+    const int64_t pstride = bwd_part_count(P.m, P.q);
+    const int c1 = P.n > 0 ? psi1_bwd_ctas(P, num_sms) : 0;
+    const int64_t extra = (rt_bwd_doubles(P, num_sms) + pstride - 1) / pstride;
+    *geom = LaunchGeom{int(8 * c1 + 1 + extra), 448, 0};
+    return 0;
+  }
   if (use_tc(P, true)) return plan_backward_tc(P, num_sms, geom);
   const int qi = pick_q(P.q);
 #define CALL_PB(QQ) plan_bwd_q<QQ>(P, num_sms, geom)

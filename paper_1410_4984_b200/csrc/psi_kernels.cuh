@@ -49,6 +49,7 @@ struct BwdConst {
   double* d_mu;       // n x q col-major (ld = ld_g), fp64
   double* d_s;
   int64_t ld_g;
+  const double* fwd_rt;  // row-tile path: the forward's feature / pair-sum region (rt_fwd_region)
 };
 
 // Packed per-CTA partial layouts (fp64, CTA-private rows, single-writer per slot):
@@ -96,10 +97,20 @@ int psi1_fwd_rows(const PsiConst& P, int num_sms);
 int psi1_bwd_ctas(const PsiConst& P, int num_sms);  // each CTA writes 8 per-warp partial rows
 int psi1_forward(const PsiConst& P, double* part_rows, int64_t pstride, int rows, int* err_flag, void* stream,
                  int with_kl);
-// Pair-row tensor-core forward (psi_pairs.cu): Phi into packed[4 + p] (after the psi1 reduce).
-bool pairs_supported(const PsiConst& P);
-int64_t pairs_part_doubles(const PsiConst& P, int num_sms);
-int psi2_forward_pairs(const PsiConst& P, double* phi_part, double* packed, int num_sms, void* stream);
+// Row-tile tensor-core psi2 (psi_rowtile.cu).  rt_forward writes Phi into packed[4 + p] (run it
+// after the psi1 reduce) and keeps the per-pair gradient sums + feature arrays in `base`
+// (rt_fwd_doubles) for rt_backward, which accumulates the psi2 parts of d_mu / d_s and writes the
+// pair part of [dvar, dl, dz] (+ the datapoint part of dl) into the partial row `prow`.
+bool rt_supported(const PsiConst& P);
+bool use_rt(const PsiConst& P);
+int64_t rt_fwd_doubles(const PsiConst& P, int num_sms);
+int64_t rt_bwd_doubles(const PsiConst& P, int num_sms);
+int rt_forward(const PsiConst& P, double* base, double* packed, int num_sms, void* stream);
+int rt_backward(const PsiConst& P, const BwdConst& B, double* bbase, double* prow, int num_sms, void* stream);
+// Where the forward placed the row-tile region inside its partial buffer (BwdConst::fwd_rt).
+const double* rt_fwd_region(const PsiConst& P, const double* fwd_part, int num_sms);
+// Fixed-order reduction of backward partial rows into packed grads (psi_tc.cu).
+int bwd_reduce_rows(const double* part, int64_t pstride, int rows, double* packed, double dvar_psi0, void* stream);
 int psi1_backward(const PsiConst& P, const BwdConst& B, double* part_rows, int64_t pstride, int ctas, void* stream);
 
 // psi1_expected: out n x m col-major fp64 (ld_out).

@@ -658,6 +658,13 @@ int launch_bwd_tc_q(const PsiConst& P0, const BwdConst& B, double* part, double*
 
 bool tc_supported(const PsiConst& P) { return P.m >= 1 && P.m <= 128 && P.q >= 1 && P.q <= 32; }
 
+int bwd_reduce_rows(const double* part, int64_t pstride, int rows, double* packed, double dvar_psi0, void* stream) {
+  bwd_reduce_tc<<<int((pstride + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(part, pstride, rows,
+                                                                                          pstride, packed, dvar_psi0);
+  g_tc_launches.fetch_add(1);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
 // Backward TMEM budget per pipeline: 2 n1 + n2 <= 256 columns.
 bool tc_backward_fits(const PsiConst& P) {
   return tc_supported(P) && P.q <= 16 && bwd_tc_smem_bytes(P, instantiated_q(P.q)) <= 227 * 1024;

@@ -366,6 +366,7 @@ void engine_grad_pass(sgpx_engine* e) {
     B.d_mu = e->dmu.get<double>();
     B.d_s = e->ds.get<double>();
     B.ld_g = e->in.n;
+    B.fwd_rt = rt_fwd_region(e->P, e->fpart.get<double>(), ctx->num_sms);
     LaunchGeom g{};
     if (plan_backward(e->P, ctx->num_sms, &g)) throw CudaError("psi backward: launch planning failed");
     e->bpart.ensure(sizeof(double) * bwd_part_count(e->P.m, e->P.q) * std::max(1, g.grid));
@@ -616,6 +617,7 @@ int sgpx_sweep_stats(sgpx_ctx* ctx, int expected, sgpx_cmat mu, sgpx_cmat s, sgp
     B.d_mu = ctx->dmu.get<double>();
     B.d_s = ctx->ds.get<double>();
     B.ld_g = n;
+    B.fwd_rt = rt_fwd_region(P, ctx->fpart.get<double>(), ctx->num_sms);
     if (plan_backward(P, ctx->num_sms, &g)) throw CudaError("psi backward: launch planning failed");
     ctx->bpart.ensure(sizeof(double) * bwd_part_count(P.m, P.q) * std::max(1, g.grid));
     const int64_t gcount = sgpx_packed_grads_count(m, q);

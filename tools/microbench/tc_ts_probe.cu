@@ -1,0 +1,147 @@
+// tc_ts_probe.cu -- kind::tf32 MMA with the A operand in TMEM (written by tcgen05.st 32x32b:
+// TMEM lane = row m, column = k) and B in shared memory, in two roles:
+//   (1) B K-major:  D = A (M x K) * B^T, B stored [N][K] canonical K-major
+//   (2) B MN-major: D = A (M x K) * X,  X stored [K][N] canonical K-major (read transposed)
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+
+constexpr int M = 128, K = 32, N = 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ int canon(int r, int k, int kdim) {
+  return (r >> 3) * (kdim * 8) + (k >> 2) * 32 + (r & 7) * 4 + (k & 3);
+}
+__device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+
+__global__ void probe(const float* A, const float* B, float* D, int trans, uint32_t lbo, uint32_t sbo, uint32_t kstep) {
+  __shared__ __align__(1024) float sb[N * K];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (!trans)
+    for (int i = tid; i < N * K; i += blockDim.x) sb[canon(i / K, i % K, K)] = B[i];  // B[n][k]
+  else
+    for (int i = tid; i < K * N; i += blockDim.x) sb[canon(i / N, i % N, N)] = B[i];  // X[k][n]
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "r"(64));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  // A -> TMEM columns [32, 64): thread = row
+  {
+    const int row = 32 * warp + lane;
+    uint32_t r[32];
+    for (int k = 0; k < 32; ++k) r[k] = __float_as_uint(A[row * K + k]);
+    const uint32_t ta = tmem + 32 + (uint32_t(32 * warp) << 16);
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(ta),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(trans ? 1 : 0) << 16) |
+                         (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+  if (tid == 0) {
+    for (int ks = 0; ks < K / 8; ++ks) {
+      const uint64_t db = make_desc(smem_u32(sb) + ks * kstep, lbo, sbo);
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+          "r"(tmem + 32 + ks * 8), "l"(db), "r"(idesc), "r"(ks ? 1 : 0));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&mbar)));
+  }
+  {
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(smem_u32(&mbar)), "r"(0));
+    }
+  }
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  uint32_t r[32];
+  const uint32_t taddr = tmem + (uint32_t(32 * warp) << 16);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;");
+  const int row = 32 * warp + lane;
+  for (int j = 0; j < N; ++j) D[row * N + j] = __uint_as_float(r[j]);
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64));
+}
+
+int main() {
+  std::vector<float> a(M * K), b(N * K), d(M * N);
+  uint64_t s = 99;
+  auto rnd = [&] {
+    s = s * 6364136223846793005ull + 1442695040888963407ull;
+    return float(int((s >> 40) % 2001) - 1000) / 256.0f;
+  };
+  for (auto& v : a) v = rnd();
+  for (auto& v : b) v = rnd();
+  float *dA, *dB, *dD;
+  cudaMalloc(&dA, a.size() * 4);
+  cudaMalloc(&dB, b.size() * 4);
+  cudaMalloc(&dD, d.size() * 4);
+  cudaMemcpy(dA, a.data(), a.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, b.data(), b.size() * 4, cudaMemcpyHostToDevice);
+  struct Cand { int trans; uint32_t lbo, sbo, kstep; };
+  const Cand cands[] = {{0, 128, K * 32, 256},           // K-major B[n][k]
+                        {1, 128, N * 32, N * 32}, {1, N * 32, 128, N * 32},   // MN-major from X[k][n]
+                        {1, 128, 256, N * 32}, {1, 256, 128, N * 32}};
+  int ok_km = 0, ok_mn = 0;
+  for (auto& c : cands) {
+    cudaMemset(dD, 0, d.size() * 4);
+    probe<<<1, 128>>>(dA, dB, dD, c.trans, c.lbo, c.sbo, c.kstep);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      printf("CUDA error %s\n", cudaGetErrorString(e));
+      return 2;
+    }
+    cudaMemcpy(d.data(), dD, d.size() * 4, cudaMemcpyDeviceToHost);
+    double maxerr = 0, maxref = 0;
+    for (int i = 0; i < M; ++i)
+      for (int j = 0; j < N; ++j) {
+        double ref = 0;
+        for (int k = 0; k < K; ++k) ref += double(a[i * K + k]) * (c.trans ? b[k * N + j] : b[j * K + k]);
+        maxerr = std::fmax(maxerr, std::fabs(ref - d[i * N + j]));
+        maxref = std::fmax(maxref, std::fabs(ref));
+      }
+    const bool ok = maxerr / maxref < 1e-6;
+    printf("A=tmem trans=%d LBO=%4u SBO=%4u kstep=%4u: max|err| %.3e (max|ref| %.1f)%s\n", c.trans, c.lbo, c.sbo,
+           c.kstep, maxerr, maxref, ok ? "  <-- OK" : "");
+    if (ok) (c.trans ? ok_mn : ok_km) = 1;
+  }
+  printf("TS PROBE %s (K-major %d, MN-major %d)\n", ok_km && ok_mn ? "OK" : "FAIL", ok_km, ok_mn);
+  return ok_km && ok_mn ? 0 : 1;
+}
