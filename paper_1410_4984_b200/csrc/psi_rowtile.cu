@@ -24,11 +24,13 @@
 // polynomial) stored back to TMEM as tf32 hi/lo, MMA3 with A = G read from TMEM, and the MMA3
 // accumulator drained into fp64 registers every chunk.  All GEMMs use 3xTF32 (hi*hi + hi*lo +
 // lo*hi), ~fp32 accuracy; every cross-chunk / cross-CTA sum is fp64 in a fixed order.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -44,39 +46,74 @@ using namespace dev;
 
 constexpr int kCH = 96;                 // streamed rows per chunk (MMA1 N, MMA3 K)
 constexpr int kGroups = 3;              // consumer warps per TMEM lane quarter (32 columns each)
-constexpr int kCons = 128 * kGroups;    // consumer threads
-constexpr int kThreads = kCons + 64;    // + loader warp + MMA warp
+constexpr int kCons = 128 * kGroups;    // consumer threads   (warps 0 .. 11)
+constexpr int kDrain = 128;             // accumulator drain threads (warps 12 .. 15)
+constexpr int kWarpLoad = (kCons + kDrain) / 32;  // loader warp (16)
+constexpr int kWarpMma = kWarpLoad + 1;           // MMA warp (17)
+constexpr int kThreads = kCons + kDrain + 64;
 constexpr int kPadRows = 384;           // feature-array row padding: lcm(kCH, 128)
-constexpr int kMaxRing = 4;
 constexpr float kNegHuge = -1.0e30f;    // B_n of padded datapoints: 2^(~-1e30) = 0
 
-template <int Q>
+// BF: G = 2^D stored as bf16x2 hi / lo in place of D (kind::f16 MMA3, ~2^-18 relative, up to
+// four D/G stages) or as tf32 hi / lo next to it (kind::tf32 MMA3, ~2^-22, two stages).  The
+// forward uses bf16; the backward uses tf32 because its per-datapoint sums feed differences
+// (mu^2 T0 - 2 mu T1 + T2, and the pair / datapoint parts of d l) that amplify relative error.
+template <int Q, bool BF>
 struct RT {
   static constexpr int K1 = (2 * Q + 2 + 7) / 8 * 8;  // MMA1 depth
   static constexpr int NH = 2 * Q + 1;                // MMA3 useful columns
   static constexpr int N3 = (NH + 15) / 16 * 16;      // MMA3 N
-  static constexpr int XF = kCH * K1;                 // floats of one streamed X part (hi or lo)
-  static constexpr int YF = N3 * kCH;                 // floats of one streamed Y part (hi or lo)
-  static constexpr int SF = 2 * XF + 2 * YF;          // floats per ring stage
+  static constexpr int XF = kCH * K1;                 // floats of one streamed X part (tf32 hi or lo)
+  static constexpr int YB = N3 * kCH;                 // elements of one Y^T part (hi or lo)
+  static constexpr int YFl = BF ? YB / 2 : YB;        // floats of one Y^T part
+  static constexpr int PF = 2 * XF + 2 * YFl;         // floats per processed stage
   static constexpr int AF = 128 * K1;                 // floats of one static part (hi or lo)
-  // MMA3 as G_hi * [Y_hi ; Y_lo] (N = 2 N3) + G_lo * Y_hi (N = N3) when both accumulator stages of
-  // 2 N3 columns fit next to the D / G stages; else three N3 passes.
-  static constexpr bool kConcat = 4 * kCH + 4 * N3 <= 512;
+  static constexpr int SW = BF ? kCH : 2 * kCH;       // TMEM columns per D/G stage
+  // MMA3 as G_hi * [Y_hi ; Y_lo] (N = 2 N3) + G_lo * Y_hi (N = N3) when the 2 N3-column
+  // accumulators fit next to the (at least 3, resp. 2) D/G stages; else three N3 passes.
+  static constexpr bool kConcat = (BF ? 3 : 2) * SW + 4 * N3 <= 512;
   static constexpr int AccW = kConcat ? 2 * N3 : N3;   // TMEM columns per accumulator stage
+  static constexpr int kS = BF ? ((512 - 2 * AccW) / SW >= 4 ? 4 : 3) : 2;  // D/G stages
 };
 
 __host__ __device__ constexpr int rt_k1(int q) { return (2 * q + 2 + 7) / 8 * 8; }
 __host__ __device__ constexpr int rt_n3(int q) { return (2 * q + 1 + 15) / 16 * 16; }
+__host__ __device__ constexpr int rt_pf(int q, bool bf) {
+  return 2 * kCH * rt_k1(q) + (bf ? 1 : 2) * rt_n3(q) * kCH;
+}
 inline int64_t pad_rows(int64_t r) { return (r + kPadRows - 1) / kPadRows * kPadRows; }
 
-size_t rt_fixed_smem(int q) { return size_t(4) * 2 * 2 * 128 * rt_k1(q) + 256; }
-size_t rt_stage_bytes(int q) { return size_t(4) * (2 * kCH * rt_k1(q) + 2 * rt_n3(q) * kCH); }
-int rt_ring(int q) {
-  const size_t cap = 227 * 1024, fixed = rt_fixed_smem(q), st = rt_stage_bytes(q);
-  if (fixed + 2 * st > cap) return 0;
-  return int(std::min<size_t>(kMaxRing, (cap - fixed) / st));
+// Shared-memory pipeline depths: static tile buffers (nA) and streamed operand stages (nP); the
+// deepest configuration that fits 227 KB.
+struct RtCfg {
+  int nA, nP;
+  size_t smem;
+};
+__host__ __device__ constexpr int rt_stages(int q, bool bf) {  // RT<Q, BF>::kS on the host
+  return bf ? ((512 - 2 * ((3 * kCH + 4 * rt_n3(q) <= 512) ? 2 * rt_n3(q) : rt_n3(q))) / kCH >= 4 ? 4 : 3) : 2;
 }
-size_t rt_smem(int q) { return rt_fixed_smem(q) + size_t(rt_ring(q)) * rt_stage_bytes(q); }
+RtCfg rt_cfg(int q, bool bf) {
+  // operand stages: MMA1 runs kS chunks ahead, so the TMA ring needs kS + 2 slots to keep two
+  // loads in flight; a single static-tile buffer if that is what makes room.
+  const size_t K1 = rt_k1(q);
+  const size_t a = 4 * 2 * 128 * K1, pst = 4 * size_t(rt_pf(q, bf));
+  const size_t bars = 512, cap = 227 * 1024;
+  const int ks = rt_stages(q, bf);
+  for (int slack = 2; slack >= 0; --slack)
+    for (int na = 2; na >= 1; --na) {
+      const int np = ks + slack;
+      const size_t sz = na * a + np * pst + bars;
+      if (np <= 8 && sz <= cap) return RtCfg{na, np, sz};
+    }
+  return RtCfg{0, 0, 0};
+}
+
+// bf16x2 (round to nearest): low half = a (even element), high half = b
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(b), "f"(a));
+  return d;
+}
 
 __device__ __forceinline__ void put_split(float* hi, float* lo, int off4, const float (&x)[4]) {
   float h[4], l[4];
@@ -93,11 +130,54 @@ __device__ __forceinline__ void put_split(float* hi, float* lo, int off4, const 
 // Feature builders (elementwise, HBM-bound)
 // ---------------------------------------------------------------------------------------------
 
-// Pair rows F_p (canonical K-major, all rows), p < p_pad; zero rows past P.
+__device__ __forceinline__ void put_rows(float* hi, float* lo, int64_t r, const float* f, int K1) {
+  float* hb = hi + (r >> 3) * (K1 * 8);
+  float* lb = lo + (r >> 3) * (K1 * 8);
+  const int rr = int(r & 7);
+  for (int k = 0; k < K1; k += 4) {
+    const float x[4] = {f[k], f[k + 1], f[k + 2], f[k + 3]};
+    put_split(hb, lb, (k >> 2) * 32 + rr * 4, x);
+  }
+}
+
+// One row of a processed-stage chunk [X hi | X lo | Y^T hi | Y^T lo] (layouts of the MMA1 / MMA3
+// B operands): X row jj (K1 features), Y column jj (N3 features, rows past NH zero).
+template <int Q, bool BF>
+__device__ __forceinline__ void put_pre_row(float* chunk, int jj, const float* x, const float* y) {
+  using C = RT<Q, BF>;
+  constexpr int K1 = C::K1, N3 = C::N3, XF = C::XF, YB = C::YB;
+#pragma unroll
+  for (int k = 0; k < K1; k += 4) {
+    const float x4[4] = {x[k], x[k + 1], x[k + 2], x[k + 3]};
+    put_split(chunk, chunk + XF, (jj >> 3) * (K1 * 8) + (k >> 2) * 32 + (jj & 7) * 4, x4);
+  }
+  if (BF) {  // Y^T as bf16 hi / lo, canonical K-major (rows = features, 8 bf16 per core-matrix row)
+    __nv_bfloat16* yh = reinterpret_cast<__nv_bfloat16*>(chunk + 2 * XF);
+#pragma unroll
+    for (int f = 0; f < N3; ++f) {
+      const int off = (f >> 3) * (kCH * 8) + (jj >> 3) * 64 + (f & 7) * 8 + (jj & 7);
+      const __nv_bfloat16 hi = __float2bfloat16_rn(y[f]);
+      yh[off] = hi;
+      yh[YB + off] = __float2bfloat16_rn(y[f] - __bfloat162float(hi));
+    }
+  } else {   // Y^T as tf32 hi / lo, canonical K-major (4 tf32 per core-matrix row)
+    float* yh = chunk + 2 * XF;
+#pragma unroll
+    for (int f = 0; f < N3; ++f) {
+      const int off = (f >> 3) * (kCH * 8) + (jj >> 2) * 32 + (f & 7) * 4 + (jj & 3);
+      const float hi = tc::tf32_hi(y[f]);
+      yh[off] = hi;
+      yh[YB + off] = y[f] - hi;
+    }
+  }
+}
+
+// Pair rows F_p, p < p_pad (zero rows past P): canonical K-major hi / lo (static operand of the
+// forward).
 template <int Q>
 __global__ void __launch_bounds__(256) rt_pair_rows_kernel(PsiConst P, int64_t p_pad, float* __restrict__ fh,
                                                             float* __restrict__ fl) {
-  constexpr int K1 = RT<Q>::K1;
+  constexpr int K1 = RT<Q, true>::K1;
   const int m = P.m, qv = P.qv;
   const int64_t npairs = int64_t(m) * (m + 1) / 2;
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < p_pad; p += int64_t(gridDim.x) * blockDim.x) {
@@ -125,24 +205,17 @@ __global__ void __launch_bounds__(256) rt_pair_rows_kernel(PsiConst P, int64_t p
       f[2 * Q] = -0.25f * kLog2e * c;
       f[2 * Q + 1] = 1.f;
     }
-    const int r = int(p & 7);
-    float* hb = fh + (p >> 3) * (K1 * 8);
-    float* lb = fl + (p >> 3) * (K1 * 8);
-#pragma unroll
-    for (int k = 0; k < K1; k += 4) {
-      const float x[4] = {f[k], f[k + 1], f[k + 2], f[k + 3]};
-      put_split(hb, lb, (k >> 2) * 32 + r * 4, x);
-    }
+    put_rows(fh, fl, p, f, K1);
   }
 }
 
-// Datapoint rows H_n (canonical K-major, all rows) and the chunked transposed gradient features
-// H'^T (per 96-row chunk: [hi | lo][N3 x 96], rows = features).  Padded rows: H = [0.., 0, -huge].
+// Datapoint rows H_n, n < n_pad (padded rows [0 .., 0, -huge]): canonical K-major hi / lo (static
+// operand of the backward) and, per 96-row chunk, the forward's streamed operands
+// X = H_n, Y = [1, d2 mu, d2] in the processed-stage layout.
 template <int Q>
 __global__ void __launch_bounds__(256) rt_data_rows_kernel(PsiConst P, int64_t n_pad, float* __restrict__ hh,
-                                                            float* __restrict__ hl, float* __restrict__ hp) {
-  using C = RT<Q>;
-  constexpr int K1 = C::K1, N3 = C::N3;
+                                                            float* __restrict__ hl, float* __restrict__ pre) {
+  constexpr int K1 = RT<Q, true>::K1;
   for (int64_t n = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; n < n_pad; n += int64_t(gridDim.x) * blockDim.x) {
     const bool valid = n < P.n;
     const int64_t nn = valid ? n : 0;
@@ -153,11 +226,12 @@ __global__ void __launch_bounds__(256) rt_data_rows_kernel(PsiConst P, int64_t n
       rm[q] = __ldg(P.mu + qq * P.ld_mu + nn);
       rs[q] = P.expected ? __ldg(P.s + qq * P.ld_s + nn) : 0.0;
     }
-    float h[K1], g[N3];
+    constexpr int N3 = RT<Q, true>::N3;
+    float h[K1], y[N3];
 #pragma unroll
     for (int k = 0; k < K1; ++k) h[k] = 0.f;
 #pragma unroll
-    for (int k = 0; k < N3; ++k) g[k] = 0.f;
+    for (int k = 0; k < N3; ++k) y[k] = 0.f;
     if (valid) {
       float bsum = 2.f * P.log2_var;
 #pragma unroll
@@ -171,48 +245,34 @@ __global__ void __launch_bounds__(256) rt_data_rows_kernel(PsiConst P, int64_t n
           h[q] = 2.f * kLog2e * d2 * mu;
           h[Q + q] = -kLog2e * d2;
           bsum = fmaf(-0.5f, log2f(t), fmaf(-kLog2e * d2 * mu, mu, bsum));
-          g[1 + q] = d2 * mu;
-          g[1 + Q + q] = d2;
+          y[1 + q] = d2 * mu;
+          y[1 + Q + q] = d2;
         }
       h[2 * Q] = 1.f;
       h[2 * Q + 1] = bsum;
-      g[0] = 1.f;
+      y[0] = 1.f;
     } else {
       h[2 * Q + 1] = kNegHuge;
     }
-    const int r = int(n & 7);
-    float* hb = hh + (n >> 3) * (K1 * 8);
-    float* lb = hl + (n >> 3) * (K1 * 8);
-#pragma unroll
-    for (int k = 0; k < K1; k += 4) {
-      const float x[4] = {h[k], h[k + 1], h[k + 2], h[k + 3]};
-      put_split(hb, lb, (k >> 2) * 32 + r * 4, x);
-    }
-    // H'^T chunk: element (feature f, column j) at canon(f, j, kCH)
-    float* ch = hp + (n / kCH) * (2 * N3 * kCH);
-    const int j = int(n % kCH);
-#pragma unroll
-    for (int f = 0; f < N3; ++f) {
-      const int off = (f >> 3) * (kCH * 8) + (j >> 2) * 32 + (f & 7) * 4 + (j & 3);
-      const float hi = tc::tf32_hi(g[f]);
-      ch[off] = hi;
-      ch[N3 * kCH + off] = g[f] - hi;
-    }
+    put_rows(hh, hl, n, h, K1);
+    put_pre_row<Q, true>(pre + (n / kCH) * RT<Q, true>::PF, int(n % kCH), h, y);
   }
 }
 
-// Backward streamed Y for pair chunks: F'^T (per 96-pair chunk [hi | lo][N3 x 96]),
-// F'_p = w_p [1, zb (Q), zb^2 (Q)], w_p = U_ab + U_ba (a < b) or U_aa.
+// Backward streamed operands, precomputed: X = F_p, Y = w_p [1, zb, zb^2].
 template <int Q>
-__global__ void __launch_bounds__(256) rt_pair_weights_kernel(PsiConst P, const float* __restrict__ u,
-                                                               int64_t p_pad, float* __restrict__ fp) {
-  constexpr int N3 = RT<Q>::N3;
+__global__ void __launch_bounds__(256) rt_pair_pre_kernel(PsiConst P, const float* __restrict__ u, int64_t p_pad,
+                                                           float* __restrict__ pre) {
+  using C = RT<Q, false>;
+  constexpr int K1 = C::K1, N3 = C::N3;
   const int m = P.m, qv = P.qv, mv = P.mv;
   const int64_t npairs = int64_t(m) * (m + 1) / 2;
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < p_pad; p += int64_t(gridDim.x) * blockDim.x) {
-    float g[N3];
+    float f[K1], y[N3];
 #pragma unroll
-    for (int k = 0; k < N3; ++k) g[k] = 0.f;
+    for (int k = 0; k < K1; ++k) f[k] = 0.f;
+#pragma unroll
+    for (int k = 0; k < N3; ++k) y[k] = 0.f;
     if (p < npairs) {
       int a = 0;
       int64_t rem = p;
@@ -222,84 +282,102 @@ __global__ void __launch_bounds__(256) rt_pair_weights_kernel(PsiConst P, const 
       }
       const int b = a + int(rem);
       const float w = a == b ? u[a * mv + a] : u[a * mv + b] + u[b * mv + a];
-      g[0] = w;
+      float c = 0.f;
 #pragma unroll
       for (int q = 0; q < Q; ++q)
         if (q < P.q) {
-          const float zbar = 0.5f * (P.zc[a * qv + q] + P.zc[b * qv + q]);
-          g[1 + q] = w * zbar;
-          g[1 + Q + q] = w * zbar * zbar;
+          const float za = P.zc[a * qv + q], zb = P.zc[b * qv + q];
+          const float zbar = 0.5f * (za + zb), dz = za - zb;
+          f[q] = zbar;
+          f[Q + q] = zbar * zbar;
+          c = fmaf(P.il2[q] * dz, dz, c);
+          y[1 + q] = w * zbar;
+          y[1 + Q + q] = w * zbar * zbar;
         }
+      f[2 * Q] = -0.25f * kLog2e * c;
+      f[2 * Q + 1] = 1.f;
+      y[0] = w;
     }
-    float* ch = fp + (p / kCH) * (2 * N3 * kCH);
-    const int j = int(p % kCH);
-#pragma unroll
-    for (int f = 0; f < N3; ++f) {
-      const int off = (f >> 3) * (kCH * 8) + (j >> 2) * 32 + (f & 7) * 4 + (j & 3);
-      const float hi = tc::tf32_hi(g[f]);
-      ch[off] = hi;
-      ch[N3 * kCH + off] = g[f] - hi;
-    }
+    put_pre_row<Q, false>(pre + (p / kCH) * C::PF, int(p % kCH), f, y);
   }
 }
 
 // ---------------------------------------------------------------------------------------------
 // The row-tile pipeline
 // ---------------------------------------------------------------------------------------------
+// (slot, phase) of a circular pipeline of n stages, advanced incrementally (no integer division
+// on the single-thread issue paths).
+struct RingPos {
+  int slot = 0, n = 1;
+  uint32_t phase = 0;
+  __device__ __forceinline__ void next() {
+    if (++slot == n) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+};
+__device__ __forceinline__ RingPos ring(int n) {
+  RingPos r;
+  r.n = n;
+  return r;
+}
+
 struct RowTileArgs {
-  const float* a_hi;  // static rows (canonical K-major arrays over all rows)
+  const float* a_hi;  // static rows: canonical K-major hi / lo arrays over all rows
   const float* a_lo;
-  const float* x_hi;  // streamed rows
-  const float* x_lo;
-  const float* y;     // streamed chunked Y^T ([chunk][hi|lo][N3 x kCH])
-  int ring;
+  const float* pre;   // streamed chunks in processed-stage layout [chunk][PF]
+  int nA, nP;         // pipeline depths (rt_cfg)
   int mode;           // 0 forward (pairs static, datapoints streamed), 1 backward
   // forward: tile = blockIdx.x, chunks [blockIdx.y * cps, min(+cps, nchunks)) of the datapoints
   // backward: tiles blockIdx.x + i * gridDim.x < ntiles, all nchunks pair chunks each
   int64_t ntiles, nchunks, cps;
   int64_t nrows_static;    // valid static rows (P or N)
   double* out;             // forward: pair_part [split][p][NH]; backward: T [n][NH]
-  int dbg;                 // SGPX_RT_DBG (timing experiments only): 1 skip G math, 2 skip MMA3, 4 skip MMA1
+  int dbg;  // SGPX_RT_DBG (timing experiments only): 1 skip G math, 2 skip MMA3, 4 skip MMA1
 };
 
-template <int Q>
-__global__ void __launch_bounds__(kThreads, 1)
-    rowtile_kernel(PsiConst P, BwdConst B, RowTileArgs R) {
-  using C = RT<Q>;
+template <int Q, bool BF>
+__global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTileArgs R) {
+  using C = RT<Q, BF>;
   constexpr int K1 = C::K1, KS1 = K1 / 8, N3 = C::N3, NH = C::NH;
-  constexpr int SF = C::SF, XF = C::XF, YF = C::YF, AF = C::AF;
-  constexpr uint32_t kStage = 2 * kCH;  // TMEM columns per D/G stage (hi in place of D, lo after)
-  constexpr uint32_t kAcc0 = 4 * kCH;   // two accumulator stages of AccW columns
+  constexpr int PF = C::PF, XF = C::XF, YB = C::YB, YFl = C::YFl, AF = C::AF;
+  constexpr int kS = C::kS;             // D/G stages of SW TMEM columns
+  constexpr int SW = C::SW;
+  constexpr uint32_t kAcc0 = kS * SW;   // two accumulator stages of AccW columns
   constexpr int AccW = C::AccW;
   constexpr bool kConcat = C::kConcat;
   extern __shared__ __align__(1024) float sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  float* Abuf = sm;                       // [2][hi|lo][AF]
-  float* Ring = Abuf + 4 * AF;            // [ring][SF]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Ring + R.ring * SF);
-  uint64_t* b_full = bar;                 // [kMaxRing] stage landed (tx)
-  uint64_t* b_empty = bar + 4;            // [kMaxRing] MMA1 + MMA3 done with the stage
-  uint64_t* a_full = bar + 8;             // [2] static tile landed (tx)
-  uint64_t* a_empty = bar + 10;           // [2] MMA1s of the tile done
-  uint64_t* d_full = bar + 12;            // [2] exponents ready
-  uint64_t* g_full = bar + 14;            // [2] G stored (consumers)
-  uint64_t* c_full = bar + 16;            // [2] MMA3 accumulator ready
-  uint64_t* c_empty = bar + 18;           // [2] accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 20);
+  const int nA = R.nA, nP = R.nP;
+  float* Abuf = sm;                       // [nA][hi|lo][AF]
+  float* Proc = Abuf + nA * 2 * AF;       // [nP][Xh | Xl | Yh | Yl]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Proc + nP * PF);
+  uint64_t* a_full = bar;                 // [2] static tile landed (tx)
+  uint64_t* a_empty = bar + 2;            // [2] MMA1s of the tile done
+  uint64_t* p_full = bar + 4;             // [8] streamed operands landed (tx)
+  uint64_t* p_empty = bar + 12;           // [8] MMA1 + MMA3 done with them
+  uint64_t* d_full = bar + 20;            // [kS] exponents ready
+  uint64_t* g_full = bar + 24;            // [kS] G stored (consumers)
+  uint64_t* c_full = bar + 28;            // [2] MMA3 accumulator ready
+  uint64_t* c_empty = bar + 30;           // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 32);
 
   if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
   if (tid == 0) {
-    for (int i = 0; i < kMaxRing; ++i) {
-      tc::mbar_init(&b_full[i], 1);
-      tc::mbar_init(&b_empty[i], 1);
-    }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&a_full[i], 1);
       tc::mbar_init(&a_empty[i], 1);
+      tc::mbar_init(&c_full[i], 1);
+      tc::mbar_init(&c_empty[i], kDrain);
+    }
+    for (int i = 0; i < 8; ++i) {
+      tc::mbar_init(&p_full[i], 1);
+      tc::mbar_init(&p_empty[i], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
       tc::mbar_init(&d_full[i], 1);
       tc::mbar_init(&g_full[i], kCons);
-      tc::mbar_init(&c_full[i], 1);
-      tc::mbar_init(&c_empty[i], kCons);
     }
     tc::mbar_fence_init();
   }
@@ -323,46 +401,48 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t total = my_tiles * cpt;
   auto tile_of = [&](int64_t i) -> int64_t { return R.mode == 0 ? int64_t(blockIdx.x) : blockIdx.x + i * gridDim.x; };
 
-  if (warp == kCons / 32) {
-    // ---------------- loader ----------------
+  if (warp == kWarpLoad) {
+    // ---------------- loader: static tiles + streamed operand chunks (1D TMA) ----------------
     if (lane == 0) {
+      RingPos ra = ring(nA), rp = ring(nP);
+      int64_t ti = 0, j = 0;
       for (int64_t c = 0; c < total; ++c) {
-        const int64_t ti = c / cpt, j = c - ti * cpt;
-        if (j == 0) {  // static tile of this row tile into A buffer ti & 1
-          const int ab = int(ti & 1);
-          if (ti >= 2) tc::mbar_wait(&a_empty[ab], uint32_t((ti >> 1) - 1) & 1);
+        if (j == 0) {
+          if (ti >= nA) tc::mbar_wait(&a_empty[ra.slot], ra.phase ^ 1u);
           const int64_t row0 = tile_of(ti) * 128;
-          tc::mbar_arrive_expect_tx(&a_full[ab], uint32_t(2 * AF * 4));
-          tc::bulk_g2s(Abuf + ab * 2 * AF, R.a_hi + row0 * K1, uint32_t(AF * 4), &a_full[ab]);
-          tc::bulk_g2s(Abuf + ab * 2 * AF + AF, R.a_lo + row0 * K1, uint32_t(AF * 4), &a_full[ab]);
+          float* dst = Abuf + ra.slot * 2 * AF;
+          tc::mbar_arrive_expect_tx(&a_full[ra.slot], uint32_t(2 * AF * 4));
+          tc::bulk_g2s(dst, R.a_hi + row0 * K1, uint32_t(AF * 4), &a_full[ra.slot]);
+          tc::bulk_g2s(dst + AF, R.a_lo + row0 * K1, uint32_t(AF * 4), &a_full[ra.slot]);
+          ra.next();
         }
-        const int slot = int(c % R.ring);
-        if (c >= R.ring) tc::mbar_wait(&b_empty[slot], uint32_t((c / R.ring) - 1) & 1);
-        const int64_t chunk = c_first + j;
-        const int64_t xr0 = chunk * kCH;
-        float* st = Ring + slot * SF;
-        tc::mbar_arrive_expect_tx(&b_full[slot], uint32_t(SF * 4));
-        tc::bulk_g2s(st, R.x_hi + xr0 * K1, uint32_t(XF * 4), &b_full[slot]);
-        tc::bulk_g2s(st + XF, R.x_lo + xr0 * K1, uint32_t(XF * 4), &b_full[slot]);
-        tc::bulk_g2s(st + 2 * XF, R.y + chunk * (2 * YF), uint32_t(2 * YF * 4), &b_full[slot]);
+        if (c >= nP) tc::mbar_wait(&p_empty[rp.slot], rp.phase ^ 1u);
+        tc::mbar_arrive_expect_tx(&p_full[rp.slot], uint32_t(PF * 4));
+        tc::bulk_g2s(Proc + rp.slot * PF, R.pre + (c_first + j) * PF, uint32_t(PF * 4), &p_full[rp.slot]);
+        rp.next();
+        if (++j == cpt) {
+          j = 0;
+          ++ti;
+        }
       }
     }
     __syncwarp();
-  } else if (warp == kCons / 32 + 1) {
+  } else if (warp == kWarpMma) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      const uint32_t id1 = tc::idesc_tf32(128, kCH), id3 = tc::idesc_tf32(128, N3);
-      auto mma1 = [&](int64_t c) {
-        const int64_t ti = c / cpt, j = c - ti * cpt;
-        const int ab = int(ti & 1), slot = int(c % R.ring);
-        if (j == 0) tc::mbar_wait(&a_full[ab], uint32_t(ti >> 1) & 1);
-        tc::mbar_wait(&b_full[slot], uint32_t(c / R.ring) & 1);
+      const uint32_t id1 = tc::idesc_tf32(128, kCH);
+      // MMA1 runs kS chunks ahead of MMA3 (one per D/G stage): separate positions for the two
+      RingPos a1 = ring(nA), p1 = ring(nP), s1 = ring(kS), p3 = ring(nP), s3 = ring(kS), c3 = ring(2);
+      int64_t j1 = 0;
+      auto mma1 = [&]() {
+        if (j1 == 0) tc::mbar_wait(&a_full[a1.slot], a1.phase);
+        tc::mbar_wait(&p_full[p1.slot], p1.phase);
         tc::fence_after();
-        const float* a = Abuf + ab * 2 * AF;
-        const float* x = Ring + slot * SF;
+        const float* a = Abuf + a1.slot * 2 * AF;
+        const float* x = Proc + p1.slot * PF;
         const uint64_t ah = tc::desc(tc::smem_u32(a), K1), al = tc::desc(tc::smem_u32(a + AF), K1);
         const uint64_t xh = tc::desc(tc::smem_u32(x), K1), xl = tc::desc(tc::smem_u32(x + XF), K1);
-        const uint32_t d = tmem + uint32_t(c & 1) * kStage;
+        const uint32_t d = tmem + uint32_t(s1.slot) * SW;
 #pragma unroll
         for (int t = 0; t < 3; ++t) {
           const uint64_t aa = t == 2 ? al : ah, bb = t == 1 ? xl : xh;
@@ -370,146 +450,190 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int ks = 0; ks < KS1; ++ks)
             if (!(R.dbg & 4)) tc::mma_ss(d, aa + 16 * ks, bb + 16 * ks, id1, (t | ks) ? 1u : 0u);
         }
-        tc::commit(&d_full[c & 1]);
-        if (j == cpt - 1) tc::commit(&a_empty[ab]);
+        tc::commit(&d_full[s1.slot]);
+        s1.next();
+        p1.next();
+        if (++j1 == cpt) {
+          tc::commit(&a_empty[a1.slot]);
+          a1.next();
+          j1 = 0;
+        }
       };
+      // bf16 G of stage s: consumer group g stored datapoints [32 g, 32 g + 32) as bf16x2 hi in
+      // columns [32 g, 32 g + 16) and lo in [32 g + 16, 32 g + 32); K-step k (16 datapoints) of hi
+      // is at column 32 (k / 2) + 8 (k % 2), lo 16 columns further.  tf32 G: hi in place of D,
+      // lo kCH columns further, K-step k (8 datapoints) at column 8 k.
       auto mma3 = [&](int64_t c) {
-        const int st = int(c & 1), slot = int(c % R.ring);
-        tc::mbar_wait(&g_full[st], uint32_t(c >> 1) & 1);
-        if (c >= 2) tc::mbar_wait(&c_empty[st], uint32_t((c >> 1) - 1) & 1);
+        tc::mbar_wait(&g_full[s3.slot], s3.phase);
+        if (c >= 2) tc::mbar_wait(&c_empty[c3.slot], c3.phase ^ 1u);
         tc::fence_after();
-        const float* y = Ring + slot * SF + 2 * XF;
-        const uint64_t yh = tc::desc(tc::smem_u32(y), kCH), yl = tc::desc(tc::smem_u32(y + YF), kCH);
-        const uint32_t gh = tmem + uint32_t(st) * kStage, gl = gh + kCH;
-        const uint32_t acc = tmem + kAcc0 + uint32_t(st) * AccW;
-        if (kConcat) {
-          const uint32_t id3c = tc::idesc_tf32(128, 2 * N3);
+        const float* y = Proc + p3.slot * PF + 2 * XF;
+        const uint32_t g0 = tmem + uint32_t(s3.slot) * SW;
+        const uint32_t acc = tmem + kAcc0 + uint32_t(c3.slot) * AccW;
+        if (!(R.dbg & 2)) {
+          if (BF) {
+            const uint32_t id3 = tc::idesc_bf16(128, N3), id3c = tc::idesc_bf16(128, 2 * N3);
+            const uint64_t yh = tc::desc_sbo(tc::smem_u32(y), kCH * 16);
+            const uint64_t yl = tc::desc_sbo(tc::smem_u32(y + YFl), kCH * 16);
 #pragma unroll
-          for (int ks = 0; ks < kCH / 8; ++ks)
-            if (!(R.dbg & 2)) tc::mma_ts(acc, gh + 8 * ks, yh + 16 * ks, id3c, ks ? 1u : 0u);
+            for (int k = 0; k < kCH / 16; ++k) {
+              const uint32_t gh = g0 + 32 * (k >> 1) + 8 * (k & 1), gl = gh + 16;
+              if (kConcat) {
+                tc::mma_ts_f16(acc, gh, yh + 16 * k, id3c, k ? 1u : 0u);
+                tc::mma_ts_f16(acc, gl, yh + 16 * k, id3, 1u);
+              } else {
+                tc::mma_ts_f16(acc, gh, yh + 16 * k, id3, k ? 1u : 0u);
+                tc::mma_ts_f16(acc, gh, yl + 16 * k, id3, 1u);
+                tc::mma_ts_f16(acc, gl, yh + 16 * k, id3, 1u);
+              }
+            }
+          } else {
+            const uint32_t id3 = tc::idesc_tf32(128, N3), id3c = tc::idesc_tf32(128, 2 * N3);
+            const uint64_t yh = tc::desc(tc::smem_u32(y), kCH), yl = tc::desc(tc::smem_u32(y + YFl), kCH);
+            const uint32_t gh = g0, gl = g0 + kCH;
+            if (kConcat) {
 #pragma unroll
-          for (int ks = 0; ks < kCH / 8; ++ks)
-            if (!(R.dbg & 2)) tc::mma_ts(acc, gl + 8 * ks, yh + 16 * ks, id3, 1u);
-        } else {
+              for (int k = 0; k < kCH / 8; ++k) tc::mma_ts(acc, gh + 8 * k, yh + 16 * k, id3c, k ? 1u : 0u);
 #pragma unroll
-          for (int t = 0; t < 3; ++t) {
-            const uint32_t ga = t == 2 ? gl : gh;
-            const uint64_t bb = t == 1 ? yl : yh;
+              for (int k = 0; k < kCH / 8; ++k) tc::mma_ts(acc, gl + 8 * k, yh + 16 * k, id3, 1u);
+            } else {
 #pragma unroll
-            for (int ks = 0; ks < kCH / 8; ++ks)
-              if (!(R.dbg & 2)) tc::mma_ts(acc, ga + 8 * ks, bb + 16 * ks, id3, (t | ks) ? 1u : 0u);
+              for (int t = 0; t < 3; ++t) {
+                const uint32_t ga = t == 2 ? gl : gh;
+                const uint64_t bb = t == 1 ? yl : yh;
+#pragma unroll
+                for (int k = 0; k < kCH / 8; ++k) tc::mma_ts(acc, ga + 8 * k, bb + 16 * k, id3, (t | k) ? 1u : 0u);
+              }
+            }
           }
         }
-        tc::commit(&c_full[st]);
-        tc::commit(&b_empty[slot]);
+        tc::commit(&c_full[c3.slot]);
+        tc::commit(&p_empty[p3.slot]);
+        s3.next();
+        p3.next();
+        c3.next();
       };
-      if (total > 0) mma1(0);
-      if (total > 1) mma1(1);
+      for (int64_t c = 0; c < total && c < kS; ++c) mma1();
       for (int64_t c = 0; c < total; ++c) {
         mma3(c);
-        if (c + 2 < total) mma1(c + 2);
+        if (c + kS < total) mma1();
       }
     }
     __syncwarp();
-  } else {
-    // ---------------- consumers: G = 2^D, stored back as tf32 hi / lo ----------------
-    const int g = warp >> 2, quarter = warp & 3, row = 32 * quarter + lane;
+  } else if (tid >= kCons) {
+    // ---------------- drain warps: MMA3 accumulator -> fp64 registers, tile epilogue ----------------
+    const int quarter = warp & 3, row = 32 * quarter + lane;
     const uint32_t lane_off = uint32_t(32 * quarter) << 16;
-    // group g drains accumulator columns [g * NHG, (g + 1) * NHG) of its row into fp64
-    constexpr int NHG = (NH + kGroups - 1) / kGroups;
-    double acc[NHG];
+    double acc[NH];
 #pragma unroll
-    for (int k = 0; k < NHG; ++k) acc[k] = 0.0;
-
-    auto drain_cols = [&](auto gconst, int64_t c) {
-      constexpr int G0 = decltype(gconst)::value * NHG;
-      const int st = int(c & 1);
-      const uint32_t a0 = tmem + kAcc0 + uint32_t(st) * AccW + lane_off;
+    for (int k = 0; k < NH; ++k) acc[k] = 0.0;
+    RingPos s = ring(2);
+    int64_t dj = 0, dti = 0;
+    for (int64_t c = 0; c < total; ++c) {
+      tc::mbar_wait(&c_full[s.slot], s.phase);
+      tc::fence_after();
+      const uint32_t a0 = tmem + kAcc0 + uint32_t(s.slot) * AccW + lane_off;
 #pragma unroll
-      for (int k0 = (G0 / 8) * 8; k0 < G0 + NHG && k0 < NH; k0 += 8) {
+      for (int k0 = 0; k0 < NH; k0 += 8) {
         uint32_t r[8], r2[8];
         tc::ld8(a0 + k0, r);
         if (kConcat) tc::ld8(a0 + N3 + k0, r2);
         tc::ld_wait();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const int k = k0 + kk;
-          if (k >= G0 && k < G0 + NHG && k < NH) {
+        for (int kk = 0; kk < 8; ++kk)
+          if (k0 + kk < NH) {
             float v = __uint_as_float(r[kk]);
             if (kConcat) v += __uint_as_float(r2[kk]);
-            acc[k - G0] += double(v);
+            acc[k0 + kk] += double(v);
           }
-        }
       }
-    };
-    auto flush_cols = [&](auto gconst, int64_t ti) {
-      constexpr int G0 = decltype(gconst)::value * NHG;
-      const int64_t row_g = tile_of(ti) * 128 + row;
-      if (row_g < R.nrows_static) {
-        double* o = R.mode == 0 ? R.out + (int64_t(blockIdx.y) * R.nrows_static + row_g) * NH : R.out + row_g * NH;
-#pragma unroll
-        for (int i = 0; i < NHG; ++i)
-          if (G0 + i < NH) o[G0 + i] = acc[i];
-      }
-#pragma unroll
-      for (int i = 0; i < NHG; ++i) acc[i] = 0.0;
-    };
-    auto drain = [&](int64_t c) {
-      const int st = int(c & 1);
-      tc::mbar_wait(&c_full[st], uint32_t(c >> 1) & 1);
-      tc::fence_after();
-      if (g == 0) drain_cols(std::integral_constant<int, 0>{}, c);
-      else if (g == 1) drain_cols(std::integral_constant<int, 1>{}, c);
-      else drain_cols(std::integral_constant<int, 2>{}, c);
       tc::fence_before();
-      tc::mbar_arrive(&c_empty[st]);
-      const int64_t ti = c / cpt, j = c - ti * cpt;
-      if (j != cpt - 1) return;
-      if (g == 0) flush_cols(std::integral_constant<int, 0>{}, ti);
-      else if (g == 1) flush_cols(std::integral_constant<int, 1>{}, ti);
-      else flush_cols(std::integral_constant<int, 2>{}, ti);
-    };
-
+      tc::mbar_arrive(&c_empty[s.slot]);
+      s.next();
+      if (++dj == cpt) {  // tile complete: write its rows
+        dj = 0;
+        const int64_t row_g = tile_of(dti) * 128 + row;
+        if (row_g < R.nrows_static) {
+          double* o = R.mode == 0 ? R.out + (int64_t(blockIdx.y) * R.nrows_static + row_g) * NH : R.out + row_g * NH;
+#pragma unroll
+          for (int k = 0; k < NH; ++k) o[k] = acc[k];
+        }
+#pragma unroll
+        for (int k = 0; k < NH; ++k) acc[k] = 0.0;
+        ++dti;
+      }
+    }
+    if (R.mode == 0 && total == 0) {  // empty datapoint split: zero partial sums
+      const int64_t row_g = int64_t(blockIdx.x) * 128 + row;
+      if (row_g < R.nrows_static)
+        for (int k = 0; k < NH; ++k) R.out[(int64_t(blockIdx.y) * R.nrows_static + row_g) * NH + k] = 0.0;
+    }
+  } else {
+    // ---------------- consumers: G = 2^D, stored back as hi / lo (bf16x2 in place, or tf32) ----------------
+    const int g = warp >> 2, quarter = warp & 3;
+    const uint32_t lane_off = uint32_t(32 * quarter) << 16;
+    RingPos sd = ring(kS);
     for (int64_t c = 0; c < total; ++c) {
-      const int st = int(c & 1);
-      tc::mbar_wait(&d_full[st], uint32_t(c >> 1) & 1);
+      tc::mbar_wait(&d_full[sd.slot], sd.phase);
       tc::fence_after();
-      const uint32_t dcol = tmem + uint32_t(st) * kStage + uint32_t(32 * g) + lane_off;
-#pragma unroll
-      for (int h16 = 0; h16 < 32; h16 += 16) {  // two halves of 16 columns (register pressure)
-        if (R.dbg & 1) break;
-        uint32_t r[16];
-        tc::ld16(dcol + h16, r);
+      const uint32_t dcol = tmem + uint32_t(sd.slot) * SW + uint32_t(32 * g) + lane_off;
+      if (!(R.dbg & 1)) {
+        uint32_t r0[16], r1[16];
+        tc::ld16(dcol, r0);
+        tc::ld16(dcol + 16, r1);
         tc::ld_wait();
-        uint32_t hi[16], lo[16];
-#pragma unroll
-        for (int i = 0; i < 16; i += 4) {
+        auto exps = [&](const uint32_t (&r)[16], int i, float (&v)[4]) {
           // 3 of 4 exponentials on MUFU.EX2, 1 of 4 on the FMA pipe
-          float v[4];
           v[0] = ex2(__uint_as_float(r[i]));
           v[1] = ex2(__uint_as_float(r[i + 1]));
           v[2] = ex2(__uint_as_float(r[i + 2]));
           v[3] = ex2_poly(__uint_as_float(r[i + 3]));
+        };
+        if (BF) {
+          uint32_t hi[16], lo[16];
+          auto half = [&](const uint32_t (&r)[16], int base) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float h = tc::tf32_hi(v[u]);
-            hi[i + u] = __float_as_uint(h);
-            lo[i + u] = __float_as_uint(v[u] - h);
-          }
+            for (int i = 0; i < 16; i += 4) {
+              float v[4];
+              exps(r, i, v);
+#pragma unroll
+              for (int u = 0; u < 4; u += 2) {
+                const uint32_t h = pack_bf16x2(v[u], v[u + 1]);
+                const float e0 = v[u] - __uint_as_float(h << 16), e1 = v[u + 1] - __uint_as_float(h & 0xFFFF0000u);
+                hi[base + (i + u) / 2] = h;
+                lo[base + (i + u) / 2] = pack_bf16x2(e0, e1);
+              }
+            }
+          };
+          half(r0, 0);
+          half(r1, 8);
+          tc::st16(dcol, hi);
+          tc::st16(dcol + 16, lo);
+        } else {
+          auto half = [&](const uint32_t (&r)[16], uint32_t col) {
+            uint32_t hi[16], lo[16];
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+              float v[4];
+              exps(r, i, v);
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const float h = tc::tf32_hi(v[u]);
+                hi[i + u] = __float_as_uint(h);
+                lo[i + u] = __float_as_uint(v[u] - h);
+              }
+            }
+            tc::st16(col, hi);
+            tc::st16(col + kCH, lo);
+          };
+          half(r0, dcol);
+          half(r1, dcol + 16);
         }
-        tc::st16(dcol + h16, hi);
-        tc::st16(dcol + kCH + h16, lo);
+        tc::st_wait();
       }
-      tc::st_wait();
       tc::fence_before();
-      tc::mbar_arrive(&g_full[st]);
-      if (c >= 1) drain(c - 1);
-    }
-    if (total >= 1) drain(total - 1);
-    if (R.mode == 0 && total == 0) {  // empty datapoint split: zero partial sums
-      const int64_t row_g = int64_t(blockIdx.x) * 128 + row;
-      if (g == 0 && row_g < R.nrows_static)
-        for (int k = 0; k < NH; ++k) R.out[(int64_t(blockIdx.y) * R.nrows_static + row_g) * NH + k] = 0.0;
+      tc::mbar_arrive(&g_full[sd.slot]);
+      sd.next();
     }
   }
   tc::fence_before();
@@ -662,15 +786,15 @@ struct FwdLayout {  // inside the forward partial buffer, after the psi1 rows (o
   int ns;
   int64_t nchunks;  // datapoint chunks
   int64_t npairs, p_pad, n_pad;
-  int64_t off_part, off_sums, off_floats;  // pair_part, pair_sums, then float arrays
-  int64_t f_fh, f_fl, f_hh, f_hl, f_hp, floats;  // float offsets relative to off_floats
-  int64_t doubles;                          // total doubles after the psi1 rows
+  int64_t off_part, off_sums, off_floats;           // pair_part, pair_sums, then float arrays
+  int64_t f_fh, f_fl, f_hh, f_hl, f_pre, floats;  // float offsets relative to off_floats
+  int64_t doubles;                                  // total doubles after the psi1 rows
 };
 
 FwdLayout fwd_layout(const PsiConst& P, int num_sms) {
   FwdLayout L{};
   const int q = instantiated_q(P.q);
-  const int K1 = rt_k1(q), N3 = rt_n3(q), NH = 2 * q + 1;
+  const int K1 = rt_k1(q), NH = 2 * q + 1;
   L.npairs = int64_t(P.m) * (P.m + 1) / 2;
   L.p_pad = pad_rows(L.npairs);
   L.n_pad = pad_rows(std::max<int64_t>(P.n, 1));
@@ -696,14 +820,14 @@ FwdLayout fwd_layout(const PsiConst& P, int num_sms) {
   L.f_fl = L.f_fh + L.p_pad * K1;
   L.f_hh = L.f_fl + L.p_pad * K1;
   L.f_hl = L.f_hh + L.n_pad * K1;
-  L.f_hp = L.f_hl + L.n_pad * K1;
-  L.floats = L.f_hp + (L.n_pad / kCH) * 2 * N3 * kCH;
+  L.f_pre = L.f_hl + L.n_pad * K1;
+  L.floats = L.f_pre + (L.n_pad / kCH) * rt_pf(q, true);
   L.doubles = L.off_floats + (L.floats + 1) / 2 + 2;
   return L;
 }
 
-float* floats_at(double* base, const FwdLayout& L) {
-  uintptr_t u = reinterpret_cast<uintptr_t>(base + L.off_floats - 2);
+float* floats_at(double* base, int64_t off_doubles) {
+  uintptr_t u = reinterpret_cast<uintptr_t>(base + off_doubles - 2);
   u = (u + 15) & ~uintptr_t(15);
   return reinterpret_cast<float*>(u);
 }
@@ -725,7 +849,8 @@ BwdLayout bwd_layout(const PsiConst& P, int num_sms) {
   L.off_t = 0;
   L.off_dl = L.off_t + std::max<int64_t>(P.n, 1) * (2 * q + 1);
   L.off_floats = (L.off_dl + int64_t(L.epi_blocks) * q + 1) / 2 * 2 + 2;
-  L.doubles = L.off_floats + (pad_rows(npairs) / kCH * 2 * rt_n3(q) * kCH + 1) / 2 + 2;
+  const int64_t pf = rt_pf(q, false);
+  L.doubles = L.off_floats + ((pad_rows(npairs) / kCH) * pf + 1) / 2 + 4;
   return L;
 }
 
@@ -737,40 +862,49 @@ int rt_dbg() {
   return v;
 }
 
+template <int Q, bool BF>
+int launch_rowtile(const PsiConst& P, RowTileArgs R, dim3 grid, cudaStream_t st) {
+  const RtCfg cfg = rt_cfg(Q, BF);
+  R.nA = cfg.nA;
+  R.nP = cfg.nP;
+  R.dbg = rt_dbg();
+  auto kern = rowtile_kernel<Q, BF>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cfg.smem)) != cudaSuccess) return 3;
+  kern<<<grid, kThreads, cfg.smem, st>>>(P, R);
+  g_tc_launches.fetch_add(1);
+  const cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "sgpx: rowtile launch (%u x %u, smem %zu): %s\n", grid.x, grid.y, cfg.smem, cudaGetErrorString(e));
+    return 3;
+  }
+  return 0;
+}
+
 template <int Q>
 int rt_forward_q(const PsiConst& P, double* base, double* packed, int num_sms, cudaStream_t st) {
-  using C = RT<Q>;
+  using C = RT<Q, true>;
   const FwdLayout L = fwd_layout(P, num_sms);
-  float* fl = floats_at(base, L);
-  float *fh = fl + L.f_fh, *flo = fl + L.f_fl, *hh = fl + L.f_hh, *hl = fl + L.f_hl, *hp = fl + L.f_hp;
+  float* fl = floats_at(base, L.off_floats);
   const int blocks_p = int(std::min<int64_t>((L.p_pad + 255) / 256, int64_t(num_sms) * 8));
-  rt_pair_rows_kernel<Q><<<blocks_p, 256, 0, st>>>(P, L.p_pad, fh, flo);
+  rt_pair_rows_kernel<Q><<<blocks_p, 256, 0, st>>>(P, L.p_pad, fl + L.f_fh, fl + L.f_fl);
   const int blocks_n = int(std::min<int64_t>((L.n_pad + 255) / 256, int64_t(num_sms) * 8));
-  rt_data_rows_kernel<Q><<<blocks_n, 256, 0, st>>>(P, L.n_pad, hh, hl, hp);
+  rt_data_rows_kernel<Q><<<blocks_n, 256, 0, st>>>(P, L.n_pad, fl + L.f_hh, fl + L.f_hl, fl + L.f_pre);
   g_tc_launches.fetch_add(2);
   RowTileArgs R{};
-  R.a_hi = fh;
-  R.a_lo = flo;
-  R.x_hi = hh;
-  R.x_lo = hl;
-  R.y = hp;
-  R.ring = rt_ring(Q);
+  R.a_hi = fl + L.f_fh;
+  R.a_lo = fl + L.f_fl;
+  R.pre = fl + L.f_pre;
   R.mode = 0;
-  R.dbg = rt_dbg();
   R.ntiles = (L.npairs + 127) / 128;
   R.nchunks = L.nchunks;
   R.cps = (L.nchunks + L.ns - 1) / L.ns;
   R.nrows_static = L.npairs;
   R.out = base + L.off_part;
-  const size_t smem = rt_smem(Q);
-  auto kern = rowtile_kernel<Q>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return 3;
-  BwdConst B{};
-  kern<<<dim3(unsigned(R.ntiles), unsigned(L.ns)), kThreads, smem, st>>>(P, B, R);
+  if (int rc = launch_rowtile<Q, true>(P, R, dim3(unsigned(R.ntiles), unsigned(L.ns)), st)) return rc;
   const int64_t tot = L.npairs * C::NH;
   rt_pair_reduce_kernel<<<int(std::min<int64_t>((tot + 255) / 256, 4096)), 256, 0, st>>>(
       base + L.off_part, L.ns, L.npairs, C::NH, base + L.off_sums, packed);
-  g_tc_launches.fetch_add(2);
+  g_tc_launches.fetch_add(1);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
@@ -779,32 +913,23 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
   const FwdLayout F = fwd_layout(P, num_sms);
   const BwdLayout L = bwd_layout(P, num_sms);
   double* fbase = const_cast<double*>(B.fwd_rt);
-  float* ff = floats_at(fbase, F);
-  uintptr_t u = reinterpret_cast<uintptr_t>(bbase + L.off_floats - 2);
-  float* fp = reinterpret_cast<float*>((u + 15) & ~uintptr_t(15));
+  float* ff = floats_at(fbase, F.off_floats);
+  float* pre = floats_at(bbase, L.off_floats);
   const int blocks_p = int(std::min<int64_t>((F.p_pad + 255) / 256, int64_t(num_sms) * 8));
-  rt_pair_weights_kernel<Q><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, fp);
+  rt_pair_pre_kernel<Q><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, pre);
   g_tc_launches.fetch_add(1);
   if (P.n > 0) {
     RowTileArgs R{};
     R.a_hi = ff + F.f_hh;
     R.a_lo = ff + F.f_hl;
-    R.x_hi = ff + F.f_fh;
-    R.x_lo = ff + F.f_fl;
-    R.y = fp;
-    R.ring = rt_ring(Q);
+    R.pre = pre;
     R.mode = 1;
-    R.dbg = rt_dbg();
     R.ntiles = L.ntiles;
     R.nchunks = L.pchunks;
     R.cps = L.pchunks;
     R.nrows_static = P.n;
     R.out = bbase + L.off_t;
-    const size_t smem = rt_smem(Q);
-    auto kern = rowtile_kernel<Q>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return 3;
-    kern<<<L.grid, kThreads, smem, st>>>(P, B, R);
-    g_tc_launches.fetch_add(1);
+    if (int rc = launch_rowtile<Q, false>(P, R, dim3(unsigned(L.grid)), st)) return rc;
   }
   rt_pair_grads_kernel<Q><<<std::max(1, (P.m * P.q + 255) / 256), 256, 0, st>>>(P, B.u, fbase + F.off_sums, prow);
   g_tc_launches.fetch_add(1);
@@ -835,7 +960,7 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
 
 bool rt_supported(const PsiConst& P) {
   const int q = instantiated_q(P.q);
-  return P.q >= 1 && q <= 16 && P.m >= 1 && rt_ring(q) >= 2;
+  return P.q >= 1 && q <= 16 && P.m >= 1 && rt_cfg(q, true).nP >= 2 && rt_cfg(q, false).nP >= 2;
 }
 int64_t rt_fwd_doubles(const PsiConst& P, int num_sms) { return fwd_layout(P, num_sms).doubles; }
 int64_t rt_bwd_doubles(const PsiConst& P, int num_sms) { return bwd_layout(P, num_sms).doubles; }
