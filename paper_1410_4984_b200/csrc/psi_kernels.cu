@@ -697,17 +697,19 @@ int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* pac
     if (int rc = plan_backward(P, num_sms, &g)) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t pstride = bwd_part_count(P.m, P.q);
-    const int c1 = P.n > 0 ? psi1_bwd_ctas(P, num_sms) : 0, rows = 8 * c1 + 1;
+    const int r1 = P.n > 0 ? psi1_bwd_rows(P, num_sms) : 0, rows = r1 + 1;
     if (cudaMemsetAsync(part, 0, sizeof(double) * pstride * rows, st) != cudaSuccess) return 3;
     if (ev_begin) cudaEventRecord(cudaEvent_t(ev_begin), st);
     // psi1 first: it writes d_mu / d_s (psi1 + KL parts); the psi2 kernel accumulates into them
-    if (c1 > 0) {
-      if (int rc = psi1_backward(P, B, part, pstride, c1, stream)) return rc;
+    if (r1 > 0) {
+      if (int rc = psi1_backward(P, B, part, pstride, r1, stream)) return rc;
     }
-    if (int rc = rt_backward(P, B, part + int64_t(rows) * pstride, part + int64_t(8 * c1) * pstride, num_sms, stream))
+    if (int rc = rt_backward(P, B, part + int64_t(rows) * pstride, part + int64_t(r1) * pstride, num_sms, stream))
       return rc;
     if (ev_end) cudaEventRecord(cudaEvent_t(ev_end), st);
-    if (int rc = bwd_reduce_rows(part, pstride, rows, packed, B.d_phi * double(P.n), stream)) return rc;
+    const int64_t rt_rows = (rt_bwd_doubles(P, num_sms) + pstride - 1) / pstride;
+    double* tmp = part + (int64_t(rows) + rt_rows) * pstride;
+    if (int rc = bwd_reduce_rows(part, pstride, rows, packed, B.d_phi * double(P.n), tmp, stream)) return rc;
     if (geom) *geom = g;
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
   }
@@ -737,9 +739,10 @@ int plan_forward(const PsiConst& P, int num_sms, LaunchGeom* geom) {
 int plan_backward(const PsiConst& P, int num_sms, LaunchGeom* geom) {
   if (use_rt(P)) {  // psi1 rows (8 per CTA) + 1 psi2 row + the row-tile scratch
     const int64_t pstride = bwd_part_count(P.m, P.q);
-    const int c1 = P.n > 0 ? psi1_bwd_ctas(P, num_sms) : 0;
-    const int64_t extra = (rt_bwd_doubles(P, num_sms) + pstride - 1) / pstride;
-    *geom = LaunchGeom{int(8 * c1 + 1 + extra), 448, 0};
+    const int r1 = P.n > 0 ? psi1_bwd_rows(P, num_sms) : 0;
+    const int64_t extra = (rt_bwd_doubles(P, num_sms) + pstride - 1) / pstride +
+                          (bwd_reduce_tmp_doubles(pstride) + pstride - 1) / pstride;
+    *geom = LaunchGeom{int(r1 + 1 + extra), 448, 0};
     return 0;
   }
   if (use_tc(P, true)) return plan_backward_tc(P, num_sms, geom);

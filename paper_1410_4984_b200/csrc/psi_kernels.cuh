@@ -94,7 +94,14 @@ int psi_backward_tc(const PsiConst& P, const BwdConst& B, double* part, double* 
 
 // Standalone psi1 passes (psi1_kernels.cu), paired with the TC psi2 kernels.
 int psi1_fwd_rows(const PsiConst& P, int num_sms);
-int psi1_bwd_ctas(const PsiConst& P, int num_sms);  // each CTA writes 8 per-warp partial rows
+int psi1_bwd_ctas(const PsiConst& P, int num_sms);  // legacy kernel: each CTA writes 8 per-warp rows
+int psi1_bwd_rows(const PsiConst& P, int num_sms);  // partial rows psi1_backward writes
+// Tiled psi1 (psi1_tile.cu, M <= 128): one partial row per CTA.
+bool psi1_tile_supported(const PsiConst& P, bool bwd);
+int psi1_tile_rows(const PsiConst& P, int num_sms);
+int psi1_tile_forward(const PsiConst& P, double* part, int64_t pstride, int rows, int* err_flag, int with_kl,
+                      void* stream);
+int psi1_tile_backward(const PsiConst& P, const BwdConst& B, double* part, int64_t pstride, int rows, void* stream);
 int psi1_forward(const PsiConst& P, double* part_rows, int64_t pstride, int rows, int* err_flag, void* stream,
                  int with_kl);
 // Row-tile tensor-core psi2 (psi_rowtile.cu).  rt_forward writes Phi into packed[4 + p] (run it
@@ -110,8 +117,11 @@ int rt_backward(const PsiConst& P, const BwdConst& B, double* bbase, double* pro
 // Where the forward placed the row-tile region inside its partial buffer (BwdConst::fwd_rt).
 const double* rt_fwd_region(const PsiConst& P, const double* fwd_part, int num_sms);
 // Fixed-order reduction of backward partial rows into packed grads (psi_tc.cu).
-int bwd_reduce_rows(const double* part, int64_t pstride, int rows, double* packed, double dvar_psi0, void* stream);
-int psi1_backward(const PsiConst& P, const BwdConst& B, double* part_rows, int64_t pstride, int ctas, void* stream);
+// tmp: bwd_reduce_tmp_doubles(pstride) doubles of scratch.
+int64_t bwd_reduce_tmp_doubles(int64_t pstride);
+int bwd_reduce_rows(const double* part, int64_t pstride, int rows, double* packed, double dvar_psi0, double* tmp,
+                    void* stream);
+int psi1_backward(const PsiConst& P, const BwdConst& B, double* part_rows, int64_t pstride, int rows, void* stream);
 
 // psi1_expected: out n x m col-major fp64 (ld_out).
 int psi1_matrix(const PsiConst& P, double* out, int64_t ld_out, void* stream);

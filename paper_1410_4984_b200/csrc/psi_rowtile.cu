@@ -659,68 +659,77 @@ __global__ void rt_pair_reduce_kernel(const double* __restrict__ part, int ns, i
 // Per-pair gradient terms (psi_stats.hpp:279-326 restated on the pair sums):
 //   dz_a += w_p [-(z_a - z_b)/(2 l^2) Phi_p + A_p - zb_p Bq_p]  (and the mirror for b)
 //   dl   += w_p Phi_p (z_a - z_b)^2 / l^3 / 2,   dvar += 2 w_p Phi_p / var
-// One thread per (a, q) walks its pairs in a fixed order; dl / dvar by one block.
-// Writes one backward partial row [dvar, dl (Q), dz (a + q M)].
+// rt_pair_dz_kernel: one thread per (a, q) walks its pairs in a fixed order.
+// rt_pair_dl_kernel: block k < Q sums dl_k, block Q sums dvar (fixed-order tree).
+// Together they write one backward partial row [dvar, dl (Q), dz (a + q M)].
+struct PairIdx {
+  int m;
+  __device__ int64_t start(int a) const { return int64_t(a) * m - int64_t(a) * (a - 1) / 2; }
+  __device__ int64_t of(int a, int b) const { return start(a) + (b - a); }  // a <= b
+  __device__ void inv(int64_t p, int& a, int& b) const {                     // m1-major upper triangle
+    const double t = 2.0 * m + 1.0;
+    int x = int((t - sqrt(t * t - 8.0 * double(p))) * 0.5);
+    x = x < 0 ? 0 : (x >= m ? m - 1 : x);
+    while (x + 1 < m && start(x + 1) <= p) ++x;
+    while (x > 0 && start(x) > p) --x;
+    a = x;
+    b = int(p - start(x)) + x;
+  }
+};
+
 template <int Q>
-__global__ void rt_pair_grads_kernel(PsiConst P, const float* __restrict__ u, const double* __restrict__ sums,
-                                     double* __restrict__ row) {
+__global__ void rt_pair_dz_kernel(PsiConst P, const float* __restrict__ u, const double* __restrict__ sums,
+                                  double* __restrict__ row) {
   constexpr int NH = 2 * Q + 1;
   const int m = P.m, mv = P.mv, q_n = P.q;
-  auto pidx = [&](int a, int b) -> int64_t {  // a <= b
-    return int64_t(a) * m - int64_t(a) * (a - 1) / 2 + (b - a);
-  };
-  auto zc = [&](int a, int q) -> double { return P.z64[q * m + a] - P.center[q]; };
-  auto wgt = [&](int a, int b) -> double {
-    return a == b ? double(u[a * mv + a]) : double(u[a * mv + b]) + double(u[b * mv + a]);
-  };
+  const PairIdx pi{m};
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m * q_n; i += gridDim.x * blockDim.x) {
     const int a = i % m, q = i / m;
     const double il2 = 1.0 / (P.ls[q] * P.ls[q]);
+    const double za = P.z64[q * m + a] - P.center[q];
     double s = 0.0;
     for (int b = 0; b < m; ++b) {
       const int lo = a < b ? a : b, hi = a < b ? b : a;
-      const double* r = sums + pidx(lo, hi) * NH;
-      const double zbar = 0.5 * (zc(lo, q) + zc(hi, q));
+      const double* r = sums + pi.of(lo, hi) * NH;
+      const double zb = P.z64[q * m + b] - P.center[q];
+      const double zbar = 0.5 * (za + zb);
       const double common = r[1 + q] - zbar * r[1 + Q + q];
-      const double t = -(zc(a, q) - zc(b, q)) * 0.5 * il2 * r[0] + common;
-      // the diagonal pair carries z_a in both slots
-      s += wgt(lo, hi) * (a == b ? 2.0 * t : t);
+      const double t = -(za - zb) * 0.5 * il2 * r[0] + common;
+      const double w = lo == hi ? double(u[a * mv + a]) : double(u[lo * mv + hi]) + double(u[hi * mv + lo]);
+      s += w * (a == b ? 2.0 * t : t);  // the diagonal pair carries z_a in both slots
     }
     row[1 + q_n + a + int64_t(q) * m] = s;
   }
-  if (blockIdx.x == 0) {
-    __shared__ double red[256];
-    for (int k = 0; k <= q_n; ++k) {  // k < q_n: dl_k, k == q_n: dvar
-      double s = 0.0;
-      for (int64_t p = threadIdx.x; p < int64_t(m) * (m + 1) / 2; p += blockDim.x) {
-        int a = 0;
-        int64_t rem = p;
-        while (rem >= m - a) {
-          rem -= m - a;
-          ++a;
-        }
-        const int b = a + int(rem);
-        const double ph = sums[p * NH] * wgt(a, b);
-        if (k < q_n) {
-          const double dz = zc(a, k) - zc(b, k), ls = P.ls[k];
-          s += ph * dz * dz / (2.0 * ls * ls * ls);
-        } else {
-          s += ph * 2.0 / P.variance_d;
-        }
-      }
-      red[threadIdx.x] = s;
-      __syncthreads();
-      for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-        __syncthreads();
-      }
-      if (threadIdx.x == 0) {
-        if (k < q_n) row[1 + k] = red[0];
-        else row[0] = red[0];
-      }
-      __syncthreads();
+}
+
+template <int Q>
+__global__ void __launch_bounds__(256) rt_pair_dl_kernel(PsiConst P, const float* __restrict__ u,
+                                                         const double* __restrict__ sums, double* __restrict__ row) {
+  constexpr int NH = 2 * Q + 1;
+  __shared__ double red[256];
+  const int m = P.m, mv = P.mv, k = blockIdx.x;
+  const PairIdx pi{m};
+  const int64_t npairs = int64_t(m) * (m + 1) / 2;
+  double s = 0.0;
+  for (int64_t p = threadIdx.x; p < npairs; p += blockDim.x) {
+    int a, b;
+    pi.inv(p, a, b);
+    const double w = a == b ? double(u[a * mv + a]) : double(u[a * mv + b]) + double(u[b * mv + a]);
+    const double ph = sums[p * NH] * w;
+    if (k < P.q) {
+      const double dz = P.z64[k * m + a] - P.z64[k * m + b], ls = P.ls[k];
+      s += ph * dz * dz / (2.0 * ls * ls * ls);
+    } else {
+      s += ph * 2.0 / P.variance_d;
     }
   }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) row[k < P.q ? 1 + k : 0] = red[0];
 }
 
 // Backward epilogue (psi_stats.hpp:279-326 restated on the per-datapoint sums T_n):
@@ -931,8 +940,9 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
     R.out = bbase + L.off_t;
     if (int rc = launch_rowtile<Q, false>(P, R, dim3(unsigned(L.grid)), st)) return rc;
   }
-  rt_pair_grads_kernel<Q><<<std::max(1, (P.m * P.q + 255) / 256), 256, 0, st>>>(P, B.u, fbase + F.off_sums, prow);
-  g_tc_launches.fetch_add(1);
+  rt_pair_dz_kernel<Q><<<std::max(1, (P.m * P.q + 127) / 128), 128, 0, st>>>(P, B.u, fbase + F.off_sums, prow);
+  rt_pair_dl_kernel<Q><<<P.q + 1, 256, 0, st>>>(P, B.u, fbase + F.off_sums, prow);
+  g_tc_launches.fetch_add(2);
   if (P.n > 0) {
     rt_bwd_epilogue_kernel<Q><<<L.epi_blocks, 256, 0, st>>>(P, B, bbase + L.off_t, bbase + L.off_dl);
     rt_dl_reduce_kernel<<<1, 32, 0, st>>>(bbase + L.off_dl, L.epi_blocks, Q, P.q, prow);

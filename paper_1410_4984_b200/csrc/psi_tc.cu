@@ -597,7 +597,7 @@ int plan_bwd_tc_q(const PsiConst& P, int num_sms, LaunchGeom* geom) {
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return 3;
   const int64_t nchunks = (P.n + 31) / 32;
   const int g2 = int(std::min<int64_t>(nchunks, num_sms));
-  *geom = LaunchGeom{g2 + 8 * psi1_bwd_ctas(P, num_sms), kThreadsTC, smem};
+  *geom = LaunchGeom{g2 + psi1_bwd_rows(P, num_sms), kThreadsTC, smem};
   return 0;
 }
 
@@ -636,12 +636,12 @@ int launch_bwd_tc_q(const PsiConst& P0, const BwdConst& B, double* part, double*
   if (int rc = plan_bwd_tc_q<Q>(P, num_sms, &g)) return rc;
   const int64_t nchunks = (P.n + 31) / 32;
   const int64_t pstride = bwd_part_count(P.m, P.q);
-  const int g2 = int(std::min<int64_t>(nchunks, num_sms)), c1 = (g.grid - g2) / 8;
+  const int g2 = int(std::min<int64_t>(nchunks, num_sms)), r1 = g.grid - g2;
   if (nchunks > 0) {
     if (cudaMemsetAsync(part, 0, sizeof(double) * pstride * g.grid, st) != cudaSuccess) return 3;
     if (e0) cudaEventRecord(e0, st);
     // psi1 first: it writes d_mu / d_s (psi1 + KL parts); the psi2 kernel accumulates into them
-    if (int rc = psi1_backward(P, B, part + int64_t(g2) * pstride, pstride, c1, st)) return rc;
+    if (int rc = psi1_backward(P, B, part + int64_t(g2) * pstride, pstride, r1, st)) return rc;
     psi_bwd_tc_kernel<Q><<<g2, g.threads, g.smem, st>>>(P, B, nchunks, part, pstride);
     g_tc_launches.fetch_add(1);
     if (e1) cudaEventRecord(e1, st);
@@ -658,10 +658,40 @@ int launch_bwd_tc_q(const PsiConst& P0, const BwdConst& B, double* part, double*
 
 bool tc_supported(const PsiConst& P) { return P.m >= 1 && P.m <= 128 && P.q >= 1 && P.q <= 32; }
 
-int bwd_reduce_rows(const double* part, int64_t pstride, int rows, double* packed, double dvar_psi0, void* stream) {
-  bwd_reduce_tc<<<int((pstride + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(part, pstride, rows,
-                                                                                          pstride, packed, dvar_psi0);
-  g_tc_launches.fetch_add(1);
+// Two-level fixed-order reduction of `rows` partial rows: row groups in parallel (level 1), then
+// the group sums in ascending order (level 2).  tmp: kReduceGroups * pstride doubles.
+namespace {
+constexpr int kReduceGroups = 64;
+__global__ void rows_partial_kernel(const double* __restrict__ part, int64_t pstride, int rows, int groups,
+                                    double* __restrict__ tmp) {
+  const int g = blockIdx.y;
+  const int r0 = int(int64_t(g) * rows / groups), r1 = int(int64_t(g + 1) * rows / groups);
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < pstride; k += int64_t(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int r = r0; r < r1; ++r) s += part[int64_t(r) * pstride + k];
+    tmp[int64_t(g) * pstride + k] = s;
+  }
+}
+__global__ void rows_final_bwd_kernel(const double* __restrict__ tmp, int groups, int64_t pstride,
+                                      double* __restrict__ packed, double dvar0) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < pstride; k += int64_t(gridDim.x) * blockDim.x) {
+    double s = k == 0 ? dvar0 : 0.0;
+    for (int g = 0; g < groups; ++g) s += tmp[int64_t(g) * pstride + k];
+    packed[k] = s;
+  }
+}
+}  // namespace
+
+int64_t bwd_reduce_tmp_doubles(int64_t pstride) { return int64_t(kReduceGroups) * pstride; }
+
+int bwd_reduce_rows(const double* part, int64_t pstride, int rows, double* packed, double dvar0, double* tmp,
+                    void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int groups = std::max(1, std::min(kReduceGroups, rows));
+  const int cb = int(std::min<int64_t>((pstride + 255) / 256, 64));
+  rows_partial_kernel<<<dim3(cb, groups), 256, 0, st>>>(part, pstride, rows, groups, tmp);
+  rows_final_bwd_kernel<<<cb, 256, 0, st>>>(tmp, groups, pstride, packed, dvar0);
+  g_tc_launches.fetch_add(2);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
