@@ -43,6 +43,16 @@ VARIANCE, LENGTHSCALE, BETA, S_INIT = 1.0, 1.0, 100.0, 0.5
 PEAK_FP32_TFLOPS = 71.7  # measured FFMA peak, profiles/r01_pipe_microbench.log (148 SMs @ 1965 MHz)
 
 
+def tensor_peak():
+    """Dense bf16 tensor peak from the driver-written MEASURED_PEAKS.json (sustained: the psi
+    kernels run inside a long step), else the profiling recipe's nominal 2250 TF/s."""
+    try:
+        pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(pk["bf16_tflops_sustained"]), "MEASURED_PEAKS.json bf16_tflops_sustained"
+    except Exception:
+        return 2250.0, "nominal dense bf16 (B200_PROFILING.md fallback)"
+
+
 def algorithmic_flops(q, d, m):
     """per datapoint and eval, FMA = 2 flops.
     psi2 fwd 4Q+3 / bwd 11Q+4 per (n, pair); psi1 fwd 4Q+2+2D / bwd 11Q+4+2D per (n, m)."""
@@ -275,6 +285,8 @@ def run_b200(args, world, rank, local_rank):
     fwd_s = float(np.mean(fwd_k))
     bwd_tf = n_local * bwd_flops / bwd_s / 1e12
     fwd_tf = n_local * fwd_flops / fwd_s / 1e12
+    psi_tf = n_local * (fwd_flops + bwd_flops) / (fwd_s + bwd_s) / 1e12
+    t_peak, t_src = tensor_peak()
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic_bwd.json")
     if os.path.exists(tpath):
@@ -326,19 +338,21 @@ def run_b200(args, world, rank, local_rank):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
-            "vs_baseline": None, "dtype": "f32 (fp64 accumulation + fp64 M-sized algebra)",
+            "vs_baseline": None, "dtype": "f32-equivalent: 3xTF32 / bf16x2-split tcgen05 MMAs, fp32 exp2, fp64 accumulation and M-sized algebra",
             "data": "synthetic (torch Philox seed 0: mu,Y ~ N(0,1), S=0.5, Z = M rows of mu; var=l=1, beta=100)",
             "config": {"workload": desc, "N": n_global, "Q": q, "D": d, "M": m, "n_local": n_local,
                        "parallelism": f"dp{world}", "l2": "inputs 560 MB > L2 and 256 MB L2 flush before each "
                                                          "timed step (untimed)"},
-            "roofline": {"bound": "fp32", "kernel": "psi_bwd_kernel", "achieved": bwd_tf,
-                         "peak": PEAK_FP32_TFLOPS, "unit": "TFLOP/s", "frac": bwd_tf / PEAK_FP32_TFLOPS,
-                         "traffic": traffic,
-                         "peak_source": "measured FFMA peak (profiles/r01_pipe_microbench.log); MEASURED_PEAKS.json "
-                                        "has no FP32 figure",
-                         "flops_per_launch": n_local * bwd_flops, "avg_launch_ms": bwd_s * 1e3,
-                         "fwd_kernel": {"achieved": fwd_tf, "avg_launch_ms": fwd_s * 1e3,
-                                        "flops_per_launch": n_local * fwd_flops}},
+            "roofline": {"bound": "tensor", "kernel": "psi passes (psi1 + psi2 forward and backward launch sequences)",
+                         "achieved": psi_tf, "peak": t_peak, "unit": "TFLOP/s", "frac": psi_tf / t_peak,
+                         "traffic": traffic, "peak_source": t_src,
+                         "flops_per_launch": n_local * (fwd_flops + bwd_flops), "avg_launch_ms": (fwd_s + bwd_s) * 1e3,
+                         "work": "SURVEY.md 8(d) algorithmic FP32-class flops P(15Q+7)+M(15Q+4D+6) per datapoint "
+                                 "(FMA = 2), executed as 3xTF32 / bf16x2 tcgen05 MMAs + MUFU/FMA exp2",
+                         "fp32_simt": {"peak": PEAK_FP32_TFLOPS, "frac": psi_tf / PEAK_FP32_TFLOPS,
+                                       "note": "SURVEY 8(d) FP32-FMA roofline; > 1 means beyond a SIMT design"},
+                         "fwd": {"achieved": fwd_tf, "avg_launch_ms": fwd_s * 1e3, "flops_per_launch": n_local * fwd_flops},
+                         "bwd": {"achieved": bwd_tf, "avg_launch_ms": bwd_s * 1e3, "flops_per_launch": n_local * bwd_flops}},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_all, "d2h_bytes_per_step": d2h_all,
                     "ms_per_step": e2e_s / args.steps * 1e3},
             "cpu_baseline": cpu,
