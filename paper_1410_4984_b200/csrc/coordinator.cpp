@@ -64,52 +64,78 @@ void chol_solve(const Mat& L, Mat& B) {
   }
 }
 
-Mat gemm(const Mat& A, bool ta, const Mat& B, bool tb) {
-  const int64_t m = ta ? A.c : A.r, k = ta ? A.r : A.c, n = tb ? B.r : B.c;
-  Mat C(m, n);
-  if (!ta) {
-    // C[:, j..j+3] += A[:, p] * B(p, j..j+3): each A column is streamed once per 4 output columns.
-    int64_t j = 0;
-    for (; j + 4 <= n; j += 4) {
-      double* __restrict__ c0 = C.col(j);
-      double* __restrict__ c1 = C.col(j + 1);
-      double* __restrict__ c2 = C.col(j + 2);
-      double* __restrict__ c3 = C.col(j + 3);
+static Mat transpose(const Mat& a) {
+  Mat t(a.c, a.r);
+  for (int64_t j = 0; j < a.c; ++j)
+    for (int64_t i = 0; i < a.r; ++i) t(j, i) = a(i, j);
+  return t;
+}
+
+// C = A B (column-major), 8 x 4 register blocks of C (GCC vector types, AVX2 with
+// -march=x86-64-v3) accumulated over p in ascending order: each element's summation order is
+// fixed, so results are bitwise reproducible.
+typedef double v4d __attribute__((vector_size(32)));
+static inline v4d load4(const double* p) {
+  v4d v;
+  __builtin_memcpy(&v, p, sizeof(v));
+  return v;
+}
+static inline void store4(double* p, v4d v) { __builtin_memcpy(p, &v, sizeof(v)); }
+
+static void gemm_nn(const Mat& A, const Mat& B, Mat& C) {
+  const int64_t m = A.r, k = A.c, n = B.c;
+  const double* __restrict__ a = A.v.data();
+  const double* __restrict__ b = B.v.data();
+  double* __restrict__ c = C.v.data();
+  int64_t j0 = 0;
+  for (; j0 + 4 <= n; j0 += 4) {
+    int64_t i0 = 0;
+    for (; i0 + 8 <= m; i0 += 8) {
+      v4d c00 = {0, 0, 0, 0}, c01 = c00, c10 = c00, c11 = c00, c20 = c00, c21 = c00, c30 = c00, c31 = c00;
+      const double* b0 = b + j0 * k;
       for (int64_t p = 0; p < k; ++p) {
-        const double b0 = tb ? B(j, p) : B(p, j), b1 = tb ? B(j + 1, p) : B(p, j + 1);
-        const double b2 = tb ? B(j + 2, p) : B(p, j + 2), b3 = tb ? B(j + 3, p) : B(p, j + 3);
-        const double* __restrict__ ap = A.col(p);
-        for (int64_t i = 0; i < m; ++i) {
-          const double a = ap[i];
-          c0[i] += a * b0;
-          c1[i] += a * b1;
-          c2[i] += a * b2;
-          c3[i] += a * b3;
-        }
+        const v4d a0 = load4(a + p * m + i0), a1 = load4(a + p * m + i0 + 4);
+        const double s0 = b0[p], s1 = b0[k + p], s2 = b0[2 * k + p], s3 = b0[3 * k + p];
+        c00 += a0 * s0;
+        c01 += a1 * s0;
+        c10 += a0 * s1;
+        c11 += a1 * s1;
+        c20 += a0 * s2;
+        c21 += a1 * s2;
+        c30 += a0 * s3;
+        c31 += a1 * s3;
       }
+      store4(c + j0 * m + i0, c00);
+      store4(c + j0 * m + i0 + 4, c01);
+      store4(c + (j0 + 1) * m + i0, c10);
+      store4(c + (j0 + 1) * m + i0 + 4, c11);
+      store4(c + (j0 + 2) * m + i0, c20);
+      store4(c + (j0 + 2) * m + i0 + 4, c21);
+      store4(c + (j0 + 3) * m + i0, c30);
+      store4(c + (j0 + 3) * m + i0 + 4, c31);
     }
-    for (; j < n; ++j) {
-      double* cj = C.col(j);
-      for (int64_t p = 0; p < k; ++p) {
-        const double b = tb ? B(j, p) : B(p, j);
-        const double* ap = A.col(p);
-        for (int64_t i = 0; i < m; ++i) cj[i] += ap[i] * b;
-      }
+    for (; i0 < m; ++i0) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int64_t p = 0; p < k; ++p)
+        for (int jj = 0; jj < 4; ++jj) acc[jj] += a[p * m + i0] * b[(j0 + jj) * k + p];
+      for (int jj = 0; jj < 4; ++jj) c[(j0 + jj) * m + i0] = acc[jj];
     }
-  } else {
-    for (int64_t j = 0; j < n; ++j)
-      for (int64_t i = 0; i < m; ++i) {
-        const double* ai = A.col(i);
-        double s = 0.0;
-        if (!tb) {
-          const double* bj = B.col(j);
-          for (int64_t p = 0; p < k; ++p) s += ai[p] * bj[p];
-        } else {
-          for (int64_t p = 0; p < k; ++p) s += ai[p] * B(j, p);
-        }
-        C(i, j) = s;
-      }
   }
+  for (; j0 < n; ++j0)
+    for (int64_t i = 0; i < m; ++i) {
+      double acc = 0.0;
+      for (int64_t p = 0; p < k; ++p) acc += a[p * m + i] * b[j0 * k + p];
+      c[j0 * m + i] = acc;
+    }
+}
+
+Mat gemm(const Mat& A, bool ta, const Mat& B, bool tb) {
+  const int64_t m = ta ? A.c : A.r, n = tb ? B.r : B.c;
+  Mat C(m, n);
+  if (ta && tb) gemm_nn(transpose(A), transpose(B), C);
+  else if (ta) gemm_nn(transpose(A), B, C);
+  else if (tb) gemm_nn(A, transpose(B), C);
+  else gemm_nn(A, B, C);
   return C;
 }
 
