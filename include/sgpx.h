@@ -215,6 +215,11 @@ int sgpx_engine_grad_pass(sgpx_engine* eng, double** packed_dev, int64_t* count)
 int sgpx_engine_finish(sgpx_engine* eng, sgpx_eval_result* out);
 /* Local per-datapoint gradients (KL included), device, n_local x Q col-major (ld = n_local). */
 int sgpx_engine_local_grads_device(sgpx_engine* eng, double** d_mu, double** d_s);
+/* Register host buffers (n_local x Q, column-major with ld; pinned for overlap) that every
+ * subsequent evaluate(with_grads) fills with d_mu / d_S -- streamed per sub-shard on a copy
+ * stream while the remaining sub-shards compute (the reference's Engine returns local grads
+ * in its result, parallel.hpp:424-429).  Null data pointers unregister. */
+int sgpx_engine_set_local_grads_out(sgpx_engine* eng, sgpx_mmat d_mu, sgpx_mmat d_s);
 int sgpx_engine_copy_local_grads(sgpx_engine* eng, sgpx_mmat d_mu, sgpx_mmat d_s);
 
 #ifdef __cplusplus

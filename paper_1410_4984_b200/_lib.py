@@ -96,6 +96,7 @@ SIGNATURES = {
     "sgpx_engine_finish": (C.c_int, [C.c_void_p, C.POINTER(eval_result)]),
     "sgpx_engine_local_grads_device": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "sgpx_engine_copy_local_grads": (C.c_int, [C.c_void_p, mmat, mmat]),
+    "sgpx_engine_set_local_grads_out": (C.c_int, [C.c_void_p, mmat, mmat]),
 }
 
 _lib = None

@@ -50,6 +50,7 @@ struct BwdConst {
   double* d_s;
   int64_t ld_g;
   const double* fwd_rt;  // row-tile path: the forward's feature / pair-sum region (rt_fwd_region)
+  int skip_pair_terms;   // sub-shard passes: the per-pair gradient terms are added by one call only
 };
 
 // Packed per-CTA partial layouts (fp64, CTA-private rows, single-writer per slot):
@@ -116,6 +117,9 @@ int rt_forward(const PsiConst& P, double* base, double* packed, int num_sms, voi
 int rt_backward(const PsiConst& P, const BwdConst& B, double* bbase, double* prow, int num_sms, void* stream);
 // Where the forward placed the row-tile region inside its partial buffer (BwdConst::fwd_rt).
 const double* rt_fwd_region(const PsiConst& P, const double* fwd_part, int num_sms);
+// The forward's reduced per-pair sums inside that region (npairs x (2Q+1) doubles): sub-shard
+// forwards add theirs into the first sub-shard's before the gradient pass.
+double* rt_fwd_pair_sums(const PsiConst& P, double* region, int num_sms, int64_t* count);
 // Fixed-order reduction of backward partial rows into packed grads (psi_tc.cu).
 // tmp: bwd_reduce_tmp_doubles(pstride) doubles of scratch.
 int64_t bwd_reduce_tmp_doubles(int64_t pstride);

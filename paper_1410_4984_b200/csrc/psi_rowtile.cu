@@ -940,9 +940,11 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
     R.out = bbase + L.off_t;
     if (int rc = launch_rowtile<Q, false>(P, R, dim3(unsigned(L.grid)), st)) return rc;
   }
-  rt_pair_dz_kernel<Q><<<std::max(1, (P.m * P.q + 127) / 128), 128, 0, st>>>(P, B.u, fbase + F.off_sums, prow);
-  rt_pair_dl_kernel<Q><<<P.q + 1, 256, 0, st>>>(P, B.u, fbase + F.off_sums, prow);
-  g_tc_launches.fetch_add(2);
+  if (!B.skip_pair_terms) {
+    rt_pair_dz_kernel<Q><<<std::max(1, (P.m * P.q + 127) / 128), 128, 0, st>>>(P, B.u, fbase + F.off_sums, prow);
+    rt_pair_dl_kernel<Q><<<P.q + 1, 256, 0, st>>>(P, B.u, fbase + F.off_sums, prow);
+    g_tc_launches.fetch_add(2);
+  }
   if (P.n > 0) {
     rt_bwd_epilogue_kernel<Q><<<L.epi_blocks, 256, 0, st>>>(P, B, bbase + L.off_t, bbase + L.off_dl);
     rt_dl_reduce_kernel<<<1, 32, 0, st>>>(bbase + L.off_dl, L.epi_blocks, Q, P.q, prow);
@@ -973,6 +975,11 @@ bool rt_supported(const PsiConst& P) {
   return P.q >= 1 && q <= 16 && P.m >= 1 && rt_cfg(q, true).nP >= 2 && rt_cfg(q, false).nP >= 2;
 }
 int64_t rt_fwd_doubles(const PsiConst& P, int num_sms) { return fwd_layout(P, num_sms).doubles; }
+double* rt_fwd_pair_sums(const PsiConst& P, double* region, int num_sms, int64_t* count) {
+  const FwdLayout L = fwd_layout(P, num_sms);
+  *count = L.npairs * (2 * instantiated_q(P.q) + 1);
+  return region + L.off_sums;
+}
 int64_t rt_bwd_doubles(const PsiConst& P, int num_sms) { return bwd_layout(P, num_sms).doubles; }
 
 int rt_forward(const PsiConst& P, double* base, double* packed, int num_sms, void* stream) {

@@ -287,14 +287,74 @@ struct sgpx_engine {
   cudaEvent_t ev[8] = {};  // 0-1 stats pass, 2-3 grad pass, 4-5 fwd kernel, 6-7 bwd kernel
   double coord_s = 0.0;
   LaunchGeom gf{}, gb{};
+  // Sub-shard pipeline: the shard's rows are processed as K contiguous sub-shards so that the
+  // host<->device traffic of one (mu, S in; d mu, d S out) overlaps the kernels of another.
+  struct Sub {
+    int64_t n0 = 0, n = 0;
+    PsiConst P{};
+    int64_t foff = 0, boff = 0;  // doubles into fpart / bpart
+  };
+  std::vector<Sub> subs;
+  DevBuf pstats_sub, pgrads_sub;
+  cudaStream_t copy = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_out;
+  // deferred upload of host mu / S (broadcast with host views), streamed by the stats pass
+  bool pending_upload = false;
+  sgpx_cmat h_mu{}, h_s{};
+  // registered host outputs for d mu / d S, streamed by the gradient pass
+  bool has_gout = false;
+  sgpx_mmat g_mu{}, g_s{};
   ~sgpx_engine() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto e : ev_in) cudaEventDestroy(e);
+    for (auto e : ev_out) cudaEventDestroy(e);
+    if (copy) cudaStreamDestroy(copy);
   }
 };
 
 namespace sgpx {
 namespace {
+
+__global__ void sum_parts_kernel(const double* __restrict__ parts, int k, int64_t count, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < k; ++j) s += parts[int64_t(j) * count + i];
+    out[i] = s;
+  }
+}
+
+// Sub-shard plan: one piece when the shard is device resident (nothing to overlap; every split
+// costs kernel efficiency), else up to 4 pieces (>= 250k rows each) so the host transfers of one
+// overlap the kernels of the others; boundaries on multiples of 384 rows (feature tile grain).
+void plan_subs(sgpx_engine* e) {
+  const int64_t n = e->in.n;
+  const bool transfers = e->pending_upload || (e->has_gout && e->latent);
+  const int k = !transfers ? 1 : (n >= 1000000 ? 4 : (n >= 500000 ? 2 : 1));
+  e->subs.clear();
+  const int64_t step = (n / k + 383) / 384 * 384;
+  for (int64_t n0 = 0; n0 < n || (n == 0 && e->subs.empty()); n0 += step) {
+    sgpx_engine::Sub sub;
+    sub.n0 = n0;
+    sub.n = std::min(step, n - n0);
+    sub.P = e->P;
+    sub.P.n = sub.n;
+    sub.P.mu = e->P.mu + n0;
+    sub.P.s = e->P.s ? e->P.s + n0 : nullptr;
+    sub.P.y = e->P.y + n0;
+    e->subs.push_back(sub);
+    if (n == 0) break;
+  }
+  const size_t need = e->subs.size();
+  while (e->ev_in.size() < need) {
+    cudaEvent_t a, b;
+    CUDA_OK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    e->ev_in.push_back(a);
+    e->ev_out.push_back(b);
+  }
+  if (!e->copy) CUDA_OK(cudaStreamCreateWithFlags(&e->copy, cudaStreamNonBlocking));
+}
 
 void engine_stats_pass(sgpx_engine* e) {
   require(e->has_data && e->has_params, "engine: set_data and broadcast must precede evaluate");
@@ -303,20 +363,55 @@ void engine_stats_pass(sgpx_engine* e) {
   e->pstats.ensure(sizeof(double) * count);
   e->err.ensure(sizeof(int));
   CUDA_OK(cudaMemsetAsync(e->err.p, 0, sizeof(int), ctx->stream));
-  LaunchGeom g{};
-  if (e->in.n > 0) {
-    if (plan_forward(e->P, ctx->num_sms, &g)) throw CudaError("psi forward: launch planning failed");
-    e->fpart.ensure(sizeof(double) * fwd_part_count(e->P.m, e->P.d) * std::max(1, g.grid));
-    CUDA_OK(cudaEventRecord(e->ev[0], ctx->stream));
-    if (psi_forward(e->P, e->fpart.get<double>(), e->pstats.get<double>(), e->err.get<int>(), ctx->num_sms,
-                    ctx->stream, &e->gf, e->ev[4], e->ev[5]))
-      throw CudaError(std::string("psi forward launch: ") + cudaGetErrorString(cudaGetLastError()));
-    CUDA_OK(cudaEventRecord(e->ev[1], ctx->stream));
-  } else {
+  if (e->in.n == 0) {
     CUDA_OK(cudaMemsetAsync(e->pstats.p, 0, sizeof(double) * count, ctx->stream));
     CUDA_OK(cudaEventRecord(e->ev[0], ctx->stream));
     CUDA_OK(cudaEventRecord(e->ev[1], ctx->stream));
+    e->coordinated = false;
+    return;
   }
+  plan_subs(e);
+  const int k = int(e->subs.size());
+  // partial-buffer layout: one region per sub-shard
+  int64_t foff = 0;
+  for (auto& sub : e->subs) {
+    LaunchGeom g{};
+    if (plan_forward(sub.P, ctx->num_sms, &g)) throw CudaError("psi forward: launch planning failed");
+    sub.foff = foff;
+    foff += fwd_part_count(sub.P.m, sub.P.d) * std::max(1, g.grid);
+  }
+  e->fpart.ensure(sizeof(double) * foff);
+  if (k > 1) e->pstats_sub.ensure(sizeof(double) * count * k);
+  CUDA_OK(cudaEventRecord(e->ev[0], ctx->stream));
+  if (e->pending_upload) {  // copy stream: mu / S of sub-shard j, then the forward of j waits for it
+    CUDA_OK(cudaEventRecord(e->ev_out[0], ctx->stream));  // previous users of the device rows are done
+    CUDA_OK(cudaStreamWaitEvent(e->copy, e->ev_out[0], 0));
+    for (int j = 0; j < k; ++j) {
+      const auto& sub = e->subs[j];
+      const int64_t q = e->cfg.q, n = e->cfg.n_local;
+      const int64_t ldm = e->h_mu.ld ? e->h_mu.ld : n, lds = e->h_s.ld ? e->h_s.ld : n;
+      CUDA_OK(cudaMemcpy2DAsync(e->own_x.get<double>() + sub.n0, sizeof(double) * n, e->h_mu.data + sub.n0,
+                                  sizeof(double) * ldm, sizeof(double) * sub.n, q, cudaMemcpyHostToDevice, e->copy));
+      CUDA_OK(cudaMemcpy2DAsync(e->own_s.get<double>() + sub.n0, sizeof(double) * n, e->h_s.data + sub.n0,
+                                  sizeof(double) * lds, sizeof(double) * sub.n, q, cudaMemcpyHostToDevice, e->copy));
+      CUDA_OK(cudaEventRecord(e->ev_in[j], e->copy));
+    }
+  }
+  for (int j = 0; j < k; ++j) {
+    auto& sub = e->subs[j];
+    if (e->pending_upload) CUDA_OK(cudaStreamWaitEvent(ctx->stream, e->ev_in[j], 0));
+    double* out = k > 1 ? e->pstats_sub.get<double>() + int64_t(j) * count : e->pstats.get<double>();
+    if (psi_forward(sub.P, e->fpart.get<double>() + sub.foff, out, e->err.get<int>(), ctx->num_sms, ctx->stream,
+                    &e->gf, j == 0 ? e->ev[4] : nullptr, j == k - 1 ? e->ev[5] : nullptr))
+      throw CudaError(std::string("psi forward launch: ") + cudaGetErrorString(cudaGetLastError()));
+  }
+  if (k > 1) {
+    sum_parts_kernel<<<int(std::min<int64_t>((count + 255) / 256, 1024)), 256, 0, ctx->stream>>>(
+        e->pstats_sub.get<double>(), k, count, e->pstats.get<double>());
+    CUDA_OK(cudaGetLastError());
+  }
+  e->pending_upload = false;
+  CUDA_OK(cudaEventRecord(e->ev[1], ctx->stream));
   e->coordinated = false;
 }
 
@@ -357,22 +452,49 @@ void engine_grad_pass(sgpx_engine* e) {
   e->ds.ensure(sizeof(double) * std::max<int64_t>(1, e->in.n * e->cfg.q));
   CUDA_OK(cudaEventRecord(e->ev[2], ctx->stream));
   if (e->in.n > 0) {
-    BwdConst B{};
-    B.u = e->u.get<float>();
-    B.dpsi = e->dpsi.get<float>();
-    B.d_phi = e->res.adj.d_phi;
-    B.add_kl = e->latent ? 1 : 0;
-    B.write_local = e->latent ? 1 : 0;
-    B.d_mu = e->dmu.get<double>();
-    B.d_s = e->ds.get<double>();
-    B.ld_g = e->in.n;
-    B.fwd_rt = rt_fwd_region(e->P, e->fpart.get<double>(), ctx->num_sms);
-    LaunchGeom g{};
-    if (plan_backward(e->P, ctx->num_sms, &g)) throw CudaError("psi backward: launch planning failed");
-    e->bpart.ensure(sizeof(double) * bwd_part_count(e->P.m, e->P.q) * std::max(1, g.grid));
-    if (psi_backward(e->P, B, e->bpart.get<double>(), e->pgrads.get<double>(), ctx->num_sms, ctx->stream, &e->gb,
-                     e->ev[6], e->ev[7]))
-      throw CudaError(std::string("psi backward launch: ") + cudaGetErrorString(cudaGetLastError()));
+    const int k = int(e->subs.size());
+    int64_t boff = 0;
+    for (auto& sub : e->subs) {
+      LaunchGeom g{};
+      if (plan_backward(sub.P, ctx->num_sms, &g)) throw CudaError("psi backward: launch planning failed");
+      sub.boff = boff;
+      boff += bwd_part_count(sub.P.m, sub.P.q) * std::max(1, g.grid);
+    }
+    e->bpart.ensure(sizeof(double) * boff);
+    if (k > 1) e->pgrads_sub.ensure(sizeof(double) * count * k);
+    const bool stream_out = e->has_gout && e->latent;
+    for (int j = 0; j < k; ++j) {
+      auto& sub = e->subs[j];
+      BwdConst B{};
+      B.u = e->u.get<float>();
+      B.dpsi = e->dpsi.get<float>();
+      B.d_phi = e->res.adj.d_phi;
+      B.add_kl = e->latent ? 1 : 0;
+      B.write_local = e->latent ? 1 : 0;
+      B.d_mu = e->dmu.get<double>() + sub.n0;
+      B.d_s = e->ds.get<double>() + sub.n0;
+      B.ld_g = e->in.n;
+      B.fwd_rt = rt_fwd_region(sub.P, e->fpart.get<double>() + sub.foff, ctx->num_sms);
+      double* out = k > 1 ? e->pgrads_sub.get<double>() + int64_t(j) * count : e->pgrads.get<double>();
+      if (psi_backward(sub.P, B, e->bpart.get<double>() + sub.boff, out, ctx->num_sms, ctx->stream, &e->gb,
+                       j == 0 ? e->ev[6] : nullptr, j == k - 1 ? e->ev[7] : nullptr))
+        throw CudaError(std::string("psi backward launch: ") + cudaGetErrorString(cudaGetLastError()));
+      if (stream_out) {  // d mu / d S of this sub-shard are final: copy them out while the next runs
+        const int64_t q = e->cfg.q, n = e->cfg.n_local;
+        const int64_t ldm = e->g_mu.ld ? e->g_mu.ld : n, lds = e->g_s.ld ? e->g_s.ld : n;
+        CUDA_OK(cudaEventRecord(e->ev_out[j], ctx->stream));
+        CUDA_OK(cudaStreamWaitEvent(e->copy, e->ev_out[j], 0));
+        CUDA_OK(cudaMemcpy2DAsync(e->g_mu.data + sub.n0, sizeof(double) * ldm, e->dmu.get<double>() + sub.n0,
+                                    sizeof(double) * n, sizeof(double) * sub.n, q, cudaMemcpyDeviceToHost, e->copy));
+        CUDA_OK(cudaMemcpy2DAsync(e->g_s.data + sub.n0, sizeof(double) * lds, e->ds.get<double>() + sub.n0,
+                                    sizeof(double) * n, sizeof(double) * sub.n, q, cudaMemcpyDeviceToHost, e->copy));
+      }
+    }
+    if (k > 1) {
+      sum_parts_kernel<<<int(std::min<int64_t>((count + 255) / 256, 1024)), 256, 0, ctx->stream>>>(
+          e->pgrads_sub.get<double>(), k, count, e->pgrads.get<double>());
+      CUDA_OK(cudaGetLastError());
+    }
   } else {
     CUDA_OK(cudaMemsetAsync(e->pgrads.p, 0, sizeof(double) * count, ctx->stream));
   }
@@ -400,6 +522,7 @@ void engine_finish(sgpx_engine* e, sgpx_eval_result* out) {
     e->h_grads.ensure(sizeof(double) * count);
     CUDA_OK(cudaMemcpyAsync(e->h_grads.p, e->pgrads.p, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    if (e->copy) CUDA_OK(cudaStreamSynchronize(e->copy));  // streamed d mu / d S have landed
     const double* g = e->h_grads.get<double>();
     coord::KernGrads kg = coord::kern_grads_zz(e->z, e->kernel, e->res.adj.d_kmm);
     double tr = 0.0;
@@ -849,13 +972,18 @@ int sgpx_engine_broadcast(sgpx_engine* e, const sgpx_kernel_spec* kernel, double
       require(mu.rows == e->cfg.n_local && s.rows == e->cfg.n_local && mu.cols == e->cfg.q && s.cols == e->cfg.q,
               "broadcast: local parameter row mismatch");
       if (on_device) {
+        e->pending_upload = false;
         e->in.mu = mu.data;
         e->in.ld_mu = mu.ld ? mu.ld : e->cfg.n_local;
         e->in.s = s.data;
         e->in.ld_s = s.ld ? s.ld : e->cfg.n_local;
-      } else {
-        upload(e->ctx, e->own_x, mu, false);
-        upload(e->ctx, e->own_s, s, false);
+      } else {  // deferred: the stats pass streams the rows in sub-shards (overlapped with its kernels)
+        const size_t bytes = sizeof(double) * std::max<int64_t>(1, e->cfg.n_local * e->cfg.q);
+        e->own_x.ensure(bytes);
+        e->own_s.ensure(bytes);
+        e->h_mu = mu;
+        e->h_s = s;
+        e->pending_upload = e->cfg.n_local * e->cfg.q > 0;
         e->in.mu = e->own_x.get<double>();
         e->in.ld_mu = e->cfg.n_local;
         e->in.s = e->own_s.get<double>();
@@ -918,6 +1046,23 @@ int sgpx_engine_evaluate(sgpx_engine* e, int with_grads, sgpx_eval_result* out) 
     if (with_grads) engine_grad_pass(e);
     engine_finish(e, out);
     out->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+int sgpx_engine_set_local_grads_out(sgpx_engine* e, sgpx_mmat d_mu, sgpx_mmat d_s) {
+  return guard([&] {
+    require(e != nullptr, "engine is null");
+    require(e->latent, "regression engines hold no local gradients");
+    if (d_mu.data == nullptr && d_s.data == nullptr) {
+      e->has_gout = false;
+      return;
+    }
+    const int64_t n = e->cfg.n_local, q = e->cfg.q;
+    require(d_mu.rows == n && d_mu.cols == q && d_s.rows == n && d_s.cols == q, "local grads must be n_local x Q");
+    require(d_mu.data && d_s.data, "local grads out: null data");
+    e->g_mu = d_mu;
+    e->g_s = d_s;
+    e->has_gout = true;
   });
 }
 

@@ -113,6 +113,9 @@ class DistributedEngine:
         self.passes.eng.set_local_grads_out(dmu, ds)
 
     def evaluate(self, with_grads: bool = True, local_to_host: bool = True) -> sgp.EvalResult:
+        eng = getattr(self.passes, "eng", None)
+        if eng is not None and with_grads and local_to_host and self.kind == sgp.ModelKind.latent:
+            eng._register_grads_out()  # d_mu / d_S stream to the host during the gradient pass
         packed = self.passes.stats_pass()
         self.dist.all_reduce(packed, op=self.dist.ReduceOp.SUM, group=self.group)  # allreduce #1
         self.passes.coordinate(packed, with_grads)

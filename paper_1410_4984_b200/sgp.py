@@ -412,6 +412,7 @@ class Engine:
         check(self._lib.sgpx_engine_create(self.ctx.handle, C.byref(cfg), C.byref(h)))
         self._h = h
         self.m = m
+        self._grads_registered = False
         x, s, y, on_dev = self._data
         if on_dev:
             xv = device_view(x)
@@ -460,8 +461,28 @@ class Engine:
         return r, bufs
 
     def set_local_grads_out(self, dmu, ds):
-        """Preallocated host buffers (pinned for speed) that evaluate() fills with d_mu / d_s."""
+        """Preallocated host buffers (pinned for overlap) that evaluate() fills with d_mu / d_s.
+        The engine streams them per sub-shard while the rest of the gradient pass computes
+        (sgpx_engine_set_local_grads_out); ``None`` unregisters."""
+        if dmu is None:
+            self._grads_out = None
+            if self._h is not None:
+                nm = L.mmat(None, 0, 0, 0)
+                check(self._lib.sgpx_engine_set_local_grads_out(self._h, nm, nm))
+            return
+        n, q = self.n, self.q
+        for a in (dmu, ds):
+            if a.shape != (n, q) or a.dtype != np.float64 or not a.flags.f_contiguous:
+                raise SgpxInvalidArgument("local grads out: Fortran-ordered float64 n_local x Q arrays required")
         self._grads_out = (dmu, ds)
+        self._grads_registered = False
+
+    def _register_grads_out(self):
+        if getattr(self, "_grads_out", None) is not None and not getattr(self, "_grads_registered", False) \
+                and self._h is not None:
+            dmu, ds = self._grads_out
+            check(self._lib.sgpx_engine_set_local_grads_out(self._h, _cm(dmu), _cm(ds)))
+            self._grads_registered = True
 
     def _pack(self, r, bufs, with_grads, local_to_host=True) -> EvalResult:
         stats = SufficientStats(r.phi, bufs["psi_y"], bufs["phi_big"], r.yy, int(r.n_count))
@@ -472,7 +493,10 @@ class Engine:
             g.d_variance = r.d_variance
             g.d_beta = r.d_beta
             if self.kind == ModelKind.latent and local_to_host:
-                g.d_mu, g.d_s = self.local_grads(getattr(self, "_grads_out", None))
+                if getattr(self, "_grads_registered", False):
+                    g.d_mu, g.d_s = self._grads_out  # streamed by the engine during evaluate()
+                else:
+                    g.d_mu, g.d_s = self.local_grads(getattr(self, "_grads_out", None))
         t = EngineTimings(r.stats_pass_s, r.coordinator_s, r.grad_pass_s, r.wall_s, r.fwd_kernel_s, r.bwd_kernel_s,
                           r.fwd_grid, r.bwd_grid)
         return EvalResult(BoundBreakdown._from(r.bound), stats, bool(r.has_grads), g, t, r.jitter_factor_used)
@@ -480,6 +504,12 @@ class Engine:
     def evaluate(self, with_grads: bool = True, local_to_host: bool = True) -> EvalResult:
         """Engine::evaluate (parallel.hpp:370-450)."""
         r, bufs = self._result_buffers()
+        if local_to_host and with_grads and self.kind == ModelKind.latent:
+            self._register_grads_out()
+        elif getattr(self, "_grads_registered", False):  # device-only evaluation: do not stream
+            nm = L.mmat(None, 0, 0, 0)
+            check(self._lib.sgpx_engine_set_local_grads_out(self._h, nm, nm))
+            self._grads_registered = False
         check(self._lib.sgpx_engine_evaluate(self._h, 1 if with_grads else 0, C.byref(r)))
         return self._pack(r, bufs, with_grads, local_to_host)
 

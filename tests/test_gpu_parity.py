@@ -170,3 +170,36 @@ def test_multi_chunk_parity(sgp, orc, shape):
     assert norm_rel_err(g.d_lengthscales, wg.d_lengthscales) < GRAD_TOL
     assert norm_rel_err(g.d_mu, wg.d_mu) < GRAD_TOL
     assert norm_rel_err(g.d_s, wg.d_s) < GRAD_TOL
+
+
+def test_engine_subshard_pipeline(sgp):
+    """Host-resident mu / S (streamed per sub-shard with the kernels) and registered host
+    gradient outputs give the same evaluation as the device-resident single pass."""
+    import torch
+
+    n, q, d, m = 600_000, 4, 3, 24  # >= 500k rows: two sub-shards
+    mu, s, y, z, var, ls = problem(9, n, q, d, m)
+    k = sgp.KernelSpec(var, ls)
+    dev = torch.device("cuda", 0)
+    ctx = sgp.Context(0)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    # device-resident reference run
+    mu_t = torch.from_numpy(np.asfortranarray(mu)).to(dev).t().contiguous().t()
+    s_t = torch.from_numpy(np.asfortranarray(s)).to(dev).t().contiguous().t()
+    y_t = torch.from_numpy(np.asfortranarray(y)).to(dev).t().contiguous().t()
+    e1 = sgp.Engine(sgp.ModelKind.latent, mu_t, s_t, y_t, ctx=ctx)
+    e1.broadcast(k, 50.0, z, mu_t, s_t)
+    r1 = e1.evaluate(True)
+    # host path: deferred, streamed upload + registered (pinned) gradient outputs
+    e2 = sgp.Engine(sgp.ModelKind.latent, mu, s, y, ctx=ctx)
+    gmu = torch.empty(q, n, dtype=torch.float64, pin_memory=True).numpy().T
+    gs = torch.empty(q, n, dtype=torch.float64, pin_memory=True).numpy().T
+    e2.set_local_grads_out(gmu, gs)
+    for _ in range(2):  # second evaluation reuses the registered buffers
+        e2.broadcast(k, 50.0, z, mu, s)
+        r2 = e2.evaluate(True)
+    assert rel_err(r2.bound.total, r1.bound.total) < 1e-12
+    assert norm_rel_err(r2.grads.d_z, r1.grads.d_z) < 1e-10
+    assert norm_rel_err(r2.grads.d_lengthscales, r1.grads.d_lengthscales) < 1e-10
+    assert r2.grads.d_mu is gmu and r2.grads.d_s is gs
+    assert norm_rel_err(gmu, r1.grads.d_mu) < 1e-13 and norm_rel_err(gs, r1.grads.d_s) < 1e-13
