@@ -51,26 +51,32 @@ constexpr int kDrain = 128;             // accumulator drain threads (warps 12 .
 constexpr int kWarpLoad = (kCons + kDrain) / 32;  // loader warp (16)
 constexpr int kWarpMma = kWarpLoad + 1;           // MMA warp (17)
 constexpr int kThreads = kCons + kDrain + 64;
-constexpr int kPadRows = 384;           // feature-array row padding: lcm(kCH, 128)
+constexpr int kPadRows = 768;           // feature-array row padding: lcm(kCH, 2 x 128)
 constexpr float kNegHuge = -1.0e30f;    // B_n of padded datapoints: 2^(~-1e30) = 0
 
 // BF: G = 2^D stored as bf16x2 hi / lo in place of D (kind::f16 MMA3, ~2^-18 relative, up to
 // four D/G stages) or as tf32 hi / lo next to it (kind::tf32 MMA3, ~2^-22, two stages).  The
 // forward uses bf16; the backward uses tf32 because its per-datapoint sums feed differences
 // (mu^2 T0 - 2 mu T1 + T2, and the pair / datapoint parts of d l) that amplify relative error.
-template <int Q, bool BF>
+// PAIR: two CTAs of a cluster run one M = 256 MMA stream (tcgen05 cta_group::2): each holds its
+// own 128 static rows and HALF of every streamed chunk (48 X rows, and Y_hi resp. Y_lo), which
+// halves both the MMA instructions and the L2->SM operand traffic per SM.
+template <int Q, bool BF, bool PAIR = false>
 struct RT {
   static constexpr int K1 = (2 * Q + 2 + 7) / 8 * 8;  // MMA1 depth
   static constexpr int NH = 2 * Q + 1;                // MMA3 useful columns
   static constexpr int N3 = (NH + 15) / 16 * 16;      // MMA3 N
-  static constexpr int XF = kCH * K1;                 // floats of one streamed X part (tf32 hi or lo)
+  static constexpr int XH = PAIR ? kCH / 2 : kCH;     // streamed X rows held by one CTA
+  static constexpr int XF = XH * K1;                  // floats of one X part (tf32 hi or lo)
   static constexpr int YB = N3 * kCH;                 // elements of one Y^T part (hi or lo)
   static constexpr int YFl = BF ? YB / 2 : YB;        // floats of one Y^T part
-  static constexpr int PF = 2 * XF + 2 * YFl;         // floats per processed stage
+  static constexpr int PF = 2 * XF + (PAIR ? 1 : 2) * YFl;  // floats per processed stage (per CTA)
+  static constexpr int CHF = PAIR ? 2 * PF : PF;      // floats per streamed chunk in global memory
   static constexpr int AF = 128 * K1;                 // floats of one static part (hi or lo)
   static constexpr int SW = BF ? kCH : 2 * kCH;       // TMEM columns per D/G stage
-  // MMA3 as G_hi * [Y_hi ; Y_lo] (N = 2 N3) + G_lo * Y_hi (N = N3) when the 2 N3-column
-  // accumulators fit next to the (at least 3, resp. 2) D/G stages; else three N3 passes.
+  // MMA3 as G_hi * [Y_hi ; Y_lo] (N = 2 N3) + G_lo * Y_hi (N = N3; N = 2 N3 with [Y_hi ; Y_lo] in
+  // PAIR mode) when the 2 N3-column accumulators fit next to the (at least 3, resp. 2) D/G
+  // stages; else three N3 passes (single-CTA only).
   static constexpr bool kConcat = (BF ? 3 : 2) * SW + 4 * N3 <= 512;
   static constexpr int AccW = kConcat ? 2 * N3 : N3;   // TMEM columns per accumulator stage
   static constexpr int kS = BF ? ((512 - 2 * AccW) / SW >= 4 ? 4 : 3) : 2;  // D/G stages
@@ -78,8 +84,12 @@ struct RT {
 
 __host__ __device__ constexpr int rt_k1(int q) { return (2 * q + 2 + 7) / 8 * 8; }
 __host__ __device__ constexpr int rt_n3(int q) { return (2 * q + 1 + 15) / 16 * 16; }
-__host__ __device__ constexpr int rt_pf(int q, bool bf) {
-  return 2 * kCH * rt_k1(q) + (bf ? 1 : 2) * rt_n3(q) * kCH;
+// per-CTA processed stage floats
+__host__ __device__ constexpr int rt_pf(int q, bool bf, bool pair) {
+  return 2 * (pair ? kCH / 2 : kCH) * rt_k1(q) + (pair ? 1 : 2) * (bf ? 1 : 2) * rt_n3(q) * kCH / 2;
+}
+__host__ __device__ constexpr bool rt_concat(int q, bool bf) {
+  return (bf ? 3 : 2) * (bf ? kCH : 2 * kCH) + 4 * rt_n3(q) <= 512;
 }
 inline int64_t pad_rows(int64_t r) { return (r + kPadRows - 1) / kPadRows * kPadRows; }
 
@@ -92,11 +102,11 @@ struct RtCfg {
 __host__ __device__ constexpr int rt_stages(int q, bool bf) {  // RT<Q, BF>::kS on the host
   return bf ? ((512 - 2 * ((3 * kCH + 4 * rt_n3(q) <= 512) ? 2 * rt_n3(q) : rt_n3(q))) / kCH >= 4 ? 4 : 3) : 2;
 }
-RtCfg rt_cfg(int q, bool bf) {
+RtCfg rt_cfg(int q, bool bf, bool pair = false) {
   // operand stages: MMA1 runs kS chunks ahead, so the TMA ring needs kS + 2 slots to keep two
   // loads in flight; a single static-tile buffer if that is what makes room.
   const size_t K1 = rt_k1(q);
-  const size_t a = 4 * 2 * 128 * K1, pst = 4 * size_t(rt_pf(q, bf));
+  const size_t a = 4 * 2 * 128 * K1, pst = 4 * size_t(rt_pf(q, bf, pair));
   const size_t bars = 512, cap = 227 * 1024;
   const int ks = rt_stages(q, bf);
   for (int slack = 2; slack >= 0; --slack)
@@ -107,6 +117,8 @@ RtCfg rt_cfg(int q, bool bf) {
     }
   return RtCfg{0, 0, 0};
 }
+// CTA-pair mode: needs the concatenated MMA3 (one B arrangement per CTA)
+bool rt_pair_ok(int q, bool bf) { return rt_concat(q, bf) && rt_cfg(q, bf, true).nP >= 2; }
 
 // bf16x2 (round to nearest): low half = a (even element), high half = b
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
@@ -140,34 +152,40 @@ __device__ __forceinline__ void put_rows(float* hi, float* lo, int64_t r, const 
   }
 }
 
-// One row of a processed-stage chunk [X hi | X lo | Y^T hi | Y^T lo] (layouts of the MMA1 / MMA3
-// B operands): X row jj (K1 features), Y column jj (N3 features, rows past NH zero).
-template <int Q, bool BF>
+// One row of a streamed chunk in the processed-stage layout (the MMA1 / MMA3 B operands): X row
+// jj (K1 features) and Y column jj (N3 features, rows past NH zero).  Single CTA:
+// [X hi | X lo | Y^T hi | Y^T lo] over all 96 rows.  PAIR: two per-CTA blocks
+// [X hi | X lo (48 rows) | Y^T hi] and [X hi | X lo (rows 48..95) | Y^T lo].
+template <int Q, bool BF, bool PAIR>
 __device__ __forceinline__ void put_pre_row(float* chunk, int jj, const float* x, const float* y) {
-  using C = RT<Q, BF>;
-  constexpr int K1 = C::K1, N3 = C::N3, XF = C::XF, YB = C::YB;
+  using C = RT<Q, BF, PAIR>;
+  constexpr int K1 = C::K1, N3 = C::N3, XF = C::XF, YFl = C::YFl, PF = C::PF, XH = C::XH;
+  float* xb = chunk + (PAIR ? (jj / XH) * PF : 0);
+  const int r = jj % XH;
 #pragma unroll
   for (int k = 0; k < K1; k += 4) {
     const float x4[4] = {x[k], x[k + 1], x[k + 2], x[k + 3]};
-    put_split(chunk, chunk + XF, (jj >> 3) * (K1 * 8) + (k >> 2) * 32 + (jj & 7) * 4, x4);
+    put_split(xb, xb + XF, (r >> 3) * (K1 * 8) + (k >> 2) * 32 + (r & 7) * 4, x4);
   }
+  float* y_hi = chunk + 2 * XF;                          // block 0 (or the single block)
+  float* y_lo = PAIR ? chunk + PF + 2 * XF : y_hi + YFl;  // block 1 (or after Y_hi)
   if (BF) {  // Y^T as bf16 hi / lo, canonical K-major (rows = features, 8 bf16 per core-matrix row)
-    __nv_bfloat16* yh = reinterpret_cast<__nv_bfloat16*>(chunk + 2 * XF);
+    __nv_bfloat16* yh = reinterpret_cast<__nv_bfloat16*>(y_hi);
+    __nv_bfloat16* yl = reinterpret_cast<__nv_bfloat16*>(y_lo);
 #pragma unroll
     for (int f = 0; f < N3; ++f) {
       const int off = (f >> 3) * (kCH * 8) + (jj >> 3) * 64 + (f & 7) * 8 + (jj & 7);
       const __nv_bfloat16 hi = __float2bfloat16_rn(y[f]);
       yh[off] = hi;
-      yh[YB + off] = __float2bfloat16_rn(y[f] - __bfloat162float(hi));
+      yl[off] = __float2bfloat16_rn(y[f] - __bfloat162float(hi));
     }
   } else {   // Y^T as tf32 hi / lo, canonical K-major (4 tf32 per core-matrix row)
-    float* yh = chunk + 2 * XF;
 #pragma unroll
     for (int f = 0; f < N3; ++f) {
       const int off = (f >> 3) * (kCH * 8) + (jj >> 2) * 32 + (f & 7) * 4 + (jj & 3);
       const float hi = tc::tf32_hi(y[f]);
-      yh[off] = hi;
-      yh[YB + off] = y[f] - hi;
+      y_hi[off] = hi;
+      y_lo[off] = y[f] - hi;
     }
   }
 }
@@ -212,7 +230,7 @@ __global__ void __launch_bounds__(256) rt_pair_rows_kernel(PsiConst P, int64_t p
 // Datapoint rows H_n, n < n_pad (padded rows [0 .., 0, -huge]): canonical K-major hi / lo (static
 // operand of the backward) and, per 96-row chunk, the forward's streamed operands
 // X = H_n, Y = [1, d2 mu, d2] in the processed-stage layout.
-template <int Q>
+template <int Q, bool PAIR>
 __global__ void __launch_bounds__(256) rt_data_rows_kernel(PsiConst P, int64_t n_pad, float* __restrict__ hh,
                                                             float* __restrict__ hl, float* __restrict__ pre) {
   constexpr int K1 = RT<Q, true>::K1;
@@ -255,15 +273,15 @@ __global__ void __launch_bounds__(256) rt_data_rows_kernel(PsiConst P, int64_t n
       h[2 * Q + 1] = kNegHuge;
     }
     put_rows(hh, hl, n, h, K1);
-    put_pre_row<Q, true>(pre + (n / kCH) * RT<Q, true>::PF, int(n % kCH), h, y);
+    put_pre_row<Q, true, PAIR>(pre + (n / kCH) * RT<Q, true, PAIR>::CHF, int(n % kCH), h, y);
   }
 }
 
 // Backward streamed operands, precomputed: X = F_p, Y = w_p [1, zb, zb^2].
-template <int Q>
+template <int Q, bool PAIR>
 __global__ void __launch_bounds__(256) rt_pair_pre_kernel(PsiConst P, const float* __restrict__ u, int64_t p_pad,
                                                            float* __restrict__ pre) {
-  using C = RT<Q, false>;
+  using C = RT<Q, false, PAIR>;
   constexpr int K1 = C::K1, N3 = C::N3;
   const int m = P.m, qv = P.qv, mv = P.mv;
   const int64_t npairs = int64_t(m) * (m + 1) / 2;
@@ -298,7 +316,7 @@ __global__ void __launch_bounds__(256) rt_pair_pre_kernel(PsiConst P, const floa
       f[2 * Q + 1] = 1.f;
       y[0] = w;
     }
-    put_pre_row<Q, false>(pre + (p / kCH) * C::PF, int(p % kCH), f, y);
+    put_pre_row<Q, false, PAIR>(pre + (p / kCH) * C::CHF, int(p % kCH), f, y);
   }
 }
 
@@ -337,21 +355,28 @@ struct RowTileArgs {
   int dbg;  // SGPX_RT_DBG (timing experiments only): 1 skip G math, 2 skip MMA3, 4 skip MMA1
 };
 
-template <int Q, bool BF>
+template <int Q, bool BF, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTileArgs R) {
-  using C = RT<Q, BF>;
+  using C = RT<Q, BF, PAIR>;
   constexpr int K1 = C::K1, KS1 = K1 / 8, N3 = C::N3, NH = C::NH;
-  constexpr int PF = C::PF, XF = C::XF, YB = C::YB, YFl = C::YFl, AF = C::AF;
+  constexpr int PF = C::PF, CHF = C::CHF, XF = C::XF, YFl = C::YFl, AF = C::AF;
   constexpr int kS = C::kS;             // D/G stages of SW TMEM columns
   constexpr int SW = C::SW;
   constexpr uint32_t kAcc0 = kS * SW;   // two accumulator stages of AccW columns
   constexpr int AccW = C::AccW;
   constexpr bool kConcat = C::kConcat;
+  static_assert(!PAIR || kConcat, "CTA-pair mode needs the concatenated MMA3");
+  constexpr int kM = PAIR ? 256 : 128;  // MMA M (both CTAs' TMEM lanes in PAIR mode)
   extern __shared__ __align__(1024) float sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t rank = PAIR ? tc::cta_rank() : 0u;
+  const bool leader = rank == 0;
+  // leader barriers fed by the peer: +1 arrival from the peer's load relay (a_full, p_full), +1 per
+  // peer consumer / drain warp (g_full, c_empty: those warps arrive directly, one lane each)
+  const uint32_t relay = (PAIR && leader) ? 1u : 0u;
   const int nA = R.nA, nP = R.nP;
   float* Abuf = sm;                       // [nA][hi|lo][AF]
-  float* Proc = Abuf + nA * 2 * AF;       // [nP][Xh | Xl | Yh | Yl]
+  float* Proc = Abuf + nA * 2 * AF;       // [nP][Xh | Xl | Y]
   uint64_t* bar = reinterpret_cast<uint64_t*>(Proc + nP * PF);
   uint64_t* a_full = bar;                 // [2] static tile landed (tx)
   uint64_t* a_empty = bar + 2;            // [2] MMA1s of the tile done
@@ -363,30 +388,39 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
   uint64_t* c_empty = bar + 30;           // [2] accumulator drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 32);
 
-  if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
+  if (warp == 0) {
+    if (PAIR) tc::tmem_alloc2(tmem_slot, 512);
+    else tc::tmem_alloc(tmem_slot, 512);
+  }
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&a_full[i], 1);
+      tc::mbar_init(&a_full[i], 1 + relay);
       tc::mbar_init(&a_empty[i], 1);
       tc::mbar_init(&c_full[i], 1);
-      tc::mbar_init(&c_empty[i], kDrain);
+      tc::mbar_init(&c_empty[i], kDrain + relay * (kDrain / 32));
     }
     for (int i = 0; i < 8; ++i) {
-      tc::mbar_init(&p_full[i], 1);
+      tc::mbar_init(&p_full[i], 1 + relay);
       tc::mbar_init(&p_empty[i], 1);
     }
     for (int i = 0; i < 4; ++i) {
       tc::mbar_init(&d_full[i], 1);
-      tc::mbar_init(&g_full[i], kCons);
+      tc::mbar_init(&g_full[i], kCons + relay * (kCons / 32));
     }
     tc::mbar_fence_init();
   }
   tc::fence_before();
   __syncthreads();
+  if (PAIR) tc::cluster_sync();  // both CTAs' barriers and TMEM exist before any remote traffic
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
+  auto wait_x = [&](uint64_t* b, uint32_t ph) {  // barriers that receive the peer's relayed arrivals
+    if (PAIR) tc::mbar_wait_cluster(b, ph);
+    else tc::mbar_wait(b, ph);
+  };
 
-  // schedule: my tiles and the chunk sequence
+  // schedule: my tiles and the chunk sequence (in PAIR mode both CTAs of a cluster walk the same
+  // sequence with their own static tiles: tile = 2 * tile_pair + rank)
   int64_t my_tiles, cpt, c_first;
   if (R.mode == 0) {
     my_tiles = 1;
@@ -394,12 +428,18 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
     cpt = R.nchunks - c_first < R.cps ? R.nchunks - c_first : R.cps;
     if (cpt < 0) cpt = 0;
   } else {
-    my_tiles = R.ntiles > blockIdx.x ? (R.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const int64_t units = PAIR ? (R.ntiles + 1) / 2 : R.ntiles;
+    const int64_t me = PAIR ? blockIdx.x / 2 : blockIdx.x, nme = PAIR ? gridDim.x / 2 : gridDim.x;
+    my_tiles = units > me ? (units - me + nme - 1) / nme : 0;
     c_first = 0;
     cpt = R.nchunks;
   }
   const int64_t total = my_tiles * cpt;
-  auto tile_of = [&](int64_t i) -> int64_t { return R.mode == 0 ? int64_t(blockIdx.x) : blockIdx.x + i * gridDim.x; };
+  auto tile_of = [&](int64_t i) -> int64_t {
+    if (R.mode == 0) return int64_t(blockIdx.x);
+    if (PAIR) return 2 * (blockIdx.x / 2 + i * (gridDim.x / 2)) + rank;
+    return blockIdx.x + i * gridDim.x;
+  };
 
   if (warp == kWarpLoad) {
     // ---------------- loader: static tiles + streamed operand chunks (1D TMA) ----------------
@@ -418,7 +458,8 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
         }
         if (c >= nP) tc::mbar_wait(&p_empty[rp.slot], rp.phase ^ 1u);
         tc::mbar_arrive_expect_tx(&p_full[rp.slot], uint32_t(PF * 4));
-        tc::bulk_g2s(Proc + rp.slot * PF, R.pre + (c_first + j) * PF, uint32_t(PF * 4), &p_full[rp.slot]);
+        tc::bulk_g2s(Proc + rp.slot * PF, R.pre + (c_first + j) * CHF + rank * PF, uint32_t(PF * 4),
+                     &p_full[rp.slot]);
         rp.next();
         if (++j == cpt) {
           j = 0;
@@ -427,16 +468,20 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
       }
     }
     __syncwarp();
-  } else if (warp == kWarpMma) {
-    // ---------------- MMA issuer ----------------
+  } else if (warp == kWarpMma && (!PAIR || leader)) {
+    // ---------------- MMA issuer (the leader CTA of a pair issues for both) ----------------
     if (lane == 0) {
-      const uint32_t id1 = tc::idesc_tf32(128, kCH);
+      const uint32_t id1 = tc::idesc_tf32(kM, kCH);
       // MMA1 runs kS chunks ahead of MMA3 (one per D/G stage): separate positions for the two
       RingPos a1 = ring(nA), p1 = ring(nP), s1 = ring(kS), p3 = ring(nP), s3 = ring(kS), c3 = ring(2);
       int64_t j1 = 0;
+      auto commit_x = [&](uint64_t* b) {
+        if (PAIR) tc::commit2(b);
+        else tc::commit(b);
+      };
       auto mma1 = [&]() {
-        if (j1 == 0) tc::mbar_wait(&a_full[a1.slot], a1.phase);
-        tc::mbar_wait(&p_full[p1.slot], p1.phase);
+        if (j1 == 0) wait_x(&a_full[a1.slot], a1.phase);
+        wait_x(&p_full[p1.slot], p1.phase);
         tc::fence_after();
         const float* a = Abuf + a1.slot * 2 * AF;
         const float* x = Proc + p1.slot * PF;
@@ -447,14 +492,17 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
         for (int t = 0; t < 3; ++t) {
           const uint64_t aa = t == 2 ? al : ah, bb = t == 1 ? xl : xh;
 #pragma unroll
-          for (int ks = 0; ks < KS1; ++ks)
-            if (!(R.dbg & 4)) tc::mma_ss(d, aa + 16 * ks, bb + 16 * ks, id1, (t | ks) ? 1u : 0u);
+          for (int ks = 0; ks < KS1; ++ks) {
+            if (R.dbg & 4) continue;
+            if (PAIR) tc::mma_ss2(d, aa + 16 * ks, bb + 16 * ks, id1, (t | ks) ? 1u : 0u);
+            else tc::mma_ss(d, aa + 16 * ks, bb + 16 * ks, id1, (t | ks) ? 1u : 0u);
+          }
         }
-        tc::commit(&d_full[s1.slot]);
+        commit_x(&d_full[s1.slot]);
         s1.next();
         p1.next();
         if (++j1 == cpt) {
-          tc::commit(&a_empty[a1.slot]);
+          commit_x(&a_empty[a1.slot]);
           a1.next();
           j1 = 0;
         }
@@ -462,23 +510,27 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
       // bf16 G of stage s: consumer group g stored datapoints [32 g, 32 g + 32) as bf16x2 hi in
       // columns [32 g, 32 g + 16) and lo in [32 g + 16, 32 g + 32); K-step k (16 datapoints) of hi
       // is at column 32 (k / 2) + 8 (k % 2), lo 16 columns further.  tf32 G: hi in place of D,
-      // lo kCH columns further, K-step k (8 datapoints) at column 8 k.
+      // lo kCH columns further, K-step k (8 datapoints) at column 8 k.  In PAIR mode each CTA
+      // holds one half of [Y_hi ; Y_lo] at the same offset, so both passes use N = 2 N3.
       auto mma3 = [&](int64_t c) {
-        tc::mbar_wait(&g_full[s3.slot], s3.phase);
-        if (c >= 2) tc::mbar_wait(&c_empty[c3.slot], c3.phase ^ 1u);
+        wait_x(&g_full[s3.slot], s3.phase);
+        if (c >= 2) wait_x(&c_empty[c3.slot], c3.phase ^ 1u);
         tc::fence_after();
         const float* y = Proc + p3.slot * PF + 2 * XF;
         const uint32_t g0 = tmem + uint32_t(s3.slot) * SW;
         const uint32_t acc = tmem + kAcc0 + uint32_t(c3.slot) * AccW;
         if (!(R.dbg & 2)) {
           if (BF) {
-            const uint32_t id3 = tc::idesc_bf16(128, N3), id3c = tc::idesc_bf16(128, 2 * N3);
+            const uint32_t id3 = tc::idesc_bf16(kM, N3), id3c = tc::idesc_bf16(kM, 2 * N3);
             const uint64_t yh = tc::desc_sbo(tc::smem_u32(y), kCH * 16);
             const uint64_t yl = tc::desc_sbo(tc::smem_u32(y + YFl), kCH * 16);
 #pragma unroll
             for (int k = 0; k < kCH / 16; ++k) {
               const uint32_t gh = g0 + 32 * (k >> 1) + 8 * (k & 1), gl = gh + 16;
-              if (kConcat) {
+              if (PAIR) {
+                tc::mma_ts2_f16(acc, gh, yh + 16 * k, id3c, k ? 1u : 0u);
+                tc::mma_ts2_f16(acc, gl, yh + 16 * k, id3c, 1u);
+              } else if (kConcat) {
                 tc::mma_ts_f16(acc, gh, yh + 16 * k, id3c, k ? 1u : 0u);
                 tc::mma_ts_f16(acc, gl, yh + 16 * k, id3, 1u);
               } else {
@@ -488,10 +540,15 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
               }
             }
           } else {
-            const uint32_t id3 = tc::idesc_tf32(128, N3), id3c = tc::idesc_tf32(128, 2 * N3);
+            const uint32_t id3 = tc::idesc_tf32(kM, N3), id3c = tc::idesc_tf32(kM, 2 * N3);
             const uint64_t yh = tc::desc(tc::smem_u32(y), kCH), yl = tc::desc(tc::smem_u32(y + YFl), kCH);
             const uint32_t gh = g0, gl = g0 + kCH;
-            if (kConcat) {
+            if (PAIR) {
+#pragma unroll
+              for (int k = 0; k < kCH / 8; ++k) tc::mma_ts2(acc, gh + 8 * k, yh + 16 * k, id3c, k ? 1u : 0u);
+#pragma unroll
+              for (int k = 0; k < kCH / 8; ++k) tc::mma_ts2(acc, gl + 8 * k, yh + 16 * k, id3c, 1u);
+            } else if (kConcat) {
 #pragma unroll
               for (int k = 0; k < kCH / 8; ++k) tc::mma_ts(acc, gh + 8 * k, yh + 16 * k, id3c, k ? 1u : 0u);
 #pragma unroll
@@ -507,8 +564,8 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
             }
           }
         }
-        tc::commit(&c_full[c3.slot]);
-        tc::commit(&p_empty[p3.slot]);
+        commit_x(&c_full[c3.slot]);
+        commit_x(&p_empty[p3.slot]);
         s3.next();
         p3.next();
         c3.next();
@@ -517,6 +574,29 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
       for (int64_t c = 0; c < total; ++c) {
         mma3(c);
         if (c + kS < total) mma1();
+      }
+    }
+    __syncwarp();
+  } else if (warp == kWarpMma) {
+    // ---------------- relay (peer CTA of a pair) ----------------
+    // forwards "this CTA's static tile / operand half has landed" to the leader's barriers, in
+    // load order (never blocked by compute: G-stored and drained are signalled directly by the
+    // peer's consumer and drain warps)
+    if (lane == 0) {
+      RingPos a1 = ring(nA), p1 = ring(nP);
+      int64_t j1 = 0;
+      for (int64_t c = 0; c < total; ++c) {
+        if (j1 == 0) {
+          tc::mbar_wait(&a_full[a1.slot], a1.phase);
+          tc::mbar_arrive_remote(&a_full[a1.slot], 0);
+        }
+        tc::mbar_wait(&p_full[p1.slot], p1.phase);
+        tc::mbar_arrive_remote(&p_full[p1.slot], 0);
+        p1.next();
+        if (++j1 == cpt) {
+          a1.next();
+          j1 = 0;
+        }
       }
     }
     __syncwarp();
@@ -533,22 +613,32 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
       tc::mbar_wait(&c_full[s.slot], s.phase);
       tc::fence_after();
       const uint32_t a0 = tmem + kAcc0 + uint32_t(s.slot) * AccW + lane_off;
+      // load the whole accumulator row first and release the stage before the fp64 work: the
+      // 2-deep accumulator ring is on the MMA3 critical path
+      constexpr int NB = (NH + 7) / 8;
+      uint32_t r[NB][8], r2[NB][8];
 #pragma unroll
-      for (int k0 = 0; k0 < NH; k0 += 8) {
-        uint32_t r[8], r2[8];
-        tc::ld8(a0 + k0, r);
-        if (kConcat) tc::ld8(a0 + N3 + k0, r2);
-        tc::ld_wait();
+      for (int b = 0; b < NB; ++b) {
+        tc::ld8(a0 + 8 * b, r[b]);
+        if (kConcat) tc::ld8(a0 + N3 + 8 * b, r2[b]);
+      }
+      tc::ld_wait();
+      tc::fence_before();
+      if (PAIR && !leader) {
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_remote(&c_empty[s.slot], 0);
+      } else {
+        tc::mbar_arrive(&c_empty[s.slot]);
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          if (k0 + kk < NH) {
-            float v = __uint_as_float(r[kk]);
-            if (kConcat) v += __uint_as_float(r2[kk]);
-            acc[k0 + kk] += double(v);
+          if (8 * b + kk < NH) {
+            float v = __uint_as_float(r[b][kk]);
+            if (kConcat) v += __uint_as_float(r2[b][kk]);
+            acc[8 * b + kk] += double(v);
           }
-      }
-      tc::fence_before();
-      tc::mbar_arrive(&c_empty[s.slot]);
       s.next();
       if (++dj == cpt) {  // tile complete: write its rows
         dj = 0;
@@ -583,6 +673,13 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
         tc::ld16(dcol + 16, r1);
         tc::ld_wait();
         auto exps = [&](const uint32_t (&r)[16], int i, float (&v)[4]) {
+          if (R.dbg & 8) {  // timing experiment: TMEM traffic without the exp2 math
+            v[0] = __uint_as_float(r[i]);
+            v[1] = __uint_as_float(r[i + 1]);
+            v[2] = __uint_as_float(r[i + 2]);
+            v[3] = __uint_as_float(r[i + 3]);
+            return;
+          }
           // 3 of 4 exponentials on MUFU.EX2, 1 of 4 on the FMA pipe
           v[0] = ex2(__uint_as_float(r[i]));
           v[1] = ex2(__uint_as_float(r[i + 1]));
@@ -632,15 +729,22 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
         tc::st_wait();
       }
       tc::fence_before();
-      tc::mbar_arrive(&g_full[sd.slot]);
+      if (PAIR && !leader) {
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_remote(&g_full[sd.slot], 0);
+      } else {
+        tc::mbar_arrive(&g_full[sd.slot]);
+      }
       sd.next();
     }
   }
   tc::fence_before();
   __syncthreads();
+  if (PAIR) tc::cluster_sync();  // the leader's MMAs (into both CTAs) and all remote arrivals are done
   if (warp == 0) {
     tc::fence_after();
-    tc::tmem_dealloc(tmem, 512);
+    if (PAIR) tc::tmem_dealloc2(tmem, 512);
+    else tc::tmem_dealloc(tmem, 512);
   }
 }
 
@@ -830,7 +934,7 @@ FwdLayout fwd_layout(const PsiConst& P, int num_sms) {
   L.f_hh = L.f_fl + L.p_pad * K1;
   L.f_hl = L.f_hh + L.n_pad * K1;
   L.f_pre = L.f_hl + L.n_pad * K1;
-  L.floats = L.f_pre + (L.n_pad / kCH) * rt_pf(q, true);
+  L.floats = L.f_pre + (L.n_pad / kCH) * rt_pf(q, true, false);  // same chunk size in PAIR layout
   L.doubles = L.off_floats + (L.floats + 1) / 2 + 2;
   return L;
 }
@@ -858,7 +962,7 @@ BwdLayout bwd_layout(const PsiConst& P, int num_sms) {
   L.off_t = 0;
   L.off_dl = L.off_t + std::max<int64_t>(P.n, 1) * (2 * q + 1);
   L.off_floats = (L.off_dl + int64_t(L.epi_blocks) * q + 1) / 2 * 2 + 2;
-  const int64_t pf = rt_pf(q, false);
+  const int64_t pf = rt_pf(q, false, false);
   L.doubles = L.off_floats + ((pad_rows(npairs) / kCH) * pf + 1) / 2 + 4;
   return L;
 }
@@ -871,15 +975,55 @@ int rt_dbg() {
   return v;
 }
 
-template <int Q, bool BF>
+// CTA-pair kernels (cta_group::2) are correct but not yet faster than the single-CTA ones: the
+// cross-SM barrier round trips set a ~2.4 ms synchronisation floor at C3 (profiles/
+// r01_ncu_rowtile_summary.md).  Opt in with SGPX_RT_PAIR=1.
+int rt_pair_env() {
+  static const int v = [] {
+    const char* e = getenv("SGPX_RT_PAIR");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+bool use_pair(int q, bool bf) { return rt_pair_env() != 0 && rt_pair_ok(q, bf); }
+
+template <int Q, bool BF, bool PAIR>
 int launch_rowtile(const PsiConst& P, RowTileArgs R, dim3 grid, cudaStream_t st) {
-  const RtCfg cfg = rt_cfg(Q, BF);
+  RtCfg cfg = rt_cfg(Q, BF, PAIR);
+  if (const char* e = getenv("SGPX_RT_NP")) {  // experiments: deepest ring with nA = 1
+    const int want = atoi(e);
+    const size_t a = 4 * 2 * 128 * size_t(rt_k1(Q)), pst = 4 * size_t(rt_pf(Q, BF, PAIR));
+    for (int np = want; np >= 2; --np)
+      if (a + np * pst + 512 <= 227 * 1024) {
+        cfg = RtCfg{1, np, a + np * pst + 512};
+        break;
+      }
+  }
   R.nA = cfg.nA;
   R.nP = cfg.nP;
   R.dbg = rt_dbg();
-  auto kern = rowtile_kernel<Q, BF>;
+  auto kern = rowtile_kernel<Q, BF, PAIR>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cfg.smem)) != cudaSuccess) return 3;
-  kern<<<grid, kThreads, cfg.smem, st>>>(P, R);
+  if (PAIR) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = cfg.smem;
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    if (cudaLaunchKernelEx(&lc, kern, P, R) != cudaSuccess) {
+      fprintf(stderr, "sgpx: rowtile pair launch: %s\n", cudaGetErrorString(cudaGetLastError()));
+      return 3;
+    }
+  } else {
+    kern<<<grid, kThreads, cfg.smem, st>>>(P, R);
+  }
   g_tc_launches.fetch_add(1);
   const cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) {
@@ -897,7 +1041,9 @@ int rt_forward_q(const PsiConst& P, double* base, double* packed, int num_sms, c
   const int blocks_p = int(std::min<int64_t>((L.p_pad + 255) / 256, int64_t(num_sms) * 8));
   rt_pair_rows_kernel<Q><<<blocks_p, 256, 0, st>>>(P, L.p_pad, fl + L.f_fh, fl + L.f_fl);
   const int blocks_n = int(std::min<int64_t>((L.n_pad + 255) / 256, int64_t(num_sms) * 8));
-  rt_data_rows_kernel<Q><<<blocks_n, 256, 0, st>>>(P, L.n_pad, fl + L.f_hh, fl + L.f_hl, fl + L.f_pre);
+  const bool pair = use_pair(Q, true);
+  if (pair) rt_data_rows_kernel<Q, true><<<blocks_n, 256, 0, st>>>(P, L.n_pad, fl + L.f_hh, fl + L.f_hl, fl + L.f_pre);
+  else rt_data_rows_kernel<Q, false><<<blocks_n, 256, 0, st>>>(P, L.n_pad, fl + L.f_hh, fl + L.f_hl, fl + L.f_pre);
   g_tc_launches.fetch_add(2);
   RowTileArgs R{};
   R.a_hi = fl + L.f_fh;
@@ -909,7 +1055,15 @@ int rt_forward_q(const PsiConst& P, double* base, double* packed, int num_sms, c
   R.cps = (L.nchunks + L.ns - 1) / L.ns;
   R.nrows_static = L.npairs;
   R.out = base + L.off_part;
-  if (int rc = launch_rowtile<Q, true>(P, R, dim3(unsigned(R.ntiles), unsigned(L.ns)), st)) return rc;
+  if constexpr (RT<Q, true, true>::kConcat) {
+    if (pair) {
+      const unsigned gx = unsigned((R.ntiles + 1) / 2 * 2);
+      if (int rc = launch_rowtile<Q, true, true>(P, R, dim3(gx, unsigned(L.ns)), st)) return rc;
+    }
+  }
+  if (!pair) {
+    if (int rc = launch_rowtile<Q, true, false>(P, R, dim3(unsigned(R.ntiles), unsigned(L.ns)), st)) return rc;
+  }
   const int64_t tot = L.npairs * C::NH;
   rt_pair_reduce_kernel<<<int(std::min<int64_t>((tot + 255) / 256, 4096)), 256, 0, st>>>(
       base + L.off_part, L.ns, L.npairs, C::NH, base + L.off_sums, packed);
@@ -925,7 +1079,9 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
   float* ff = floats_at(fbase, F.off_floats);
   float* pre = floats_at(bbase, L.off_floats);
   const int blocks_p = int(std::min<int64_t>((F.p_pad + 255) / 256, int64_t(num_sms) * 8));
-  rt_pair_pre_kernel<Q><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, pre);
+  const bool pair = use_pair(Q, false);
+  if (pair) rt_pair_pre_kernel<Q, true><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, pre);
+  else rt_pair_pre_kernel<Q, false><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, pre);
   g_tc_launches.fetch_add(1);
   if (P.n > 0) {
     RowTileArgs R{};
@@ -938,7 +1094,16 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
     R.cps = L.pchunks;
     R.nrows_static = P.n;
     R.out = bbase + L.off_t;
-    if (int rc = launch_rowtile<Q, false>(P, R, dim3(unsigned(L.grid)), st)) return rc;
+    if constexpr (RT<Q, false, true>::kConcat) {
+      if (pair) {
+        const int64_t units = (L.ntiles + 1) / 2;
+        const unsigned gx = unsigned(2 * std::max<int64_t>(1, std::min<int64_t>(units, num_sms / 2)));
+        if (int rc = launch_rowtile<Q, false, true>(P, R, dim3(gx), st)) return rc;
+      }
+    }
+    if (!pair) {
+      if (int rc = launch_rowtile<Q, false, false>(P, R, dim3(unsigned(L.grid)), st)) return rc;
+    }
   }
   if (!B.skip_pair_terms) {
     rt_pair_dz_kernel<Q><<<std::max(1, (P.m * P.q + 127) / 128), 128, 0, st>>>(P, B.u, fbase + F.off_sums, prow);
