@@ -70,54 +70,76 @@ __device__ __forceinline__ void load_chunk(const PsiConst& P, int64_t n0, float*
                                            int nthr, double* yy_acc, double* kl_acc, int* err_flag, bool fwd,
                                            bool fwd_layout_y) {
   const int d = P.d;
-  for (int i = tid; i < kN * Q; i += nthr) {
-    const int nl = i % kN, q = i / kN;
-    const int64_t n = n0 + nl;
-    float mu = 0.f, d1 = 0.f;
-    if (q < P.q && n < P.n) {
-      const double md = P.mu[q * P.ld_mu + n];
-      const double sd = P.expected ? P.s[q * P.ld_s + n] : 0.0;
-      if (fwd) {  // validation (psi_stats.hpp:119-120) + KL partial (parallel.hpp:148-149)
-        if (!isfinite(md)) atomicOr(err_flag, 1);
-        if (P.expected && !(sd > 0.0 && isfinite(sd))) atomicOr(err_flag, 4);
-        if (P.expected) *kl_acc += 0.5 * (sd + md * md - log(sd) - 1.0);
-      }
-      mu = float(md - P.center[q]);
-      d1 = 1.f / (float(sd) + P.l2[q]);
+  {
+    constexpr int kB = (kN * Q + 255) / 256;  // per-thread batch for 256 threads
+    double mb[kB], sb[kB];
+#pragma unroll
+    for (int t = 0; t < kB; ++t) {
+      const int i = tid + t * nthr;
+      const int nl = i % kN, q = i / kN;
+      const int64_t n = n0 + nl;
+      const bool ok = i < kN * Q && q < P.q && n < P.n;
+      mb[t] = ok ? __ldg(P.mu + q * P.ld_mu + n) : 0.0;
+      sb[t] = (ok && P.expected) ? __ldg(P.s + q * P.ld_s + n) : 0.0;
     }
-    sm[L.mus + q * kN + nl] = mu;
-    sm[L.d1s + q * kN + nl] = d1;
+#pragma unroll
+    for (int t = 0; t < kB; ++t) {
+      const int i = tid + t * nthr;
+      if (i >= kN * Q) break;
+      const int nl = i % kN, q = i / kN;
+      const int64_t n = n0 + nl;
+      float mu = 0.f, d1 = 0.f;
+      if (q < P.q && n < P.n) {
+        const double md = mb[t], sd = sb[t];
+        if (fwd) {  // validation (psi_stats.hpp:119-120) + KL partial (parallel.hpp:148-149)
+          if (!isfinite(md)) atomicOr(err_flag, 1);
+          if (P.expected && !(sd > 0.0 && isfinite(sd))) atomicOr(err_flag, 4);
+          if (P.expected) *kl_acc += 0.5 * (sd + md * md - log(sd) - 1.0);
+        }
+        mu = float(md - P.center[q]);
+        d1 = 1.f / (float(sd) + P.l2[q]);
+      }
+      sm[L.mus + q * kN + nl] = mu;
+      sm[L.d1s + q * kN + nl] = d1;
+    }
   }
-  for (int nl = tid; nl < kN; nl += nthr) {
+  __syncthreads();  // d1 of the chunk is staged
+  for (int nl = tid; nl < kN; nl += nthr) {  // b1 = log2 var - 1/2 sum_q log2(1 + S/l^2) = log2 var + 1/2 sum log2(d1 l^2)
     const int64_t n = n0 + nl;
     float b1 = -CUDART_INF_F;
     if (n < P.n) {
       b1 = P.log2_var;
 #pragma unroll
       for (int q = 0; q < Q; ++q)
-        if (q < P.q) {
-          const float sv = P.expected ? float(P.s[q * P.ld_s + n]) : 0.f;
-          b1 += -0.5f * log2f(1.f + sv * P.il2[q]);
-        }
+        if (q < P.q) b1 += 0.5f * log2f(sm[L.d1s + q * kN + nl] * P.l2[q]);
     }
     sm[L.b1s + nl] = b1;
   }
-  for (int i = tid; i < kN * d; i += nthr) {
-    const int nl = i % kN, dd = i / kN;
-    const int64_t n = n0 + nl;
-    float yv = 0.f;
-    if (n < P.n) {
-      const double y = P.y[dd * P.ld_y + n];
+  // y tile: batches of 8 independent loads per thread (one memory latency per batch)
+  for (int i0 = tid; i0 < kN * d; i0 += 8 * nthr) {
+    double yb[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int i = i0 + t * nthr;
+      const int nl = i % kN, dd = i / kN;
+      const int64_t n = n0 + nl;
+      yb[t] = (i < kN * d && n < P.n) ? __ldg(P.y + dd * P.ld_y + n) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int i = i0 + t * nthr;
+      if (i >= kN * d) break;
+      const int nl = i % kN, dd = i / kN;
+      const double y = yb[t];
       if (yy_acc) {
         if (fwd && !isfinite(y)) atomicOr(err_flag, 1);
         *yy_acc += y * y;
       }
-      yv = float(y);
+      if (fwd_layout_y)
+        sm[L.ys + nl * L.d4 + dd] = float(y);
+      else
+        sm[L.ys + dd * kN + nl] = float(y);
     }
-    if (fwd_layout_y)
-      sm[L.ys + nl * L.d4 + dd] = yv;
-    else
-      sm[L.ys + dd * kN + nl] = yv;
   }
 }
 
