@@ -470,14 +470,16 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
     __syncwarp();
   } else if (warp == kWarpMma && (!PAIR || leader)) {
     // ---------------- MMA issuer (the leader CTA of a pair issues for both) ----------------
-    if (lane == 0) {
+    // The whole warp runs the issue loop (warp-uniform operands in uniform registers); elect.sync
+    // inside each tcgen05 asm picks the issuing lane.
+    {
       const uint32_t id1 = tc::idesc_tf32(kM, kCH);
       // MMA1 runs kS chunks ahead of MMA3 (one per D/G stage): separate positions for the two
       RingPos a1 = ring(nA), p1 = ring(nP), s1 = ring(kS), p3 = ring(nP), s3 = ring(kS), c3 = ring(2);
       int64_t j1 = 0;
       auto commit_x = [&](uint64_t* b) {
-        if (PAIR) tc::commit2(b);
-        else tc::commit(b);
+        if (PAIR) tc::commit2_w(b);
+        else tc::commit_w(b);
       };
       auto mma1 = [&]() {
         if (j1 == 0) wait_x(&a_full[a1.slot], a1.phase);
@@ -494,8 +496,8 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
 #pragma unroll
           for (int ks = 0; ks < KS1; ++ks) {
             if (R.dbg & 4) continue;
-            if (PAIR) tc::mma_ss2(d, aa + 16 * ks, bb + 16 * ks, id1, (t | ks) ? 1u : 0u);
-            else tc::mma_ss(d, aa + 16 * ks, bb + 16 * ks, id1, (t | ks) ? 1u : 0u);
+            if (PAIR) tc::mma_ss2_w(d, aa + 16 * ks, bb + 16 * ks, id1, (t | ks) ? 1u : 0u);
+            else tc::mma_ss_w(d, aa + 16 * ks, bb + 16 * ks, id1, (t | ks) ? 1u : 0u);
           }
         }
         commit_x(&d_full[s1.slot]);
@@ -528,15 +530,15 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
             for (int k = 0; k < kCH / 16; ++k) {
               const uint32_t gh = g0 + 32 * (k >> 1) + 8 * (k & 1), gl = gh + 16;
               if (PAIR) {
-                tc::mma_ts2_f16(acc, gh, yh + 16 * k, id3c, k ? 1u : 0u);
-                tc::mma_ts2_f16(acc, gl, yh + 16 * k, id3c, 1u);
+                tc::mma_ts2_f16_w(acc, gh, yh + 16 * k, id3c, k ? 1u : 0u);
+                tc::mma_ts2_f16_w(acc, gl, yh + 16 * k, id3c, 1u);
               } else if (kConcat) {
-                tc::mma_ts_f16(acc, gh, yh + 16 * k, id3c, k ? 1u : 0u);
-                tc::mma_ts_f16(acc, gl, yh + 16 * k, id3, 1u);
+                tc::mma_ts_f16_w(acc, gh, yh + 16 * k, id3c, k ? 1u : 0u);
+                tc::mma_ts_f16_w(acc, gl, yh + 16 * k, id3, 1u);
               } else {
-                tc::mma_ts_f16(acc, gh, yh + 16 * k, id3, k ? 1u : 0u);
-                tc::mma_ts_f16(acc, gh, yl + 16 * k, id3, 1u);
-                tc::mma_ts_f16(acc, gl, yh + 16 * k, id3, 1u);
+                tc::mma_ts_f16_w(acc, gh, yh + 16 * k, id3, k ? 1u : 0u);
+                tc::mma_ts_f16_w(acc, gh, yl + 16 * k, id3, 1u);
+                tc::mma_ts_f16_w(acc, gl, yh + 16 * k, id3, 1u);
               }
             }
           } else {
@@ -545,21 +547,21 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
             const uint32_t gh = g0, gl = g0 + kCH;
             if (PAIR) {
 #pragma unroll
-              for (int k = 0; k < kCH / 8; ++k) tc::mma_ts2(acc, gh + 8 * k, yh + 16 * k, id3c, k ? 1u : 0u);
+              for (int k = 0; k < kCH / 8; ++k) tc::mma_ts2_w(acc, gh + 8 * k, yh + 16 * k, id3c, k ? 1u : 0u);
 #pragma unroll
-              for (int k = 0; k < kCH / 8; ++k) tc::mma_ts2(acc, gl + 8 * k, yh + 16 * k, id3c, 1u);
+              for (int k = 0; k < kCH / 8; ++k) tc::mma_ts2_w(acc, gl + 8 * k, yh + 16 * k, id3c, 1u);
             } else if (kConcat) {
 #pragma unroll
-              for (int k = 0; k < kCH / 8; ++k) tc::mma_ts(acc, gh + 8 * k, yh + 16 * k, id3c, k ? 1u : 0u);
+              for (int k = 0; k < kCH / 8; ++k) tc::mma_ts_w(acc, gh + 8 * k, yh + 16 * k, id3c, k ? 1u : 0u);
 #pragma unroll
-              for (int k = 0; k < kCH / 8; ++k) tc::mma_ts(acc, gl + 8 * k, yh + 16 * k, id3, 1u);
+              for (int k = 0; k < kCH / 8; ++k) tc::mma_ts_w(acc, gl + 8 * k, yh + 16 * k, id3, 1u);
             } else {
 #pragma unroll
               for (int t = 0; t < 3; ++t) {
                 const uint32_t ga = t == 2 ? gl : gh;
                 const uint64_t bb = t == 1 ? yl : yh;
 #pragma unroll
-                for (int k = 0; k < kCH / 8; ++k) tc::mma_ts(acc, ga + 8 * k, bb + 16 * k, id3, (t | k) ? 1u : 0u);
+                for (int k = 0; k < kCH / 8; ++k) tc::mma_ts_w(acc, ga + 8 * k, bb + 16 * k, id3, (t | k) ? 1u : 0u);
               }
             }
           }
