@@ -443,7 +443,8 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
 
   if (warp == kWarpLoad) {
     // ---------------- loader: static tiles + streamed operand chunks (1D TMA) ----------------
-    if (lane == 0) {
+    // warp-uniform loop; elect.sync picks the issuing lane
+    {
       RingPos ra = ring(nA), rp = ring(nP);
       int64_t ti = 0, j = 0;
       for (int64_t c = 0; c < total; ++c) {
@@ -451,14 +452,14 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
           if (ti >= nA) tc::mbar_wait(&a_empty[ra.slot], ra.phase ^ 1u);
           const int64_t row0 = tile_of(ti) * 128;
           float* dst = Abuf + ra.slot * 2 * AF;
-          tc::mbar_arrive_expect_tx(&a_full[ra.slot], uint32_t(2 * AF * 4));
-          tc::bulk_g2s(dst, R.a_hi + row0 * K1, uint32_t(AF * 4), &a_full[ra.slot]);
-          tc::bulk_g2s(dst + AF, R.a_lo + row0 * K1, uint32_t(AF * 4), &a_full[ra.slot]);
+          tc::mbar_arrive_expect_tx_w(&a_full[ra.slot], uint32_t(2 * AF * 4));
+          tc::bulk_g2s_w(dst, R.a_hi + row0 * K1, uint32_t(AF * 4), &a_full[ra.slot]);
+          tc::bulk_g2s_w(dst + AF, R.a_lo + row0 * K1, uint32_t(AF * 4), &a_full[ra.slot]);
           ra.next();
         }
         if (c >= nP) tc::mbar_wait(&p_empty[rp.slot], rp.phase ^ 1u);
-        tc::mbar_arrive_expect_tx(&p_full[rp.slot], uint32_t(PF * 4));
-        tc::bulk_g2s(Proc + rp.slot * PF, R.pre + (c_first + j) * CHF + rank * PF, uint32_t(PF * 4),
+        tc::mbar_arrive_expect_tx_w(&p_full[rp.slot], uint32_t(PF * 4));
+        tc::bulk_g2s_w(Proc + rp.slot * PF, R.pre + (c_first + j) * CHF + rank * PF, uint32_t(PF * 4),
                      &p_full[rp.slot]);
         rp.next();
         if (++j == cpt) {
