@@ -10,7 +10,8 @@ import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG_DIR)
-LIB_PATH = os.path.join(PKG_DIR, "libsgpx.so")
+# SGPX_LIB: alternative in-tree build (A/B timing experiments)
+LIB_PATH = os.path.join(PKG_DIR, os.environ.get("SGPX_LIB", "libsgpx.so"))
 HEADER_PATH = os.path.join(ROOT, "include", "sgpx.h")
 
 SGPX_OK, SGPX_INVALID_ARGUMENT, SGPX_NUMERIC, SGPX_CUDA, SGPX_NCCL, SGPX_INTERNAL = range(6)

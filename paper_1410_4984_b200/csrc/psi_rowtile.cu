@@ -25,6 +25,7 @@
 // accumulator drained into fp64 registers every chunk.  All GEMMs use 3xTF32 (hi*hi + hi*lo +
 // lo*hi), ~fp32 accuracy; every cross-chunk / cross-CTA sum is fp64 in a fixed order.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -54,10 +55,12 @@ constexpr int kThreads = kCons + kDrain + 64;
 constexpr int kPadRows = 768;           // feature-array row padding: lcm(kCH, 2 x 128)
 constexpr float kNegHuge = -1.0e30f;    // B_n of padded datapoints: 2^(~-1e30) = 0
 
-// BF: G = 2^D stored as bf16x2 hi / lo in place of D (kind::f16 MMA3, ~2^-18 relative, up to
-// four D/G stages) or as tf32 hi / lo next to it (kind::tf32 MMA3, ~2^-22, two stages).  The
-// forward uses bf16; the backward uses tf32 because its per-datapoint sums feed differences
-// (mu^2 T0 - 2 mu T1 + T2, and the pair / datapoint parts of d l) that amplify relative error.
+// MMA3 operands G = 2^D and Y as 16-bit hi / lo pieces (G packed in place of D, kind::f16 with A
+// from TMEM, up to four D/G stages).  BF (forward): bf16 pieces, ~2^-17 relative.  !BF (backward):
+// fp16 pieces, ~2^-22 (the accuracy of 3xTF32 at twice the K per MMA), because its per-datapoint
+// sums feed differences (mu^2 T0 - 2 mu T1 + T2, and the pair / datapoint parts of d l) that
+// amplify relative error; G is scaled by 2^15 (folded into the exponent) and every Y column by a
+// power of two (rt_yscale_kernel) so that both stay inside the fp16 normal range.
 // PAIR: two CTAs of a cluster run one M = 256 MMA stream (tcgen05 cta_group::2): each holds its
 // own 128 static rows and HALF of every streamed chunk (48 X rows, and Y_hi resp. Y_lo), which
 // halves both the MMA instructions and the L2->SM operand traffic per SM.
@@ -69,27 +72,29 @@ struct RT {
   static constexpr int XH = PAIR ? kCH / 2 : kCH;     // streamed X rows held by one CTA
   static constexpr int XF = XH * K1;                  // floats of one X part (tf32 hi or lo)
   static constexpr int YB = N3 * kCH;                 // elements of one Y^T part (hi or lo)
-  static constexpr int YFl = BF ? YB / 2 : YB;        // floats of one Y^T part
+  static constexpr int YFl = YB / 2;                  // floats of one Y^T part (16-bit pieces)
   static constexpr int PF = 2 * XF + (PAIR ? 1 : 2) * YFl;  // floats per processed stage (per CTA)
   static constexpr int CHF = PAIR ? 2 * PF : PF;      // floats per streamed chunk in global memory
   static constexpr int AF = 128 * K1;                 // floats of one static part (hi or lo)
-  static constexpr int SW = BF ? kCH : 2 * kCH;       // TMEM columns per D/G stage
+  static constexpr int SW = kCH;                      // TMEM columns per D/G stage
   // MMA3 as G_hi * [Y_hi ; Y_lo] (N = 2 N3) + G_lo * Y_hi (N = N3; N = 2 N3 with [Y_hi ; Y_lo] in
   // PAIR mode) when the 2 N3-column accumulators fit next to the (at least 3, resp. 2) D/G
   // stages; else three N3 passes (single-CTA only).
-  static constexpr bool kConcat = (BF ? 3 : 2) * SW + 4 * N3 <= 512;
+  static constexpr bool kConcat = 3 * SW + 4 * N3 <= 512;
   static constexpr int AccW = kConcat ? 2 * N3 : N3;   // TMEM columns per accumulator stage
-  static constexpr int kS = BF ? ((512 - 2 * AccW) / SW >= 4 ? 4 : 3) : 2;  // D/G stages
+  static constexpr int kS = (512 - 2 * AccW) / SW >= 4 ? 4 : 3;  // D/G stages
 };
 
 __host__ __device__ constexpr int rt_k1(int q) { return (2 * q + 2 + 7) / 8 * 8; }
 __host__ __device__ constexpr int rt_n3(int q) { return (2 * q + 1 + 15) / 16 * 16; }
 // per-CTA processed stage floats
 __host__ __device__ constexpr int rt_pf(int q, bool bf, bool pair) {
-  return 2 * (pair ? kCH / 2 : kCH) * rt_k1(q) + (pair ? 1 : 2) * (bf ? 1 : 2) * rt_n3(q) * kCH / 2;
+  (void)bf;
+  return 2 * (pair ? kCH / 2 : kCH) * rt_k1(q) + (pair ? 1 : 2) * rt_n3(q) * kCH / 2;
 }
 __host__ __device__ constexpr bool rt_concat(int q, bool bf) {
-  return (bf ? 3 : 2) * (bf ? kCH : 2 * kCH) + 4 * rt_n3(q) <= 512;
+  (void)bf;
+  return 3 * kCH + 4 * rt_n3(q) <= 512;
 }
 inline int64_t pad_rows(int64_t r) { return (r + kPadRows - 1) / kPadRows * kPadRows; }
 
@@ -100,7 +105,8 @@ struct RtCfg {
   size_t smem;
 };
 __host__ __device__ constexpr int rt_stages(int q, bool bf) {  // RT<Q, BF>::kS on the host
-  return bf ? ((512 - 2 * ((3 * kCH + 4 * rt_n3(q) <= 512) ? 2 * rt_n3(q) : rt_n3(q))) / kCH >= 4 ? 4 : 3) : 2;
+  (void)bf;
+  return (512 - 2 * ((3 * kCH + 4 * rt_n3(q) <= 512) ? 2 * rt_n3(q) : rt_n3(q))) / kCH >= 4 ? 4 : 3;
 }
 RtCfg rt_cfg(int q, bool bf, bool pair = false) {
   // operand stages: MMA1 runs kS chunks ahead, so the TMA ring needs kS + 2 slots to keep two
@@ -125,6 +131,10 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   uint32_t d;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(b), "f"(a));
   return d;
+}
+
+__device__ __forceinline__ uint32_t h2u(__half2 h) {
+  return uint32_t(__half_as_ushort(__low2half(h))) | (uint32_t(__half_as_ushort(__high2half(h))) << 16);
 }
 
 __device__ __forceinline__ void put_split(float* hi, float* lo, int off4, const float (&x)[4]) {
@@ -157,7 +167,8 @@ __device__ __forceinline__ void put_rows(float* hi, float* lo, int64_t r, const 
 // [X hi | X lo | Y^T hi | Y^T lo] over all 96 rows.  PAIR: two per-CTA blocks
 // [X hi | X lo (48 rows) | Y^T hi] and [X hi | X lo (rows 48..95) | Y^T lo].
 template <int Q, bool BF, bool PAIR>
-__device__ __forceinline__ void put_pre_row(float* chunk, int jj, const float* x, const float* y) {
+__device__ __forceinline__ void put_pre_row(float* chunk, int jj, const float* x, const float* y,
+                                            const float* yscale = nullptr) {
   using C = RT<Q, BF, PAIR>;
   constexpr int K1 = C::K1, N3 = C::N3, XF = C::XF, YFl = C::YFl, PF = C::PF, XH = C::XH;
   float* xb = chunk + (PAIR ? (jj / XH) * PF : 0);
@@ -179,16 +190,35 @@ __device__ __forceinline__ void put_pre_row(float* chunk, int jj, const float* x
       yh[off] = hi;
       yl[off] = __float2bfloat16_rn(y[f] - __bfloat162float(hi));
     }
-  } else {   // Y^T as tf32 hi / lo, canonical K-major (4 tf32 per core-matrix row)
+  } else {   // Y^T * yscale as fp16 hi / lo, same layout
+    __half* yh = reinterpret_cast<__half*>(y_hi);
+    __half* yl = reinterpret_cast<__half*>(y_lo);
 #pragma unroll
     for (int f = 0; f < N3; ++f) {
-      const int off = (f >> 3) * (kCH * 8) + (jj >> 2) * 32 + (f & 7) * 4 + (jj & 3);
-      const float hi = tc::tf32_hi(y[f]);
-      y_hi[off] = hi;
-      y_lo[off] = y[f] - hi;
+      const int off = (f >> 3) * (kCH * 8) + (jj >> 3) * 64 + (f & 7) * 8 + (jj & 7);
+      const float v = f < C::NH ? y[f] * yscale[f] : 0.f;
+      const __half hi = __float2half_rn(v);
+      yh[off] = hi;
+      yl[off] = __float2half_rn(v - __half2float(hi));
     }
   }
 }
+
+// Closed-form index of the m1-major upper triangle (psi_stats.hpp:85-97).
+struct PairIdx {
+  int m;
+  __device__ int64_t start(int a) const { return int64_t(a) * m - int64_t(a) * (a - 1) / 2; }
+  __device__ int64_t of(int a, int b) const { return start(a) + (b - a); }  // a <= b
+  __device__ void inv(int64_t p, int& a, int& b) const {                     // m1-major upper triangle
+    const double t = 2.0 * m + 1.0;
+    int x = int((t - sqrt(t * t - 8.0 * double(p))) * 0.5);
+    x = x < 0 ? 0 : (x >= m ? m - 1 : x);
+    while (x + 1 < m && start(x + 1) <= p) ++x;
+    while (x > 0 && start(x) > p) --x;
+    a = x;
+    b = int(p - start(x)) + x;
+  }
+};
 
 // Pair rows F_p, p < p_pad (zero rows past P): canonical K-major hi / lo (static operand of the
 // forward).
@@ -277,10 +307,55 @@ __global__ void __launch_bounds__(256) rt_data_rows_kernel(PsiConst P, int64_t n
   }
 }
 
-// Backward streamed operands, precomputed: X = F_p, Y = w_p [1, zb, zb^2].
+// Backward fp16 scales: yscale[k] = 2^(14 - e_k) with max_p |Y_pk| = m 2^e_k (m in [1/2, 1)), so
+// every scaled column peaks in [2^13, 2^14); yinv[k] = 2^-15 / yscale[k] undoes it and the 2^15 of
+// G.  One block, fixed-order reduction.
+template <int Q>
+__global__ void __launch_bounds__(256) rt_yscale_kernel(PsiConst P, const float* __restrict__ u, float* __restrict__ ys) {
+  constexpr int NH = 2 * Q + 1;
+  __shared__ float red[8][NH];
+  const int m = P.m, mv = P.mv;
+  const PairIdx pi{m};
+  const int64_t npairs = int64_t(m) * (m + 1) / 2;
+  float mx[NH];
+#pragma unroll
+  for (int k = 0; k < NH; ++k) mx[k] = 0.f;
+  for (int64_t p = threadIdx.x; p < npairs; p += blockDim.x) {
+    int a, b;
+    pi.inv(p, a, b);
+    const float w = fabsf(a == b ? u[a * mv + a] : u[a * mv + b] + u[b * mv + a]);
+    mx[0] = fmaxf(mx[0], w);
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      if (q < P.q) {
+        const float zb = fabsf(0.5f * (P.zc[a * P.qv + q] + P.zc[b * P.qv + q]));
+        mx[1 + q] = fmaxf(mx[1 + q], w * zb);
+        mx[1 + Q + q] = fmaxf(mx[1 + Q + q], w * zb * zb);
+      }
+  }
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NH; ++k) {
+    float v = mx[k];
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red[wp][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < NH) {
+    float v = 0.f;
+    for (int i = 0; i < 8; ++i) v = fmaxf(v, red[i][threadIdx.x]);
+    int e = 0;
+    if (v > 0.f && isfinite(v)) frexpf(v, &e);
+    ys[threadIdx.x] = ldexpf(1.f, 14 - e);
+    ys[64 + threadIdx.x] = ldexpf(1.f, e - 29);
+  }
+}
+
+// Backward streamed operands, precomputed: X = F_p (C_ab + 15, so G = 2^15 v), Y = w_p [1, zb, zb^2]
+// (scaled by yscale).
 template <int Q, bool PAIR>
 __global__ void __launch_bounds__(256) rt_pair_pre_kernel(PsiConst P, const float* __restrict__ u, int64_t p_pad,
-                                                           float* __restrict__ pre) {
+                                                           const float* __restrict__ ys, float* __restrict__ pre) {
   using C = RT<Q, false, PAIR>;
   constexpr int K1 = C::K1, N3 = C::N3;
   const int m = P.m, qv = P.qv, mv = P.mv;
@@ -312,11 +387,11 @@ __global__ void __launch_bounds__(256) rt_pair_pre_kernel(PsiConst P, const floa
           y[1 + q] = w * zbar;
           y[1 + Q + q] = w * zbar * zbar;
         }
-      f[2 * Q] = -0.25f * kLog2e * c;
+      f[2 * Q] = 15.f - 0.25f * kLog2e * c;
       f[2 * Q + 1] = 1.f;
       y[0] = w;
     }
-    put_pre_row<Q, false, PAIR>(pre + (p / kCH) * C::CHF, int(p % kCH), f, y);
+    put_pre_row<Q, false, PAIR>(pre + (p / kCH) * C::CHF, int(p % kCH), f, y, ys);
   }
 }
 
@@ -352,6 +427,7 @@ struct RowTileArgs {
   int64_t ntiles, nchunks, cps;
   int64_t nrows_static;    // valid static rows (P or N)
   double* out;             // forward: pair_part [split][p][NH]; backward: T [n][NH]
+  const float* yinv;       // backward: per-column output scale (rt_yscale_kernel), else null
   int dbg;  // SGPX_RT_DBG (timing experiments only): 1 skip G math, 2 skip MMA3, 4 skip MMA1
 };
 
@@ -523,47 +599,23 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
         const uint32_t g0 = tmem + uint32_t(s3.slot) * SW;
         const uint32_t acc = tmem + kAcc0 + uint32_t(c3.slot) * AccW;
         if (!(R.dbg & 2)) {
-          if (BF) {
-            const uint32_t id3 = tc::idesc_bf16(kM, N3), id3c = tc::idesc_bf16(kM, 2 * N3);
-            const uint64_t yh = tc::desc_sbo(tc::smem_u32(y), kCH * 16);
-            const uint64_t yl = tc::desc_sbo(tc::smem_u32(y + YFl), kCH * 16);
+          const uint32_t id3 = BF ? tc::idesc_bf16(kM, N3) : tc::idesc_f16(kM, N3);
+          const uint32_t id3c = BF ? tc::idesc_bf16(kM, 2 * N3) : tc::idesc_f16(kM, 2 * N3);
+          const uint64_t yh = tc::desc_sbo(tc::smem_u32(y), kCH * 16);
+          const uint64_t yl = tc::desc_sbo(tc::smem_u32(y + YFl), kCH * 16);
 #pragma unroll
-            for (int k = 0; k < kCH / 16; ++k) {
-              const uint32_t gh = g0 + 32 * (k >> 1) + 8 * (k & 1), gl = gh + 16;
-              if (PAIR) {
-                tc::mma_ts2_f16_w(acc, gh, yh + 16 * k, id3c, k ? 1u : 0u);
-                tc::mma_ts2_f16_w(acc, gl, yh + 16 * k, id3c, 1u);
-              } else if (kConcat) {
-                tc::mma_ts_f16_w(acc, gh, yh + 16 * k, id3c, k ? 1u : 0u);
-                tc::mma_ts_f16_w(acc, gl, yh + 16 * k, id3, 1u);
-              } else {
-                tc::mma_ts_f16_w(acc, gh, yh + 16 * k, id3, k ? 1u : 0u);
-                tc::mma_ts_f16_w(acc, gh, yl + 16 * k, id3, 1u);
-                tc::mma_ts_f16_w(acc, gl, yh + 16 * k, id3, 1u);
-              }
-            }
-          } else {
-            const uint32_t id3 = tc::idesc_tf32(kM, N3), id3c = tc::idesc_tf32(kM, 2 * N3);
-            const uint64_t yh = tc::desc(tc::smem_u32(y), kCH), yl = tc::desc(tc::smem_u32(y + YFl), kCH);
-            const uint32_t gh = g0, gl = g0 + kCH;
+          for (int k = 0; k < kCH / 16; ++k) {
+            const uint32_t gh = g0 + 32 * (k >> 1) + 8 * (k & 1), gl = gh + 16;
             if (PAIR) {
-#pragma unroll
-              for (int k = 0; k < kCH / 8; ++k) tc::mma_ts2_w(acc, gh + 8 * k, yh + 16 * k, id3c, k ? 1u : 0u);
-#pragma unroll
-              for (int k = 0; k < kCH / 8; ++k) tc::mma_ts2_w(acc, gl + 8 * k, yh + 16 * k, id3c, 1u);
+              tc::mma_ts2_f16_w(acc, gh, yh + 16 * k, id3c, k ? 1u : 0u);
+              tc::mma_ts2_f16_w(acc, gl, yh + 16 * k, id3c, 1u);
             } else if (kConcat) {
-#pragma unroll
-              for (int k = 0; k < kCH / 8; ++k) tc::mma_ts_w(acc, gh + 8 * k, yh + 16 * k, id3c, k ? 1u : 0u);
-#pragma unroll
-              for (int k = 0; k < kCH / 8; ++k) tc::mma_ts_w(acc, gl + 8 * k, yh + 16 * k, id3, 1u);
+              tc::mma_ts_f16_w(acc, gh, yh + 16 * k, id3c, k ? 1u : 0u);
+              tc::mma_ts_f16_w(acc, gl, yh + 16 * k, id3, 1u);
             } else {
-#pragma unroll
-              for (int t = 0; t < 3; ++t) {
-                const uint32_t ga = t == 2 ? gl : gh;
-                const uint64_t bb = t == 1 ? yl : yh;
-#pragma unroll
-                for (int k = 0; k < kCH / 8; ++k) tc::mma_ts_w(acc, ga + 8 * k, bb + 16 * k, id3, (t | k) ? 1u : 0u);
-              }
+              tc::mma_ts_f16_w(acc, gh, yh + 16 * k, id3, k ? 1u : 0u);
+              tc::mma_ts_f16_w(acc, gh, yl + 16 * k, id3, 1u);
+              tc::mma_ts_f16_w(acc, gl, yh + 16 * k, id3, 1u);
             }
           }
         }
@@ -649,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
         if (row_g < R.nrows_static) {
           double* o = R.mode == 0 ? R.out + (int64_t(blockIdx.y) * R.nrows_static + row_g) * NH : R.out + row_g * NH;
 #pragma unroll
-          for (int k = 0; k < NH; ++k) o[k] = acc[k];
+          for (int k = 0; k < NH; ++k) o[k] = BF ? acc[k] : acc[k] * double(__ldg(R.yinv + k));
         }
 #pragma unroll
         for (int k = 0; k < NH; ++k) acc[k] = 0.0;
@@ -689,46 +741,32 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
           v[2] = ex2(__uint_as_float(r[i + 2]));
           v[3] = ex2_poly(__uint_as_float(r[i + 3]));
         };
-        if (BF) {
-          uint32_t hi[16], lo[16];
-          auto half = [&](const uint32_t (&r)[16], int base) {
+        uint32_t hi[16], lo[16];
+        auto half = [&](const uint32_t (&r)[16], int base) {
 #pragma unroll
-            for (int i = 0; i < 16; i += 4) {
-              float v[4];
-              exps(r, i, v);
+          for (int i = 0; i < 16; i += 4) {
+            float v[4];
+            exps(r, i, v);
 #pragma unroll
-              for (int u = 0; u < 4; u += 2) {
+            for (int u = 0; u < 4; u += 2) {
+              if (BF) {
                 const uint32_t h = pack_bf16x2(v[u], v[u + 1]);
                 const float e0 = v[u] - __uint_as_float(h << 16), e1 = v[u + 1] - __uint_as_float(h & 0xFFFF0000u);
                 hi[base + (i + u) / 2] = h;
                 lo[base + (i + u) / 2] = pack_bf16x2(e0, e1);
+              } else {
+                const __half2 h = __floats2half2_rn(v[u], v[u + 1]);
+                const float2 hf = __half22float2(h);
+                hi[base + (i + u) / 2] = h2u(h);
+                lo[base + (i + u) / 2] = h2u(__floats2half2_rn(v[u] - hf.x, v[u + 1] - hf.y));
               }
             }
-          };
-          half(r0, 0);
-          half(r1, 8);
-          tc::st16(dcol, hi);
-          tc::st16(dcol + 16, lo);
-        } else {
-          auto half = [&](const uint32_t (&r)[16], uint32_t col) {
-            uint32_t hi[16], lo[16];
-#pragma unroll
-            for (int i = 0; i < 16; i += 4) {
-              float v[4];
-              exps(r, i, v);
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const float h = tc::tf32_hi(v[u]);
-                hi[i + u] = __float_as_uint(h);
-                lo[i + u] = __float_as_uint(v[u] - h);
-              }
-            }
-            tc::st16(col, hi);
-            tc::st16(col + kCH, lo);
-          };
-          half(r0, dcol);
-          half(r1, dcol + 16);
-        }
+          }
+        };
+        half(r0, 0);
+        half(r1, 8);
+        tc::st16(dcol, hi);
+        tc::st16(dcol + 16, lo);
         tc::st_wait();
       }
       tc::fence_before();
@@ -769,20 +807,6 @@ __global__ void rt_pair_reduce_kernel(const double* __restrict__ part, int ns, i
 // rt_pair_dz_kernel: one thread per (a, q) walks its pairs in a fixed order.
 // rt_pair_dl_kernel: block k < Q sums dl_k, block Q sums dvar (fixed-order tree).
 // Together they write one backward partial row [dvar, dl (Q), dz (a + q M)].
-struct PairIdx {
-  int m;
-  __device__ int64_t start(int a) const { return int64_t(a) * m - int64_t(a) * (a - 1) / 2; }
-  __device__ int64_t of(int a, int b) const { return start(a) + (b - a); }  // a <= b
-  __device__ void inv(int64_t p, int& a, int& b) const {                     // m1-major upper triangle
-    const double t = 2.0 * m + 1.0;
-    int x = int((t - sqrt(t * t - 8.0 * double(p))) * 0.5);
-    x = x < 0 ? 0 : (x >= m ? m - 1 : x);
-    while (x + 1 < m && start(x + 1) <= p) ++x;
-    while (x > 0 && start(x) > p) --x;
-    a = x;
-    b = int(p - start(x)) + x;
-  }
-};
 
 template <int Q>
 __global__ void rt_pair_dz_kernel(PsiConst P, const float* __restrict__ u, const double* __restrict__ sums,
@@ -951,7 +975,7 @@ float* floats_at(double* base, int64_t off_doubles) {
 struct BwdLayout {  // inside the backward scratch (offsets in doubles)
   int grid, epi_blocks;
   int64_t ntiles, pchunks;
-  int64_t off_t, off_dl, off_floats, doubles;
+  int64_t off_t, off_dl, off_ys, off_floats, doubles;
 };
 
 BwdLayout bwd_layout(const PsiConst& P, int num_sms) {
@@ -964,7 +988,8 @@ BwdLayout bwd_layout(const PsiConst& P, int num_sms) {
   L.epi_blocks = int(std::max<int64_t>(1, std::min<int64_t>((P.n + 255) / 256, int64_t(num_sms) * 4)));
   L.off_t = 0;
   L.off_dl = L.off_t + std::max<int64_t>(P.n, 1) * (2 * q + 1);
-  L.off_floats = (L.off_dl + int64_t(L.epi_blocks) * q + 1) / 2 * 2 + 2;
+  L.off_ys = L.off_dl + int64_t(L.epi_blocks) * q;  // 128 floats: yscale[64], yinv[64]
+  L.off_floats = (L.off_ys + 64 + 1) / 2 * 2 + 2;
   const int64_t pf = rt_pf(q, false, false);
   L.doubles = L.off_floats + ((pad_rows(npairs) / kCH) * pf + 1) / 2 + 4;
   return L;
@@ -1083,9 +1108,11 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
   float* pre = floats_at(bbase, L.off_floats);
   const int blocks_p = int(std::min<int64_t>((F.p_pad + 255) / 256, int64_t(num_sms) * 8));
   const bool pair = use_pair(Q, false);
-  if (pair) rt_pair_pre_kernel<Q, true><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, pre);
-  else rt_pair_pre_kernel<Q, false><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, pre);
-  g_tc_launches.fetch_add(1);
+  float* ys = reinterpret_cast<float*>(bbase + L.off_ys);
+  rt_yscale_kernel<Q><<<1, 256, 0, st>>>(P, B.u, ys);
+  if (pair) rt_pair_pre_kernel<Q, true><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, ys, pre);
+  else rt_pair_pre_kernel<Q, false><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, ys, pre);
+  g_tc_launches.fetch_add(2);
   if (P.n > 0) {
     RowTileArgs R{};
     R.a_hi = ff + F.f_hh;
@@ -1097,6 +1124,7 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
     R.cps = L.pchunks;
     R.nrows_static = P.n;
     R.out = bbase + L.off_t;
+    R.yinv = ys + 64;
     if constexpr (RT<Q, false, true>::kConcat) {
       if (pair) {
         const int64_t units = (L.ntiles + 1) / 2;

@@ -38,6 +38,11 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
 }
 
+// Instruction descriptor: D f32, A/B fp16 (kind::f16), both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_f16(int m, int n) {
+  return (1u << 4) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
+
 // Instruction descriptor: D f32, A/B tf32, both K-major, M x N.
 __host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
@@ -161,6 +166,13 @@ __device__ __forceinline__ void mma_ts2_f16_w(uint32_t d, uint32_t a, uint64_t b
                "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
                "r"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// shared -> TMEM copy of a canonical K-major [128 x 8 u32] block (lane = row), warp-uniform;
+// executes in issue order with this thread's tcgen05.mma
+__device__ __forceinline__ void cp_128x256b_w(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+               "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n\t}" ::"r"(taddr),
+               "l"(sdesc));
+}
 __device__ __forceinline__ void commit_w(uint64_t* mbar) {
   asm volatile("{\n\t.reg .pred e;\n\t" SGPX_ELECT
                "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
@@ -261,6 +273,9 @@ __device__ __forceinline__ void bulk_g2s_w(void* dst_smem, const void* src_gmem,
 // Named barrier over `count` threads (multiple of 32).
 __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 // ---- TMEM <-> registers (32x32b shapes: thread i of the warp <-> lane base+i) ----------------
