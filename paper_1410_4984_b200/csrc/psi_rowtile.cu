@@ -2,13 +2,14 @@
 //
 // Reference: psi_stats.hpp:221-326 (pair blocks of the psi2 sweep and their adjoints).
 // In log2 units, with mu and z translated by the mean of Z, every psi2 exponent
-// is a bilinear form of a pair feature row F_p and a datapoint feature row H_n (p = (a <= b)):
+// is a bilinear form of a pair feature row F_p and a datapoint feature row H_n (p = (a <= b)),
+// written in lengthscale units so that every feature is O(1) for O(l) data:
 //
 //   log2 v_pn = F_p . H_n
-//   F_p = [zb_q (Q), zb_q^2 (Q), C_ab, 1],            zb = (z_a + z_b) / 2,
-//                                                     C_ab = -(log2e/4) sum_q (z_aq - z_bq)^2 / l_q^2
-//   H_n = [2 L d2 mu (Q), -L d2 (Q), 1, B_n],         d2 = 1 / (2 S + l^2), L = log2e,
-//                                                     B_n = 2 log2 var - sum_q [log2(1 + 2S/l^2)/2 + L d2 mu^2]
+//   F_p = [zb_q / l_q (Q), (zb_q / l_q)^2 (Q), C_ab, 1],   zb = (z_a + z_b) / 2,
+//                                                        C_ab = -(log2e/4) sum_q (z_aq - z_bq)^2 / l_q^2
+//   H_n = [2 L (mu_q / l_q) / t_q (Q), -L / t_q (Q), 1, B_n],   t = 1 + 2 S / l^2 = 1 / (d2 l^2),
+//         L = log2e,  B_n = 2 log2 var - sum_q [log2(t_q)/2 + L d2 mu^2]
 //
 // and every psi2 sum the bound and its gradient need is a second GEMM over the weights
 // G = v (fp32 hi/lo in TMEM):
@@ -22,8 +23,10 @@
 // ring of streamed 96-row chunks (B of MMA1 + B of MMA3, fed by 1D TMA bulk copies), MMA1 into a
 // double-buffered TMEM stage, 12 consumer warps turning D into G = 2^D (MUFU.EX2 + an FMA-pipe
 // polynomial) stored back to TMEM as tf32 hi/lo, MMA3 with A = G read from TMEM, and the MMA3
-// accumulator drained into fp64 registers every chunk.  All GEMMs use 3xTF32 (hi*hi + hi*lo +
-// lo*hi), ~fp32 accuracy; every cross-chunk / cross-CTA sum is fp64 in a fixed order.
+// accumulator drained into fp64 registers every chunk.  Every GEMM is a 3-piece split
+// (hi*hi + hi*lo + lo*hi) of 16-bit pieces: MMA1 fp16 (~2^-22 relative, features clamped to the
+// fp16 range), MMA3 bf16 (forward) or scaled fp16 (backward); every cross-chunk / cross-CTA sum is
+// fp64 in a fixed order.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -53,7 +56,8 @@ constexpr int kWarpLoad = (kCons + kDrain) / 32;  // loader warp (16)
 constexpr int kWarpMma = kWarpLoad + 1;           // MMA warp (17)
 constexpr int kThreads = kCons + kDrain + 64;
 constexpr int kPadRows = 768;           // feature-array row padding: lcm(kCH, 2 x 128)
-constexpr float kNegHuge = -1.0e30f;    // B_n of padded datapoints: 2^(~-1e30) = 0
+constexpr float kNegHuge = -6.0e4f;     // B_n of padded datapoints (fp16-representable): 2^-6e4 = 0
+constexpr float kHalfMax = 6.0e4f;      // exponent features are clamped to the fp16 range
 
 // MMA3 operands G = 2^D and Y as 16-bit hi / lo pieces (G packed in place of D, kind::f16 with A
 // from TMEM, up to four D/G stages).  BF (forward): bf16 pieces, ~2^-17 relative.  !BF (backward):
@@ -66,16 +70,16 @@ constexpr float kNegHuge = -1.0e30f;    // B_n of padded datapoints: 2^(~-1e30) 
 // halves both the MMA instructions and the L2->SM operand traffic per SM.
 template <int Q, bool BF, bool PAIR = false>
 struct RT {
-  static constexpr int K1 = (2 * Q + 2 + 7) / 8 * 8;  // MMA1 depth
+  static constexpr int K1 = (2 * Q + 2 + 15) / 16 * 8;  // MMA1 depth in half2 words (K = 2 K1 halves)
   static constexpr int NH = 2 * Q + 1;                // MMA3 useful columns
   static constexpr int N3 = (NH + 15) / 16 * 16;      // MMA3 N
   static constexpr int XH = PAIR ? kCH / 2 : kCH;     // streamed X rows held by one CTA
-  static constexpr int XF = XH * K1;                  // floats of one X part (tf32 hi or lo)
+  static constexpr int XF = XH * K1;                  // words of one X part (fp16 hi or lo)
   static constexpr int YB = N3 * kCH;                 // elements of one Y^T part (hi or lo)
   static constexpr int YFl = YB / 2;                  // floats of one Y^T part (16-bit pieces)
   static constexpr int PF = 2 * XF + (PAIR ? 1 : 2) * YFl;  // floats per processed stage (per CTA)
   static constexpr int CHF = PAIR ? 2 * PF : PF;      // floats per streamed chunk in global memory
-  static constexpr int AF = 128 * K1;                 // floats of one static part (hi or lo)
+  static constexpr int AF = 128 * K1;                 // words of one static part (hi or lo)
   static constexpr int SW = kCH;                      // TMEM columns per D/G stage
   // MMA3 as G_hi * [Y_hi ; Y_lo] (N = 2 N3) + G_lo * Y_hi (N = N3; N = 2 N3 with [Y_hi ; Y_lo] in
   // PAIR mode) when the 2 N3-column accumulators fit next to the (at least 3, resp. 2) D/G
@@ -85,7 +89,7 @@ struct RT {
   static constexpr int kS = (512 - 2 * AccW) / SW >= 4 ? 4 : 3;  // D/G stages
 };
 
-__host__ __device__ constexpr int rt_k1(int q) { return (2 * q + 2 + 7) / 8 * 8; }
+__host__ __device__ constexpr int rt_k1(int q) { return (2 * q + 2 + 15) / 16 * 8; }
 __host__ __device__ constexpr int rt_n3(int q) { return (2 * q + 1 + 15) / 16 * 16; }
 // per-CTA processed stage floats
 __host__ __device__ constexpr int rt_pf(int q, bool bf, bool pair) {
@@ -137,29 +141,35 @@ __device__ __forceinline__ uint32_t h2u(__half2 h) {
   return uint32_t(__half_as_ushort(__low2half(h))) | (uint32_t(__half_as_ushort(__high2half(h))) << 16);
 }
 
-__device__ __forceinline__ void put_split(float* hi, float* lo, int off4, const float (&x)[4]) {
-  float h[4], l[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    h[u] = tc::tf32_hi(x[u]);
-    l[u] = x[u] - h[u];
-  }
-  *reinterpret_cast<float4*>(hi + off4) = make_float4(h[0], h[1], h[2], h[3]);
-  *reinterpret_cast<float4*>(lo + off4) = make_float4(l[0], l[1], l[2], l[3]);
-}
 
 // ---------------------------------------------------------------------------------------------
 // Feature builders (elementwise, HBM-bound)
 // ---------------------------------------------------------------------------------------------
 
-__device__ __forceinline__ void put_rows(float* hi, float* lo, int64_t r, const float* f, int K1) {
-  float* hb = hi + (r >> 3) * (K1 * 8);
-  float* lb = lo + (r >> 3) * (K1 * 8);
-  const int rr = int(r & 7);
+// fp16 hi / lo pieces of features k, k+1 packed as half2 words (low half = even k), clamped to the
+// fp16 range
+__device__ __forceinline__ void split_pair(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  x0 = fminf(fmaxf(x0, -kHalfMax), kHalfMax);
+  x1 = fminf(fmaxf(x1, -kHalfMax), kHalfMax);
+  const __half2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  hi = h2u(h);
+  lo = h2u(__floats2half2_rn(x0 - hf.x, x1 - hf.y));
+}
+// 2 K1 features of one row as K1 hi / lo words at word offset `row_off + (k / 4) * 32 + ...` of a
+// canonical K-major tile (core matrix = 8 rows x 4 words)
+__device__ __forceinline__ void put_feat_words(float* hi, float* lo, int row_off, const float* f, int K1) {
   for (int k = 0; k < K1; k += 4) {
-    const float x[4] = {f[k], f[k + 1], f[k + 2], f[k + 3]};
-    put_split(hb, lb, (k >> 2) * 32 + rr * 4, x);
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) split_pair(f[2 * (k + u)], f[2 * (k + u) + 1], h[u], l[u]);
+    *reinterpret_cast<uint4*>(hi + row_off + (k >> 2) * 32) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(lo + row_off + (k >> 2) * 32) = make_uint4(l[0], l[1], l[2], l[3]);
   }
+}
+__device__ __forceinline__ void put_rows(float* hi, float* lo, int64_t r, const float* f, int K1) {
+  const int64_t base = (r >> 3) * (K1 * 8);
+  put_feat_words(hi + base, lo + base, int(r & 7) * 4, f, K1);
 }
 
 // One row of a streamed chunk in the processed-stage layout (the MMA1 / MMA3 B operands): X row
@@ -173,11 +183,7 @@ __device__ __forceinline__ void put_pre_row(float* chunk, int jj, const float* x
   constexpr int K1 = C::K1, N3 = C::N3, XF = C::XF, YFl = C::YFl, PF = C::PF, XH = C::XH;
   float* xb = chunk + (PAIR ? (jj / XH) * PF : 0);
   const int r = jj % XH;
-#pragma unroll
-  for (int k = 0; k < K1; k += 4) {
-    const float x4[4] = {x[k], x[k + 1], x[k + 2], x[k + 3]};
-    put_split(xb, xb + XF, (r >> 3) * (K1 * 8) + (k >> 2) * 32 + (r & 7) * 4, x4);
-  }
+  put_feat_words(xb, xb + XF, (r >> 3) * (K1 * 8) + (r & 7) * 4, x, K1);
   float* y_hi = chunk + 2 * XF;                          // block 0 (or the single block)
   float* y_lo = PAIR ? chunk + PF + 2 * XF : y_hi + YFl;  // block 1 (or after Y_hi)
   if (BF) {  // Y^T as bf16 hi / lo, canonical K-major (rows = features, 8 bf16 per core-matrix row)
@@ -229,9 +235,9 @@ __global__ void __launch_bounds__(256) rt_pair_rows_kernel(PsiConst P, int64_t p
   const int m = P.m, qv = P.qv;
   const int64_t npairs = int64_t(m) * (m + 1) / 2;
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < p_pad; p += int64_t(gridDim.x) * blockDim.x) {
-    float f[K1];
+    float f[2 * K1];
 #pragma unroll
-    for (int k = 0; k < K1; ++k) f[k] = 0.f;
+    for (int k = 0; k < 2 * K1; ++k) f[k] = 0.f;
     if (p < npairs) {
       int a = 0;
       int64_t rem = p;
@@ -246,8 +252,9 @@ __global__ void __launch_bounds__(256) rt_pair_rows_kernel(PsiConst P, int64_t p
         if (q < P.q) {
           const float za = P.zc[a * qv + q], zb = P.zc[b * qv + q];
           const float zbar = 0.5f * (za + zb), dz = za - zb;
-          f[q] = zbar;
-          f[Q + q] = zbar * zbar;
+          const float zs = zbar * sqrtf(P.il2[q]);  // lengthscale units
+          f[q] = zs;
+          f[Q + q] = zs * zs;
           c = fmaf(P.il2[q] * dz, dz, c);
         }
       f[2 * Q] = -0.25f * kLog2e * c;
@@ -275,9 +282,9 @@ __global__ void __launch_bounds__(256) rt_data_rows_kernel(PsiConst P, int64_t n
       rs[q] = P.expected ? __ldg(P.s + qq * P.ld_s + nn) : 0.0;
     }
     constexpr int N3 = RT<Q, true>::N3;
-    float h[K1], y[N3];
+    float h[2 * K1], y[N3];
 #pragma unroll
-    for (int k = 0; k < K1; ++k) h[k] = 0.f;
+    for (int k = 0; k < 2 * K1; ++k) h[k] = 0.f;
 #pragma unroll
     for (int k = 0; k < N3; ++k) y[k] = 0.f;
     if (valid) {
@@ -290,8 +297,9 @@ __global__ void __launch_bounds__(256) rt_data_rows_kernel(PsiConst P, int64_t n
           const float il2 = P.il2[q];
           const float t = fmaf(2.f * sv, il2, 1.f);
           const float d2 = il2 / t;  // 1 / (2 S + l^2)
-          h[q] = 2.f * kLog2e * d2 * mu;
-          h[Q + q] = -kLog2e * d2;
+          const float it = 1.f / t;  // d2 l^2
+          h[q] = 2.f * kLog2e * (mu * sqrtf(il2)) * it;
+          h[Q + q] = -kLog2e * it;
           bsum = fmaf(-0.5f, log2f(t), fmaf(-kLog2e * d2 * mu, mu, bsum));
           y[1 + q] = d2 * mu;
           y[1 + Q + q] = d2;
@@ -361,9 +369,9 @@ __global__ void __launch_bounds__(256) rt_pair_pre_kernel(PsiConst P, const floa
   const int m = P.m, qv = P.qv, mv = P.mv;
   const int64_t npairs = int64_t(m) * (m + 1) / 2;
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < p_pad; p += int64_t(gridDim.x) * blockDim.x) {
-    float f[K1], y[N3];
+    float f[2 * K1], y[N3];
 #pragma unroll
-    for (int k = 0; k < K1; ++k) f[k] = 0.f;
+    for (int k = 0; k < 2 * K1; ++k) f[k] = 0.f;
 #pragma unroll
     for (int k = 0; k < N3; ++k) y[k] = 0.f;
     if (p < npairs) {
@@ -381,8 +389,9 @@ __global__ void __launch_bounds__(256) rt_pair_pre_kernel(PsiConst P, const floa
         if (q < P.q) {
           const float za = P.zc[a * qv + q], zb = P.zc[b * qv + q];
           const float zbar = 0.5f * (za + zb), dz = za - zb;
-          f[q] = zbar;
-          f[Q + q] = zbar * zbar;
+          const float zs = zbar * sqrtf(P.il2[q]);  // lengthscale units
+          f[q] = zs;
+          f[Q + q] = zs * zs;
           c = fmaf(P.il2[q] * dz, dz, c);
           y[1 + q] = w * zbar;
           y[1 + Q + q] = w * zbar * zbar;
@@ -550,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
     // The whole warp runs the issue loop (warp-uniform operands in uniform registers); elect.sync
     // inside each tcgen05 asm picks the issuing lane.
     {
-      const uint32_t id1 = tc::idesc_tf32(kM, kCH);
+      const uint32_t id1 = tc::idesc_f16(kM, kCH);
       // MMA1 runs kS chunks ahead of MMA3 (one per D/G stage): separate positions for the two
       RingPos a1 = ring(nA), p1 = ring(nP), s1 = ring(kS), p3 = ring(nP), s3 = ring(kS), c3 = ring(2);
       int64_t j1 = 0;
@@ -573,8 +582,8 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
 #pragma unroll
           for (int ks = 0; ks < KS1; ++ks) {
             if (R.dbg & 4) continue;
-            if (PAIR) tc::mma_ss2_w(d, aa + 16 * ks, bb + 16 * ks, id1, (t | ks) ? 1u : 0u);
-            else tc::mma_ss_w(d, aa + 16 * ks, bb + 16 * ks, id1, (t | ks) ? 1u : 0u);
+            if (PAIR) tc::mma_ss2_f16_w(d, aa + 16 * ks, bb + 16 * ks, id1, (t | ks) ? 1u : 0u);
+            else tc::mma_ss_f16_w(d, aa + 16 * ks, bb + 16 * ks, id1, (t | ks) ? 1u : 0u);
           }
         }
         commit_x(&d_full[s1.slot]);
