@@ -22,7 +22,7 @@
 // Both passes are one kernel template: a static 128-row tile (A of MMA1) in shared memory, a
 // ring of streamed 96-row chunks (B of MMA1 + B of MMA3, fed by 1D TMA bulk copies), MMA1 into a
 // double-buffered TMEM stage, 12 consumer warps turning D into G = 2^D (MUFU.EX2 + an FMA-pipe
-// polynomial) stored back to TMEM as tf32 hi/lo, MMA3 with A = G read from TMEM, and the MMA3
+// polynomial) stored back to TMEM as 16-bit hi/lo pairs, MMA3 with A = G read from TMEM, and the MMA3
 // accumulator drained into fp64 registers every chunk.  Every GEMM is a 3-piece split
 // (hi*hi + hi*lo + lo*hi) of 16-bit pieces: MMA1 fp16 (~2^-22 relative, features clamped to the
 // fp16 range), MMA3 bf16 (forward) or scaled fp16 (backward); every cross-chunk / cross-CTA sum is
@@ -595,11 +595,10 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
           j1 = 0;
         }
       };
-      // bf16 G of stage s: consumer group g stored datapoints [32 g, 32 g + 32) as bf16x2 hi in
-      // columns [32 g, 32 g + 16) and lo in [32 g + 16, 32 g + 32); K-step k (16 datapoints) of hi
-      // is at column 32 (k / 2) + 8 (k % 2), lo 16 columns further.  tf32 G: hi in place of D,
-      // lo kCH columns further, K-step k (8 datapoints) at column 8 k.  In PAIR mode each CTA
-      // holds one half of [Y_hi ; Y_lo] at the same offset, so both passes use N = 2 N3.
+      // G of stage s (bf16 or fp16 pieces): consumer group g stored datapoints [32 g, 32 g + 32) as
+      // 16-bit pairs, hi in columns [32 g, 32 g + 16) and lo in [32 g + 16, 32 g + 32); K-step k (16
+      // datapoints) of hi is at column 32 (k / 2) + 8 (k % 2), lo 16 columns further.  In PAIR mode
+      // each CTA holds one half of [Y_hi ; Y_lo] at the same offset, so both passes use N = 2 N3.
       auto mma3 = [&](int64_t c) {
         wait_x(&g_full[s3.slot], s3.phase);
         if (c >= 2) wait_x(&c_empty[c3.slot], c3.phase ^ 1u);
@@ -723,7 +722,7 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
         for (int k = 0; k < NH; ++k) R.out[(int64_t(blockIdx.y) * R.nrows_static + row_g) * NH + k] = 0.0;
     }
   } else {
-    // ---------------- consumers: G = 2^D, stored back as hi / lo (bf16x2 in place, or tf32) ----------------
+    // ---------------- consumers: G = 2^D, stored back in place as bf16x2 / fp16x2 hi / lo ----------------
     const int g = warp >> 2, quarter = warp & 3;
     const uint32_t lane_off = uint32_t(32 * quarter) << 16;
     RingPos sd = ring(kS);
