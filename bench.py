@@ -338,7 +338,7 @@ def run_b200(args, world, rank, local_rank):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
-            "vs_baseline": None, "dtype": "f32-equivalent: 3xTF32 / bf16x2-split tcgen05 MMAs, fp32 exp2, fp64 accumulation and M-sized algebra",
+            "vs_baseline": None, "dtype": "f32-equivalent: 3-piece fp16 / bf16 split tcgen05 MMAs (~2^-22 / 2^-17 rel.), fp32 exp2, fp64 accumulation and M-sized algebra",
             "data": "synthetic (torch Philox seed 0: mu,Y ~ N(0,1), S=0.5, Z = M rows of mu; var=l=1, beta=100)",
             "config": {"workload": desc, "N": n_global, "Q": q, "D": d, "M": m, "n_local": n_local,
                        "parallelism": f"dp{world}", "l2": "inputs 560 MB > L2 and 256 MB L2 flush before each "
@@ -348,7 +348,7 @@ def run_b200(args, world, rank, local_rank):
                          "traffic": traffic, "peak_source": t_src,
                          "flops_per_launch": n_local * (fwd_flops + bwd_flops), "avg_launch_ms": (fwd_s + bwd_s) * 1e3,
                          "work": "SURVEY.md 8(d) algorithmic FP32-class flops P(15Q+7)+M(15Q+4D+6) per datapoint "
-                                 "(FMA = 2), executed as 3xTF32 / bf16x2 tcgen05 MMAs + MUFU/FMA exp2",
+                                 "(FMA = 2), executed as 3-piece fp16 / bf16 split tcgen05 MMAs + MUFU/FMA exp2",
                          "fp32_simt": {"peak": PEAK_FP32_TFLOPS, "frac": psi_tf / PEAK_FP32_TFLOPS,
                                        "note": "SURVEY 8(d) FP32-FMA roofline; > 1 means beyond a SIMT design"},
                          "fwd": {"achieved": fwd_tf, "avg_launch_ms": fwd_s * 1e3, "flops_per_launch": n_local * fwd_flops},

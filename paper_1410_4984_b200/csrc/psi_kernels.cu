@@ -453,12 +453,32 @@ __global__ void __launch_bounds__(512)
   }
 }
 
+// Fixed-order column sums of nparts partial rows: a block covers 32 columns with 8 warps, warp w
+// summing rows w, w + 8, ... (coalesced across the columns), then the 8 partial sums in order.
+// Launch with 256 threads and ceil(count / 32) blocks.
+__device__ __forceinline__ bool colsum8(const double* __restrict__ part, int64_t pstride, int nparts, int64_t count,
+                                        int64_t& k, double& sum) {
+  __shared__ double red[8][32];
+  const int kk = threadIdx.x & 31, w = threadIdx.x >> 5;
+  k = int64_t(blockIdx.x) * 32 + kk;
+  double s = 0.0;
+  if (k < count)
+    for (int c = w; c < nparts; c += 8) s += part[c * pstride + k];
+  red[w][kk] = s;
+  __syncthreads();
+  if (w != 0 || k >= count) return false;
+  sum = red[0][kk];
+  for (int i = 1; i < 8; ++i) sum += red[i][kk];
+  return true;
+}
+
 // Fixed-order reduction of the per-CTA forward partials into the packed stats vector.
-__global__ void fwd_reduce_kernel(const double* __restrict__ part, int64_t pstride, int nparts, int64_t count,
-                                  double* __restrict__ packed, double phi_val, double n_count) {
-  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < count; k += int64_t(gridDim.x) * blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < nparts; ++c) s += part[c * pstride + k];
+__global__ void __launch_bounds__(256) fwd_reduce_kernel(const double* __restrict__ part, int64_t pstride, int nparts,
+                                                         int64_t count, double* __restrict__ packed, double phi_val,
+                                                         double n_count) {
+  int64_t k;
+  double s;
+  if (colsum8(part, pstride, nparts, count, k, s)) {
     if (k == 0)
       packed[1] = s;
     else if (k == 1)
@@ -472,13 +492,11 @@ __global__ void fwd_reduce_kernel(const double* __restrict__ part, int64_t pstri
   }
 }
 
-__global__ void bwd_reduce_kernel(const double* __restrict__ part, int64_t pstride, int nparts, int64_t count,
-                                  double* __restrict__ packed, double dvar0) {
-  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < count; k += int64_t(gridDim.x) * blockDim.x) {
-    double s = (k == 0) ? dvar0 : 0.0;
-    for (int c = 0; c < nparts; ++c) s += part[c * pstride + k];
-    packed[k] = s;
-  }
+__global__ void __launch_bounds__(256) bwd_reduce_kernel(const double* __restrict__ part, int64_t pstride, int nparts,
+                                                         int64_t count, double* __restrict__ packed, double dvar0) {
+  int64_t k;
+  double s;
+  if (colsum8(part, pstride, nparts, count, k, s)) packed[k] = (k == 0 ? dvar0 : 0.0) + s;
 }
 
 template <int Q>
@@ -578,7 +596,7 @@ int launch_fwd(const PsiConst& P, double* part, double* packed, int* err_flag, i
     if (e1) cudaEventRecord(e1, st);
     g_launches.fetch_add(1);
   }
-  fwd_reduce_kernel<<<int((pstride + 255) / 256), 256, 0, st>>>(part, pstride, g.grid, pstride, packed,
+  fwd_reduce_kernel<<<int((pstride + 31) / 32), 256, 0, st>>>(part, pstride, g.grid, pstride, packed,
                                                                  double(P.n) * P.variance_d, double(P.n));
   g_launches.fetch_add(1);
   if (geom) *geom = g;
@@ -599,7 +617,7 @@ int launch_bwd(const PsiConst& P, const BwdConst& B, double* part, double* packe
     if (e1) cudaEventRecord(e1, st);
     g_launches.fetch_add(1);
   }
-  bwd_reduce_kernel<<<int((pstride + 255) / 256), 256, 0, st>>>(part, pstride, g.grid, pstride, packed,
+  bwd_reduce_kernel<<<int((pstride + 31) / 32), 256, 0, st>>>(part, pstride, g.grid, pstride, packed,
                                                                  B.d_phi * double(P.n));
   g_launches.fetch_add(1);
   if (geom) *geom = g;
@@ -672,7 +690,7 @@ int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, 
     if (g1 > 0) {
       if (int rc = psi1_forward(P, part, pstride, g1, err_flag, stream, 1)) return rc;
     }
-    fwd_reduce_kernel<<<int((pstride + 255) / 256), 256, 0, st>>>(part, pstride, g1, pstride, packed,
+    fwd_reduce_kernel<<<int((pstride + 31) / 32), 256, 0, st>>>(part, pstride, g1, pstride, packed,
                                                                    double(P.n) * P.variance_d, double(P.n));
     g_launches.fetch_add(1);
     if (int rc = rt_forward(P, part + int64_t(g1) * pstride, packed, num_sms, stream)) return rc;

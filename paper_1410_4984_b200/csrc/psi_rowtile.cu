@@ -916,14 +916,22 @@ __global__ void __launch_bounds__(256) rt_bwd_epilogue_kernel(PsiConst P, BwdCon
   }
 }
 
-// sum of the per-block dl rows into the partial row (fixed order)
-__global__ void rt_dl_reduce_kernel(const double* __restrict__ dl_rows, int rows, int qpad, int q,
-                                    double* __restrict__ row) {
-  const int k = threadIdx.x;
-  if (k < q) {
+// sum of the per-block dl rows into the partial row: one block, thread t sums rows t, t + 256, ...
+// of every column, then a fixed tree (deterministic)
+__global__ void __launch_bounds__(256) rt_dl_reduce_kernel(const double* __restrict__ dl_rows, int rows, int qpad, int q,
+                                                           double* __restrict__ row) {
+  __shared__ double red[256];
+  for (int k = 0; k < q; ++k) {
     double s = 0.0;
-    for (int i = 0; i < rows; ++i) s += dl_rows[int64_t(i) * qpad + k];
-    row[1 + k] += s;
+    for (int i = threadIdx.x; i < rows; i += 256) s += dl_rows[int64_t(i) * qpad + k];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) row[1 + k] += red[0];
+    __syncthreads();
   }
 }
 
@@ -1151,7 +1159,7 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
   }
   if (P.n > 0) {
     rt_bwd_epilogue_kernel<Q><<<L.epi_blocks, 256, 0, st>>>(P, B, bbase + L.off_t, bbase + L.off_dl);
-    rt_dl_reduce_kernel<<<1, 32, 0, st>>>(bbase + L.off_dl, L.epi_blocks, Q, P.q, prow);
+    rt_dl_reduce_kernel<<<1, 256, 0, st>>>(bbase + L.off_dl, L.epi_blocks, Q, P.q, prow);
     g_tc_launches.fetch_add(2);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 3;

@@ -284,6 +284,7 @@ struct sgpx_engine {
   // coordinator results of the current evaluation
   coord::Result res;
   bool coordinated = false, with_grads = false;
+  bool pairs_folded = false;  // sub-shard pair sums folded into the first (once per forward)
   cudaEvent_t ev[8] = {};  // 0-1 stats pass, 2-3 grad pass, 4-5 fwd kernel, 6-7 bwd kernel
   double coord_s = 0.0;
   LaunchGeom gf{}, gb{};
@@ -324,13 +325,26 @@ __global__ void sum_parts_kernel(const double* __restrict__ parts, int k, int64_
   }
 }
 
+// dst[i] += src[i] (sub-shard pair sums folded into the first, in sub-shard order)
+__global__ void add_into_kernel(double* __restrict__ dst, const double* __restrict__ src, int64_t count) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] += src[i];
+}
+
 // Sub-shard plan: one piece when the shard is device resident (nothing to overlap; every split
 // costs kernel efficiency), else up to 4 pieces (>= 250k rows each) so the host transfers of one
 // overlap the kernels of the others; boundaries on multiples of 384 rows (feature tile grain).
 void plan_subs(sgpx_engine* e) {
   const int64_t n = e->in.n;
   const bool transfers = e->pending_upload || (e->has_gout && e->latent);
-  const int k = !transfers ? 1 : (n >= 1000000 ? 4 : (n >= 500000 ? 2 : 1));
+  int k = !transfers ? 1 : (n >= 1000000 ? 4 : (n >= 500000 ? 2 : 1));
+  if (transfers) {
+    static const int forced = [] {  // SGPX_SUBS: sub-shard count override (pipeline experiments)
+      const char* v = getenv("SGPX_SUBS");
+      return v ? atoi(v) : 0;
+    }();
+    if (forced > 0) k = int(std::min<int64_t>(forced, std::max<int64_t>(1, n / 384)));
+  }
   e->subs.clear();
   const int64_t step = (n / k + 383) / 384 * 384;
   for (int64_t n0 = 0; n0 < n || (n == 0 && e->subs.empty()); n0 += step) {
@@ -360,6 +374,7 @@ void engine_stats_pass(sgpx_engine* e) {
   require(e->has_data && e->has_params, "engine: set_data and broadcast must precede evaluate");
   sgpx_ctx* ctx = e->ctx;
   const int64_t count = sgpx_packed_stats_count(e->cfg.m, e->cfg.d);
+  e->pairs_folded = false;
   e->pstats.ensure(sizeof(double) * count);
   e->err.ensure(sizeof(int));
   CUDA_OK(cudaMemsetAsync(e->err.p, 0, sizeof(int), ctx->stream));
@@ -462,6 +477,26 @@ void engine_grad_pass(sgpx_engine* e) {
     }
     e->bpart.ensure(sizeof(double) * boff);
     if (k > 1) e->pgrads_sub.ensure(sizeof(double) * count * k);
+    // the per-pair gradient terms are linear in the forward pair sums: fold every sub-shard's sums
+    // into the first and add the terms once (row-tile path)
+    const bool fold = k > 1 && use_rt(e->subs[0].P);
+    if (fold && !e->pairs_folded) {
+      e->pairs_folded = true;
+      int64_t np = 0;
+      auto sums = [&](int j, int64_t* n) {
+        const auto& sj = e->subs[j];
+        double* region = const_cast<double*>(rt_fwd_region(sj.P, e->fpart.get<double>() + sj.foff, ctx->num_sms));
+        return rt_fwd_pair_sums(sj.P, region, ctx->num_sms, n);
+      };
+      double* s0 = sums(0, &np);
+      for (int j = 1; j < k; ++j) {
+        int64_t nj = 0;
+        const double* sj = sums(j, &nj);
+        if (nj != np) throw CudaError("sub-shard pair sums differ in size");
+        add_into_kernel<<<int(std::min<int64_t>((np + 255) / 256, 1024)), 256, 0, ctx->stream>>>(s0, sj, np);
+      }
+      CUDA_OK(cudaGetLastError());
+    }
     const bool stream_out = e->has_gout && e->latent;
     for (int j = 0; j < k; ++j) {
       auto& sub = e->subs[j];
@@ -475,6 +510,7 @@ void engine_grad_pass(sgpx_engine* e) {
       B.d_s = e->ds.get<double>() + sub.n0;
       B.ld_g = e->in.n;
       B.fwd_rt = rt_fwd_region(sub.P, e->fpart.get<double>() + sub.foff, ctx->num_sms);
+      B.skip_pair_terms = (fold && j > 0) ? 1 : 0;
       double* out = k > 1 ? e->pgrads_sub.get<double>() + int64_t(j) * count : e->pgrads.get<double>();
       if (psi_backward(sub.P, B, e->bpart.get<double>() + sub.boff, out, ctx->num_sms, ctx->stream, &e->gb,
                        j == 0 ? e->ev[6] : nullptr, j == k - 1 ? e->ev[7] : nullptr))
