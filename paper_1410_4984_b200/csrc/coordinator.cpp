@@ -168,8 +168,19 @@ Mat chol_inverse(const Mat& L) {
     const double* wj = W.col(j);
     for (int64_t i = j; i < n; ++i) {
       const double* wi = W.col(i);
-      double s = 0.0;
-      for (int64_t k = i; k < n; ++k) s += wi[k] * wj[k];  // rows k >= max(i, j) = i
+      // rows k >= max(i, j) = i; four vector accumulators over k in a fixed order
+      int64_t k = i;
+      v4d a0 = {0, 0, 0, 0}, a1 = a0, a2 = a0, a3 = a0;
+      for (; k + 16 <= n; k += 16) {
+        a0 += load4(wi + k) * load4(wj + k);
+        a1 += load4(wi + k + 4) * load4(wj + k + 4);
+        a2 += load4(wi + k + 8) * load4(wj + k + 8);
+        a3 += load4(wi + k + 12) * load4(wj + k + 12);
+      }
+      for (; k + 4 <= n; k += 4) a0 += load4(wi + k) * load4(wj + k);
+      const v4d t = (a0 + a1) + (a2 + a3);
+      double s = (t[0] + t[1]) + (t[2] + t[3]);
+      for (; k < n; ++k) s += wi[k] * wj[k];
       X(i, j) = s;
       X(j, i) = s;
     }
