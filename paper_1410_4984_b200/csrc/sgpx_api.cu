@@ -332,31 +332,61 @@ __global__ void add_into_kernel(double* __restrict__ dst, const double* __restri
 }
 
 // Sub-shard plan: one piece when the shard is device resident (nothing to overlap; every split
-// costs kernel efficiency), else up to 4 pieces (>= 250k rows each) so the host transfers of one
-// overlap the kernels of the others; boundaries on multiples of 384 rows (feature tile grain).
+// costs kernel efficiency), else weighted pieces with boundaries on multiples of 384 rows (feature
+// tile grain) so the host transfers of one piece overlap the kernels of the others.
+// Sub-shard weights: transfers overlap the kernels of the neighbouring pieces, so small first and
+// last pieces shorten the pipeline fill (first upload) and drain (last read-back).
+std::vector<double> sub_weights(int64_t n, bool transfers) {
+  if (!transfers) return {1.0};
+  if (const char* v = getenv("SGPX_SUBS")) {  // override (pipeline experiments): "k" or "w1,w2,..."
+    std::vector<double> w;
+    std::string str(v);
+    size_t pos = 0;
+    while (pos <= str.size()) {
+      const size_t nx = str.find(',', pos);
+      const std::string tok = str.substr(pos, nx == std::string::npos ? std::string::npos : nx - pos);
+      if (!tok.empty()) w.push_back(atof(tok.c_str()));
+      if (nx == std::string::npos) break;
+      pos = nx + 1;
+    }
+    if (w.size() == 1 && w[0] >= 1.0) w.assign(size_t(w[0]), 1.0);
+    bool ok = !w.empty();
+    for (double x : w) ok = ok && x > 0.0;
+    if (ok) return w;
+  }
+  if (n >= 1000000) return {1.0, 1.5, 2.0, 2.0, 1.5, 1.0};  // measured best at C3 (tools/e2e_timeline.py)
+  if (n >= 500000) return {1.0, 1.0};
+  return {1.0};
+}
+
 void plan_subs(sgpx_engine* e) {
   const int64_t n = e->in.n;
   const bool transfers = e->pending_upload || (e->has_gout && e->latent);
-  int k = !transfers ? 1 : (n >= 1000000 ? 4 : (n >= 500000 ? 2 : 1));
-  if (transfers) {
-    static const int forced = [] {  // SGPX_SUBS: sub-shard count override (pipeline experiments)
-      const char* v = getenv("SGPX_SUBS");
-      return v ? atoi(v) : 0;
-    }();
-    if (forced > 0) k = int(std::min<int64_t>(forced, std::max<int64_t>(1, n / 384)));
-  }
+  std::vector<double> w = sub_weights(n, transfers);
+  // at least 384 rows (the feature tile grain) per piece
+  while (w.size() > 1 && int64_t(w.size()) * 384 > n) w.pop_back();
+  double wsum = 0.0;
+  for (double x : w) wsum += x;
   e->subs.clear();
-  const int64_t step = (n / k + 383) / 384 * 384;
-  for (int64_t n0 = 0; n0 < n || (n == 0 && e->subs.empty()); n0 += step) {
+  int64_t n0 = 0;
+  double acc = 0.0;
+  for (size_t j = 0; j < w.size() || (n == 0 && e->subs.empty()); ++j) {
+    int64_t n1 = n;
+    if (j + 1 < w.size()) {
+      acc += w[j];
+      n1 = std::min<int64_t>(n, (int64_t(double(n) * acc / wsum) + 383) / 384 * 384);
+    }
+    if (n1 <= n0 && n > 0) continue;
     sgpx_engine::Sub sub;
     sub.n0 = n0;
-    sub.n = std::min(step, n - n0);
+    sub.n = n1 - n0;
     sub.P = e->P;
     sub.P.n = sub.n;
     sub.P.mu = e->P.mu + n0;
     sub.P.s = e->P.s ? e->P.s + n0 : nullptr;
     sub.P.y = e->P.y + n0;
     e->subs.push_back(sub);
+    n0 = n1;
     if (n == 0) break;
   }
   const size_t need = e->subs.size();
