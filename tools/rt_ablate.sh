@@ -1,7 +1,8 @@
 #!/bin/bash
 # Row-tile kernel durations (forward, backward) under SGPX_RT_DBG timing experiments:
-#   1 G = 0 stores only (no TMEM loads / exp2), 2 skip MMA3, 4 skip MMA1, 8 no exp2 math,
-#   16 no operand streaming, 32 drain without TMEM loads.   usage: tools/rt_ablate.sh 0 1 2 ...
+#   1 skip the G math, 2 skip MMA3, 4 skip MMA1, 8 TMEM traffic without the exp2 math
+#   (1/4/8 leave non-finite statistics, so only the kernels before the failing step are timed).
+#   usage: tools/rt_ablate.sh 0 2 3 ...
 cd "$(dirname "$0")/.."
 for d in "$@"; do
   t=$(SGPX_RT_DBG=$d ncu --metrics gpu__time_duration.sum --clock-control none -k regex:rowtile --csv \
