@@ -271,7 +271,7 @@ Stats unpack_stats(const double* p, int64_t m, int64_t d) {
 }
 
 Result coordinate(bool latent, int64_t n, int64_t d, const Stats& st, const Mat& z, const Kernel& k, double beta,
-                  double jitter_factor, bool with_adjoints) {
+                  double jitter_factor, bool with_adjoints, bool defer_host_only) {
   const int64_t m = z.r;
   require(beta > 0.0 && std::isfinite(beta), "bound: beta must be positive");
   require(n >= 1 && d >= 1, "bound: need N >= 1 and D >= 1");
@@ -321,6 +321,27 @@ Result coordinate(bool latent, int64_t n, int64_t d, const Stats& st, const Mat&
   adj.d_phi_big = Mat(m, m);
   for (size_t i = 0; i < ggt.v.size(); ++i)
     adj.d_phi_big.v[i] = -0.5 * beta * dd * a_inv.v[i] - 0.5 * beta * beta * beta * ggt.v[i] + 0.5 * beta * dd * kmm_inv.v[i];
+  r.kmm_inv = kmm_inv;
+  r.a_inv = a_inv;
+  r.g = g;
+  r.ggt = ggt;
+  r.ap = ap;
+  r.kp = kp;
+  r.pg = pg;
+  r.deferred = true;
+  if (!defer_host_only) complete_adjoints(r, st, n, d, beta);
+  return r;
+}
+
+void complete_adjoints(Result& r, const Stats& st, int64_t n, int64_t d, double beta) {
+  if (!r.deferred) return;
+  const int64_t m = r.g.r;
+  const double nd = double(n), dd = double(d);
+  const Mat& kmm_inv = r.kmm_inv;
+  const Mat& a_inv = r.a_inv;
+  const Mat& g = r.g;
+  const Mat& ggt = r.ggt;
+  Adjoints& adj = r.adj;
   Mat kpk = gemm(gemm(kmm_inv, false, st.phi_big, false), false, kmm_inv, false);
   symmetrize(kpk);
   adj.d_kmm = Mat(m, m);
@@ -331,9 +352,13 @@ Result coordinate(bool latent, int64_t n, int64_t d, const Stats& st, const Mat&
   for (size_t i = 0; i < g.v.size(); ++i) tr_gphig += g.v[i] * phig.v[i];
   // d_beta: the sum of the workers' beta_share (parallel.hpp:185-195) equals this
   // global expression (bound.hpp:217-223) evaluated on the reduced statistics.
-  adj.d_beta = 0.5 * dd * nd / beta - 0.5 * dd * ap - 0.5 * st.yy + beta * pg - 0.5 * beta * beta * tr_gphig -
-               0.5 * dd * st.phi + 0.5 * dd * kp;
-  return r;
+  adj.d_beta = 0.5 * dd * nd / beta - 0.5 * dd * r.ap - 0.5 * st.yy + beta * r.pg - 0.5 * beta * beta * tr_gphig -
+               0.5 * dd * st.phi + 0.5 * dd * r.kp;
+  r.deferred = false;
+  r.kmm_inv = Mat();
+  r.a_inv = Mat();
+  r.g = Mat();
+  r.ggt = Mat();
 }
 
 KernGrads kern_grads_zz(const Mat& z, const Kernel& k, const Mat& up) {

@@ -84,11 +84,19 @@ struct Result {
   Breakdown bd;
   GramFactor gram;
   Adjoints adj;
+  // deferred adjoints: d_kmm and d_beta are only needed by the host-side gradient assembly, so
+  // the engine computes them (complete_adjoints) while the gradient kernels run
+  bool deferred = false;
+  Mat kmm_inv, a_inv, g, ggt;
+  double ap = 0, kp = 0, pg = 0;
 };
 
-// factor_gram + bound_core (+ KL for the latent model) + adjoints_from_core.
+// factor_gram + bound_core (+ KL for the latent model) + adjoints_from_core.  With
+// defer_host_only, only the adjoints the device pass needs (d_phi, d_psi_y, d_phi_big) are formed;
+// complete_adjoints adds d_kmm and d_beta (same arithmetic, bitwise identical results).
 Result coordinate(bool latent, int64_t n, int64_t d, const Stats& st, const Mat& z, const Kernel& k, double beta,
-                  double jitter_factor, bool with_adjoints);
+                  double jitter_factor, bool with_adjoints, bool defer_host_only = false);
+void complete_adjoints(Result& r, const Stats& st, int64_t n, int64_t d, double beta);
 
 struct KernGrads {
   double d_variance = 0;

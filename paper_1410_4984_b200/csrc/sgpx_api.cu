@@ -283,6 +283,7 @@ struct sgpx_engine {
   HostBuf h_stats, h_grads, h_u, h_dpsi, h_err, h_stage;
   // coordinator results of the current evaluation
   coord::Result res;
+  coord::Stats st;  // unpacked statistics of the last coordinate() (complete_adjoints needs them)
   bool coordinated = false, with_grads = false;
   bool pairs_folded = false;  // sub-shard pair sums folded into the first (once per forward)
   cudaEvent_t ev[8] = {};  // 0-1 stats pass, 2-3 grad pass, 4-5 fwd kernel, 6-7 bwd kernel
@@ -471,9 +472,11 @@ void engine_coordinate(sgpx_engine* e, bool with_grads) {
   CUDA_OK(cudaStreamSynchronize(ctx->stream));
   const auto t_host = std::chrono::steady_clock::now();  // host algebra only (the sync waited for the kernels)
   check_err_flag(*e->h_err.get<int>());
-  coord::Stats st = coord::unpack_stats(e->h_stats.get<double>(), e->cfg.m, e->cfg.d);
-  e->res = coord::coordinate(e->latent, e->cfg.n_global, e->cfg.d, st, e->z, e->kernel, e->beta, e->cfg.jitter_factor,
-                             with_grads);
+  e->st = coord::unpack_stats(e->h_stats.get<double>(), e->cfg.m, e->cfg.d);
+  // d_kmm / d_beta are deferred until the gradient kernels are enqueued (they run on the host
+  // while the device works; complete_adjoints)
+  e->res = coord::coordinate(e->latent, e->cfg.n_global, e->cfg.d, e->st, e->z, e->kernel, e->beta,
+                             e->cfg.jitter_factor, with_grads, /*defer_host_only=*/true);
   e->with_grads = with_grads;
   if (with_grads) {
     stage_adjoints(e->P, e->res.adj.d_phi_big, e->res.adj.d_psi_y, e->h_u, e->h_dpsi);
@@ -565,6 +568,8 @@ void engine_grad_pass(sgpx_engine* e) {
     CUDA_OK(cudaMemsetAsync(e->pgrads.p, 0, sizeof(double) * count, ctx->stream));
   }
   CUDA_OK(cudaEventRecord(e->ev[3], ctx->stream));
+  // host-only adjoints, overlapping the kernels just enqueued
+  coord::complete_adjoints(e->res, e->st, e->cfg.n_global, e->cfg.d, e->beta);
 }
 
 void engine_finish(sgpx_engine* e, sgpx_eval_result* out) {
@@ -590,6 +595,7 @@ void engine_finish(sgpx_engine* e, sgpx_eval_result* out) {
     CUDA_OK(cudaStreamSynchronize(ctx->stream));
     if (e->copy) CUDA_OK(cudaStreamSynchronize(e->copy));  // streamed d mu / d S have landed
     const double* g = e->h_grads.get<double>();
+    coord::complete_adjoints(e->res, e->st, e->cfg.n_global, e->cfg.d, e->beta);
     coord::KernGrads kg = coord::kern_grads_zz(e->z, e->kernel, e->res.adj.d_kmm);
     double tr = 0.0;
     for (int64_t i = 0; i < m; ++i) tr += e->res.adj.d_kmm(i, i);
