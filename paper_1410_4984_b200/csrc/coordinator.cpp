@@ -270,15 +270,22 @@ Stats unpack_stats(const double* p, int64_t m, int64_t d) {
   return s;
 }
 
+Prefactor prefactor(const Mat& z, const Kernel& k, double jitter_factor) {
+  Prefactor p;
+  p.gram = factor_gram(z, k, jitter_factor);
+  p.kmm_inv = chol_inverse(p.gram.L);
+  return p;
+}
+
 Result coordinate(bool latent, int64_t n, int64_t d, const Stats& st, const Mat& z, const Kernel& k, double beta,
-                  double jitter_factor, bool with_adjoints, bool defer_host_only) {
+                  double jitter_factor, bool with_adjoints, bool defer_host_only, const Prefactor* pre) {
   const int64_t m = z.r;
   require(beta > 0.0 && std::isfinite(beta), "bound: beta must be positive");
   require(n >= 1 && d >= 1, "bound: need N >= 1 and D >= 1");
   require(int64_t(st.n) == n, "bound: stats n_count does not match N");
   require(st.phi >= 0.0 && st.yy >= 0.0, "bound: phi and yy must be non-negative");
   Result r;
-  r.gram = factor_gram(z, k, jitter_factor);
+  r.gram = pre ? pre->gram : factor_gram(z, k, jitter_factor);
   // bound_core (bound.hpp:84-119).  The Kmm factor of factor_gram is exactly
   // factor_spd(Kmm)'s first (successful) attempt.
   const Mat& Lk = r.gram.L;
@@ -290,7 +297,7 @@ Result coordinate(bool latent, int64_t n, int64_t d, const Stats& st, const Mat&
   const double log_det_a = log_det_chol(La);
   const Mat a_inv = chol_inverse(La);
   const Mat g = gemm(a_inv, false, st.psi_y, false);
-  const Mat kmm_inv = chol_inverse(Lk);
+  const Mat kmm_inv = pre ? pre->kmm_inv : chol_inverse(Lk);
   const double log_2pi = 1.8378770664093454835606594728112;
   const double nd = double(n), dd = double(d);
   Breakdown& bd = r.bd;

@@ -94,8 +94,17 @@ struct Result {
 // factor_gram + bound_core (+ KL for the latent model) + adjoints_from_core.  With
 // defer_host_only, only the adjoints the device pass needs (d_phi, d_psi_y, d_phi_big) are formed;
 // complete_adjoints adds d_kmm and d_beta (same arithmetic, bitwise identical results).
+// The Z-only part of the coordinator (factor_gram and (Kmm)^-1): the engine forms it while the
+// statistics pass runs on the device.
+struct Prefactor {
+  GramFactor gram;
+  Mat kmm_inv;
+};
+Prefactor prefactor(const Mat& z, const Kernel& k, double jitter_factor);
+
 Result coordinate(bool latent, int64_t n, int64_t d, const Stats& st, const Mat& z, const Kernel& k, double beta,
-                  double jitter_factor, bool with_adjoints, bool defer_host_only = false);
+                  double jitter_factor, bool with_adjoints, bool defer_host_only = false,
+                  const Prefactor* pre = nullptr);
 void complete_adjoints(Result& r, const Stats& st, int64_t n, int64_t d, double beta);
 
 struct KernGrads {

@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <exception>
 #include <memory>
 #include <string>
 #include <vector>
@@ -469,14 +470,24 @@ void engine_coordinate(sgpx_engine* e, bool with_grads) {
   e->h_err.ensure(sizeof(int));
   CUDA_OK(cudaMemcpyAsync(e->h_stats.p, e->pstats.p, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_OK(cudaMemcpyAsync(e->h_err.p, e->err.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  // Z-only algebra while the statistics pass is still running on the device; its errors are
+  // reported after the pass's own (data validation first, as in the reference)
+  coord::Prefactor pre;
+  std::exception_ptr pre_err;
+  try {
+    pre = coord::prefactor(e->z, e->kernel, e->cfg.jitter_factor);
+  } catch (...) {
+    pre_err = std::current_exception();
+  }
   CUDA_OK(cudaStreamSynchronize(ctx->stream));
   const auto t_host = std::chrono::steady_clock::now();  // host algebra only (the sync waited for the kernels)
   check_err_flag(*e->h_err.get<int>());
+  if (pre_err) std::rethrow_exception(pre_err);
   e->st = coord::unpack_stats(e->h_stats.get<double>(), e->cfg.m, e->cfg.d);
   // d_kmm / d_beta are deferred until the gradient kernels are enqueued (they run on the host
   // while the device works; complete_adjoints)
   e->res = coord::coordinate(e->latent, e->cfg.n_global, e->cfg.d, e->st, e->z, e->kernel, e->beta,
-                             e->cfg.jitter_factor, with_grads, /*defer_host_only=*/true);
+                             e->cfg.jitter_factor, with_grads, /*defer_host_only=*/true, &pre);
   e->with_grads = with_grads;
   if (with_grads) {
     stage_adjoints(e->P, e->res.adj.d_phi_big, e->res.adj.d_psi_y, e->h_u, e->h_dpsi);
