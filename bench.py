@@ -70,7 +70,7 @@ def env_int(name, default):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms during the timed region."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -81,17 +81,31 @@ class ClockSampler:
         self.proc = None
         self.path = f"/tmp/sgpx_clocks_{os.getpid()}.csv"
 
+    def _lines(self):
+        try:
+            with open(self.path) as f:
+                return sum(1 for _ in f)
+        except OSError:
+            return 0
+
     def __enter__(self):
         try:
-            self.f = open(self.path, "w")
+            self.f = open(self.path, "w", buffering=1)
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
                                          stderr=subprocess.DEVNULL)
+            # nvidia-smi takes a few hundred ms to start: wait for its first sample so that the
+            # samples of the timed region (taken from here on) are not lost to the start-up
+            t0 = time.time()
+            while self._lines() == 0 and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+        self.first = self._lines()
         return self
 
     def __exit__(self, *a):
+        self.last = self._lines()
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -105,7 +119,10 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+        lines = open(self.path).read().splitlines()
+        # the samples taken inside the timed region (plus the one just before it, if none landed)
+        lines = lines[max(0, self.first - 1):max(self.first, self.last)] if self.last > self.first else lines[-1:]
+        for line in lines:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 9:
                 continue
