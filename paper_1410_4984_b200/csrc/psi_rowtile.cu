@@ -817,17 +817,20 @@ __global__ void rt_pair_reduce_kernel(const double* __restrict__ part, int ns, i
 // Together they write one backward partial row [dvar, dl (Q), dz (a + q M)].
 
 template <int Q>
-__global__ void rt_pair_dz_kernel(PsiConst P, const float* __restrict__ u, const double* __restrict__ sums,
-                                  double* __restrict__ row) {
+__global__ void __launch_bounds__(256) rt_pair_dz_kernel(PsiConst P, const float* __restrict__ u,
+                                                         const double* __restrict__ sums, double* __restrict__ row) {
+  // one warp per (a, q): lane l takes b = l, l + 32, ... in order, then a fixed shuffle tree
   constexpr int NH = 2 * Q + 1;
   const int m = P.m, mv = P.mv, q_n = P.q;
   const PairIdx pi{m};
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m * q_n; i += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int nw = int(gridDim.x * blockDim.x) >> 5;
+  for (int i = int(blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m * q_n; i += nw) {
     const int a = i % m, q = i / m;
     const double il2 = 1.0 / (P.ls[q] * P.ls[q]);
     const double za = P.z64[q * m + a] - P.center[q];
     double s = 0.0;
-    for (int b = 0; b < m; ++b) {
+    for (int b = lane; b < m; b += 32) {
       const int lo = a < b ? a : b, hi = a < b ? b : a;
       const double* r = sums + pi.of(lo, hi) * NH;
       const double zb = P.z64[q * m + b] - P.center[q];
@@ -837,7 +840,8 @@ __global__ void rt_pair_dz_kernel(PsiConst P, const float* __restrict__ u, const
       const double w = lo == hi ? double(u[a * mv + a]) : double(u[lo * mv + hi]) + double(u[hi * mv + lo]);
       s += w * (a == b ? 2.0 * t : t);  // the diagonal pair carries z_a in both slots
     }
-    row[1 + q_n + a + int64_t(q) * m] = s;
+    s = warp_sum_d(s);
+    if (lane == 0) row[1 + q_n + a + int64_t(q) * m] = s;
   }
 }
 
@@ -1153,7 +1157,7 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
     }
   }
   if (!B.skip_pair_terms) {
-    rt_pair_dz_kernel<Q><<<std::max(1, (P.m * P.q + 127) / 128), 128, 0, st>>>(P, B.u, fbase + F.off_sums, prow);
+    rt_pair_dz_kernel<Q><<<std::max(1, (P.m * P.q + 7) / 8), 256, 0, st>>>(P, B.u, fbase + F.off_sums, prow);
     rt_pair_dl_kernel<Q><<<P.q + 1, 256, 0, st>>>(P, B.u, fbase + F.off_sums, prow);
     g_tc_launches.fetch_add(2);
   }
