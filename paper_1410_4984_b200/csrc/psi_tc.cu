@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   constexpr int Q4 = (Q + 3) / 4;
   extern __shared__ __align__(1024) float sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5, nthr = blockDim.x;
-  const int m = P.m, mv = P.mv, qv = P.qv, d = P.d;
+  const int m = P.m, mv = P.mv, qv = P.qv;
   const TCLayout L = tc_layout(P.q, m);
   float* p = sm;
   float* B1 = p;
