@@ -37,6 +37,7 @@ struct PsiConst {
   float il2[kMaxQ], l2[kMaxQ];
   double ls[kMaxQ];
   unsigned long long* prof;   // optional per-phase cycle counters (SGPX_TC_PROFILE=1), else null
+  int rt_pieces;              // row-tile MMA1 fp16 pieces: 2 or 3, 0 = decide per call (rt_decide_pieces)
 };
 
 // Backward-only inputs.
@@ -114,6 +115,13 @@ bool use_rt(const PsiConst& P);
 int64_t rt_fwd_doubles(const PsiConst& P, int num_sms);
 int64_t rt_bwd_doubles(const PsiConst& P, int num_sms);
 int rt_forward(const PsiConst& P, double* base, double* packed, int num_sms, void* stream);
+// Row-tile exponent piece count for these inputs (2 or 3; < 0 on a CUDA error): the device-side
+// spread check (synchronises the stream), or the SGPX_PSI_PIECES override.
+int rt_decide_pieces(const PsiConst& P, void* stream);
+// Host-side variant on host mu (column-major, ld): 16 evenly spaced blocks of `stride` rows, for
+// callers whose mu is still on its way to the device.
+int rt_decide_pieces_host(const PsiConst& P, const double* mu_host, int64_t ld, int64_t n, int64_t stride,
+                          const double* z_host, int64_t m);
 int rt_backward(const PsiConst& P, const BwdConst& B, double* bbase, double* prow, int num_sms, void* stream);
 // Where the forward placed the row-tile region inside its partial buffer (BwdConst::fwd_rt).
 const double* rt_fwd_region(const PsiConst& P, const double* fwd_part, int num_sms);

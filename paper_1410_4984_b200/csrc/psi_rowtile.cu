@@ -36,6 +36,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <type_traits>
 
 #include "psi_common.cuh"
@@ -68,7 +69,9 @@ constexpr float kHalfMax = 6.0e4f;      // exponent features are clamped to the 
 // PAIR: two CTAs of a cluster run one M = 256 MMA stream (tcgen05 cta_group::2): each holds its
 // own 128 static rows and HALF of every streamed chunk (48 X rows, and Y_hi resp. Y_lo), which
 // halves both the MMA instructions and the L2->SM operand traffic per SM.
-template <int Q, bool BF, bool PAIR = false>
+// NP: fp16 pieces per exponent feature (2: hi/lo ~2^-22; 3: hi/mid/lo ~2^-33, six MMA1 products,
+// selected for wide latent spreads by rt_pieces()).
+template <int Q, bool BF, bool PAIR = false, int NP = 2>
 struct RT {
   static constexpr int K1 = (2 * Q + 2 + 15) / 16 * 8;  // MMA1 depth in half2 words (K = 2 K1 halves)
   static constexpr int NH = 2 * Q + 1;                // MMA3 useful columns
@@ -77,7 +80,7 @@ struct RT {
   static constexpr int XF = XH * K1;                  // words of one X part (fp16 hi or lo)
   static constexpr int YB = N3 * kCH;                 // elements of one Y^T part (hi or lo)
   static constexpr int YFl = YB / 2;                  // floats of one Y^T part (16-bit pieces)
-  static constexpr int PF = 2 * XF + (PAIR ? 1 : 2) * YFl;  // floats per processed stage (per CTA)
+  static constexpr int PF = NP * XF + (PAIR ? 1 : 2) * YFl;  // words per processed stage (per CTA)
   static constexpr int CHF = PAIR ? 2 * PF : PF;      // floats per streamed chunk in global memory
   static constexpr int AF = 128 * K1;                 // words of one static part (hi or lo)
   static constexpr int SW = kCH;                      // TMEM columns per D/G stage
@@ -92,9 +95,9 @@ struct RT {
 __host__ __device__ constexpr int rt_k1(int q) { return (2 * q + 2 + 15) / 16 * 8; }
 __host__ __device__ constexpr int rt_n3(int q) { return (2 * q + 1 + 15) / 16 * 16; }
 // per-CTA processed stage floats
-__host__ __device__ constexpr int rt_pf(int q, bool bf, bool pair) {
+__host__ __device__ constexpr int rt_pf(int q, bool bf, bool pair, int np = 2) {
   (void)bf;
-  return 2 * (pair ? kCH / 2 : kCH) * rt_k1(q) + (pair ? 1 : 2) * rt_n3(q) * kCH / 2;
+  return np * (pair ? kCH / 2 : kCH) * rt_k1(q) + (pair ? 1 : 2) * rt_n3(q) * kCH / 2;
 }
 __host__ __device__ constexpr bool rt_concat(int q, bool bf) {
   (void)bf;
@@ -112,11 +115,11 @@ __host__ __device__ constexpr int rt_stages(int q, bool bf) {  // RT<Q, BF>::kS 
   (void)bf;
   return (512 - 2 * ((3 * kCH + 4 * rt_n3(q) <= 512) ? 2 * rt_n3(q) : rt_n3(q))) / kCH >= 4 ? 4 : 3;
 }
-RtCfg rt_cfg(int q, bool bf, bool pair = false) {
+RtCfg rt_cfg(int q, bool bf, bool pair = false, int np = 2) {
   // operand stages: MMA1 runs kS chunks ahead, so the TMA ring needs kS + 2 slots to keep two
   // loads in flight; a single static-tile buffer if that is what makes room.
   const size_t K1 = rt_k1(q);
-  const size_t a = 4 * 2 * 128 * K1, pst = 4 * size_t(rt_pf(q, bf, pair));
+  const size_t a = 4 * size_t(np) * 128 * K1, pst = 4 * size_t(rt_pf(q, bf, pair, np));
   const size_t bars = 512, cap = 227 * 1024;
   const int ks = rt_stages(q, bf);
   for (int slack = 2; slack >= 0; --slack)
@@ -146,46 +149,53 @@ __device__ __forceinline__ uint32_t h2u(__half2 h) {
 // Feature builders (elementwise, HBM-bound)
 // ---------------------------------------------------------------------------------------------
 
-// fp16 hi / lo pieces of features k, k+1 packed as half2 words (low half = even k), clamped to the
-// fp16 range
-__device__ __forceinline__ void split_pair(float x0, float x1, uint32_t& hi, uint32_t& lo) {
-  x0 = fminf(fmaxf(x0, -kHalfMax), kHalfMax);
-  x1 = fminf(fmaxf(x1, -kHalfMax), kHalfMax);
-  const __half2 h = __floats2half2_rn(x0, x1);
-  const float2 hf = __half22float2(h);
-  hi = h2u(h);
-  lo = h2u(__floats2half2_rn(x0 - hf.x, x1 - hf.y));
-}
-// 2 K1 features of one row as K1 hi / lo words at word offset `row_off + (k / 4) * 32 + ...` of a
-// canonical K-major tile (core matrix = 8 rows x 4 words)
-__device__ __forceinline__ void put_feat_words(float* hi, float* lo, int row_off, const float* f, int K1) {
-  for (int k = 0; k < K1; k += 4) {
-    uint32_t h[4], l[4];
+// fp16 pieces of features k, k+1 packed as half2 words (low half = even k), clamped to the fp16
+// range: NP = 2 -> hi, lo (~2^-22); NP = 3 -> hi, mid, lo (~2^-33, from fp64 features)
+template <int NP>
+__device__ __forceinline__ void split_pair(double x0, double x1, uint32_t (&w)[NP]) {
+  x0 = fmin(fmax(x0, -double(kHalfMax)), double(kHalfMax));
+  x1 = fmin(fmax(x1, -double(kHalfMax)), double(kHalfMax));
 #pragma unroll
-    for (int u = 0; u < 4; ++u) split_pair(f[2 * (k + u)], f[2 * (k + u) + 1], h[u], l[u]);
-    *reinterpret_cast<uint4*>(hi + row_off + (k >> 2) * 32) = make_uint4(h[0], h[1], h[2], h[3]);
-    *reinterpret_cast<uint4*>(lo + row_off + (k >> 2) * 32) = make_uint4(l[0], l[1], l[2], l[3]);
+  for (int i = 0; i < NP; ++i) {
+    const __half2 h = __floats2half2_rn(float(x0), float(x1));
+    w[i] = h2u(h);
+    const float2 hf = __half22float2(h);
+    x0 -= double(hf.x);
+    x1 -= double(hf.y);
   }
 }
-__device__ __forceinline__ void put_rows(float* hi, float* lo, int64_t r, const float* f, int K1) {
-  const int64_t base = (r >> 3) * (K1 * 8);
-  put_feat_words(hi + base, lo + base, int(r & 7) * 4, f, K1);
+// 2 K1 features of one row as NP pieces of K1 words at word offset `row_off` of a canonical
+// K-major tile (core matrix = 8 rows x 4 words); piece i at base + i * pstride
+template <int NP>
+__device__ __forceinline__ void put_feat_words(float* base, int64_t pstride, int64_t row_off, const double* f, int K1) {
+  for (int k = 0; k < K1; k += 4) {
+    uint32_t w[4][NP];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) split_pair<NP>(f[2 * (k + u)], f[2 * (k + u) + 1], w[u]);
+#pragma unroll
+    for (int i = 0; i < NP; ++i)
+      *reinterpret_cast<uint4*>(base + i * pstride + row_off + (k >> 2) * 32) = make_uint4(w[0][i], w[1][i], w[2][i], w[3][i]);
+  }
+}
+template <int NP>
+__device__ __forceinline__ void put_rows(float* base, int64_t pstride, int64_t r, const double* f, int K1) {
+  put_feat_words<NP>(base, pstride, (r >> 3) * (K1 * 8) + (r & 7) * 4, f, K1);
 }
 
 // One row of a streamed chunk in the processed-stage layout (the MMA1 / MMA3 B operands): X row
 // jj (K1 features) and Y column jj (N3 features, rows past NH zero).  Single CTA:
 // [X hi | X lo | Y^T hi | Y^T lo] over all 96 rows.  PAIR: two per-CTA blocks
 // [X hi | X lo (48 rows) | Y^T hi] and [X hi | X lo (rows 48..95) | Y^T lo].
-template <int Q, bool BF, bool PAIR>
-__device__ __forceinline__ void put_pre_row(float* chunk, int jj, const float* x, const float* y,
+template <int Q, bool BF, bool PAIR, int NP>
+__device__ __forceinline__ void put_pre_row(float* chunk, int jj, const double* x, const float* y,
                                             const float* yscale = nullptr) {
-  using C = RT<Q, BF, PAIR>;
+  using C = RT<Q, BF, PAIR, NP>;
   constexpr int K1 = C::K1, N3 = C::N3, XF = C::XF, YFl = C::YFl, PF = C::PF, XH = C::XH;
   float* xb = chunk + (PAIR ? (jj / XH) * PF : 0);
   const int r = jj % XH;
-  put_feat_words(xb, xb + XF, (r >> 3) * (K1 * 8) + (r & 7) * 4, x, K1);
-  float* y_hi = chunk + 2 * XF;                          // block 0 (or the single block)
-  float* y_lo = PAIR ? chunk + PF + 2 * XF : y_hi + YFl;  // block 1 (or after Y_hi)
+  put_feat_words<NP>(xb, XF, (r >> 3) * (K1 * 8) + (r & 7) * 4, x, K1);
+  float* y_hi = chunk + NP * XF;                          // block 0 (or the single block)
+  float* y_lo = PAIR ? chunk + PF + NP * XF : y_hi + YFl;  // block 1 (or after Y_hi)
   if (BF) {  // Y^T as bf16 hi / lo, canonical K-major (rows = features, 8 bf16 per core-matrix row)
     __nv_bfloat16* yh = reinterpret_cast<__nv_bfloat16*>(y_hi);
     __nv_bfloat16* yl = reinterpret_cast<__nv_bfloat16*>(y_lo);
@@ -226,18 +236,40 @@ struct PairIdx {
   }
 };
 
-// Pair rows F_p, p < p_pad (zero rows past P): canonical K-major hi / lo (static operand of the
-// forward).
-template <int Q>
-__global__ void __launch_bounds__(256) rt_pair_rows_kernel(PsiConst P, int64_t p_pad, float* __restrict__ fh,
-                                                            float* __restrict__ fl) {
+// Pair feature row F_p (fp64, lengthscale units) of pair (a, b); zbar (centred, unscaled) returned.
+template <int Q, int KF>
+__device__ __forceinline__ void pair_features(const PsiConst& P, int a, int b, double (&f)[KF], double (&zbar)[Q]) {
+  const int m = P.m;
+  double c = 0.0;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    zbar[q] = 0.0;
+    if (q < P.q) {
+      const double za = P.z64[q * m + a] - P.center[q], zb = P.z64[q * m + b] - P.center[q];
+      const double il = 1.0 / P.ls[q];
+      const double zm = 0.5 * (za + zb), dz = (za - zb) * il;
+      zbar[q] = zm;
+      f[q] = zm * il;
+      f[Q + q] = (zm * il) * (zm * il);
+      c += dz * dz;
+    }
+  }
+  f[2 * Q] = -0.25 * double(kLog2e) * c;
+  f[2 * Q + 1] = 1.0;
+}
+
+// Pair rows F_p, p < p_pad (zero rows past P): canonical K-major pieces (static operand of the
+// forward), piece i at fs + i * pstride.
+template <int Q, int NP>
+__global__ void __launch_bounds__(256) rt_pair_rows_kernel(PsiConst P, int64_t p_pad, float* __restrict__ fs,
+                                                            int64_t pstride) {
   constexpr int K1 = RT<Q, true>::K1;
-  const int m = P.m, qv = P.qv;
+  const int m = P.m;
   const int64_t npairs = int64_t(m) * (m + 1) / 2;
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < p_pad; p += int64_t(gridDim.x) * blockDim.x) {
-    float f[2 * K1];
+    double f[2 * K1], zb[Q];
 #pragma unroll
-    for (int k = 0; k < 2 * K1; ++k) f[k] = 0.f;
+    for (int k = 0; k < 2 * K1; ++k) f[k] = 0.0;
     if (p < npairs) {
       int a = 0;
       int64_t rem = p;
@@ -245,31 +277,18 @@ __global__ void __launch_bounds__(256) rt_pair_rows_kernel(PsiConst P, int64_t p
         rem -= m - a;
         ++a;
       }
-      const int b = a + int(rem);
-      float c = 0.f;
-#pragma unroll
-      for (int q = 0; q < Q; ++q)
-        if (q < P.q) {
-          const float za = P.zc[a * qv + q], zb = P.zc[b * qv + q];
-          const float zbar = 0.5f * (za + zb), dz = za - zb;
-          const float zs = zbar * sqrtf(P.il2[q]);  // lengthscale units
-          f[q] = zs;
-          f[Q + q] = zs * zs;
-          c = fmaf(P.il2[q] * dz, dz, c);
-        }
-      f[2 * Q] = -0.25f * kLog2e * c;
-      f[2 * Q + 1] = 1.f;
+      pair_features<Q>(P, a, a + int(rem), f, zb);
     }
-    put_rows(fh, fl, p, f, K1);
+    put_rows<NP>(fs, pstride, p, f, K1);
   }
 }
 
-// Datapoint rows H_n, n < n_pad (padded rows [0 .., 0, -huge]): canonical K-major hi / lo (static
-// operand of the backward) and, per 96-row chunk, the forward's streamed operands
-// X = H_n, Y = [1, d2 mu, d2] in the processed-stage layout.
-template <int Q, bool PAIR>
-__global__ void __launch_bounds__(256) rt_data_rows_kernel(PsiConst P, int64_t n_pad, float* __restrict__ hh,
-                                                            float* __restrict__ hl, float* __restrict__ pre) {
+// Datapoint rows H_n, n < n_pad (padded rows [0 .., 0, -huge]): canonical K-major pieces (static
+// operand of the backward, piece i at hs + i * pstride) and, per 96-row chunk, the forward's
+// streamed operands X = H_n, Y = [1, d2 mu, d2] in the processed-stage layout.
+template <int Q, bool PAIR, int NP>
+__global__ void __launch_bounds__(256) rt_data_rows_kernel(PsiConst P, int64_t n_pad, float* __restrict__ hs,
+                                                            int64_t pstride, float* __restrict__ pre) {
   constexpr int K1 = RT<Q, true>::K1;
   for (int64_t n = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; n < n_pad; n += int64_t(gridDim.x) * blockDim.x) {
     const bool valid = n < P.n;
@@ -282,36 +301,36 @@ __global__ void __launch_bounds__(256) rt_data_rows_kernel(PsiConst P, int64_t n
       rs[q] = P.expected ? __ldg(P.s + qq * P.ld_s + nn) : 0.0;
     }
     constexpr int N3 = RT<Q, true>::N3;
-    float h[2 * K1], y[N3];
+    double h[2 * K1];
+    float y[N3];
 #pragma unroll
-    for (int k = 0; k < 2 * K1; ++k) h[k] = 0.f;
+    for (int k = 0; k < 2 * K1; ++k) h[k] = 0.0;
 #pragma unroll
     for (int k = 0; k < N3; ++k) y[k] = 0.f;
     if (valid) {
-      float bsum = 2.f * P.log2_var;
+      double bsum = 2.0 * double(P.log2_var);
 #pragma unroll
       for (int q = 0; q < Q; ++q)
         if (q < P.q) {
-          const float mu = float(rm[q] - P.center[q]);
-          const float sv = float(rs[q]);
-          const float il2 = P.il2[q];
-          const float t = fmaf(2.f * sv, il2, 1.f);
-          const float d2 = il2 / t;  // 1 / (2 S + l^2)
-          const float it = 1.f / t;  // d2 l^2
-          h[q] = 2.f * kLog2e * (mu * sqrtf(il2)) * it;
-          h[Q + q] = -kLog2e * it;
-          bsum = fmaf(-0.5f, log2f(t), fmaf(-kLog2e * d2 * mu, mu, bsum));
-          y[1 + q] = d2 * mu;
-          y[1 + Q + q] = d2;
+          const double mu = rm[q] - P.center[q];
+          const double il = 1.0 / P.ls[q], il2 = il * il;
+          const double t = 1.0 + 2.0 * rs[q] * il2;
+          const double it = 1.0 / t;     // d2 l^2
+          const double d2 = il2 * it;    // 1 / (2 S + l^2)
+          h[q] = 2.0 * double(kLog2e) * (mu * il) * it;
+          h[Q + q] = -double(kLog2e) * it;
+          bsum += -0.5 * log2(t) - double(kLog2e) * d2 * mu * mu;
+          y[1 + q] = float(d2 * mu);
+          y[1 + Q + q] = float(d2);
         }
-      h[2 * Q] = 1.f;
+      h[2 * Q] = 1.0;
       h[2 * Q + 1] = bsum;
       y[0] = 1.f;
     } else {
       h[2 * Q + 1] = kNegHuge;
     }
-    put_rows(hh, hl, n, h, K1);
-    put_pre_row<Q, true, PAIR>(pre + (n / kCH) * RT<Q, true, PAIR>::CHF, int(n % kCH), h, y);
+    put_rows<NP>(hs, pstride, n, h, K1);
+    put_pre_row<Q, true, PAIR, NP>(pre + (n / kCH) * RT<Q, true, PAIR, NP>::CHF, int(n % kCH), h, y);
   }
 }
 
@@ -361,17 +380,18 @@ __global__ void __launch_bounds__(256) rt_yscale_kernel(PsiConst P, const float*
 
 // Backward streamed operands, precomputed: X = F_p (C_ab + 15, so G = 2^15 v), Y = w_p [1, zb, zb^2]
 // (scaled by yscale).
-template <int Q, bool PAIR>
+template <int Q, bool PAIR, int NP>
 __global__ void __launch_bounds__(256) rt_pair_pre_kernel(PsiConst P, const float* __restrict__ u, int64_t p_pad,
                                                            const float* __restrict__ ys, float* __restrict__ pre) {
-  using C = RT<Q, false, PAIR>;
+  using C = RT<Q, false, PAIR, NP>;
   constexpr int K1 = C::K1, N3 = C::N3;
-  const int m = P.m, qv = P.qv, mv = P.mv;
+  const int m = P.m, mv = P.mv;
   const int64_t npairs = int64_t(m) * (m + 1) / 2;
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < p_pad; p += int64_t(gridDim.x) * blockDim.x) {
-    float f[2 * K1], y[N3];
+    double f[2 * K1], zb[Q];
+    float y[N3];
 #pragma unroll
-    for (int k = 0; k < 2 * K1; ++k) f[k] = 0.f;
+    for (int k = 0; k < 2 * K1; ++k) f[k] = 0.0;
 #pragma unroll
     for (int k = 0; k < N3; ++k) y[k] = 0.f;
     if (p < npairs) {
@@ -382,25 +402,18 @@ __global__ void __launch_bounds__(256) rt_pair_pre_kernel(PsiConst P, const floa
         ++a;
       }
       const int b = a + int(rem);
+      pair_features<Q>(P, a, b, f, zb);
+      f[2 * Q] += 15.0;  // C_ab + 15 (pairs with H's constant 1)
       const float w = a == b ? u[a * mv + a] : u[a * mv + b] + u[b * mv + a];
-      float c = 0.f;
 #pragma unroll
       for (int q = 0; q < Q; ++q)
         if (q < P.q) {
-          const float za = P.zc[a * qv + q], zb = P.zc[b * qv + q];
-          const float zbar = 0.5f * (za + zb), dz = za - zb;
-          const float zs = zbar * sqrtf(P.il2[q]);  // lengthscale units
-          f[q] = zs;
-          f[Q + q] = zs * zs;
-          c = fmaf(P.il2[q] * dz, dz, c);
-          y[1 + q] = w * zbar;
-          y[1 + Q + q] = w * zbar * zbar;
+          y[1 + q] = float(w * zb[q]);
+          y[1 + Q + q] = float(w * zb[q] * zb[q]);
         }
-      f[2 * Q] = 15.f - 0.25f * kLog2e * c;
-      f[2 * Q + 1] = 1.f;
       y[0] = w;
     }
-    put_pre_row<Q, false, PAIR>(pre + (p / kCH) * C::CHF, int(p % kCH), f, y, ys);
+    put_pre_row<Q, false, PAIR, NP>(pre + (p / kCH) * C::CHF, int(p % kCH), f, y, ys);
   }
 }
 
@@ -426,8 +439,8 @@ __device__ __forceinline__ RingPos ring(int n) {
 }
 
 struct RowTileArgs {
-  const float* a_hi;  // static rows: canonical K-major hi / lo arrays over all rows
-  const float* a_lo;
+  const float* a;      // static rows: NP canonical K-major piece arrays over all rows, a_stride apart
+  int64_t a_stride;
   const float* pre;   // streamed chunks in processed-stage layout [chunk][PF]
   int nA, nP;         // pipeline depths (rt_cfg)
   int mode;           // 0 forward (pairs static, datapoints streamed), 1 backward
@@ -440,9 +453,9 @@ struct RowTileArgs {
   int dbg;  // SGPX_RT_DBG (timing experiments only): 1 skip G math, 2 skip MMA3, 4 skip MMA1
 };
 
-template <int Q, bool BF, bool PAIR>
+template <int Q, bool BF, bool PAIR, int NP>
 __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTileArgs R) {
-  using C = RT<Q, BF, PAIR>;
+  using C = RT<Q, BF, PAIR, NP>;
   constexpr int K1 = C::K1, KS1 = K1 / 8, N3 = C::N3, NH = C::NH;
   constexpr int PF = C::PF, CHF = C::CHF, XF = C::XF, YFl = C::YFl, AF = C::AF;
   constexpr int kS = C::kS;             // D/G stages of SW TMEM columns
@@ -460,8 +473,8 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
   // peer consumer / drain warp (g_full, c_empty: those warps arrive directly, one lane each)
   const uint32_t relay = (PAIR && leader) ? 1u : 0u;
   const int nA = R.nA, nP = R.nP;
-  float* Abuf = sm;                       // [nA][hi|lo][AF]
-  float* Proc = Abuf + nA * 2 * AF;       // [nP][Xh | Xl | Y]
+  float* Abuf = sm;                       // [nA][NP pieces][AF]
+  float* Proc = Abuf + nA * NP * AF;      // [nP][X pieces | Y]
   uint64_t* bar = reinterpret_cast<uint64_t*>(Proc + nP * PF);
   uint64_t* a_full = bar;                 // [2] static tile landed (tx)
   uint64_t* a_empty = bar + 2;            // [2] MMA1s of the tile done
@@ -536,10 +549,11 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
         if (j == 0) {
           if (ti >= nA) tc::mbar_wait(&a_empty[ra.slot], ra.phase ^ 1u);
           const int64_t row0 = tile_of(ti) * 128;
-          float* dst = Abuf + ra.slot * 2 * AF;
-          tc::mbar_arrive_expect_tx_w(&a_full[ra.slot], uint32_t(2 * AF * 4));
-          tc::bulk_g2s_w(dst, R.a_hi + row0 * K1, uint32_t(AF * 4), &a_full[ra.slot]);
-          tc::bulk_g2s_w(dst + AF, R.a_lo + row0 * K1, uint32_t(AF * 4), &a_full[ra.slot]);
+          float* dst = Abuf + ra.slot * NP * AF;
+          tc::mbar_arrive_expect_tx_w(&a_full[ra.slot], uint32_t(NP * AF * 4));
+#pragma unroll
+          for (int i = 0; i < NP; ++i)
+            tc::bulk_g2s_w(dst + i * AF, R.a + i * R.a_stride + row0 * K1, uint32_t(AF * 4), &a_full[ra.slot]);
           ra.next();
         }
         if (c >= nP) tc::mbar_wait(&p_empty[rp.slot], rp.phase ^ 1u);
@@ -571,14 +585,17 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
         if (j1 == 0) wait_x(&a_full[a1.slot], a1.phase);
         wait_x(&p_full[p1.slot], p1.phase);
         tc::fence_after();
-        const float* a = Abuf + a1.slot * 2 * AF;
+        const float* a = Abuf + a1.slot * NP * AF;
         const float* x = Proc + p1.slot * PF;
-        const uint64_t ah = tc::desc(tc::smem_u32(a), K1), al = tc::desc(tc::smem_u32(a + AF), K1);
-        const uint64_t xh = tc::desc(tc::smem_u32(x), K1), xl = tc::desc(tc::smem_u32(x + XF), K1);
         const uint32_t d = tmem + uint32_t(s1.slot) * SW;
+        // piece products whose weight is >= 2^-22 (NP = 2: hh, hl, lh) or >= 2^-33 (NP = 3: with
+        // piece 1 = mid, 2 = lo: hh, hm, mh, mm, hl, lh)
+        constexpr int NT = NP == 2 ? 3 : 6;
+        constexpr int PA[6] = {0, 0, 1, 1, 0, 2}, PB[6] = {0, 1, 0, 1, 2, 0};
 #pragma unroll
-        for (int t = 0; t < 3; ++t) {
-          const uint64_t aa = t == 2 ? al : ah, bb = t == 1 ? xl : xh;
+        for (int t = 0; t < NT; ++t) {
+          const uint64_t aa = tc::desc(tc::smem_u32(a + PA[t] * AF), K1);
+          const uint64_t bb = tc::desc(tc::smem_u32(x + PB[t] * XF), K1);
 #pragma unroll
           for (int ks = 0; ks < KS1; ++ks) {
             if (R.dbg & 4) continue;
@@ -603,7 +620,7 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
         wait_x(&g_full[s3.slot], s3.phase);
         if (c >= 2) wait_x(&c_empty[c3.slot], c3.phase ^ 1u);
         tc::fence_after();
-        const float* y = Proc + p3.slot * PF + 2 * XF;
+        const float* y = Proc + p3.slot * PF + NP * XF;
         const uint32_t g0 = tmem + uint32_t(s3.slot) * SW;
         const uint32_t acc = tmem + kAcc0 + uint32_t(c3.slot) * AccW;
         if (!(R.dbg & 2)) {
@@ -946,8 +963,8 @@ struct FwdLayout {  // inside the forward partial buffer, after the psi1 rows (o
   int ns;
   int64_t nchunks;  // datapoint chunks
   int64_t npairs, p_pad, n_pad;
-  int64_t off_part, off_sums, off_floats;           // pair_part, pair_sums, then float arrays
-  int64_t f_fh, f_fl, f_hh, f_hl, f_pre, floats;  // float offsets relative to off_floats
+  int64_t off_part, off_sums, off_floats;  // pair_part, pair_sums, then 32-bit operand arrays
+  int64_t f_fs, f_hs, f_pre, floats;       // word offsets relative to off_floats (sized for 3 pieces)
   int64_t doubles;                                  // total doubles after the psi1 rows
 };
 
@@ -976,12 +993,10 @@ FwdLayout fwd_layout(const PsiConst& P, int num_sms) {
   L.off_part = 0;
   L.off_sums = int64_t(L.ns) * L.npairs * NH;
   L.off_floats = (L.off_sums + L.npairs * NH + 1) / 2 * 2 + 2;  // 16-byte aligned (+ slack)
-  L.f_fh = 0;
-  L.f_fl = L.f_fh + L.p_pad * K1;
-  L.f_hh = L.f_fl + L.p_pad * K1;
-  L.f_hl = L.f_hh + L.n_pad * K1;
-  L.f_pre = L.f_hl + L.n_pad * K1;
-  L.floats = L.f_pre + (L.n_pad / kCH) * rt_pf(q, true, false);  // same chunk size in PAIR layout
+  L.f_fs = 0;                                  // pair pieces, p_pad * K1 words apart
+  L.f_hs = L.f_fs + 3 * L.p_pad * K1;          // datapoint pieces, n_pad * K1 words apart
+  L.f_pre = L.f_hs + 3 * L.n_pad * K1;
+  L.floats = L.f_pre + (L.n_pad / kCH) * rt_pf(q, true, false, 3);  // same chunk size in PAIR layout
   L.doubles = L.off_floats + (L.floats + 1) / 2 + 2;
   return L;
 }
@@ -1010,9 +1025,93 @@ BwdLayout bwd_layout(const PsiConst& P, int num_sms) {
   L.off_dl = L.off_t + std::max<int64_t>(P.n, 1) * (2 * q + 1);
   L.off_ys = L.off_dl + int64_t(L.epi_blocks) * q;  // 128 floats: yscale[64], yinv[64]
   L.off_floats = (L.off_ys + 64 + 1) / 2 * 2 + 2;
-  const int64_t pf = rt_pf(q, false, false);
+  const int64_t pf = rt_pf(q, false, false, 3);
   L.doubles = L.off_floats + ((pad_rows(npairs) / kCH) * pf + 1) / 2 + 4;
   return L;
+}
+
+// ---- exponent piece count: the data spread decides (DESIGN.md §4 accuracy envelope) ----
+// spread2 = max(mean_n sum_q ((mu_nq - c_q) / l_q)^2, mean_a sum_q ((z_aq - c_q) / l_q)^2); the
+// two-piece MMA1 holds the 1e-5 / 5e-5 tolerances up to spread2 ~ 60 (tools/dbg_spread.py), beyond
+// it the three-piece MMA1 runs.  Fixed-order reductions: the decision is deterministic, so the
+// forward and the backward of one evaluation agree.
+constexpr int kSpreadBlocks = 256;
+constexpr double kSpread2Fast = 60.0;
+
+__global__ void __launch_bounds__(256) rt_spread_partial_kernel(PsiConst P, double* __restrict__ part) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int q = 0; q < P.q; ++q) {
+    const double il = 1.0 / P.ls[q], c = P.center[q];
+    for (int64_t n = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; n < P.n; n += int64_t(gridDim.x) * blockDim.x) {
+      const double v = (P.mu[q * P.ld_mu + n] - c) * il;
+      s += v * v;
+    }
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void __launch_bounds__(256) rt_spread_final_kernel(PsiConst P, const double* __restrict__ part, int nb,
+                                                              float* __restrict__ out) {
+  __shared__ double rmu[256], rz[256];
+  double smu = 0.0, sz = 0.0;
+  for (int i = threadIdx.x; i < nb; i += 256) smu += part[i];
+  for (int i = threadIdx.x; i < P.m * P.q; i += 256) {
+    const int q = i / P.m;
+    const double v = (P.z64[i] - P.center[q]) * (1.0 / P.ls[q]);
+    sz += v * v;
+  }
+  rmu[threadIdx.x] = smu;
+  rz[threadIdx.x] = sz;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      rmu[threadIdx.x] += rmu[threadIdx.x + w];
+      rz[threadIdx.x] += rz[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double mmu = P.n > 0 ? rmu[0] / double(P.n) : 0.0, mz = P.m > 0 ? rz[0] / double(P.m) : 0.0;
+    out[0] = float(mmu > mz ? mmu : mz);
+  }
+}
+
+int rt_forced_pieces() {
+  static const int forced = [] {
+    const char* e = getenv("SGPX_PSI_PIECES");  // 2 or 3: fixed piece count (experiments)
+    const int v = e ? atoi(e) : 0;
+    return (v == 2 || v == 3) ? v : 0;
+  }();
+  return forced;
+}
+
+int rt_pieces(const PsiConst& P, cudaStream_t st) {
+  if (P.rt_pieces == 2 || P.rt_pieces == 3) return P.rt_pieces;
+  if (const int f = rt_forced_pieces()) return f;
+  if (P.n <= 0) return 2;
+  static std::mutex mu;
+  static double* part = nullptr;
+  static float* out = nullptr;
+  static float* host = nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!part) {
+    if (cudaMalloc(&part, sizeof(double) * kSpreadBlocks) != cudaSuccess) return 3;
+    if (cudaMalloc(&out, sizeof(float)) != cudaSuccess) return 3;
+    if (cudaMallocHost(&host, sizeof(float)) != cudaSuccess) return 3;
+  }
+  rt_spread_partial_kernel<<<kSpreadBlocks, 256, 0, st>>>(P, part);
+  rt_spread_final_kernel<<<1, 256, 0, st>>>(P, part, kSpreadBlocks, out);
+  g_tc_launches.fetch_add(2);
+  if (cudaMemcpyAsync(host, out, sizeof(float), cudaMemcpyDeviceToHost, st) != cudaSuccess) return 3;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return 3;
+  return double(*host) > kSpread2Fast ? 3 : 2;
 }
 
 int rt_dbg() {
@@ -1035,12 +1134,12 @@ int rt_pair_env() {
 }
 bool use_pair(int q, bool bf) { return rt_pair_env() != 0 && rt_pair_ok(q, bf); }
 
-template <int Q, bool BF, bool PAIR>
+template <int Q, bool BF, bool PAIR, int NP>
 int launch_rowtile(const PsiConst& P, RowTileArgs R, dim3 grid, cudaStream_t st) {
-  RtCfg cfg = rt_cfg(Q, BF, PAIR);
+  RtCfg cfg = rt_cfg(Q, BF, PAIR, NP);
   if (const char* e = getenv("SGPX_RT_NP")) {  // experiments: deepest ring with nA = 1
     const int want = atoi(e);
-    const size_t a = 4 * 2 * 128 * size_t(rt_k1(Q)), pst = 4 * size_t(rt_pf(Q, BF, PAIR));
+    const size_t a = 4 * size_t(NP) * 128 * size_t(rt_k1(Q)), pst = 4 * size_t(rt_pf(Q, BF, PAIR, NP));
     for (int np = want; np >= 2; --np)
       if (a + np * pst + 512 <= 227 * 1024) {
         cfg = RtCfg{1, np, a + np * pst + 512};
@@ -1050,7 +1149,7 @@ int launch_rowtile(const PsiConst& P, RowTileArgs R, dim3 grid, cudaStream_t st)
   R.nA = cfg.nA;
   R.nP = cfg.nP;
   R.dbg = rt_dbg();
-  auto kern = rowtile_kernel<Q, BF, PAIR>;
+  auto kern = rowtile_kernel<Q, BF, PAIR, NP>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cfg.smem)) != cudaSuccess) return 3;
   if (PAIR) {
     cudaLaunchConfig_t lc = {};
@@ -1086,16 +1185,12 @@ int rt_forward_q(const PsiConst& P, double* base, double* packed, int num_sms, c
   using C = RT<Q, true>;
   const FwdLayout L = fwd_layout(P, num_sms);
   float* fl = floats_at(base, L.off_floats);
-  const int blocks_p = int(std::min<int64_t>((L.p_pad + 255) / 256, int64_t(num_sms) * 8));
-  rt_pair_rows_kernel<Q><<<blocks_p, 256, 0, st>>>(P, L.p_pad, fl + L.f_fh, fl + L.f_fl);
-  const int blocks_n = int(std::min<int64_t>((L.n_pad + 255) / 256, int64_t(num_sms) * 8));
-  const bool pair = use_pair(Q, true);
-  if (pair) rt_data_rows_kernel<Q, true><<<blocks_n, 256, 0, st>>>(P, L.n_pad, fl + L.f_hh, fl + L.f_hl, fl + L.f_pre);
-  else rt_data_rows_kernel<Q, false><<<blocks_n, 256, 0, st>>>(P, L.n_pad, fl + L.f_hh, fl + L.f_hl, fl + L.f_pre);
-  g_tc_launches.fetch_add(2);
+  const int np = rt_pieces(P, st);
+  if (np != 2 && np != 3) return 3;
+  const bool pair = np == 2 && use_pair(Q, true);
   RowTileArgs R{};
-  R.a_hi = fl + L.f_fh;
-  R.a_lo = fl + L.f_fl;
+  R.a = fl + L.f_fs;
+  R.a_stride = L.p_pad * C::K1;
   R.pre = fl + L.f_pre;
   R.mode = 0;
   R.ntiles = (L.npairs + 127) / 128;
@@ -1103,15 +1198,26 @@ int rt_forward_q(const PsiConst& P, double* base, double* packed, int num_sms, c
   R.cps = (L.nchunks + L.ns - 1) / L.ns;
   R.nrows_static = L.npairs;
   R.out = base + L.off_part;
-  if constexpr (RT<Q, true, true>::kConcat) {
-    if (pair) {
-      const unsigned gx = unsigned((R.ntiles + 1) / 2 * 2);
-      if (int rc = launch_rowtile<Q, true, true>(P, R, dim3(gx, unsigned(L.ns)), st)) return rc;
+  const int blocks_p = int(std::min<int64_t>((L.p_pad + 255) / 256, int64_t(num_sms) * 8));
+  const int blocks_n = int(std::min<int64_t>((L.n_pad + 255) / 256, int64_t(num_sms) * 8));
+  auto run = [&](auto np_tag) -> int {
+    constexpr int NP = decltype(np_tag)::value;
+    rt_pair_rows_kernel<Q, NP><<<blocks_p, 256, 0, st>>>(P, L.p_pad, fl + L.f_fs, L.p_pad * C::K1);
+    if (NP == 2 && pair)
+      rt_data_rows_kernel<Q, true, 2><<<blocks_n, 256, 0, st>>>(P, L.n_pad, fl + L.f_hs, L.n_pad * C::K1, fl + L.f_pre);
+    else
+      rt_data_rows_kernel<Q, false, NP><<<blocks_n, 256, 0, st>>>(P, L.n_pad, fl + L.f_hs, L.n_pad * C::K1,
+                                                                  fl + L.f_pre);
+    g_tc_launches.fetch_add(2);
+    if constexpr (NP == 2 && RT<Q, true, true>::kConcat) {
+      if (pair) {
+        const unsigned gx = unsigned((R.ntiles + 1) / 2 * 2);
+        return launch_rowtile<Q, true, true, 2>(P, R, dim3(gx, unsigned(L.ns)), st);
+      }
     }
-  }
-  if (!pair) {
-    if (int rc = launch_rowtile<Q, true, false>(P, R, dim3(unsigned(R.ntiles), unsigned(L.ns)), st)) return rc;
-  }
+    return launch_rowtile<Q, true, false, NP>(P, R, dim3(unsigned(R.ntiles), unsigned(L.ns)), st);
+  };
+  if (int rc = np == 3 ? run(std::integral_constant<int, 3>{}) : run(std::integral_constant<int, 2>{})) return rc;
   const int64_t tot = L.npairs * C::NH;
   rt_pair_reduce_kernel<<<int(std::min<int64_t>((tot + 255) / 256, 4096)), 256, 0, st>>>(
       base + L.off_part, L.ns, L.npairs, C::NH, base + L.off_sums, packed);
@@ -1127,16 +1233,20 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
   float* ff = floats_at(fbase, F.off_floats);
   float* pre = floats_at(bbase, L.off_floats);
   const int blocks_p = int(std::min<int64_t>((F.p_pad + 255) / 256, int64_t(num_sms) * 8));
-  const bool pair = use_pair(Q, false);
+  // the forward's piece count (same deterministic decision on the same inputs)
+  const int np = rt_pieces(P, st);
+  if (np != 2 && np != 3) return 3;
+  const bool pair = np == 2 && use_pair(Q, false);
   float* ys = reinterpret_cast<float*>(bbase + L.off_ys);
   rt_yscale_kernel<Q><<<1, 256, 0, st>>>(P, B.u, ys);
-  if (pair) rt_pair_pre_kernel<Q, true><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, ys, pre);
-  else rt_pair_pre_kernel<Q, false><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, ys, pre);
+  if (pair) rt_pair_pre_kernel<Q, true, 2><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, ys, pre);
+  else if (np == 3) rt_pair_pre_kernel<Q, false, 3><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, ys, pre);
+  else rt_pair_pre_kernel<Q, false, 2><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, ys, pre);
   g_tc_launches.fetch_add(2);
   if (P.n > 0) {
     RowTileArgs R{};
-    R.a_hi = ff + F.f_hh;
-    R.a_lo = ff + F.f_hl;
+    R.a = ff + F.f_hs;
+    R.a_stride = F.n_pad * RT<Q, false>::K1;
     R.pre = pre;
     R.mode = 1;
     R.ntiles = L.ntiles;
@@ -1149,11 +1259,13 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
       if (pair) {
         const int64_t units = (L.ntiles + 1) / 2;
         const unsigned gx = unsigned(2 * std::max<int64_t>(1, std::min<int64_t>(units, num_sms / 2)));
-        if (int rc = launch_rowtile<Q, false, true>(P, R, dim3(gx), st)) return rc;
+        if (int rc = launch_rowtile<Q, false, true, 2>(P, R, dim3(gx), st)) return rc;
       }
     }
     if (!pair) {
-      if (int rc = launch_rowtile<Q, false, false>(P, R, dim3(unsigned(L.grid)), st)) return rc;
+      const int rc = np == 3 ? launch_rowtile<Q, false, false, 3>(P, R, dim3(unsigned(L.grid)), st)
+                             : launch_rowtile<Q, false, false, 2>(P, R, dim3(unsigned(L.grid)), st);
+      if (rc) return rc;
     }
   }
   if (!B.skip_pair_terms) {
@@ -1188,7 +1300,8 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
 
 bool rt_supported(const PsiConst& P) {
   const int q = instantiated_q(P.q);
-  return P.q >= 1 && q <= 16 && P.m >= 1 && rt_cfg(q, true).nP >= 2 && rt_cfg(q, false).nP >= 2;
+  return P.q >= 1 && q <= 16 && P.m >= 1 && rt_cfg(q, true).nP >= 2 && rt_cfg(q, false).nP >= 2 &&
+         rt_cfg(q, true, false, 3).nP >= 2 && rt_cfg(q, false, false, 3).nP >= 2;
 }
 int64_t rt_fwd_doubles(const PsiConst& P, int num_sms) { return fwd_layout(P, num_sms).doubles; }
 double* rt_fwd_pair_sums(const PsiConst& P, double* region, int num_sms, int64_t* count) {
@@ -1198,6 +1311,38 @@ double* rt_fwd_pair_sums(const PsiConst& P, double* region, int num_sms, int64_t
 }
 int64_t rt_bwd_doubles(const PsiConst& P, int num_sms) { return bwd_layout(P, num_sms).doubles; }
 
+int rt_decide_pieces(const PsiConst& P, void* stream) {
+  const int np = rt_pieces(P, static_cast<cudaStream_t>(stream));
+  return (np == 2 || np == 3) ? np : -1;
+}
+int rt_decide_pieces_host(const PsiConst& P, const double* mu_host, int64_t ld, int64_t n, int64_t stride,
+                          const double* z_host, int64_t m) {
+  if (const int f = rt_forced_pieces()) return f;
+  // `stride` = rows per sampled block: 16 evenly spaced contiguous blocks (cache-friendly on pinned
+  // host memory)
+  double smu = 0.0;
+  int64_t cnt = 0;
+  const int64_t blocks = 16, len = std::max<int64_t>(1, std::min<int64_t>(stride, n));
+  for (int q = 0; q < P.q; ++q) {
+    const double il = 1.0 / P.ls[q], c = P.center[q];
+    for (int64_t b = 0; b < blocks; ++b) {
+      const int64_t i0 = std::min<int64_t>(n - len, (n - len) * b / (blocks - 1));
+      for (int64_t i = i0; i < i0 + len; ++i) {
+        const double v = (mu_host[q * ld + i] - c) * il;
+        smu += v * v;
+        if (q == 0) ++cnt;
+      }
+    }
+  }
+  double sz = 0.0;
+  for (int64_t a = 0; a < m; ++a)
+    for (int q = 0; q < P.q; ++q) {
+      const double v = (z_host[q * m + a] - P.center[q]) / P.ls[q];
+      sz += v * v;
+    }
+  const double mmu = cnt ? smu / double(cnt) : 0.0, mz = m ? sz / double(m) : 0.0;
+  return std::max(mmu, mz) > kSpread2Fast ? 3 : 2;
+}
 int rt_forward(const PsiConst& P, double* base, double* packed, int num_sms, void* stream) {
   SGPX_RT_DISPATCH(rt_forward_q, P, base, packed, num_sms, static_cast<cudaStream_t>(stream))
 }

@@ -287,6 +287,7 @@ struct sgpx_engine {
   coord::Stats st;  // unpacked statistics of the last coordinate() (complete_adjoints needs them)
   bool coordinated = false, with_grads = false;
   bool pairs_folded = false;  // sub-shard pair sums folded into the first (once per forward)
+  int rt_np = 0;              // exponent piece count for the current data (0: not decided yet)
   cudaEvent_t ev[8] = {};  // 0-1 stats pass, 2-3 grad pass, 4-5 fwd kernel, 6-7 bwd kernel
   double coord_s = 0.0;
   LaunchGeom gf{}, gb{};
@@ -429,6 +430,24 @@ void engine_stats_pass(sgpx_engine* e) {
   }
   e->fpart.ensure(sizeof(double) * foff);
   if (k > 1) e->pstats_sub.ensure(sizeof(double) * count * k);
+  // exponent piece count for this evaluation, decided once for the forward and
+  // the backward of every sub-shard: on a sample of the host rows while they are still to be
+  // uploaded, else by the device check (the stream is between evaluations here)
+  if (use_rt(e->P) && e->in.n > 0) {
+    if (e->rt_np == 0) {  // cached until the next set_data / broadcast
+      if (e->pending_upload) {
+        const int64_t n = e->cfg.n_local, ldm = e->h_mu.ld ? e->h_mu.ld : n;
+        e->rt_np = rt_decide_pieces_host(e->P, e->h_mu.data, ldm, n, 256, e->z.v.data(), e->z.r);
+      } else {
+        e->rt_np = rt_decide_pieces(e->P, ctx->stream);
+        if (e->rt_np < 0) {
+          e->rt_np = 0;
+          throw CudaError("exponent precision check failed");
+        }
+      }
+    }
+    for (auto& sub : e->subs) sub.P.rt_pieces = e->rt_np;
+  }
   CUDA_OK(cudaEventRecord(e->ev[0], ctx->stream));
   if (e->pending_upload) {  // copy stream: mu / S of sub-shard j, then the forward of j waits for it
     CUDA_OK(cudaEventRecord(e->ev_out[0], ctx->stream));  // previous users of the device rows are done
@@ -1024,6 +1043,7 @@ int sgpx_engine_set_data(sgpx_engine* e, sgpx_cmat x_or_mu, sgpx_cmat s, sgpx_cm
       in.ld_s = n;
     }
     e->has_data = true;
+    e->rt_np = 0;
     if (e->has_params) {
       e->P.mu = in.mu;
       e->P.ld_mu = in.ld_mu;
@@ -1078,6 +1098,7 @@ int sgpx_engine_broadcast(sgpx_engine* e, const sgpx_kernel_spec* kernel, double
     e->beta = beta;
     e->P = make_const(e->ctx, e->in, k, zm, e->zc, e->z64, e->h_stage);
     e->has_params = true;
+    e->rt_np = 0;
     e->coordinated = false;
   });
 }
