@@ -1293,6 +1293,7 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
     case 10: return fn<10>(__VA_ARGS__);       \
     case 12: return fn<12>(__VA_ARGS__);       \
     case 16: return fn<16>(__VA_ARGS__);       \
+    case 20: return fn<20>(__VA_ARGS__);       \
     default: return 1;                         \
   }
 
@@ -1300,7 +1301,7 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
 
 bool rt_supported(const PsiConst& P) {
   const int q = instantiated_q(P.q);
-  return P.q >= 1 && q <= 16 && P.m >= 1 && rt_cfg(q, true).nP >= 2 && rt_cfg(q, false).nP >= 2 &&
+  return P.q >= 1 && q <= 20 && P.m >= 1 && rt_cfg(q, true).nP >= 2 && rt_cfg(q, false).nP >= 2 &&
          rt_cfg(q, true, false, 3).nP >= 2 && rt_cfg(q, false, false, 3).nP >= 2;
 }
 int64_t rt_fwd_doubles(const PsiConst& P, int num_sms) { return fwd_layout(P, num_sms).doubles; }

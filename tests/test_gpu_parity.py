@@ -62,7 +62,8 @@ def test_stats_parity(sgp, orc, shape, expected):
 
 
 @pytest.mark.parametrize("shape", [(300, 3, 4, 7), (1, 1, 1, 1), (33, 2, 1, 5), (257, 10, 10, 100),
-                                   (100, 1, 3, 50), (64, 20, 5, 12), (1000, 8, 2, 33)])
+                                   (100, 1, 3, 50), (64, 20, 5, 12), (1000, 8, 2, 33), (64, 12, 5, 12),
+                                   (2000, 16, 6, 50)])
 @pytest.mark.parametrize("expected", [True, False])
 def test_grads_parity(sgp, orc, shape, expected):
     n, q, d, m = shape
@@ -152,7 +153,7 @@ def test_engine_evaluate_parity(sgp, orc, latent):
         assert norm_rel_err(g.d_s, ref.d_s) < GRAD_TOL
 
 
-@pytest.mark.parametrize("shape", [(100000, 8, 50, 48), (30000, 10, 50, 100)])
+@pytest.mark.parametrize("shape", [(100000, 8, 50, 48), (30000, 10, 50, 100), (2000, 20, 6, 256), (20000, 18, 10, 64)])
 def test_multi_chunk_parity(sgp, orc, shape):
     """Shards large enough that every CTA of every kernel walks many chunks (pipelined producer /
     consumer rings wrap several times; psi1 tiles exceed one per thread)."""
