@@ -286,10 +286,18 @@ __global__ void __launch_bounds__(256) rt_pair_rows_kernel(PsiConst P, int64_t p
 // Datapoint rows H_n, n < n_pad (padded rows [0 .., 0, -huge]): canonical K-major pieces (static
 // operand of the backward, piece i at hs + i * pstride) and, per 96-row chunk, the forward's
 // streamed operands X = H_n, Y = [1, d2 mu, d2] in the processed-stage layout.
-template <int Q, bool PAIR, int NP>
+// Forward G scale: G = 2^sg v with v <= sigma^4 (c2 <= sigma^4, pconst <= 1, exp <= 1), so G stays
+// below 2^15 in fp16; folded into the streamed copy of B_n and undone by the output scale.
+__host__ __device__ inline int rt_fwd_gshift(float log2_var) { return 15 - int(ceilf(2.0f * log2_var)); }
+
+template <int Q, bool BF, bool PAIR, int NP>
 __global__ void __launch_bounds__(256) rt_data_rows_kernel(PsiConst P, int64_t n_pad, float* __restrict__ hs,
-                                                            int64_t pstride, float* __restrict__ pre) {
+                                                            int64_t pstride, float* __restrict__ pre,
+                                                            const float* __restrict__ ys) {
   constexpr int K1 = RT<Q, true>::K1;
+  float ysc[RT<Q, true>::N3];
+#pragma unroll
+  for (int k = 0; k < RT<Q, true>::N3; ++k) ysc[k] = BF ? 1.f : __ldg(ys + k);
   for (int64_t n = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; n < n_pad; n += int64_t(gridDim.x) * blockDim.x) {
     const bool valid = n < P.n;
     const int64_t nn = valid ? n : 0;
@@ -330,8 +338,52 @@ __global__ void __launch_bounds__(256) rt_data_rows_kernel(PsiConst P, int64_t n
       h[2 * Q + 1] = kNegHuge;
     }
     put_rows<NP>(hs, pstride, n, h, K1);
-    put_pre_row<Q, true, PAIR, NP>(pre + (n / kCH) * RT<Q, true, PAIR, NP>::CHF, int(n % kCH), h, y);
+    if (!BF && valid) h[2 * Q + 1] += double(rt_fwd_gshift(P.log2_var));
+    put_pre_row<Q, BF, PAIR, NP>(pre + (n / kCH) * RT<Q, BF, PAIR, NP>::CHF, int(n % kCH), h, y, ysc);
   }
+}
+
+// Forward fp16 column scales of Y = [1, d2 mu, d2]: per-q maxima of |d2 mu| and d2 over the rows
+// (non-negative floats order as their bit patterns, so atomicMax on the bits is exact and
+// order-independent); `mx` is zeroed by the caller.
+template <int Q>
+__global__ void __launch_bounds__(256) rt_fwd_ymax_kernel(PsiConst P, unsigned* __restrict__ mx) {
+  float a[2 * Q];
+#pragma unroll
+  for (int k = 0; k < 2 * Q; ++k) a[k] = 0.f;
+  for (int64_t n = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; n < P.n; n += int64_t(gridDim.x) * blockDim.x) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      if (q < P.q) {
+        const double mu = __ldg(P.mu + q * P.ld_mu + n) - P.center[q];
+        const double sv = P.expected ? __ldg(P.s + q * P.ld_s + n) : 0.0;
+        const double il2 = 1.0 / (P.ls[q] * P.ls[q]);
+        const double d2 = il2 / (1.0 + 2.0 * sv * il2);
+        a[q] = fmaxf(a[q], fabsf(float(d2 * mu)));
+        a[Q + q] = fmaxf(a[Q + q], float(d2));
+      }
+  }
+#pragma unroll
+  for (int k = 0; k < 2 * Q; ++k) {
+    float v = a[k];
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0 && v > 0.f) atomicMax(mx + k, __float_as_uint(v));
+  }
+}
+
+// ys[k] = 2^(14 - e_k) for a column maximum m 2^e_k (m in [1/2, 1)); ys[64 + k] undoes it and the
+// G scale 2^sg.
+template <int Q>
+__global__ void rt_fwd_yscale_kernel(PsiConst P, const unsigned* __restrict__ mx, float* __restrict__ ys) {
+  const int k = threadIdx.x;
+  if (k >= 64) return;
+  float v = 0.f;
+  if (k == 0) v = 1.f;
+  else if (k <= 2 * Q) v = __uint_as_float(mx[k - 1]);
+  int e = 0;
+  if (v > 0.f && isfinite(v)) frexpf(v, &e);
+  ys[k] = ldexpf(1.f, 14 - e);
+  ys[64 + k] = ldexpf(1.f, e - 14 - rt_fwd_gshift(P.log2_var));
 }
 
 // Backward fp16 scales: yscale[k] = 2^(14 - e_k) with max_p |Y_pk| = m 2^e_k (m in [1/2, 1)), so
@@ -964,7 +1016,7 @@ struct FwdLayout {  // inside the forward partial buffer, after the psi1 rows (o
   int64_t nchunks;  // datapoint chunks
   int64_t npairs, p_pad, n_pad;
   int64_t off_part, off_sums, off_floats;  // pair_part, pair_sums, then 32-bit operand arrays
-  int64_t f_fs, f_hs, f_pre, floats;       // word offsets relative to off_floats (sized for 3 pieces)
+  int64_t f_fs, f_hs, f_pre, f_ys, floats;  // word offsets relative to off_floats (sized for 3 pieces)
   int64_t doubles;                                  // total doubles after the psi1 rows
 };
 
@@ -996,7 +1048,8 @@ FwdLayout fwd_layout(const PsiConst& P, int num_sms) {
   L.f_fs = 0;                                  // pair pieces, p_pad * K1 words apart
   L.f_hs = L.f_fs + 3 * L.p_pad * K1;          // datapoint pieces, n_pad * K1 words apart
   L.f_pre = L.f_hs + 3 * L.n_pad * K1;
-  L.floats = L.f_pre + (L.n_pad / kCH) * rt_pf(q, true, false, 3);  // same chunk size in PAIR layout
+  L.f_ys = L.f_pre + (L.n_pad / kCH) * rt_pf(q, true, false, 3);    // same chunk size in PAIR layout
+  L.floats = L.f_ys + 192;  // forward Y scales: yscale[64], yinv[64], column maxima[64] (bits)
   L.doubles = L.off_floats + (L.floats + 1) / 2 + 2;
   return L;
 }
@@ -1125,6 +1178,17 @@ int rt_dbg() {
 // CTA-pair kernels (cta_group::2) are correct but not yet faster than the single-CTA ones: the
 // cross-SM barrier round trips set a ~2.4 ms synchronisation floor at C3 (profiles/
 // r01_ncu_rowtile_summary.md).  Opt in with SGPX_RT_PAIR=1.
+// Forward MMA3 pieces: bf16 hi / lo (~2^-17, 16 % faster consumers) with the two-piece MMA1, fp16
+// hi / lo (~2^-22, scaled) with the three-piece MMA1: the wide-spread regime where the d_z assembly
+// R1 - zbar R0 from the pair sums cancels.  SGPX_RT_FWD_BF16=0|1 overrides (A/B).
+bool rt_fwd_bf16(int np) {
+  static const int v = [] {
+    const char* e = getenv("SGPX_RT_FWD_BF16");
+    return e ? (atoi(e) != 0 ? 1 : 0) : -1;
+  }();
+  return v < 0 ? np == 2 : v == 1;
+}
+
 int rt_pair_env() {
   static const int v = [] {
     const char* e = getenv("SGPX_RT_PAIR");
@@ -1200,24 +1264,42 @@ int rt_forward_q(const PsiConst& P, double* base, double* packed, int num_sms, c
   R.out = base + L.off_part;
   const int blocks_p = int(std::min<int64_t>((L.p_pad + 255) / 256, int64_t(num_sms) * 8));
   const int blocks_n = int(std::min<int64_t>((L.n_pad + 255) / 256, int64_t(num_sms) * 8));
-  auto run = [&](auto np_tag) -> int {
+  float* ys = fl + L.f_ys;
+  const bool bf = rt_fwd_bf16(np);
+  if (!bf) {  // fp16 pieces (~2^-22): column scales of Y from the data
+    unsigned* mx = reinterpret_cast<unsigned*>(ys + 128);
+    if (cudaMemsetAsync(mx, 0, 64 * sizeof(unsigned), st) != cudaSuccess) return 3;
+    const int blocks_m = int(std::max<int64_t>(1, std::min<int64_t>((P.n + 255) / 256, int64_t(num_sms) * 4)));
+    rt_fwd_ymax_kernel<Q><<<blocks_m, 256, 0, st>>>(P, mx);
+    rt_fwd_yscale_kernel<Q><<<1, 64, 0, st>>>(P, mx, ys);
+    g_tc_launches.fetch_add(2);
+    R.yinv = ys + 64;
+  }
+  auto run = [&](auto np_tag, auto bf_tag) -> int {
     constexpr int NP = decltype(np_tag)::value;
+    constexpr bool BF = decltype(bf_tag)::value;
     rt_pair_rows_kernel<Q, NP><<<blocks_p, 256, 0, st>>>(P, L.p_pad, fl + L.f_fs, L.p_pad * C::K1);
     if (NP == 2 && pair)
-      rt_data_rows_kernel<Q, true, 2><<<blocks_n, 256, 0, st>>>(P, L.n_pad, fl + L.f_hs, L.n_pad * C::K1, fl + L.f_pre);
+      rt_data_rows_kernel<Q, BF, true, 2><<<blocks_n, 256, 0, st>>>(P, L.n_pad, fl + L.f_hs, L.n_pad * C::K1,
+                                                                    fl + L.f_pre, ys);
     else
-      rt_data_rows_kernel<Q, false, NP><<<blocks_n, 256, 0, st>>>(P, L.n_pad, fl + L.f_hs, L.n_pad * C::K1,
-                                                                  fl + L.f_pre);
+      rt_data_rows_kernel<Q, BF, false, NP><<<blocks_n, 256, 0, st>>>(P, L.n_pad, fl + L.f_hs, L.n_pad * C::K1,
+                                                                      fl + L.f_pre, ys);
     g_tc_launches.fetch_add(2);
-    if constexpr (NP == 2 && RT<Q, true, true>::kConcat) {
+    if constexpr (NP == 2 && RT<Q, BF, true>::kConcat) {
       if (pair) {
         const unsigned gx = unsigned((R.ntiles + 1) / 2 * 2);
-        return launch_rowtile<Q, true, true, 2>(P, R, dim3(gx, unsigned(L.ns)), st);
+        return launch_rowtile<Q, BF, true, 2>(P, R, dim3(gx, unsigned(L.ns)), st);
       }
     }
-    return launch_rowtile<Q, true, false, NP>(P, R, dim3(unsigned(R.ntiles), unsigned(L.ns)), st);
+    return launch_rowtile<Q, BF, false, NP>(P, R, dim3(unsigned(R.ntiles), unsigned(L.ns)), st);
   };
-  if (int rc = np == 3 ? run(std::integral_constant<int, 3>{}) : run(std::integral_constant<int, 2>{})) return rc;
+  using T2 = std::integral_constant<int, 2>;
+  using T3 = std::integral_constant<int, 3>;
+  using BT = std::true_type;
+  using BFa = std::false_type;
+  const int rc = np == 3 ? (bf ? run(T3{}, BT{}) : run(T3{}, BFa{})) : (bf ? run(T2{}, BT{}) : run(T2{}, BFa{}));
+  if (rc) return rc;
   const int64_t tot = L.npairs * C::NH;
   rt_pair_reduce_kernel<<<int(std::min<int64_t>((tot + 255) / 256, 4096)), 256, 0, st>>>(
       base + L.off_part, L.ns, L.npairs, C::NH, base + L.off_sums, packed);
