@@ -642,12 +642,20 @@ int impl_forced() {
   return forced;
 }
 
-// Row-tile tensor-core psi2 (default for the expected / GP-LVM path when it fits); SGPX_PSI_IMPL=simt|tc
-// selects the older kernels.  The deterministic (SGPR) path stays on the direct-difference kernels:
-// its kernel is narrower (den = 1/l^2, no 2S), the weighted pairs sit closer to z-bar and the
-// backward's exponent-as-GEMM sums (T1 - zbar T0) cancel harder, so d_z exceeds the 5e-5 tolerance
-// from Q ~ 8 on (tools/dbg_q.py).
-bool use_rt(const PsiConst& P) { return impl_forced() == 0 && P.expected && rt_supported(P); }
+// Row-tile tensor-core psi2: the default where it fits; SGPX_PSI_IMPL=simt|tc selects the older
+// kernels.  The deterministic (SGPR) kernel is narrower (den = 1/l^2, no 2S), so its pairs with
+// weight sit closer to z-bar and the assembly from the exponent-as-GEMM sums cancels harder: it runs
+// in the precise mode (rt_pieces) and only up to Q = 12 — beyond that d_l from the backward sums
+// exceeds the 5e-5 tolerance (6e-5 .. 9e-5 at Q = 18 / 20), and the direct-difference kernels run
+// (tools/dbg_q.py, profiles/accuracy/r01_q_sweep_*.log).  SGPX_RT_DET=0|1 overrides (A/B).
+bool use_rt(const PsiConst& P) {
+  static const int det = [] {
+    const char* e = getenv("SGPX_RT_DET");
+    return e ? (atoi(e) != 0 ? 1 : 0) : -1;
+  }();
+  const bool det_ok = det < 0 ? instantiated_q(P.q) <= 12 : det == 1;
+  return impl_forced() == 0 && (P.expected || det_ok) && rt_supported(P);
+}
 
 const double* rt_fwd_region(const PsiConst& P, const double* fwd_part, int num_sms) {
   return fwd_part + int64_t(psi1_fwd_rows(P, num_sms)) * fwd_part_count(P.m, P.d);

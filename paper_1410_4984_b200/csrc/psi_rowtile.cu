@@ -1148,6 +1148,7 @@ int rt_forced_pieces() {
 int rt_pieces(const PsiConst& P, cudaStream_t st) {
   if (P.rt_pieces == 2 || P.rt_pieces == 3) return P.rt_pieces;
   if (const int f = rt_forced_pieces()) return f;
+  if (!P.expected) return 3;  // deterministic kernel (den = 1/l^2): always the precise mode
   if (P.n <= 0) return 2;
   static std::mutex mu;
   static double* part = nullptr;
@@ -1401,6 +1402,7 @@ int rt_decide_pieces(const PsiConst& P, void* stream) {
 int rt_decide_pieces_host(const PsiConst& P, const double* mu_host, int64_t ld, int64_t n, int64_t stride,
                           const double* z_host, int64_t m) {
   if (const int f = rt_forced_pieces()) return f;
+  if (!P.expected) return 3;
   // `stride` = rows per sampled block: 16 evenly spaced contiguous blocks (cache-friendly on pinned
   // host memory)
   double smu = 0.0;
