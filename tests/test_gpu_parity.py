@@ -173,6 +173,24 @@ def test_multi_chunk_parity(sgp, orc, shape):
     assert norm_rel_err(g.d_s, wg.d_s) < GRAD_TOL
 
 
+@pytest.mark.parametrize("shape", [(100000, 8, 1, 48), (3000, 8, 1, 500), (20000, 12, 3, 100)])
+def test_sgpr_multi_chunk_parity(sgp, orc, shape):
+    """Deterministic (SGPR) mode on the row-tile path (precise mode, Q <= 12), many chunks per CTA;
+    (3000, 8, 1, 500) is the C4 shape at an oracle-sized N (125,250 pairs)."""
+    n, q, d, m = shape
+    x, _, y, z, var, ls = problem(11, n, q, d, m)
+    rng = np.random.default_rng(12)
+    adj = sym_adj(rng, m, d)
+    k = sgp.KernelSpec(var, ls)
+    st, g = sgp.sweep_stats(False, x, None, y, z, k, adj=sgp.StatsAdjoints(*adj))
+    wst, wg = orc.sweep_stats(False, x, None, y, z, var, ls, adj=adj)
+    assert norm_rel_err(st.phi_big, wst.phi_big) < STAT_TOL
+    assert norm_rel_err(st.psi_y, wst.psi_y) < STAT_TOL
+    assert norm_rel_err(g.d_z, wg.d_z) < GRAD_TOL
+    assert norm_rel_err(g.d_lengthscales, wg.d_lengthscales) < GRAD_TOL
+    assert rel_err(g.d_variance, wg.d_variance) < GRAD_TOL
+
+
 @pytest.mark.parametrize("spread", [1.0, 2.0, 8.0, 16.0])
 def test_data_spread_envelope(sgp, orc, spread):
     """mu ~ N(0, spread^2) with Z drawn from mu and l in [0.5, 2]: the exponent-as-GEMM features
