@@ -221,13 +221,19 @@ def test_data_spread_envelope(sgp, orc, spread):
     assert norm_rel_err(g.d_z, wg.d_z) < grad_tol
 
 
-def test_engine_subshard_pipeline(sgp):
+@pytest.mark.parametrize("spread", [1.0, 8.0])
+def test_engine_subshard_pipeline(sgp, spread):
     """Host-resident mu / S (streamed per sub-shard with the kernels) and registered host
-    gradient outputs give the same evaluation as the device-resident single pass."""
+    gradient outputs give the same evaluation as the device-resident single pass.  spread 8
+    selects the precise mode (host-sample decision for the streamed path, device reduction for the
+    resident one); its forward Y scales are per sub-shard, so the two runs agree to the fp16-piece
+    rounding instead of bitwise."""
     import torch
 
     n, q, d, m = 600_000, 4, 3, 24  # >= 500k rows: two sub-shards
     mu, s, y, z, var, ls = problem(9, n, q, d, m)
+    mu = mu * spread
+    z = z * spread
     k = sgp.KernelSpec(var, ls)
     dev = torch.device("cuda", 0)
     ctx = sgp.Context(0)
@@ -247,8 +253,9 @@ def test_engine_subshard_pipeline(sgp):
     for _ in range(2):  # second evaluation reuses the registered buffers
         e2.broadcast(k, 50.0, z, mu, s)
         r2 = e2.evaluate(True)
-    assert rel_err(r2.bound.total, r1.bound.total) < 1e-12
-    assert norm_rel_err(r2.grads.d_z, r1.grads.d_z) < 1e-10
-    assert norm_rel_err(r2.grads.d_lengthscales, r1.grads.d_lengthscales) < 1e-10
+    tb, tg, tl = (1e-12, 1e-10, 1e-13) if spread == 1.0 else (1e-7, 2e-5, 1e-6)
+    assert rel_err(r2.bound.total, r1.bound.total) < tb
+    assert norm_rel_err(r2.grads.d_z, r1.grads.d_z) < tg
+    assert norm_rel_err(r2.grads.d_lengthscales, r1.grads.d_lengthscales) < tg
     assert r2.grads.d_mu is gmu and r2.grads.d_s is gs
-    assert norm_rel_err(gmu, r1.grads.d_mu) < 1e-13 and norm_rel_err(gs, r1.grads.d_s) < 1e-13
+    assert norm_rel_err(gmu, r1.grads.d_mu) < tl and norm_rel_err(gs, r1.grads.d_s) < tl
