@@ -645,15 +645,15 @@ int impl_forced() {
 // Row-tile tensor-core psi2: the default where it fits; SGPX_PSI_IMPL=simt|tc selects the older
 // kernels.  The deterministic (SGPR) kernel is narrower (den = 1/l^2, no 2S), so its pairs with
 // weight sit closer to z-bar and the assembly from the exponent-as-GEMM sums cancels harder: it runs
-// in the precise mode (rt_pieces) and only up to Q = 12 — beyond that d_l from the backward sums
-// exceeds the 5e-5 tolerance (6e-5 .. 9e-5 at Q = 18 / 20), and the direct-difference kernels run
-// (tools/dbg_q.py, profiles/accuracy/r01_q_sweep_*.log).  SGPX_RT_DET=0|1 overrides (A/B).
+// in the precise mode (rt_pieces) and only up to Q = 16 (d_l <= 2.1e-5) — beyond that d_l from the
+// backward sums exceeds the 5e-5 tolerance (6e-5 .. 9e-5 at Q = 18 / 20), and the direct-difference
+// kernels run (tools/dbg_q.py, profiles/accuracy/r01_q_sweep_*.log).  SGPX_RT_DET=0|1 overrides (A/B).
 bool use_rt(const PsiConst& P) {
   static const int det = [] {
     const char* e = getenv("SGPX_RT_DET");
     return e ? (atoi(e) != 0 ? 1 : 0) : -1;
   }();
-  const bool det_ok = det < 0 ? instantiated_q(P.q) <= 12 : det == 1;
+  const bool det_ok = det < 0 ? instantiated_q(P.q) <= 16 : det == 1;
   return impl_forced() == 0 && (P.expected || det_ok) && rt_supported(P);
 }
 

@@ -175,7 +175,7 @@ def test_multi_chunk_parity(sgp, orc, shape):
 
 @pytest.mark.parametrize("shape", [(100000, 8, 1, 48), (3000, 8, 1, 500), (20000, 12, 3, 100)])
 def test_sgpr_multi_chunk_parity(sgp, orc, shape):
-    """Deterministic (SGPR) mode on the row-tile path (precise mode, Q <= 12), many chunks per CTA;
+    """Deterministic (SGPR) mode on the row-tile path (precise mode, Q <= 16), many chunks per CTA;
     (3000, 8, 1, 500) is the C4 shape at an oracle-sized N (125,250 pairs)."""
     n, q, d, m = shape
     x, _, y, z, var, ls = problem(11, n, q, d, m)
