@@ -173,7 +173,8 @@ def test_multi_chunk_parity(sgp, orc, shape):
     assert norm_rel_err(g.d_s, wg.d_s) < GRAD_TOL
 
 
-@pytest.mark.parametrize("shape", [(100000, 8, 1, 48), (3000, 8, 1, 500), (20000, 12, 3, 100)])
+@pytest.mark.parametrize("shape", [(100000, 8, 1, 48), (3000, 8, 1, 500), (20000, 12, 3, 100),
+                                   (20000, 16, 2, 64)])
 def test_sgpr_multi_chunk_parity(sgp, orc, shape):
     """Deterministic (SGPR) mode on the row-tile path (precise mode, Q <= 16), many chunks per CTA;
     (3000, 8, 1, 500) is the C4 shape at an oracle-sized N (125,250 pairs)."""
