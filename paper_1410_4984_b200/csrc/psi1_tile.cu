@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(256, 2)
     double v = k < P.q ? 0.0 : dv_acc;
 #pragma unroll
     for (int q = 0; q < Q; ++q)
-      if (q == k) v = dl_acc[q];
+      if (q == k && k < P.q) v = dl_acc[q];  // k == P.q is d var (a padded template Q has q == P.q)
     red[tid] = v;
     __syncthreads();
     for (int w = nthr / 2; w > 0; w >>= 1) {

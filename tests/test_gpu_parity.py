@@ -173,6 +173,37 @@ def test_multi_chunk_parity(sgp, orc, shape):
     assert norm_rel_err(g.d_s, wg.d_s) < GRAD_TOL
 
 
+def _random_shapes(count=10, seed=2024):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        out.append((int(rng.integers(1, 5000)), int(rng.choice([1, 2, 3, 5, 7, 9, 10, 11, 13, 16, 17, 20])),
+                    int(rng.integers(0, 13)), int(rng.integers(1, 141)), bool(rng.integers(0, 2))))
+    return out
+
+
+@pytest.mark.parametrize("shape", _random_shapes())
+def test_random_shapes_parity(sgp, orc, shape):
+    """Seeded random (N, Q, D, M, mode): ragged N (not a multiple of any chunk), Q between the
+    instantiated widths, D = 0 allowed, M up to 140 (psi1 beyond the 128-wide tile)."""
+    n, q, d, m, expected = shape
+    m = min(m, n)  # Z = distinct rows of mu
+    mu, s, y, z, var, ls = problem(31, n, q, d, m)
+    adj = sym_adj(np.random.default_rng(32), m, d)
+    k = sgp.KernelSpec(var, ls)
+    st, g = sgp.sweep_stats(expected, mu, s if expected else None, y, z, k, adj=sgp.StatsAdjoints(*adj))
+    wst, wg = orc.sweep_stats(expected, mu, s if expected else None, y, z, var, ls, adj=adj)
+    assert norm_rel_err(st.phi_big, wst.phi_big) < STAT_TOL
+    if d > 0:
+        assert norm_rel_err(st.psi_y, wst.psi_y) < STAT_TOL
+    assert norm_rel_err(g.d_z, wg.d_z) < GRAD_TOL
+    assert norm_rel_err(g.d_lengthscales, wg.d_lengthscales) < GRAD_TOL
+    assert rel_err(g.d_variance, wg.d_variance) < GRAD_TOL or norm_rel_err(g.d_variance, wg.d_variance) < GRAD_TOL
+    if expected:
+        assert norm_rel_err(g.d_mu, wg.d_mu) < GRAD_TOL
+        assert norm_rel_err(g.d_s, wg.d_s) < GRAD_TOL
+
+
 @pytest.mark.parametrize("shape", [(100000, 8, 1, 48), (3000, 8, 1, 500), (20000, 12, 3, 100),
                                    (20000, 16, 2, 64)])
 def test_sgpr_multi_chunk_parity(sgp, orc, shape):
