@@ -169,6 +169,7 @@ def test_multi_chunk_parity(sgp, orc, shape):
     assert norm_rel_err(st.psi_y, wst.psi_y) < STAT_TOL
     assert norm_rel_err(g.d_z, wg.d_z) < GRAD_TOL
     assert norm_rel_err(g.d_lengthscales, wg.d_lengthscales) < GRAD_TOL
+    assert rel_err(g.d_variance, wg.d_variance) < GRAD_TOL
     assert norm_rel_err(g.d_mu, wg.d_mu) < GRAD_TOL
     assert norm_rel_err(g.d_s, wg.d_s) < GRAD_TOL
 
@@ -182,7 +183,7 @@ def _random_shapes(count=10, seed=2024):
     return out
 
 
-@pytest.mark.parametrize("shape", _random_shapes())
+@pytest.mark.parametrize("shape", _random_shapes() + _random_shapes(12, seed=7))
 def test_random_shapes_parity(sgp, orc, shape):
     """Seeded random (N, Q, D, M, mode): ragged N (not a multiple of any chunk), Q between the
     instantiated widths, D = 0 allowed, M up to 140 (psi1 beyond the 128-wide tile)."""
