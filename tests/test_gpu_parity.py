@@ -130,9 +130,12 @@ def test_bitwise_determinism(sgp):
 
 
 @pytest.mark.parametrize("latent", [True, False])
-def test_engine_evaluate_parity(sgp, orc, latent):
-    """Engine::evaluate(true): bound and every gradient segment vs the oracle engine."""
-    mu, s, y, z, var, ls = problem(6, 3000, 10, 10, 100)
+@pytest.mark.parametrize("shape", [(3000, 10, 10, 100), (2500, 7, 4, 60), (1500, 13, 3, 140)])
+def test_engine_evaluate_parity(sgp, orc, latent, shape):
+    """Engine::evaluate(true): bound and every gradient segment vs the oracle engine (exact and
+    padded Q, psi1 on the tile and on the M > 128 kernels)."""
+    n, q, d, m = shape
+    mu, s, y, z, var, ls = problem(6, n, q, d, m)
     beta = 100.0
     k = sgp.KernelSpec(var, ls)
     eng = sgp.Engine(sgp.ModelKind.latent if latent else sgp.ModelKind.regression, mu, s if latent else None, y)
