@@ -186,6 +186,29 @@ def _random_shapes(count=10, seed=2024):
     return out
 
 
+@pytest.mark.parametrize("shape", _random_shapes(8, seed=99))
+def test_random_engine_parity(sgp, orc, shape):
+    """Engine::evaluate(true) on seeded random shapes / modes: bound, KL, d beta and every gradient."""
+    n, q, d, m, latent = shape
+    d = max(d, 1)
+    m = min(m, n)
+    mu, s, y, z, var, ls = problem(41, n, q, d, m)
+    k = sgp.KernelSpec(var, ls)
+    eng = sgp.Engine(sgp.ModelKind.latent if latent else sgp.ModelKind.regression, mu, s if latent else None, y)
+    eng.broadcast(k, 30.0, z)
+    r = eng.evaluate(True)
+    ref = orc.engine_evaluate(latent, mu, s, y, z, var, ls, 30.0, workers=4)
+    assert rel_err(r.bound.total, ref.bound["total"]) < BOUND_TOL
+    g = r.grads
+    assert norm_rel_err(g.d_z, ref.d_z) < GRAD_TOL
+    assert norm_rel_err(g.d_lengthscales, ref.d_lengthscales) < GRAD_TOL
+    assert rel_err(g.d_variance, ref.d_variance) < GRAD_TOL or norm_rel_err(g.d_variance, ref.d_variance) < GRAD_TOL
+    assert norm_rel_err(g.d_beta, ref.d_beta) < GRAD_TOL
+    if latent:
+        assert norm_rel_err(g.d_mu, ref.d_mu) < GRAD_TOL
+        assert norm_rel_err(g.d_s, ref.d_s) < GRAD_TOL
+
+
 @pytest.mark.parametrize("shape", _random_shapes() + _random_shapes(12, seed=7))
 def test_random_shapes_parity(sgp, orc, shape):
     """Seeded random (N, Q, D, M, mode): ragged N (not a multiple of any chunk), Q between the
