@@ -209,6 +209,28 @@ def test_random_engine_parity(sgp, orc, shape):
         assert norm_rel_err(g.d_s, ref.d_s) < GRAD_TOL
 
 
+@pytest.mark.parametrize("shape", _random_shapes(6, seed=5))
+def test_random_shapes_precise_mode(sgp, orc, shape):
+    """Wide latent spread (mu ~ N(0, 4^2): spread^2 >> 60) selects the precise mode (three-piece
+    MMA1, fp16 forward MMA3) on random shapes, padded Q included; expected mode."""
+    n, q, d, m, _ = shape
+    m = min(m, n)
+    mu, s, y, z, var, ls = problem(51, n, q, d, m)
+    mu, z = 4.0 * mu, 4.0 * z
+    adj = sym_adj(np.random.default_rng(52), m, d)
+    k = sgp.KernelSpec(var, ls)
+    st, g = sgp.sweep_stats(True, mu, s, y, z, k, adj=sgp.StatsAdjoints(*adj))
+    wst, wg = orc.sweep_stats(True, mu, s, y, z, var, ls, adj=adj)
+    assert norm_rel_err(st.phi_big, wst.phi_big) < 3e-5
+    if d > 0:
+        assert norm_rel_err(st.psi_y, wst.psi_y) < STAT_TOL
+    assert norm_rel_err(g.d_z, wg.d_z) < GRAD_TOL
+    assert norm_rel_err(g.d_lengthscales, wg.d_lengthscales) < GRAD_TOL
+    assert rel_err(g.d_variance, wg.d_variance) < GRAD_TOL or norm_rel_err(g.d_variance, wg.d_variance) < GRAD_TOL
+    assert norm_rel_err(g.d_mu, wg.d_mu) < GRAD_TOL
+    assert norm_rel_err(g.d_s, wg.d_s) < GRAD_TOL
+
+
 @pytest.mark.parametrize("shape", _random_shapes() + _random_shapes(12, seed=7))
 def test_random_shapes_parity(sgp, orc, shape):
     """Seeded random (N, Q, D, M, mode): ragged N (not a multiple of any chunk), Q between the
