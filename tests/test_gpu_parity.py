@@ -63,7 +63,7 @@ def test_stats_parity(sgp, orc, shape, expected):
 
 @pytest.mark.parametrize("shape", [(300, 3, 4, 7), (1, 1, 1, 1), (33, 2, 1, 5), (257, 10, 10, 100),
                                    (100, 1, 3, 50), (64, 20, 5, 12), (1000, 8, 2, 33), (64, 12, 5, 12),
-                                   (2000, 16, 6, 50)])
+                                   (2000, 16, 6, 50), (500, 21, 3, 20), (300, 32, 2, 16)])
 @pytest.mark.parametrize("expected", [True, False])
 def test_grads_parity(sgp, orc, shape, expected):
     n, q, d, m = shape
