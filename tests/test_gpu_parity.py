@@ -302,8 +302,9 @@ def test_data_spread_envelope(sgp, orc, spread):
     assert norm_rel_err(g.d_z, wg.d_z) < grad_tol
 
 
+@pytest.mark.parametrize("q", [4, 7])
 @pytest.mark.parametrize("spread", [1.0, 8.0])
-def test_engine_subshard_pipeline(sgp, spread):
+def test_engine_subshard_pipeline(sgp, spread, q):
     """Host-resident mu / S (streamed per sub-shard with the kernels) and registered host
     gradient outputs give the same evaluation as the device-resident single pass.  spread 8
     selects the precise mode (host-sample decision for the streamed path, device reduction for the
@@ -311,7 +312,7 @@ def test_engine_subshard_pipeline(sgp, spread):
     rounding instead of bitwise."""
     import torch
 
-    n, q, d, m = 600_000, 4, 3, 24  # >= 500k rows: two sub-shards
+    n, d, m = 600_000, 3, 24  # >= 500k rows: two sub-shards
     mu, s, y, z, var, ls = problem(9, n, q, d, m)
     mu = mu * spread
     z = z * spread
