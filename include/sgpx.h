@@ -31,8 +31,16 @@
  *   - Threading: a context (one device + one stream + scratch) is
  *     single-threaded; different contexts may be driven concurrently from
  *     different host threads (reference: pure, reentrant).
- *   - Arithmetic: exponent/Psi tiles in FP32 (FFMA + MUFU.EX2), every sum
- *     across datapoints and across CTAs in fp64, all M-sized algebra in fp64.
+ *   - Arithmetic (the precision mode, SGPX_PREC_*, recorded in every result):
+ *       fast     psi2 exponents as a bilinear form on tcgen05 (two fp16 pieces, ~2^-22
+ *                relative on the feature products), G = 2^D on MUFU.EX2 / FMA (2^-22), the
+ *                psi2 contraction as 16-bit split MMAs (bf16 hi/lo ~2^-17 forward, scaled fp16
+ *                hi/lo ~2^-22 backward), psi1 in fp32 tiles;
+ *       precise  as fast with three fp16 exponent pieces (~2^-33) and fp16 forward MMA3 pieces;
+ *       direct   direct-difference exponents in fp64 (the reference's own form), fp32 exp2 of
+ *                the fraction (2^-22), fp64 contractions;
+ *     every sum across datapoints and across CTAs is fp64, all M-sized algebra is fp64.  AUTO
+ *     picks fast / precise / direct from the spread of the inducing points.
  *   - There is no CPU fallback: without a CUDA device every compute entry point
  *     returns SGPX_CUDA.
  */
@@ -52,7 +60,13 @@ extern "C" {
 #define SGPX_NCCL 4
 #define SGPX_INTERNAL 5
 
-#define SGPX_ABI_VERSION 1
+#define SGPX_ABI_VERSION 2
+
+/* Precision modes (sgpx_engine_config.precision, sgpx_ctx_set_precision). */
+#define SGPX_PREC_AUTO 0
+#define SGPX_PREC_FAST 2
+#define SGPX_PREC_PRECISE 3
+#define SGPX_PREC_DIRECT 4
 
 /* Column-major views (Eigen::Ref<const Matrix> / Eigen::Ref<Matrix>). */
 typedef struct {
@@ -124,6 +138,11 @@ int sgpx_ctx_set_stream(sgpx_ctx* ctx, void* cuda_stream);
 int sgpx_ctx_synchronize(sgpx_ctx* ctx);
 /* Kernel launches issued by this context since creation (profiling evidence). */
 int64_t sgpx_ctx_launch_count(const sgpx_ctx* ctx);
+/* Precision mode of the one-shot entry points (sgpx_sweep_stats); SGPX_PREC_AUTO by default. */
+int sgpx_ctx_set_precision(sgpx_ctx* ctx, int precision);
+/* Mode the last sgpx_sweep_stats of this context ran in (SGPX_PREC_FAST / PRECISE / DIRECT; 0 if
+ * none) and, optionally, the inducing-point spread Tz that decided it. */
+int sgpx_ctx_last_precision(const sgpx_ctx* ctx, double* z_spread);
 
 /* ---- the sweep (psi_stats.hpp:108-326) ------------------------------------- */
 /* expected != 0: q(X) = N(mu, diag s) path (Bayesian GP-LVM); otherwise mu is X
@@ -174,6 +193,7 @@ typedef struct {
   int64_t n_local;   /* rows owned here */
   int64_t q, d, m;
   double jitter_factor; /* factor_gram start (default 1e-6, parallel.hpp:327) */
+  int precision;        /* SGPX_PREC_* (AUTO: chosen per broadcast from the inducing points) */
 } sgpx_engine_config;
 
 typedef struct {
@@ -192,6 +212,8 @@ typedef struct {
   double stats_pass_s, coordinator_s, grad_pass_s, wall_s;
   double fwd_kernel_s, bwd_kernel_s; /* the psi forward / backward kernels alone */
   int fwd_grid, bwd_grid;            /* persistent CTAs launched */
+  int precision_used;                /* SGPX_PREC_FAST / PRECISE / DIRECT of this evaluation */
+  double z_spread;                   /* Tz = max_a sum_q ((z_aq - c_q) / l_q)^2, c = mean of Z */
 } sgpx_eval_result;
 
 int sgpx_engine_create(sgpx_ctx* ctx, const sgpx_engine_config* cfg, sgpx_engine** out);
@@ -201,7 +223,11 @@ int sgpx_engine_destroy(sgpx_engine* eng);
  * x_or_mu, s: n_local x Q (s ignored for regression). */
 int sgpx_engine_set_data(sgpx_engine* eng, sgpx_cmat x_or_mu, sgpx_cmat s, sgpx_cmat y, int on_device);
 /* Engine::broadcast: global params (kernel, beta, Z: host memory, M x Q); mu/s (latent) optional
- * local slice, n_local x Q (data == NULL keeps the current; on_device != 0: device pointers, adopted). */
+ * local slice, n_local x Q (data == NULL keeps the current; on_device != 0: device pointers, adopted).
+ * Host mu / s are NOT copied here: the next stats pass streams them to the device in sub-shards,
+ * overlapped with its kernels, so the caller keeps both host buffers alive and unchanged until that
+ * pass (sgpx_engine_evaluate / sgpx_engine_stats_pass) has returned.  A later set_data cancels the
+ * pending upload. */
 int sgpx_engine_broadcast(sgpx_engine* eng, const sgpx_kernel_spec* kernel, double beta, sgpx_cmat z, sgpx_cmat mu,
                           sgpx_cmat s, int on_device);
 /* Single-rank Engine::evaluate(with_grads): the whole pipeline, no collective. */

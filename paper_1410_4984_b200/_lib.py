@@ -15,6 +15,9 @@ LIB_PATH = os.path.join(PKG_DIR, os.environ.get("SGPX_LIB", "libsgpx.so"))
 HEADER_PATH = os.path.join(ROOT, "include", "sgpx.h")
 
 SGPX_OK, SGPX_INVALID_ARGUMENT, SGPX_NUMERIC, SGPX_CUDA, SGPX_NCCL, SGPX_INTERNAL = range(6)
+SGPX_PREC_AUTO, SGPX_PREC_FAST, SGPX_PREC_PRECISE, SGPX_PREC_DIRECT = 0, 2, 3, 4
+PRECISION_NAMES = {SGPX_PREC_AUTO: "auto", SGPX_PREC_FAST: "fast", SGPX_PREC_PRECISE: "precise",
+                   SGPX_PREC_DIRECT: "direct"}
 
 
 class cmat(C.Structure):
@@ -52,7 +55,8 @@ class bound_breakdown(C.Structure):
 
 class engine_config(C.Structure):
     _fields_ = [("kind", C.c_int), ("n_global", C.c_int64), ("row_begin", C.c_int64), ("n_local", C.c_int64),
-                ("q", C.c_int64), ("d", C.c_int64), ("m", C.c_int64), ("jitter_factor", C.c_double)]
+                ("q", C.c_int64), ("d", C.c_int64), ("m", C.c_int64), ("jitter_factor", C.c_double),
+                ("precision", C.c_int)]
 
 
 class eval_result(C.Structure):
@@ -61,7 +65,8 @@ class eval_result(C.Structure):
                 ("d_lengthscales", C.c_void_p), ("d_variance", C.c_double), ("d_beta", C.c_double),
                 ("jitter_factor_used", C.c_double), ("stats_pass_s", C.c_double), ("coordinator_s", C.c_double),
                 ("grad_pass_s", C.c_double), ("wall_s", C.c_double), ("fwd_kernel_s", C.c_double),
-                ("bwd_kernel_s", C.c_double), ("fwd_grid", C.c_int), ("bwd_grid", C.c_int)]
+                ("bwd_kernel_s", C.c_double), ("fwd_grid", C.c_int), ("bwd_grid", C.c_int),
+                ("precision_used", C.c_int), ("z_spread", C.c_double)]
 
 
 # name -> (restype, argtypes)
@@ -74,6 +79,8 @@ SIGNATURES = {
     "sgpx_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "sgpx_ctx_synchronize": (C.c_int, [C.c_void_p]),
     "sgpx_ctx_launch_count": (C.c_int64, [C.c_void_p]),
+    "sgpx_ctx_set_precision": (C.c_int, [C.c_void_p, C.c_int]),
+    "sgpx_ctx_last_precision": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "sgpx_sweep_stats": (C.c_int, [C.c_void_p, C.c_int, cmat, cmat, cmat, cmat, C.POINTER(kernel_spec),
                                    C.POINTER(tile_config), C.POINTER(stats_adjoints), C.POINTER(sufficient_stats),
                                    C.POINTER(stats_grads)]),

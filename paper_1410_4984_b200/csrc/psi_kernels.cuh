@@ -18,7 +18,15 @@
 
 namespace sgpx {
 
-constexpr int kMaxQ = 32;
+constexpr int kMaxQ = 64;
+
+// Exponent / precision mode of one evaluation, decided on the host from the
+// inducing points before any launch (psi_select_mode) and recorded in every result:
+//   kModeFast     row-tile tcgen05 path, two fp16 pieces per exponent feature, bf16 forward MMA3
+//   kModePrecise  row-tile tcgen05 path, three fp16 pieces, scaled fp16 forward MMA3
+//   kModeDirect   direct-difference kernels with fp64 exponents (psi_direct.cu): accurate for any
+//                 spread of the data and any Q <= kMaxQ
+constexpr int kModeAuto = 0, kModeFast = 2, kModePrecise = 3, kModeDirect = 4;
 
 // Per-launch constants (passed by value; ~0.7 KB of kernel parameter space).
 struct PsiConst {
@@ -37,7 +45,7 @@ struct PsiConst {
   float il2[kMaxQ], l2[kMaxQ];
   double ls[kMaxQ];
   unsigned long long* prof;   // optional per-phase cycle counters (SGPX_TC_PROFILE=1), else null
-  int rt_pieces;              // row-tile MMA1 fp16 pieces: 2 or 3, 0 = decide per call (rt_decide_pieces)
+  int mode;                   // kModeFast / kModePrecise / kModeDirect (psi_select_mode)
 };
 
 // Backward-only inputs.
@@ -65,40 +73,43 @@ struct LaunchGeom {
   size_t smem;
 };
 
-// Latent dimensions with an instantiated kernel; other Q are zero-padded up.
+// Latent dimensions with an instantiated row-tile / psi1 kernel; other Q are zero-padded up.
 int instantiated_q(int q);
-// Launch geometry the launchers will use (grid = persistent CTAs), so callers can
-// size the per-CTA partial buffers: rows x fwd_part_count / bwd_part_count.
+
+// Spread of the inducing points in lengthscale units about the centre P.center:
+// Tz = max_a sum_q ((z_aq - c_q) / l_q)^2 (z: m x q column-major, host).  The exponent-as-GEMM
+// error of the row-tile path grows with it; datapoints far from every inducing point
+// do not need a bound (their terms underflow; the feature kernel zeroes rows whose exponents cannot
+// reach the fp16 range).
+double psi_z_spread(const PsiConst& P, const double* z_host, int64_t m);
+// Mode for these inputs: `requested` (kModeAuto or a forced mode; SGPX_PSI_MODE=fast|precise|direct
+// overrides auto for experiments) resolved against the measured envelope and the row-tile
+// instantiations.  Forced fast / precise fall back to direct where the row-tile path cannot run.
+int psi_select_mode(const PsiConst& P, const double* z_host, int64_t m, int requested);
+
+// Launch geometry the launchers will use, so callers can size the partial buffers:
+// geom->grid rows of fwd_part_count / bwd_part_count doubles.
 int plan_forward(const PsiConst& P, int num_sms, LaunchGeom* geom);
 int plan_backward(const PsiConst& P, int num_sms, LaunchGeom* geom);
 
-// Host launchers (psi_kernels.cu).  All are asynchronous on `stream`.
-// Forward: writes `part` (grid rows of fwd_part_count) and reduces them into
-// `packed` (sgpx packed-stats layout, see sgpx.h) in fixed CTA order.  err_flag
-// receives bit 1 for non-finite mu / x / y, bit 4 for a non-positive or non-finite S.
-// ev_begin / ev_end (cudaEvent_t, nullable) are recorded immediately around the
-// main kernel so callers can time it alone (roofline evidence).
+// Host launchers, asynchronous on `stream`, by P.mode.  Forward: packed statistics (sgpx.h
+// layout) and, in `part`, the pair sums and feature arrays the backward reuses; err_flag receives
+// bit 1 for non-finite mu / x / y, bit 4 for a non-positive or non-finite S.  Backward: d mu / d S
+// (B.write_local) and the packed gradient vector.  ev_begin / ev_end (cudaEvent_t, nullable) are
+// recorded around the psi kernels so callers can time them alone (roofline evidence).
 int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, int num_sms,
                 void* stream, LaunchGeom* geom, void* ev_begin = nullptr, void* ev_end = nullptr);
 int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
                  LaunchGeom* geom, void* ev_begin = nullptr, void* ev_end = nullptr);
-// Tensor-core (tcgen05) variants, psi_tc.cu.  tc_supported: shapes they handle (M <= 128, Q <= 32).
-bool tc_supported(const PsiConst& P);
-bool tc_backward_available();
-bool tc_backward_fits(const PsiConst& P);
-bool use_tc(const PsiConst& P, bool backward);
-int plan_forward_tc(const PsiConst& P, int num_sms, LaunchGeom* geom);
-int psi_forward_tc(const PsiConst& P, double* part, double* packed, int* err_flag, int num_sms, void* stream,
-                   LaunchGeom* geom, void* ev_begin, void* ev_end);
-int plan_backward_tc(const PsiConst& P, int num_sms, LaunchGeom* geom);
-int psi_backward_tc(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
-                    LaunchGeom* geom, void* ev_begin, void* ev_end);
+// Where the forward left the region the backward reads (BwdConst::fwd_rt), and the per-pair sums
+// inside it: sub-shard forwards add theirs into the first sub-shard's before the gradient pass.
+const double* fwd_region(const PsiConst& P, const double* fwd_part, int num_sms);
+double* fwd_pair_sums(const PsiConst& P, double* region, int num_sms, int64_t* count);
 
-// Standalone psi1 passes (psi1_kernels.cu), paired with the TC psi2 kernels.
+// psi1 kernels paired with the row-tile psi2 (psi1_kernels.cu: any M; psi1_tile.cu: M <= 128).
 int psi1_fwd_rows(const PsiConst& P, int num_sms);
-int psi1_bwd_ctas(const PsiConst& P, int num_sms);  // legacy kernel: each CTA writes 8 per-warp rows
-int psi1_bwd_rows(const PsiConst& P, int num_sms);  // partial rows psi1_backward writes
-// Tiled psi1 (psi1_tile.cu, M <= 128): one partial row per CTA.
+int psi1_bwd_ctas(const PsiConst& P, int num_sms);
+int psi1_bwd_rows(const PsiConst& P, int num_sms);
 bool psi1_tile_supported(const PsiConst& P, bool bwd);
 int psi1_tile_rows(const PsiConst& P, int num_sms);
 int psi1_tile_forward(const PsiConst& P, double* part, int64_t pstride, int rows, int* err_flag, int with_kl,
@@ -106,6 +117,7 @@ int psi1_tile_forward(const PsiConst& P, double* part, int64_t pstride, int rows
 int psi1_tile_backward(const PsiConst& P, const BwdConst& B, double* part, int64_t pstride, int rows, void* stream);
 int psi1_forward(const PsiConst& P, double* part_rows, int64_t pstride, int rows, int* err_flag, void* stream,
                  int with_kl);
+int psi1_backward(const PsiConst& P, const BwdConst& B, double* part_rows, int64_t pstride, int rows, void* stream);
 // Row-tile tensor-core psi2 (psi_rowtile.cu).  rt_forward writes Phi into packed[4 + p] (run it
 // after the psi1 reduce) and keeps the per-pair gradient sums + feature arrays in `base`
 // (rt_fwd_doubles) for rt_backward, which accumulates the psi2 parts of d_mu / d_s and writes the
@@ -115,25 +127,22 @@ bool use_rt(const PsiConst& P);
 int64_t rt_fwd_doubles(const PsiConst& P, int num_sms);
 int64_t rt_bwd_doubles(const PsiConst& P, int num_sms);
 int rt_forward(const PsiConst& P, double* base, double* packed, int num_sms, void* stream);
-// Row-tile exponent piece count for these inputs (2 or 3; < 0 on a CUDA error): the device-side
-// spread check (synchronises the stream), or the SGPX_PSI_PIECES override.
-int rt_decide_pieces(const PsiConst& P, void* stream);
-// Host-side variant on host mu (column-major, ld): 16 evenly spaced blocks of `stride` rows, for
-// callers whose mu is still on its way to the device.
-int rt_decide_pieces_host(const PsiConst& P, const double* mu_host, int64_t ld, int64_t n, int64_t stride,
-                          const double* z_host, int64_t m);
 int rt_backward(const PsiConst& P, const BwdConst& B, double* bbase, double* prow, int num_sms, void* stream);
-// Where the forward placed the row-tile region inside its partial buffer (BwdConst::fwd_rt).
-const double* rt_fwd_region(const PsiConst& P, const double* fwd_part, int num_sms);
-// The forward's reduced per-pair sums inside that region (npairs x (2Q+1) doubles): sub-shard
-// forwards add theirs into the first sub-shard's before the gradient pass.
 double* rt_fwd_pair_sums(const PsiConst& P, double* region, int num_sms, int64_t* count);
-// Fixed-order reduction of backward partial rows into packed grads (psi_tc.cu).
+// Direct-difference kernels (psi_direct.cu): the complete forward (validation, yy, KL, Phi, Psi) and
+// backward (d mu, d S, d Z, d l, d var) with fp64 exponents.
+bool direct_supported(const PsiConst& P);
+int64_t direct_fwd_doubles(const PsiConst& P, int num_sms);
+int64_t direct_bwd_doubles(const PsiConst& P, int num_sms);
+int direct_forward(const PsiConst& P, double* base, double* packed, int* err_flag, int with_kl, int num_sms,
+                   void* stream);
+int direct_backward(const PsiConst& P, const BwdConst& B, double* bbase, double* packed, int num_sms, void* stream);
+double* direct_fwd_pair_sums(const PsiConst& P, double* base, int num_sms, int64_t* count);
+// Fixed-order reduction of backward partial rows into packed grads.
 // tmp: bwd_reduce_tmp_doubles(pstride) doubles of scratch.
 int64_t bwd_reduce_tmp_doubles(int64_t pstride);
-int bwd_reduce_rows(const double* part, int64_t pstride, int rows, double* packed, double dvar_psi0, double* tmp,
+int bwd_reduce_rows(const double* part, int64_t pstride, int rows, double* packed, double dvar0, double* tmp,
                     void* stream);
-int psi1_backward(const PsiConst& P, const BwdConst& B, double* part_rows, int64_t pstride, int rows, void* stream);
 
 // psi1_expected: out n x m col-major fp64 (ld_out).
 int psi1_matrix(const PsiConst& P, double* out, int64_t ld_out, void* stream);

@@ -70,7 +70,7 @@ constexpr float kHalfMax = 6.0e4f;      // exponent features are clamped to the 
 // own 128 static rows and HALF of every streamed chunk (48 X rows, and Y_hi resp. Y_lo), which
 // halves both the MMA instructions and the L2->SM operand traffic per SM.
 // NP: fp16 pieces per exponent feature (2: hi/lo ~2^-22; 3: hi/mid/lo ~2^-33, six MMA1 products,
-// selected for wide latent spreads by rt_pieces()).
+// selected by the precise mode, psi_select_mode).
 template <int Q, bool BF, bool PAIR = false, int NP = 2>
 struct RT {
   static constexpr int K1 = (2 * Q + 2 + 15) / 16 * 8;  // MMA1 depth in half2 words (K = 2 K1 halves)
@@ -99,10 +99,6 @@ __host__ __device__ constexpr int rt_pf(int q, bool bf, bool pair, int np = 2) {
   (void)bf;
   return np * (pair ? kCH / 2 : kCH) * rt_k1(q) + (pair ? 1 : 2) * rt_n3(q) * kCH / 2;
 }
-__host__ __device__ constexpr bool rt_concat(int q, bool bf) {
-  (void)bf;
-  return 3 * kCH + 4 * rt_n3(q) <= 512;
-}
 inline int64_t pad_rows(int64_t r) { return (r + kPadRows - 1) / kPadRows * kPadRows; }
 
 // Shared-memory pipeline depths: static tile buffers (nA) and streamed operand stages (nP); the
@@ -130,8 +126,6 @@ RtCfg rt_cfg(int q, bool bf, bool pair = false, int np = 2) {
     }
   return RtCfg{0, 0, 0};
 }
-// CTA-pair mode: needs the concatenated MMA3 (one B arrangement per CTA)
-bool rt_pair_ok(int q, bool bf) { return rt_concat(q, bf) && rt_cfg(q, bf, true).nP >= 2; }
 
 // bf16x2 (round to nearest): low half = a (even element), high half = b
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
@@ -334,6 +328,17 @@ __global__ void __launch_bounds__(256) rt_data_rows_kernel(PsiConst P, int64_t n
       h[2 * Q] = 1.0;
       h[2 * Q + 1] = bsum;
       y[0] = 1.f;
+      // A datapoint with B_n < -0.9 * 6e4 sits > 150 lengthscales (in the sqrt(t)-scaled metric) from
+      // every inducing point within the row-tile envelope (Tz <= 600, psi_select_mode): all of its
+      // psi2 terms are below 2^-30000, zero in fp64 as well.  Zeroing the row keeps its features out
+      // of the fp16 clamp, where a clamped B_n with an unclamped cross term would not cancel.
+      if (bsum < -0.9 * double(kHalfMax)) {
+#pragma unroll
+        for (int k = 0; k < 2 * K1; ++k) h[k] = 0.0;
+#pragma unroll
+        for (int k = 0; k < N3; ++k) y[k] = 0.f;
+        h[2 * Q + 1] = kNegHuge;
+      }
     } else {
       h[2 * Q + 1] = kNegHuge;
     }
@@ -1083,90 +1088,8 @@ BwdLayout bwd_layout(const PsiConst& P, int num_sms) {
   return L;
 }
 
-// ---- exponent piece count: the data spread decides (DESIGN.md §4 accuracy envelope) ----
-// spread2 = max(mean_n sum_q ((mu_nq - c_q) / l_q)^2, mean_a sum_q ((z_aq - c_q) / l_q)^2); the
-// two-piece MMA1 holds the 1e-5 / 5e-5 tolerances up to spread2 ~ 60 (tools/dbg_spread.py), beyond
-// it the three-piece MMA1 runs.  Fixed-order reductions: the decision is deterministic, so the
-// forward and the backward of one evaluation agree.
-constexpr int kSpreadBlocks = 256;
-constexpr double kSpread2Fast = 60.0;
-
-__global__ void __launch_bounds__(256) rt_spread_partial_kernel(PsiConst P, double* __restrict__ part) {
-  __shared__ double red[256];
-  double s = 0.0;
-  for (int q = 0; q < P.q; ++q) {
-    const double il = 1.0 / P.ls[q], c = P.center[q];
-    for (int64_t n = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; n < P.n; n += int64_t(gridDim.x) * blockDim.x) {
-      const double v = (P.mu[q * P.ld_mu + n] - c) * il;
-      s += v * v;
-    }
-  }
-  red[threadIdx.x] = s;
-  __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
-}
-
-__global__ void __launch_bounds__(256) rt_spread_final_kernel(PsiConst P, const double* __restrict__ part, int nb,
-                                                              float* __restrict__ out) {
-  __shared__ double rmu[256], rz[256];
-  double smu = 0.0, sz = 0.0;
-  for (int i = threadIdx.x; i < nb; i += 256) smu += part[i];
-  for (int i = threadIdx.x; i < P.m * P.q; i += 256) {
-    const int q = i / P.m;
-    const double v = (P.z64[i] - P.center[q]) * (1.0 / P.ls[q]);
-    sz += v * v;
-  }
-  rmu[threadIdx.x] = smu;
-  rz[threadIdx.x] = sz;
-  __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (threadIdx.x < w) {
-      rmu[threadIdx.x] += rmu[threadIdx.x + w];
-      rz[threadIdx.x] += rz[threadIdx.x + w];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const double mmu = P.n > 0 ? rmu[0] / double(P.n) : 0.0, mz = P.m > 0 ? rz[0] / double(P.m) : 0.0;
-    out[0] = float(mmu > mz ? mmu : mz);
-  }
-}
-
-int rt_forced_pieces() {
-  static const int forced = [] {
-    const char* e = getenv("SGPX_PSI_PIECES");  // 2 or 3: fixed piece count (experiments)
-    const int v = e ? atoi(e) : 0;
-    return (v == 2 || v == 3) ? v : 0;
-  }();
-  return forced;
-}
-
-int rt_pieces(const PsiConst& P, cudaStream_t st) {
-  if (P.rt_pieces == 2 || P.rt_pieces == 3) return P.rt_pieces;
-  if (const int f = rt_forced_pieces()) return f;
-  if (!P.expected) return 3;  // deterministic kernel (den = 1/l^2): always the precise mode
-  if (P.n <= 0) return 2;
-  static std::mutex mu;
-  static double* part = nullptr;
-  static float* out = nullptr;
-  static float* host = nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  if (!part) {
-    if (cudaMalloc(&part, sizeof(double) * kSpreadBlocks) != cudaSuccess) return 3;
-    if (cudaMalloc(&out, sizeof(float)) != cudaSuccess) return 3;
-    if (cudaMallocHost(&host, sizeof(float)) != cudaSuccess) return 3;
-  }
-  rt_spread_partial_kernel<<<kSpreadBlocks, 256, 0, st>>>(P, part);
-  rt_spread_final_kernel<<<1, 256, 0, st>>>(P, part, kSpreadBlocks, out);
-  g_tc_launches.fetch_add(2);
-  if (cudaMemcpyAsync(host, out, sizeof(float), cudaMemcpyDeviceToHost, st) != cudaSuccess) return 3;
-  if (cudaStreamSynchronize(st) != cudaSuccess) return 3;
-  return double(*host) > kSpread2Fast ? 3 : 2;
-}
+// Exponent piece count of this evaluation's mode (psi_select_mode decides on the host).
+int rt_pieces(const PsiConst& P) { return P.mode == kModePrecise ? 3 : 2; }
 
 int rt_dbg() {
   static const int v = [] {
@@ -1176,9 +1099,6 @@ int rt_dbg() {
   return v;
 }
 
-// CTA-pair kernels (cta_group::2) are correct but not yet faster than the single-CTA ones: the
-// cross-SM barrier round trips set a ~2.4 ms synchronisation floor at C3 (profiles/
-// r01_ncu_rowtile_summary.md).  Opt in with SGPX_RT_PAIR=1.
 // Forward MMA3 pieces: bf16 hi / lo (~2^-17, 16 % faster consumers) with the two-piece MMA1, fp16
 // hi / lo (~2^-22, scaled) with the three-piece MMA1: the wide-spread regime where the d_z assembly
 // R1 - zbar R0 from the pair sums cancels.  SGPX_RT_FWD_BF16=0|1 overrides (A/B).
@@ -1189,15 +1109,6 @@ bool rt_fwd_bf16(int np) {
   }();
   return v < 0 ? np == 2 : v == 1;
 }
-
-int rt_pair_env() {
-  static const int v = [] {
-    const char* e = getenv("SGPX_RT_PAIR");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-bool use_pair(int q, bool bf) { return rt_pair_env() != 0 && rt_pair_ok(q, bf); }
 
 template <int Q, bool BF, bool PAIR, int NP>
 int launch_rowtile(const PsiConst& P, RowTileArgs R, dim3 grid, cudaStream_t st) {
@@ -1250,9 +1161,7 @@ int rt_forward_q(const PsiConst& P, double* base, double* packed, int num_sms, c
   using C = RT<Q, true>;
   const FwdLayout L = fwd_layout(P, num_sms);
   float* fl = floats_at(base, L.off_floats);
-  const int np = rt_pieces(P, st);
-  if (np != 2 && np != 3) return 3;
-  const bool pair = np == 2 && use_pair(Q, true);
+  const int np = rt_pieces(P);
   RowTileArgs R{};
   R.a = fl + L.f_fs;
   R.a_stride = L.p_pad * C::K1;
@@ -1280,19 +1189,9 @@ int rt_forward_q(const PsiConst& P, double* base, double* packed, int num_sms, c
     constexpr int NP = decltype(np_tag)::value;
     constexpr bool BF = decltype(bf_tag)::value;
     rt_pair_rows_kernel<Q, NP><<<blocks_p, 256, 0, st>>>(P, L.p_pad, fl + L.f_fs, L.p_pad * C::K1);
-    if (NP == 2 && pair)
-      rt_data_rows_kernel<Q, BF, true, 2><<<blocks_n, 256, 0, st>>>(P, L.n_pad, fl + L.f_hs, L.n_pad * C::K1,
+    rt_data_rows_kernel<Q, BF, false, NP><<<blocks_n, 256, 0, st>>>(P, L.n_pad, fl + L.f_hs, L.n_pad * C::K1,
                                                                     fl + L.f_pre, ys);
-    else
-      rt_data_rows_kernel<Q, BF, false, NP><<<blocks_n, 256, 0, st>>>(P, L.n_pad, fl + L.f_hs, L.n_pad * C::K1,
-                                                                      fl + L.f_pre, ys);
     g_tc_launches.fetch_add(2);
-    if constexpr (NP == 2 && RT<Q, BF, true>::kConcat) {
-      if (pair) {
-        const unsigned gx = unsigned((R.ntiles + 1) / 2 * 2);
-        return launch_rowtile<Q, BF, true, 2>(P, R, dim3(gx, unsigned(L.ns)), st);
-      }
-    }
     return launch_rowtile<Q, BF, false, NP>(P, R, dim3(unsigned(R.ntiles), unsigned(L.ns)), st);
   };
   using T2 = std::integral_constant<int, 2>;
@@ -1317,13 +1216,10 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
   float* pre = floats_at(bbase, L.off_floats);
   const int blocks_p = int(std::min<int64_t>((F.p_pad + 255) / 256, int64_t(num_sms) * 8));
   // the forward's piece count (same deterministic decision on the same inputs)
-  const int np = rt_pieces(P, st);
-  if (np != 2 && np != 3) return 3;
-  const bool pair = np == 2 && use_pair(Q, false);
+  const int np = rt_pieces(P);
   float* ys = reinterpret_cast<float*>(bbase + L.off_ys);
   rt_yscale_kernel<Q><<<1, 256, 0, st>>>(P, B.u, ys);
-  if (pair) rt_pair_pre_kernel<Q, true, 2><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, ys, pre);
-  else if (np == 3) rt_pair_pre_kernel<Q, false, 3><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, ys, pre);
+  if (np == 3) rt_pair_pre_kernel<Q, false, 3><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, ys, pre);
   else rt_pair_pre_kernel<Q, false, 2><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, ys, pre);
   g_tc_launches.fetch_add(2);
   if (P.n > 0) {
@@ -1338,18 +1234,9 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
     R.nrows_static = P.n;
     R.out = bbase + L.off_t;
     R.yinv = ys + 64;
-    if constexpr (RT<Q, false, true>::kConcat) {
-      if (pair) {
-        const int64_t units = (L.ntiles + 1) / 2;
-        const unsigned gx = unsigned(2 * std::max<int64_t>(1, std::min<int64_t>(units, num_sms / 2)));
-        if (int rc = launch_rowtile<Q, false, true, 2>(P, R, dim3(gx), st)) return rc;
-      }
-    }
-    if (!pair) {
-      const int rc = np == 3 ? launch_rowtile<Q, false, false, 3>(P, R, dim3(unsigned(L.grid)), st)
-                             : launch_rowtile<Q, false, false, 2>(P, R, dim3(unsigned(L.grid)), st);
-      if (rc) return rc;
-    }
+    const int rc = np == 3 ? launch_rowtile<Q, false, false, 3>(P, R, dim3(unsigned(L.grid)), st)
+                           : launch_rowtile<Q, false, false, 2>(P, R, dim3(unsigned(L.grid)), st);
+    if (rc) return rc;
   }
   if (!B.skip_pair_terms) {
     rt_pair_dz_kernel<Q><<<std::max(1, (P.m * P.q + 7) / 8), 256, 0, st>>>(P, B.u, fbase + F.off_sums, prow);
@@ -1395,39 +1282,6 @@ double* rt_fwd_pair_sums(const PsiConst& P, double* region, int num_sms, int64_t
 }
 int64_t rt_bwd_doubles(const PsiConst& P, int num_sms) { return bwd_layout(P, num_sms).doubles; }
 
-int rt_decide_pieces(const PsiConst& P, void* stream) {
-  const int np = rt_pieces(P, static_cast<cudaStream_t>(stream));
-  return (np == 2 || np == 3) ? np : -1;
-}
-int rt_decide_pieces_host(const PsiConst& P, const double* mu_host, int64_t ld, int64_t n, int64_t stride,
-                          const double* z_host, int64_t m) {
-  if (const int f = rt_forced_pieces()) return f;
-  if (!P.expected) return 3;
-  // `stride` = rows per sampled block: 16 evenly spaced contiguous blocks (cache-friendly on pinned
-  // host memory)
-  double smu = 0.0;
-  int64_t cnt = 0;
-  const int64_t blocks = 16, len = std::max<int64_t>(1, std::min<int64_t>(stride, n));
-  for (int q = 0; q < P.q; ++q) {
-    const double il = 1.0 / P.ls[q], c = P.center[q];
-    for (int64_t b = 0; b < blocks; ++b) {
-      const int64_t i0 = std::min<int64_t>(n - len, (n - len) * b / (blocks - 1));
-      for (int64_t i = i0; i < i0 + len; ++i) {
-        const double v = (mu_host[q * ld + i] - c) * il;
-        smu += v * v;
-        if (q == 0) ++cnt;
-      }
-    }
-  }
-  double sz = 0.0;
-  for (int64_t a = 0; a < m; ++a)
-    for (int q = 0; q < P.q; ++q) {
-      const double v = (z_host[q * m + a] - P.center[q]) / P.ls[q];
-      sz += v * v;
-    }
-  const double mmu = cnt ? smu / double(cnt) : 0.0, mz = m ? sz / double(m) : 0.0;
-  return std::max(mmu, mz) > kSpread2Fast ? 3 : 2;
-}
 int rt_forward(const PsiConst& P, double* base, double* packed, int num_sms, void* stream) {
   SGPX_RT_DISPATCH(rt_forward_q, P, base, packed, num_sms, static_cast<cudaStream_t>(stream))
 }

@@ -150,6 +150,9 @@ struct sgpx_ctx {
   // scratch of the one-shot sweep / psi1 entry points
   DevBuf mu, s, y, zc, z64, fpart, bpart, pstats, pgrads, u, dpsi, dmu, ds, err, out;
   HostBuf h_stats, h_grads, h_u, h_dpsi, h_err, h_stage;
+  int precision = SGPX_PREC_AUTO;  // requested mode of the one-shot entry points
+  int last_mode = 0;               // mode the last sweep ran in
+  double last_z_spread = 0.0;
 };
 
 // Device-side state of one shard (one rank, or one sweep call).
@@ -165,8 +168,8 @@ struct ShardInputs {
 
 // Build the per-launch constants and upload the centred fp32 / fp64 copies of Z.
 PsiConst make_const(sgpx_ctx* ctx, const ShardInputs& in, const coord::Kernel& k, const coord::Mat& z, DevBuf& zc_buf,
-                    DevBuf& z64_buf, HostBuf& staging) {
-  require(in.q >= 1 && in.q <= kMaxQ, "latent dimension Q must be in [1, 32] on the B200 path");
+                    DevBuf& z64_buf, HostBuf& staging, int precision) {
+  require(in.q >= 1 && in.q <= kMaxQ, "latent dimension Q must be in [1, 64] on the B200 path");
   PsiConst P{};
   P.n = in.n;
   P.ld_mu = in.ld_mu;
@@ -176,7 +179,7 @@ PsiConst make_const(sgpx_ctx* ctx, const ShardInputs& in, const coord::Kernel& k
   P.s = in.s;
   P.y = in.y;
   P.q = int(in.q);
-  P.qv = int(round4(instantiated_q(int(in.q))));
+  P.qv = int(round4(std::max<int64_t>(instantiated_q(int(in.q)), in.q)));
   P.m = int(in.m);
   P.mv = int(round4(in.m));
   P.d = int(in.d);
@@ -216,6 +219,8 @@ PsiConst make_const(sgpx_ctx* ctx, const ShardInputs& in, const coord::Kernel& k
   CUDA_OK(cudaStreamSynchronize(ctx->stream));
   P.zc = zc_buf.get<float>();
   P.z64 = z64_buf.get<double>();
+  P.mode = psi_select_mode(P, z.v.data(), z.r, precision);
+  require(P.mode > 0, "latent dimension Q exceeds the instantiated kernels");
   return P;
 }
 
@@ -287,9 +292,9 @@ struct sgpx_engine {
   coord::Stats st;  // unpacked statistics of the last coordinate() (complete_adjoints needs them)
   bool coordinated = false, with_grads = false;
   bool pairs_folded = false;  // sub-shard pair sums folded into the first (once per forward)
-  int rt_np = 0;              // exponent piece count for the current data (0: not decided yet)
   cudaEvent_t ev[8] = {};  // 0-1 stats pass, 2-3 grad pass, 4-5 fwd kernel, 6-7 bwd kernel
   double coord_s = 0.0;
+  double z_spread = 0.0;
   LaunchGeom gf{}, gb{};
   // Sub-shard pipeline: the shard's rows are processed as K contiguous sub-shards so that the
   // host<->device traffic of one (mu, S in; d mu, d S out) overlaps the kernels of another.
@@ -430,24 +435,6 @@ void engine_stats_pass(sgpx_engine* e) {
   }
   e->fpart.ensure(sizeof(double) * foff);
   if (k > 1) e->pstats_sub.ensure(sizeof(double) * count * k);
-  // exponent piece count for this evaluation, decided once for the forward and
-  // the backward of every sub-shard: on a sample of the host rows while they are still to be
-  // uploaded, else by the device check (the stream is between evaluations here)
-  if (use_rt(e->P) && e->in.n > 0) {
-    if (e->rt_np == 0) {  // cached until the next set_data / broadcast
-      if (e->pending_upload) {
-        const int64_t n = e->cfg.n_local, ldm = e->h_mu.ld ? e->h_mu.ld : n;
-        e->rt_np = rt_decide_pieces_host(e->P, e->h_mu.data, ldm, n, 256, e->z.v.data(), e->z.r);
-      } else {
-        e->rt_np = rt_decide_pieces(e->P, ctx->stream);
-        if (e->rt_np < 0) {
-          e->rt_np = 0;
-          throw CudaError("exponent precision check failed");
-        }
-      }
-    }
-    for (auto& sub : e->subs) sub.P.rt_pieces = e->rt_np;
-  }
   CUDA_OK(cudaEventRecord(e->ev[0], ctx->stream));
   if (e->pending_upload) {  // copy stream: mu / S of sub-shard j, then the forward of j waits for it
     CUDA_OK(cudaEventRecord(e->ev_out[0], ctx->stream));  // previous users of the device rows are done
@@ -542,14 +529,14 @@ void engine_grad_pass(sgpx_engine* e) {
     if (k > 1) e->pgrads_sub.ensure(sizeof(double) * count * k);
     // the per-pair gradient terms are linear in the forward pair sums: fold every sub-shard's sums
     // into the first and add the terms once (row-tile path)
-    const bool fold = k > 1 && use_rt(e->subs[0].P);
+    const bool fold = k > 1;
     if (fold && !e->pairs_folded) {
       e->pairs_folded = true;
       int64_t np = 0;
       auto sums = [&](int j, int64_t* n) {
         const auto& sj = e->subs[j];
-        double* region = const_cast<double*>(rt_fwd_region(sj.P, e->fpart.get<double>() + sj.foff, ctx->num_sms));
-        return rt_fwd_pair_sums(sj.P, region, ctx->num_sms, n);
+        double* region = const_cast<double*>(fwd_region(sj.P, e->fpart.get<double>() + sj.foff, ctx->num_sms));
+        return fwd_pair_sums(sj.P, region, ctx->num_sms, n);
       };
       double* s0 = sums(0, &np);
       for (int j = 1; j < k; ++j) {
@@ -572,7 +559,7 @@ void engine_grad_pass(sgpx_engine* e) {
       B.d_mu = e->dmu.get<double>() + sub.n0;
       B.d_s = e->ds.get<double>() + sub.n0;
       B.ld_g = e->in.n;
-      B.fwd_rt = rt_fwd_region(sub.P, e->fpart.get<double>() + sub.foff, ctx->num_sms);
+      B.fwd_rt = fwd_region(sub.P, e->fpart.get<double>() + sub.foff, ctx->num_sms);
       B.skip_pair_terms = (fold && j > 0) ? 1 : 0;
       double* out = k > 1 ? e->pgrads_sub.get<double>() + int64_t(j) * count : e->pgrads.get<double>();
       if (psi_backward(sub.P, B, e->bpart.get<double>() + sub.boff, out, ctx->num_sms, ctx->stream, &e->gb,
@@ -654,6 +641,8 @@ void engine_finish(sgpx_engine* e, sgpx_eval_result* out) {
   out->fwd_grid = e->gf.grid;
   out->bwd_grid = e->with_grads ? e->gb.grid : 0;
   out->coordinator_s = e->coord_s;
+  out->precision_used = e->P.mode;
+  out->z_spread = e->z_spread;
 }
 
 }  // namespace
@@ -724,6 +713,22 @@ int sgpx_ctx_synchronize(sgpx_ctx* ctx) {
 }
 
 int64_t sgpx_ctx_launch_count(const sgpx_ctx* ctx) { return ctx ? launches_issued() - ctx->launches0 : 0; }
+
+int sgpx_ctx_set_precision(sgpx_ctx* ctx, int precision) {
+  return guard([&] {
+    require(ctx != nullptr, "ctx is null");
+    require(precision == SGPX_PREC_AUTO || precision == SGPX_PREC_FAST || precision == SGPX_PREC_PRECISE ||
+                precision == SGPX_PREC_DIRECT,
+            "unknown precision mode");
+    ctx->precision = precision;
+  });
+}
+
+int sgpx_ctx_last_precision(const sgpx_ctx* ctx, double* z_spread) {
+  if (!ctx) return 0;
+  if (z_spread) *z_spread = ctx->last_z_spread;
+  return ctx->last_mode;
+}
 
 int64_t sgpx_packed_stats_count(int64_t m, int64_t d) { return 4 + m * (m + 1) / 2 + m * d; }
 int64_t sgpx_packed_grads_count(int64_t m, int64_t q) { return 1 + q + m * q; }
@@ -801,7 +806,9 @@ int sgpx_sweep_stats(sgpx_ctx* ctx, int expected, sgpx_cmat mu, sgpx_cmat s, sgp
     in.ld_s = n;
     in.y = ctx->y.get<double>();
     in.ld_y = n;
-    PsiConst P = make_const(ctx, in, k, zm, ctx->zc, ctx->z64, ctx->h_stage);
+    PsiConst P = make_const(ctx, in, k, zm, ctx->zc, ctx->z64, ctx->h_stage, ctx->precision);
+    ctx->last_mode = P.mode;
+    ctx->last_z_spread = psi_z_spread(P, zm.v.data(), zm.r);
     LaunchGeom g{};
     if (plan_forward(P, ctx->num_sms, &g)) throw CudaError("psi forward: launch planning failed");
     ctx->fpart.ensure(sizeof(double) * fwd_part_count(P.m, P.d) * std::max(1, g.grid));
@@ -842,7 +849,7 @@ int sgpx_sweep_stats(sgpx_ctx* ctx, int expected, sgpx_cmat mu, sgpx_cmat s, sgp
     B.d_mu = ctx->dmu.get<double>();
     B.d_s = ctx->ds.get<double>();
     B.ld_g = n;
-    B.fwd_rt = rt_fwd_region(P, ctx->fpart.get<double>(), ctx->num_sms);
+    B.fwd_rt = fwd_region(P, ctx->fpart.get<double>(), ctx->num_sms);
     if (plan_backward(P, ctx->num_sms, &g)) throw CudaError("psi backward: launch planning failed");
     ctx->bpart.ensure(sizeof(double) * bwd_part_count(P.m, P.q) * std::max(1, g.grid));
     const int64_t gcount = sgpx_packed_grads_count(m, q);
@@ -900,7 +907,7 @@ int sgpx_psi1_expected(sgpx_ctx* ctx, sgpx_cmat mu, sgpx_cmat s, sgpx_cmat z, co
     in.ld_mu = n;
     in.s = ctx->s.get<double>();
     in.ld_s = n;
-    PsiConst P = make_const(ctx, in, k, zm, ctx->zc, ctx->z64, ctx->h_stage);
+    PsiConst P = make_const(ctx, in, k, zm, ctx->zc, ctx->z64, ctx->h_stage, SGPX_PREC_DIRECT);
     ctx->out.ensure(sizeof(double) * n * m);
     // validation (VariationalPosterior::validate, psi_stats.hpp:20-25) via the forward err flag is
     // not run here; check on the host copy instead.
@@ -982,7 +989,10 @@ int sgpx_engine_create(sgpx_ctx* ctx, const sgpx_engine_config* cfg, sgpx_engine
     require(cfg->kind == 0 || cfg->kind == 1, "engine_create: kind must be 0 (regression) or 1 (latent)");
     require(cfg->n_local >= 0 && cfg->row_begin >= 0 && cfg->row_begin + cfg->n_local <= cfg->n_global,
             "engine_create: shard rows outside [0, N)");
-    require(cfg->q >= 1 && cfg->q <= kMaxQ, "engine_create: Q must be in [1, 32]");
+    require(cfg->q >= 1 && cfg->q <= kMaxQ, "engine_create: Q must be in [1, 64]");
+    require(cfg->precision == SGPX_PREC_AUTO || cfg->precision == SGPX_PREC_FAST ||
+                cfg->precision == SGPX_PREC_PRECISE || cfg->precision == SGPX_PREC_DIRECT,
+            "engine_create: unknown precision mode");
     require(cfg->m >= 1 && cfg->d >= 1, "engine_create: need M >= 1 and D >= 1");
     require(cfg->jitter_factor >= 0.0, "factor_gram: jitter factor must be non-negative");
     CUDA_OK(cudaSetDevice(ctx->device));
@@ -1043,7 +1053,7 @@ int sgpx_engine_set_data(sgpx_engine* e, sgpx_cmat x_or_mu, sgpx_cmat s, sgpx_cm
       in.ld_s = n;
     }
     e->has_data = true;
-    e->rt_np = 0;
+    e->pending_upload = false;  // rows set here replace any host views of an earlier broadcast
     if (e->has_params) {
       e->P.mu = in.mu;
       e->P.ld_mu = in.ld_mu;
@@ -1096,9 +1106,9 @@ int sgpx_engine_broadcast(sgpx_engine* e, const sgpx_kernel_spec* kernel, double
     e->kernel = k;
     e->z = zm;
     e->beta = beta;
-    e->P = make_const(e->ctx, e->in, k, zm, e->zc, e->z64, e->h_stage);
+    e->P = make_const(e->ctx, e->in, k, zm, e->zc, e->z64, e->h_stage, e->cfg.precision);
+    e->z_spread = psi_z_spread(e->P, zm.v.data(), zm.r);
     e->has_params = true;
-    e->rt_np = 0;
     e->coordinated = false;
   });
 }

@@ -211,6 +211,16 @@ class Context:
     def launch_count(self) -> int:
         return int(self._lib.sgpx_ctx_launch_count(self.handle))
 
+    def set_precision(self, precision: str | int = "auto"):
+        """Precision mode of the one-shot entry points: "auto" | "fast" | "precise" | "direct"."""
+        check(self._lib.sgpx_ctx_set_precision(self.handle, precision_code(precision)))
+
+    def last_precision(self):
+        """(mode name, Tz) of the last sweep_stats on this context."""
+        tz = C.c_double()
+        mode = int(self._lib.sgpx_ctx_last_precision(self.handle, C.byref(tz)))
+        return L.PRECISION_NAMES.get(mode, "none"), tz.value
+
     def close(self):
         if getattr(self, "handle", None):
             self._lib.sgpx_ctx_destroy(self.handle)
@@ -232,6 +242,15 @@ class Context:
         return d[device]
 
 
+def precision_code(precision) -> int:
+    if isinstance(precision, str):
+        codes = {v: k for k, v in L.PRECISION_NAMES.items()}
+        if precision not in codes:
+            raise SgpxInvalidArgument(f"unknown precision mode {precision!r}")
+        return codes[precision]
+    return int(precision)
+
+
 def device_count() -> int:
     return int(L.load().sgpx_device_count())
 
@@ -240,9 +259,13 @@ def device_count() -> int:
 # the sweep and its wrappers (psi_stats.hpp:108-426)
 # ---------------------------------------------------------------------------
 def sweep_stats(expected: bool, mu, s, y, z, kernel: KernelSpec, tiles: TileConfig | None = None,
-                adj: StatsAdjoints | None = None, want_grads: bool = False, ctx: Context | None = None):
-    """detail::sweep_stats on the B200: returns (SufficientStats, StatsGrads | None)."""
+                adj: StatsAdjoints | None = None, want_grads: bool = False, ctx: Context | None = None,
+                precision: str | None = None):
+    """detail::sweep_stats on the B200: returns (SufficientStats, StatsGrads | None).
+    ``precision`` (optional) sets the context's mode for this and later calls."""
     ctx = ctx or Context.default()
+    if precision is not None:
+        ctx.set_precision(precision)
     mu = _F(mu)
     y = _F(y)
     z = _F(z)
@@ -363,6 +386,8 @@ class EngineTimings:
     bwd_kernel_s: float = 0.0
     fwd_grid: int = 0
     bwd_grid: int = 0
+    precision: str = "auto"
+    z_spread: float = 0.0
 
 
 @dataclass
@@ -386,7 +411,8 @@ class Engine:
     """
 
     def __init__(self, kind, x_or_mu, s, y, workers: int = 1, tiles: TileConfig | None = None,
-                 jitter_factor: float = 1e-6, ctx: Context | None = None, _n_global=None, _row_begin=0):
+                 jitter_factor: float = 1e-6, ctx: Context | None = None, _n_global=None, _row_begin=0,
+                 precision: str = "auto"):
         self.kind = ModelKind(kind)
         if workers != 1:
             raise SgpxInvalidArgument("one Engine per GPU: use engine_dist.DistributedEngine for several ranks")
@@ -400,6 +426,7 @@ class Engine:
         self.n_global = n if _n_global is None else _n_global
         self.row_begin = _row_begin
         self.jitter_factor = jitter_factor
+        self.precision = precision_code(precision)
         self._keep = []
         self.m = None
         self._h = None
@@ -407,7 +434,7 @@ class Engine:
 
     def _create(self, m: int):
         cfg = L.engine_config(int(self.kind), self.n_global, self.row_begin, self.n, self.q, self.d, m,
-                              self.jitter_factor)
+                              self.jitter_factor, self.precision)
         h = C.c_void_p()
         check(self._lib.sgpx_engine_create(self.ctx.handle, C.byref(cfg), C.byref(h)))
         self._h = h
@@ -498,7 +525,8 @@ class Engine:
                 else:
                     g.d_mu, g.d_s = self.local_grads(getattr(self, "_grads_out", None))
         t = EngineTimings(r.stats_pass_s, r.coordinator_s, r.grad_pass_s, r.wall_s, r.fwd_kernel_s, r.bwd_kernel_s,
-                          r.fwd_grid, r.bwd_grid)
+                          r.fwd_grid, r.bwd_grid, L.PRECISION_NAMES.get(int(r.precision_used), "none"),
+                          float(r.z_spread))
         return EvalResult(BoundBreakdown._from(r.bound), stats, bool(r.has_grads), g, t, r.jitter_factor_used)
 
     def evaluate(self, with_grads: bool = True, local_to_host: bool = True) -> EvalResult:

@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
         assert name in _lib.SIGNATURES, f"{name} missing a ctypes signature"
-    assert lib.sgpx_abi_version() == 1
+    assert lib.sgpx_abi_version() == 2
 
 
 def test_no_cpu_fallback_without_device():

@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 from conftest import rel_err
-from paper_1410_4984_b200.rng import Rng
+from ref_rng import Rng
 
 
 # ---------------------------------------------------------------------------
