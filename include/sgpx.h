@@ -16,6 +16,10 @@
  *                           adjoints_from_core (bound.hpp:196-226)
  *   sgpx_finish_host        gradient assembly of Engine::evaluate (parallel.hpp:414-421):
  *                           kern_grads(Z,Z,dKmm) (kernels.hpp:124-164) + jitter term
+ *   sgpx_rng_*              sgp::Rng::normal_matrix (common.hpp:45-97) generated on the device,
+ *                           the init_gplvm Z-row choice (model.hpp:420-429)
+ *   sgpx_io_*               write_matrix_bin / read_matrix_bin (io.hpp:114-153) + a streamed
+ *                           loader straight into device memory
  *
  * Conventions
  *   - All matrices at this boundary are fp64, column-major with a leading
@@ -59,6 +63,7 @@ extern "C" {
 #define SGPX_CUDA 3
 #define SGPX_NCCL 4
 #define SGPX_INTERNAL 5
+#define SGPX_IO 6 /* file input / output (the reference's std::runtime_error in io.hpp) */
 
 #define SGPX_ABI_VERSION 2
 
@@ -247,6 +252,22 @@ int sgpx_engine_local_grads_device(sgpx_engine* eng, double** d_mu, double** d_s
  * in its result, parallel.hpp:424-429).  Null data pointers unregister. */
 int sgpx_engine_set_local_grads_out(sgpx_engine* eng, sgpx_mmat d_mu, sgpx_mmat d_s);
 int sgpx_engine_copy_local_grads(sgpx_engine* eng, sgpx_mmat d_mu, sgpx_mmat d_s);
+
+/* ---- seeded inputs and binary matrices ------------------------------------ */
+/* Rng(seed).normal_matrix(rows, cols) (common.hpp:86-91), bit-for-bit the reference's splitmix64 +
+ * Box-Muller stream up to the last-ulp differences of the device's fp64 log / sin / cos; out is
+ * column-major (ld), device memory if on_device != 0, else host. */
+int sgpx_rng_normal_matrix(sgpx_ctx* ctx, uint64_t seed, int64_t rows, int64_t cols, sgpx_mmat out, int on_device);
+/* The M distinct row indices init_gplvm picks for Z with Rng(seed) (partial Fisher-Yates,
+ * model.hpp:420-429); idx has m entries. */
+int sgpx_rng_choose_rows(uint64_t seed, int64_t n, int64_t m, int64_t* idx);
+/* Raw binary matrices: <base>.shape = "rows cols\n", <base>.bin = row-major little-endian fp64
+ * (io.hpp:114-153).  Host read / write use column-major views; the device loader streams the file
+ * through pinned slabs and transposes on the device (dev_out: device memory, column-major). */
+int sgpx_io_matrix_shape(const char* base, int64_t* rows, int64_t* cols);
+int sgpx_io_read_matrix(const char* base, sgpx_mmat out);
+int sgpx_io_write_matrix(const char* base, sgpx_cmat m);
+int sgpx_io_load_matrix_device(sgpx_ctx* ctx, const char* base, sgpx_mmat dev_out);
 
 #ifdef __cplusplus
 }

@@ -20,28 +20,46 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liboracle.so")
+# CPU-baseline build of the same source: -ffast-math lets g++ vectorise the exp loops through glibc's
+# libmvec (AVX2 _ZGVdN4v_exp) and the tile sums, the way Eigen's packet math evaluates the reference's
+# array expressions.  Timing only; the checker is always the strict build.
+SIMD_LIB_PATH = os.path.join(_HERE, "liboracle_simd.so")
 SRC_PATH = os.path.join(_HERE, "sgp_oracle.cpp")
 
 _lib = None
+_simd_lib = None
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle restatement (g++, portable x86-64-v3 so it runs on the GPU box host)."""
-    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(SRC_PATH):
-        cmd = ["g++", "-std=c++17", "-O3", "-march=x86-64-v3", "-fPIC", "-shared", "-pthread",
-               "-o", LIB_PATH, SRC_PATH]
-        subprocess.check_call(cmd)
+    """Compile the oracle restatement (g++, portable x86-64-v3 so it runs on the GPU box host), strict
+    and SIMD-baseline builds."""
+    for path, extra in ((LIB_PATH, []), (SIMD_LIB_PATH, ["-ffast-math"])):
+        if force or not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(SRC_PATH):
+            cmd = ["g++", "-std=c++17", "-O3", "-march=x86-64-v3", *extra, "-fPIC", "-shared", "-pthread",
+                   "-o", path, SRC_PATH]
+            subprocess.check_call(cmd)
     return LIB_PATH
 
 
-def lib():
-    global _lib
+def _load(path):
+    lb = C.CDLL(path)
+    lb.oracle_last_error.restype = C.c_char_p
+    lb.oracle_rng_normal_matrix.restype = None
+    lb.oracle_rng_uniform.restype = None
+    lb.oracle_rng_choose_rows.restype = None
+    return lb
+
+
+def lib(simd: bool = False):
+    global _lib, _simd_lib
+    if simd:
+        if _simd_lib is None:
+            build()
+            _simd_lib = _load(SIMD_LIB_PATH)
+        return _simd_lib
     if _lib is None:
         build()
-        _lib = C.CDLL(LIB_PATH)
-        _lib.oracle_last_error.restype = C.c_char_p
-        _lib.oracle_rng_normal_matrix.restype = None
-        _lib.oracle_rng_uniform.restype = None
+        _lib = _load(LIB_PATH)
     return _lib
 
 
@@ -236,8 +254,9 @@ class EvalResult:
 
 
 def engine_evaluate(latent, x_or_mu, s, y, z, variance, lengthscales, beta, workers=1, with_grads=True,
-                    block_span=64, thread_span=1024, jitter_factor=1e-6) -> EvalResult:
-    """Restatement of Engine(kind, ...).evaluate(with_grads) (parallel.hpp:370-450)."""
+                    block_span=64, thread_span=1024, jitter_factor=1e-6, simd=False) -> EvalResult:
+    """Restatement of Engine(kind, ...).evaluate(with_grads) (parallel.hpp:370-450).  ``simd``: the
+    vectorised CPU-baseline build (timing), else the strict checker."""
     x = F(x_or_mu)
     y = F(y)
     z = F(z)
@@ -256,7 +275,7 @@ def engine_evaluate(latent, x_or_mu, s, y, z, variance, lengthscales, beta, work
     gs = np.zeros(2)
     dls = np.zeros(q)
     times = np.zeros(2)
-    _check(lib().oracle_engine_evaluate(
+    _check(lib(simd).oracle_engine_evaluate(
         C.c_int(1 if latent else 0), _i64(n), _i64(q), _i64(d), _i64(m), _p(x), _p(s), _p(y), _p(z),
         _d(variance), _p(ls), _d(beta), C.c_int(workers), _i64(block_span), _i64(thread_span), _d(jitter_factor),
         C.c_int(1 if with_grads else 0), _p(bd), _p(sc), _p(psi_y), _p(phi_big), _p(d_mu), _p(d_s), _p(d_z),
@@ -277,6 +296,13 @@ def rng_normal_matrix(seed, rows, cols):
     """Rng(seed).normal_matrix(rows, cols) (common.hpp:86-91), column-major result."""
     out = np.zeros((rows, cols), order="F")
     lib().oracle_rng_normal_matrix(C.c_uint64(seed), _i64(rows), _i64(cols), _p(out))
+    return out
+
+
+def rng_choose_rows(seed, n, m):
+    """init_gplvm's M distinct Z rows (model.hpp:420-429, partial Fisher-Yates with Rng(seed))."""
+    out = np.zeros(m, dtype=np.int64)
+    lib().oracle_rng_choose_rows(C.c_uint64(seed), _i64(n), _i64(m), out.ctypes.data_as(C.c_void_p))
     return out
 
 

@@ -1170,6 +1170,18 @@ void oracle_rng_normal_matrix(uint64_t seed, int64_t rows, int64_t cols, double*
     for (Index j = 0; j < cols; ++j) out[i + j * rows] = r.normal();
 }
 
+// init_gplvm's Z rows (model.hpp:420-429): partial Fisher-Yates over 0..n-1 with Rng(seed).
+void oracle_rng_choose_rows(uint64_t seed, int64_t n, int64_t m, int64_t* out) {
+  Rng r(seed);
+  std::vector<int64_t> idx(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) idx[size_t(i)] = i;
+  for (int64_t i = 0; i < m; ++i) {
+    const int64_t j = i + int64_t(r.index(uint64_t(n - i)));
+    std::swap(idx[size_t(i)], idx[size_t(j)]);
+    out[i] = idx[size_t(i)];
+  }
+}
+
 void oracle_rng_uniform(uint64_t seed, int64_t count, double* out) {
   Rng r(seed);
   for (Index i = 0; i < count; ++i) out[i] = r.uniform();

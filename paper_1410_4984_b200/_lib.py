@@ -14,7 +14,7 @@ ROOT = os.path.dirname(PKG_DIR)
 LIB_PATH = os.path.join(PKG_DIR, os.environ.get("SGPX_LIB", "libsgpx.so"))
 HEADER_PATH = os.path.join(ROOT, "include", "sgpx.h")
 
-SGPX_OK, SGPX_INVALID_ARGUMENT, SGPX_NUMERIC, SGPX_CUDA, SGPX_NCCL, SGPX_INTERNAL = range(6)
+SGPX_OK, SGPX_INVALID_ARGUMENT, SGPX_NUMERIC, SGPX_CUDA, SGPX_NCCL, SGPX_INTERNAL, SGPX_IO = range(7)
 SGPX_PREC_AUTO, SGPX_PREC_FAST, SGPX_PREC_PRECISE, SGPX_PREC_DIRECT = 0, 2, 3, 4
 PRECISION_NAMES = {SGPX_PREC_AUTO: "auto", SGPX_PREC_FAST: "fast", SGPX_PREC_PRECISE: "precise",
                    SGPX_PREC_DIRECT: "direct"}
@@ -105,6 +105,12 @@ SIGNATURES = {
     "sgpx_engine_local_grads_device": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "sgpx_engine_copy_local_grads": (C.c_int, [C.c_void_p, mmat, mmat]),
     "sgpx_engine_set_local_grads_out": (C.c_int, [C.c_void_p, mmat, mmat]),
+    "sgpx_rng_normal_matrix": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int64, C.c_int64, mmat, C.c_int]),
+    "sgpx_rng_choose_rows": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.c_void_p]),
+    "sgpx_io_matrix_shape": (C.c_int, [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "sgpx_io_read_matrix": (C.c_int, [C.c_char_p, mmat]),
+    "sgpx_io_write_matrix": (C.c_int, [C.c_char_p, cmat]),
+    "sgpx_io_load_matrix_device": (C.c_int, [C.c_void_p, C.c_char_p, mmat]),
 }
 
 _lib = None
@@ -145,7 +151,13 @@ class SgpxCudaError(SgpxError):
     code = SGPX_CUDA
 
 
-_ERRORS = {SGPX_INVALID_ARGUMENT: SgpxInvalidArgument, SGPX_NUMERIC: SgpxNumericError, SGPX_CUDA: SgpxCudaError}
+class SgpxIoError(SgpxError, OSError):
+    """std::runtime_error of the reference's io.hpp."""
+    code = SGPX_IO
+
+
+_ERRORS = {SGPX_INVALID_ARGUMENT: SgpxInvalidArgument, SGPX_NUMERIC: SgpxNumericError, SGPX_CUDA: SgpxCudaError,
+           SGPX_IO: SgpxIoError}
 
 
 def check(rc: int):

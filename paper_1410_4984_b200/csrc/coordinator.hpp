@@ -19,6 +19,10 @@ struct InvalidArgument : std::invalid_argument {
 struct NumericError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+// File input / output failures (the reference's std::runtime_error in io.hpp).
+struct IoError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 inline void require(bool c, const std::string& msg) {
   if (!c) throw InvalidArgument(msg);
 }

@@ -144,6 +144,16 @@ int64_t bwd_reduce_tmp_doubles(int64_t pstride);
 int bwd_reduce_rows(const double* part, int64_t pstride, int rows, double* packed, double dvar0, double* tmp,
                     void* stream);
 
+// Seeded inputs and binary matrices (synth.cu): Rng(seed).normal_matrix on the device (column-major,
+// ld), the init_gplvm partial Fisher-Yates row choice, the io.hpp binary format (host read / write and
+// a streamed device loader).  IO failures throw IoError.
+int rng_normal_device(uint64_t seed, int64_t rows, int64_t cols, double* out, int64_t ld, void* stream);
+void rng_choose_rows(uint64_t seed, int64_t n, int64_t m, int64_t* idx_out);
+void io_read_shape(const char* base, int64_t* rows, int64_t* cols);
+void io_read_host(const char* base, double* out, int64_t ld);
+void io_write_host(const char* base, const double* a, int64_t rows, int64_t cols, int64_t ld);
+void io_load_device(const char* base, double* dev_out, int64_t ld, void* stream);
+
 // psi1_expected: out n x m col-major fp64 (ld_out).
 int psi1_matrix(const PsiConst& P, double* out, int64_t ld_out, void* stream);
 // Number of __global__ launches issued so far by this process (evidence counter).

@@ -51,6 +51,9 @@ int guard(F&& f) {
   } catch (const CudaError& e) {
     g_last_error = e.what();
     return SGPX_CUDA;
+  } catch (const IoError& e) {
+    g_last_error = e.what();
+    return SGPX_IO;
   } catch (const std::exception& e) {
     g_last_error = e.what();
     return SGPX_INTERNAL;
@@ -1201,6 +1204,75 @@ int sgpx_engine_copy_local_grads(sgpx_engine* e, sgpx_mmat d_mu, sgpx_mmat d_s) 
     CUDA_OK(cudaMemcpy2DAsync(d_s.data, sizeof(double) * (d_s.ld ? d_s.ld : n), e->ds.p, sizeof(double) * n,
                                 sizeof(double) * n, q, cudaMemcpyDeviceToHost, e->ctx->stream));
     CUDA_OK(cudaStreamSynchronize(e->ctx->stream));
+  });
+}
+
+// ---- seeded inputs and binary matrices (common.hpp:45-97, model.hpp:420-429, io.hpp:114-153) ----
+int sgpx_rng_normal_matrix(sgpx_ctx* ctx, uint64_t seed, int64_t rows, int64_t cols, sgpx_mmat out, int on_device) {
+  return guard([&] {
+    require(ctx != nullptr, "ctx is null");
+    require(rows >= 0 && cols >= 0 && out.rows == rows && out.cols == cols, "rng: output must be rows x cols");
+    require(rows * cols == 0 || out.data != nullptr, "rng: null output");
+    const int64_t ld = out.ld ? out.ld : rows;
+    require(ld >= rows, "rng: leading dimension smaller than rows");
+    if (rows * cols == 0) return;
+    CUDA_OK(cudaSetDevice(ctx->device));
+    if (on_device) {
+      if (rng_normal_device(seed, rows, cols, out.data, ld, ctx->stream)) throw CudaError("rng launch failed");
+      CUDA_OK(cudaStreamSynchronize(ctx->stream));
+      return;
+    }
+    ctx->out.ensure(sizeof(double) * rows * cols);
+    if (rng_normal_device(seed, rows, cols, ctx->out.get<double>(), rows, ctx->stream))
+      throw CudaError("rng launch failed");
+    CUDA_OK(cudaMemcpy2DAsync(out.data, sizeof(double) * ld, ctx->out.p, sizeof(double) * rows, sizeof(double) * rows,
+                                cols, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sgpx_rng_choose_rows(uint64_t seed, int64_t n, int64_t m, int64_t* idx) {
+  return guard([&] {
+    require(m >= 1 && m <= n, "init_gplvm: need 1 <= M <= N");
+    require(idx != nullptr, "rng: null output");
+    rng_choose_rows(seed, n, m, idx);
+  });
+}
+
+int sgpx_io_matrix_shape(const char* base, int64_t* rows, int64_t* cols) {
+  return guard([&] {
+    require(base && rows && cols, "io: null argument");
+    io_read_shape(base, rows, cols);
+  });
+}
+
+int sgpx_io_read_matrix(const char* base, sgpx_mmat out) {
+  return guard([&] {
+    require(base != nullptr, "io: null path");
+    int64_t r = 0, c = 0;
+    io_read_shape(base, &r, &c);
+    require(out.rows == r && out.cols == c && (r * c == 0 || out.data), "io: output shape differs from the file");
+    io_read_host(base, out.data, out.ld ? out.ld : r);
+  });
+}
+
+int sgpx_io_write_matrix(const char* base, sgpx_cmat m) {
+  return guard([&] {
+    require(base != nullptr, "io: null path");
+    check_view(m, "matrix");
+    io_write_host(base, m.data, m.rows, m.cols, m.ld ? m.ld : m.rows);
+  });
+}
+
+int sgpx_io_load_matrix_device(sgpx_ctx* ctx, const char* base, sgpx_mmat dev_out) {
+  return guard([&] {
+    require(ctx && base, "io: null argument");
+    int64_t r = 0, c = 0;
+    io_read_shape(base, &r, &c);
+    require(dev_out.rows == r && dev_out.cols == c && (r * c == 0 || dev_out.data),
+            "io: output shape differs from the file");
+    CUDA_OK(cudaSetDevice(ctx->device));
+    io_load_device(base, dev_out.data, dev_out.ld ? dev_out.ld : r, ctx->stream);
   });
 }
 

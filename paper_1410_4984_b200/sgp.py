@@ -625,3 +625,60 @@ def finish_host(packed_grads, z, kernel: KernelSpec, d_kmm, jitter_factor):
     check(L.load().sgpx_finish_host(m, q, p(pg), _cm(z), C.byref(ks), p(dk), float(jitter_factor), p(dz),
                                     C.byref(dv), p(dls)))
     return dz, dv.value, dls
+
+
+# ---------------------------------------------------------------------------
+# seeded inputs and binary matrices (common.hpp:45-97, model.hpp:420-429, io.hpp:114-153)
+# ---------------------------------------------------------------------------
+def rng_normal_matrix(seed: int, rows: int, cols: int, device=None, ctx: Context | None = None):
+    """Rng(seed).normal_matrix(rows, cols), generated on the GPU.  ``device``: return a column-major
+    CUDA float64 tensor there (the data never visits the host); else a Fortran-ordered numpy array."""
+    ctx = ctx or Context.default()
+    lib = L.load()
+    if device is not None:
+        import torch
+
+        t = torch.empty((cols, rows), dtype=torch.float64, device=device).t()
+        v = device_view(t) if rows * cols else L.cmat(None, rows, cols, max(rows, 1))
+        check(lib.sgpx_rng_normal_matrix(ctx.handle, C.c_uint64(seed), rows, cols, v, 1))
+        return t
+    out = np.zeros((rows, cols), order="F")
+    check(lib.sgpx_rng_normal_matrix(ctx.handle, C.c_uint64(seed), rows, cols, _cm(out), 0))
+    return out
+
+
+def rng_choose_rows(seed: int, n: int, m: int) -> np.ndarray:
+    """The M distinct rows init_gplvm takes for Z (partial Fisher-Yates with Rng(seed))."""
+    idx = np.zeros(m, dtype=np.int64)
+    check(L.load().sgpx_rng_choose_rows(C.c_uint64(seed), n, m, idx.ctypes.data_as(C.c_void_p)))
+    return idx
+
+
+def write_matrix_bin(base: str, a):
+    """write_matrix_bin (io.hpp:119-132): <base>.shape + row-major float64 <base>.bin."""
+    a = _F(a)
+    check(L.load().sgpx_io_write_matrix(str(base).encode(), _cm(a)))
+
+
+def read_matrix_bin(base: str) -> np.ndarray:
+    """read_matrix_bin (io.hpp:134-153)."""
+    r, c = C.c_int64(), C.c_int64()
+    lib = L.load()
+    check(lib.sgpx_io_matrix_shape(str(base).encode(), C.byref(r), C.byref(c)))
+    out = np.zeros((r.value, c.value), order="F")
+    check(lib.sgpx_io_read_matrix(str(base).encode(), _cm(out)))
+    return out
+
+
+def load_matrix_bin_device(base: str, device="cuda", ctx: Context | None = None):
+    """read_matrix_bin straight into a column-major CUDA tensor (pinned slabs + device transpose)."""
+    import torch
+
+    ctx = ctx or Context.default()
+    lib = L.load()
+    r, c = C.c_int64(), C.c_int64()
+    check(lib.sgpx_io_matrix_shape(str(base).encode(), C.byref(r), C.byref(c)))
+    t = torch.empty((c.value, r.value), dtype=torch.float64, device=device).t()
+    v = device_view(t) if r.value * c.value else L.cmat(None, r.value, c.value, max(r.value, 1))
+    check(lib.sgpx_io_load_matrix_device(ctx.handle, str(base).encode(), v))
+    return t

@@ -1,0 +1,285 @@
+"""GPU parity where the numbers are quoted, and the accuracy envelope.
+
+* The benchmark configurations at their own shapes against the fp64 oracle engine
+  (Engine::evaluate(true), parallel.hpp:370-450): C3 at the full north-star size N = 1M through the
+  host-buffer (sub-shard streaming) path, C2 at its exact shape, the C5 shape with D = 100 and the C4
+  shape (SGPR, M = 500).  Inputs come from the reference's own generator (sgp::Rng, common.hpp:45-97)
+  so both sides see identical data.
+* Every comparison asserts the reference's element-wise rel_err (proj/tests/support/oracles.hpp:55-58,
+  |a-b| / max(|a|, |b|, 1)) next to the norm-wise error.
+* The precision-mode envelope: wide and clustered latent spaces, far outlier rows,
+  far clusters without inducing points, in both modes; the mode the engine picked is checked too.
+
+Tolerances: the north star's 1e-4 for the mixed path element-wise; norm-wise 1e-5 for statistics /
+bound terms, 5e-5 for gradients; the direct (fp64-exponent) mode 1e-5 element-wise.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import norm_rel_err, rel_err
+
+pytestmark = pytest.mark.gpu
+
+ELEM_TOL = 1e-4
+STAT_TOL = 1e-5
+GRAD_TOL = 5e-5
+DIRECT_TOL = 1e-5
+THREADS = max(1, os.cpu_count() or 1)
+
+
+@pytest.fixture(scope="module")
+def sgp():
+    from paper_1410_4984_b200 import sgp as m
+
+    if m.device_count() == 0:
+        pytest.fail("no CUDA device visible to libsgpx (gpu tests must run on the B200)")
+    return m
+
+
+def _check_eval(r, ref, latent, elem_tol=ELEM_TOL, bound_tol=STAT_TOL):
+    from paper_1410_4984_b200 import sgp as m
+
+    errs = {}
+    assert rel_err(r.bound.total, ref.bound["total"]) < bound_tol
+    for f in m.BOUND_FIELDS:
+        assert rel_err(getattr(r.bound, f), ref.bound[f]) < bound_tol, f
+    g = r.grads
+    pairs = dict(d_z=(g.d_z, ref.d_z), d_ls=(g.d_lengthscales, ref.d_lengthscales),
+                 d_var=([g.d_variance], [ref.d_variance]), d_beta=([g.d_beta], [ref.d_beta]))
+    if latent:
+        pairs.update(d_mu=(g.d_mu, ref.d_mu), d_s=(g.d_s, ref.d_s))
+    for k, (a, b) in pairs.items():
+        errs[k] = (rel_err(a, b), norm_rel_err(a, b))
+        assert errs[k][0] < elem_tol, (k, errs[k])
+        assert errs[k][1] < GRAD_TOL, (k, errs[k])
+    return errs
+
+
+# ---------------------------------------------------------------------------------------------
+# the reference's generator and binary matrices on the device
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("seed,rows,cols", [(0, 1001, 7), (42, 3, 5), (7, 20000, 1)])
+def test_rng_stream_matches_reference(sgp, orc, seed, rows, cols):
+    want = orc.rng_normal_matrix(seed, rows, cols)
+    host = sgp.rng_normal_matrix(seed, rows, cols)
+    dev = sgp.rng_normal_matrix(seed, rows, cols, device="cuda").cpu().numpy()
+    # CUDA's fp64 log / sin / cos are within 2 ulp of glibc's
+    assert np.max(np.abs(host - want) / np.maximum(np.abs(want), 1e-300)) < 1e-14
+    assert np.array_equal(host, dev)
+    assert np.array_equal(sgp.rng_choose_rows(seed + 2, rows, min(rows, 50)),
+                          orc.rng_choose_rows(seed + 2, rows, min(rows, 50)))
+
+
+def test_binary_matrix_roundtrip(sgp, tmp_path):
+    a = sgp.rng_normal_matrix(3, 70001, 13)
+    base = str(tmp_path / "y")
+    sgp.write_matrix_bin(base, a)
+    assert open(base + ".shape").read() == "70001 13\n"
+    raw = np.fromfile(base + ".bin", dtype="<f8").reshape(70001, 13)  # row-major little-endian
+    assert np.array_equal(raw, a)
+    assert np.array_equal(sgp.read_matrix_bin(base), a)
+    assert np.array_equal(sgp.load_matrix_bin_device(base).cpu().numpy(), a)
+    with open(base + ".bin", "r+b") as f:
+        f.truncate(8 * 13 * 100 + 8)
+    with pytest.raises(sgp.SgpxError, match="truncated at row 100"):
+        sgp.read_matrix_bin(base)
+    with pytest.raises(sgp.SgpxError, match="cannot open"):
+        sgp.read_matrix_bin(str(tmp_path / "missing"))
+
+
+# ---------------------------------------------------------------------------------------------
+# benchmark configurations vs the oracle engine
+# ---------------------------------------------------------------------------------------------
+def test_c3_north_star_full_n(sgp, orc):
+    """C3 (N = 1M, Q = 10, D = 50, M = 100): host mu / S / Y streamed to the device in sub-shards
+    with the kernels, d mu / d S streamed back into registered pinned buffers — the e2e path of
+    the benchmark — against the fp64 oracle engine on the same Rng inputs."""
+    import torch
+
+    from paper_1410_4984_b200 import synthetic
+
+    w = synthetic.make(True, 1_000_000, 10, 50, 100, seed=0)
+    eng = sgp.Engine(sgp.ModelKind.latent, w.mu, w.s, w.y)
+    n, q = w.mu.shape
+    gmu = torch.empty(q, n, dtype=torch.float64, pin_memory=True).numpy().T
+    gs = torch.empty(q, n, dtype=torch.float64, pin_memory=True).numpy().T
+    eng.set_local_grads_out(gmu, gs)
+    eng.broadcast(w.kernel, w.beta, w.z, w.mu, w.s)
+    r = eng.evaluate(True)
+    assert r.timing.precision == "fast"
+    ref = orc.engine_evaluate(True, w.mu, w.s, w.y, w.z, w.variance, w.lengthscales, w.beta, workers=THREADS)
+    errs = _check_eval(r, ref, True)
+    print("C3 1M:", {k: f"{a:.1e}/{b:.1e}" for k, (a, b) in errs.items()})
+
+
+def test_c2_exact_shape(sgp, orc):
+    """C2 (N = 100k, Q = 10, D = 10, M = 100), device-resident."""
+    from paper_1410_4984_b200 import synthetic
+
+    w = synthetic.make(True, 100_000, 10, 10, 100, seed=5, device="cuda")
+    eng = sgp.Engine(sgp.ModelKind.latent, w.mu, w.s, w.y)
+    eng.broadcast(w.kernel, w.beta, w.z)
+    r = eng.evaluate(True)
+    mu, s, y = (np.asfortranarray(t.cpu().numpy()) for t in (w.mu, w.s, w.y))
+    ref = orc.engine_evaluate(True, mu, s, y, w.z, w.variance, w.lengthscales, w.beta, workers=THREADS)
+    _check_eval(r, ref, True)
+
+
+def test_c5_shape_d100(sgp, orc):
+    """C5 shape (Q = 20, D = 100, M = 256: 32,896 pairs) at an oracle-sized N."""
+    from paper_1410_4984_b200 import synthetic
+
+    w = synthetic.make(True, 20_000, 20, 100, 256, seed=11)
+    eng = sgp.Engine(sgp.ModelKind.latent, w.mu, w.s, w.y)
+    eng.broadcast(w.kernel, w.beta, w.z)
+    r = eng.evaluate(True)
+    ref = orc.engine_evaluate(True, w.mu, w.s, w.y, w.z, w.variance, w.lengthscales, w.beta, workers=THREADS)
+    _check_eval(r, ref, True)
+
+
+def test_c4_shape_sgpr(sgp, orc):
+    """C4 shape (SGPR, Q = 8, D = 1, M = 500: 125,250 pairs) at an oracle-sized N."""
+    from paper_1410_4984_b200 import synthetic
+
+    w = synthetic.make(False, 20_000, 8, 1, 500, seed=21)
+    eng = sgp.Engine(sgp.ModelKind.regression, w.mu, None, w.y)
+    eng.broadcast(w.kernel, w.beta, w.z)
+    r = eng.evaluate(True)
+    ref = orc.engine_evaluate(False, w.mu, None, w.y, w.z, w.variance, w.lengthscales, w.beta, workers=THREADS)
+    _check_eval(r, ref, False)
+
+
+# ---------------------------------------------------------------------------------------------
+# the accuracy envelope
+# ---------------------------------------------------------------------------------------------
+def _layout(kind, f, n=4000, q=10, d=10, m=100, seed=1):
+    rng = np.random.default_rng(seed)
+    s = rng.uniform(0.25, 1.0, (n, q))
+    y = rng.normal(size=(n, d))
+    ls = rng.uniform(0.5, 2.0, q)
+    if kind == "gauss":  # mu ~ N(0, f^2), Z from mu
+        mu = f * rng.normal(size=(n, q))
+        z = mu[rng.choice(n, m, replace=False)] + 0.05 * rng.normal(size=(m, q))
+    elif kind == "bimodal":  # two clusters at +-f l along q = 0, inducing points in both
+        mu = rng.normal(size=(n, q))
+        mu[:, 0] += np.where(np.arange(n) % 2 == 0, 1.0, -1.0) * f * ls[0]
+        z = mu[rng.choice(n, m, replace=False)] + 0.05 * rng.normal(size=(m, q))
+    elif kind == "farcluster":  # 10 % of the rows f l away, no inducing point there
+        mu = rng.normal(size=(n, q))
+        z = mu[rng.choice(n, m, replace=False)] + 0.05 * rng.normal(size=(m, q))
+        mu[: n // 10, 0] += f * ls[0]
+    elif kind == "outliers":  # 8 rows f l away along every dimension
+        mu = rng.normal(size=(n, q))
+        z = mu[rng.choice(np.arange(8, n), m, replace=False)] + 0.05 * rng.normal(size=(m, q))
+        mu[:8] += f * ls
+    elif kind == "zcluster":  # a small far cluster (5 % of rows) holding 5 inducing points
+        mu = rng.normal(size=(n, q))
+        k = n // 20
+        mu[:k, 0] += f * ls[0]
+        idx = np.concatenate([rng.choice(k, 5, replace=False), rng.choice(np.arange(k, n), m - 5, replace=False)])
+        z = mu[idx] + 0.05 * rng.normal(size=(m, q))
+    a = rng.normal(size=(m, m))
+    adj = (-0.7, rng.normal(size=(m, d)), a + a.T)
+    return mu, s, y, z, ls, adj
+
+
+ENVELOPE = [  # (layout, expected mode latent, expected mode SGPR)
+    ("gauss", 1, "fast", "precise"), ("gauss", 2, "fast", "direct"), ("gauss", 3, "precise", "direct"),
+    ("gauss", 8, "direct", "direct"), ("gauss", 16, "direct", "direct"), ("gauss", 24, "direct", "direct"),
+    ("gauss", 32, "direct", "direct"), ("bimodal", 10, "precise", "direct"), ("bimodal", 30, "direct", "direct"),
+    ("bimodal", 300, "direct", "direct"), ("farcluster", 300, "fast", "precise"),
+    ("outliers", 30, "fast", "precise"), ("outliers", 1000, "fast", "precise"),
+    ("zcluster", 20, "precise", "direct"), ("zcluster", 60, "direct", "direct"),
+]
+
+
+@pytest.mark.parametrize("expected", [True, False])
+@pytest.mark.parametrize("case", ENVELOPE, ids=lambda c: f"{c[0]}{c[1]}")
+def test_accuracy_envelope(sgp, orc, case, expected):
+    kind, f, mode_latent, mode_det = case
+    mu, s, y, z, ls, adj = _layout(kind, f)
+    k = sgp.KernelSpec(1.3, ls)
+    ctx = sgp.Context.default()
+    ctx.set_precision("auto")
+    st, g = sgp.sweep_stats(expected, mu, s if expected else None, y, z, k, adj=sgp.StatsAdjoints(*adj))
+    mode, tz = ctx.last_precision()
+    assert mode == (mode_latent if expected else mode_det), (mode, tz)
+    wst, wg = orc.sweep_stats(expected, mu, s if expected else None, y, z, 1.3, ls, adj=adj)
+    pairs = dict(phi=(st.phi_big, wst.phi_big, STAT_TOL), psi=(st.psi_y, wst.psi_y, STAT_TOL),
+                 dz=(g.d_z, wg.d_z, GRAD_TOL), dl=(g.d_lengthscales, wg.d_lengthscales, GRAD_TOL),
+                 dvar=([g.d_variance], [wg.d_variance], GRAD_TOL))
+    if expected:
+        pairs.update(dmu=(g.d_mu, wg.d_mu, GRAD_TOL), ds=(g.d_s, wg.d_s, GRAD_TOL))
+    elem_tol = DIRECT_TOL if mode == "direct" else ELEM_TOL
+    for name, (a, b, tol) in pairs.items():
+        assert np.all(np.isfinite(a)), name
+        assert rel_err(a, b) < elem_tol, (name, rel_err(a, b), mode)
+        assert norm_rel_err(a, b) < tol, (name, norm_rel_err(a, b), mode)
+
+
+def _random_shapes(count, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        out.append((int(rng.integers(1, 3000)), int(rng.choice([1, 3, 7, 10, 20, 24, 29, 32, 40, 64])),
+                    int(rng.integers(0, 9)), int(rng.integers(1, 90)), bool(rng.integers(0, 2))))
+    return out
+
+
+@pytest.mark.parametrize("shape", _random_shapes(12, seed=77))
+def test_direct_mode_parity(sgp, orc, shape):
+    """The direct (fp64-exponent) kernels forced on seeded random shapes, Q up to 64 (beyond the
+    row-tile instantiations they are the only path), both modes, ragged N, D = 0."""
+    n, q, d, m, expected = shape
+    m = min(m, n)
+    rng = np.random.default_rng(n + q)
+    mu = 3.0 * rng.normal(size=(n, q))
+    s = rng.uniform(0.25, 1.0, (n, q))
+    y = rng.normal(size=(n, d))
+    z = mu[rng.choice(n, m, replace=False)]
+    ls = rng.uniform(0.5, 2.0, q)
+    a = rng.normal(size=(m, m))
+    adj = (0.3, rng.normal(size=(m, d)), a + a.T)
+    ctx = sgp.Context.default()
+    k = sgp.KernelSpec(0.8, ls)
+    st, g = sgp.sweep_stats(expected, mu, s if expected else None, y, z, k, adj=sgp.StatsAdjoints(*adj),
+                            precision="direct")
+    assert ctx.last_precision()[0] == "direct"
+    ctx.set_precision("auto")
+    wst, wg = orc.sweep_stats(expected, mu, s if expected else None, y, z, 0.8, ls, adj=adj)
+    assert rel_err(st.yy, wst.yy) < 1e-13 and st.n_count == wst.n_count
+    outs = [(st.phi_big, wst.phi_big), (g.d_z, wg.d_z), (g.d_lengthscales, wg.d_lengthscales),
+            ([g.d_variance], [wg.d_variance])]
+    if d:
+        outs.append((st.psi_y, wst.psi_y))
+    if expected:
+        outs += [(g.d_mu, wg.d_mu), (g.d_s, wg.d_s)]
+    for a_, b_ in outs:
+        assert rel_err(a_, b_) < DIRECT_TOL
+        assert norm_rel_err(a_, b_) < DIRECT_TOL
+
+
+def test_direct_mode_engine_subshards(sgp, orc):
+    """The direct path through the engine's host-buffer sub-shard pipeline (pair sums folded across
+    sub-shards, d mu / d S streamed out), a bimodal latent space at +-300 l."""
+    import torch
+
+    n, q, d, m = 520_000, 3, 2, 12
+    rng = np.random.default_rng(3)
+    mu = rng.normal(size=(n, q))
+    mu[:, 0] += np.where(np.arange(n) % 2 == 0, 300.0, -300.0)
+    s = rng.uniform(0.25, 1.0, (n, q))
+    y = rng.normal(size=(n, d))
+    z = mu[rng.choice(n, m, replace=False)]
+    ls = np.ones(q)
+    eng = sgp.Engine(sgp.ModelKind.latent, mu, s, y)
+    gmu = torch.empty(q, n, dtype=torch.float64, pin_memory=True).numpy().T
+    gs = torch.empty(q, n, dtype=torch.float64, pin_memory=True).numpy().T
+    eng.set_local_grads_out(gmu, gs)
+    eng.broadcast(sgp.KernelSpec(1.0, ls), 20.0, z, mu, s)
+    r = eng.evaluate(True)
+    assert r.timing.precision == "direct"
+    ref = orc.engine_evaluate(True, mu, s, y, z, 1.0, ls, 20.0, workers=THREADS)
+    _check_eval(r, ref, True, elem_tol=DIRECT_TOL, bound_tol=1e-9)
