@@ -219,6 +219,7 @@ typedef struct {
   int fwd_grid, bwd_grid;            /* persistent CTAs launched */
   int precision_used;                /* SGPX_PREC_FAST / PRECISE / DIRECT of this evaluation */
   double z_spread;                   /* Tz = max_a sum_q ((z_aq - c_q) / l_q)^2, c = mean of Z */
+  double psi2_fwd_kernel_s, psi2_bwd_kernel_s; /* the main psi2 kernel of each pass alone (first sub-shard) */
 } sgpx_eval_result;
 
 int sgpx_engine_create(sgpx_ctx* ctx, const sgpx_engine_config* cfg, sgpx_engine** out);

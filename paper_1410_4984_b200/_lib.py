@@ -66,7 +66,8 @@ class eval_result(C.Structure):
                 ("jitter_factor_used", C.c_double), ("stats_pass_s", C.c_double), ("coordinator_s", C.c_double),
                 ("grad_pass_s", C.c_double), ("wall_s", C.c_double), ("fwd_kernel_s", C.c_double),
                 ("bwd_kernel_s", C.c_double), ("fwd_grid", C.c_int), ("bwd_grid", C.c_int),
-                ("precision_used", C.c_int), ("z_spread", C.c_double)]
+                ("precision_used", C.c_int), ("z_spread", C.c_double), ("psi2_fwd_kernel_s", C.c_double),
+                ("psi2_bwd_kernel_s", C.c_double)]
 
 
 # name -> (restype, argtypes)

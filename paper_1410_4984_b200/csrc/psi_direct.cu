@@ -687,8 +687,10 @@ int dir_forward_q(const PsiConst& P, double* base, double* packed, int* err_flag
   const DirFwd L = dir_fwd_layout(P, num_sms);
   dir_rows_kernel<<<L.nrb, 256, 0, st>>>(P, with_kl, base + L.off_rows, err_flag);
   if (P.n > 0 && P.m > 0) {
+    if (P.ev_psi2[0]) cudaEventRecord(static_cast<cudaEvent_t>(P.ev_psi2[0]), st);
     dir_pair_fwd_kernel<Q><<<dim3(unsigned((L.npairs + kPairThreads - 1) / kPairThreads), unsigned(L.ns2)),
                              kPairThreads, 0, st>>>(P, L.npairs, L.cps2, base + L.off_ppart);
+    if (P.ev_psi2[1]) cudaEventRecord(static_cast<cudaEvent_t>(P.ev_psi2[1]), st);
     if (P.d > 0)
       dir_psi1_fwd_kernel<Q><<<dim3(unsigned((P.m + 31) / 32), unsigned(L.ns1), unsigned((P.d + 63) / 64)), 256, 0,
                                st>>>(P, L.cps1, base + L.off_p1);
@@ -717,7 +719,9 @@ int dir_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* 
     nr1 = L.g1;
     nr2 = L.g2;
     dir_psi1_bwd_kernel<Q><<<L.g1, kBwdThreads, 0, st>>>(P, B, L.rstride, bbase + L.off_rows1);
+    if (P.ev_psi2[0]) cudaEventRecord(static_cast<cudaEvent_t>(P.ev_psi2[0]), st);
     dir_pair_bwd_kernel<Q><<<L.g2, kBwdThreads, 0, st>>>(P, B, F.npairs, bbase + L.off_dl2);
+    if (P.ev_psi2[1]) cudaEventRecord(static_cast<cudaEvent_t>(P.ev_psi2[1]), st);
     g_tc_launches.fetch_add(2);
   }
   if (!B.skip_pair_terms) {

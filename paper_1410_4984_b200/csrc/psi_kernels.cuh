@@ -46,6 +46,7 @@ struct PsiConst {
   double ls[kMaxQ];
   unsigned long long* prof;   // optional per-phase cycle counters (SGPX_TC_PROFILE=1), else null
   int mode;                   // kModeFast / kModePrecise / kModeDirect (psi_select_mode)
+  void* ev_psi2[2];           // optional cudaEvent_t pair recorded around the main psi2 kernel (roofline)
 };
 
 // Backward-only inputs.

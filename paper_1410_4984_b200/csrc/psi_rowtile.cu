@@ -1145,7 +1145,9 @@ int launch_rowtile(const PsiConst& P, RowTileArgs R, dim3 grid, cudaStream_t st)
       return 3;
     }
   } else {
+    if (P.ev_psi2[0]) cudaEventRecord(static_cast<cudaEvent_t>(P.ev_psi2[0]), st);
     kern<<<grid, kThreads, cfg.smem, st>>>(P, R);
+    if (P.ev_psi2[1]) cudaEventRecord(static_cast<cudaEvent_t>(P.ev_psi2[1]), st);
   }
   g_tc_launches.fetch_add(1);
   const cudaError_t e = cudaPeekAtLastError();

@@ -295,7 +295,7 @@ struct sgpx_engine {
   coord::Stats st;  // unpacked statistics of the last coordinate() (complete_adjoints needs them)
   bool coordinated = false, with_grads = false;
   bool pairs_folded = false;  // sub-shard pair sums folded into the first (once per forward)
-  cudaEvent_t ev[8] = {};  // 0-1 stats pass, 2-3 grad pass, 4-5 fwd kernel, 6-7 bwd kernel
+  cudaEvent_t ev[12] = {};  // 0-1 stats pass, 2-3 grad pass, 4-5 fwd psi, 6-7 bwd psi, 8-11 psi2 kernels
   double coord_s = 0.0;
   double z_spread = 0.0;
   LaunchGeom gf{}, gb{};
@@ -457,6 +457,8 @@ void engine_stats_pass(sgpx_engine* e) {
     auto& sub = e->subs[j];
     if (e->pending_upload) CUDA_OK(cudaStreamWaitEvent(ctx->stream, e->ev_in[j], 0));
     double* out = k > 1 ? e->pstats_sub.get<double>() + int64_t(j) * count : e->pstats.get<double>();
+    sub.P.ev_psi2[0] = j == 0 ? e->ev[8] : nullptr;  // the first sub-shard's main psi2 kernel (roofline)
+    sub.P.ev_psi2[1] = j == 0 ? e->ev[9] : nullptr;
     if (psi_forward(sub.P, e->fpart.get<double>() + sub.foff, out, e->err.get<int>(), ctx->num_sms, ctx->stream,
                     &e->gf, j == 0 ? e->ev[4] : nullptr, j == k - 1 ? e->ev[5] : nullptr))
       throw CudaError(std::string("psi forward launch: ") + cudaGetErrorString(cudaGetLastError()));
@@ -565,6 +567,8 @@ void engine_grad_pass(sgpx_engine* e) {
       B.fwd_rt = fwd_region(sub.P, e->fpart.get<double>() + sub.foff, ctx->num_sms);
       B.skip_pair_terms = (fold && j > 0) ? 1 : 0;
       double* out = k > 1 ? e->pgrads_sub.get<double>() + int64_t(j) * count : e->pgrads.get<double>();
+      sub.P.ev_psi2[0] = j == 0 ? e->ev[10] : nullptr;
+      sub.P.ev_psi2[1] = j == 0 ? e->ev[11] : nullptr;
       if (psi_backward(sub.P, B, e->bpart.get<double>() + sub.boff, out, ctx->num_sms, ctx->stream, &e->gb,
                        j == 0 ? e->ev[6] : nullptr, j == k - 1 ? e->ev[7] : nullptr))
         throw CudaError(std::string("psi backward launch: ") + cudaGetErrorString(cudaGetLastError()));
@@ -630,17 +634,31 @@ void engine_finish(sgpx_engine* e, sgpx_eval_result* out) {
     ms = 0.f;
     if (e->in.n > 0) cudaEventElapsedTime(&ms, e->ev[6], e->ev[7]);
     out->bwd_kernel_s = ms * 1e-3;
+    ms = 0.f;
+    if (e->in.n > 0 && cudaEventElapsedTime(&ms, e->ev[10], e->ev[11]) != cudaSuccess) {
+      cudaGetLastError();
+      ms = 0.f;
+    }
+    out->psi2_bwd_kernel_s = ms * 1e-3;
   } else {
     CUDA_OK(cudaStreamSynchronize(ctx->stream));
     out->d_variance = 0.0;
     out->d_beta = 0.0;
     out->grad_pass_s = 0.0;
+    out->bwd_kernel_s = 0.0;
+    out->psi2_bwd_kernel_s = 0.0;
   }
   cudaEventElapsedTime(&ms, e->ev[0], e->ev[1]);
   out->stats_pass_s = ms * 1e-3;
   ms = 0.f;
   if (e->in.n > 0) cudaEventElapsedTime(&ms, e->ev[4], e->ev[5]);
   out->fwd_kernel_s = ms * 1e-3;
+  ms = 0.f;
+  if (e->in.n > 0 && cudaEventElapsedTime(&ms, e->ev[8], e->ev[9]) != cudaSuccess) {
+    cudaGetLastError();
+    ms = 0.f;
+  }
+  out->psi2_fwd_kernel_s = ms * 1e-3;
   out->fwd_grid = e->gf.grid;
   out->bwd_grid = e->with_grads ? e->gb.grid : 0;
   out->coordinator_s = e->coord_s;

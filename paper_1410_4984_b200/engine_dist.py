@@ -42,7 +42,8 @@ class CudaPasses:
     the psi kernels are ordered on one stream without extra synchronisation.
     """
 
-    def __init__(self, kind, x_or_mu, s, y, n_global, row_begin, jitter_factor=1e-6, device=None):
+    def __init__(self, kind, x_or_mu, s, y, n_global, row_begin, jitter_factor=1e-6, device=None,
+                 precision="auto"):
         import torch
 
         self.torch = torch
@@ -51,7 +52,7 @@ class CudaPasses:
         self.stream = torch.cuda.current_stream(dev)
         self.ctx.set_stream(self.stream.cuda_stream)
         self.eng = sgp.Engine(kind, x_or_mu, s, y, ctx=self.ctx, _n_global=n_global, _row_begin=row_begin,
-                              jitter_factor=jitter_factor)
+                              jitter_factor=jitter_factor, precision=precision)
         self.kind = sgp.ModelKind(kind)
         self._lib = L.load()
 
@@ -89,7 +90,7 @@ class DistributedEngine:
     """
 
     def __init__(self, kind, x_or_mu_local, s_local, y_local, n_global: int, row_begin: int, group=None,
-                 passes=None, jitter_factor: float = 1e-6):
+                 passes=None, jitter_factor: float = 1e-6, precision: str = "auto"):
         import torch.distributed as dist
 
         self.dist = dist
@@ -99,7 +100,7 @@ class DistributedEngine:
         self.row_begin = row_begin
         self.n_local = y_local.shape[0]
         self.passes = passes or CudaPasses(kind, x_or_mu_local, s_local, y_local, n_global, row_begin,
-                                           jitter_factor=jitter_factor)
+                                           jitter_factor=jitter_factor, precision=precision)
 
     @staticmethod
     def shard_of(n_global: int, rank: int, world: int):
@@ -111,6 +112,9 @@ class DistributedEngine:
 
     def set_local_grads_out(self, dmu, ds):
         self.passes.eng.set_local_grads_out(dmu, ds)
+
+    def local_grads(self, out=None):
+        return self.passes.eng.local_grads(out)
 
     def evaluate(self, with_grads: bool = True, local_to_host: bool = True) -> sgp.EvalResult:
         eng = getattr(self.passes, "eng", None)

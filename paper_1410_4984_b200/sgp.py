@@ -388,6 +388,8 @@ class EngineTimings:
     bwd_grid: int = 0
     precision: str = "auto"
     z_spread: float = 0.0
+    psi2_fwd_kernel_s: float = 0.0
+    psi2_bwd_kernel_s: float = 0.0
 
 
 @dataclass
@@ -526,7 +528,7 @@ class Engine:
                     g.d_mu, g.d_s = self.local_grads(getattr(self, "_grads_out", None))
         t = EngineTimings(r.stats_pass_s, r.coordinator_s, r.grad_pass_s, r.wall_s, r.fwd_kernel_s, r.bwd_kernel_s,
                           r.fwd_grid, r.bwd_grid, L.PRECISION_NAMES.get(int(r.precision_used), "none"),
-                          float(r.z_spread))
+                          float(r.z_spread), float(r.psi2_fwd_kernel_s), float(r.psi2_bwd_kernel_s))
         return EvalResult(BoundBreakdown._from(r.bound), stats, bool(r.has_grads), g, t, r.jitter_factor_used)
 
     def evaluate(self, with_grads: bool = True, local_to_host: bool = True) -> EvalResult:
