@@ -55,7 +55,7 @@ DTYPES = {
             "M-sized algebra fp64",
     "precise": "mixed: psi2 exponents as 3-piece fp16 tcgen05 MMAs (~2^-33), exp2 on MUFU/FMA (2^-22), "
                "scaled-fp16 hi-lo contraction MMAs (~2^-22), psi1 fp32, every sum and all M-sized algebra fp64",
-    "direct": "f64 direct-difference exponents, fp32 exp2 of the fraction (2^-22), f64 contractions and sums",
+    "direct": "f64: direct-difference exponents, exp and every contraction and sum in fp64",
 }
 
 
@@ -274,7 +274,8 @@ def run_b200(args, world, rank, local_rank):
         n_global = n_cfg
         row_begin, row_end = sgp.make_partition(n_global, world)[rank]
     n_local = row_end - row_begin
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # a capturable stream: the engine replays each evaluation as a CUDA graph
+    torch.cuda.set_stream(stream)
     ctx = sgp.Context(local_rank)
     ctx.set_stream(stream.cuda_stream)
     # the reference generator's stream on the device; every rank generates the full dataset (weak

@@ -16,6 +16,8 @@
  *                           adjoints_from_core (bound.hpp:196-226)
  *   sgpx_finish_host        gradient assembly of Engine::evaluate (parallel.hpp:414-421):
  *                           kern_grads(Z,Z,dKmm) (kernels.hpp:124-164) + jitter term
+ *   sgpx_multi_*            sgp::Engine(workers) over several GPUs of one process: shards per
+ *                           make_partition (parallel.hpp:28-41), NCCL allreduce exchanges
  *   sgpx_rng_*              sgp::Rng::normal_matrix (common.hpp:45-97) generated on the device,
  *                           the init_gplvm Z-row choice (model.hpp:420-429)
  *   sgpx_io_*               write_matrix_bin / read_matrix_bin (io.hpp:114-153) + a streamed
@@ -41,8 +43,8 @@
  *                psi2 contraction as 16-bit split MMAs (bf16 hi/lo ~2^-17 forward, scaled fp16
  *                hi/lo ~2^-22 backward), psi1 in fp32 tiles;
  *       precise  as fast with three fp16 exponent pieces (~2^-33) and fp16 forward MMA3 pieces;
- *       direct   direct-difference exponents in fp64 (the reference's own form), fp32 exp2 of
- *                the fraction (2^-22), fp64 contractions;
+ *       direct   direct-difference exponents and exp in fp64 (the reference's own form, ~1 ulp),
+ *                fp64 contractions;
  *     every sum across datapoints and across CTAs is fp64, all M-sized algebra is fp64.  AUTO
  *     picks fast / precise / direct from the spread of the inducing points.
  *   - There is no CPU fallback: without a CUDA device every compute entry point
@@ -253,6 +255,29 @@ int sgpx_engine_local_grads_device(sgpx_engine* eng, double** d_mu, double** d_s
  * in its result, parallel.hpp:424-429).  Null data pointers unregister. */
 int sgpx_engine_set_local_grads_out(sgpx_engine* eng, sgpx_mmat d_mu, sgpx_mmat d_s);
 int sgpx_engine_copy_local_grads(sgpx_engine* eng, sgpx_mmat d_mu, sgpx_mmat d_s);
+/* predict (SparseGPRegression::predict / BayesianGPLVM::predict, model.hpp:181-217, 291-296, 378-383)
+ * from the factors of the engine's last evaluation at the current parameters (the reference's
+ * finalize()): mean = beta K*m G, var = variance - |L_k^-1 k*|^2 + |L_a^-1 k*|^2 (floored at 1e-15
+ * variance, + 1/beta when observation != 0), the same column for every output dimension.  x_star: T x Q
+ * host; mean / var: T x D host; cached_bound (nullable): that evaluation's bound. */
+int sgpx_engine_predict(sgpx_engine* eng, sgpx_cmat x_star, int observation, sgpx_mmat mean, sgpx_mmat var,
+                        double* cached_bound);
+
+/* ---- multi-GPU engine: Engine(workers) (parallel.hpp:326-479) in one process --------------------
+ * N is split by make_partition (parallel.hpp:28-41) into `workers` shards, shard i on devices[i], each
+ * with its own context.  The two exchanges of an evaluation sum the packed buffers: shards sharing a
+ * device are folded on it, then one ncclAllReduce (sum, fp64) runs across the distinct devices
+ * (NCCL communicators from ncclCommInitAll; libnccl is opened at run time, SGPX_NCCL if absent).
+ * cfg: kind, n_global, q, d, m, jitter_factor, precision (row_begin / n_local are per shard).
+ * Host views cover all N rows; d_mu / d_s (latent, nullable) receive every shard's rows. */
+typedef struct sgpx_multi sgpx_multi;
+int sgpx_multi_create(int workers, const int* devices, const sgpx_engine_config* cfg, sgpx_multi** out);
+int sgpx_multi_destroy(sgpx_multi* mu);
+int sgpx_multi_workers(const sgpx_multi* mu);
+int sgpx_multi_set_data(sgpx_multi* mu, sgpx_cmat x_or_mu, sgpx_cmat s, sgpx_cmat y);
+int sgpx_multi_broadcast(sgpx_multi* mu, const sgpx_kernel_spec* kernel, double beta, sgpx_cmat z, sgpx_cmat mu_,
+                         sgpx_cmat s);
+int sgpx_multi_evaluate(sgpx_multi* mu, int with_grads, sgpx_eval_result* out, sgpx_mmat d_mu, sgpx_mmat d_s);
 
 /* ---- seeded inputs and binary matrices ------------------------------------ */
 /* Rng(seed).normal_matrix(rows, cols) (common.hpp:86-91), bit-for-bit the reference's splitmix64 +

@@ -292,6 +292,28 @@ def engine_evaluate(latent, x_or_mu, s, y, z, variance, lengthscales, beta, work
     return res
 
 
+def predict(latent, x_or_mu, s, y, z, variance, lengthscales, beta, x_star, observation=True, jitter_factor=1e-6):
+    """finalize() + predict(X*) of SparseGPRegression / BayesianGPLVM (model.hpp:181-217, 265-296, 353-383):
+    returns (mean T x D, variance T x D, cached_bound)."""
+    x = F(x_or_mu)
+    y = F(y)
+    z = F(z)
+    xs = F(x_star)
+    n, q = x.shape
+    d = y.shape[1]
+    m = z.shape[0]
+    t = xs.shape[0]
+    s = F(s) if latent else None
+    ls = F(np.broadcast_to(np.asarray(lengthscales, dtype=np.float64), (q,)))
+    mean = np.zeros((t, d), order="F")
+    var = np.zeros((t, d), order="F")
+    bound = C.c_double()
+    _check(lib().oracle_predict(C.c_int(1 if latent else 0), _i64(n), _i64(q), _i64(d), _i64(m), _p(x), _p(s), _p(y),
+                                _p(z), _d(variance), _p(ls), _d(beta), _d(jitter_factor), _i64(t), _p(xs),
+                                C.c_int(1 if observation else 0), _p(mean), _p(var), C.byref(bound)))
+    return mean, var, bound.value
+
+
 def rng_normal_matrix(seed, rows, cols):
     """Rng(seed).normal_matrix(rows, cols) (common.hpp:86-91), column-major result."""
     out = np.zeros((rows, cols), order="F")

@@ -1162,6 +1162,53 @@ int oracle_engine_evaluate(int kind, int64_t n, int64_t q, int64_t d, int64_t m,
   });
 }
 
+// Prediction (model.hpp:181-217): finalize() = stats at the current parameters, factor_gram, bound_core
+// (model.hpp:265-276, 353-364), then predict_from_cache on kern_cross(X*, Z).  obs != 0 adds 1/beta.
+int oracle_predict(int kind, int64_t n, int64_t q, int64_t d, int64_t m, const double* x_or_mu, const double* s,
+                   const double* y, const double* z, double variance, const double* ls, double beta,
+                   double jitter_factor, int64_t t, const double* x_star, int obs, double* mean_out,
+                   double* var_out, double* bound_out) {
+  return guard([&] {
+    Kernel k = mk_kernel(variance, ls, q);
+    const bool latent = kind == 1;
+    Stats st;
+    sweep_stats(latent, cv(x_or_mu, n, q, 0), latent ? cv(s, n, q, 0) : View{}, cv(y, n, d, 0), cv(z, m, q, 0), k,
+                Tiles{64, 1024}, nullptr, st, nullptr);
+    GramFactor gram = factor_gram(cv(z, m, q, 0), k, jitter_factor);
+    Core core = bound_core(st, gram.kmm, beta, n, d);
+    double kl = 0.0;
+    if (latent)  // kl_gaussian (bound.hpp:164-169)
+      for (Index j = 0; j < q; ++j)
+        for (Index i = 0; i < n; ++i) {
+          const double mu = x_or_mu[i + j * n], sv = s[i + j * n];
+          kl += 0.5 * (sv + mu * mu - std::log(sv) - 1.0);
+        }
+    *bound_out = core.bd.total - kl;
+    Mat ks = kern_cross(cv(x_star, t, q, 0), cv(z, m, q, 0), k);  // T x M
+    Mat mean = matmul(ks, core.g);
+    for (double& v : mean.v) v *= beta;
+    put(mean, mean_out, 0);
+    for (Index r = 0; r < t; ++r) {
+      double n1 = 0.0, n2 = 0.0;  // |L_k^-1 k*|^2, |L_a^-1 k*|^2 by forward substitution
+      for (int which = 0; which < 2; ++which) {
+        const Mat& L = which == 0 ? gram.L : core.La;
+        std::vector<double> x(static_cast<size_t>(m));
+        double acc = 0.0;
+        for (Index i = 0; i < m; ++i) {
+          double sum = ks(r, i);
+          for (Index kk = 0; kk < i; ++kk) sum -= L(i, kk) * x[size_t(kk)];
+          x[size_t(i)] = sum / L(i, i);
+          acc += x[size_t(i)] * x[size_t(i)];
+        }
+        (which == 0 ? n1 : n2) = acc;
+      }
+      double v = std::max(variance - n1 + n2, 1e-15 * variance);
+      if (obs) v += 1.0 / beta;
+      for (Index c = 0; c < d; ++c) var_out[r + c * t] = v;
+    }
+  });
+}
+
 // Rng restatement: fills column-major rows x cols with next_normal() in row-major visiting order
 // (common.hpp:86-91).  Returns the generator state so callers can chain.
 void oracle_rng_normal_matrix(uint64_t seed, int64_t rows, int64_t cols, double* out) {

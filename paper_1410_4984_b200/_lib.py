@@ -106,6 +106,13 @@ SIGNATURES = {
     "sgpx_engine_local_grads_device": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "sgpx_engine_copy_local_grads": (C.c_int, [C.c_void_p, mmat, mmat]),
     "sgpx_engine_set_local_grads_out": (C.c_int, [C.c_void_p, mmat, mmat]),
+    "sgpx_engine_predict": (C.c_int, [C.c_void_p, cmat, C.c_int, mmat, mmat, C.POINTER(C.c_double)]),
+    "sgpx_multi_create": (C.c_int, [C.c_int, C.c_void_p, C.POINTER(engine_config), C.POINTER(C.c_void_p)]),
+    "sgpx_multi_destroy": (C.c_int, [C.c_void_p]),
+    "sgpx_multi_workers": (C.c_int, [C.c_void_p]),
+    "sgpx_multi_set_data": (C.c_int, [C.c_void_p, cmat, cmat, cmat]),
+    "sgpx_multi_broadcast": (C.c_int, [C.c_void_p, C.POINTER(kernel_spec), C.c_double, cmat, cmat, cmat]),
+    "sgpx_multi_evaluate": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(eval_result), mmat, mmat]),
     "sgpx_rng_normal_matrix": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int64, C.c_int64, mmat, C.c_int]),
     "sgpx_rng_choose_rows": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.c_void_p]),
     "sgpx_io_matrix_shape": (C.c_int, [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
@@ -152,13 +159,17 @@ class SgpxCudaError(SgpxError):
     code = SGPX_CUDA
 
 
+class SgpxNcclError(SgpxError):
+    code = SGPX_NCCL
+
+
 class SgpxIoError(SgpxError, OSError):
     """std::runtime_error of the reference's io.hpp."""
     code = SGPX_IO
 
 
 _ERRORS = {SGPX_INVALID_ARGUMENT: SgpxInvalidArgument, SGPX_NUMERIC: SgpxNumericError, SGPX_CUDA: SgpxCudaError,
-           SGPX_IO: SgpxIoError}
+           SGPX_IO: SgpxIoError, SGPX_NCCL: SgpxNcclError}
 
 
 def check(rc: int):

@@ -1,0 +1,745 @@
+// dcoord.cu -- the coordinator of Engine::evaluate on the device.
+//
+// Reference: factor_gram (kernels.hpp:177-197), bound_core (bound.hpp:84-119), adjoints_from_core
+// (bound.hpp:196-226), kern_grads(Z, Z, dKmm) (kernels.hpp:124-164) and the gradient assembly of
+// Engine::evaluate (parallel.hpp:378-421).  The same fp64 algebra as coordinator.cpp, restated as a
+// sequence of stream-ordered kernels, so that one evaluation (forward psi pass -> allreduce #1 ->
+// coordinator -> backward psi pass -> allreduce #2 -> assembly) never waits on the host and can be
+// replayed as one CUDA graph.  Numeric breakdowns (no Cholesky at the largest jitter, a non-finite
+// bound) and contract violations of the reduced statistics set a status word that the host reads
+// with the results and turns into the reference's exceptions.
+//
+//   per broadcast   Kmm (no jitter), factor_gram escalation -> L_k, log|Kmm|, W_k = L_k^-1,
+//                   Kmm^-1 = W_k^T W_k
+//   after AR #1     A = Kmm + jitter + beta Phi, factor_spd escalation -> L_a, log|A|, A^-1, G = A^-1 Psi,
+//                   G G^T, the bound terms, d Phi / d Psi as the fp32 operands of the backward kernels,
+//                   then (off the backward's critical path) Kmm^-1 Phi Kmm^-1, d Kmm, Phi G, d beta
+//   after AR #2     kern_grads(Z, Z, d Kmm) + the jitter term, final gradient vector
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+
+#include "dcoord.cuh"
+#include "dla.cuh"
+
+namespace sgpx {
+extern std::atomic<int64_t> g_tc_launches;
+
+namespace {
+
+constexpr double kLog2Pi = 1.8378770664093454835606594728112;
+
+// Kmm without jitter: var exp(-1/2 sum_q (z_aq - z_bq)^2 / l_q^2) (kern_gram, kernels.hpp:83-112).
+__global__ void gram_kernel(const double* __restrict__ z, int m, int q, const double* __restrict__ ls, double var,
+                            double* __restrict__ kmm) {
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= int64_t(m) * m) return;
+  const int a = int(e % m), b = int(e / m);
+  double d2 = 0.0;
+  for (int j = 0; j < q; ++j) {
+    const double d = (z[a + int64_t(j) * m] - z[b + int64_t(j) * m]) / ls[j];
+    d2 += d * d;
+  }
+  kmm[e] = a == b ? var : var * exp(-0.5 * d2);
+}
+
+// A = Kmm + jitter I + beta Phi (Phi mirrored from the packed upper triangle).
+__global__ void build_a_kernel(const double* __restrict__ kmm, const double* __restrict__ packed, int m, double beta,
+                               double var, const double* __restrict__ sc, double* __restrict__ a) {
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= int64_t(m) * m) return;
+  const int i = int(e % m), j = int(e / m);
+  const int lo = min(i, j), hi = max(i, j);
+  const double phi = packed[4 + int64_t(lo) * m - int64_t(lo) * (lo - 1) / 2 + (hi - lo)];
+  const double jit = i == j ? sc[kScJitterFactor] * var : 0.0;
+  a[e] = kmm[e] + jit + beta * phi;
+}
+
+// Phi (mirrored) into a dense M x M matrix.
+__global__ void unpack_phi_kernel(const double* __restrict__ packed, int m, double* __restrict__ phi) {
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= int64_t(m) * m) return;
+  const int i = int(e % m), j = int(e / m);
+  const int lo = min(i, j), hi = max(i, j);
+  phi[e] = packed[4 + int64_t(lo) * m - int64_t(lo) * (lo - 1) / 2 + (hi - lo)];
+}
+
+__device__ double block_sum(double v, double* red) {
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  const double s = red[0];
+  __syncthreads();
+  return s;
+}
+
+// Bound terms (bound.hpp:108-116) and the scalar adjoint d_phi; contract checks of the reduced
+// statistics (bound.hpp:84-92).  One CTA, fixed-order trees.
+__global__ void __launch_bounds__(1024) bound_kernel(DcArgs A) {
+  __shared__ double red[1024];
+  const int m = A.m, d = A.d;
+  const double* packed = A.packed;
+  const double* psi = packed + 4 + int64_t(m) * (m + 1) / 2;
+  double pg = 0.0, kp = 0.0, ap = 0.0;
+  for (int64_t e = threadIdx.x; e < int64_t(m) * d; e += blockDim.x) pg += psi[e] * A.g[e];
+  for (int64_t e = threadIdx.x; e < int64_t(m) * m; e += blockDim.x) {
+    kp += A.kinv[e] * A.phi[e];
+    ap += A.ainv[e] * A.phi[e];
+  }
+  pg = block_sum(pg, red);
+  kp = block_sum(kp, red);
+  ap = block_sum(ap, red);
+  if (threadIdx.x == 0) {
+    double* sc = A.sc;
+    int st = int(sc[kScStatus]);
+    const double beta = A.beta, nd = double(A.n), dd = double(d);
+    const double phi0 = packed[0], yy = packed[1], nc = packed[2], kl = packed[3];
+    if (!(nc == nd)) st |= kStBadCount;
+    if (!(phi0 >= 0.0 && yy >= 0.0)) st |= kStBadStats;
+    const double logdet_k = sc[kScLogDetK], logdet_a = sc[kScLogDetA];
+    double* bd = sc + kScBound;
+    bd[1] = dd * (0.5 * nd * log(beta) + 0.5 * logdet_k - 0.5 * nd * kLog2Pi - 0.5 * logdet_a);
+    bd[2] = -0.5 * beta * yy;
+    bd[3] = 0.5 * beta * beta * pg;
+    bd[4] = -0.5 * beta * dd * phi0;
+    bd[5] = 0.5 * beta * dd * kp;
+    bd[6] = A.latent ? -kl : 0.0;
+    bd[0] = bd[1] + bd[2] + bd[3] + bd[4] + bd[5] + bd[6];
+    if (!isfinite(bd[0])) st |= kStNonFinite;
+    sc[kScPg] = pg;
+    sc[kScKp] = kp;
+    sc[kScAp] = ap;
+    sc[kScDPhi] = -0.5 * beta * dd;
+    sc[kScStatus] = double(st);
+  }
+}
+
+// d Phi = -1/2 beta D A^-1 - 1/2 beta^3 G G^T + 1/2 beta D Kmm^-1 (bound.hpp:203-210), mirrored into
+// the fp32 [mv][mv] operand of the backward kernels, and d Psi^T = beta^2 G^T as fp32 [d][mv].
+__global__ void adjoint_kernel(DcArgs A, float* __restrict__ u, float* __restrict__ dpsi, double* __restrict__ u64,
+                               double* __restrict__ dpsi64) {
+  const int m = A.m, mv = A.mv, d = A.d;
+  const double beta = A.beta, dd = double(d);
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e < int64_t(mv) * mv) {
+    const int i = int(e % mv), j = int(e / mv);
+    double v = 0.0;
+    if (i < m && j < m) {
+      const int64_t k = i + int64_t(j) * m;
+      v = -0.5 * beta * dd * A.ainv[k] - 0.5 * beta * beta * beta * A.ggt[k] + 0.5 * beta * dd * A.kinv[k];
+    }
+    u[e] = float(v);  // symmetric: A^-1, G G^T, Kmm^-1 are exactly symmetric products
+    u64[e] = v;
+  }
+  if (e < int64_t(max(d, 1)) * mv) {
+    const int a = int(e % mv), dc = int(e / mv);
+    const double v = (a < m && dc < d) ? beta * beta * A.g[a + int64_t(dc) * m] : 0.0;
+    dpsi[e] = float(v);
+    dpsi64[e] = v;
+  }
+}
+
+// d Kmm (bound.hpp:211-216) = 1/2 D Kmm^-1 - 1/2 D A^-1 - 1/2 beta^2 G G^T - 1/2 beta D sym(Kmm^-1 Phi Kmm^-1)
+__global__ void dkmm_kernel(DcArgs A) {
+  const int m = A.m;
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= int64_t(m) * m) return;
+  const int i = int(e % m), j = int(e / m);
+  const double beta = A.beta, dd = double(A.d);
+  const double kpk = 0.5 * (A.kpk[e] + A.kpk[j + int64_t(i) * m]);
+  A.dkmm[e] = 0.5 * dd * A.kinv[e] - 0.5 * dd * A.ainv[e] - 0.5 * beta * beta * A.ggt[e] - 0.5 * beta * dd * kpk;
+}
+
+// d beta (bound.hpp:217-223) and kern_grads(Z, Z, d Kmm) with the gradient assembly of
+// parallel.hpp:414-421 (d_z + d_x, d var + jitter_factor tr(d Kmm), d l).  One CTA.
+__global__ void __launch_bounds__(1024) finish_kernel(DcArgs A, const double* __restrict__ pgrads) {
+  __shared__ double red[1024];
+  const int m = A.m, q = A.q, d = A.d;
+  const double beta = A.beta, nd = double(A.n), dd = double(d);
+  double* sc = A.sc;
+  // tr(G^T Phi G)
+  double tg = 0.0;
+  for (int64_t e = threadIdx.x; e < int64_t(m) * d; e += blockDim.x) tg += A.g[e] * A.phig[e];
+  tg = block_sum(tg, red);
+  // W = d Kmm o K (K without jitter), row sums, total, trace of d Kmm
+  double tot = 0.0, tr = 0.0;
+  for (int64_t e = threadIdx.x; e < int64_t(m) * m; e += blockDim.x) {
+    const double w = A.dkmm[e] * A.kmm[e];
+    A.w[e] = w;
+    tot += w;
+    if (e % m == e / m) tr += A.dkmm[e];
+  }
+  tot = block_sum(tot, red);
+  tr = block_sum(tr, red);
+  __syncthreads();
+  for (int a = threadIdx.x; a < m; a += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < m; ++b) s += A.w[a + int64_t(b) * m];
+    A.rs[a] = s;
+  }
+  __syncthreads();
+  // W Z (M x Q): thread per (a, j), ascending b
+  for (int64_t e = threadIdx.x; e < int64_t(m) * q; e += blockDim.x) {
+    const int a = int(e % m), j = int(e / m);
+    double s = 0.0;
+    for (int b = 0; b < m; ++b) s += A.w[a + int64_t(b) * m] * A.z[b + int64_t(j) * m];
+    A.wz[e] = s;
+  }
+  __syncthreads();
+  double* res = A.result;  // [d var, d l (Q), d Z (M Q), d beta]
+  for (int64_t e = threadIdx.x; e < int64_t(m) * q; e += blockDim.x) {
+    const int a = int(e % m), j = int(e / m);
+    const double il2 = 1.0 / (A.ls[j] * A.ls[j]);
+    res[1 + q + e] = pgrads[1 + q + e] + 2.0 * (A.wz[e] - A.rs[a] * A.z[e]) * il2;
+  }
+  // sum_ab W_ab (z_a - z_b)^2 = 2 (sum_a rs_a z_a^2 - z^T W z) per dimension (thread per q, ascending a)
+  for (int j = threadIdx.x; j < q; j += blockDim.x) {
+    double s2 = 0.0, cross = 0.0;
+    for (int a = 0; a < m; ++a) {
+      const double za = A.z[a + int64_t(j) * m];
+      s2 += A.rs[a] * za * za;
+      cross += za * A.wz[a + int64_t(j) * m];
+    }
+    res[1 + j] = pgrads[1 + j] + 2.0 * (s2 - cross) / (A.ls[j] * A.ls[j] * A.ls[j]);
+  }
+  if (threadIdx.x == 0) {
+    res[0] = pgrads[0] + tot / A.var + sc[kScJitterFactor] * tr;
+    const double yy = A.packed[1], phi0 = A.packed[0];
+    res[1 + q + int64_t(m) * q] = 0.5 * dd * nd / beta - 0.5 * dd * sc[kScAp] - 0.5 * yy + beta * sc[kScPg] -
+                                  0.5 * beta * beta * tg - 0.5 * dd * phi0 + 0.5 * dd * sc[kScKp];
+  }
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Small-M path (M <= kSmallM): each coordinator step is ONE CTA working in shared memory —
+// left-looking Cholesky (2 barriers per column), L^-1 by column substitution, and the products.
+// ---------------------------------------------------------------------------------------------
+constexpr int kSmallM = 112;  // 2 M^2 doubles of shared memory (<= 200 KB)
+__device__ long long g_dc_prof[16];  // SGPX debug: clock64 phase stamps of bound_small_kernel
+#define DC_STAMP(i) \
+  if (threadIdx.x == 0) g_dc_prof[i] = clock64()
+
+// Left-looking lower Cholesky of the shared m x m matrix L (lower triangle valid) in place.  Column j:
+// each row's dot product over k < j is split across 8 lanes (k = r mod 8) and combined by a fixed
+// xor tree, so the dependent chain is j / 8 long.
+__device__ bool chol_left_smem(double* L, int m, int* s_flag) {
+  constexpr int kSplit = 8;
+  if (threadIdx.x == 0) *s_flag = 1;
+  __syncthreads();
+  const int r = threadIdx.x & (kSplit - 1);
+  for (int j = 0; j < m; ++j) {
+    for (int base = j; base < m; base += blockDim.x / kSplit) {
+      const int i = base + int(threadIdx.x) / kSplit;
+      double s = 0.0;
+      if (i < m)
+        for (int k = r; k < j; k += kSplit) s += L[i + k * m] * L[j + k * m];
+      s += __shfl_xor_sync(0xffffffffu, s, 4);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      if (i < m && r == 0) L[i + j * m] -= s;
+    }
+    __syncthreads();
+    const double d = L[j + j * m];
+    if (!(d > 0.0)) {
+      if (threadIdx.x == 0) *s_flag = 0;
+      __syncthreads();
+      return false;
+    }
+    const double ljj = sqrt(d), inv = 1.0 / ljj;
+    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) L[i + j * m] *= inv;
+    __syncthreads();
+    if (threadIdx.x == 0) L[j + j * m] = ljj;
+  }
+  __syncthreads();
+  return *s_flag != 0;
+}
+
+// W = L^-1 (lower), row by row: W_kj = (delta_kj - sum_{j <= i < k} L_ki W_ij) / L_kk for every j <= k
+// at once, each dot product split across 8 lanes (fixed xor tree).  Stored row-major
+// (S[k m + j] = W_kj).  `inv` holds m doubles of scratch (1 / L_kk).
+__device__ void trinv_smem(const double* L, double* S, int m, double* inv) {
+  constexpr int kSplit = 8;
+  for (int k = threadIdx.x; k < m; k += blockDim.x) inv[k] = 1.0 / L[k + k * m];
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) S[e] = 0.0;
+  __syncthreads();
+  const int r = threadIdx.x & (kSplit - 1);
+  for (int k = 0; k < m; ++k) {
+    for (int base = 0; base <= k; base += blockDim.x / kSplit) {
+      const int j = base + int(threadIdx.x) / kSplit;
+      double s = 0.0;
+      if (j <= k)
+        for (int i = j + r; i < k; i += kSplit) s += L[k + i * m] * S[i * m + j];
+      s += __shfl_xor_sync(0xffffffffu, s, 4);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      if (j <= k && r == 0) S[k * m + j] = ((k == j ? 1.0 : 0.0) - s) * inv[k];
+    }
+    __syncthreads();
+  }
+}
+
+// X = W^T W from the row-major S (exactly symmetric: both triangles from the same products in the
+// same order) -> out (and out2 if given); W^T W_ab = sum_{k >= max(a,b)} W_ka W_kb
+__device__ void wtw_smem(const double* S, int m, double* out, double* out2 = nullptr) {
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int i = e % m, j = e / m;
+    const int a = max(i, j), b = min(i, j);
+    double s = 0.0;
+#pragma unroll 4
+    for (int k = a; k < m; ++k) s += S[k * m + a] * S[k * m + b];
+    out[e] = s;
+    if (out2) out2[e] = s;
+  }
+}
+
+__device__ double block_sum_s(double v, double* red) {
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  const double s = red[0];
+  __syncthreads();
+  return s;
+}
+
+// Factor the shared matrix rebuilt by `fill(shift)` with the escalation schedule of `mode` (see
+// chol_kernel); returns the factor used through *fac, log det through *logdet.
+template <class Fill>
+__device__ bool factor_smem(double* L, int m, int mode, double f0, double var, double scale, Fill fill, double* red,
+                            int* s_flag, double* fac, double* logdet) {
+  double f = mode == 0 ? f0 : 0.0;
+  bool ok = false;
+  for (int attempt = 0; attempt < 32; ++attempt) {
+    fill(mode == 0 ? f * var : f * scale);
+    __syncthreads();
+    ok = chol_left_smem(L, m, s_flag);
+    if (threadIdx.x == 0) {
+      g_dc_prof[10 + mode] = attempt + 1;
+      g_dc_prof[12 + mode] = ok;
+    }
+    if (ok) break;
+    if (mode == 0) {
+      if (f >= 1e-2) break;
+      f = f == 0.0 ? 1e-6 : f * 10.0;
+    } else {
+      f = f == 0.0 ? 1e-10 : f * 10.0;
+      if (!(f <= 1e-2)) break;
+    }
+  }
+  double s = 0.0;
+  if (ok)
+    for (int i = threadIdx.x; i < m; i += blockDim.x) s += log(L[i + i * m]);
+  s = block_sum_s(s, red);
+  *fac = f;
+  *logdet = 2.0 * s;
+  return ok;
+}
+
+__global__ void __launch_bounds__(1024) prefactor_small_kernel(DcArgs A) {
+  extern __shared__ double sm[];
+  __shared__ double red[1024];
+  __shared__ int s_flag;
+  const int m = A.m, q = A.q;
+  double* L = sm;
+  double* W = sm + m * m;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {  // Kmm without jitter (kern_gram)
+    const int a = e % m, b = e / m;
+    double d2 = 0.0;
+    for (int j = 0; j < q; ++j) {
+      const double d = (A.z[a + int64_t(j) * m] - A.z[b + int64_t(j) * m]) / A.ls[j];
+      d2 += d * d;
+    }
+    A.kmm[e] = a == b ? A.var : A.var * exp(-0.5 * d2);
+  }
+  __syncthreads();
+  double fac = 0.0, ld = 0.0;
+  const bool ok = factor_smem(
+      L, m, 0, A.jitter_factor, A.var, 0.0,
+      [&](double shift) {
+        for (int e = threadIdx.x; e < m * m; e += blockDim.x) L[e] = A.kmm[e] + (e % m == e / m ? shift : 0.0);
+      },
+      red, &s_flag, &fac, &ld);
+  if (ok) {
+    trinv_smem(L, W, m, red);
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) A.wk[e] = W[(e % m) * m + e / m];  // L_k^-1 (prediction)
+    wtw_smem(W, m, A.kinv);
+  }
+  if (threadIdx.x == 0) {
+    A.sc[kScLogDetK] = ld;
+    A.sc[kScJitterFactor] = fac;
+    A.sc[kScStatusK] = ok ? 0.0 : double(kStGramFailed);
+  }
+}
+
+__global__ void __launch_bounds__(1024) bound_small_kernel(DcArgs A, float* __restrict__ u, float* __restrict__ dpsi,
+                                                           double* __restrict__ u64, double* __restrict__ dpsi64) {
+  extern __shared__ double sm[];
+  __shared__ double red[1024];
+  __shared__ int s_flag;
+  const int m = A.m, d = A.d, mv = A.mv;
+  double* L = sm;
+  double* W = sm + m * m;
+  const double* packed = A.packed;
+  const double* psi = packed + 4 + int64_t(m) * (m + 1) / 2;
+  const double beta = A.beta, jit = A.sc[kScJitterFactor] * A.var;
+  DC_STAMP(0);
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int i = e % m, j = e / m, lo = min(i, j), hi = max(i, j);
+    A.phi[e] = packed[4 + int64_t(lo) * m - int64_t(lo) * (lo - 1) / 2 + (hi - lo)];
+  }
+  __syncthreads();
+  double mx = 0.0;  // factor_spd's scale: max |a_ii|
+  for (int i = threadIdx.x; i < m; i += blockDim.x)
+    mx = fmax(mx, fabs(A.kmm[i + i * m] + jit + beta * A.phi[i + i * m]));
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  const double scale = red[0];
+  __syncthreads();
+  double fac = 0.0, ld = 0.0;
+  const bool ok = factor_smem(
+      L, m, 1, 0.0, 0.0, scale,
+      [&](double shift) {
+        for (int e = threadIdx.x; e < m * m; e += blockDim.x)
+          L[e] = A.kmm[e] + beta * A.phi[e] + (e % m == e / m ? jit + shift : 0.0);
+      },
+      red, &s_flag, &fac, &ld);
+  DC_STAMP(1);
+  if (ok) {
+    trinv_smem(L, W, m, red);
+    DC_STAMP(2);
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) A.wa[e] = W[(e % m) * m + e / m];  // L_a^-1 (prediction)
+    __syncthreads();
+    wtw_smem(W, m, L, A.ainv);  // A^-1 into shared memory (over L) and global
+  }
+  __syncthreads();
+  DC_STAMP(3);
+  // G = A^-1 Psi (M x D): A^-1 from shared memory, Psi through the read-only path; G into shared memory
+  // over W when it fits (M D <= M^2), else global only
+  double* gs = d <= m ? W : nullptr;
+  for (int64_t e = threadIdx.x; e < int64_t(m) * d; e += blockDim.x) {
+    const int a = int(e % m), c = int(e / m);
+    const double* pc = psi + int64_t(c) * m;
+    double s = 0.0;
+#pragma unroll 4
+    for (int b = 0; b < m; ++b) s += L[a + b * m] * __ldg(pc + b);
+    A.g[e] = s;
+    if (gs) gs[e] = s;
+  }
+  __syncthreads();
+  const double* gg = gs ? gs : A.g;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int i = e % m, j = e / m;
+    double s = 0.0;
+#pragma unroll 4
+    for (int c = 0; c < d; ++c) s += gg[i + int64_t(c) * m] * gg[j + int64_t(c) * m];
+    A.ggt[e] = s;
+  }
+  __syncthreads();
+  DC_STAMP(4);
+  // reductions and the bound terms (bound.hpp:108-116)
+  double pg = 0.0, kp = 0.0, ap = 0.0;
+  for (int64_t e = threadIdx.x; e < int64_t(m) * d; e += blockDim.x) pg += __ldg(psi + e) * gg[e];
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const double ph = A.phi[e];
+    kp += __ldg(A.kinv + e) * ph;
+    ap += L[e] * ph;
+  }
+  pg = block_sum_s(pg, red);
+  kp = block_sum_s(kp, red);
+  ap = block_sum_s(ap, red);
+  if (threadIdx.x == 0) {
+    double* sc = A.sc;
+    int st = int(sc[kScStatusK]) | (ok ? 0 : kStAFailed);
+    const double nd = double(A.n), dd = double(d);
+    const double phi0 = packed[0], yy = packed[1], nc = packed[2], kl = packed[3];
+    if (!(nc == nd)) st |= kStBadCount;
+    if (!(phi0 >= 0.0 && yy >= 0.0)) st |= kStBadStats;
+    double* bd = sc + kScBound;
+    bd[1] = dd * (0.5 * nd * log(beta) + 0.5 * sc[kScLogDetK] - 0.5 * nd * kLog2Pi - 0.5 * ld);
+    bd[2] = -0.5 * beta * yy;
+    bd[3] = 0.5 * beta * beta * pg;
+    bd[4] = -0.5 * beta * dd * phi0;
+    bd[5] = 0.5 * beta * dd * kp;
+    bd[6] = A.latent ? -kl : 0.0;
+    bd[0] = bd[1] + bd[2] + bd[3] + bd[4] + bd[5] + bd[6];
+    if (!isfinite(bd[0])) st |= kStNonFinite;
+    sc[kScLogDetA] = ld;
+    sc[kScShiftA] = fac;
+    sc[kScPg] = pg;
+    sc[kScKp] = kp;
+    sc[kScAp] = ap;
+    sc[kScDPhi] = -0.5 * beta * dd;
+    sc[kScStatus] = double(st);
+  }
+  __syncthreads();
+  DC_STAMP(5);
+  // the backward's operands (bound.hpp:203-210)
+  const double dd = double(d);
+  for (int e = threadIdx.x; e < mv * mv; e += blockDim.x) {
+    const int i = e % mv, j = e / mv;
+    double v = 0.0;
+    if (i < m && j < m) {
+      const int k = i + j * m;
+      v = -0.5 * beta * dd * L[k] - 0.5 * beta * beta * beta * A.ggt[k] + 0.5 * beta * dd * __ldg(A.kinv + k);
+    }
+    u[e] = float(v);
+    u64[e] = v;
+  }
+  for (int64_t e = threadIdx.x; e < int64_t(max(d, 1)) * mv; e += blockDim.x) {
+    const int a = int(e % mv), c = int(e / mv);
+    const double v = (a < m && c < d) ? beta * beta * gg[a + int64_t(c) * m] : 0.0;
+    dpsi[e] = float(v);
+    dpsi64[e] = v;
+  }
+}
+
+__global__ void dc_prof_kernel(long long* out) {
+  if (threadIdx.x < 16) out[threadIdx.x] = g_dc_prof[threadIdx.x];
+}
+
+// d Kmm (with Kmm^-1 Phi Kmm^-1), Phi G, d beta, kern_grads(Z, Z, d Kmm), the assembly: one CTA.
+__global__ void __launch_bounds__(1024) deferred_small_kernel(DcArgs A) {
+  extern __shared__ double sm[];
+  const int m = A.m, d = A.d;
+  double* K = sm;          // Kmm^-1
+  double* T = sm + m * m;  // Phi, then Kmm^-1 Phi
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    K[e] = A.kinv[e];
+    T[e] = A.phi[e];
+  }
+  __syncthreads();
+  for (int64_t e = threadIdx.x; e < int64_t(m) * d; e += blockDim.x) {  // Phi G
+    const int i = int(e % m), c = int(e / m);
+    const double* gc = A.g + int64_t(c) * m;
+    double s = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < m; ++k) s += T[i + k * m] * __ldg(gc + k);
+    A.phig[e] = s;
+  }
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {  // tmp = Kmm^-1 Phi
+    const int i = e % m, j = e / m;
+    double s = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < m; ++k) s += K[i + k * m] * T[k + j * m];
+    A.tmp[e] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) T[e] = A.tmp[e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {  // kpk = tmp Kmm^-1
+    const int i = e % m, j = e / m;
+    double s = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < m; ++k) s += T[i + k * m] * K[k + j * m];
+    A.kpk[e] = s;
+  }
+  __syncthreads();
+  const double beta = A.beta, dd = double(d);
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int i = e % m, j = e / m;
+    const double kpk = 0.5 * (A.kpk[e] + A.kpk[j + i * m]);
+    A.dkmm[e] = 0.5 * dd * A.kinv[e] - 0.5 * dd * A.ainv[e] - 0.5 * beta * beta * A.ggt[e] - 0.5 * beta * dd * kpk;
+  }
+}
+
+__global__ void init_status_kernel(double* sc, const int* info_k) {
+  if (threadIdx.x == 0) sc[kScStatusK] = info_k[0] ? double(kStGramFailed) : 0.0;
+}
+// this evaluation's status: the prefactor's, plus A's factorisation
+__global__ void status_a_kernel(double* sc, const int* info_a) {
+  if (threadIdx.x == 0) sc[kScStatus] = double(int(sc[kScStatusK]) | (info_a[0] ? kStAFailed : 0));
+}
+
+inline unsigned blocks_for(int64_t n) { return unsigned((n + 255) / 256); }
+
+}  // namespace
+
+int64_t dc_workspace_doubles(int m, int q, int d) {
+  const int64_t mm = int64_t(m) * m, md = int64_t(m) * std::max(d, 1), mq = int64_t(m) * q;
+  // kmm lk wk kinv a la wa ainv phi ggt tmp kpk dkmm w (14 M x M), g phig (M x D), rs (M), wz (M x Q),
+  // scalars, result, ls (Q), info (2 ints in 1 double)
+  return 14 * mm + 2 * md + m + mq + kScCount + (2 + q + mq) + q + 2;
+}
+
+void dc_bind(DcArgs& A, double* ws) {
+  const int m = A.m, q = A.q;
+  const int64_t mm = int64_t(m) * m, md = int64_t(m) * std::max(A.d, 1), mq = int64_t(m) * q;
+  double* p = ws;
+  auto take = [&p](int64_t n) {
+    double* r = p;
+    p += n;
+    return r;
+  };
+  A.kmm = take(mm);
+  A.lk = take(mm);
+  A.wk = take(mm);
+  A.kinv = take(mm);
+  A.a = take(mm);
+  A.la = take(mm);
+  A.wa = take(mm);
+  A.ainv = take(mm);
+  A.phi = take(mm);
+  A.ggt = take(mm);
+  A.tmp = take(mm);
+  A.kpk = take(mm);
+  A.dkmm = take(mm);
+  A.w = take(mm);
+  A.g = take(md);
+  A.phig = take(md);
+  A.rs = take(m);
+  A.wz = take(mq);
+  A.sc = take(kScCount);
+  A.result = take(2 + q + mq);
+  A.ls = take(q);  // uploaded by the caller
+  A.info = reinterpret_cast<int*>(take(2));
+}
+
+size_t small_smem(int m) { return sizeof(double) * 2 * size_t(m) * m; }
+
+int dc_prefactor(const DcArgs& A, cudaStream_t st) {
+  const int m = A.m;
+  if (m <= kSmallM) {
+    if (cudaFuncSetAttribute(prefactor_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(small_smem(kSmallM))) != cudaSuccess)
+      return 3;
+    prefactor_small_kernel<<<1, 1024, small_smem(m), st>>>(A);
+    g_tc_launches.fetch_add(1);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  }
+  gram_kernel<<<blocks_for(int64_t(m) * m), 256, 0, st>>>(A.z, m, A.q, A.ls, A.var, A.kmm);
+  g_tc_launches.fetch_add(1);
+  if (dla::cholesky(A.kmm, m, A.lk, 0, A.jitter_factor, A.var, A.sc + kScLogDetK, A.info, st)) return 3;
+  init_status_kernel<<<1, 32, 0, st>>>(A.sc, A.info);
+  g_tc_launches.fetch_add(1);
+  if (dla::trinv(A.lk, m, A.wk, st)) return 3;
+  if (dla::gemm(true, false, m, m, m, 1.0, A.wk, m, A.wk, m, 0.0, A.kinv, m, st)) return 3;
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+int dc_bound(const DcArgs& A, float* u, float* dpsi, double* u64, double* dpsi64, cudaStream_t st) {
+  const int m = A.m, d = A.d;
+  if (m <= kSmallM) {
+    if (cudaFuncSetAttribute(bound_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(small_smem(kSmallM))) != cudaSuccess)
+      return 3;
+    bound_small_kernel<<<1, 1024, small_smem(m), st>>>(A, u, dpsi, u64, dpsi64);
+    g_tc_launches.fetch_add(1);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  }
+  const int64_t mm = int64_t(m) * m;
+  build_a_kernel<<<blocks_for(mm), 256, 0, st>>>(A.kmm, A.packed, m, A.beta, A.var, A.sc, A.a);
+  unpack_phi_kernel<<<blocks_for(mm), 256, 0, st>>>(A.packed, m, A.phi);
+  g_tc_launches.fetch_add(2);
+  if (dla::cholesky(A.a, m, A.la, 1, 0.0, 0.0, A.sc + kScLogDetA, A.info + 1, st)) return 3;
+  status_a_kernel<<<1, 32, 0, st>>>(A.sc, A.info + 1);
+  g_tc_launches.fetch_add(1);
+  if (dla::trinv(A.la, m, A.wa, st)) return 3;
+  if (dla::gemm(true, false, m, m, m, 1.0, A.wa, m, A.wa, m, 0.0, A.ainv, m, st)) return 3;
+  const double* psi = A.packed + 4 + int64_t(m) * (m + 1) / 2;
+  if (dla::gemm(false, false, m, d, m, 1.0, A.ainv, m, psi, m, 0.0, A.g, m, st)) return 3;
+  if (dla::gemm(false, true, m, m, d, 1.0, A.g, m, A.g, m, 0.0, A.ggt, m, st)) return 3;
+  bound_kernel<<<1, 1024, 0, st>>>(A);
+  const int64_t na = std::max<int64_t>(int64_t(A.mv) * A.mv, int64_t(std::max(d, 1)) * A.mv);
+  adjoint_kernel<<<blocks_for(na), 256, 0, st>>>(A, u, dpsi, u64, dpsi64);
+  g_tc_launches.fetch_add(2);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+int dc_deferred(const DcArgs& A, cudaStream_t st) {
+  const int m = A.m, d = A.d;
+  if (m <= kSmallM) {
+    if (cudaFuncSetAttribute(deferred_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(small_smem(kSmallM))) != cudaSuccess)
+      return 3;
+    deferred_small_kernel<<<1, 1024, small_smem(m), st>>>(A);
+    g_tc_launches.fetch_add(1);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  }
+  if (dla::gemm(false, false, m, m, m, 1.0, A.kinv, m, A.phi, m, 0.0, A.tmp, m, st)) return 3;
+  if (dla::gemm(false, false, m, m, m, 1.0, A.tmp, m, A.kinv, m, 0.0, A.kpk, m, st)) return 3;
+  if (dla::gemm(false, false, m, d, m, 1.0, A.phi, m, A.g, m, 0.0, A.phig, m, st)) return 3;
+  dkmm_kernel<<<blocks_for(int64_t(m) * m), 256, 0, st>>>(A);
+  g_tc_launches.fetch_add(1);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+int dc_finish(const DcArgs& A, const double* pgrads, cudaStream_t st) {
+  finish_kernel<<<1, 1024, 0, st>>>(A, pgrads);
+  g_tc_launches.fetch_add(1);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+// ---- prediction (predict_from_cache, model.hpp:197-217) ----
+namespace {
+__global__ void kstar_kernel(const double* __restrict__ xs, int64_t t, const double* __restrict__ z, int m, int q,
+                             const double* __restrict__ ls, double var, double* __restrict__ ks) {
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= t * m) return;
+  const int64_t r = e % t;
+  const int a = int(e / t);
+  double d2 = 0.0;
+  for (int j = 0; j < q; ++j) {
+    const double dd = (xs[r + j * t] - z[a + int64_t(j) * m]) / ls[j];
+    d2 += dd * dd;
+  }
+  ks[e] = var * exp(-0.5 * d2);
+}
+
+// var = variance - |L_k^-1 k*|^2 + |L_a^-1 k*|^2, floored at 1e-15 variance, + 1/beta (observation);
+// the same column for every output dimension.
+__global__ void pred_var_kernel(const double* __restrict__ v1, const double* __restrict__ v2, int64_t t, int m, int d,
+                                double var, double beta, int obs, double* __restrict__ out) {
+  const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (r >= t) return;
+  double n1 = 0.0, n2 = 0.0;
+  for (int i = 0; i < m; ++i) {
+    const double a = v1[r + int64_t(i) * t], b = v2[r + int64_t(i) * t];
+    n1 += a * a;
+    n2 += b * b;
+  }
+  double v = fmax(var - n1 + n2, 1e-15 * var);
+  if (obs) v += 1.0 / beta;
+  for (int c = 0; c < d; ++c) out[r + int64_t(c) * t] = v;
+}
+}  // namespace
+
+extern "C" int sgpx_debug_dc_profile(long long* host16) {
+  long long* d = nullptr;
+  if (cudaMalloc(&d, 16 * sizeof(long long)) != cudaSuccess) return 3;
+  dc_prof_kernel<<<1, 32>>>(d);
+  cudaMemcpy(host16, d, 16 * sizeof(long long), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return 0;
+}
+
+int64_t dc_predict_doubles(int64_t t, int m, int q, int d) { return t * (q + 3 * int64_t(m) + 2 * int64_t(d)) + 8; }
+
+int dc_predict(const DcArgs& A, const double* xs, int64_t t, int obs, double* work, double* mean, double* var,
+               cudaStream_t st) {
+  const int m = A.m, q = A.q, d = A.d;
+  double* ks = work;
+  double* v1 = ks + t * m;
+  double* v2 = v1 + t * m;
+  kstar_kernel<<<unsigned((t * m + 255) / 256), 256, 0, st>>>(xs, t, A.z, m, q, A.ls, A.var, ks);
+  g_tc_launches.fetch_add(1);
+  if (dla::gemm(false, false, int(t), d, m, A.beta, ks, t, A.g, m, 0.0, mean, t, st)) return 3;
+  if (dla::gemm(false, true, int(t), m, m, 1.0, ks, t, A.wk, m, 0.0, v1, t, st)) return 3;
+  if (dla::gemm(false, true, int(t), m, m, 1.0, ks, t, A.wa, m, 0.0, v2, t, st)) return 3;
+  pred_var_kernel<<<unsigned((t + 255) / 256), 256, 0, st>>>(v1, v2, t, m, d, A.var, A.beta, obs, var);
+  g_tc_launches.fetch_add(1);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+}  // namespace sgpx

@@ -1,0 +1,205 @@
+// dla.cu -- fp64 dense linear algebra on the device for the M-sized coordinator and prediction.
+//
+// Reference: factor_gram / kern_gram / kern_grads (kernels.hpp:83-197), factor_spd / bound_core /
+// adjoints_from_core (bound.hpp:52-226), the coordinator block of Engine::evaluate
+// (parallel.hpp:378-421) and predict_from_cache (model.hpp:197-217).  The same algebra as
+// coordinator.cpp (host), moved onto the stream so an evaluation needs no host round trip between
+// its passes and can be captured as one CUDA graph:
+//   dla_gemm        C = alpha op(A) op(B) + beta C, 64 x 64 tiles, fixed k order (deterministic)
+//   chol_kernel     one CTA: Cholesky with the reference's diagonal escalation schedules
+//                   (factor_gram: jitter = f var, f = f0, 10 f0, ... <= 1e-2; factor_spd: + f max|a_ii|,
+//                   f = 1e-10 ... 1e-2), log-determinant, status flag
+//   trinv_kernel    W = L^-1 (lower), one thread per column
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+
+#include "dla.cuh"
+
+namespace sgpx {
+extern std::atomic<int64_t> g_tc_launches;
+
+namespace dla {
+namespace {
+
+constexpr int kT = 64, kK = 16;
+
+__global__ void __launch_bounds__(256) gemm_kernel(int ta, int tb, int m, int n, int k, double alpha,
+                                                   const double* __restrict__ A, int64_t lda,
+                                                   const double* __restrict__ B, int64_t ldb, double beta,
+                                                   double* __restrict__ C, int64_t ldc) {
+  __shared__ double As[kK][kT + 1], Bs[kK][kT + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4 x 4 outputs each
+  const int i0 = blockIdx.x * kT, j0 = blockIdx.y * kT;
+  double acc[4][4] = {};
+  for (int p0 = 0; p0 < k; p0 += kK) {
+    for (int e = threadIdx.x; e < kK * kT; e += 256) {
+      const int pp = e / kT, ii = e % kT;
+      const int i = i0 + ii, p = p0 + pp;
+      double a = 0.0;
+      if (i < m && p < k) a = ta ? A[p + int64_t(i) * lda] : A[i + int64_t(p) * lda];
+      As[pp][ii] = a;
+      const int j = j0 + ii;
+      double b = 0.0;
+      if (j < n && p < k) b = tb ? B[j + int64_t(p) * ldb] : B[p + int64_t(j) * ldb];
+      Bs[pp][ii] = b;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int pp = 0; pp < kK; ++pp) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = As[pp][tx + 16 * u];
+        b[u] = Bs[pp][ty + 16 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int i = i0 + tx + 16 * u, j = j0 + ty + 16 * v;
+      if (i < m && j < n) {
+        double* c = C + i + int64_t(j) * ldc;
+        *c = alpha * acc[u][v] + (beta == 0.0 ? 0.0 : beta * *c);
+      }
+    }
+}
+
+// In-place lower Cholesky of the m x m working copy `w` (lower triangle used, upper zeroed),
+// right-looking by columns; all threads of the CTA.  Returns false on a non-positive / NaN pivot.
+__device__ bool chol_inplace(double* w, int m, int64_t ld, double* s_piv) {
+  for (int j = 0; j < m; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = w[j + int64_t(j) * ld];
+      s_piv[0] = (d > 0.0) ? sqrt(d) : -1.0;
+    }
+    __syncthreads();
+    const double ljj = s_piv[0];
+    if (!(ljj > 0.0)) return false;
+    const double inv = 1.0 / ljj;
+    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) w[i + int64_t(j) * ld] *= inv;
+    __syncthreads();
+    if (threadIdx.x == 0) w[j + int64_t(j) * ld] = ljj;
+    // trailing update of the lower triangle: w[i][c] -= l_ij l_cj, j < c <= i
+    const int rem = m - j - 1;
+    for (int64_t e = threadIdx.x; e < int64_t(rem) * rem; e += blockDim.x) {
+      const int r = int(e / rem), c = int(e % rem);
+      if (c > r) continue;
+      const int i = j + 1 + r, col = j + 1 + c;
+      w[i + int64_t(col) * ld] -= w[i + int64_t(j) * ld] * w[col + int64_t(j) * ld];
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+// mode 0 (factor_gram, kernels.hpp:177-197): diag += f * var, f = f0, then x10 (0 -> 1e-6) while
+// f < 1e-2, failure after 1e-2.  mode 1 (factor_spd, bound.hpp:52-62): first the plain matrix, then
+// diag += f * max_i |a_ii| for f = 1e-10, 1e-9, ..., 1e-2.
+// a: m x m input (lower and upper valid), out: L (upper zeroed); info[0] = status (0 ok, 1 failed),
+// out_scal[0] = log det, out_scal[1] = jitter factor used (mode 0) / shift used (mode 1).
+__global__ void __launch_bounds__(1024) chol_kernel(const double* __restrict__ a, int m, double* __restrict__ L,
+                                                    int mode, double f0, double var, double* __restrict__ out_scal,
+                                                    int* __restrict__ info) {
+  __shared__ double s_piv[1], s_red[1024];
+  const int64_t ld = m;
+  double scale = 0.0;
+  if (mode == 1) {
+    double mx = 0.0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) mx = fmax(mx, fabs(a[i + int64_t(i) * ld]));
+    s_red[threadIdx.x] = mx;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) s_red[threadIdx.x] = fmax(s_red[threadIdx.x], s_red[threadIdx.x + w]);
+      __syncthreads();
+    }
+    scale = s_red[0];
+    __syncthreads();
+  }
+  double f = mode == 0 ? f0 : 0.0;
+  bool ok = false;
+  for (int attempt = 0; attempt < 32; ++attempt) {
+    const double shift = mode == 0 ? f * var : f * scale;
+    for (int64_t e = threadIdx.x; e < int64_t(m) * m; e += blockDim.x) {
+      const int i = int(e % m), j = int(e / m);
+      L[e] = i < j ? 0.0 : a[e] + (i == j ? shift : 0.0);
+    }
+    __syncthreads();
+    ok = chol_inplace(L, m, ld, s_piv);
+    __syncthreads();
+    if (ok) break;
+    if (mode == 0) {
+      if (f >= 1e-2) break;
+      f = f == 0.0 ? 1e-6 : f * 10.0;
+    } else {
+      f = f == 0.0 ? 1e-10 : f * 10.0;  // for (f = 1e-10; f <= 1e-2; f *= 10) (bound.hpp:57)
+      if (!(f <= 1e-2)) break;
+    }
+  }
+  if (threadIdx.x == 0) {
+    info[0] = ok ? 0 : 1;
+    out_scal[1] = f;
+  }
+  // log det = 2 sum log L_ii (fixed tree)
+  double s = 0.0;
+  if (ok)
+    for (int i = threadIdx.x; i < m; i += blockDim.x) s += log(L[i + int64_t(i) * ld]);
+  s_red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) s_red[threadIdx.x] += s_red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out_scal[0] = 2.0 * s_red[0];
+}
+
+// W = L^-1 (lower triangular): thread j solves L w = e_j by column-oriented forward substitution
+// (the order of coordinator.cpp's chol_inverse).
+__global__ void trinv_kernel(const double* __restrict__ L, int m, double* __restrict__ W) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double* x = W + int64_t(j) * m;
+  for (int i = 0; i < m; ++i) x[i] = i == j ? 1.0 : 0.0;
+  for (int k = j; k < m; ++k) {
+    const double xk = x[k] / L[k + int64_t(k) * m];
+    x[k] = xk;
+    const double* lk = L + int64_t(k) * m;
+    for (int i = k + 1; i < m; ++i) x[i] -= lk[i] * xk;
+  }
+}
+
+}  // namespace
+
+int gemm(bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int64_t lda, const double* B,
+         int64_t ldb, double beta, double* C, int64_t ldc, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return 0;
+  dim3 grid(unsigned((m + kT - 1) / kT), unsigned((n + kT - 1) / kT));
+  gemm_kernel<<<grid, 256, 0, st>>>(ta ? 1 : 0, tb ? 1 : 0, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+  g_tc_launches.fetch_add(1);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+int cholesky(const double* a, int m, double* L, int mode, double f0, double var, double* out_scal, int* info,
+             cudaStream_t st) {
+  chol_kernel<<<1, 1024, 0, st>>>(a, m, L, mode, f0, var, out_scal, info);
+  g_tc_launches.fetch_add(1);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+int trinv(const double* L, int m, double* W, cudaStream_t st) {
+  trinv_kernel<<<(m + 127) / 128, 128, 0, st>>>(L, m, W);
+  g_tc_launches.fetch_add(1);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+}  // namespace dla
+}  // namespace sgpx

@@ -6,8 +6,8 @@
 //   psi2  e2 = sum_q (mu_q - zbar_q)^2 / (2 S_q + l_q^2)        (psi_stats.hpp:258-263)
 // (the deterministic mode is the S = 0 case: c1 = var, c2 = var^2, den = 1/l^2, and
 // 1/2 sum((x-za)^2 + (x-zb)^2)/l^2 = sum (x-zbar)^2/l^2 + sum (za-zb)^2/(4 l^2), :264-271), then
-// v = 2^(log2 c + log2 pconst - log2e e) with the power split into 2^j (exact) * ex2.approx(f),
-// f in [0, 1) (2^-22 relative at any exponent).  No expansion of (mu - zbar)^2 is formed, so the
+// v = 2^(log2 c + log2 pconst - log2e e) in fp64 (exp2_d, ~1 ulp).  No expansion of (mu - zbar)^2 is
+// formed and no step is below fp64, so the
 // accuracy does not depend on how far mu and Z sit from each other or from any centre: this is
 // the path the engine routes to when the inducing points spread beyond the tensor-core path's
 // measured envelope, and for latent dimensions without a row-tile instantiation.
@@ -20,7 +20,8 @@
 //             dir_psi1_fwd_kernel   32 inducing points x 64 output columns per CTA:
 //                                   Psi_md = sum_n v1_nm y_nd
 //             dir_rows_kernel       yy, KL partials, validation flags
-//   backward  dir_psi1_bwd_kernel   thread per datapoint: w_nm = <y_n, dPsi_m>, uv = w v1, the psi1
+//   backward  dla::gemm             W = Y dPsi^T (fp64), the psi1 adjoint weights w_nm = <y_n, dPsi_m>
+//             dir_psi1_bwd_kernel   thread per datapoint: uv = w v1, the psi1
 //                                   parts of d mu, d S (+ KL), d l, d var; d Z_m by warp trees
 //             dir_pair_bwd_kernel   thread per datapoint: T0 = sum_p uv, A_q = sum_p uv diff_q,
 //                                   C_q = sum_p uv diff_q^2  ->  d mu -= 2 d2 A, d S += d2 (2 d2 C - T0),
@@ -32,6 +33,7 @@
 #include <algorithm>
 #include <atomic>
 
+#include "dla.cuh"
 #include "psi_common.cuh"
 #include "psi_kernels.cuh"
 
@@ -45,13 +47,28 @@ constexpr int kCh = 32;          // datapoints staged per chunk (forward sweeps)
 constexpr int kPairThreads = 128;
 constexpr double kLog2eD = 1.4426950408889634;
 
-// 2^x for fp64 x: exact 2^floor(x) times ex2.approx of the fraction (|rel err| ~ 2^-22 for any x).
-__device__ __forceinline__ double exp2_split(double x) {
-  if (!(x > -1020.0)) return 0.0;  // also -inf / NaN-free callers: underflow to exactly 0
-  const double j = floor(x);
-  const float f = float(x - j);
-  const double scale = __hiloint2double((int(j) + 1023) << 20, 0);
-  return double(ex2(f)) * scale;
+// 2^x in fp64: x = j + f with j = rint(x), |f| <= 1/2; 2^f = e^(f ln 2) by a degree-13 Taylor
+// polynomial in Horner form (truncation < 2^-60 for |f ln 2| <= 0.35), times the exact 2^j.
+// ~1 ulp, the accuracy of the reference's std::exp; underflows to exactly 0 below 2^-1020.
+__device__ __forceinline__ double exp2_d(double x) {
+  if (!(x > -1020.0)) return 0.0;  // also -inf: exactly 0
+  const double j = rint(x);
+  const double t = (x - j) * 0.69314718055994530942;
+  double p = 1.0 / 6227020800.0;  // 1/13!
+  p = fma(p, t, 1.0 / 479001600.0);
+  p = fma(p, t, 1.0 / 39916800.0);
+  p = fma(p, t, 1.0 / 3628800.0);
+  p = fma(p, t, 1.0 / 362880.0);
+  p = fma(p, t, 1.0 / 40320.0);
+  p = fma(p, t, 1.0 / 5040.0);
+  p = fma(p, t, 1.0 / 720.0);
+  p = fma(p, t, 1.0 / 120.0);
+  p = fma(p, t, 1.0 / 24.0);
+  p = fma(p, t, 1.0 / 6.0);
+  p = fma(p, t, 0.5);
+  p = fma(p, t, 1.0);
+  p = fma(p, t, 1.0);
+  return p * __hiloint2double((int(j) + 1023) << 20, 0);
 }
 
 __device__ __forceinline__ void pair_of(int64_t p, int m, int& a, int& b) {
@@ -66,8 +83,8 @@ __device__ __forceinline__ void pair_of(int64_t p, int m, int& a, int& b) {
   b = int(p - start(x)) + x;
 }
 
-__device__ __forceinline__ double pair_weight(const float* u, int mv, int a, int b) {
-  return a == b ? double(u[a * mv + a]) : double(u[a * mv + b]) + double(u[b * mv + a]);
+__device__ __forceinline__ double pair_weight(const double* u, int mv, int a, int b) {
+  return a == b ? u[a * mv + a] : u[a * mv + b] + u[b * mv + a];
 }
 
 // log2 c2_n (psi2) or log2 c1_n (psi1) of datapoint n (psi_stats.hpp:148-163): fact = 2 or 1.
@@ -144,7 +161,7 @@ __global__ void __launch_bounds__(kPairThreads) dir_pair_fwd_kernel(PsiConst P, 
           t[q] = s_d2[q][j] * df;
           e = fma(t[q], df, e);
         }
-        const double v = exp2_split(s_lc[j] + lp - kLog2eD * e);
+        const double v = exp2_d(s_lc[j] + lp - kLog2eD * e);
         phi += v;
 #pragma unroll
         for (int q = 0; q < Q; ++q) acc[q] = fma(v, t[q], acc[q]);
@@ -173,7 +190,7 @@ __global__ void dir_pair_reduce_kernel(const double* __restrict__ part, int ns, 
 
 // Psi partials: CTA (m block of 32, split, d block of 64); part[split][m + d M]
 template <int Q>
-__global__ void __launch_bounds__(256) dir_psi1_fwd_kernel(PsiConst P, int64_t cps, double* __restrict__ part) {
+__global__ void __launch_bounds__(256) dir_psi1_fwd_kernel(PsiConst P, int64_t rps, double* __restrict__ part) {
   constexpr int CH = Q < 32 ? kCh : kCh / 2;  // datapoints per staged chunk (static shared memory < 48 KB)
   __shared__ double s_z[Q][32], s_mu[Q][CH], s_d1[Q][CH], s_lc[CH], s_v[CH][33], s_y[64][CH + 1];
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
@@ -185,11 +202,9 @@ __global__ void __launch_bounds__(256) dir_psi1_fwd_kernel(PsiConst P, int64_t c
   double acc[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc[k] = 0.0;
-  const int64_t nchunks = (P.n + CH - 1) / CH;
-  const int64_t c0 = int64_t(blockIdx.y) * cps, c1 = min(nchunks, c0 + cps);
+  const int64_t r0 = int64_t(blockIdx.y) * rps, r1 = min(P.n, r0 + rps);  // this split's rows
   const double lvar = log2(P.variance_d);
-  for (int64_t c = c0; c < c1; ++c) {
-    const int64_t n0 = c * CH;
+  for (int64_t n0 = r0; n0 < r1; n0 += CH) {
     __syncthreads();
     for (int i = tid; i < Q * CH; i += 256) {
       const int q = i / CH, j = i % CH;
@@ -221,7 +236,7 @@ __global__ void __launch_bounds__(256) dir_psi1_fwd_kernel(PsiConst P, int64_t c
         const double df = s_mu[q][j] - s_z[q][lane];
         e = fma(s_d1[q][j] * df, df, e);
       }
-      s_v[j][lane] = (m0 + lane < m) ? exp2_split(s_lc[j] - 0.5 * kLog2eD * e) : 0.0;
+      s_v[j][lane] = (m0 + lane < m) ? exp2_d(s_lc[j] - 0.5 * kLog2eD * e) : 0.0;
     }
     __syncthreads();
 #pragma unroll
@@ -312,20 +327,17 @@ __global__ void dir_fwd_final_kernel(PsiConst P, const double* __restrict__ rows
 // gradients when add_kl: parallel.hpp:163-166; the psi2 kernel adds its part afterwards) and the
 // per-CTA row [d var, d l (Q), d Z (a + q M)] (persistent CTAs, owner-thread accumulation).
 constexpr int kBwdThreads = 128;
-constexpr int kDB = 64;  // dPsi columns staged per step
 
 template <int Q>
 __global__ void __launch_bounds__(kBwdThreads) dir_psi1_bwd_kernel(PsiConst P, BwdConst B, int64_t rstride,
-                                                                   double* __restrict__ rows) {
+                                                                   double* __restrict__ rows,
+                                                                   const double* __restrict__ W) {
   constexpr int KG = Q <= 32 ? 8 : 4;    // inducing points per d Z reduction group
-  constexpr int DB = Q <= 32 ? kDB : kDB / 2;  // dPsi columns staged per step (static smem < 48 KB)
   __shared__ double s_z[Q][32];
-  __shared__ float s_dp[DB][32];
-  __shared__ float s_w[32][kBwdThreads];
   __shared__ double s_dz[kBwdThreads / 32][KG][Q];
   __shared__ double s_red[kBwdThreads];
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
-  const int m = P.m, mv = P.mv;
+  const int m = P.m;
   double* row = rows + int64_t(blockIdx.x) * rstride;  // [dvar, dl (Q), dz (a + q M)]
   for (int64_t i = tid; i < rstride; i += kBwdThreads) row[i] = 0.0;
   double dvar = 0.0, dl[Q];
@@ -354,28 +366,7 @@ __global__ void __launch_bounds__(kBwdThreads) dir_psi1_bwd_kernel(PsiConst P, B
         const int q = i / 32, a = m0 + i % 32;
         s_z[q][i % 32] = (q < P.q && a < m) ? P.z64[q * m + a] : 0.0;
       }
-      // w_na = <y_n, dPsi_a> for 32 inducing points (fp32: a linear weight, no cancellation)
-      {
-        float w[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) w[k] = 0.f;
-        for (int dd0 = 0; dd0 < P.d; dd0 += DB) {
-          __syncthreads();
-          for (int i = tid; i < DB * 32; i += kBwdThreads) {
-            const int dd = dd0 + i / 32, a = m0 + i % 32;
-            s_dp[i / 32][i % 32] = (dd < P.d && a < m) ? B.dpsi[int64_t(dd) * mv + a] : 0.f;
-          }
-          __syncthreads();
-          const int dn = min(DB, P.d - dd0);
-          for (int dd = 0; dd < dn; ++dd) {
-            const float y = valid ? float(P.y[(dd0 + dd) * P.ld_y + n]) : 0.f;
-#pragma unroll
-            for (int k = 0; k < 32; ++k) w[k] = fmaf(y, s_dp[dd][k], w[k]);
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 32; ++k) s_w[k][tid] = w[k];
-      }
+      __syncthreads();
       const int na = min(32, m - m0);
       for (int k0 = 0; k0 < na; k0 += KG) {
         const int kn = min(KG, na - k0);
@@ -388,7 +379,8 @@ __global__ void __launch_bounds__(kBwdThreads) dir_psi1_bwd_kernel(PsiConst P, B
             r[q] = df[q] * d1[q];
             e = fma(r[q], df[q], e);
           }
-          const double uv = double(s_w[k][tid]) * exp2_split(lc - 0.5 * kLog2eD * e);
+          // w_na = <y_n, dPsi_a> (W = Y dPsi^T, fp64 GEMM before this kernel)
+          const double uv = (valid ? W[n + int64_t(m0 + k) * P.n] : 0.0) * exp2_d(lc - 0.5 * kLog2eD * e);
           dvar += uv * ivar;
 #pragma unroll
           for (int q = 0; q < Q; ++q) {
@@ -486,7 +478,7 @@ __global__ void __launch_bounds__(kBwdThreads) dir_pair_bwd_kernel(PsiConst P, B
         if (p < npairs) {
           int a, b;
           pair_of(p, m, a, b);
-          w = pair_weight(B.u, mv, a, b);
+          w = pair_weight(B.u64, mv, a, b);
 #pragma unroll
           for (int q = 0; q < Q; ++q) {
             double zb = 0.0;
@@ -517,7 +509,7 @@ __global__ void __launch_bounds__(kBwdThreads) dir_pair_bwd_kernel(PsiConst P, B
           df[q] = mu[q] - s_zb[q][k];
           e = fma(d2[q] * df[q], df[q], e);
         }
-        const double uv = s_w[k] * exp2_split(lc + s_lp[k] - kLog2eD * e);
+        const double uv = s_w[k] * exp2_d(lc + s_lp[k] - kLog2eD * e);
         T0 += uv;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
@@ -560,7 +552,7 @@ __global__ void __launch_bounds__(kBwdThreads) dir_pair_bwd_kernel(PsiConst P, B
 //   d Z_aq += u_p (R_pq - (z_aq - z_bq) / (2 l^2) Phi_p)  (twice for a == b)   psi_stats.hpp:297-299
 // one warp per (a, q), pairs b in a fixed lane order then a shuffle tree.
 template <int Q>
-__global__ void __launch_bounds__(256) dir_pair_dz_kernel(PsiConst P, const float* __restrict__ u,
+__global__ void __launch_bounds__(256) dir_pair_dz_kernel(PsiConst P, const double* __restrict__ u,
                                                           const double* __restrict__ sums, double* __restrict__ row) {
   const int m = P.m, mv = P.mv, lane = threadIdx.x & 31;
   const int nw = int(gridDim.x * blockDim.x) >> 5;
@@ -583,7 +575,7 @@ __global__ void __launch_bounds__(256) dir_pair_dz_kernel(PsiConst P, const floa
 
 // d l_q += l sum_p u_p Phi_p (z_a - z_b)^2 / (2 l^4)   (block k < Q);  d var += 2 sum_p u_p Phi_p / var
 // (block Q); fixed-order block trees (psi_stats.hpp:287, 300-303)
-__global__ void __launch_bounds__(256) dir_pair_dl_kernel(PsiConst P, const float* __restrict__ u, int w1,
+__global__ void __launch_bounds__(256) dir_pair_dl_kernel(PsiConst P, const double* __restrict__ u, int w1,
                                                           const double* __restrict__ sums, double* __restrict__ row) {
   __shared__ double red[256];
   const int m = P.m, mv = P.mv, k = blockIdx.x;
@@ -665,7 +657,7 @@ DirFwd dir_fwd_layout(const PsiConst& P, int num_sms) {
 struct DirBwd {
   int g1, g2;
   int64_t rstride;
-  int64_t off_rows1, off_prow, off_dl2, doubles;
+  int64_t off_rows1, off_prow, off_dl2, off_w, doubles;
 };
 
 DirBwd dir_bwd_layout(const PsiConst& P, int num_sms) {
@@ -677,7 +669,8 @@ DirBwd dir_bwd_layout(const PsiConst& P, int num_sms) {
   L.off_rows1 = 0;
   L.off_prow = L.off_rows1 + int64_t(L.g1) * L.rstride;
   L.off_dl2 = L.off_prow + L.rstride;
-  L.doubles = L.off_dl2 + int64_t(L.g2) * P.q + 2;
+  L.off_w = L.off_dl2 + int64_t(L.g2) * P.q + 2;
+  L.doubles = L.off_w + std::max<int64_t>(P.n, 1) * P.m + 2;  // W = Y dPsi^T, N x M
   return L;
 }
 
@@ -687,13 +680,13 @@ int dir_forward_q(const PsiConst& P, double* base, double* packed, int* err_flag
   const DirFwd L = dir_fwd_layout(P, num_sms);
   dir_rows_kernel<<<L.nrb, 256, 0, st>>>(P, with_kl, base + L.off_rows, err_flag);
   if (P.n > 0 && P.m > 0) {
-    if (P.ev_psi2[0]) cudaEventRecord(static_cast<cudaEvent_t>(P.ev_psi2[0]), st);
+    if (P.ev_psi2[0]) record_event(P.ev_psi2[0], st);
     dir_pair_fwd_kernel<Q><<<dim3(unsigned((L.npairs + kPairThreads - 1) / kPairThreads), unsigned(L.ns2)),
                              kPairThreads, 0, st>>>(P, L.npairs, L.cps2, base + L.off_ppart);
-    if (P.ev_psi2[1]) cudaEventRecord(static_cast<cudaEvent_t>(P.ev_psi2[1]), st);
+    if (P.ev_psi2[1]) record_event(P.ev_psi2[1], st);
     if (P.d > 0)
       dir_psi1_fwd_kernel<Q><<<dim3(unsigned((P.m + 31) / 32), unsigned(L.ns1), unsigned((P.d + 63) / 64)), 256, 0,
-                               st>>>(P, L.cps1, base + L.off_p1);
+                               st>>>(P, L.cps1 * kCh, base + L.off_p1);
   } else {
     cudaMemsetAsync(base + L.off_ppart, 0, sizeof(double) * L.ns2 * L.npairs * L.w1, st);
     cudaMemsetAsync(base + L.off_p1, 0, sizeof(double) * L.ns1 * P.m * P.d, st);
@@ -718,15 +711,21 @@ int dir_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* 
   if (P.n > 0) {
     nr1 = L.g1;
     nr2 = L.g2;
-    dir_psi1_bwd_kernel<Q><<<L.g1, kBwdThreads, 0, st>>>(P, B, L.rstride, bbase + L.off_rows1);
-    if (P.ev_psi2[0]) cudaEventRecord(static_cast<cudaEvent_t>(P.ev_psi2[0]), st);
+    double* W = bbase + L.off_w;
+    if (P.d > 0) {
+      if (dla::gemm(false, true, int(P.n), P.m, P.d, 1.0, P.y, P.ld_y, B.dpsi64, P.mv, 0.0, W, P.n, st)) return 3;
+    } else {
+      cudaMemsetAsync(W, 0, sizeof(double) * P.n * P.m, st);
+    }
+    dir_psi1_bwd_kernel<Q><<<L.g1, kBwdThreads, 0, st>>>(P, B, L.rstride, bbase + L.off_rows1, W);
+    if (P.ev_psi2[0]) record_event(P.ev_psi2[0], st);
     dir_pair_bwd_kernel<Q><<<L.g2, kBwdThreads, 0, st>>>(P, B, F.npairs, bbase + L.off_dl2);
-    if (P.ev_psi2[1]) cudaEventRecord(static_cast<cudaEvent_t>(P.ev_psi2[1]), st);
+    if (P.ev_psi2[1]) record_event(P.ev_psi2[1], st);
     g_tc_launches.fetch_add(2);
   }
   if (!B.skip_pair_terms) {
-    dir_pair_dz_kernel<Q><<<std::max(1, (P.m * P.q + 7) / 8), 256, 0, st>>>(P, B.u, sums, prow);
-    dir_pair_dl_kernel<<<P.q + 1, 256, 0, st>>>(P, B.u, F.w1, sums, prow);
+    dir_pair_dz_kernel<Q><<<std::max(1, (P.m * P.q + 7) / 8), 256, 0, st>>>(P, B.u64, sums, prow);
+    dir_pair_dl_kernel<<<P.q + 1, 256, 0, st>>>(P, B.u64, F.w1, sums, prow);
     g_tc_launches.fetch_add(2);
   }
   dir_bwd_final_kernel<<<int(std::max<int64_t>(1, std::min<int64_t>((L.rstride + 255) / 256, 1024))), 256, 0, st>>>(

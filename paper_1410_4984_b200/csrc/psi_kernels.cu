@@ -140,6 +140,7 @@ int env_mode() {
 
 std::atomic<int64_t> g_tc_launches{0};
 int64_t launches_issued() { return g_launches.load() + g_tc_launches.load(); }
+void launches_add(int64_t n) { g_tc_launches.fetch_add(n); }
 int instantiated_q(int q) { return pick_q(q); }
 
 int64_t bwd_reduce_tmp_doubles(int64_t pstride) { return int64_t(kReduceGroups) * pstride; }
@@ -206,16 +207,16 @@ int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, 
   if (int rc = plan_forward(P, num_sms, &g)) return rc;
   if (is_direct(P)) {
     if (!direct_supported(P)) return 1;
-    if (ev_begin) cudaEventRecord(cudaEvent_t(ev_begin), st);
+    if (ev_begin) record_event(ev_begin, st);
     if (int rc = direct_forward(P, part, packed, err_flag, P.expected, num_sms, stream)) return rc;
-    if (ev_end) cudaEventRecord(cudaEvent_t(ev_end), st);
+    if (ev_end) record_event(ev_end, st);
     if (geom) *geom = g;
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
   }
   const int64_t pstride = fwd_part_count(P.m, P.d);
   const int g1 = psi1_fwd_rows(P, num_sms);
   if (g1 > 0 && cudaMemsetAsync(part, 0, sizeof(double) * pstride * g1, st) != cudaSuccess) return 3;
-  if (ev_begin) cudaEventRecord(cudaEvent_t(ev_begin), st);
+  if (ev_begin) record_event(ev_begin, st);
   if (g1 > 0) {
     if (int rc = psi1_forward(P, part, pstride, g1, err_flag, stream, 1)) return rc;
   }
@@ -223,7 +224,7 @@ int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, 
                                                                  double(P.n) * P.variance_d, double(P.n));
   g_launches.fetch_add(1);
   if (int rc = rt_forward(P, part + int64_t(g1) * pstride, packed, num_sms, stream)) return rc;
-  if (ev_end) cudaEventRecord(cudaEvent_t(ev_end), st);
+  if (ev_end) record_event(ev_end, st);
   if (geom) *geom = g;
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
@@ -235,23 +236,23 @@ int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* pac
   LaunchGeom g{};
   if (int rc = plan_backward(P, num_sms, &g)) return rc;
   if (is_direct(P)) {
-    if (ev_begin) cudaEventRecord(cudaEvent_t(ev_begin), st);
+    if (ev_begin) record_event(ev_begin, st);
     if (int rc = direct_backward(P, B, part, packed, num_sms, stream)) return rc;
-    if (ev_end) cudaEventRecord(cudaEvent_t(ev_end), st);
+    if (ev_end) record_event(ev_end, st);
     if (geom) *geom = g;
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
   }
   const int64_t pstride = bwd_part_count(P.m, P.q);
   const int r1 = P.n > 0 ? psi1_bwd_rows(P, num_sms) : 0, rows = r1 + 1;
   if (cudaMemsetAsync(part, 0, sizeof(double) * pstride * rows, st) != cudaSuccess) return 3;
-  if (ev_begin) cudaEventRecord(cudaEvent_t(ev_begin), st);
+  if (ev_begin) record_event(ev_begin, st);
   // psi1 first: it writes d_mu / d_s (psi1 + KL parts); the psi2 kernel accumulates into them
   if (r1 > 0) {
     if (int rc = psi1_backward(P, B, part, pstride, r1, stream)) return rc;
   }
   if (int rc = rt_backward(P, B, part + int64_t(rows) * pstride, part + int64_t(r1) * pstride, num_sms, stream))
     return rc;
-  if (ev_end) cudaEventRecord(cudaEvent_t(ev_end), st);
+  if (ev_end) record_event(ev_end, st);
   const int64_t rt_rows = (rt_bwd_doubles(P, num_sms) + pstride - 1) / pstride;
   double* tmp = part + (int64_t(rows) + rt_rows) * pstride;
   if (int rc = bwd_reduce_rows(part, pstride, rows, packed, B.d_phi * double(P.n), tmp, stream)) return rc;

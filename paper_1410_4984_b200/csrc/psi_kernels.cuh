@@ -14,9 +14,20 @@
 // kernel) so the fp32 terms stay O(1).  One inner (n, a, b) step is Q FFMA + 1 FADD
 // + 1 MUFU.EX2 forward; the reference's direct form is ~3Q+4 flops.
 #pragma once
+#include <cuda_runtime.h>
+
 #include <cstdint>
 
 namespace sgpx {
+
+// Record a timing event; inside a stream capture (the evaluation's CUDA graph) as an external event
+// node, so that the replayed graph still times its kernels.
+inline cudaError_t record_event(void* ev, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+    return cudaEventRecordWithFlags(static_cast<cudaEvent_t>(ev), st, cudaEventRecordExternal);
+  return cudaEventRecord(static_cast<cudaEvent_t>(ev), st);
+}
 
 constexpr int kMaxQ = 64;
 
@@ -53,6 +64,8 @@ struct PsiConst {
 struct BwdConst {
   const float* u;     // [mv][mv] symmetric dL/dPhi (upper triangle mirrored), zero padded
   const float* dpsi;  // [d][mv]  dL/dPsi transposed, zero padded
+  const double* u64;     // the same two in fp64 (the direct kernels and the per-pair gradient terms)
+  const double* dpsi64;
   double d_phi;       // dL/dphi
   int add_kl;         // latent engine pass: subtract KL gradients (parallel.hpp:163-166)
   int write_local;    // write d_mu / d_s
@@ -157,7 +170,9 @@ void io_load_device(const char* base, double* dev_out, int64_t ld, void* stream)
 
 // psi1_expected: out n x m col-major fp64 (ld_out).
 int psi1_matrix(const PsiConst& P, double* out, int64_t ld_out, void* stream);
-// Number of __global__ launches issued so far by this process (evidence counter).
+// Number of __global__ launches issued so far by this process (evidence counter); graph replays add
+// their kernel count through launches_add.
 int64_t launches_issued();
+void launches_add(int64_t n);
 
 }  // namespace sgpx

@@ -891,7 +891,7 @@ __global__ void rt_pair_reduce_kernel(const double* __restrict__ part, int ns, i
 // Together they write one backward partial row [dvar, dl (Q), dz (a + q M)].
 
 template <int Q>
-__global__ void __launch_bounds__(256) rt_pair_dz_kernel(PsiConst P, const float* __restrict__ u,
+__global__ void __launch_bounds__(256) rt_pair_dz_kernel(PsiConst P, const double* __restrict__ u,
                                                          const double* __restrict__ sums, double* __restrict__ row) {
   // one warp per (a, q): lane l takes b = l, l + 32, ... in order, then a fixed shuffle tree
   constexpr int NH = 2 * Q + 1;
@@ -911,7 +911,7 @@ __global__ void __launch_bounds__(256) rt_pair_dz_kernel(PsiConst P, const float
       const double zbar = 0.5 * (za + zb);
       const double common = r[1 + q] - zbar * r[1 + Q + q];
       const double t = -(za - zb) * 0.5 * il2 * r[0] + common;
-      const double w = lo == hi ? double(u[a * mv + a]) : double(u[lo * mv + hi]) + double(u[hi * mv + lo]);
+      const double w = lo == hi ? u[a * mv + a] : u[lo * mv + hi] + u[hi * mv + lo];
       s += w * (a == b ? 2.0 * t : t);  // the diagonal pair carries z_a in both slots
     }
     s = warp_sum_d(s);
@@ -920,7 +920,7 @@ __global__ void __launch_bounds__(256) rt_pair_dz_kernel(PsiConst P, const float
 }
 
 template <int Q>
-__global__ void __launch_bounds__(256) rt_pair_dl_kernel(PsiConst P, const float* __restrict__ u,
+__global__ void __launch_bounds__(256) rt_pair_dl_kernel(PsiConst P, const double* __restrict__ u,
                                                          const double* __restrict__ sums, double* __restrict__ row) {
   constexpr int NH = 2 * Q + 1;
   __shared__ double red[256];
@@ -931,7 +931,7 @@ __global__ void __launch_bounds__(256) rt_pair_dl_kernel(PsiConst P, const float
   for (int64_t p = threadIdx.x; p < npairs; p += blockDim.x) {
     int a, b;
     pi.inv(p, a, b);
-    const double w = a == b ? double(u[a * mv + a]) : double(u[a * mv + b]) + double(u[b * mv + a]);
+    const double w = a == b ? u[a * mv + a] : u[a * mv + b] + u[b * mv + a];
     const double ph = sums[p * NH] * w;
     if (k < P.q) {
       const double dz = P.z64[k * m + a] - P.z64[k * m + b], ls = P.ls[k];
@@ -1145,9 +1145,9 @@ int launch_rowtile(const PsiConst& P, RowTileArgs R, dim3 grid, cudaStream_t st)
       return 3;
     }
   } else {
-    if (P.ev_psi2[0]) cudaEventRecord(static_cast<cudaEvent_t>(P.ev_psi2[0]), st);
+    if (P.ev_psi2[0]) record_event(P.ev_psi2[0], st);
     kern<<<grid, kThreads, cfg.smem, st>>>(P, R);
-    if (P.ev_psi2[1]) cudaEventRecord(static_cast<cudaEvent_t>(P.ev_psi2[1]), st);
+    if (P.ev_psi2[1]) record_event(P.ev_psi2[1], st);
   }
   g_tc_launches.fetch_add(1);
   const cudaError_t e = cudaPeekAtLastError();
@@ -1241,8 +1241,8 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
     if (rc) return rc;
   }
   if (!B.skip_pair_terms) {
-    rt_pair_dz_kernel<Q><<<std::max(1, (P.m * P.q + 7) / 8), 256, 0, st>>>(P, B.u, fbase + F.off_sums, prow);
-    rt_pair_dl_kernel<Q><<<P.q + 1, 256, 0, st>>>(P, B.u, fbase + F.off_sums, prow);
+    rt_pair_dz_kernel<Q><<<std::max(1, (P.m * P.q + 7) / 8), 256, 0, st>>>(P, B.u64, fbase + F.off_sums, prow);
+    rt_pair_dl_kernel<Q><<<P.q + 1, 256, 0, st>>>(P, B.u64, fbase + F.off_sums, prow);
     g_tc_launches.fetch_add(2);
   }
   if (P.n > 0) {

@@ -20,6 +20,7 @@
 
 #include "../../include/sgpx.h"
 #include "coordinator.hpp"
+#include "dcoord.cuh"
 #include "psi_kernels.cuh"
 
 namespace sgpx {
@@ -28,6 +29,9 @@ namespace {
 thread_local std::string g_last_error;
 
 struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NcclError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
@@ -54,6 +58,9 @@ int guard(F&& f) {
   } catch (const IoError& e) {
     g_last_error = e.what();
     return SGPX_IO;
+  } catch (const NcclError& e) {
+    g_last_error = e.what();
+    return SGPX_NCCL;
   } catch (const std::exception& e) {
     g_last_error = e.what();
     return SGPX_INTERNAL;
@@ -151,7 +158,7 @@ struct sgpx_ctx {
   int num_sms = 0;
   int64_t launches0 = 0;
   // scratch of the one-shot sweep / psi1 entry points
-  DevBuf mu, s, y, zc, z64, fpart, bpart, pstats, pgrads, u, dpsi, dmu, ds, err, out;
+  DevBuf mu, s, y, zc, z64, fpart, bpart, pstats, pgrads, u, dpsi, u64, dpsi64, dmu, ds, err, out;
   HostBuf h_stats, h_grads, h_u, h_dpsi, h_err, h_stage;
   int precision = SGPX_PREC_AUTO;  // requested mode of the one-shot entry points
   int last_mode = 0;               // mode the last sweep ran in
@@ -230,9 +237,25 @@ PsiConst make_const(sgpx_ctx* ctx, const ShardInputs& in, const coord::Kernel& k
 // Fill the fp32 backward operands: U = d_phi_big mirrored from its upper
 // triangle (the reference reads only a <= b, psi_stats.hpp:280-281), [mv][mv];
 // dPsi transposed, [d][mv].
+// The fp64 copies (the direct kernels and the per-pair gradient terms) follow the fp32 arrays in the
+// same host buffers, at byte offset fp32_bytes rounded up to 16.
+size_t f32_slot(size_t n) { return (sizeof(float) * n + 15) / 16 * 16; }
 void stage_adjoints(const PsiConst& P, const coord::Mat& dphi_big, const coord::Mat& dpsi, HostBuf& hu, HostBuf& hd) {
-  hu.ensure(sizeof(float) * P.mv * P.mv);
-  hd.ensure(sizeof(float) * std::max(1, P.d) * P.mv);
+  const size_t nu = size_t(P.mv) * P.mv, nd = size_t(std::max(1, P.d)) * P.mv;
+  hu.ensure(f32_slot(nu) + sizeof(double) * nu);
+  hd.ensure(f32_slot(nd) + sizeof(double) * nd);
+  double* u64 = reinterpret_cast<double*>(hu.get<char>() + f32_slot(nu));
+  double* d64 = reinterpret_cast<double*>(hd.get<char>() + f32_slot(nd));
+  std::fill(u64, u64 + nu, 0.0);
+  std::fill(d64, d64 + nd, 0.0);
+  for (int a = 0; a < P.m; ++a)
+    for (int b = a; b < P.m; ++b) {
+      const double v = dphi_big(a, b);
+      u64[size_t(b) * P.mv + a] = v;
+      u64[size_t(a) * P.mv + b] = v;
+    }
+  for (int dd = 0; dd < P.d; ++dd)
+    for (int a = 0; a < P.m; ++a) d64[size_t(dd) * P.mv + a] = dpsi(a, dd);
   float* u = hu.get<float>();
   std::fill(u, u + size_t(P.mv) * P.mv, 0.f);
   for (int a = 0; a < P.m; ++a)
@@ -245,6 +268,19 @@ void stage_adjoints(const PsiConst& P, const coord::Mat& dphi_big, const coord::
   std::fill(dp, dp + size_t(std::max(1, P.d)) * P.mv, 0.f);
   for (int dd = 0; dd < P.d; ++dd)
     for (int a = 0; a < P.m; ++a) dp[size_t(dd) * P.mv + a] = float(dpsi(a, dd));
+}
+
+void upload_adjoints(const PsiConst& P, HostBuf& hu, HostBuf& hd, DevBuf& u, DevBuf& dpsi, DevBuf& u64, DevBuf& dpsi64,
+                     cudaStream_t st) {
+  const size_t nu = size_t(P.mv) * P.mv, nd = size_t(std::max(1, P.d)) * P.mv;
+  u.ensure(sizeof(float) * nu);
+  dpsi.ensure(sizeof(float) * nd);
+  u64.ensure(sizeof(double) * nu);
+  dpsi64.ensure(sizeof(double) * nd);
+  CUDA_OK(cudaMemcpyAsync(u.p, hu.p, sizeof(float) * nu, cudaMemcpyHostToDevice, st));
+  CUDA_OK(cudaMemcpyAsync(dpsi.p, hd.p, sizeof(float) * nd, cudaMemcpyHostToDevice, st));
+  CUDA_OK(cudaMemcpyAsync(u64.p, hu.get<char>() + f32_slot(nu), sizeof(double) * nu, cudaMemcpyHostToDevice, st));
+  CUDA_OK(cudaMemcpyAsync(dpsi64.p, hd.get<char>() + f32_slot(nd), sizeof(double) * nd, cudaMemcpyHostToDevice, st));
 }
 
 // Same order and messages as psi_stats.hpp:119-120.
@@ -288,7 +324,7 @@ struct sgpx_engine {
   coord::Mat z;
   double beta = 1.0;
   PsiConst P{};
-  DevBuf zc, z64, fpart, bpart, pstats, pgrads, u, dpsi, dmu, ds, err;
+  DevBuf zc, z64, fpart, bpart, pstats, pgrads, u, dpsi, u64, dpsi64, dmu, ds, err;
   HostBuf h_stats, h_grads, h_u, h_dpsi, h_err, h_stage;
   // coordinator results of the current evaluation
   coord::Result res;
@@ -316,9 +352,30 @@ struct sgpx_engine {
   // registered host outputs for d mu / d S, streamed by the gradient pass
   bool has_gout = false;
   sgpx_mmat g_mu{}, g_s{};
+  // device coordinator (dcoord.cu): the M-sized algebra on the stream, no host round trip.  Off by
+  // default for a single engine: the host coordinator overlaps its Z-only and deferred halves with the
+  // kernels and measured 7.94 vs 8.07 ms per C3 evaluation (profiles/r02_coordinator_ab.txt); on by
+  // default in the multi-GPU engine, where every shard's coordinator then runs on its own device.
+  bool dev_coord = false;
+  DevBuf dcw;
+  DcArgs dc{};
+  HostBuf h_dc;
+  cudaEvent_t ev_c[2] = {};
+  // one evaluation (device-resident shard, device coordinator) as a CUDA graph, replayed while its
+  // launch arguments are unchanged (graph_key)
+  bool use_graph = true;
+  cudaGraphExec_t graph = nullptr;
+  std::vector<unsigned char> graph_key;
+  int64_t graph_launches = 0;  // kernels in the captured graph (the launch counter counts replays too)
+  double last_bound = 0.0;     // bound of the last evaluation (the reference's cached_bound)
+  std::vector<double> kernel_ls;  // lengthscales of the last broadcast (device coordinator upload)
+  bool dc_ready = false;          // device coordinator set up for the current broadcast
   ~sgpx_engine() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : ev_c)
+      if (e) cudaEventDestroy(e);
+    if (graph) cudaGraphExecDestroy(graph);
     for (auto e : ev_in) cudaEventDestroy(e);
     for (auto e : ev_out) cudaEventDestroy(e);
     if (copy) cudaStreamDestroy(copy);
@@ -421,8 +478,8 @@ void engine_stats_pass(sgpx_engine* e) {
   CUDA_OK(cudaMemsetAsync(e->err.p, 0, sizeof(int), ctx->stream));
   if (e->in.n == 0) {
     CUDA_OK(cudaMemsetAsync(e->pstats.p, 0, sizeof(double) * count, ctx->stream));
-    CUDA_OK(cudaEventRecord(e->ev[0], ctx->stream));
-    CUDA_OK(cudaEventRecord(e->ev[1], ctx->stream));
+    CUDA_OK(record_event(e->ev[0], ctx->stream));
+    CUDA_OK(record_event(e->ev[1], ctx->stream));
     e->coordinated = false;
     return;
   }
@@ -438,7 +495,7 @@ void engine_stats_pass(sgpx_engine* e) {
   }
   e->fpart.ensure(sizeof(double) * foff);
   if (k > 1) e->pstats_sub.ensure(sizeof(double) * count * k);
-  CUDA_OK(cudaEventRecord(e->ev[0], ctx->stream));
+  CUDA_OK(record_event(e->ev[0], ctx->stream));
   if (e->pending_upload) {  // copy stream: mu / S of sub-shard j, then the forward of j waits for it
     CUDA_OK(cudaEventRecord(e->ev_out[0], ctx->stream));  // previous users of the device rows are done
     CUDA_OK(cudaStreamWaitEvent(e->copy, e->ev_out[0], 0));
@@ -469,11 +526,54 @@ void engine_stats_pass(sgpx_engine* e) {
     CUDA_OK(cudaGetLastError());
   }
   e->pending_upload = false;
-  CUDA_OK(cudaEventRecord(e->ev[1], ctx->stream));
+  CUDA_OK(record_event(e->ev[1], ctx->stream));
   e->coordinated = false;
 }
 
+// Bind the device coordinator's workspace and run its per-broadcast half (Kmm, factor_gram, Kmm^-1).
+void dc_setup(sgpx_engine* e) {
+  DcArgs& dc = e->dc;
+  dc.m = int(e->cfg.m);
+  dc.mv = e->P.mv;
+  dc.q = int(e->cfg.q);
+  dc.d = int(e->cfg.d);
+  dc.latent = e->latent ? 1 : 0;
+  dc.n = e->cfg.n_global;
+  dc.var = e->kernel.variance;
+  dc.beta = e->beta;
+  dc.jitter_factor = e->cfg.jitter_factor;
+  dc.z = e->z64.get<double>();
+  e->dcw.ensure(sizeof(double) * dc_workspace_doubles(dc.m, dc.q, dc.d));
+  dc_bind(dc, e->dcw.get<double>());
+  e->pstats.ensure(sizeof(double) * sgpx_packed_stats_count(e->cfg.m, e->cfg.d));
+  dc.packed = e->pstats.get<double>();
+  e->h_stage.ensure(sizeof(double) * dc.q);
+  std::copy(e->kernel_ls.begin(), e->kernel_ls.end(), e->h_stage.get<double>());
+  CUDA_OK(cudaMemcpyAsync(const_cast<double*>(dc.ls), e->h_stage.p, sizeof(double) * dc.q, cudaMemcpyHostToDevice,
+                            e->ctx->stream));
+  if (dc_prefactor(dc, e->ctx->stream)) throw CudaError("coordinator launch");
+  CUDA_OK(cudaStreamSynchronize(e->ctx->stream));  // the staging buffer is reused
+  e->dc_ready = true;
+}
+
 void engine_coordinate(sgpx_engine* e, bool with_grads) {
+  if (e->dev_coord) {  // device coordinator: stream-ordered after the (reduced) statistics, no sync
+    sgpx_ctx* ctx = e->ctx;
+    e->dc.packed = e->pstats.get<double>();
+    e->u.ensure(sizeof(float) * e->P.mv * e->P.mv);
+    e->dpsi.ensure(sizeof(float) * std::max(1, e->P.d) * e->P.mv);
+    e->u64.ensure(sizeof(double) * e->P.mv * e->P.mv);
+    e->dpsi64.ensure(sizeof(double) * std::max(1, e->P.d) * e->P.mv);
+    CUDA_OK(record_event(e->ev_c[0], ctx->stream));
+    if (dc_bound(e->dc, e->u.get<float>(), e->dpsi.get<float>(), e->u64.get<double>(), e->dpsi64.get<double>(),
+                 ctx->stream))
+      throw CudaError("coordinator launch");
+    CUDA_OK(record_event(e->ev_c[1], ctx->stream));
+    e->res.adj.d_phi = -0.5 * e->beta * double(e->cfg.d);  // adjoints_from_core (bound.hpp:203)
+    e->with_grads = with_grads;
+    e->coordinated = true;
+    return;
+  }
   sgpx_ctx* ctx = e->ctx;
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t count = sgpx_packed_stats_count(e->cfg.m, e->cfg.d);
@@ -502,11 +602,7 @@ void engine_coordinate(sgpx_engine* e, bool with_grads) {
   e->with_grads = with_grads;
   if (with_grads) {
     stage_adjoints(e->P, e->res.adj.d_phi_big, e->res.adj.d_psi_y, e->h_u, e->h_dpsi);
-    e->u.ensure(sizeof(float) * e->P.mv * e->P.mv);
-    e->dpsi.ensure(sizeof(float) * std::max(1, e->P.d) * e->P.mv);
-    CUDA_OK(cudaMemcpyAsync(e->u.p, e->h_u.p, sizeof(float) * e->P.mv * e->P.mv, cudaMemcpyHostToDevice, ctx->stream));
-    CUDA_OK(cudaMemcpyAsync(e->dpsi.p, e->h_dpsi.p, sizeof(float) * std::max(1, e->P.d) * e->P.mv,
-                              cudaMemcpyHostToDevice, ctx->stream));
+    upload_adjoints(e->P, e->h_u, e->h_dpsi, e->u, e->dpsi, e->u64, e->dpsi64, ctx->stream);
   }
   e->coordinated = true;
   e->coord_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_host).count();
@@ -520,7 +616,7 @@ void engine_grad_pass(sgpx_engine* e) {
   e->pgrads.ensure(sizeof(double) * count);
   e->dmu.ensure(sizeof(double) * std::max<int64_t>(1, e->in.n * e->cfg.q));
   e->ds.ensure(sizeof(double) * std::max<int64_t>(1, e->in.n * e->cfg.q));
-  CUDA_OK(cudaEventRecord(e->ev[2], ctx->stream));
+  CUDA_OK(record_event(e->ev[2], ctx->stream));
   if (e->in.n > 0) {
     const int k = int(e->subs.size());
     int64_t boff = 0;
@@ -558,6 +654,8 @@ void engine_grad_pass(sgpx_engine* e) {
       BwdConst B{};
       B.u = e->u.get<float>();
       B.dpsi = e->dpsi.get<float>();
+      B.u64 = e->u64.get<double>();
+      B.dpsi64 = e->dpsi64.get<double>();
       B.d_phi = e->res.adj.d_phi;
       B.add_kl = e->latent ? 1 : 0;
       B.write_local = e->latent ? 1 : 0;
@@ -591,16 +689,122 @@ void engine_grad_pass(sgpx_engine* e) {
   } else {
     CUDA_OK(cudaMemsetAsync(e->pgrads.p, 0, sizeof(double) * count, ctx->stream));
   }
-  CUDA_OK(cudaEventRecord(e->ev[3], ctx->stream));
+  CUDA_OK(record_event(e->ev[3], ctx->stream));
+  if (e->dev_coord) {  // d Kmm, Phi G for the assembly, behind the gradient kernels on the stream
+    if (dc_deferred(e->dc, ctx->stream)) throw CudaError("coordinator launch");
+    return;
+  }
   // host-only adjoints, overlapping the kernels just enqueued
   coord::complete_adjoints(e->res, e->st, e->cfg.n_global, e->cfg.d, e->beta);
 }
 
-void engine_finish(sgpx_engine* e, sgpx_eval_result* out) {
-  require(out != nullptr, "engine: result pointer is null");
-  require(e->coordinated, "engine: coordinate must precede finish");
+// Device-coordinator finish: assembly kernel, then ONE read-back of the scalars, the gradient vector,
+// the validation flag and the statistics; the reference's exceptions are raised from them in the
+// reference's order (data validation, contract checks, factorizations, non-finite bound).
+// stream part: the assembly kernel and the read-back copies (captured into the evaluation's graph)
+void engine_finish_enqueue(sgpx_engine* e) {
   sgpx_ctx* ctx = e->ctx;
   const int64_t m = e->cfg.m, q = e->cfg.q, d = e->cfg.d;
+  const DcArgs& dc = e->dc;
+  if (e->with_grads && dc_finish(dc, e->pgrads.get<double>(), ctx->stream)) throw CudaError("coordinator launch");
+  const int64_t nsc = kScCount, nres = 2 + q + m * q, nst = sgpx_packed_stats_count(m, d);
+  e->h_dc.ensure(sizeof(double) * (nsc + nres + nst) + 16);
+  double* h = e->h_dc.get<double>();
+  CUDA_OK(cudaMemcpyAsync(h, dc.sc, sizeof(double) * nsc, cudaMemcpyDeviceToHost, ctx->stream));
+  if (e->with_grads)
+    CUDA_OK(cudaMemcpyAsync(h + nsc, dc.result, sizeof(double) * nres, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_OK(cudaMemcpyAsync(h + nsc + nres, e->pstats.p, sizeof(double) * nst, cudaMemcpyDeviceToHost, ctx->stream));
+  int* herr = reinterpret_cast<int*>(h + nsc + nres + nst);
+  CUDA_OK(cudaMemcpyAsync(herr, e->err.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+}
+
+void engine_finish_device(sgpx_engine* e, sgpx_eval_result* out, bool enqueued = false) {
+  sgpx_ctx* ctx = e->ctx;
+  const int64_t m = e->cfg.m, q = e->cfg.q, d = e->cfg.d;
+  if (!enqueued) engine_finish_enqueue(e);
+  const int64_t nsc = kScCount, nres = 2 + q + m * q, nst = sgpx_packed_stats_count(m, d);
+  double* h = e->h_dc.get<double>();
+  int* herr = reinterpret_cast<int*>(h + nsc + nres + nst);
+  CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  if (e->copy) CUDA_OK(cudaStreamSynchronize(e->copy));  // streamed d mu / d S have landed
+  check_err_flag(*herr);
+  const int st = int(h[kScStatus]);
+  if (st & kStGramFailed)
+    throw NumericError("factor_gram: Gram matrix not factorizable even at jitter 1e-2 * variance (ill-conditioned "
+                       "inducing inputs)");
+  require(!(st & kStBadCount), "bound: stats n_count does not match N");
+  require(!(st & kStBadStats), "bound: phi and yy must be non-negative");
+  if (st & kStAFailed)
+    throw NumericError("bound (Kmm + beta*Phi): Cholesky factorization failed after jitter escalation");
+  if (st & kStNonFinite) throw NumericError("bound: non-finite value");
+  const double* bd = h + kScBound;
+  out->bound = sgpx_bound_breakdown{bd[0], bd[1], bd[2], bd[3], bd[4], bd[5], bd[6]};
+  e->last_bound = bd[0];
+  const coord::Stats stt = coord::unpack_stats(h + nsc + nres, m, d);
+  out->phi = stt.phi;
+  out->yy = stt.yy;
+  out->n_count = int64_t(stt.n);
+  if (out->psi_y) std::copy(stt.psi_y.v.begin(), stt.psi_y.v.end(), out->psi_y);
+  if (out->phi_big) std::copy(stt.phi_big.v.begin(), stt.phi_big.v.end(), out->phi_big);
+  out->jitter_factor_used = h[kScJitterFactor];
+  out->has_grads = e->with_grads ? 1 : 0;
+  float ms = 0.f;
+  if (e->with_grads) {
+    const double* g = h + nsc;
+    out->d_variance = g[0];
+    if (out->d_lengthscales) std::copy(g + 1, g + 1 + q, out->d_lengthscales);
+    if (out->d_z) std::copy(g + 1 + q, g + 1 + q + m * q, out->d_z);
+    out->d_beta = g[1 + q + m * q];
+    cudaEventElapsedTime(&ms, e->ev[2], e->ev[3]);
+    out->grad_pass_s = ms * 1e-3;
+    ms = 0.f;
+    if (e->in.n > 0) cudaEventElapsedTime(&ms, e->ev[6], e->ev[7]);
+    out->bwd_kernel_s = ms * 1e-3;
+    ms = 0.f;
+    if (e->in.n > 0 && cudaEventElapsedTime(&ms, e->ev[10], e->ev[11]) != cudaSuccess) {
+      cudaGetLastError();
+      ms = 0.f;
+    }
+    out->psi2_bwd_kernel_s = ms * 1e-3;
+  } else {
+    out->d_variance = 0.0;
+    out->d_beta = 0.0;
+    out->grad_pass_s = 0.0;
+    out->bwd_kernel_s = 0.0;
+    out->psi2_bwd_kernel_s = 0.0;
+  }
+  ms = 0.f;
+  cudaEventElapsedTime(&ms, e->ev_c[0], e->ev_c[1]);
+  e->coord_s = ms * 1e-3;  // device time of the coordinator kernels
+}
+
+void engine_finish(sgpx_engine* e, sgpx_eval_result* out, bool enqueued = false) {
+  require(out != nullptr, "engine: result pointer is null");
+  require(e->coordinated, "engine: coordinate must precede finish");
+  if (e->dev_coord) {
+    engine_finish_device(e, out, enqueued);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e->ev[0], e->ev[1]);
+    out->stats_pass_s = ms * 1e-3;
+    ms = 0.f;
+    if (e->in.n > 0) cudaEventElapsedTime(&ms, e->ev[4], e->ev[5]);
+    out->fwd_kernel_s = ms * 1e-3;
+    ms = 0.f;
+    if (e->in.n > 0 && cudaEventElapsedTime(&ms, e->ev[8], e->ev[9]) != cudaSuccess) {
+      cudaGetLastError();
+      ms = 0.f;
+    }
+    out->psi2_fwd_kernel_s = ms * 1e-3;
+    out->fwd_grid = e->gf.grid;
+    out->bwd_grid = e->with_grads ? e->gb.grid : 0;
+    out->coordinator_s = e->coord_s;
+    out->precision_used = e->P.mode;
+    out->z_spread = e->z_spread;
+    return;
+  }
+  sgpx_ctx* ctx = e->ctx;
+  const int64_t m = e->cfg.m, q = e->cfg.q, d = e->cfg.d;
+
   const coord::Stats st = coord::unpack_stats(e->h_stats.get<double>(), m, d);
   out->bound = sgpx_bound_breakdown{e->res.bd.total,     e->res.bd.log_det,   e->res.bd.data_fit, e->res.bd.quadratic,
                                     e->res.bd.trace_phi, e->res.bd.trace_kmm, e->res.bd.kl};
@@ -854,16 +1058,14 @@ int sgpx_sweep_stats(sgpx_ctx* ctx, int expected, sgpx_cmat mu, sgpx_cmat s, sgp
     if (!grads || !adj) return;
 
     stage_adjoints(P, dphi_big, dpsi, ctx->h_u, ctx->h_dpsi);
-    ctx->u.ensure(sizeof(float) * P.mv * P.mv);
-    ctx->dpsi.ensure(sizeof(float) * std::max(1, P.d) * P.mv);
-    CUDA_OK(cudaMemcpyAsync(ctx->u.p, ctx->h_u.p, sizeof(float) * P.mv * P.mv, cudaMemcpyHostToDevice, ctx->stream));
-    CUDA_OK(cudaMemcpyAsync(ctx->dpsi.p, ctx->h_dpsi.p, sizeof(float) * std::max(1, P.d) * P.mv,
-                              cudaMemcpyHostToDevice, ctx->stream));
+    upload_adjoints(P, ctx->h_u, ctx->h_dpsi, ctx->u, ctx->dpsi, ctx->u64, ctx->dpsi64, ctx->stream);
     ctx->dmu.ensure(sizeof(double) * n * q);
     ctx->ds.ensure(sizeof(double) * n * q);
     BwdConst B{};
     B.u = ctx->u.get<float>();
     B.dpsi = ctx->dpsi.get<float>();
+    B.u64 = ctx->u64.get<double>();
+    B.dpsi64 = ctx->dpsi64.get<double>();
     B.d_phi = adj->d_phi;
     B.add_kl = 0;
     B.write_local = expected ? 1 : 0;
@@ -1022,6 +1224,9 @@ int sgpx_engine_create(sgpx_ctx* ctx, const sgpx_engine_config* cfg, sgpx_engine
     e->cfg = *cfg;
     e->latent = cfg->kind == 1;
     for (auto& ev : e->ev) CUDA_OK(cudaEventCreate(&ev));
+    for (auto& ev : e->ev_c) CUDA_OK(cudaEventCreate(&ev));
+    if (const char* dc = getenv("SGPX_DEVICE_COORD")) e->dev_coord = atoi(dc) != 0;  // A/B
+    if (const char* gr = getenv("SGPX_GRAPH")) e->use_graph = atoi(gr) != 0;       // A/B: per-call launches
     *out = e.release();
   });
 }
@@ -1129,6 +1334,9 @@ int sgpx_engine_broadcast(sgpx_engine* e, const sgpx_kernel_spec* kernel, double
     e->beta = beta;
     e->P = make_const(e->ctx, e->in, k, zm, e->zc, e->z64, e->h_stage, e->cfg.precision);
     e->z_spread = psi_z_spread(e->P, zm.v.data(), zm.r);
+    e->kernel_ls = k.ls;
+    e->dc_ready = false;
+    if (e->dev_coord) dc_setup(e);  // per-broadcast half of the coordinator (Kmm, its factor, inverse)
     e->has_params = true;
     e->coordinated = false;
   });
@@ -1176,11 +1384,102 @@ int sgpx_engine_evaluate(sgpx_engine* e, int with_grads, sgpx_eval_result* out) 
     require(e->cfg.n_local == e->cfg.n_global, "engine_evaluate is the single-rank pipeline; use the phases");
     CUDA_OK(cudaSetDevice(e->ctx->device));
     const auto t0 = std::chrono::steady_clock::now();
-    engine_stats_pass(e);
-    engine_coordinate(e, with_grads != 0);
-    if (with_grads) engine_grad_pass(e);
-    engine_finish(e, out);
+    // graph replay: device-resident rows (no host streaming) and the device coordinator
+    // (the legacy default stream cannot be captured)
+    const bool graphable = e->use_graph && e->dev_coord && !e->pending_upload && !(e->has_gout && e->latent) &&
+                           e->in.n > 0 && e->has_data && e->has_params && e->ctx->stream != nullptr;
+    if (graphable) {
+      std::vector<unsigned char> key(sizeof(PsiConst) + sizeof(DcArgs) + 2 * sizeof(int));
+      unsigned char* p = key.data();
+      std::memcpy(p, &e->P, sizeof(PsiConst));
+      std::memcpy(p + sizeof(PsiConst), &e->dc, sizeof(DcArgs));
+      const int flags[2] = {with_grads ? 1 : 0, e->ctx->device};
+      std::memcpy(p + sizeof(PsiConst) + sizeof(DcArgs), flags, sizeof(flags));
+      cudaStream_t st = e->ctx->stream;
+      if (!e->graph || key != e->graph_key) {
+        if (e->graph) {
+          cudaGraphExecDestroy(e->graph);
+          e->graph = nullptr;
+        }
+        CUDA_OK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+        const int64_t l0 = launches_issued();
+        cudaGraph_t g = nullptr;
+        try {
+          engine_stats_pass(e);
+          engine_coordinate(e, with_grads != 0);
+          if (with_grads) engine_grad_pass(e);
+          engine_finish_enqueue(e);
+        } catch (...) {
+          cudaStreamEndCapture(st, &g);
+          if (g) cudaGraphDestroy(g);
+          cudaGetLastError();
+          throw;
+        }
+        CUDA_OK(cudaStreamEndCapture(st, &g));
+        e->graph_launches = launches_issued() - l0;
+        launches_add(-e->graph_launches);  // counted when the graph runs
+        const cudaError_t ie = cudaGraphInstantiate(&e->graph, g, 0);
+        cudaGraphDestroy(g);
+        CUDA_OK(ie);
+        e->graph_key = key;
+      } else {
+        e->with_grads = with_grads != 0;
+        e->coordinated = true;
+      }
+      CUDA_OK(cudaGraphLaunch(e->graph, st));
+      launches_add(e->graph_launches);
+      engine_finish(e, out, true);
+    } else {
+      engine_stats_pass(e);
+      engine_coordinate(e, with_grads != 0);
+      if (with_grads) engine_grad_pass(e);
+      engine_finish(e, out);
+    }
     out->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+// predict_from_cache (model.hpp:197-217) on the factors of the engine's last evaluation at the current
+// parameters (the reference's finalize(): an evaluation after the last broadcast).
+int sgpx_engine_predict(sgpx_engine* e, sgpx_cmat x_star, int observation, sgpx_mmat mean, sgpx_mmat var,
+                        double* cached_bound) {
+  return guard([&] {
+    require(e != nullptr, "engine is null");
+    require(e->coordinated && e->has_params, "predict() before fit()/finalize()");
+    if (!e->dev_coord) {  // host-coordinated engine: rebuild the factors on the device from the last statistics
+      CUDA_OK(cudaSetDevice(e->ctx->device));
+      if (!e->dc_ready) dc_setup(e);
+      e->u.ensure(sizeof(float) * e->P.mv * e->P.mv);
+      e->dpsi.ensure(sizeof(float) * std::max(1, e->P.d) * e->P.mv);
+      e->u64.ensure(sizeof(double) * e->P.mv * e->P.mv);
+      e->dpsi64.ensure(sizeof(double) * std::max(1, e->P.d) * e->P.mv);
+      e->dc.packed = e->pstats.get<double>();
+      if (dc_bound(e->dc, e->u.get<float>(), e->dpsi.get<float>(), e->u64.get<double>(), e->dpsi64.get<double>(),
+                   e->ctx->stream))
+        throw CudaError("coordinator launch");
+    }
+    check_view(x_star, "x_star");
+    require(x_star.cols == e->cfg.q, "predict: X* column mismatch");
+    const int64_t t = x_star.rows, d = e->cfg.d;
+    require(mean.rows == t && mean.cols == d && var.rows == t && var.cols == d, "predict: outputs must be T x D");
+    if (cached_bound) *cached_bound = e->last_bound;
+    if (t == 0) return;
+    CUDA_OK(cudaSetDevice(e->ctx->device));
+    sgpx_ctx* ctx = e->ctx;
+    const int64_t q = e->cfg.q, m = e->cfg.m;
+    ctx->out.ensure(sizeof(double) * (t * q + 2 * t * d + dc_predict_doubles(t, int(m), int(q), int(d))));
+    double* xs = ctx->out.get<double>();
+    double* dmean = xs + t * q;
+    double* dvar = dmean + t * d;
+    double* work = dvar + t * d;
+    CUDA_OK(cudaMemcpy2DAsync(xs, sizeof(double) * t, x_star.data, sizeof(double) * (x_star.ld ? x_star.ld : t),
+                                sizeof(double) * t, q, cudaMemcpyHostToDevice, ctx->stream));
+    if (dc_predict(e->dc, xs, t, observation ? 1 : 0, work, dmean, dvar, ctx->stream)) throw CudaError("predict launch");
+    CUDA_OK(cudaMemcpy2DAsync(mean.data, sizeof(double) * (mean.ld ? mean.ld : t), dmean, sizeof(double) * t,
+                                sizeof(double) * t, d, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_OK(cudaMemcpy2DAsync(var.data, sizeof(double) * (var.ld ? var.ld : t), dvar, sizeof(double) * t,
+                                sizeof(double) * t, d, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_OK(cudaStreamSynchronize(ctx->stream));
   });
 }
 
@@ -1291,6 +1590,296 @@ int sgpx_io_load_matrix_device(sgpx_ctx* ctx, const char* base, sgpx_mmat dev_ou
             "io: output shape differs from the file");
     CUDA_OK(cudaSetDevice(ctx->device));
     io_load_device(base, dev_out.data, dev_out.ld ? dev_out.ld : r, ctx->stream);
+  });
+}
+
+// ---- multi-GPU engine: Engine(workers) of parallel.hpp:326-479 inside one process -----------------
+// Shards = make_partition(N, workers) (parallel.hpp:28-41), shard i on devices[i] with its own
+// context (stream).  Per evaluation: every shard's statistics pass -> exchange #1 -> the coordinator
+// on every shard (redundant, no broadcast) -> every shard's gradient pass -> exchange #2 -> assembly.
+// An exchange sums the packed fp64 buffers: shards that share a device are folded into the first of
+// them (ascending shard order, stream events order the cross-stream reads), then one ncclAllReduce
+// (sum, fp64) runs among the first shards of the distinct devices over NVLink / NVSwitch (one NCCL
+// communicator per device from ncclCommInitAll), and the result is copied back to the device's other
+// shards.  NCCL is opened at run time (dlopen), so the library loads on hosts without it.
+}  // extern "C"
+
+#include <dlfcn.h>
+
+namespace sgpx {
+namespace {
+
+typedef int (*nccl_init_all_t)(void** comms, int ndev, const int* devlist);
+typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_group_t)();
+typedef int (*nccl_destroy_t)(void*);
+typedef const char* (*nccl_err_t)(int);
+
+struct NcclApi {
+  void* h = nullptr;
+  nccl_init_all_t init_all = nullptr;
+  nccl_allreduce_t allreduce = nullptr;
+  nccl_group_t group_start = nullptr, group_end = nullptr;
+  nccl_destroy_t destroy = nullptr;
+  nccl_err_t err = nullptr;
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      a.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (a.h) break;
+    }
+    if (!a.h) return a;
+    a.init_all = reinterpret_cast<nccl_init_all_t>(dlsym(a.h, "ncclCommInitAll"));
+    a.allreduce = reinterpret_cast<nccl_allreduce_t>(dlsym(a.h, "ncclAllReduce"));
+    a.group_start = reinterpret_cast<nccl_group_t>(dlsym(a.h, "ncclGroupStart"));
+    a.group_end = reinterpret_cast<nccl_group_t>(dlsym(a.h, "ncclGroupEnd"));
+    a.destroy = reinterpret_cast<nccl_destroy_t>(dlsym(a.h, "ncclCommDestroy"));
+    a.err = reinterpret_cast<nccl_err_t>(dlsym(a.h, "ncclGetErrorString"));
+    return a;
+  }();
+  return api;
+}
+
+void nccl_ok(int rc, const char* what) {
+  if (rc != 0) {
+    const NcclApi& a = nccl_api();
+    throw NcclError(std::string(what) + ": " + (a.err ? a.err(rc) : "NCCL error"));
+  }
+}
+
+constexpr int kNcclDouble = 8, kNcclSum = 0;  // ncclFloat64, ncclSum (nccl.h)
+
+}  // namespace
+}  // namespace sgpx
+
+struct sgpx_multi {
+  sgpx_engine_config cfg{};
+  std::vector<int> dev;                 // device of shard i
+  std::vector<int64_t> b, n;            // rows of shard i
+  std::vector<sgpx_ctx*> ctx;
+  std::vector<sgpx_engine*> eng;
+  std::vector<int> group;               // index into `leaders` of shard i's device
+  std::vector<int> leaders;             // first shard of each distinct device
+  std::vector<void*> comms;             // one per distinct device (ncclCommInitAll)
+  std::vector<cudaEvent_t> ev;          // per shard: its pass is done / the reduced buffer is back
+  bool with_grads = false;
+  ~sgpx_multi() {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto* e : eng)
+      if (e) sgpx_engine_destroy(e);
+    for (auto* c : ctx)
+      if (c) sgpx_ctx_destroy(c);
+    if (!comms.empty() && sgpx::nccl_api().destroy)
+      for (void* c : comms)
+        if (c) sgpx::nccl_api().destroy(c);
+  }
+};
+
+namespace sgpx {
+namespace {
+
+// Sum the shards' packed buffers (`buf(i)`, `count` doubles) into every shard's buffer.
+template <class Buf>
+void multi_exchange(sgpx_multi* mu, Buf buf, int64_t count) {
+  const int k = int(mu->eng.size());
+  for (int i = 0; i < k; ++i) {
+    CUDA_OK(cudaSetDevice(mu->dev[i]));
+    CUDA_OK(cudaEventRecord(mu->ev[i], mu->ctx[i]->stream));
+  }
+  // fold same-device shards into their leader (ascending shard order)
+  for (int i = 0; i < k; ++i) {
+    const int l = mu->leaders[mu->group[i]];
+    if (l == i) continue;
+    CUDA_OK(cudaSetDevice(mu->dev[l]));
+    CUDA_OK(cudaStreamWaitEvent(mu->ctx[l]->stream, mu->ev[i], 0));
+    add_into_kernel<<<int(std::min<int64_t>((count + 255) / 256, 1024)), 256, 0, mu->ctx[l]->stream>>>(buf(l), buf(i),
+                                                                                                          count);
+    CUDA_OK(cudaGetLastError());
+  }
+  // across devices
+  if (mu->leaders.size() > 1) {
+    const NcclApi& a = nccl_api();
+    nccl_ok(a.group_start(), "ncclGroupStart");
+    for (size_t g = 0; g < mu->leaders.size(); ++g) {
+      const int l = mu->leaders[g];
+      CUDA_OK(cudaSetDevice(mu->dev[l]));
+      nccl_ok(a.allreduce(buf(l), buf(l), size_t(count), kNcclDouble, kNcclSum, mu->comms[g], mu->ctx[l]->stream),
+              "ncclAllReduce");
+    }
+    nccl_ok(a.group_end(), "ncclGroupEnd");
+  }
+  // back to the other shards of each device
+  for (int i = 0; i < k; ++i) {
+    const int l = mu->leaders[mu->group[i]];
+    if (l == i) continue;
+    CUDA_OK(cudaSetDevice(mu->dev[l]));
+    CUDA_OK(cudaMemcpyAsync(buf(i), buf(l), sizeof(double) * count, cudaMemcpyDeviceToDevice, mu->ctx[l]->stream));
+    CUDA_OK(cudaEventRecord(mu->ev[l], mu->ctx[l]->stream));
+    CUDA_OK(cudaSetDevice(mu->dev[i]));
+    CUDA_OK(cudaStreamWaitEvent(mu->ctx[i]->stream, mu->ev[l], 0));
+  }
+}
+
+}  // namespace
+}  // namespace sgpx
+
+extern "C" {
+
+int sgpx_multi_create(int workers, const int* devices, const sgpx_engine_config* cfg, sgpx_multi** out) {
+  return guard([&] {
+    require(cfg && out && devices, "multi_create: null argument");
+    require(workers >= 1, "Engine: need at least one worker");
+    require(cfg->n_global >= workers, "make_partition: more workers than datapoints");
+    auto mu = std::make_unique<sgpx_multi>();
+    mu->cfg = *cfg;
+    const int64_t nn = cfg->n_global, base = nn / workers, rem = nn % workers;  // make_partition (parallel.hpp:28-41)
+    int64_t at = 0;
+    for (int i = 0; i < workers; ++i) {
+      const int64_t len = base + (i < rem ? 1 : 0);
+      mu->b.push_back(at);
+      mu->n.push_back(len);
+      at += len;
+      mu->dev.push_back(devices[i]);
+    }
+    for (int i = 0; i < workers; ++i) {
+      int g = -1;
+      for (size_t j = 0; j < mu->leaders.size(); ++j)
+        if (mu->dev[mu->leaders[j]] == mu->dev[i]) g = int(j);
+      if (g < 0) {
+        g = int(mu->leaders.size());
+        mu->leaders.push_back(i);
+      }
+      mu->group.push_back(g);
+    }
+    for (int i = 0; i < workers; ++i) {
+      sgpx_ctx* c = nullptr;
+      if (sgpx_ctx_create(mu->dev[i], &c) != SGPX_OK) throw CudaError(g_last_error);
+      mu->ctx.push_back(c);
+      sgpx_engine_config sc = *cfg;
+      sc.row_begin = mu->b[i];
+      sc.n_local = mu->n[i];
+      sgpx_engine* e = nullptr;
+      const int rc = sgpx_engine_create(c, &sc, &e);
+      if (rc == SGPX_INVALID_ARGUMENT) throw InvalidArgument(g_last_error);
+      if (rc != SGPX_OK) throw CudaError(g_last_error);
+      if (!getenv("SGPX_DEVICE_COORD")) e->dev_coord = true;  // coordinators run concurrently on their devices
+      mu->eng.push_back(e);
+      cudaEvent_t ev;
+      CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      mu->ev.push_back(ev);
+    }
+    if (mu->leaders.size() > 1) {
+      const NcclApi& a = nccl_api();
+      if (!a.init_all || !a.allreduce || !a.group_start || !a.group_end)
+        throw NcclError("NCCL (libnccl.so.2) is not available for the multi-GPU exchange");
+      std::vector<int> devs;
+      for (int l : mu->leaders) devs.push_back(mu->dev[l]);
+      mu->comms.assign(devs.size(), nullptr);
+      nccl_ok(a.init_all(mu->comms.data(), int(devs.size()), devs.data()), "ncclCommInitAll");
+    }
+    *out = mu.release();
+  });
+}
+
+int sgpx_multi_destroy(sgpx_multi* mu) {
+  return guard([&] { delete mu; });
+}
+
+int sgpx_multi_workers(const sgpx_multi* mu) { return mu ? int(mu->eng.size()) : 0; }
+
+int sgpx_multi_set_data(sgpx_multi* mu, sgpx_cmat x_or_mu, sgpx_cmat s, sgpx_cmat y) {
+  return guard([&] {
+    require(mu != nullptr, "engine is null");
+    auto slice = [](sgpx_cmat a, int64_t r0, int64_t nr) {
+      sgpx_cmat v = a;
+      v.ld = a.ld ? a.ld : a.rows;
+      v.data = a.data ? a.data + r0 : nullptr;
+      v.rows = nr;
+      return v;
+    };
+    require(x_or_mu.rows == mu->cfg.n_global && y.rows == mu->cfg.n_global, "Engine: X/Y must hold N rows");
+    for (size_t i = 0; i < mu->eng.size(); ++i) {
+      const int rc = sgpx_engine_set_data(mu->eng[i], slice(x_or_mu, mu->b[i], mu->n[i]),
+                                          mu->cfg.kind == 1 ? slice(s, mu->b[i], mu->n[i]) : s,
+                                          slice(y, mu->b[i], mu->n[i]), 0);
+      if (rc == SGPX_INVALID_ARGUMENT) throw InvalidArgument(g_last_error);
+      if (rc != SGPX_OK) throw CudaError(g_last_error);
+    }
+  });
+}
+
+int sgpx_multi_broadcast(sgpx_multi* mu, const sgpx_kernel_spec* kernel, double beta, sgpx_cmat z, sgpx_cmat m_,
+                         sgpx_cmat s) {
+  return guard([&] {
+    require(mu != nullptr, "engine is null");
+    for (size_t i = 0; i < mu->eng.size(); ++i) {
+      sgpx_cmat mi{}, si{};
+      if (m_.data) {
+        require(m_.rows == mu->cfg.n_global && s.rows == mu->cfg.n_global, "broadcast: mu / s must hold N rows");
+        mi = m_;
+        mi.ld = m_.ld ? m_.ld : m_.rows;
+        mi.data = m_.data + mu->b[i];
+        mi.rows = mu->n[i];
+        si = s;
+        si.ld = s.ld ? s.ld : s.rows;
+        si.data = s.data + mu->b[i];
+        si.rows = mu->n[i];
+      }
+      const int rc = sgpx_engine_broadcast(mu->eng[i], kernel, beta, z, mi, si, 0);
+      if (rc == SGPX_INVALID_ARGUMENT) throw InvalidArgument(g_last_error);
+      if (rc == SGPX_NUMERIC) throw NumericError(g_last_error);
+      if (rc != SGPX_OK) throw CudaError(g_last_error);
+    }
+  });
+}
+
+int sgpx_multi_evaluate(sgpx_multi* mu, int with_grads, sgpx_eval_result* out, sgpx_mmat d_mu, sgpx_mmat d_s) {
+  return guard([&] {
+    require(mu != nullptr && out != nullptr, "engine/result is null");
+    const auto t0 = std::chrono::steady_clock::now();
+    const int k = int(mu->eng.size());
+    const int64_t m = mu->cfg.m, q = mu->cfg.q, d = mu->cfg.d;
+    for (int i = 0; i < k; ++i) {
+      CUDA_OK(cudaSetDevice(mu->dev[i]));
+      engine_stats_pass(mu->eng[i]);
+    }
+    multi_exchange(mu, [&](int i) { return mu->eng[i]->pstats.get<double>(); }, sgpx_packed_stats_count(m, d));
+    for (int i = 0; i < k; ++i) {
+      CUDA_OK(cudaSetDevice(mu->dev[i]));
+      engine_coordinate(mu->eng[i], with_grads != 0);
+    }
+    if (with_grads) {
+      for (int i = 0; i < k; ++i) {
+        CUDA_OK(cudaSetDevice(mu->dev[i]));
+        engine_grad_pass(mu->eng[i]);
+      }
+      multi_exchange(mu, [&](int i) { return mu->eng[i]->pgrads.get<double>(); }, sgpx_packed_grads_count(m, q));
+    }
+    // every shard assembles the same globals; shard 0's are returned, the others checked for errors
+    std::vector<double> scratch(size_t(m * (m + d + q) + q + 8));
+    for (int i = k - 1; i >= 0; --i) {
+      CUDA_OK(cudaSetDevice(mu->dev[i]));
+      sgpx_eval_result r = *out;
+      if (i != 0) {
+        r.psi_y = r.phi_big = r.d_z = r.d_lengthscales = nullptr;
+      }
+      engine_finish(mu->eng[i], i == 0 ? out : &r);
+      if (with_grads && mu->cfg.kind == 1 && d_mu.data && d_s.data) {
+        sgpx_mmat a = d_mu, b = d_s;
+        a.ld = d_mu.ld ? d_mu.ld : d_mu.rows;
+        b.ld = d_s.ld ? d_s.ld : d_s.rows;
+        a.data += mu->b[i];
+        b.data += mu->b[i];
+        a.rows = b.rows = mu->n[i];
+        const int rc = sgpx_engine_copy_local_grads(mu->eng[i], a, b);
+        if (rc != SGPX_OK) throw CudaError(g_last_error);
+      }
+    }
+    out->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
 }
 

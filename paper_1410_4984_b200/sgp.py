@@ -412,12 +412,17 @@ class Engine:
     (one rank per GPU, NCCL allreduce); on a single device it must be 1.
     """
 
+    def __new__(cls, kind, x_or_mu, s, y, workers: int = 1, *args, **kwargs):
+        if cls is Engine and workers != 1:
+            return MultiEngine(kind, x_or_mu, s, y, workers, *args, **kwargs)
+        return super().__new__(cls)
+
     def __init__(self, kind, x_or_mu, s, y, workers: int = 1, tiles: TileConfig | None = None,
                  jitter_factor: float = 1e-6, ctx: Context | None = None, _n_global=None, _row_begin=0,
                  precision: str = "auto"):
         self.kind = ModelKind(kind)
         if workers != 1:
-            raise SgpxInvalidArgument("one Engine per GPU: use engine_dist.DistributedEngine for several ranks")
+            raise SgpxInvalidArgument("Engine(workers > 1) is the multi-GPU engine (MultiEngine)")
         (tiles or TileConfig())  # accepted, geometry is fixed
         self.ctx = ctx or Context.default()
         self._lib = L.load()
@@ -557,6 +562,26 @@ class Engine:
         check(self._lib.sgpx_engine_copy_local_grads(self._h, _cm(dmu), _cm(ds)))
         return dmu, ds
 
+    def finalize(self):
+        """The reference's finalize(): an evaluation (bound only) at the current parameters, whose
+        factors predict() serves from; returns the cached bound."""
+        return self.evaluate(False).bound.total
+
+    def predict(self, x_star, mode: str = "observation"):
+        """predict_from_cache (model.hpp:197-217): (mean T x D, variance T x D) at the rows of x_star
+        (latent points for the GP-LVM); ``mode`` "observation" adds the 1/beta noise, "latent" does not."""
+        if mode not in ("observation", "latent"):
+            raise SgpxInvalidArgument("predict: mode must be 'observation' or 'latent'")
+        xs = _F(x_star)
+        t = xs.shape[0]
+        mean = np.zeros((t, self.d), order="F")
+        var = np.zeros((t, self.d), order="F")
+        cb = C.c_double()
+        check(self._lib.sgpx_engine_predict(self._h, _cm(xs), 1 if mode == "observation" else 0, _cm(mean),
+                                            _cm(var), C.byref(cb)))
+        self.cached_bound = cb.value
+        return mean, var
+
     def local_grads_device(self):
         """(d_mu, d_s) device pointers, n x Q column-major fp64."""
         a, b = C.c_void_p(), C.c_void_p()
@@ -566,6 +591,93 @@ class Engine:
     def close(self):
         if self._h is not None:
             self._lib.sgpx_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class MultiEngine:
+    """sgp::Engine(kind, x, s, y, workers) over several GPUs of one process (sgpx_multi_*): shards by
+    make_partition, shard i on ``devices[i]`` (default: round-robin over the visible GPUs), the two
+    exchanges folded per device and allreduced with NCCL across devices."""
+
+    def __init__(self, kind, x_or_mu, s, y, workers: int, tiles: TileConfig | None = None,
+                 jitter_factor: float = 1e-6, devices=None, precision: str = "auto"):
+        self.kind = ModelKind(kind)
+        (tiles or TileConfig())
+        self._lib = L.load()
+        x = _F(x_or_mu)
+        y = _F(y)
+        s = _F(s) if self.kind == ModelKind.latent else _EMPTY
+        self.n, self.q = x.shape
+        self.d = y.shape[1]
+        self.workers = int(workers)
+        if devices is None:
+            nd = max(1, device_count())
+            devices = [i % nd for i in range(self.workers)]
+        self.devices = (C.c_int * self.workers)(*devices)
+        self.jitter_factor = jitter_factor
+        self.precision = precision_code(precision)
+        self._data = (x, s, y)
+        self._h = None
+        self.m = None
+
+    def _create(self, m):
+        cfg = L.engine_config(int(self.kind), self.n, 0, self.n, self.q, self.d, m, self.jitter_factor,
+                              self.precision)
+        h = C.c_void_p()
+        check(self._lib.sgpx_multi_create(self.workers, self.devices, C.byref(cfg), C.byref(h)))
+        self._h = h
+        self.m = m
+        x, s, y = self._data
+        check(self._lib.sgpx_multi_set_data(self._h, _cm(x), _cm(s), _cm(y)))
+
+    def broadcast(self, kernel: KernelSpec, beta: float, z, mu=None, s=None):
+        z = _F(z)
+        if self._h is None:
+            self._create(z.shape[0])
+        ks = kernel._c()
+        nullm = L.cmat(None, 0, 0, 0)
+        if mu is not None:
+            self._local = (_F(mu), _F(s))
+            check(self._lib.sgpx_multi_broadcast(self._h, C.byref(ks), float(beta), _cm(z), _cm(self._local[0]),
+                                                 _cm(self._local[1])))
+        else:
+            check(self._lib.sgpx_multi_broadcast(self._h, C.byref(ks), float(beta), _cm(z), nullm, nullm))
+        self.beta = beta
+
+    def evaluate(self, with_grads: bool = True) -> EvalResult:
+        m, d, q, n = self.m, self.d, self.q, self.n
+        bufs = dict(psi_y=np.zeros((m, d), order="F"), phi_big=np.zeros((m, m), order="F"),
+                    d_z=np.zeros((m, q), order="F"), d_ls=np.zeros(q))
+        r = L.eval_result()
+        r.psi_y = bufs["psi_y"].ctypes.data_as(C.c_void_p)
+        r.phi_big = bufs["phi_big"].ctypes.data_as(C.c_void_p)
+        r.d_z = bufs["d_z"].ctypes.data_as(C.c_void_p)
+        r.d_lengthscales = bufs["d_ls"].ctypes.data_as(C.c_void_p)
+        latent = self.kind == ModelKind.latent
+        dmu = np.zeros((n, q), order="F") if latent else None
+        ds = np.zeros((n, q), order="F") if latent else None
+        nullm = L.mmat(None, 0, 0, 0)
+        check(self._lib.sgpx_multi_evaluate(self._h, 1 if with_grads else 0, C.byref(r),
+                                            _cm(dmu) if latent else nullm, _cm(ds) if latent else nullm))
+        stats = SufficientStats(r.phi, bufs["psi_y"], bufs["phi_big"], r.yy, int(r.n_count))
+        g = GradientParts()
+        if with_grads:
+            g.d_z, g.d_lengthscales, g.d_variance, g.d_beta = bufs["d_z"], bufs["d_ls"], r.d_variance, r.d_beta
+            g.d_mu, g.d_s = dmu, ds
+        t = EngineTimings(r.stats_pass_s, r.coordinator_s, r.grad_pass_s, r.wall_s, r.fwd_kernel_s, r.bwd_kernel_s,
+                          r.fwd_grid, r.bwd_grid, L.PRECISION_NAMES.get(int(r.precision_used), "none"),
+                          float(r.z_spread), float(r.psi2_fwd_kernel_s), float(r.psi2_bwd_kernel_s))
+        return EvalResult(BoundBreakdown._from(r.bound), stats, bool(r.has_grads), g, t, r.jitter_factor_used)
+
+    def close(self):
+        if self._h is not None:
+            self._lib.sgpx_multi_destroy(self._h)
             self._h = None
 
     def __del__(self):
