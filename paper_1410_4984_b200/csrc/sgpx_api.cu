@@ -808,6 +808,7 @@ void engine_finish(sgpx_engine* e, sgpx_eval_result* out, bool enqueued = false)
   const coord::Stats st = coord::unpack_stats(e->h_stats.get<double>(), m, d);
   out->bound = sgpx_bound_breakdown{e->res.bd.total,     e->res.bd.log_det,   e->res.bd.data_fit, e->res.bd.quadratic,
                                     e->res.bd.trace_phi, e->res.bd.trace_kmm, e->res.bd.kl};
+  e->last_bound = e->res.bd.total;
   out->phi = st.phi;
   out->yy = st.yy;
   out->n_count = int64_t(st.n);

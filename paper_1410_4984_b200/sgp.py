@@ -572,6 +572,8 @@ class Engine:
         (latent points for the GP-LVM); ``mode`` "observation" adds the 1/beta noise, "latent" does not."""
         if mode not in ("observation", "latent"):
             raise SgpxInvalidArgument("predict: mode must be 'observation' or 'latent'")
+        if self._h is None:
+            raise SgpxInvalidArgument("predict() before fit()/finalize()")
         xs = _F(x_star)
         t = xs.shape[0]
         mean = np.zeros((t, self.d), order="F")
