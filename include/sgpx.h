@@ -18,6 +18,8 @@
  *                           kern_grads(Z,Z,dKmm) (kernels.hpp:124-164) + jitter term
  *   sgpx_multi_*            sgp::Engine(workers) over several GPUs of one process: shards per
  *                           make_partition (parallel.hpp:28-41), NCCL allreduce exchanges
+ *   sgpx_fit_*              FitSession + LbfgsState (model.hpp:100-168, optimizer.hpp:20-458) with
+ *                           the parameter vector and the L-BFGS history resident on the device
  *   sgpx_rng_*              sgp::Rng::normal_matrix (common.hpp:45-97) generated on the device,
  *                           the init_gplvm Z-row choice (model.hpp:420-429)
  *   sgpx_io_*               write_matrix_bin / read_matrix_bin (io.hpp:114-153) + a streamed
@@ -278,6 +280,46 @@ int sgpx_multi_set_data(sgpx_multi* mu, sgpx_cmat x_or_mu, sgpx_cmat s, sgpx_cma
 int sgpx_multi_broadcast(sgpx_multi* mu, const sgpx_kernel_spec* kernel, double beta, sgpx_cmat z, sgpx_cmat mu_,
                          sgpx_cmat s);
 int sgpx_multi_evaluate(sgpx_multi* mu, int with_grads, sgpx_eval_result* out, sgpx_mmat d_mu, sgpx_mmat d_s);
+
+/* ---- the optimisation loop, resident on the device ----------------------------------------------
+ * FitSession (model.hpp:100-168) with LbfgsState (optimizer.hpp:205-458) and the packed, log-transformed
+ * parameter vector (optimizer.hpp:20-144) kept in device memory: each evaluation broadcasts the
+ * device-resident mu / S to the engine and reads its d mu / d S in place; only the M-sized segment and
+ * the line search's scalars cross to the host.  The objective is -bound (DistributedObjective,
+ * model.hpp:61-92). */
+typedef struct {
+  int memory;           /* history pairs (10) */
+  double c1, c2;        /* Wolfe constants (1e-4, 0.9) */
+  double g_tol, f_tol;  /* gradient 2-norm stop (1e-5), relative value-change stop (1e-9) */
+  int max_iters;        /* 500 */
+  int max_evals;        /* 0 = unlimited */
+  int max_line_search;  /* 40 */
+} sgpx_lbfgs_options;   /* LbfgsOptions, optimizer.hpp:154-163 */
+
+#define SGPX_FIT_RUNNING (-1)
+#define SGPX_FIT_GRADIENT_CONVERGED 0
+#define SGPX_FIT_VALUE_CONVERGED 1
+#define SGPX_FIT_MAX_ITERATIONS 2
+#define SGPX_FIT_MAX_EVALUATIONS 3
+#define SGPX_FIT_LINE_SEARCH_FAILED 4
+
+typedef struct sgpx_fit sgpx_fit;
+void sgpx_lbfgs_default_options(sgpx_lbfgs_options* opts);
+/* Pack the starting parameters (mu / s: host n_local x Q, NULL data for regression) and evaluate once
+ * (LbfgsState::initialize).  The engine must have its data set; it stays owned by the caller. */
+int sgpx_fit_create(sgpx_engine* eng, int64_t n_local, const sgpx_kernel_spec* kernel, double beta, sgpx_cmat z,
+                    sgpx_cmat mu, sgpx_cmat s, const sgpx_lbfgs_options* opts, sgpx_fit** out);
+/* One outer L-BFGS iteration (LbfgsState::step); *advanced = 0 once converged / stopped. */
+int sgpx_fit_step(sgpx_fit* fit, int* advanced);
+/* value = -bound at the current iterate, |grad|, iterations, evaluations, status (SGPX_FIT_*). */
+int sgpx_fit_state(const sgpx_fit* fit, double* value, double* grad_norm, int* iterations, int* total_evals,
+                   int* last_step_evals, int* status);
+const char* sgpx_fit_message(const sgpx_fit* fit);
+const char* sgpx_fit_last_error(void);
+/* current_params (unpack): host outputs, any may be NULL (z: M x Q, mu / s: n_local x Q). */
+int sgpx_fit_params(const sgpx_fit* fit, double* variance, double* lengthscales, double* beta, sgpx_mmat z,
+                    sgpx_mmat mu, sgpx_mmat s);
+int sgpx_fit_destroy(sgpx_fit* fit);
 
 /* ---- seeded inputs and binary matrices ------------------------------------ */
 /* Rng(seed).normal_matrix(rows, cols) (common.hpp:86-91), bit-for-bit the reference's splitmix64 +

@@ -314,6 +314,33 @@ def predict(latent, x_or_mu, s, y, z, variance, lengthscales, beta, x_star, obse
     return mean, var, bound.value
 
 
+def fit(latent, x_or_mu, s, y, z, variance, lengthscales, beta, iters, workers=1):
+    """FitSession + LbfgsState (model.hpp:100-168, optimizer.hpp:20-458) on the oracle engine: `iters`
+    sync_steps.  Returns dict(values=-bound per accepted iterate, grad_norms, status, evals, params)."""
+    x = F(x_or_mu)
+    y = F(y)
+    z = F(z)
+    n, q = x.shape
+    d = y.shape[1]
+    m = z.shape[0]
+    s = F(s) if latent else None
+    ls = F(np.broadcast_to(np.asarray(lengthscales, dtype=np.float64), (q,)))
+    values = np.full(iters + 1, np.nan)
+    gnorms = np.full(iters + 1, np.nan)
+    status, evals = C.c_int(), C.c_int()
+    var_o, beta_o = C.c_double(), C.c_double()
+    ls_o = np.zeros(q)
+    z_o = np.zeros((m, q), order="F")
+    mu_o = np.zeros((n, q), order="F") if latent else None
+    s_o = np.zeros((n, q), order="F") if latent else None
+    _check(lib().oracle_fit(C.c_int(1 if latent else 0), _i64(n), _i64(q), _i64(d), _i64(m), _p(x), _p(s), _p(y),
+                            _p(z), _d(variance), _p(ls), _d(beta), C.c_int(workers), C.c_int(iters), _p(values),
+                            _p(gnorms), C.byref(status), C.byref(evals), C.byref(var_o), _p(ls_o), C.byref(beta_o),
+                            _p(z_o), _p(mu_o), _p(s_o)))
+    return dict(values=values, grad_norms=gnorms, status=status.value, evals=evals.value,
+                params=dict(variance=var_o.value, lengthscales=ls_o, beta=beta_o.value, z=z_o, mu=mu_o, s=s_o))
+
+
 def rng_normal_matrix(seed, rows, cols):
     """Rng(seed).normal_matrix(rows, cols) (common.hpp:86-91), column-major result."""
     out = np.zeros((rows, cols), order="F")

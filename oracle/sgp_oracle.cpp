@@ -41,6 +41,8 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <deque>
+#include <functional>
 #include <vector>
 
 namespace oracle {
@@ -976,6 +978,241 @@ static EvalOut engine_evaluate(bool latent, const View& x_or_mu, const View& s, 
 // C ABI for the test / baseline harness (ctypes).  Errors: 0 ok, 1 invalid
 // argument (std::invalid_argument), 2 numeric (NumericError), 3 other.
 // ---------------------------------------------------------------------------
+
+// ---------------------------------------------------------------------------
+// The fitting loop: pack / unpack / pack_gradient (optimizer.hpp:20-144), LbfgsState
+// (optimizer.hpp:205-458) and FitSession (model.hpp:100-168) over the oracle engine.
+// ---------------------------------------------------------------------------
+namespace fitref {
+using Vec = std::vector<double>;
+static double vdot(const Vec& a, const Vec& b) {
+  double s = 0.0;
+  for (size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
+  return s;
+}
+static double vnorm(const Vec& a) { return std::sqrt(vdot(a, a)); }
+
+struct Layout {
+  Index q, m, n;
+  bool latent;
+  Index size() const { return 2 + q + m * q + (latent ? 2 * n * q : 0); }
+  Index z_off() const { return 2 + q; }
+  Index mu_off() const { return z_off() + m * q; }
+  Index s_off() const { return mu_off() + n * q; }
+};
+
+struct Params {
+  double var, beta;
+  Vec ls;
+  Mat z, mu, s;
+};
+
+static Vec pack(const Params& p, const Layout& L) {
+  Vec v(size_t(L.size()));
+  v[0] = std::log(p.beta);
+  v[1] = std::log(p.var);
+  for (Index j = 0; j < L.q; ++j) v[size_t(2 + j)] = std::log(p.ls[size_t(j)]);
+  for (Index i = 0; i < L.m; ++i)
+    for (Index j = 0; j < L.q; ++j) v[size_t(L.z_off() + i * L.q + j)] = p.z(i, j);
+  if (L.latent)
+    for (Index i = 0; i < L.n; ++i)
+      for (Index j = 0; j < L.q; ++j) {
+        v[size_t(L.mu_off() + i * L.q + j)] = p.mu(i, j);
+        v[size_t(L.s_off() + i * L.q + j)] = std::log(p.s(i, j));
+      }
+  return v;
+}
+
+static Params unpack(const Vec& v, const Layout& L) {
+  Params p;
+  p.beta = std::exp(v[0]);
+  p.var = std::exp(v[1]);
+  p.ls.resize(size_t(L.q));
+  for (Index j = 0; j < L.q; ++j) p.ls[size_t(j)] = std::exp(v[size_t(2 + j)]);
+  p.z = Mat(L.m, L.q);
+  for (Index i = 0; i < L.m; ++i)
+    for (Index j = 0; j < L.q; ++j) p.z(i, j) = v[size_t(L.z_off() + i * L.q + j)];
+  if (L.latent) {
+    p.mu = Mat(L.n, L.q);
+    p.s = Mat(L.n, L.q);
+    for (Index i = 0; i < L.n; ++i)
+      for (Index j = 0; j < L.q; ++j) {
+        p.mu(i, j) = v[size_t(L.mu_off() + i * L.q + j)];
+        p.s(i, j) = std::exp(v[size_t(L.s_off() + i * L.q + j)]);
+      }
+  }
+  return p;
+}
+
+struct Lbfgs {
+  int memory = 10;
+  double c1 = 1e-4, c2 = 0.9, g_tol = 1e-5, f_tol = 1e-9;
+  int max_iters = 500, max_evals = 0, max_ls = 40;
+  Vec x, g;
+  double value = 0.0;
+  struct Pair {
+    Vec s, y;
+    double rho;
+  };
+  std::deque<Pair> hist;
+  int iter = 0, evals = 0;
+  bool done = false;
+  int status = -1;
+  std::function<double(const Vec&, Vec&)> f;
+
+  double eval(const Vec& xx, Vec& gg) {
+    ++evals;
+    return f(xx, gg);
+  }
+  bool zoom(const Vec& dir, double f0, double slope0, double alo, double flo, double dlo, double ahi, double fhi,
+            double dhi, double& aout, Vec& xout, double& fout, Vec& gout) {
+    Vec gg(x.size());
+    for (int it = 0; it < max_ls; ++it) {
+      if (max_evals > 0 && evals >= max_evals) return false;
+      double a = 0.0;
+      {
+        const double d1 = dlo + dhi - 3.0 * (flo - fhi) / (alo - ahi);
+        const double disc = d1 * d1 - dlo * dhi;
+        if (disc > 0.0) {
+          const double d2 = std::sqrt(disc) * (ahi > alo ? 1.0 : -1.0);
+          a = ahi - (ahi - alo) * (dhi + d2 - d1) / (dhi - dlo + 2.0 * d2);
+        }
+        const double lo = std::min(alo, ahi), hi = std::max(alo, ahi), w = hi - lo;
+        if (!(a > lo + 0.05 * w && a < hi - 0.05 * w)) a = 0.5 * (alo + ahi);
+      }
+      for (size_t i = 0; i < x.size(); ++i) xout[i] = x[i] + a * dir[i];
+      const double fa = eval(xout, gg);
+      const double dphi = vdot(gg, dir);
+      if (!std::isfinite(fa) || fa > f0 + c1 * a * slope0 || fa >= flo) {
+        ahi = a;
+        fhi = fa;
+        dhi = dphi;
+      } else {
+        if (std::abs(dphi) <= -c2 * slope0) {
+          aout = a;
+          fout = fa;
+          gout = gg;
+          return true;
+        }
+        if (dphi * (ahi - alo) >= 0.0) {
+          ahi = alo;
+          fhi = flo;
+          dhi = dlo;
+        }
+        alo = a;
+        flo = fa;
+        dlo = dphi;
+      }
+      if (std::abs(ahi - alo) < 1e-16 * std::max(1.0, std::abs(alo))) break;
+    }
+    if (flo < f0 && alo > 0.0) {
+      for (size_t i = 0; i < x.size(); ++i) xout[i] = x[i] + alo * dir[i];
+      fout = eval(xout, gout);
+      aout = alo;
+      return std::isfinite(fout) && fout < f0;
+    }
+    return false;
+  }
+  bool line_search(const Vec& dir, double slope0, double a0, double& aout, Vec& xout, double& fout, Vec& gout) {
+    const double f0 = value;
+    double ap = 0.0, fp = f0, dp = slope0, a = a0;
+    Vec gg(x.size());
+    for (int it = 0; it < max_ls; ++it) {
+      if (max_evals > 0 && evals >= max_evals) return false;
+      for (size_t i = 0; i < x.size(); ++i) xout[i] = x[i] + a * dir[i];
+      const double fa = eval(xout, gg);
+      const double dphi = vdot(gg, dir);
+      if (!std::isfinite(fa)) {
+        a = 0.5 * (ap + a);
+        continue;
+      }
+      if (fa > f0 + c1 * a * slope0 || (it > 0 && fa >= fp))
+        return zoom(dir, f0, slope0, ap, fp, dp, a, fa, dphi, aout, xout, fout, gout);
+      if (std::abs(dphi) <= -c2 * slope0) {
+        aout = a;
+        fout = fa;
+        gout = gg;
+        return true;
+      }
+      if (dphi >= 0.0) return zoom(dir, f0, slope0, a, fa, dphi, ap, fp, dp, aout, xout, fout, gout);
+      ap = a;
+      fp = fa;
+      dp = dphi;
+      a = std::min(2.0 * a, 1e10);
+      if (a >= 1e10) return false;
+    }
+    return false;
+  }
+  bool step() {
+    if (done) return false;
+    const double gn = vnorm(g);
+    if (gn <= g_tol) {
+      done = true;
+      status = 0;
+      return false;
+    }
+    if (max_iters >= 0 && iter >= max_iters) {
+      done = true;
+      status = 2;
+      return false;
+    }
+    Vec dir(g.size());
+    for (size_t i = 0; i < g.size(); ++i) dir[i] = -g[i];
+    if (!hist.empty()) {
+      std::vector<double> al(hist.size());
+      for (Index i = Index(hist.size()) - 1; i >= 0; --i) {
+        al[size_t(i)] = hist[size_t(i)].rho * vdot(hist[size_t(i)].s, dir);
+        for (size_t k = 0; k < dir.size(); ++k) dir[k] -= al[size_t(i)] * hist[size_t(i)].y[k];
+      }
+      const auto& last = hist.back();
+      const double sc = vdot(last.s, last.y) / vdot(last.y, last.y);
+      for (double& v : dir) v *= sc;
+      for (size_t i = 0; i < hist.size(); ++i) {
+        const double b = hist[i].rho * vdot(hist[i].y, dir);
+        for (size_t k = 0; k < dir.size(); ++k) dir[k] += (al[i] - b) * hist[i].s[k];
+      }
+    }
+    double slope = vdot(g, dir);
+    if (slope >= 0.0) {
+      hist.clear();
+      for (size_t i = 0; i < g.size(); ++i) dir[i] = -g[i];
+      slope = vdot(g, dir);
+    }
+    const double a0 = hist.empty() ? std::min(1.0, 1.0 / std::max(1.0, gn)) : 1.0;
+    Vec xn(x.size()), gnv(x.size());
+    double fnew = 0.0, a = 0.0;
+    if (!line_search(dir, slope, a0, a, xn, fnew, gnv)) {
+      done = true;
+      status = (max_evals > 0 && evals >= max_evals) ? 3 : 4;
+      return false;
+    }
+    Vec sv(x.size()), yv(x.size());
+    for (size_t i = 0; i < x.size(); ++i) {
+      sv[i] = xn[i] - x[i];
+      yv[i] = gnv[i] - g[i];
+    }
+    const double sy = vdot(sv, yv);
+    if (sy > 1e-16 * vnorm(sv) * vnorm(yv)) {
+      hist.push_back({sv, yv, 1.0 / sy});
+      if (int(hist.size()) > memory) hist.pop_front();
+    }
+    const double fprev = value;
+    x = xn;
+    value = fnew;
+    g = gnv;
+    ++iter;
+    if (vnorm(g) <= g_tol) {
+      done = true;
+      status = 0;
+    } else if (std::abs(fprev - value) <= f_tol * std::max({std::abs(fprev), std::abs(value), 1.0})) {
+      done = true;
+      status = 1;
+    }
+    return true;
+  }
+};
+}  // namespace fitref
+
 static thread_local std::string g_err;
 
 template <class F>
@@ -1158,6 +1395,73 @@ int oracle_engine_evaluate(int kind, int64_t n, int64_t q, int64_t d, int64_t m,
     if (times) {
       times[0] = o.wall_s;
       times[1] = o.coordinator_s;
+    }
+  });
+}
+
+// FitSession over the oracle engine: `iters` sync_steps; values[0..] = -bound per accepted iterate,
+// final parameters out (var, ls, beta, z, mu, s).  Returns the L-BFGS status in *status.
+int oracle_fit(int kind, int64_t n, int64_t q, int64_t d, int64_t m, const double* x_or_mu, const double* s0,
+               const double* y, const double* z0, double variance, const double* ls0, double beta, int workers,
+               int iters, double* values, double* grad_norms, int* status, int* evals, double* var_out,
+               double* ls_out, double* beta_out, double* z_out, double* mu_out, double* s_out) {
+  return guard([&] {
+    const bool latent = kind == 1;
+    fitref::Layout L{q, m, latent ? n : 0, latent};
+    fitref::Params p;
+    p.var = variance;
+    p.beta = beta;
+    p.ls.assign(ls0, ls0 + q);
+    p.z = Mat(m, q);
+    std::copy(z0, z0 + m * q, p.z.v.begin());
+    if (latent) {
+      p.mu = Mat(n, q);
+      p.s = Mat(n, q);
+      std::copy(x_or_mu, x_or_mu + n * q, p.mu.v.begin());
+      std::copy(s0, s0 + n * q, p.s.v.begin());
+    }
+    const View yv = cv(y, n, d, 0);
+    fitref::Lbfgs opt;
+    opt.f = [&](const fitref::Vec& v, fitref::Vec& g) {  // DistributedObjective (model.hpp:66-84)
+      fitref::Params pp = fitref::unpack(v, L);
+      Kernel k = mk_kernel(pp.var, pp.ls.data(), q);
+      EvalOut r = latent ? engine_evaluate(true, view(pp.mu), view(pp.s), yv, view(pp.z), k, pp.beta, workers,
+                                           Tiles{64, 1024}, 1e-6, true)
+                         : engine_evaluate(false, cv(x_or_mu, n, q, 0), View{}, yv, view(pp.z), k, pp.beta, workers,
+                                           Tiles{64, 1024}, 1e-6, true);
+      g.assign(size_t(L.size()), 0.0);  // -pack_gradient (optimizer.hpp:126-144)
+      g[0] = -pp.beta * r.d_beta;
+      g[1] = -pp.var * r.d_variance;
+      for (Index j = 0; j < q; ++j) g[size_t(2 + j)] = -pp.ls[size_t(j)] * r.d_ls[size_t(j)];
+      for (Index i = 0; i < m; ++i)
+        for (Index j = 0; j < q; ++j) g[size_t(L.z_off() + i * q + j)] = -r.d_z(i, j);
+      if (latent)
+        for (Index i = 0; i < n; ++i)
+          for (Index j = 0; j < q; ++j) {
+            g[size_t(L.mu_off() + i * q + j)] = -r.d_mu(i, j);
+            g[size_t(L.s_off() + i * q + j)] = -pp.s(i, j) * r.d_s(i, j);
+          }
+      return -r.bd.total;
+    };
+    opt.x = fitref::pack(p, L);
+    opt.value = opt.eval(opt.x, opt.g);  // initialize
+    values[0] = opt.value;
+    grad_norms[0] = fitref::vnorm(opt.g);
+    int k = 0;
+    for (; k < iters && opt.step(); ++k) {
+      values[k + 1] = opt.value;
+      grad_norms[k + 1] = fitref::vnorm(opt.g);
+    }
+    *status = opt.done ? opt.status : -1;
+    *evals = opt.evals;
+    fitref::Params out = fitref::unpack(opt.x, L);
+    *var_out = out.var;
+    *beta_out = out.beta;
+    std::copy(out.ls.begin(), out.ls.end(), ls_out);
+    std::copy(out.z.v.begin(), out.z.v.end(), z_out);
+    if (latent) {
+      std::copy(out.mu.v.begin(), out.mu.v.end(), mu_out);
+      std::copy(out.s.v.begin(), out.s.v.end(), s_out);
     }
   });
 }

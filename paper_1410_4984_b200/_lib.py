@@ -70,6 +70,14 @@ class eval_result(C.Structure):
                 ("psi2_bwd_kernel_s", C.c_double)]
 
 
+class lbfgs_options(C.Structure):
+    _fields_ = [("memory", C.c_int), ("c1", C.c_double), ("c2", C.c_double), ("g_tol", C.c_double),
+                ("f_tol", C.c_double), ("max_iters", C.c_int), ("max_evals", C.c_int), ("max_line_search", C.c_int)]
+
+
+FIT_STATUS = {-1: "running", 0: "gradient_converged", 1: "value_converged", 2: "max_iterations",
+              3: "max_evaluations", 4: "line_search_failed"}
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "sgpx_last_error": (C.c_char_p, []),
@@ -113,6 +121,17 @@ SIGNATURES = {
     "sgpx_multi_set_data": (C.c_int, [C.c_void_p, cmat, cmat, cmat]),
     "sgpx_multi_broadcast": (C.c_int, [C.c_void_p, C.POINTER(kernel_spec), C.c_double, cmat, cmat, cmat]),
     "sgpx_multi_evaluate": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(eval_result), mmat, mmat]),
+    "sgpx_lbfgs_default_options": (None, [C.POINTER(lbfgs_options)]),
+    "sgpx_fit_create": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(kernel_spec), C.c_double, cmat, cmat, cmat,
+                                  C.POINTER(lbfgs_options), C.POINTER(C.c_void_p)]),
+    "sgpx_fit_step": (C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
+    "sgpx_fit_state": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int),
+                                 C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "sgpx_fit_message": (C.c_char_p, [C.c_void_p]),
+    "sgpx_fit_last_error": (C.c_char_p, []),
+    "sgpx_fit_params": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_void_p, C.POINTER(C.c_double), mmat, mmat,
+                                  mmat]),
+    "sgpx_fit_destroy": (C.c_int, [C.c_void_p]),
     "sgpx_rng_normal_matrix": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int64, C.c_int64, mmat, C.c_int]),
     "sgpx_rng_choose_rows": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.c_void_p]),
     "sgpx_io_matrix_shape": (C.c_int, [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

@@ -602,6 +602,92 @@ class Engine:
             pass
 
 
+@dataclass
+class LbfgsOptions:
+    """LbfgsOptions (optimizer.hpp:154-163)."""
+    memory: int = 10
+    c1: float = 1e-4
+    c2: float = 0.9
+    g_tol: float = 1e-5
+    f_tol: float = 1e-9
+    max_iters: int = 500
+    max_evals: int = 0
+    max_line_search: int = 40
+
+    def _c(self):
+        return L.lbfgs_options(self.memory, self.c1, self.c2, self.g_tol, self.f_tol, self.max_iters,
+                               self.max_evals, self.max_line_search)
+
+
+class FitSession:
+    """FitSession (model.hpp:100-168): the engine, the packed parameters and the stepwise L-BFGS state,
+    with the parameter vector and the L-BFGS history resident on the GPU (sgpx_fit_*).
+    ``step()`` is one sync_step; ``bound`` = -value; ``params()`` unpacks the current iterate."""
+
+    def __init__(self, kind, x_or_mu, s, y, kernel: KernelSpec, beta: float, z, options: LbfgsOptions | None = None,
+                 precision: str = "auto", ctx: Context | None = None):
+        self.kind = ModelKind(kind)
+        latent = self.kind == ModelKind.latent
+        self.engine = Engine(kind, x_or_mu, s, y, ctx=ctx, precision=precision)
+        z = _F(z)
+        self.engine._create(z.shape[0])
+        self.options = options or LbfgsOptions()
+        self._lib = L.load()
+        self.q, self.m, self.n = z.shape[1], z.shape[0], self.engine.n
+        ks = kernel._c()
+        mu_c = _cm(_F(x_or_mu)) if latent else L.cmat(None, 0, 0, 0)
+        s_c = _cm(_F(s)) if latent else L.cmat(None, 0, 0, 0)
+        self._keep = (x_or_mu, s)
+        h = C.c_void_p()
+        oc = self.options._c()
+        rc = self._lib.sgpx_fit_create(self.engine._h, self.n, C.byref(ks), float(beta), _cm(z), mu_c, s_c,
+                                       C.byref(oc), C.byref(h))
+        self._check(rc)
+        self._h = h
+
+    def _check(self, rc):
+        if rc != L.SGPX_OK:
+            msg = self._lib.sgpx_fit_last_error().decode(errors="replace")
+            raise (SgpxNumericError if rc == L.SGPX_NUMERIC else SgpxError)(msg)
+
+    def step(self) -> bool:
+        adv = C.c_int()
+        self._check(self._lib.sgpx_fit_step(self._h, C.byref(adv)))
+        return bool(adv.value)
+
+    def state(self) -> dict:
+        v, gn = C.c_double(), C.c_double()
+        it, ev, le, st = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        self._check(self._lib.sgpx_fit_state(self._h, C.byref(v), C.byref(gn), C.byref(it), C.byref(ev), C.byref(le),
+                                             C.byref(st)))
+        return dict(value=v.value, bound=-v.value, grad_norm=gn.value, iterations=it.value, total_evals=ev.value,
+                    last_step_evals=le.value, status=L.FIT_STATUS.get(st.value, "unknown"),
+                    message=self._lib.sgpx_fit_message(self._h).decode())
+
+    def params(self) -> dict:
+        var, beta = C.c_double(), C.c_double()
+        ls = np.zeros(self.q)
+        z = np.zeros((self.m, self.q), order="F")
+        latent = self.kind == ModelKind.latent
+        mu = np.zeros((self.n, self.q), order="F") if latent else None
+        s = np.zeros((self.n, self.q), order="F") if latent else None
+        nm = L.mmat(None, 0, 0, 0)
+        self._check(self._lib.sgpx_fit_params(self._h, C.byref(var), ls.ctypes.data_as(C.c_void_p), C.byref(beta),
+                                              _cm(z), _cm(mu) if latent else nm, _cm(s) if latent else nm))
+        return dict(variance=var.value, lengthscales=ls, beta=beta.value, z=z, mu=mu, s=s)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            self._lib.sgpx_fit_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class MultiEngine:
     """sgp::Engine(kind, x, s, y, workers) over several GPUs of one process (sgpx_multi_*): shards by
     make_partition, shard i on ``devices[i]`` (default: round-robin over the visible GPUs), the two

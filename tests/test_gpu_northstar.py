@@ -371,3 +371,35 @@ def test_predict_matches_reference(sgp, orc, latent, device_coord, monkeypatch):
         assert rel_err(bound, rb) < 1e-12 and rel_err(eng.cached_bound, rb) < 1e-12
     with pytest.raises(ValueError, match="column mismatch"):
         eng.predict(np.zeros((2, 4)))
+
+
+@pytest.mark.parametrize("latent", [True, False])
+def test_fit_session_matches_reference_lbfgs(sgp, orc, latent):
+    """FitSession + LbfgsState (model.hpp:100-168, optimizer.hpp:20-458) with the parameter vector and
+    the L-BFGS history on the device, against the oracle's restatement over the fp64 engine: the same
+    objective values iteration by iteration (direct mode: fp64 on both sides), the same line-search
+    evaluation count, the same final parameters."""
+    from paper_1410_4984_b200 import synthetic
+
+    w = synthetic.make(latent, 3000, 3, 4, 12, seed=31)
+    kind = sgp.ModelKind.latent if latent else sgp.ModelKind.regression
+    iters = 6
+    fs = sgp.FitSession(kind, w.mu, w.s, w.y, w.kernel, w.beta, w.z, precision="direct")
+    values = [fs.state()["value"]]
+    for _ in range(iters):
+        if not fs.step():
+            break
+        values.append(fs.state()["value"])
+    ref = orc.fit(latent, w.mu, w.s, w.y, w.z, w.variance, w.lengthscales, w.beta, iters, workers=THREADS)
+    got = np.array(values)
+    want = ref["values"][:len(got)]
+    assert np.all(np.diff(got) <= 0.0)
+    assert rel_err(got, want) < 1e-8, (got, want)
+    st = fs.state()
+    assert st["total_evals"] == ref["evals"]
+    p = fs.params()
+    rp = ref["params"]
+    assert rel_err(p["variance"], rp["variance"]) < 1e-7 and rel_err(p["beta"], rp["beta"]) < 1e-7
+    assert rel_err(p["lengthscales"], rp["lengthscales"]) < 1e-7 and rel_err(p["z"], rp["z"]) < 1e-7
+    if latent:
+        assert rel_err(p["mu"], rp["mu"]) < 1e-7 and rel_err(p["s"], rp["s"]) < 1e-7
