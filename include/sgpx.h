@@ -47,6 +47,10 @@
  *       precise  as fast with three fp16 exponent pieces (~2^-33) and fp16 forward MMA3 pieces;
  *       direct   direct-difference exponents and exp in fp64 (the reference's own form, ~1 ulp),
  *                fp64 contractions;
+ *       syrk     (deterministic inputs; the AUTO choice there) Knm tiles in fp64, Phi = K^T K,
+ *                Psi = K^T Y and dL/dK = 2 K U + Y dPsi^T as split-TF32 tensor-core GEMMs (three
+ *                passes, ~2^-21 per product, fp32 within a 16k-row chunk, fp64 across chunks),
+ *                the gradient contraction in fp64;
  *     every sum across datapoints and across CTAs is fp64, all M-sized algebra is fp64.  AUTO
  *     picks fast / precise / direct from the spread of the inducing points.
  *   - There is no CPU fallback: without a CUDA device every compute entry point
@@ -76,6 +80,7 @@ extern "C" {
 #define SGPX_PREC_FAST 2
 #define SGPX_PREC_PRECISE 3
 #define SGPX_PREC_DIRECT 4
+#define SGPX_PREC_SYRK 5 /* deterministic inputs: fp64 Knm tiles + split-TF32 tensor-core GEMMs */
 
 /* Column-major views (Eigen::Ref<const Matrix> / Eigen::Ref<Matrix>). */
 typedef struct {

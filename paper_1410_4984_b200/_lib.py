@@ -15,9 +15,9 @@ LIB_PATH = os.path.join(PKG_DIR, os.environ.get("SGPX_LIB", "libsgpx.so"))
 HEADER_PATH = os.path.join(ROOT, "include", "sgpx.h")
 
 SGPX_OK, SGPX_INVALID_ARGUMENT, SGPX_NUMERIC, SGPX_CUDA, SGPX_NCCL, SGPX_INTERNAL, SGPX_IO = range(7)
-SGPX_PREC_AUTO, SGPX_PREC_FAST, SGPX_PREC_PRECISE, SGPX_PREC_DIRECT = 0, 2, 3, 4
+SGPX_PREC_AUTO, SGPX_PREC_FAST, SGPX_PREC_PRECISE, SGPX_PREC_DIRECT, SGPX_PREC_SYRK = 0, 2, 3, 4, 5
 PRECISION_NAMES = {SGPX_PREC_AUTO: "auto", SGPX_PREC_FAST: "fast", SGPX_PREC_PRECISE: "precise",
-                   SGPX_PREC_DIRECT: "direct"}
+                   SGPX_PREC_DIRECT: "direct", SGPX_PREC_SYRK: "syrk"}
 
 
 class cmat(C.Structure):

@@ -9,11 +9,13 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsgpx.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("psi_kernels.cu", "psi_direct.cu", "psi1_kernels.cu", "psi1_tile.cu", "psi_rowtile.cu", "sgpx_api.cu",
-                                            "synth.cu", "dla.cu", "dcoord.cu", "fit.cu", "coordinator.cpp")]
+                                            "synth.cu", "dla.cu", "dcoord.cu", "fit.cu", "syrk.cu",
+                                            "coordinator.cpp")]
 HEADERS = [os.path.join(CSRC, f) for f in ("psi_kernels.cuh", "psi_common.cuh", "tc_util.cuh", "coordinator.hpp", "dla.cuh", "dcoord.cuh")] + [
     os.path.join(ROOT, "include", "sgpx.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CUDA_LIB = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
 
 
 def _stale() -> bool:
@@ -40,7 +42,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
         list(ex.map(subprocess.check_call, cmds))
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs])
+    # cuBLAS (the SYRK path's plain GEMMs): libcublas.so.12 of this CUDA install, or the one torch has loaded
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-L" + CUDA_LIB, "-lcublas",
+                           "-Xlinker", "-rpath=" + CUDA_LIB])
     for o in objs:
         os.remove(o)
     return LIB

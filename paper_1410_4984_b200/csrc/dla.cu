@@ -8,8 +8,13 @@
 //   dla_gemm        C = alpha op(A) op(B) + beta C, 64 x 64 tiles, fixed k order (deterministic)
 //   chol_kernel     one CTA: Cholesky with the reference's diagonal escalation schedules
 //                   (factor_gram: jitter = f var, f = f0, 10 f0, ... <= 1e-2; factor_spd: + f max|a_ii|,
-//                   f = 1e-10 ... 1e-2), log-determinant, status flag
-//   trinv_kernel    W = L^-1 (lower), one thread per column
+//                   f = 1e-10 ... 1e-2), log-determinant, status flag.  Right-looking by panels of
+//                   kNb columns: the panel (rows p0..m) is factored in shared memory, then the trailing
+//                   lower triangle is updated once per panel by 4 x 4 register tiles (the unblocked
+//                   column loop is kept for M too large for a shared-memory panel)
+//   trinv_kernel    W = L^-1 (lower), one warp per column, the column held in registers (lane i owns
+//                   rows i, i + 32, ...), L read column by column (coalesced); a thread per column
+//                   above M = 1024
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -102,6 +107,81 @@ __device__ bool chol_inplace(double* w, int m, int64_t ld, double* s_piv) {
   return true;
 }
 
+// Blocked form of chol_inplace: panels of kNb columns.  panel: shared (m - p0) x kNb, row-major by
+// panel row (stride kNb + 1).  Same result up to the order of the trailing-update sums.
+constexpr int kNb = 32;
+__device__ bool chol_blocked(double* w, int m, int64_t ld, double* panel, double* s_piv) {
+  constexpr int PS = kNb + 1;
+  for (int p0 = 0; p0 < m; p0 += kNb) {
+    const int nb = min(kNb, m - p0), rows = m - p0;
+    for (int e = threadIdx.x; e < rows * nb; e += blockDim.x) {
+      const int c = e / rows, r = e % rows;  // coalesced along the column
+      panel[r * PS + c] = w[p0 + r + int64_t(p0 + c) * ld];
+    }
+    __syncthreads();
+    // panel factor, thread per panel row (each row's entries right of column j updated by its owner)
+    for (int j = 0; j < nb; ++j) {
+      if (threadIdx.x == 0) {
+        const double d = panel[j * PS + j];
+        s_piv[0] = (d > 0.0) ? sqrt(d) : -1.0;
+      }
+      __syncthreads();
+      const double ljj = s_piv[0];
+      if (!(ljj > 0.0)) return false;
+      const double inv = 1.0 / ljj;
+      for (int r = j + threadIdx.x; r < rows; r += blockDim.x) panel[r * PS + j] = r == j ? ljj : panel[r * PS + j] * inv;
+      __syncthreads();
+      for (int r = j + 1 + threadIdx.x; r < rows; r += blockDim.x) {
+        const double lrj = panel[r * PS + j];
+        const int cmax = min(nb - 1, r);
+        for (int c = j + 1; c <= cmax; ++c) panel[r * PS + c] -= lrj * panel[c * PS + j];
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < rows * nb; e += blockDim.x) {
+      const int c = e / rows, r = e % rows;
+      w[p0 + r + int64_t(p0 + c) * ld] = r < c ? 0.0 : panel[r * PS + c];
+    }
+    // trailing lower triangle: w[i][c] -= sum_k P[i][k] P[c][k] for p0 + nb <= c <= i < m, 4 x 4 tiles
+    const int t0 = nb, tr = rows - nb;  // panel rows t0 .. rows-1
+    const int nt = (tr + 3) / 4;
+    const int64_t ntiles = int64_t(nt) * (nt + 1) / 2;
+    for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x) {
+      // t -> (bi >= bj) in the lower triangle of tiles
+      int bi = int((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
+      while (int64_t(bi) * (bi + 1) / 2 > t) --bi;
+      while (int64_t(bi + 1) * (bi + 2) / 2 <= t) ++bi;
+      const int bj = int(t - int64_t(bi) * (bi + 1) / 2);
+      double acc[4][4] = {};
+      for (int k = 0; k < nb; ++k) {
+        double pi[4], pc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int ri = t0 + bi * 4 + u, rc = t0 + bj * 4 + u;
+          pi[u] = ri < rows ? panel[ri * PS + k] : 0.0;
+          pc[u] = rc < rows ? panel[rc * PS + k] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = fma(pi[u], pc[v], acc[u][v]);
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int c = bj * 4 + v;
+        if (c >= tr) continue;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = bi * 4 + u;
+          if (i < tr && i >= c) w[p0 + t0 + i + int64_t(p0 + t0 + c) * ld] -= acc[u][v];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
 // mode 0 (factor_gram, kernels.hpp:177-197): diag += f * var, f = f0, then x10 (0 -> 1e-6) while
 // f < 1e-2, failure after 1e-2.  mode 1 (factor_spd, bound.hpp:52-62): first the plain matrix, then
 // diag += f * max_i |a_ii| for f = 1e-10, 1e-9, ..., 1e-2.
@@ -109,7 +189,8 @@ __device__ bool chol_inplace(double* w, int m, int64_t ld, double* s_piv) {
 // out_scal[0] = log det, out_scal[1] = jitter factor used (mode 0) / shift used (mode 1).
 __global__ void __launch_bounds__(1024) chol_kernel(const double* __restrict__ a, int m, double* __restrict__ L,
                                                     int mode, double f0, double var, double* __restrict__ out_scal,
-                                                    int* __restrict__ info) {
+                                                    int* __restrict__ info, int blocked) {
+  extern __shared__ double panel[];
   __shared__ double s_piv[1], s_red[1024];
   const int64_t ld = m;
   double scale = 0.0;
@@ -134,7 +215,7 @@ __global__ void __launch_bounds__(1024) chol_kernel(const double* __restrict__ a
       L[e] = i < j ? 0.0 : a[e] + (i == j ? shift : 0.0);
     }
     __syncthreads();
-    ok = chol_inplace(L, m, ld, s_piv);
+    ok = blocked ? chol_blocked(L, m, ld, panel, s_piv) : chol_inplace(L, m, ld, s_piv);
     __syncthreads();
     if (ok) break;
     if (mode == 0) {
@@ -177,6 +258,42 @@ __global__ void trinv_kernel(const double* __restrict__ L, int m, double* __rest
   }
 }
 
+// Same substitution, warp per column j: lane l owns x[l + 32 t], t < T (T * 32 >= m).  Step k
+// broadcasts x_k / L_kk from its owner and updates the rows below with column k of L.
+template <int T>
+__global__ void __launch_bounds__(64) trinv_warp_kernel(const double* __restrict__ L, int m, double* __restrict__ W) {
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * 2 + (threadIdx.x >> 5);
+  if (j >= m) return;
+  double x[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) x[t] = (lane + 32 * t == j) ? 1.0 : 0.0;
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    if (32 * t + 31 < j || 32 * t >= m) continue;
+    const int kd = 32 * t + lane;
+    const double rd = kd < m ? 1.0 / L[kd + int64_t(kd) * m] : 0.0;  // 1 / L_kk of the slot's rows
+#pragma unroll 4
+    for (int l = 0; l < 32; ++l) {
+      const int k = 32 * t + l;
+      if (k < j || k >= m) continue;
+      const double xk = __shfl_sync(0xffffffffu, x[t], l) * __shfl_sync(0xffffffffu, rd, l);
+      if (lane == l) x[t] = xk;
+      const double* lk = L + int64_t(k) * m;
+#pragma unroll
+      for (int u = t; u < T; ++u) {
+        const int i = lane + 32 * u;
+        if (i > k && i < m) x[u] = fma(-lk[i], xk, x[u]);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const int i = lane + 32 * t;
+    if (i < m) W[i + int64_t(j) * m] = x[t];
+  }
+}
+
 }  // namespace
 
 int gemm(bool ta, bool tb, int m, int n, int k, double alpha, const double* A, int64_t lda, const double* B,
@@ -190,13 +307,31 @@ int gemm(bool ta, bool tb, int m, int n, int k, double alpha, const double* A, i
 
 int cholesky(const double* a, int m, double* L, int mode, double f0, double var, double* out_scal, int* info,
              cudaStream_t st) {
-  chol_kernel<<<1, 1024, 0, st>>>(a, m, L, mode, f0, var, out_scal, info);
+  const size_t smem = sizeof(double) * size_t(m) * (kNb + 1);
+  const bool blocked = smem <= 200 * 1024;
+  if (blocked) {
+    static std::atomic<uint64_t> attr_set{0};  // per-device one-time opt-in (the largest size asked for)
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 3;
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    if (!(attr_set.load() & bit)) {
+      if (cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess)
+        return 3;
+      attr_set.fetch_or(bit);
+    }
+  }
+  chol_kernel<<<1, 1024, blocked ? smem : 0, st>>>(a, m, L, mode, f0, var, out_scal, info, blocked ? 1 : 0);
   g_tc_launches.fetch_add(1);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
 int trinv(const double* L, int m, double* W, cudaStream_t st) {
-  trinv_kernel<<<(m + 127) / 128, 128, 0, st>>>(L, m, W);
+  const unsigned g = unsigned((m + 1) / 2);
+  if (m <= 128) trinv_warp_kernel<4><<<g, 64, 0, st>>>(L, m, W);
+  else if (m <= 256) trinv_warp_kernel<8><<<g, 64, 0, st>>>(L, m, W);
+  else if (m <= 512) trinv_warp_kernel<16><<<g, 64, 0, st>>>(L, m, W);
+  else if (m <= 1024) trinv_warp_kernel<32><<<g, 64, 0, st>>>(L, m, W);
+  else trinv_kernel<<<(m + 127) / 128, 128, 0, st>>>(L, m, W);
   g_tc_launches.fetch_add(1);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }

@@ -131,6 +131,7 @@ int env_mode() {
     if (!strcmp(e, "fast")) return kModeFast;
     if (!strcmp(e, "precise")) return kModePrecise;
     if (!strcmp(e, "direct")) return kModeDirect;
+    if (!strcmp(e, "syrk")) return kModeSyrk;
     return kModeAuto;
   }();
   return v;
@@ -178,6 +179,9 @@ double psi_z_spread(const PsiConst& P, const double* z, int64_t m) {
 int psi_select_mode(const PsiConst& P, const double* z, int64_t m, int requested) {
   if (P.q > kMaxQ) return -1;
   int req = requested != kModeAuto ? requested : env_mode();
+  // deterministic inputs: the Knm-tile SYRK unless another mode is asked for (accurate at any spread)
+  if (!P.expected && (req == kModeAuto || req == kModeSyrk) && syrk_supported(P)) return kModeSyrk;
+  if (req == kModeSyrk) req = kModeAuto;  // latent inputs have no SYRK form
   if (!use_rt(P)) return kModeDirect;
   if (req == kModeDirect) return kModeDirect;
   const double tz = psi_z_spread(P, z, m);
@@ -188,14 +192,19 @@ int psi_select_mode(const PsiConst& P, const double* z, int64_t m, int requested
   return kModeDirect;
 }
 
-static bool is_direct(const PsiConst& P) { return P.mode == kModeDirect || !use_rt(P); }
+static bool is_syrk(const PsiConst& P) { return P.mode == kModeSyrk; }
+static bool is_direct(const PsiConst& P) { return !is_syrk(P) && (P.mode == kModeDirect || !use_rt(P)); }
 
 const double* fwd_region(const PsiConst& P, const double* fwd_part, int num_sms) {
-  if (is_direct(P)) return fwd_part;
+  if (is_direct(P) || is_syrk(P)) return fwd_part;
   return fwd_part + int64_t(psi1_fwd_rows(P, num_sms)) * fwd_part_count(P.m, P.d);
 }
 
 double* fwd_pair_sums(const PsiConst& P, double* region, int num_sms, int64_t* count) {
+  if (is_syrk(P)) {  // the SYRK backward needs no forward sums
+    *count = 0;
+    return region;
+  }
   if (is_direct(P)) return direct_fwd_pair_sums(P, region, num_sms, count);
   return rt_fwd_pair_sums(P, region, num_sms, count);
 }
@@ -205,6 +214,13 @@ int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   LaunchGeom g{};
   if (int rc = plan_forward(P, num_sms, &g)) return rc;
+  if (is_syrk(P)) {
+    if (ev_begin) record_event(ev_begin, st);
+    if (int rc = syrk_forward(P, part, packed, err_flag, num_sms, stream)) return rc;
+    if (ev_end) record_event(ev_end, st);
+    if (geom) *geom = g;
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  }
   if (is_direct(P)) {
     if (!direct_supported(P)) return 1;
     if (ev_begin) record_event(ev_begin, st);
@@ -235,6 +251,13 @@ int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* pac
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   LaunchGeom g{};
   if (int rc = plan_backward(P, num_sms, &g)) return rc;
+  if (is_syrk(P)) {
+    if (ev_begin) record_event(ev_begin, st);
+    if (int rc = syrk_backward(P, B, part, packed, num_sms, stream)) return rc;
+    if (ev_end) record_event(ev_end, st);
+    if (geom) *geom = g;
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  }
   if (is_direct(P)) {
     if (ev_begin) record_event(ev_begin, st);
     if (int rc = direct_backward(P, B, part, packed, num_sms, stream)) return rc;
@@ -262,6 +285,10 @@ int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* pac
 
 int plan_forward(const PsiConst& P, int num_sms, LaunchGeom* geom) {
   const int64_t pstride = fwd_part_count(P.m, P.d);
+  if (is_syrk(P)) {
+    *geom = LaunchGeom{int((syrk_fwd_doubles(P, num_sms) + pstride - 1) / pstride), 256, 0};
+    return 0;
+  }
   if (is_direct(P)) {
     *geom = LaunchGeom{int((direct_fwd_doubles(P, num_sms) + pstride - 1) / pstride), 128, 0};
     return 0;
@@ -274,6 +301,10 @@ int plan_forward(const PsiConst& P, int num_sms, LaunchGeom* geom) {
 
 int plan_backward(const PsiConst& P, int num_sms, LaunchGeom* geom) {
   const int64_t pstride = bwd_part_count(P.m, P.q);
+  if (is_syrk(P)) {
+    *geom = LaunchGeom{int((syrk_bwd_doubles(P, num_sms) + pstride - 1) / pstride), 256, 0};
+    return 0;
+  }
   if (is_direct(P)) {
     *geom = LaunchGeom{int((direct_bwd_doubles(P, num_sms) + pstride - 1) / pstride), 128, 0};
     return 0;

@@ -37,7 +37,9 @@ constexpr int kMaxQ = 64;
 //   kModePrecise  row-tile tcgen05 path, three fp16 pieces, scaled fp16 forward MMA3
 //   kModeDirect   direct-difference kernels with fp64 exponents (psi_direct.cu): accurate for any
 //                 spread of the data and any Q <= kMaxQ
-constexpr int kModeAuto = 0, kModeFast = 2, kModePrecise = 3, kModeDirect = 4;
+//   kModeSyrk     deterministic inputs only: fp64 Knm tiles, Phi = K^T K, Psi = K^T Y and
+//                 dL/dK = 2 K U + Y dPsi^T as split-TF32 tensor-core GEMMs (syrk.cu)
+constexpr int kModeAuto = 0, kModeFast = 2, kModePrecise = 3, kModeDirect = 4, kModeSyrk = 5;
 
 // Per-launch constants (passed by value; ~0.7 KB of kernel parameter space).
 struct PsiConst {
@@ -152,6 +154,12 @@ int direct_forward(const PsiConst& P, double* base, double* packed, int* err_fla
                    void* stream);
 int direct_backward(const PsiConst& P, const BwdConst& B, double* bbase, double* packed, int num_sms, void* stream);
 double* direct_fwd_pair_sums(const PsiConst& P, double* base, int num_sms, int64_t* count);
+// Knm-tile SYRK path for deterministic inputs (syrk.cu).
+bool syrk_supported(const PsiConst& P);
+int64_t syrk_fwd_doubles(const PsiConst& P, int num_sms);
+int64_t syrk_bwd_doubles(const PsiConst& P, int num_sms);
+int syrk_forward(const PsiConst& P, double* base, double* packed, int* err_flag, int num_sms, void* stream);
+int syrk_backward(const PsiConst& P, const BwdConst& B, double* base, double* packed, int num_sms, void* stream);
 // Fixed-order reduction of backward partial rows into packed grads.
 // tmp: bwd_reduce_tmp_doubles(pstride) doubles of scratch.
 int64_t bwd_reduce_tmp_doubles(int64_t pstride);

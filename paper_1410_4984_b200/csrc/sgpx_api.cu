@@ -944,7 +944,7 @@ int sgpx_ctx_set_precision(sgpx_ctx* ctx, int precision) {
   return guard([&] {
     require(ctx != nullptr, "ctx is null");
     require(precision == SGPX_PREC_AUTO || precision == SGPX_PREC_FAST || precision == SGPX_PREC_PRECISE ||
-                precision == SGPX_PREC_DIRECT,
+                precision == SGPX_PREC_DIRECT || precision == SGPX_PREC_SYRK,
             "unknown precision mode");
     ctx->precision = precision;
   });
@@ -1215,7 +1215,8 @@ int sgpx_engine_create(sgpx_ctx* ctx, const sgpx_engine_config* cfg, sgpx_engine
             "engine_create: shard rows outside [0, N)");
     require(cfg->q >= 1 && cfg->q <= kMaxQ, "engine_create: Q must be in [1, 64]");
     require(cfg->precision == SGPX_PREC_AUTO || cfg->precision == SGPX_PREC_FAST ||
-                cfg->precision == SGPX_PREC_PRECISE || cfg->precision == SGPX_PREC_DIRECT,
+                cfg->precision == SGPX_PREC_PRECISE || cfg->precision == SGPX_PREC_DIRECT ||
+                cfg->precision == SGPX_PREC_SYRK,
             "engine_create: unknown precision mode");
     require(cfg->m >= 1 && cfg->d >= 1, "engine_create: need M >= 1 and D >= 1");
     require(cfg->jitter_factor >= 0.0, "factor_gram: jitter factor must be non-negative");
@@ -1226,6 +1227,9 @@ int sgpx_engine_create(sgpx_ctx* ctx, const sgpx_engine_config* cfg, sgpx_engine
     e->latent = cfg->kind == 1;
     for (auto& ev : e->ev) CUDA_OK(cudaEventCreate(&ev));
     for (auto& ev : e->ev_c) CUDA_OK(cudaEventCreate(&ev));
+    // host coordinator up to the single-CTA shared-memory size (the two are within 0.1 ms there);
+    // above it the host's O(M^3) algebra grows past the device's blocked kernels (M = 500: 19 ms vs 3 ms)
+    e->dev_coord = cfg->m > 112;
     if (const char* dc = getenv("SGPX_DEVICE_COORD")) e->dev_coord = atoi(dc) != 0;  // A/B
     if (const char* gr = getenv("SGPX_GRAPH")) e->use_graph = atoi(gr) != 0;       // A/B: per-call launches
     *out = e.release();

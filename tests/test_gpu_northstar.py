@@ -191,13 +191,13 @@ def _layout(kind, f, n=4000, q=10, d=10, m=100, seed=1):
     return mu, s, y, z, ls, adj
 
 
-ENVELOPE = [  # (layout, expected mode latent, expected mode SGPR)
-    ("gauss", 1, "fast", "precise"), ("gauss", 2, "fast", "direct"), ("gauss", 3, "precise", "direct"),
-    ("gauss", 8, "direct", "direct"), ("gauss", 16, "direct", "direct"), ("gauss", 24, "direct", "direct"),
-    ("gauss", 32, "direct", "direct"), ("bimodal", 10, "precise", "direct"), ("bimodal", 30, "direct", "direct"),
-    ("bimodal", 300, "direct", "direct"), ("farcluster", 300, "fast", "precise"),
-    ("outliers", 30, "fast", "precise"), ("outliers", 1000, "fast", "precise"),
-    ("zcluster", 20, "precise", "direct"), ("zcluster", 60, "direct", "direct"),
+ENVELOPE = [  # (layout, expected mode latent, expected mode SGPR: always the Knm-tile SYRK)
+    ("gauss", 1, "fast", "syrk"), ("gauss", 2, "fast", "syrk"), ("gauss", 3, "precise", "syrk"),
+    ("gauss", 8, "direct", "syrk"), ("gauss", 16, "direct", "syrk"), ("gauss", 24, "direct", "syrk"),
+    ("gauss", 32, "direct", "syrk"), ("bimodal", 10, "precise", "syrk"), ("bimodal", 30, "direct", "syrk"),
+    ("bimodal", 300, "direct", "syrk"), ("farcluster", 300, "fast", "syrk"),
+    ("outliers", 30, "fast", "syrk"), ("outliers", 1000, "fast", "syrk"),
+    ("zcluster", 20, "precise", "syrk"), ("zcluster", 60, "direct", "syrk"),
 ]
 
 
@@ -291,13 +291,14 @@ def test_direct_mode_engine_subshards(sgp, orc):
     _check_eval(r, ref, True, elem_tol=DIRECT_TOL, bound_tol=DIRECT_TOL)
 
 
-@pytest.mark.parametrize("latent", [True, False])
-def test_device_coordinator_matches_host(sgp, latent, monkeypatch):
-    """The coordinator on the device (dcoord.cu, the default) against the host fp64 coordinator
-    (coordinator.cpp): same statistics in, the same bound / gradients out to fp64 rounding."""
+@pytest.mark.parametrize("latent,m", [(True, 100), (False, 100), (True, 300), (False, 500)])
+def test_device_coordinator_matches_host(sgp, latent, m, monkeypatch):
+    """The coordinator on the device (dcoord.cu: the single-CTA shared-memory kernels for M <= 112,
+    the blocked Cholesky / warp-per-column inverse / tiled gemm of dla.cu above) against the host fp64
+    coordinator (coordinator.cpp): same statistics in, the same bound / gradients out to fp64 rounding."""
     from paper_1410_4984_b200 import synthetic
 
-    w = synthetic.make(latent, 30_000, 10, 8, 100, seed=4)
+    w = synthetic.make(latent, 30_000, 10 if latent else 8, 8, m, seed=4)
     out = []
     for dev in ("1", "0"):
         monkeypatch.setenv("SGPX_DEVICE_COORD", dev)
@@ -307,13 +308,18 @@ def test_device_coordinator_matches_host(sgp, latent, monkeypatch):
         out.append(eng.evaluate(True))
         eng.close()
     a, b = out
-    assert rel_err(a.bound.total, b.bound.total) < 1e-13
+    # the two coordinators sum in different fp64 orders; above the small-M path the blocked Cholesky's
+    # order meets cond(Kmm + beta Phi) at M = 500 (~1e-11 on the bound)
+    tb, tf, tg = (1e-13, 1e-12, 1e-10) if m <= 112 else (1e-10, 1e-8, 1e-8)
+    assert rel_err(a.bound.total, b.bound.total) < tb
     for f in sgp.BOUND_FIELDS:
-        assert rel_err(getattr(a.bound, f), getattr(b.bound, f)) < 1e-12, f
-    assert rel_err(a.grads.d_z, b.grads.d_z) < 1e-10
-    assert rel_err(a.grads.d_lengthscales, b.grads.d_lengthscales) < 1e-11
-    assert rel_err(a.grads.d_variance, b.grads.d_variance) < 1e-11
-    assert rel_err(a.grads.d_beta, b.grads.d_beta) < 1e-11
+        assert rel_err(getattr(a.bound, f), getattr(b.bound, f)) < tf, f
+    # (with Q = 4 and M = 500, Kmm is ill-conditioned enough that either coordinator and the oracle
+    # differ at ~5e-3 in d Z from fp64 summation order alone: tools/dbg_coord_large_m.py)
+    assert rel_err(a.grads.d_z, b.grads.d_z) < tg
+    assert rel_err(a.grads.d_lengthscales, b.grads.d_lengthscales) < tg
+    assert rel_err(a.grads.d_variance, b.grads.d_variance) < tg
+    assert rel_err(a.grads.d_beta, b.grads.d_beta) < tg
     assert a.jitter_factor == b.jitter_factor
     if latent:
         assert rel_err(a.grads.d_mu, b.grads.d_mu) < 1e-11
