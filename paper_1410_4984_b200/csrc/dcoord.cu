@@ -78,6 +78,11 @@ __device__ double block_sum(double v, double* red) {
   return s;
 }
 
+__device__ __forceinline__ double dev_warp_sum(double v) {  // fixed butterfly order
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 // Bound terms (bound.hpp:108-116) and the scalar adjoint d_phi; contract checks of the reduced
 // statistics (bound.hpp:84-92).  One CTA, fixed-order trees.
 __global__ void __launch_bounds__(1024) bound_kernel(DcArgs A) {
@@ -157,6 +162,23 @@ __global__ void dkmm_kernel(DcArgs A) {
 
 // d beta (bound.hpp:217-223) and kern_grads(Z, Z, d Kmm) with the gradient assembly of
 // parallel.hpp:414-421 (d_z + d_x, d var + jitter_factor tr(d Kmm), d l).  One CTA.
+// W = d Kmm o K (K without jitter), the first step of kern_grads(Z, Z, U) (kernels.hpp:124-164)
+__global__ void w_kernel(DcArgs A) {
+  const int64_t mm = int64_t(A.m) * A.m;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < mm; e += int64_t(gridDim.x) * blockDim.x)
+    A.w[e] = A.dkmm[e] * A.kmm[e];
+}
+// row sums of W, thread per row, ascending b (coalesced across rows)
+__global__ void rowsum_kernel(DcArgs A) {
+  const int m = A.m;
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= m) return;
+  double s = 0.0;
+  for (int b = 0; b < m; ++b) s += A.w[a + int64_t(b) * m];
+  A.rs[a] = s;
+}
+
+// the tail of the gradient assembly, after W, rs and W Z (one CTA, fixed-order block sums)
 __global__ void __launch_bounds__(1024) finish_kernel(DcArgs A, const double* __restrict__ pgrads) {
   __shared__ double red[1024];
   const int m = A.m, q = A.q, d = A.d;
@@ -166,46 +188,32 @@ __global__ void __launch_bounds__(1024) finish_kernel(DcArgs A, const double* __
   double tg = 0.0;
   for (int64_t e = threadIdx.x; e < int64_t(m) * d; e += blockDim.x) tg += A.g[e] * A.phig[e];
   tg = block_sum(tg, red);
-  // W = d Kmm o K (K without jitter), row sums, total, trace of d Kmm
+  // sum W = sum of the row sums, trace of d Kmm
   double tot = 0.0, tr = 0.0;
-  for (int64_t e = threadIdx.x; e < int64_t(m) * m; e += blockDim.x) {
-    const double w = A.dkmm[e] * A.kmm[e];
-    A.w[e] = w;
-    tot += w;
-    if (e % m == e / m) tr += A.dkmm[e];
+  for (int a = threadIdx.x; a < m; a += blockDim.x) {
+    tot += A.rs[a];
+    tr += A.dkmm[a + int64_t(a) * m];
   }
   tot = block_sum(tot, red);
   tr = block_sum(tr, red);
-  __syncthreads();
-  for (int a = threadIdx.x; a < m; a += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < m; ++b) s += A.w[a + int64_t(b) * m];
-    A.rs[a] = s;
-  }
-  __syncthreads();
-  // W Z (M x Q): thread per (a, j), ascending b
-  for (int64_t e = threadIdx.x; e < int64_t(m) * q; e += blockDim.x) {
-    const int a = int(e % m), j = int(e / m);
-    double s = 0.0;
-    for (int b = 0; b < m; ++b) s += A.w[a + int64_t(b) * m] * A.z[b + int64_t(j) * m];
-    A.wz[e] = s;
-  }
-  __syncthreads();
   double* res = A.result;  // [d var, d l (Q), d Z (M Q), d beta]
   for (int64_t e = threadIdx.x; e < int64_t(m) * q; e += blockDim.x) {
     const int a = int(e % m), j = int(e / m);
     const double il2 = 1.0 / (A.ls[j] * A.ls[j]);
     res[1 + q + e] = pgrads[1 + q + e] + 2.0 * (A.wz[e] - A.rs[a] * A.z[e]) * il2;
   }
-  // sum_ab W_ab (z_a - z_b)^2 = 2 (sum_a rs_a z_a^2 - z^T W z) per dimension (thread per q, ascending a)
-  for (int j = threadIdx.x; j < q; j += blockDim.x) {
+  // sum_ab W_ab (z_a - z_b)^2 = 2 (sum_a rs_a z_a^2 - z^T W z) per dimension (a warp per q, fixed tree)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = warp; j < q; j += blockDim.x >> 5) {
     double s2 = 0.0, cross = 0.0;
-    for (int a = 0; a < m; ++a) {
+    for (int a = lane; a < m; a += 32) {
       const double za = A.z[a + int64_t(j) * m];
       s2 += A.rs[a] * za * za;
       cross += za * A.wz[a + int64_t(j) * m];
     }
-    res[1 + j] = pgrads[1 + j] + 2.0 * (s2 - cross) / (A.ls[j] * A.ls[j] * A.ls[j]);
+    s2 = dev_warp_sum(s2);
+    cross = dev_warp_sum(cross);
+    if (lane == 0) res[1 + j] = pgrads[1 + j] + 2.0 * (s2 - cross) / (A.ls[j] * A.ls[j] * A.ls[j]);
   }
   if (threadIdx.x == 0) {
     res[0] = pgrads[0] + tot / A.var + sc[kScJitterFactor] * tr;
@@ -214,7 +222,6 @@ __global__ void __launch_bounds__(1024) finish_kernel(DcArgs A, const double* __
                                   0.5 * beta * beta * tg - 0.5 * dd * phi0 + 0.5 * dd * sc[kScKp];
   }
 }
-
 
 // ---------------------------------------------------------------------------------------------
 // Small-M path (M <= kSmallM): each coordinator step is ONE CTA working in shared memory —
@@ -676,6 +683,11 @@ int dc_deferred(const DcArgs& A, cudaStream_t st) {
 }
 
 int dc_finish(const DcArgs& A, const double* pgrads, cudaStream_t st) {
+  const int m = A.m;
+  w_kernel<<<blocks_for(int64_t(m) * m), 256, 0, st>>>(A);
+  rowsum_kernel<<<(m + 127) / 128, 128, 0, st>>>(A);
+  g_tc_launches.fetch_add(2);
+  if (dla::gemm(false, false, m, A.q, m, 1.0, A.w, m, A.z, m, 0.0, A.wz, m, st)) return 3;
   finish_kernel<<<1, 1024, 0, st>>>(A, pgrads);
   g_tc_launches.fetch_add(1);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;

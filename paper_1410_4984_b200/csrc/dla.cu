@@ -9,9 +9,9 @@
 //   chol_kernel     one CTA: Cholesky with the reference's diagonal escalation schedules
 //                   (factor_gram: jitter = f var, f = f0, 10 f0, ... <= 1e-2; factor_spd: + f max|a_ii|,
 //                   f = 1e-10 ... 1e-2), log-determinant, status flag.  Right-looking by panels of
-//                   kNb columns: the panel (rows p0..m) is factored in shared memory, then the trailing
-//                   lower triangle is updated once per panel by 4 x 4 register tiles (the unblocked
-//                   column loop is kept for M too large for a shared-memory panel)
+//                   32 (16) columns: the panel (rows p0..m) is factored in shared memory, then the
+//                   trailing lower triangle is updated once per panel, a warp per 32 x 32 block (the
+//                   unblocked column loop is kept for M too large for a shared-memory panel)
 //   trinv_kernel    W = L^-1 (lower), one warp per column, the column held in registers (lane i owns
 //                   rows i, i + 32, ...), L read column by column (coalesced); a thread per column
 //                   above M = 1024
@@ -107,73 +107,76 @@ __device__ bool chol_inplace(double* w, int m, int64_t ld, double* s_piv) {
   return true;
 }
 
-// Blocked form of chol_inplace: panels of kNb columns.  panel: shared (m - p0) x kNb, row-major by
-// panel row (stride kNb + 1).  Same result up to the order of the trailing-update sums.
-constexpr int kNb = 32;
-__device__ bool chol_blocked(double* w, int m, int64_t ld, double* panel, double* s_piv) {
-  constexpr int PS = kNb + 1;
-  for (int p0 = 0; p0 < m; p0 += kNb) {
-    const int nb = min(kNb, m - p0), rows = m - p0;
-    for (int e = threadIdx.x; e < rows * nb; e += blockDim.x) {
-      const int c = e / rows, r = e % rows;  // coalesced along the column
-      panel[r * PS + c] = w[p0 + r + int64_t(p0 + c) * ld];
-    }
+// Blocked form of chol_inplace: panels of nbm (32, or 16 for large M) columns.  panel: shared
+// column-major (m - p0) x nbm with column stride RS >= m (thread-per-row accesses are conflict-free,
+// column reads by a warp broadcast).  Same result up to the order of the trailing-update sums.
+__device__ bool chol_blocked(double* w, int m, int64_t ld, double* panel, double* s_piv, int nbm, int RS) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int p0 = 0; p0 < m; p0 += nbm) {
+    const int nb = min(nbm, m - p0), rows = m - p0;
+    for (int c = warp; c < nbm; c += nwarps)
+      for (int r = lane; r < rows; r += 32) panel[c * RS + r] = c < nb ? w[p0 + r + int64_t(p0 + c) * ld] : 0.0;
     __syncthreads();
-    // panel factor, thread per panel row (each row's entries right of column j updated by its owner)
+    // panel factor, thread per panel row: the rows' entries right of column j are updated from the
+    // still-unscaled column j (times 1 / l_jj), then column j is scaled after a barrier
     for (int j = 0; j < nb; ++j) {
       if (threadIdx.x == 0) {
-        const double d = panel[j * PS + j];
+        const double d = panel[j * RS + j];
         s_piv[0] = (d > 0.0) ? sqrt(d) : -1.0;
       }
       __syncthreads();
       const double ljj = s_piv[0];
       if (!(ljj > 0.0)) return false;
       const double inv = 1.0 / ljj;
-      for (int r = j + threadIdx.x; r < rows; r += blockDim.x) panel[r * PS + j] = r == j ? ljj : panel[r * PS + j] * inv;
-      __syncthreads();
       for (int r = j + 1 + threadIdx.x; r < rows; r += blockDim.x) {
-        const double lrj = panel[r * PS + j];
+        const double lrj = panel[j * RS + r] * inv;
         const int cmax = min(nb - 1, r);
-        for (int c = j + 1; c <= cmax; ++c) panel[r * PS + c] -= lrj * panel[c * PS + j];
+#pragma unroll 4
+        for (int c = j + 1; c <= cmax; ++c) panel[c * RS + r] -= lrj * (panel[j * RS + c] * inv);
       }
       __syncthreads();
+      for (int r = j + threadIdx.x; r < rows; r += blockDim.x)
+        panel[j * RS + r] = r == j ? ljj : panel[j * RS + r] * inv;
     }
-    for (int e = threadIdx.x; e < rows * nb; e += blockDim.x) {
-      const int c = e / rows, r = e % rows;
-      w[p0 + r + int64_t(p0 + c) * ld] = r < c ? 0.0 : panel[r * PS + c];
-    }
-    // trailing lower triangle: w[i][c] -= sum_k P[i][k] P[c][k] for p0 + nb <= c <= i < m, 4 x 4 tiles
-    const int t0 = nb, tr = rows - nb;  // panel rows t0 .. rows-1
-    const int nt = (tr + 3) / 4;
-    const int64_t ntiles = int64_t(nt) * (nt + 1) / 2;
-    for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x) {
-      // t -> (bi >= bj) in the lower triangle of tiles
-      int bi = int((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
-      while (int64_t(bi) * (bi + 1) / 2 > t) --bi;
-      while (int64_t(bi + 1) * (bi + 2) / 2 <= t) ++bi;
-      const int bj = int(t - int64_t(bi) * (bi + 1) / 2);
-      double acc[4][4] = {};
-      for (int k = 0; k < nb; ++k) {
-        double pi[4], pc[4];
+    __syncthreads();
+    for (int c = warp; c < nb; c += nwarps)
+      for (int r = lane; r < rows; r += 32) w[p0 + r + int64_t(p0 + c) * ld] = r < c ? 0.0 : panel[c * RS + r];
+    // trailing lower triangle: w[i][c] -= sum_k P[i][k] P[c][k] for p0 + nb <= c <= i < m.  A warp per
+    // 32 x 32 block (I >= J), each lane a 4 x 8 register tile (lane & 7 -> rows, lane >> 3 -> columns):
+    // 12 shared loads per 32 FMAs, k ascending
+    const int t0 = nb, tr = rows - nb;
+    const int nbk = (tr + 31) / 32, nblk = nbk * (nbk + 1) / 2;
+    const int lr = lane & 7, lc = lane >> 3;
+    for (int b = warp; b < nblk; b += nwarps) {
+      int I = int((sqrt(8.0 * double(b) + 1.0) - 1.0) * 0.5);
+      while (I * (I + 1) / 2 > b) --I;
+      while ((I + 1) * (I + 2) / 2 <= b) ++I;
+      const int J = b - I * (I + 1) / 2;
+      const int i0 = I * 32 + lr * 4, j0 = J * 32 + lc * 8;  // trailing-relative
+      double acc[4][8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int ri = t0 + bi * 4 + u, rc = t0 + bj * 4 + u;
-          pi[u] = ri < rows ? panel[ri * PS + k] : 0.0;
-          pc[u] = rc < rows ? panel[rc * PS + k] : 0.0;
-        }
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc[u][v] = 0.0;
+      for (int k = 0; k < nb; ++k) {
+        const double* col = panel + k * RS + t0;
+        double av[4], bv[8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) av[u] = i0 + u < tr ? col[i0 + u] : 0.0;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) bv[v] = j0 + v < tr ? col[j0 + v] : 0.0;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int v = 0; v < 4; ++v) acc[u][v] = fma(pi[u], pc[v], acc[u][v]);
+          for (int v = 0; v < 8; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
       }
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int c = bj * 4 + v;
-        if (c >= tr) continue;
+      for (int v = 0; v < 8; ++v) {
+        const int jl = j0 + v;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int i = bi * 4 + u;
-          if (i < tr && i >= c) w[p0 + t0 + i + int64_t(p0 + t0 + c) * ld] -= acc[u][v];
+          const int il = i0 + u;
+          if (jl < tr && il < tr && il >= jl) w[p0 + t0 + il + int64_t(p0 + t0 + jl) * ld] -= acc[u][v];
         }
       }
     }
@@ -187,11 +190,11 @@ __device__ bool chol_blocked(double* w, int m, int64_t ld, double* panel, double
 // diag += f * max_i |a_ii| for f = 1e-10, 1e-9, ..., 1e-2.
 // a: m x m input (lower and upper valid), out: L (upper zeroed); info[0] = status (0 ok, 1 failed),
 // out_scal[0] = log det, out_scal[1] = jitter factor used (mode 0) / shift used (mode 1).
-__global__ void __launch_bounds__(1024) chol_kernel(const double* __restrict__ a, int m, double* __restrict__ L,
+__global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ a, int m, double* __restrict__ L,
                                                     int mode, double f0, double var, double* __restrict__ out_scal,
-                                                    int* __restrict__ info, int blocked) {
+                                                    int* __restrict__ info, int nbm) {
   extern __shared__ double panel[];
-  __shared__ double s_piv[1], s_red[1024];
+  __shared__ double s_piv[1], s_red[512];
   const int64_t ld = m;
   double scale = 0.0;
   if (mode == 1) {
@@ -210,12 +213,13 @@ __global__ void __launch_bounds__(1024) chol_kernel(const double* __restrict__ a
   bool ok = false;
   for (int attempt = 0; attempt < 32; ++attempt) {
     const double shift = mode == 0 ? f * var : f * scale;
-    for (int64_t e = threadIdx.x; e < int64_t(m) * m; e += blockDim.x) {
-      const int i = int(e % m), j = int(e / m);
-      L[e] = i < j ? 0.0 : a[e] + (i == j ? shift : 0.0);
-    }
+    for (int j = threadIdx.x >> 5; j < m; j += blockDim.x >> 5)
+      for (int i = threadIdx.x & 31; i < m; i += 32) {
+        const int64_t e = i + int64_t(j) * m;
+        L[e] = i < j ? 0.0 : a[e] + (i == j ? shift : 0.0);
+      }
     __syncthreads();
-    ok = blocked ? chol_blocked(L, m, ld, panel, s_piv) : chol_inplace(L, m, ld, s_piv);
+    ok = nbm ? chol_blocked(L, m, ld, panel, s_piv, nbm, m | 1) : chol_inplace(L, m, ld, s_piv);
     __syncthreads();
     if (ok) break;
     if (mode == 0) {
@@ -307,20 +311,24 @@ int gemm(bool ta, bool tb, int m, int n, int k, double alpha, const double* A, i
 
 int cholesky(const double* a, int m, double* L, int mode, double f0, double var, double* out_scal, int* info,
              cudaStream_t st) {
-  const size_t smem = sizeof(double) * size_t(m) * (kNb + 1);
-  const bool blocked = smem <= 200 * 1024;
-  if (blocked) {
+  // panel width 32 while the (m x 34) panel fits the opt-in shared memory, else 16, else unblocked
+  constexpr size_t kSmemMax = 200 * 1024;
+  int nbm = 0;
+  if (sizeof(double) * size_t(m | 1) * 32 <= kSmemMax) nbm = 32;
+  else if (sizeof(double) * size_t(m | 1) * 16 <= kSmemMax) nbm = 16;
+  const size_t smem = nbm ? sizeof(double) * size_t(m | 1) * nbm : 0;
+  if (nbm) {
     static std::atomic<uint64_t> attr_set{0};  // per-device one-time opt-in (the largest size asked for)
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 3;
     const uint64_t bit = uint64_t(1) << (dev & 63);
     if (!(attr_set.load() & bit)) {
-      if (cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess)
+      if (cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemMax)) != cudaSuccess)
         return 3;
       attr_set.fetch_or(bit);
     }
   }
-  chol_kernel<<<1, 1024, blocked ? smem : 0, st>>>(a, m, L, mode, f0, var, out_scal, info, blocked ? 1 : 0);
+  chol_kernel<<<1, 512, smem, st>>>(a, m, L, mode, f0, var, out_scal, info, nbm);
   g_tc_launches.fetch_add(1);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }

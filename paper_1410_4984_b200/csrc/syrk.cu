@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <thread>
@@ -429,19 +430,48 @@ int gemm3(cublasHandle_t h, cudaStream_t st, cublasOperation_t ta, cublasOperati
   return 0;
 }
 
+constexpr int kSyrkQs[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24, 32, 48, 64};
+int syrk_q(int q) {
+  for (int v : kSyrkQs)
+    if (v >= q) return v;
+  return -1;
+}
+
+inline int bwd_k(const PsiConst& P) { return (P.m + P.d + 3) / 4 * 4; }  // chunk-matrix columns, 16-byte rows
+inline int bwd_ldg(const PsiConst& P) { return (P.m + 3) / 4 * 4; }
+inline int64_t rows_pad(const PsiConst& P) { return (P.n + kSub - 1) / kSub * kSub; }
+
+// The forward's split Knm tiles are kept for the backward (one less exp pass per evaluation) while
+// they fit the budget: N x (M + D) x 8 bytes + the (x', x'^2) rows; 64 GiB by default (the C4 shape
+// at N = 10M takes 41 GB of the 180 GB), SGPX_SYRK_CACHE_GIB overrides (0 = always recompute).
+// A pure function of the shapes, so the forward and backward plans agree.
+bool syrk_cached(const PsiConst& P) {
+  double gib = 64.0;
+  if (const char* e = getenv("SGPX_SYRK_CACHE_GIB")) gib = atof(e);
+  const double bytes = double(rows_pad(P)) * (double(bwd_k(P)) * 8.0 + double(syrk_q(P.q)) * 16.0);
+  return bytes <= gib * 1073741824.0;
+}
+
+// Forward region (the backward reads its cache through BwdConst::fwd_rt): [big | small | xp] first,
+// sized for all rows when cached, else one chunk each (xp unused); then the batched GEMM output,
+// the fp64 accumulator and the per-row scalars.
 struct SyrkFwd {
-  int64_t ncols, off_big, off_small, off_c, off_acc, off_rows, doubles;
+  int64_t ncols, off_big, off_small, off_xp, off_c, off_acc, off_rows, doubles;
   int nrb;
+  bool cached;
 };
 SyrkFwd fwd_layout(const PsiConst& P, int num_sms) {
   SyrkFwd L{};
-  L.ncols = P.m + P.d;
-  const int64_t chunk_floats = kChunk * L.ncols;
+  L.cached = syrk_cached(P);
+  L.ncols = bwd_k(P);
+  const int64_t rows = L.cached ? rows_pad(P) : kChunk;
+  const int64_t mat_doubles = (rows * L.ncols + 1) / 2 / 2 * 2 + 2;  // floats -> doubles, 16-byte multiple
   L.off_big = 0;
-  L.off_small = L.off_big + (chunk_floats + 1) / 2;
-  L.off_c = L.off_small + (chunk_floats + 1) / 2;
-  L.off_acc = L.off_c + (int64_t(kBatch) * P.m * L.ncols + 1) / 2;
-  L.off_rows = L.off_acc + int64_t(P.m) * L.ncols;
+  L.off_small = L.off_big + mat_doubles;
+  L.off_xp = L.off_small + mat_doubles;
+  L.off_c = L.off_xp + (L.cached ? 2 * rows * syrk_q(P.q) : 0);
+  L.off_acc = L.off_c + (int64_t(kBatch) * P.m * (P.m + P.d) + 1) / 2;
+  L.off_rows = L.off_acc + int64_t(P.m) * (P.m + P.d);
   L.nrb = int(std::max<int64_t>(1, std::min<int64_t>((P.n + 255) / 256, 2 * int64_t(num_sms))));
   L.doubles = L.off_rows + L.nrb + 4;
   return L;
@@ -451,33 +481,26 @@ struct SyrkBwd {
   int64_t off_abig, off_asmall, off_bbig, off_bsmall, off_g, off_rows, off_os, off_acc, off_xp, doubles;
   int nby;
 };
-inline int bwd_k(const PsiConst& P) { return (P.m + P.d + 3) / 4 * 4; }  // padded: 16-byte aligned ldb
-inline int bwd_ldg(const PsiConst& P) { return (P.m + 3) / 4 * 4; }
 SyrkBwd bwd_layout(const PsiConst& P, int q) {
   SyrkBwd L{};
   const int64_t k = bwd_k(P);
+  const bool own = !syrk_cached(P);  // the chunk matrices and x' rows, when the forward keeps none
   L.nby = int((kChunk + kRedRows - 1) / kRedRows);
   L.off_abig = 0;
-  L.off_asmall = L.off_abig + (kChunk * k + 1) / 2;
-  L.off_bbig = L.off_asmall + (kChunk * k + 1) / 2;
+  L.off_asmall = L.off_abig + (own ? (kChunk * k + 1) / 2 : 0);
+  L.off_bbig = L.off_asmall + (own ? (kChunk * k + 1) / 2 : 0);
   L.off_bsmall = L.off_bbig + (k * P.m + 1) / 2;
   L.off_g = L.off_bsmall + (k * P.m + 1) / 2;
   L.off_rows = L.off_g + (kChunk * bwd_ldg(P) + 1) / 2;
   L.off_os = L.off_rows + int64_t(L.nby) * P.m * q;  // oz (Q x nby x M), then os ((1 + Q) x nby x nbx)
   L.off_acc = L.off_os + int64_t(1 + q) * L.nby * ((P.m + 31) / 32);
   L.off_xp = (L.off_acc + 1 + P.q + int64_t(P.m) * P.q + 1) / 2 * 2;  // 16-byte aligned
-  L.doubles = L.off_xp + 2 * kChunk * q + 4;
+  L.doubles = L.off_xp + (own ? 2 * kChunk * q : 0) + 4;
   return L;
 }
 
 float* as_floats(double* p) { return reinterpret_cast<float*>(p); }
 
-constexpr int kSyrkQs[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24, 32, 48, 64};
-int syrk_q(int q) {
-  for (int v : kSyrkQs)
-    if (v >= q) return v;
-  return -1;
-}
 
 template <int Q>
 int syrk_backward_q(const PsiConst& P, const BwdConst& B, double* base, double* packed, int num_sms,
@@ -492,23 +515,36 @@ int syrk_backward_q(const PsiConst& P, const BwdConst& B, double* base, double* 
   const int64_t count = 1 + P.q + int64_t(P.m) * P.q;
   cudaMemsetAsync(acc, 0, sizeof(double) * count, st);
   g_tc_launches.fetch_add(1);
+  const bool cached = syrk_cached(P);
+  double* fbase = const_cast<double*>(B.fwd_rt);
+  const SyrkFwd F = fwd_layout(P, num_sms);
   for (int64_t n0 = 0; n0 < P.n; n0 += kChunk) {
-    const int64_t nc = std::min<int64_t>(kChunk, (P.n - n0 + 3) / 4 * 4);
-    knm_split_kernel<Q><<<dim3(unsigned((nc + 255) / 256), unsigned((k + kCols - 1) / kCols)), 256, 0, st>>>(
-        P, n0, nc, k, as_floats(base + L.off_abig), as_floats(base + L.off_asmall),
-        reinterpret_cast<double2*>(base + L.off_xp));
-    g_tc_launches.fetch_add(1);
+    float *kb, *ks;
+    double2* xp;
+    int64_t nc;
+    if (cached) {  // the forward's tiles: its chunk geometry (whole kSub sub-chunks)
+      nc = std::min<int64_t>(kChunk, (P.n - n0 + kSub - 1) / kSub * kSub);
+      kb = as_floats(fbase + F.off_big) + n0 * k;
+      ks = as_floats(fbase + F.off_small) + n0 * k;
+      xp = reinterpret_cast<double2*>(fbase + F.off_xp) + n0 * Q;
+    } else {
+      nc = std::min<int64_t>(kChunk, (P.n - n0 + 3) / 4 * 4);
+      kb = as_floats(base + L.off_abig);
+      ks = as_floats(base + L.off_asmall);
+      xp = reinterpret_cast<double2*>(base + L.off_xp);
+      knm_split_kernel<Q><<<dim3(unsigned((nc + 255) / 256), unsigned((k + kCols - 1) / kCols)), 256, 0, st>>>(
+          P, n0, nc, k, kb, ks, xp);
+      g_tc_launches.fetch_add(1);
+    }
     // G^T (M x nc) = [2U ; dPsi^T ; 0]^T (M x k) . [K | Y | 0]^T (k x nc)
     const int ldg = bwd_ldg(P);
     if (gemm3(h, st, CUBLAS_OP_T, CUBLAS_OP_T, P.m, int(nc), k, as_floats(base + L.off_bbig),
-              as_floats(base + L.off_bsmall), k, as_floats(base + L.off_abig), as_floats(base + L.off_asmall),
-              int(nc), as_floats(base + L.off_g), ldg))
+              as_floats(base + L.off_bsmall), k, kb, ks, int(nc), as_floats(base + L.off_g), ldg))
       return 3;
     const int nby = int((nc + kRedRows - 1) / kRedRows);
     const int nbx = (P.m + 31) / 32;
     syrk_reduce_kernel<Q><<<dim3(unsigned(nbx), unsigned(nby)), 256, 0, st>>>(
-        P, n0, nc, as_floats(base + L.off_abig), as_floats(base + L.off_asmall), as_floats(base + L.off_g), ldg,
-        reinterpret_cast<const double2*>(base + L.off_xp), base + L.off_rows, base + L.off_os);
+        P, n0, nc, kb, ks, as_floats(base + L.off_g), ldg, xp, base + L.off_rows, base + L.off_os);
     syrk_fold_dz_kernel<<<int(std::min<int64_t>((int64_t(P.m) * P.q + 255) / 256, 256)), 256, 0, st>>>(
         P.m, P.q, nby, base + L.off_rows, acc);
     syrk_fold_sc_kernel<<<1 + P.q, 256, 0, st>>>(nby * nbx, base + L.off_os, acc);
@@ -526,7 +562,7 @@ int syrk_forward_q(const PsiConst& P, double* base, double* packed, int* err_fla
   cublasHandle_t h = handle_for_device();
   if (!h) return 3;
   double* acc = base + L.off_acc;
-  const int64_t ccount = int64_t(P.m) * L.ncols;
+  const int64_t ccount = int64_t(P.m) * (P.m + P.d);
   cudaMemsetAsync(acc, 0, sizeof(double) * ccount, st);
   syrk_rows_kernel<<<L.nrb, 256, 0, st>>>(P, base + L.off_rows, err_flag);
   g_tc_launches.fetch_add(1);
@@ -534,13 +570,14 @@ int syrk_forward_q(const PsiConst& P, double* base, double* packed, int* err_fla
     // whole sub-chunks (zero rows past N contribute nothing)
     const int64_t nc = std::min<int64_t>(kChunk, (P.n - n0 + kSub - 1) / kSub * kSub);
     const int nb = int(nc / kSub);
+    float* kb = as_floats(base + L.off_big) + (L.cached ? n0 * L.ncols : 0);
+    float* ks = as_floats(base + L.off_small) + (L.cached ? n0 * L.ncols : 0);
+    double2* xp = L.cached ? reinterpret_cast<double2*>(base + L.off_xp) + n0 * Q : nullptr;
     knm_split_kernel<Q><<<dim3(unsigned((nc + 255) / 256), unsigned((L.ncols + kCols - 1) / kCols)), 256, 0, st>>>(
-        P, n0, nc, int(L.ncols), as_floats(base + L.off_big), as_floats(base + L.off_small), nullptr);
+        P, n0, nc, int(L.ncols), kb, ks, xp);
     g_tc_launches.fetch_add(1);
     // C_i (M x (M + D)) = K_i^T [K_i | Y_i] per sub-chunk i: A = the first M columns of the chunk matrix
-    if (gemm3_batched_t(h, st, P.m, int(L.ncols), nb, int(nc), as_floats(base + L.off_big),
-                        as_floats(base + L.off_small), as_floats(base + L.off_c)))
-      return 3;
+    if (gemm3_batched_t(h, st, P.m, P.m + P.d, nb, int(nc), kb, ks, as_floats(base + L.off_c))) return 3;
     acc_add_kernel<<<int(std::min<int64_t>((ccount + 255) / 256, 1024)), 256, 0, st>>>(
         acc, as_floats(base + L.off_c), nb, ccount);
     g_tc_launches.fetch_add(1);
