@@ -8,7 +8,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsgpx.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("psi_kernels.cu", "psi_direct.cu", "psi1_kernels.cu", "psi1_tile.cu", "psi_rowtile.cu", "sgpx_api.cu",
+SOURCES = [os.path.join(CSRC, f) for f in ("psi_kernels.cu", "psi_direct.cu", "psi1_kernels.cu", "psi1_tile.cu", "psi1_tc.cu", "psi_rowtile.cu", "sgpx_api.cu",
                                             "synth.cu", "dla.cu", "dcoord.cu", "fit.cu", "syrk.cu",
                                             "coordinator.cpp")]
 HEADERS = [os.path.join(CSRC, f) for f in ("psi_kernels.cuh", "psi_common.cuh", "tc_util.cuh", "coordinator.hpp", "dla.cuh", "dcoord.cuh")] + [

@@ -322,6 +322,7 @@ int launch_psi1_bwd_q(const PsiConst& P, const BwdConst& B, double* part_rows, i
 
 // Partial rows the psi1 kernels write (callers size their partial buffers with these).
 int psi1_fwd_rows(const PsiConst& P, int num_sms) {
+  if (psi1_tc_supported(P, false)) return psi1_tc_rows(P, num_sms, false);
   if (psi1_tile_supported(P, false)) return psi1_tile_rows(P, num_sms);
   const int64_t nchunks = (P.n + 31) / 32;
   return int(std::min<int64_t>(nchunks, int64_t(num_sms) * 2));
@@ -331,6 +332,7 @@ int psi1_bwd_ctas(const PsiConst& P, int num_sms) {
   return int(std::max<int64_t>(1, std::min<int64_t>((nwchunks + 7) / 8, int64_t(num_sms) * 3)));
 }
 int psi1_bwd_rows(const PsiConst& P, int num_sms) {
+  if (psi1_tc_supported(P, true)) return psi1_tc_rows(P, num_sms, true);
   if (psi1_tile_supported(P, true)) return std::max(1, psi1_tile_rows(P, num_sms));
   return 8 * psi1_bwd_ctas(P, num_sms);
 }
@@ -355,12 +357,14 @@ int psi1_bwd_rows(const PsiConst& P, int num_sms) {
 
 int psi1_forward(const PsiConst& P, double* part_rows, int64_t pstride, int rows, int* err_flag, void* stream,
                  int with_kl) {
+  if (psi1_tc_supported(P, false)) return psi1_tc_forward(P, part_rows, pstride, rows, err_flag, with_kl, stream);
   if (psi1_tile_supported(P, false)) return psi1_tile_forward(P, part_rows, pstride, rows, err_flag, with_kl, stream);
   SGPX_P1_DISPATCH(launch_psi1_fwd_q, P, part_rows, pstride, rows, err_flag, static_cast<cudaStream_t>(stream), with_kl)
 }
 
 int psi1_backward(const PsiConst& P, const BwdConst& B, double* part_rows, int64_t pstride, int rows,
                   void* stream) {
+  if (psi1_tc_supported(P, true)) return psi1_tc_backward(P, B, part_rows, pstride, rows, stream);
   if (psi1_tile_supported(P, true)) return psi1_tile_backward(P, B, part_rows, pstride, rows, stream);
   const int ctas = rows / 8;
   SGPX_P1_DISPATCH(launch_psi1_bwd_q, P, B, part_rows, pstride, ctas, static_cast<cudaStream_t>(stream))

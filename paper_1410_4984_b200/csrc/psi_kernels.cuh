@@ -127,6 +127,12 @@ int psi1_fwd_rows(const PsiConst& P, int num_sms);
 int psi1_bwd_ctas(const PsiConst& P, int num_sms);
 int psi1_bwd_rows(const PsiConst& P, int num_sms);
 bool psi1_tile_supported(const PsiConst& P, bool bwd);
+// tcgen05 psi1 (psi1_tc.cu): M <= 128, D <= 128 forward / D <= 64 backward; SGPX_PSI1=simt disables
+bool psi1_tc_supported(const PsiConst& P, bool bwd);
+int psi1_tc_rows(const PsiConst& P, int num_sms, bool bwd);
+int psi1_tc_forward(const PsiConst& P, double* part, int64_t pstride, int rows, int* err_flag, int with_kl,
+                    void* stream);
+int psi1_tc_backward(const PsiConst& P, const BwdConst& B, double* part, int64_t pstride, int rows, void* stream);
 int psi1_tile_rows(const PsiConst& P, int num_sms);
 int psi1_tile_forward(const PsiConst& P, double* part, int64_t pstride, int rows, int* err_flag, int with_kl,
                       void* stream);
