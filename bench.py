@@ -56,6 +56,9 @@ DTYPES = {
     "precise": "mixed: psi2 exponents as 3-piece fp16 tcgen05 MMAs (~2^-33), exp2 on MUFU/FMA (2^-22), "
                "scaled-fp16 hi-lo contraction MMAs (~2^-22), psi1 fp32, every sum and all M-sized algebra fp64",
     "direct": "f64: direct-difference exponents, exp and every contraction and sum in fp64",
+    "syrk": "mixed: Knm from fp64 exponents split into tf32 hi/lo; Phi = K^T K, Psi = K^T Y and G = [K|Y][2U; dPsi^T] "
+            "as three-pass split-TF32 tcgen05 GEMMs (cuBLAS), fp32 accumulation over 512-row sub-chunks, fp64 "
+            "across; every gradient contraction and all M-sized algebra fp64",
 }
 
 
@@ -383,6 +386,24 @@ def run_b200(args, world, rank, local_rank):
         roof["mufu_floor"] = {"exps_per_launch": exps, "floor_ms": 0.75 * exps / EX2_RATE * 1e3,
                               "frac": 0.75 * exps / EX2_RATE / k2b_s,
                               "note": "3 of 4 exp2 on MUFU.EX2 (16/clk/SM at 1965 MHz), 1 of 4 on the FMA pipe"}
+    if mode == "syrk":  # the Knm-tile path: its backward pass (split tiles reused, GEMM, contraction)
+        kk = (m + d + 3) // 4 * 4
+        alg = 2.0 * n_local * m * (m + d)
+        ex = 3 * 2.0 * n_local * m * kk
+        tf32_peak = t_peak / 2
+        roof = {
+            "bound": "tensor", "kernel": "SYRK backward pass: split-TF32 G = [K|Y][2U; dPsi^T] GEMMs (cuBLAS, "
+                                         "tcgen05) + syrk_reduce_kernel (H = G o K contractions)",
+            "achieved": alg / bwd_s / 1e12 if bwd_s > 0 else None, "peak": tf32_peak, "unit": "TFLOP/s",
+            "frac": alg / bwd_s / 1e12 / tf32_peak if bwd_s > 0 else None, "traffic": None,
+            "peak_source": t_src + " / 2 (dense tf32 = half the bf16 rate)", "flops_per_launch": alg,
+            "avg_launch_ms": bwd_s * 1e3,
+            "work": "2 N M (M + D): the one exact GEMM the backward stands for (FMA = 2)",
+            "executed_mma": {"tflops": ex / bwd_s / 1e12 if bwd_s > 0 else None,
+                             "frac_of_peak": ex / bwd_s / 1e12 / tf32_peak if bwd_s > 0 else None,
+                             "flops_per_launch": ex, "note": "three tf32 piece products, inner dimension "
+                                                             "M + D padded to a multiple of 4"},
+        }
     tpath = os.path.join(ROOT, "profiles", "r02_traffic.json")
     if os.path.exists(tpath):
         try:

@@ -43,16 +43,18 @@
  *       fast     psi2 exponents as a bilinear form on tcgen05 (two fp16 pieces, ~2^-22
  *                relative on the feature products), G = 2^D on MUFU.EX2 / FMA (2^-22), the
  *                psi2 contraction as 16-bit split MMAs (bf16 hi/lo ~2^-17 forward, scaled fp16
- *                hi/lo ~2^-22 backward), psi1 in fp32 tiles;
+ *                hi/lo ~2^-22 backward); psi1 weights in fp32 (direct differences), its
+ *                Psi = G^T Y and Y dPsi^T contractions as three-pass split-tf32 tcgen05 MMAs;
  *       precise  as fast with three fp16 exponent pieces (~2^-33) and fp16 forward MMA3 pieces;
  *       direct   direct-difference exponents and exp in fp64 (the reference's own form, ~1 ulp),
  *                fp64 contractions;
  *       syrk     (deterministic inputs; the AUTO choice there) Knm tiles in fp64, Phi = K^T K,
  *                Psi = K^T Y and dL/dK = 2 K U + Y dPsi^T as split-TF32 tensor-core GEMMs (three
- *                passes, ~2^-21 per product, fp32 within a 16k-row chunk, fp64 across chunks),
+ *                passes, ~2^-21 per product, fp32 within 512-row sub-chunks, fp64 across them),
  *                the gradient contraction in fp64;
  *     every sum across datapoints and across CTAs is fp64, all M-sized algebra is fp64.  AUTO
- *     picks fast / precise / direct from the spread of the inducing points.
+ *     picks syrk for deterministic inputs and fast / precise / direct for latent inputs from the
+ *     spread of the inducing points.
  *   - There is no CPU fallback: without a CUDA device every compute entry point
  *     returns SGPX_CUDA.
  */
@@ -154,7 +156,7 @@ int sgpx_ctx_synchronize(sgpx_ctx* ctx);
 int64_t sgpx_ctx_launch_count(const sgpx_ctx* ctx);
 /* Precision mode of the one-shot entry points (sgpx_sweep_stats); SGPX_PREC_AUTO by default. */
 int sgpx_ctx_set_precision(sgpx_ctx* ctx, int precision);
-/* Mode the last sgpx_sweep_stats of this context ran in (SGPX_PREC_FAST / PRECISE / DIRECT; 0 if
+/* Mode the last sgpx_sweep_stats of this context ran in (SGPX_PREC_FAST / PRECISE / DIRECT / SYRK; 0 if
  * none) and, optionally, the inducing-point spread Tz that decided it. */
 int sgpx_ctx_last_precision(const sgpx_ctx* ctx, double* z_spread);
 
@@ -226,7 +228,7 @@ typedef struct {
   double stats_pass_s, coordinator_s, grad_pass_s, wall_s;
   double fwd_kernel_s, bwd_kernel_s; /* the psi forward / backward kernels alone */
   int fwd_grid, bwd_grid;            /* persistent CTAs launched */
-  int precision_used;                /* SGPX_PREC_FAST / PRECISE / DIRECT of this evaluation */
+  int precision_used;                /* SGPX_PREC_FAST / PRECISE / DIRECT / SYRK of this evaluation */
   double z_spread;                   /* Tz = max_a sum_q ((z_aq - c_q) / l_q)^2, c = mean of Z */
   double psi2_fwd_kernel_s, psi2_bwd_kernel_s; /* the main psi2 kernel of each pass alone (first sub-shard) */
 } sgpx_eval_result;
