@@ -383,9 +383,9 @@ def run_b200(args, world, rank, local_rank):
                                 "note": "tensor-pipe work the kernel issues: MMA1 exponent pieces + MMA3 hi/lo "
                                         "contraction products"}
         exps = n_local * p
-        roof["mufu_floor"] = {"exps_per_launch": exps, "floor_ms": 0.75 * exps / EX2_RATE * 1e3,
-                              "frac": 0.75 * exps / EX2_RATE / k2b_s,
-                              "note": "3 of 4 exp2 on MUFU.EX2 (16/clk/SM at 1965 MHz), 1 of 4 on the FMA pipe"}
+        roof["mufu_floor"] = {"exps_per_launch": exps, "floor_ms": exps / EX2_RATE * 1e3,
+                              "frac": exps / EX2_RATE / k2b_s,
+                              "note": "every exp2 on MUFU.EX2 (16/clk/SM at 1965 MHz)"}
     if mode == "syrk":  # the Knm-tile path: its backward pass (split tiles reused, GEMM, contraction)
         kk = (m + d + 3) // 4 * 4
         alg = 2.0 * n_local * m * (m + d)

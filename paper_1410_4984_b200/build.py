@@ -33,6 +33,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(CSRC, os.path.basename(src) + ".o")
         cmd = [NVCC, "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-O3,-march=x86-64-v3", "-x",
                "cu" if src.endswith(".cu") else "c++", "-c", src, "-o", obj]
+        cmd[1:1] = os.environ.get("SGPX_NVCC_DEFS", "").split()  # experiment builds (-DNAME=value)
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         cmds.append(cmd)

@@ -21,7 +21,7 @@
 //
 // Both passes are one kernel template: a static 128-row tile (A of MMA1) in shared memory, a
 // ring of streamed 96-row chunks (B of MMA1 + B of MMA3, fed by 1D TMA bulk copies), MMA1 into a
-// double-buffered TMEM stage, 12 consumer warps turning D into G = 2^D (MUFU.EX2 + an FMA-pipe
+// double-buffered TMEM stage, 12 consumer warps turning D into G = 2^D (MUFU.EX2; round 1 put 1 of 4 on an FMA-pipe
 // polynomial) stored back to TMEM as 16-bit hi/lo pairs, MMA3 with A = G read from TMEM, and the MMA3
 // accumulator drained into fp64 registers every chunk.  Every GEMM is a 3-piece split
 // (hi*hi + hi*lo + lo*hi) of 16-bit pieces: MMA1 fp16 (~2^-22 relative, features clamped to the
@@ -43,6 +43,10 @@
 #include "psi_kernels.cuh"
 #include "tc_util.cuh"
 
+#ifndef SGPX_RT_POLY
+#define SGPX_RT_POLY 0
+#endif
+
 namespace sgpx {
 extern std::atomic<int64_t> g_tc_launches;
 
@@ -58,6 +62,7 @@ constexpr int kWarpMma = kWarpLoad + 1;           // MMA warp (17)
 constexpr int kThreads = kCons + kDrain + 64;
 constexpr int kPadRows = 768;           // feature-array row padding: lcm(kCH, 2 x 128)
 constexpr float kNegHuge = -6.0e4f;     // B_n of padded datapoints (fp16-representable): 2^-6e4 = 0
+constexpr int kPolyShare = SGPX_RT_POLY;  // exponentials on the FMA pipe: 0 none, 8 one in 8, 4 one in 4 (round 1)
 constexpr float kHalfMax = 6.0e4f;      // exponent features are clamped to the fp16 range
 
 // MMA3 operands G = 2^D and Y as 16-bit hi / lo pieces (G packed in place of D, kind::f16 with A
@@ -132,6 +137,20 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   uint32_t d;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(b), "f"(a));
   return d;
+}
+
+// fp16 hi / lo split of two floats: hi = f16x2(a, b), lo = f16x2(a - hi.a, b - hi.b).  Written with the
+// packed cvt and a b16 split so ptxas reads the halves with HADD2.F32 .H0 / .H1 selectors (3
+// instructions per value; the __half2 intrinsics cost ~2 extra PRMT per value).
+__device__ __forceinline__ void split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  uint32_t h;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));
+  float ha, hb;
+  asm("{.reg .b16 l, u; mov.b32 {l, u}, %2; cvt.f32.f16 %0, l; cvt.f32.f16 %1, u;}" : "=f"(ha), "=f"(hb) : "r"(h));
+  uint32_t l2;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l2) : "f"(b - hb), "f"(a - ha));
+  hi = h;
+  lo = l2;
 }
 
 __device__ __forceinline__ uint32_t h2u(__half2 h) {
@@ -817,11 +836,13 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
             v[3] = __uint_as_float(r[i + 3]);
             return;
           }
-          // 3 of 4 exponentials on MUFU.EX2, 1 of 4 on the FMA pipe
+          // every exponential on MUFU.EX2 (issue-bound consumers: the FMA-pipe polynomial cost
+          // ~11 instructions where MUFU takes one, and MUFU stays below its 16/clk/SM rate)
           v[0] = ex2(__uint_as_float(r[i]));
           v[1] = ex2(__uint_as_float(r[i + 1]));
           v[2] = ex2(__uint_as_float(r[i + 2]));
-          v[3] = ex2_poly(__uint_as_float(r[i + 3]));
+          const bool poly = kPolyShare == 4 || (kPolyShare == 8 && (i & 4));
+          v[3] = poly ? ex2_poly(__uint_as_float(r[i + 3])) : ex2(__uint_as_float(r[i + 3]));
         };
         uint32_t hi[16], lo[16];
         auto half = [&](const uint32_t (&r)[16], int base) {
@@ -837,10 +858,7 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
                 hi[base + (i + u) / 2] = h;
                 lo[base + (i + u) / 2] = pack_bf16x2(e0, e1);
               } else {
-                const __half2 h = __floats2half2_rn(v[u], v[u + 1]);
-                const float2 hf = __half22float2(h);
-                hi[base + (i + u) / 2] = h2u(h);
-                lo[base + (i + u) / 2] = h2u(__floats2half2_rn(v[u] - hf.x, v[u + 1] - hf.y));
+                split_f16x2(v[u], v[u + 1], hi[base + (i + u) / 2], lo[base + (i + u) / 2]);
               }
             }
           }

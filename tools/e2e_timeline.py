@@ -14,8 +14,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
 
-import bench  # noqa: E402
-from paper_1410_4984_b200 import sgp  # noqa: E402
+from paper_1410_4984_b200 import sgp, synthetic  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=1_000_000)
@@ -24,11 +23,12 @@ ap.add_argument("--d", type=int, default=50)
 ap.add_argument("--m", type=int, default=100)
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
-mu, s, y, z = bench.synth_shard(a.n, a.q, a.d, a.m, 0, a.n, dev)
+w = synthetic.make(True, a.n, a.q, a.d, a.m, seed=0, device=dev)
+mu, s, y, z = w.mu, w.s, w.y, w.z
 ctx = sgp.Context(0)
 ctx.set_stream(torch.cuda.current_stream().cuda_stream)
 eng = sgp.Engine(sgp.ModelKind.latent, mu, s, y, ctx=ctx)
-kern = sgp.KernelSpec(1.0, np.ones(a.q))
+kern = w.kernel
 mu_h = torch.empty(a.q, a.n, dtype=torch.float64, pin_memory=True)
 s_h = torch.empty(a.q, a.n, dtype=torch.float64, pin_memory=True)
 mu_h.copy_(mu.t())
@@ -38,11 +38,11 @@ gmu_h = torch.empty(a.q, a.n, dtype=torch.float64, pin_memory=True)
 gs_h = torch.empty(a.q, a.n, dtype=torch.float64, pin_memory=True)
 eng.set_local_grads_out(gmu_h.numpy().T, gs_h.numpy().T)
 for _ in range(3):
-    eng.broadcast(kern, 100.0, z, mu_np, s_np)
+    eng.broadcast(kern, w.beta, z, mu_np, s_np)
     eng.evaluate(True)
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
-    eng.broadcast(kern, 100.0, z, mu_np, s_np)
+    eng.broadcast(kern, w.beta, z, mu_np, s_np)
     r = eng.evaluate(True)
     torch.cuda.synchronize()
 events = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
