@@ -11,7 +11,7 @@ LIB = os.path.join(PKG, "libsgpx.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("psi_kernels.cu", "psi_direct.cu", "psi1_kernels.cu", "psi1_tile.cu", "psi1_tc.cu", "psi_rowtile.cu", "sgpx_api.cu",
                                             "synth.cu", "dla.cu", "dcoord.cu", "fit.cu", "syrk.cu",
                                             "coordinator.cpp")]
-HEADERS = [os.path.join(CSRC, f) for f in ("psi_kernels.cuh", "psi_common.cuh", "tc_util.cuh", "coordinator.hpp", "dla.cuh", "dcoord.cuh")] + [
+HEADERS = [os.path.join(CSRC, f) for f in ("fp16_pieces.cuh", "psi_kernels.cuh", "psi_common.cuh", "tc_util.cuh", "coordinator.hpp", "dla.cuh", "dcoord.cuh")] + [
     os.path.join(ROOT, "include", "sgpx.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

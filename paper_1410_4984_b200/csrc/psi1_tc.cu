@@ -395,8 +395,8 @@ __host__ __device__ inline BwdSmem bwd_smem(int q, int d, int m) {
   big = big > rsh_bytes ? big : rsh_bytes;
   L.pb = (big + 127) / 128 * 128;                         // [piece][mp x dk]
   L.zs = L.pb + 2 * L.mp * L.dk * 4;                      // z [q][mp] and z^2 [q][mp]
-  L.hs = L.zs + 2 * q * L.mp * 4;                         // H [128][2q]: d1 mu, d1
-  L.ts = L.hs + kBwdN * 2 * q * 4;                        // T quarters [4][128][nh]
+  L.hs = L.zs + 2 * q * L.mp * 4;                         // H [128][2 q4]: d1 mu at 0, d1 at q4 (q4 = q rounded to 4)
+  L.ts = L.hs + kBwdN * 2 * ((q + 3) / 4 * 4) * 4;        // T quarters [4][128][nh]
   L.mus = L.ts + 4 * kBwdN * nh * 4;                      // [q][128]
   L.d1s = L.mus + q * kBwdN * 4;
   L.bar = (L.d1s + q * kBwdN * 4 + 15) / 16 * 16;
@@ -408,7 +408,7 @@ template <int Q>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     psi1_bwd_tc_kernel(PsiConst P, BwdConst B, int64_t nchunks, double* __restrict__ part, int64_t pstride) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  constexpr int NH = 1 + 2 * Q, KQ = (2 * Q + 3) / 4, NT = kBwdThreads;
+  constexpr int NH = 1 + 2 * Q, Q4 = (Q + 3) / 4 * 4, NT = kBwdThreads;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int d = P.d, m = P.m;
   const BwdSmem L = bwd_smem(Q, d, m);
@@ -451,11 +451,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // consumer role: datapoint row cn (TMEM lane), inducing-point quarter ch
   const int wq = warp & 3, ch = warp >> 2, cn = 32 * wq + lane;
   const int mqw = mp / 4, mb0 = ch * mqw;
-  // R role: inducing point rm, H columns [kq KQ, (kq + 1) KQ)
-  const int rm = tid & 127, kq = tid >> 7;
-  double racc[KQ];
+  // R role: inducing point rm, half rh of H (d1 mu or d1), half rn of each chunk's datapoints
+  const int rm = tid & 127, rh = (tid >> 7) & 1, rn = tid >> 8;
+  double racc[Q];
 #pragma unroll
-  for (int k = 0; k < KQ; ++k) racc[k] = 0.0;
+  for (int k = 0; k < Q; ++k) racc[k] = 0.0;
   // epilogue role: a fixed latent dimension per thread (threads past Q * (NT / Q) idle)
   const int eq = tid % Q;
   const bool ework = tid < Q * (NT / Q);
@@ -486,8 +486,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       mus[q * kBwdN + nl] = mu;
       d1s[q * kBwdN + nl] = d1;
-      hs[nl * 2 * Q + q] = d1 * mu;
-      hs[nl * 2 * Q + Q + q] = d1;
+      hs[nl * 2 * Q4 + q] = d1 * mu;
+      hs[nl * 2 * Q4 + Q4 + q] = d1;
     }
     tc::fence_async_smem();
     tc::fence_before();
@@ -524,32 +524,49 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     tc::mbar_wait(&bar[0], uint32_t(local & 1));
     tc::fence_after();
     __syncthreads();  // every warp past the wait: the Y pieces are dead, G may overwrite them
-    // G_nm = v1_nm C_nm over this thread's inducing points; T_n quarter in registers
+    // G_nm = v1_nm C_nm over this thread's inducing points, 8 at a time with z / z^2 read as 16-byte
+    // vectors (q outer); T_n quarter in registers
     float t0 = 0.f, t1[Q], t2[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) t1[q] = t2[q] = 0.f;
     for (int cb = 0; cb < mqw; cb += 8) {
+      const int mb = mb0 + cb;
       uint32_t r[8];
-      tc::ld8(tmem + (uint32_t(32 * wq) << 16) + uint32_t(mb0 + cb), r);
+      tc::ld8(tmem + (uint32_t(32 * wq) << 16) + uint32_t(mb), r);
+      float e[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) e[j] = 0.f;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const float4 za = *reinterpret_cast<const float4*>(zs + q * mp + mb);
+        const float4 zb = *reinterpret_cast<const float4*>(zs + q * mp + mb + 4);
+        const float zv[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float df = mu[q] - zv[j];
+          e[j] = fmaf(df * df, d1[q], e[j]);
+        }
+      }
       tc::ld_wait();
+      float g[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int mm = mb0 + cb + j;
-        float e = 0.f;
+        g[j] = mb + j < m ? __uint_as_float(r[j]) * ex2(fmaf(-0.5f * kLog2e, e[j], b1)) : 0.f;
+        gs[cn * gst + mb + j] = g[j];
+        t0 += g[j];
+      }
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          const float df = mu[q] - zs[q * mp + mm];
-          e = fmaf(df * df, d1[q], e);
-        }
-        const float g = mm < m ? __uint_as_float(r[j]) * ex2(fmaf(-0.5f * kLog2e, e, b1)) : 0.f;
-        gs[cn * gst + mm] = g;
-        t0 += g;
+      for (int q = 0; q < Q; ++q) {
+        const float4 za = *reinterpret_cast<const float4*>(zs + q * mp + mb);
+        const float4 zb = *reinterpret_cast<const float4*>(zs + q * mp + mb + 4);
+        const float4 wa = *reinterpret_cast<const float4*>(zs + (Q + q) * mp + mb);
+        const float4 wb = *reinterpret_cast<const float4*>(zs + (Q + q) * mp + mb + 4);
+        const float zv[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
+        const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          const float zq = zs[q * mp + mm];
-          const float gz = g * zq;
-          t1[q] += gz;
-          t2[q] = fmaf(gz, zq, t2[q]);
+        for (int j = 0; j < 8; ++j) {
+          t1[q] = fmaf(g[j], zv[j], t1[q]);
+          t2[q] = fmaf(g[j], wv[j], t2[q]);
         }
       }
     }
@@ -564,23 +581,29 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     tc::fence_before();
     __syncthreads();
-    // R_mk += sum_n G_nm H_nk  (fp32 over the chunk, fp64 across chunks)
+    // R_mk += sum_n G_nm H_nk over this thread's half of the datapoints (fp32 over 64 datapoints,
+    // fp64 across chunks; the two datapoint halves added in order at the end)
     {
-      float rr[KQ];
+      float rr[Q];
 #pragma unroll
-      for (int k = 0; k < KQ; ++k) rr[k] = 0.f;
+      for (int k = 0; k < Q; ++k) rr[k] = 0.f;
       if (rm < m) {
 #pragma unroll 2
-        for (int nl = 0; nl < kBwdN; ++nl) {
+        for (int nl = rn * (kBwdN / 2); nl < (rn + 1) * (kBwdN / 2); ++nl) {
           const float g = gs[nl * gst + rm];
-          const float* hr = hs + nl * 2 * Q + kq * KQ;
+          const float* hr = hs + nl * 2 * Q4 + rh * Q4;
 #pragma unroll
-          for (int k = 0; k < KQ; ++k)
-            if (kq * KQ + k < 2 * Q) rr[k] = fmaf(g, hr[k], rr[k]);
+          for (int k4 = 0; k4 < Q4; k4 += 4) {
+            const float4 h4 = *reinterpret_cast<const float4*>(hr + k4);
+            const float hv[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (k4 + u < Q) rr[k4 + u] = fmaf(g, hv[u], rr[k4 + u]);
+          }
         }
       }
 #pragma unroll
-      for (int k = 0; k < KQ; ++k) racc[k] += double(rr[k]);
+      for (int k = 0; k < Q; ++k) racc[k] += double(rr[k]);
     }
     // per-datapoint epilogue (psi_stats.hpp:200-219): d mu, d S (+ KL), d l, d var
     if (ework && eq < P.q) {
@@ -616,11 +639,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     tc::fence_before();
     __syncthreads();
   }
-  // d z_mq = R_mq - z_mq R_m(Q+q)   (psi_stats.hpp:214), exchanged through shared memory
+  // d z_mq = R_mq - z_mq R_m(Q+q)   (psi_stats.hpp:214), exchanged through shared memory: the two
+  // datapoint halves of each R_mk added in order
   double* rsh = reinterpret_cast<double*>(smem + L.ya);  // [2Q][128] doubles
+  for (int h = 0; h < 2; ++h) {
+    if (rn == h)
 #pragma unroll
-  for (int k = 0; k < KQ; ++k)
-    if (kq * KQ + k < 2 * Q) rsh[(kq * KQ + k) * 128 + rm] = racc[k];
+      for (int k = 0; k < Q; ++k) {
+        double* p = rsh + (rh * Q + k) * 128 + rm;
+        *p = h == 0 ? racc[k] : *p + racc[k];
+      }
+    __syncthreads();
+  }
   __syncthreads();
   double* const rowp = part + int64_t(blockIdx.x) * pstride;
   for (int i = tid; i < m * P.q; i += NT) {

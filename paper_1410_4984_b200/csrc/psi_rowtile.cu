@@ -41,6 +41,7 @@
 
 #include "psi_common.cuh"
 #include "psi_kernels.cuh"
+#include "fp16_pieces.cuh"
 #include "tc_util.cuh"
 
 #ifndef SGPX_RT_POLY
@@ -52,6 +53,10 @@ extern std::atomic<int64_t> g_tc_launches;
 
 namespace {
 using namespace dev;
+using pc::put_feat_words;
+using pc::put_rows;
+using pc::split_f16x2;
+using pc::h2u;
 
 constexpr int kCH = 96;                 // streamed rows per chunk (MMA1 N, MMA3 K)
 constexpr int kGroups = 3;              // consumer warps per TMEM lane quarter (32 columns each)
@@ -63,7 +68,7 @@ constexpr int kThreads = kCons + kDrain + 64;
 constexpr int kPadRows = 768;           // feature-array row padding: lcm(kCH, 2 x 128)
 constexpr float kNegHuge = -6.0e4f;     // B_n of padded datapoints (fp16-representable): 2^-6e4 = 0
 constexpr int kPolyShare = SGPX_RT_POLY;  // exponentials on the FMA pipe: 0 none, 8 one in 8, 4 one in 4 (round 1)
-constexpr float kHalfMax = 6.0e4f;      // exponent features are clamped to the fp16 range
+using pc::kHalfMax;
 
 // MMA3 operands G = 2^D and Y as 16-bit hi / lo pieces (G packed in place of D, kind::f16 with A
 // from TMEM, up to four D/G stages).  BF (forward): bf16 pieces, ~2^-17 relative.  !BF (backward):
@@ -139,61 +144,9 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   return d;
 }
 
-// fp16 hi / lo split of two floats: hi = f16x2(a, b), lo = f16x2(a - hi.a, b - hi.b).  Written with the
-// packed cvt and a b16 split so ptxas reads the halves with HADD2.F32 .H0 / .H1 selectors (3
-// instructions per value; the __half2 intrinsics cost ~2 extra PRMT per value).
-__device__ __forceinline__ void split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
-  uint32_t h;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));
-  float ha, hb;
-  asm("{.reg .b16 l, u; mov.b32 {l, u}, %2; cvt.f32.f16 %0, l; cvt.f32.f16 %1, u;}" : "=f"(ha), "=f"(hb) : "r"(h));
-  uint32_t l2;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l2) : "f"(b - hb), "f"(a - ha));
-  hi = h;
-  lo = l2;
-}
-
-__device__ __forceinline__ uint32_t h2u(__half2 h) {
-  return uint32_t(__half_as_ushort(__low2half(h))) | (uint32_t(__half_as_ushort(__high2half(h))) << 16);
-}
-
-
 // ---------------------------------------------------------------------------------------------
 // Feature builders (elementwise, HBM-bound)
 // ---------------------------------------------------------------------------------------------
-
-// fp16 pieces of features k, k+1 packed as half2 words (low half = even k), clamped to the fp16
-// range: NP = 2 -> hi, lo (~2^-22); NP = 3 -> hi, mid, lo (~2^-33, from fp64 features)
-template <int NP>
-__device__ __forceinline__ void split_pair(double x0, double x1, uint32_t (&w)[NP]) {
-  x0 = fmin(fmax(x0, -double(kHalfMax)), double(kHalfMax));
-  x1 = fmin(fmax(x1, -double(kHalfMax)), double(kHalfMax));
-#pragma unroll
-  for (int i = 0; i < NP; ++i) {
-    const __half2 h = __floats2half2_rn(float(x0), float(x1));
-    w[i] = h2u(h);
-    const float2 hf = __half22float2(h);
-    x0 -= double(hf.x);
-    x1 -= double(hf.y);
-  }
-}
-// 2 K1 features of one row as NP pieces of K1 words at word offset `row_off` of a canonical
-// K-major tile (core matrix = 8 rows x 4 words); piece i at base + i * pstride
-template <int NP>
-__device__ __forceinline__ void put_feat_words(float* base, int64_t pstride, int64_t row_off, const double* f, int K1) {
-  for (int k = 0; k < K1; k += 4) {
-    uint32_t w[4][NP];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) split_pair<NP>(f[2 * (k + u)], f[2 * (k + u) + 1], w[u]);
-#pragma unroll
-    for (int i = 0; i < NP; ++i)
-      *reinterpret_cast<uint4*>(base + i * pstride + row_off + (k >> 2) * 32) = make_uint4(w[0][i], w[1][i], w[2][i], w[3][i]);
-  }
-}
-template <int NP>
-__device__ __forceinline__ void put_rows(float* base, int64_t pstride, int64_t r, const double* f, int K1) {
-  put_feat_words<NP>(base, pstride, (r >> 3) * (K1 * 8) + (r & 7) * 4, f, K1);
-}
 
 // One row of a streamed chunk in the processed-stage layout (the MMA1 / MMA3 B operands): X row
 // jj (K1 features) and Y column jj (N3 features, rows past NH zero).  Single CTA:
