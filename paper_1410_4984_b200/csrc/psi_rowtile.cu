@@ -44,9 +44,6 @@
 #include "fp16_pieces.cuh"
 #include "tc_util.cuh"
 
-#ifndef SGPX_RT_POLY
-#define SGPX_RT_POLY 0
-#endif
 
 namespace sgpx {
 extern std::atomic<int64_t> g_tc_launches;
@@ -67,7 +64,6 @@ constexpr int kWarpMma = kWarpLoad + 1;           // MMA warp (17)
 constexpr int kThreads = kCons + kDrain + 64;
 constexpr int kPadRows = 768;           // feature-array row padding: lcm(kCH, 2 x 128)
 constexpr float kNegHuge = -6.0e4f;     // B_n of padded datapoints (fp16-representable): 2^-6e4 = 0
-constexpr int kPolyShare = SGPX_RT_POLY;  // exponentials on the FMA pipe: 0 none, 8 one in 8, 4 one in 4 (round 1)
 using pc::kHalfMax;
 
 // MMA3 operands G = 2^D and Y as 16-bit hi / lo pieces (G packed in place of D, kind::f16 with A
@@ -789,13 +785,12 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
             v[3] = __uint_as_float(r[i + 3]);
             return;
           }
-          // every exponential on MUFU.EX2 (issue-bound consumers: the FMA-pipe polynomial cost
-          // ~11 instructions where MUFU takes one, and MUFU stays below its 16/clk/SM rate)
+          // every exponential on MUFU.EX2 (the FMA-pipe polynomial of round 1 cost ~11 instructions
+          // where MUFU takes one; measured: one in four or one in eight on it is no faster)
           v[0] = ex2(__uint_as_float(r[i]));
           v[1] = ex2(__uint_as_float(r[i + 1]));
           v[2] = ex2(__uint_as_float(r[i + 2]));
-          const bool poly = kPolyShare == 4 || (kPolyShare == 8 && (i & 4));
-          v[3] = poly ? ex2_poly(__uint_as_float(r[i + 3])) : ex2(__uint_as_float(r[i + 3]));
+          v[3] = ex2(__uint_as_float(r[i + 3]));
         };
         uint32_t hi[16], lo[16];
         auto half = [&](const uint32_t (&r)[16], int base) {
