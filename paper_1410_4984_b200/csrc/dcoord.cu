@@ -225,84 +225,119 @@ __global__ void __launch_bounds__(1024) finish_kernel(DcArgs A, const double* __
 
 // ---------------------------------------------------------------------------------------------
 // Small-M path (M <= kSmallM): each coordinator step is ONE CTA working in shared memory —
-// left-looking Cholesky (2 barriers per column), L^-1 by column substitution, and the products.
+// right-looking Cholesky (1 barrier per column), L^-1 a warp per column, the products by 4 x 4
+// register tiles.
 // ---------------------------------------------------------------------------------------------
 constexpr int kSmallM = 112;  // 2 M^2 doubles of shared memory (<= 200 KB)
 __device__ long long g_dc_prof[16];  // SGPX debug: clock64 phase stamps of bound_small_kernel
 #define DC_STAMP(i) \
   if (threadIdx.x == 0) g_dc_prof[i] = clock64()
 
-// Left-looking lower Cholesky of the shared m x m matrix L (lower triangle valid) in place.  Column j:
-// each row's dot product over k < j is split across 8 lanes (k = r mod 8) and combined by a fixed
-// xor tree, so the dependent chain is j / 8 long.
-__device__ bool chol_left_smem(double* L, int m, int* s_flag) {
-  constexpr int kSplit = 8;
-  if (threadIdx.x == 0) *s_flag = 1;
-  __syncthreads();
-  const int r = threadIdx.x & (kSplit - 1);
+// Right-looking lower Cholesky of the shared m x m matrix L (lower triangle valid) in place, one
+// barrier per column: step j subtracts a_ij a_cj / a_jj from the trailing lower triangle with the
+// still-unscaled column j (a 32 x 32 thread grid over (row, column) offsets, no index division),
+// the columns are scaled by l_jj = sqrt(a_jj) once at the end.  dg: m doubles of scratch (l_jj).
+__device__ bool chol_right_smem(double* L, int m, double* dg) {
+  const int tr = threadIdx.x & 31, tc = threadIdx.x >> 5, nc = blockDim.x >> 5;
   for (int j = 0; j < m; ++j) {
-    for (int base = j; base < m; base += blockDim.x / kSplit) {
-      const int i = base + int(threadIdx.x) / kSplit;
-      double s = 0.0;
-      if (i < m)
-        for (int k = r; k < j; k += kSplit) s += L[i + k * m] * L[j + k * m];
-      s += __shfl_xor_sync(0xffffffffu, s, 4);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      if (i < m && r == 0) L[i + j * m] -= s;
-    }
-    __syncthreads();
     const double d = L[j + j * m];
     if (!(d > 0.0)) {
-      if (threadIdx.x == 0) *s_flag = 0;
       __syncthreads();
       return false;
     }
-    const double ljj = sqrt(d), inv = 1.0 / ljj;
-    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) L[i + j * m] *= inv;
-    __syncthreads();
-    if (threadIdx.x == 0) L[j + j * m] = ljj;
-  }
-  __syncthreads();
-  return *s_flag != 0;
-}
-
-// W = L^-1 (lower), row by row: W_kj = (delta_kj - sum_{j <= i < k} L_ki W_ij) / L_kk for every j <= k
-// at once, each dot product split across 8 lanes (fixed xor tree).  Stored row-major
-// (S[k m + j] = W_kj).  `inv` holds m doubles of scratch (1 / L_kk).
-__device__ void trinv_smem(const double* L, double* S, int m, double* inv) {
-  constexpr int kSplit = 8;
-  for (int k = threadIdx.x; k < m; k += blockDim.x) inv[k] = 1.0 / L[k + k * m];
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) S[e] = 0.0;
-  __syncthreads();
-  const int r = threadIdx.x & (kSplit - 1);
-  for (int k = 0; k < m; ++k) {
-    for (int base = 0; base <= k; base += blockDim.x / kSplit) {
-      const int j = base + int(threadIdx.x) / kSplit;
-      double s = 0.0;
-      if (j <= k)
-        for (int i = j + r; i < k; i += kSplit) s += L[k + i * m] * S[i * m + j];
-      s += __shfl_xor_sync(0xffffffffu, s, 4);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      if (j <= k && r == 0) S[k * m + j] = ((k == j ? 1.0 : 0.0) - s) * inv[k];
+    if (threadIdx.x == 0) dg[j] = sqrt(d);
+    const double inv = 1.0 / d;
+    const int R = m - j - 1;
+    const double* cj = L + j * m + j + 1;  // a_(j+1..m-1), j
+    for (int r = tr; r < R; r += 32) {
+      const double lr = cj[r] * inv;
+      for (int c = tc; c <= r; c += nc) L[(j + 1 + r) + (j + 1 + c) * m] -= lr * cj[c];
     }
     __syncthreads();
   }
-}
-
-// X = W^T W from the row-major S (exactly symmetric: both triangles from the same products in the
-// same order) -> out (and out2 if given); W^T W_ab = sum_{k >= max(a,b)} W_ka W_kb
-__device__ void wtw_smem(const double* S, int m, double* out, double* out2 = nullptr) {
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
     const int i = e % m, j = e / m;
-    const int a = max(i, j), b = min(i, j);
-    double s = 0.0;
-#pragma unroll 4
-    for (int k = a; k < m; ++k) s += S[k * m + a] * S[k * m + b];
-    out[e] = s;
-    if (out2) out2[e] = s;
+    if (i > j) L[e] /= dg[j];
+    else if (i == j) L[e] = dg[j];
   }
+  __syncthreads();
+  return true;
+}
+
+// W = L^-1 (lower): a warp per column j, the column in registers (lane l owns rows l + 32 t),
+// column-oriented substitution in the host's order (x_k /= L_kk, then x_i -= L_ik x_k).  Stored
+// row-major (S[k m + j] = W_kj), zeros above the diagonal.  m <= 128.
+__device__ void trinv_warp_smem(const double* L, double* S, int m) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = warp; j < m; j += nw) {
+    double x[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) x[t] = (lane + 32 * t == j) ? 1.0 : 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (32 * t + 31 < j || 32 * t >= m) continue;
+      for (int l = 0; l < 32; ++l) {
+        const int k = 32 * t + l;
+        if (k < j) continue;
+        if (k >= m) break;
+        const double xk = __shfl_sync(0xffffffffu, x[t], l) / L[k + k * m];
+        if (lane == l) x[t] = xk;
+#pragma unroll
+        for (int u = t; u < 4; ++u) {
+          const int i = lane + 32 * u;
+          if (i > k && i < m) x[u] -= L[i + k * m] * xk;
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int i = lane + 32 * t;
+      if (i < m) S[i * m + j] = x[t];
+    }
+  }
+}
+
+// C = A B with a(i, p), b(p, j) element accessors: 4 x 4 register tiles, one per thread, p ascending
+// (each element a single fma chain in a fixed order); c(i, j, value) stores.
+template <class FA, class FB, class FC>
+__device__ void tile_gemm(int m, int n, int k, FA a, FB b, FC c) {
+  const int tm = (m + 3) / 4, tn = (n + 3) / 4;
+  for (int t = threadIdx.x; t < tm * tn; t += blockDim.x) {
+    const int i0 = (t % tm) * 4, j0 = (t / tm) * 4;
+    double acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+    for (int p = 0; p < k; ++p) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        av[u] = i0 + u < m ? a(i0 + u, p) : 0.0;
+        bv[u] = j0 + u < n ? b(p, j0 + u) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (i0 + u < m && j0 + v < n) c(i0 + u, j0 + v, acc[u][v]);
+  }
+}
+
+// X = W^T W from the row-major S (W lower triangular: the terms below the diagonal range are exact
+// zeros; both triangles from the same products in the same order) -> out (and out2 if given)
+__device__ void wtw_smem(const double* S, int m, double* out, double* out2 = nullptr) {
+  tile_gemm(
+      m, m, m, [&](int i, int p) { return S[p * m + i]; }, [&](int p, int j) { return S[p * m + j]; },
+      [&](int i, int j, double v) {
+        out[i + j * m] = v;
+        if (out2) out2[i + j * m] = v;
+      });
 }
 
 __device__ double block_sum_s(double v, double* red) {
@@ -327,7 +362,8 @@ __device__ bool factor_smem(double* L, int m, int mode, double f0, double var, d
   for (int attempt = 0; attempt < 32; ++attempt) {
     fill(mode == 0 ? f * var : f * scale);
     __syncthreads();
-    ok = chol_left_smem(L, m, s_flag);
+    ok = chol_right_smem(L, m, red);
+    __syncthreads();
     if (threadIdx.x == 0) {
       g_dc_prof[10 + mode] = attempt + 1;
       g_dc_prof[12 + mode] = ok;
@@ -375,7 +411,8 @@ __global__ void __launch_bounds__(1024) prefactor_small_kernel(DcArgs A) {
       },
       red, &s_flag, &fac, &ld);
   if (ok) {
-    trinv_smem(L, W, m, red);
+    trinv_warp_smem(L, W, m);
+    __syncthreads();
     for (int e = threadIdx.x; e < m * m; e += blockDim.x) A.wk[e] = W[(e % m) * m + e / m];  // L_k^-1 (prediction)
     wtw_smem(W, m, A.kinv);
   }
@@ -424,7 +461,8 @@ __global__ void __launch_bounds__(1024) bound_small_kernel(DcArgs A, float* __re
       red, &s_flag, &fac, &ld);
   DC_STAMP(1);
   if (ok) {
-    trinv_smem(L, W, m, red);
+    trinv_warp_smem(L, W, m);
+    __syncthreads();
     DC_STAMP(2);
     for (int e = threadIdx.x; e < m * m; e += blockDim.x) A.wa[e] = W[(e % m) * m + e / m];  // L_a^-1 (prediction)
     __syncthreads();
@@ -435,24 +473,17 @@ __global__ void __launch_bounds__(1024) bound_small_kernel(DcArgs A, float* __re
   // G = A^-1 Psi (M x D): A^-1 from shared memory, Psi through the read-only path; G into shared memory
   // over W when it fits (M D <= M^2), else global only
   double* gs = d <= m ? W : nullptr;
-  for (int64_t e = threadIdx.x; e < int64_t(m) * d; e += blockDim.x) {
-    const int a = int(e % m), c = int(e / m);
-    const double* pc = psi + int64_t(c) * m;
-    double s = 0.0;
-#pragma unroll 4
-    for (int b = 0; b < m; ++b) s += L[a + b * m] * __ldg(pc + b);
-    A.g[e] = s;
-    if (gs) gs[e] = s;
-  }
+  tile_gemm(
+      m, d, m, [&](int i, int p) { return L[i + p * m]; }, [&](int p, int j) { return __ldg(psi + int64_t(j) * m + p); },
+      [&](int i, int j, double v) {
+        A.g[i + int64_t(j) * m] = v;
+        if (gs) gs[i + j * m] = v;
+      });
   __syncthreads();
   const double* gg = gs ? gs : A.g;
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    const int i = e % m, j = e / m;
-    double s = 0.0;
-#pragma unroll 4
-    for (int c = 0; c < d; ++c) s += gg[i + int64_t(c) * m] * gg[j + int64_t(c) * m];
-    A.ggt[e] = s;
-  }
+  tile_gemm(
+      m, m, d, [&](int i, int p) { return gg[i + int64_t(p) * m]; }, [&](int p, int j) { return gg[j + int64_t(p) * m]; },
+      [&](int i, int j, double v) { A.ggt[i + j * m] = v; });
   __syncthreads();
   DC_STAMP(4);
   // reductions and the bound terms (bound.hpp:108-116)
@@ -527,31 +558,18 @@ __global__ void __launch_bounds__(1024) deferred_small_kernel(DcArgs A) {
     T[e] = A.phi[e];
   }
   __syncthreads();
-  for (int64_t e = threadIdx.x; e < int64_t(m) * d; e += blockDim.x) {  // Phi G
-    const int i = int(e % m), c = int(e / m);
-    const double* gc = A.g + int64_t(c) * m;
-    double s = 0.0;
-#pragma unroll 4
-    for (int k = 0; k < m; ++k) s += T[i + k * m] * __ldg(gc + k);
-    A.phig[e] = s;
-  }
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {  // tmp = Kmm^-1 Phi
-    const int i = e % m, j = e / m;
-    double s = 0.0;
-#pragma unroll 4
-    for (int k = 0; k < m; ++k) s += K[i + k * m] * T[k + j * m];
-    A.tmp[e] = s;
-  }
+  tile_gemm(  // Phi G
+      m, d, m, [&](int i, int p) { return T[i + p * m]; }, [&](int p, int j) { return __ldg(A.g + int64_t(j) * m + p); },
+      [&](int i, int j, double v) { A.phig[i + int64_t(j) * m] = v; });
+  tile_gemm(  // tmp = Kmm^-1 Phi
+      m, m, m, [&](int i, int p) { return K[i + p * m]; }, [&](int p, int j) { return T[p + j * m]; },
+      [&](int i, int j, double v) { A.tmp[i + j * m] = v; });
   __syncthreads();
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) T[e] = A.tmp[e];
   __syncthreads();
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {  // kpk = tmp Kmm^-1
-    const int i = e % m, j = e / m;
-    double s = 0.0;
-#pragma unroll 4
-    for (int k = 0; k < m; ++k) s += T[i + k * m] * K[k + j * m];
-    A.kpk[e] = s;
-  }
+  tile_gemm(  // kpk = tmp Kmm^-1
+      m, m, m, [&](int i, int p) { return T[i + p * m]; }, [&](int p, int j) { return K[p + j * m]; },
+      [&](int i, int j, double v) { A.kpk[i + j * m] = v; });
   __syncthreads();
   const double beta = A.beta, dd = double(d);
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
