@@ -4,8 +4,8 @@ Tolerances (north star: <= 1e-4 relative for the mixed FP32/fp64 path):
   * statistics Phi, Psi, yy:         norm-wise relative error <= 1e-5
   * per-datapoint / global gradients: norm-wise relative error <= 5e-5
   * bound total:                      |a-b| / max(|a|,|b|,1) <= 1e-5 (reference rel_err scale)
-The exponents run in FP32 (FFMA + MUFU.EX2); every sum over datapoints and
-across CTAs is fp64.
+The mixed modes (fast / precise) run the exponents as fp16-piece tcgen05 MMAs (psi2) or fp32
+direct differences (psi1) with MUFU.EX2; every sum over datapoints and across CTAs is fp64.
 """
 import numpy as np
 import pytest
@@ -341,3 +341,28 @@ def test_engine_subshard_pipeline(sgp, spread, q):
     assert norm_rel_err(r2.grads.d_lengthscales, r1.grads.d_lengthscales) < tg
     assert r2.grads.d_mu is gmu and r2.grads.d_s is gs
     assert norm_rel_err(gmu, r1.grads.d_mu) < tl and norm_rel_err(gs, r1.grads.d_s) < tl
+
+
+@pytest.mark.parametrize("shape", [(5000, 10, 64, 128), (3001, 6, 65, 100), (2000, 4, 128, 40), (2000, 4, 129, 40),
+                                   (3, 2, 3, 2), (4097, 3, 17, 129)])
+@pytest.mark.parametrize("precision", ["fast", "precise"])
+def test_psi1_tensor_core_limits(sgp, orc, shape, precision, monkeypatch):
+    """The tcgen05 psi1 kernels at and past their limits (M <= 128; D <= 128 forward, D <= 64 backward;
+    past them the SIMT tile / row kernels take over) against the oracle, and the tensor-core path
+    against the SIMT tile kernels (SGPX_PSI1=simt) on the same inputs."""
+    n, q, d, m = shape
+    mu, s, y, z, var, ls = problem(17, n, q, d, m)
+    rng = np.random.default_rng(18)
+    adj = sym_adj(rng, m, d)
+    k = sgp.KernelSpec(var, ls)
+    st, g = sgp.sweep_stats(True, mu, s, y, z, k, adj=sgp.StatsAdjoints(*adj), precision=precision)
+    wst, wg = orc.sweep_stats(True, mu, s, y, z, var, ls, adj=adj)
+    assert rel_err(st.yy, wst.yy) < 1e-12
+    assert norm_rel_err(st.psi_y, wst.psi_y) < STAT_TOL
+    assert norm_rel_err(st.phi_big, wst.phi_big) < STAT_TOL
+    for a, b in ((g.d_z, wg.d_z), (g.d_lengthscales, wg.d_lengthscales), (g.d_mu, wg.d_mu), (g.d_s, wg.d_s)):
+        assert norm_rel_err(a, b) < GRAD_TOL
+    monkeypatch.setenv("SGPX_PSI1", "simt")
+    st2, g2 = sgp.sweep_stats(True, mu, s, y, z, k, adj=sgp.StatsAdjoints(*adj), precision=precision)
+    assert norm_rel_err(st.psi_y, st2.psi_y) < STAT_TOL
+    assert norm_rel_err(g.d_mu, g2.d_mu) < GRAD_TOL and norm_rel_err(g.d_z, g2.d_z) < GRAD_TOL
