@@ -20,7 +20,7 @@
 //            -> d mu_n, d S_n, and the per-datapoint lengthscale sums (w_p = dL/dPhi_p)
 //
 // Both passes are one kernel template: a static 128-row tile (A of MMA1) in shared memory, a
-// ring of streamed 96-row chunks (B of MMA1 + B of MMA3, fed by 1D TMA bulk copies), MMA1 into a
+// ring of streamed kCH-row chunks (B of MMA1 + B of MMA3, fed by 1D TMA bulk copies), MMA1 into a
 // double-buffered TMEM stage, 12 consumer warps turning D into G = 2^D (MUFU.EX2; round 1 put 1 of 4 on an FMA-pipe
 // polynomial) stored back to TMEM as 16-bit hi/lo pairs, MMA3 with A = G read from TMEM, and the MMA3
 // accumulator drained into fp64 registers every chunk.  Every GEMM is a 3-piece split
@@ -55,7 +55,14 @@ using pc::put_rows;
 using pc::split_f16x2;
 using pc::h2u;
 
-constexpr int kCH = 96;                 // streamed rows per chunk (MMA1 N, MMA3 K)
+#ifndef SGPX_RT_CH
+#define SGPX_RT_CH 192
+#endif
+// streamed rows per chunk (MMA1 N, MMA3 K; kPadRows a multiple of it).  192 (round 2): MMA1 at N = 192
+// halves the MMA issues per datapoint against 96 and the consumers walk two 32-datapoint blocks per
+// stage; two D/G stages of 192 TMEM columns plus the concatenated accumulators fill the 512 columns
+// (psi2 kernels at C3 2.13 / 2.16 -> 1.90 / 1.89 ms, C5 290 -> 231 ms / evaluation).
+constexpr int kCH = SGPX_RT_CH;
 constexpr int kGroups = 3;              // consumer warps per TMEM lane quarter (32 columns each)
 constexpr int kCons = 128 * kGroups;    // consumer threads   (warps 0 .. 11)
 constexpr int kDrain = 128;             // accumulator drain threads (warps 12 .. 15)
@@ -93,9 +100,10 @@ struct RT {
   // MMA3 as G_hi * [Y_hi ; Y_lo] (N = 2 N3) + G_lo * Y_hi (N = N3; N = 2 N3 with [Y_hi ; Y_lo] in
   // PAIR mode) when the 2 N3-column accumulators fit next to the (at least 3, resp. 2) D/G
   // stages; else three N3 passes (single-CTA only).
-  static constexpr bool kConcat = 3 * SW + 4 * N3 <= 512;
+  static constexpr int kSmin = SW > 128 ? 2 : 3;       // fewest D/G stages the concatenated MMA3 needs
+  static constexpr bool kConcat = kSmin * SW + 4 * N3 <= 512;
   static constexpr int AccW = kConcat ? 2 * N3 : N3;   // TMEM columns per accumulator stage
-  static constexpr int kS = (512 - 2 * AccW) / SW >= 4 ? 4 : 3;  // D/G stages
+  static constexpr int kS = (512 - 2 * AccW) / SW >= 4 ? 4 : (512 - 2 * AccW) / SW;  // D/G stages
 };
 
 __host__ __device__ constexpr int rt_k1(int q) { return (2 * q + 2 + 15) / 16 * 8; }
@@ -115,7 +123,9 @@ struct RtCfg {
 };
 __host__ __device__ constexpr int rt_stages(int q, bool bf) {  // RT<Q, BF>::kS on the host
   (void)bf;
-  return (512 - 2 * ((3 * kCH + 4 * rt_n3(q) <= 512) ? 2 * rt_n3(q) : rt_n3(q))) / kCH >= 4 ? 4 : 3;
+  return (512 - 2 * (((kCH > 128 ? 2 : 3) * kCH + 4 * rt_n3(q) <= 512) ? 2 * rt_n3(q) : rt_n3(q))) / kCH >= 4
+             ? 4
+             : (512 - 2 * (((kCH > 128 ? 2 : 3) * kCH + 4 * rt_n3(q) <= 512) ? 2 * rt_n3(q) : rt_n3(q))) / kCH;
 }
 RtCfg rt_cfg(int q, bool bf, bool pair = false, int np = 2) {
   // operand stages: MMA1 runs kS chunks ahead, so the TMA ring needs kS + 2 slots to keep two
@@ -146,7 +156,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 
 // One row of a streamed chunk in the processed-stage layout (the MMA1 / MMA3 B operands): X row
 // jj (K1 features) and Y column jj (N3 features, rows past NH zero).  Single CTA:
-// [X hi | X lo | Y^T hi | Y^T lo] over all 96 rows.  PAIR: two per-CTA blocks
+// [X hi | X lo | Y^T hi | Y^T lo] over all kCH rows.  PAIR: two per-CTA blocks
 // [X hi | X lo (48 rows) | Y^T hi] and [X hi | X lo (rows 48..95) | Y^T lo].
 template <int Q, bool BF, bool PAIR, int NP>
 __device__ __forceinline__ void put_pre_row(float* chunk, int jj, const double* x, const float* y,
@@ -246,7 +256,7 @@ __global__ void __launch_bounds__(256) rt_pair_rows_kernel(PsiConst P, int64_t p
 }
 
 // Datapoint rows H_n, n < n_pad (padded rows [0 .., 0, -huge]): canonical K-major pieces (static
-// operand of the backward, piece i at hs + i * pstride) and, per 96-row chunk, the forward's
+// operand of the backward, piece i at hs + i * pstride) and, per kCH-row chunk, the forward's
 // streamed operands X = H_n, Y = [1, d2 mu, d2] in the processed-stage layout.
 // Forward G scale: G = 2^sg v with v <= sigma^4 (c2 <= sigma^4, pconst <= 1, exp <= 1), so G stays
 // below 2^15 in fp16; folded into the streamed copy of B_n and undone by the output scale.
@@ -771,7 +781,9 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
     for (int64_t c = 0; c < total; ++c) {
       tc::mbar_wait(&d_full[sd.slot], sd.phase);
       tc::fence_after();
-      const uint32_t dcol = tmem + uint32_t(sd.slot) * SW + uint32_t(32 * g) + lane_off;
+      // this warp's 32-datapoint blocks of the stage: g, g + kGroups, ... (kCH / 32 blocks)
+      for (int blk = g; blk < kCH / 32; blk += kGroups) {
+      const uint32_t dcol = tmem + uint32_t(sd.slot) * SW + uint32_t(32 * blk) + lane_off;
       if (!(R.dbg & 1)) {
         uint32_t r0[16], r1[16];
         tc::ld16(dcol, r0);
@@ -816,6 +828,7 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
         tc::st16(dcol, hi);
         tc::st16(dcol + 16, lo);
         tc::st_wait();
+      }
       }
       tc::fence_before();
       if (PAIR && !leader) {
