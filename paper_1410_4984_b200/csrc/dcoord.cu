@@ -299,11 +299,15 @@ __device__ void trinv_warp_smem(const double* L, double* S, int m) {
 
 // C = A B with a(i, p), b(p, j) element accessors: 4 x 4 register tiles, one per thread, p ascending
 // (each element a single fma chain in a fixed order); c(i, j, value) stores.
+// A warp owns a 128 x 4 tile: lane l the rows i0 + l + 32 u (u < 4, consecutive lanes read consecutive
+// a(i, p): no bank conflicts on column-major operands), the four columns j0 .. j0 + 3 shared by the
+// warp (b(p, j) reads are broadcasts).
 template <class FA, class FB, class FC>
 __device__ void tile_gemm(int m, int n, int k, FA a, FB b, FC c) {
-  const int tm = (m + 3) / 4, tn = (n + 3) / 4;
-  for (int t = threadIdx.x; t < tm * tn; t += blockDim.x) {
-    const int i0 = (t % tm) * 4, j0 = (t / tm) * 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int tm = (m + 127) / 128, tn = (n + 3) / 4;
+  for (int t = warp; t < tm * tn; t += nw) {
+    const int ib = (t % tm) * 128, j0 = (t / tm) * 4;
     double acc[4][4];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
@@ -313,7 +317,8 @@ __device__ void tile_gemm(int m, int n, int k, FA a, FB b, FC c) {
       double av[4], bv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        av[u] = i0 + u < m ? a(i0 + u, p) : 0.0;
+        const int i = ib + lane + 32 * u;
+        av[u] = i < m ? a(i, p) : 0.0;
         bv[u] = j0 + u < n ? b(p, j0 + u) : 0.0;
       }
 #pragma unroll
@@ -324,8 +329,10 @@ __device__ void tile_gemm(int m, int n, int k, FA a, FB b, FC c) {
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int v = 0; v < 4; ++v)
-        if (i0 + u < m && j0 + v < n) c(i0 + u, j0 + v, acc[u][v]);
+      for (int v = 0; v < 4; ++v) {
+        const int i = ib + lane + 32 * u;
+        if (i < m && j0 + v < n) c(i, j0 + v, acc[u][v]);
+      }
   }
 }
 

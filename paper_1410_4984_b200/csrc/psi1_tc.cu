@@ -674,6 +674,383 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 0) tc::tmem_dealloc(tmem, 128);
 }
 
+// ---------------------------------------------------------------------------------------------
+// backward, pipelined (psi1_bwd_pipe_kernel; the default where its tiles fit, Q <= 12): the same
+// sums as psi1_bwd_tc_kernel with
+//   * the raw fp64 rows of the next chunk arriving by 2D TMA while the current one is processed
+//     (Y right after its conversion, mu / S once the epilogue has read them) -- the kernel above
+//     stalls on every chunk's global loads (ncu: long_scoreboard the top stall);
+//   * T_n quarters handed to the epilogue through TMEM (no 43 KB shared-memory quarter table);
+//   * the weights from FFMA2 pairs of inducing points,
+//         log2 v1_nm = b1_n - sum_q (a_nq - b_nq z_mq)^2,   b = sqrt(log2e d1 / 2),  a = b mu,
+//     the same direct difference as (log2e / 2) d1 (mu - z)^2 with one FFMA per term instead of
+//     FADD + FMUL + FFMA, and the T / R contractions as FFMA2 as well.
+// Per chunk: [wait rows c] convert -> S1 -> (TMA Y c+1, C MMA) -> G phase (weights, G tile, T to
+// TMEM) -> S2 -> epilogue (d mu, d S, d l, d var) -> S3 -> (TMA mu / S c+1) -> R phase -> S4.
+constexpr int kB2Threads = 512;
+struct Bwd2Smem {  // byte offsets
+  int ya, pb, zs, hs, rawy, rawms, bar, total;
+  int dk, mn, mz, gst, hst;
+};
+__host__ __device__ inline Bwd2Smem bwd2_smem(int q, int d, int m) {
+  Bwd2Smem L{};
+  const int q4 = (q + 3) / 4 * 4;
+  L.dk = (d + 7) / 8 * 8;
+  L.mn = (m + 15) / 16 * 16;                     // C MMA N (rows of the dPsi operand)
+  L.mz = (m + 3) / 4 * 4;                        // inducing points in blocks of 4
+  L.gst = L.mz + ((4 - L.mz % 32) + 32) % 32;    // G row stride >= mz, = 4 (mod 32): conflict-free 16-byte rows
+  L.hst = 4 * q4 + 4;                            // per-datapoint row: d1 mu | d1 | a | b
+  const int ya_bytes = 2 * 128 * L.dk * 4, gs_bytes = 128 * L.gst * 4, rsh_bytes = 2 * q * 128 * 8;
+  int big = ya_bytes > gs_bytes ? ya_bytes : gs_bytes;
+  big = big > rsh_bytes ? big : rsh_bytes;
+  L.ya = 0;                                      // Y pieces [2][128 x dk]; then G [128][gst]; finally R exchange
+  L.pb = (big + 127) / 128 * 128;                // dPsi pieces [2][mn x dk]
+  L.zs = L.pb + 2 * L.mn * L.dk * 4;             // z [q][mz], z^2 [q][mz]
+  L.hs = L.zs + 2 * q * L.mz * 4;                // [128][hst]
+  L.rawy = (L.hs + 128 * L.hst * 4 + 127) / 128 * 128;  // TMA box: Y [d][128] doubles
+  L.rawms = L.rawy + d * 128 * 8;                // TMA boxes: mu [q][128], S [q][128] doubles
+  L.bar = L.rawms + 2 * q * 128 * 8;
+  L.total = L.bar + 64;
+  return L;
+}
+// TMEM column of T component (t1_q, t2_q) within a quarter's block: t0 first, then the latent
+// dimensions grouped by q mod 4 (the epilogue warp of subset s reads one contiguous run)
+__host__ __device__ constexpr int bwd2_tcol(int Q, int q) {
+  int off = 1;
+  for (int s = 0; s < (q & 3); ++s) off += 2 * ((Q - s + 3) / 4);
+  return off + 2 * (q >> 2);
+}
+template <int Q>
+__host__ __device__ constexpr int bwd2_nhp() { return (1 + 2 * Q + 7) / 8 * 8; }
+template <int Q>
+__host__ __device__ constexpr int bwd2_tmem_cols() { return 128 + 4 * bwd2_nhp<Q>() + 8 <= 256 ? 256 : 512; }
+
+template <int Q>
+__global__ void __launch_bounds__(kB2Threads, 1)
+    psi1_bwd_pipe_kernel(PsiConst P, BwdConst B, int64_t nchunks, double* __restrict__ part, int64_t pstride,
+                         const __grid_constant__ CUtensorMap tm_mu, const __grid_constant__ CUtensorMap tm_s,
+                         const __grid_constant__ CUtensorMap tm_y) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  constexpr int Q4 = (Q + 3) / 4 * 4, NT = kB2Threads, NHP = bwd2_nhp<Q>(), NQS = (Q + 3) / 4;
+  constexpr int TCOLS = bwd2_tmem_cols<Q>();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int d = P.d, m = P.m, pq = P.q;
+  const Bwd2Smem L = bwd2_smem(Q, d, m);
+  const int dk = L.dk, mn = L.mn, mz = L.mz, gst = L.gst, hst = L.hst;
+  float* ya = reinterpret_cast<float*>(smem + L.ya);
+  float* gs = ya;  // after the C MMA
+  float* pb = reinterpret_cast<float*>(smem + L.pb);
+  float* zs = reinterpret_cast<float*>(smem + L.zs);
+  float* hs = reinterpret_cast<float*>(smem + L.hs);
+  double* rawy = reinterpret_cast<double*>(smem + L.rawy);
+  double* rawm = reinterpret_cast<double*>(smem + L.rawms);
+  double* raws = rawm + Q * 128;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);  // 0 Y landed, 1 mu / S landed, 2 C MMA done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L.bar + 32);
+  // static operands: dPsi (rows = inducing points, K = output dims) as tf32 pieces, z and z^2
+  for (int i = tid; i < mn * dk; i += NT) {
+    const int mm = i / dk, dd = i % dk;
+    const float v = (mm < m && dd < d) ? B.dpsi[dd * P.mv + mm] : 0.f;
+    const float hi = tc::tf32_hi(v);
+    const int o = tc::canon(mm, dd, dk);
+    pb[o] = hi;
+    pb[mn * dk + o] = v - hi;
+  }
+  for (int i = tid; i < Q * mz; i += NT) {
+    const int q = i / mz, mm = i % mz;
+    const float z = (q < pq && mm < m) ? P.zc[mm * P.qv + q] : 0.f;
+    zs[i] = z;
+    zs[Q * mz + i] = z * z;
+  }
+  if (tid == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::mbar_init(&bar[2], 1);
+    tc::mbar_fence_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tslot, TCOLS);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  const int64_t nlocal = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const uint32_t ybytes = 128u * 8u * uint32_t(d), msbytes = 128u * 8u * uint32_t(pq * (P.expected ? 2 : 1));
+  auto load_y = [&](int64_t l) {
+    tc::mbar_arrive_expect_tx(&bar[0], ybytes);
+    tma_2d(rawy, &tm_y, int((blockIdx.x + l * gridDim.x) * 128), 0, &bar[0]);
+  };
+  auto load_ms = [&](int64_t l) {
+    const int c0 = int((blockIdx.x + l * gridDim.x) * 128);
+    tc::mbar_arrive_expect_tx(&bar[1], msbytes);
+    tma_2d(rawm, &tm_mu, c0, 0, &bar[1]);
+    if (P.expected) tma_2d(raws, &tm_s, c0, 0, &bar[1]);
+  };
+  if (tid == 0 && nlocal > 0) {
+    load_y(0);
+    load_ms(0);
+  }
+  const uint32_t idesc = tc::idesc_tf32(128, mn);
+  // G phase / epilogue role: datapoint cn (TMEM lane), quarter ch (inducing-point blocks ch, ch + 4, ...;
+  // latent dimensions ch, ch + 4, ... in the epilogue)
+  const int wq = warp & 3, ch = warp >> 2, cn = 32 * wq + lane;
+  const uint32_t t_row = tmem + (uint32_t(32 * wq) << 16);
+  // R role: inducing point rm, half rh of H (d1 mu or d1), half rn of each chunk's datapoints
+  const int rm = tid & 127, rh = (tid >> 7) & 1, rn = tid >> 8;
+  double racc[Q];
+#pragma unroll
+  for (int k = 0; k < Q; ++k) racc[k] = 0.0;
+  double dl_acc[NQS];
+#pragma unroll
+  for (int j = 0; j < NQS; ++j) dl_acc[j] = 0.0;
+  double dv_acc = 0.0;
+  const double inv_var = 1.0 / P.variance_d;
+  const int nb4 = mz / 4;
+  int toff = 1;  // this warp's run of (t1, t2) columns in every quarter's block
+  for (int s = 0; s < ch; ++s) toff += 2 * ((Q - s + 3) / 4);
+  for (int64_t l = 0; l < nlocal; ++l) {
+    const int64_t n0 = (blockIdx.x + l * gridDim.x) * 128;
+    const uint32_t ph = uint32_t(l & 1);
+    tc::mbar_wait(&bar[0], ph);
+    tc::mbar_wait(&bar[1], ph);
+    // Y -> tf32 pieces (32 consecutive threads fill one core matrix: 8 datapoints x 4 dims)
+    for (int i = tid; i < 128 * dk; i += NT) {
+      const int kk = i & 3, r8 = (i >> 2) & 7, rest = i >> 5;
+      const int nl = (rest & 15) * 8 + r8, dd = (rest >> 4) * 4 + kk;
+      const float f = dd < d ? float(rawy[dd * 128 + nl]) : 0.f;
+      const float hi = tc::tf32_hi(f);
+      const int o = tc::canon(nl, dd, dk);
+      ya[o] = hi;
+      ya[128 * dk + o] = f - hi;
+    }
+    // per-datapoint rows (rows past N arrive zero-filled: finite constants, Y = 0 so G = 0)
+    for (int i = tid; i < 128 * Q4; i += NT) {
+      const int nl = i & 127, q = i >> 7;
+      float mu = 0.f, d1 = 0.f;
+      if (q < pq) {
+        const double sd = P.expected ? raws[q * 128 + nl] : 0.0;
+        mu = float(rawm[q * 128 + nl] - P.center[q]);
+        d1 = 1.f / (float(sd) + P.l2[q]);
+      }
+      const float bq = sqrtf(0.5f * kLog2e * d1);
+      float* h = hs + nl * hst;
+      h[q] = d1 * mu;
+      h[Q4 + q] = d1;
+      h[2 * Q4 + q] = bq * mu;
+      h[3 * Q4 + q] = bq;
+    }
+    tc::fence_async_smem();
+    tc::fence_before();
+    __syncthreads();  // S1: Y pieces and rows ready; raw Y consumed
+    if (tid == 0 && l + 1 < nlocal) load_y(l + 1);
+    if (warp == 0) {
+      tc::fence_after();
+      const uint32_t a = tc::smem_u32(ya), b = tc::smem_u32(pb);
+      const uint32_t alo = a + 128 * dk * 4, blo = b + mn * dk * 4;
+      for (int ks = 0; ks < dk / 8; ++ks) {
+        const uint32_t o = uint32_t(ks) * 256;
+        tc::mma_ss_w(tmem, tc::desc(a + o, dk), tc::desc(b + o, dk), idesc, ks == 0 ? 0u : 1u);
+        tc::mma_ss_w(tmem, tc::desc(a + o, dk), tc::desc(blo + o, dk), idesc, 1u);
+        tc::mma_ss_w(tmem, tc::desc(alo + o, dk), tc::desc(b + o, dk), idesc, 1u);
+      }
+      tc::commit_w(&bar[2]);
+    }
+    // G phase constants while the MMAs run
+    float av[Q4], bv[Q4];
+    float b1 = P.log2_var;
+    {
+      const float* h = hs + cn * hst;
+#pragma unroll
+      for (int k4 = 0; k4 < Q4; k4 += 4) {
+        const float4 x = *reinterpret_cast<const float4*>(h + 2 * Q4 + k4);
+        const float4 y = *reinterpret_cast<const float4*>(h + 3 * Q4 + k4);
+        const float4 w = *reinterpret_cast<const float4*>(h + Q4 + k4);
+        av[k4] = x.x, av[k4 + 1] = x.y, av[k4 + 2] = x.z, av[k4 + 3] = x.w;
+        bv[k4] = y.x, bv[k4 + 1] = y.y, bv[k4 + 2] = y.z, bv[k4 + 3] = y.w;
+        const float wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (k4 + u < Q && k4 + u < pq) b1 += 0.5f * log2f(wv[u] * P.l2[k4 + u]);
+      }
+    }
+    tc::mbar_wait(&bar[2], ph);
+    tc::fence_after();
+    float2 t0 = make_float2(0.f, 0.f), t1[Q], t2[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) t1[q] = t2[q] = make_float2(0.f, 0.f);
+    const float2 b12 = make_float2(b1, b1);
+    for (int blk = ch; blk < nb4; blk += 4) {
+      const int mb = 4 * blk;
+      uint32_t r[4];
+      tc::ld4(t_row + uint32_t(mb), r);
+      float2 e01 = make_float2(0.f, 0.f), e23 = e01;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const float4 z = *reinterpret_cast<const float4*>(zs + q * mz + mb);
+        const float2 nb = make_float2(-bv[q], -bv[q]), aa = make_float2(av[q], av[q]);
+        const float2 u01 = __ffma2_rn(nb, make_float2(z.x, z.y), aa);
+        const float2 u23 = __ffma2_rn(nb, make_float2(z.z, z.w), aa);
+        e01 = __ffma2_rn(u01, u01, e01);
+        e23 = __ffma2_rn(u23, u23, e23);
+      }
+      e01 = __fadd2_rn(b12, make_float2(-e01.x, -e01.y));
+      e23 = __fadd2_rn(b12, make_float2(-e23.x, -e23.y));
+      tc::ld_wait();
+      const float2 g01 = __fmul2_rn(make_float2(__uint_as_float(r[0]), __uint_as_float(r[1])),
+                                    make_float2(ex2(e01.x), ex2(e01.y)));
+      const float2 g23 = __fmul2_rn(make_float2(__uint_as_float(r[2]), __uint_as_float(r[3])),
+                                    make_float2(ex2(e23.x), ex2(e23.y)));
+      *reinterpret_cast<float4*>(gs + cn * gst + mb) = make_float4(g01.x, g01.y, g23.x, g23.y);
+      t0 = __fadd2_rn(t0, g01);
+      t0 = __fadd2_rn(t0, g23);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const float4 z = *reinterpret_cast<const float4*>(zs + q * mz + mb);
+        const float4 w = *reinterpret_cast<const float4*>(zs + (Q + q) * mz + mb);
+        t1[q] = __ffma2_rn(g01, make_float2(z.x, z.y), t1[q]);
+        t1[q] = __ffma2_rn(g23, make_float2(z.z, z.w), t1[q]);
+        t2[q] = __ffma2_rn(g01, make_float2(w.x, w.y), t2[q]);
+        t2[q] = __ffma2_rn(g23, make_float2(w.z, w.w), t2[q]);
+      }
+    }
+    {  // this quarter's T_n -> TMEM columns 128 + ch * NHP (t0, then the latent dims grouped by q mod 4)
+      uint32_t w[NHP];
+#pragma unroll
+      for (int j = 0; j < NHP; ++j) w[j] = 0u;
+      w[0] = __float_as_uint(t0.x + t0.y);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        w[bwd2_tcol(Q, q)] = __float_as_uint(t1[q].x + t1[q].y);
+        w[bwd2_tcol(Q, q) + 1] = __float_as_uint(t2[q].x + t2[q].y);
+      }
+#pragma unroll
+      for (int c8 = 0; c8 < NHP / 8; ++c8)
+        tc::st8(t_row + uint32_t(128 + ch * NHP + 8 * c8), *reinterpret_cast<const uint32_t(*)[8]>(w + 8 * c8));
+      tc::st_wait();
+    }
+    tc::fence_before();
+    __syncthreads();  // S2: G tile and every quarter of T complete
+    tc::fence_after();
+    // per-datapoint epilogue (psi_stats.hpp:200-219): d mu, d S (+ KL), d l, d var for datapoint cn,
+    // latent dimensions ch, ch + 4, ...; the four T quarters summed in order in fp64
+    {
+      const int64_t n = n0 + cn;
+      double p0 = 0.0, p1[NQS], p2[NQS];
+#pragma unroll
+      for (int j = 0; j < NQS; ++j) p1[j] = p2[j] = 0.0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t w0, w[8];
+        tc::ld1(t_row + uint32_t(128 + c * NHP), w0);
+        tc::ld8(t_row + uint32_t(128 + c * NHP + toff), w);
+        tc::ld_wait();
+        p0 += double(__uint_as_float(w0));
+#pragma unroll
+        for (int j = 0; j < NQS; ++j) {
+          p1[j] += double(__uint_as_float(w[2 * j]));
+          p2[j] += double(__uint_as_float(w[2 * j + 1]));
+        }
+      }
+      if (n < P.n) {
+        if (ch == 0) dv_acc += p0 * inv_var;
+#pragma unroll
+        for (int j = 0; j < NQS; ++j) {
+          const int q = ch + 4 * j;
+          if (q < pq) {
+            const double mu64 = rawm[q * 128 + cn];
+            const double s = P.expected ? raws[q * 128 + cn] : 0.0, l = P.ls[q];
+            const double mu_ = mu64 - P.center[q];
+            const double dd1 = double(hs[cn * hst + Q4 + q]);
+            const double q1 = mu_ * mu_ * p0 - 2.0 * mu_ * p1[j] + p2[j];
+            dl_acc[j] += s * dd1 * p0 / l + l * dd1 * dd1 * q1;
+            if (B.write_local) {
+              double dmu = -dd1 * (mu_ * p0 - p1[j]);
+              double ds = -0.5 * dd1 * p0 + 0.5 * dd1 * dd1 * q1;
+              if (B.add_kl) {  // KL(q || N(0, I)) enters the bound with a minus sign (parallel.hpp:163-166)
+                dmu -= mu64;
+                ds -= 0.5 * (1.0 - 1.0 / s);
+              }
+              B.d_mu[q * B.ld_g + n] = dmu;
+              if (P.expected) B.d_s[q * B.ld_g + n] = ds;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();  // S3: raw mu / S consumed
+    if (tid == 0 && l + 1 < nlocal) load_ms(l + 1);
+    // R_mk += sum_n G_nm H_nk over this thread's half of the datapoints (fp32 over 64 datapoints,
+    // fp64 across chunks; the two datapoint halves added in order at the end)
+    {
+      float2 rr[Q4 / 2];
+#pragma unroll
+      for (int k = 0; k < Q4 / 2; ++k) rr[k] = make_float2(0.f, 0.f);
+      if (rm < m) {
+#pragma unroll 2
+        for (int nl = rn * 64; nl < rn * 64 + 64; ++nl) {
+          const float g = gs[nl * gst + rm];
+          const float2 gg = make_float2(g, g);
+          const float* hr = hs + nl * hst + rh * Q4;
+#pragma unroll
+          for (int k4 = 0; k4 < Q4; k4 += 4) {
+            const float4 h4 = *reinterpret_cast<const float4*>(hr + k4);
+            rr[k4 / 2] = __ffma2_rn(gg, make_float2(h4.x, h4.y), rr[k4 / 2]);
+            rr[k4 / 2 + 1] = __ffma2_rn(gg, make_float2(h4.z, h4.w), rr[k4 / 2 + 1]);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < Q; ++k) racc[k] += double((k & 1) ? rr[k / 2].y : rr[k / 2].x);
+    }
+    tc::fence_before();
+    __syncthreads();  // S4: G tile and rows consumed
+  }
+  // d z_mq = R_mq - z_mq R_m(Q+q)   (psi_stats.hpp:214), exchanged through shared memory: the two
+  // datapoint halves of each R_mk added in order
+  double* rsh = reinterpret_cast<double*>(smem + L.ya);  // [2Q][128] doubles
+  for (int h = 0; h < 2; ++h) {
+    if (rn == h)
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        double* p = rsh + (rh * Q + k) * 128 + rm;
+        *p = h == 0 ? racc[k] : *p + racc[k];
+      }
+    __syncthreads();
+  }
+  double* const rowp = part + int64_t(blockIdx.x) * pstride;
+  for (int i = tid; i < m * pq; i += NT) {
+    const int m_ = i % m, q = i / m;
+    const double z = zs[q * mz + m_];
+    rowp[1 + pq + m_ + int64_t(q) * m] = rsh[q * 128 + m_] - z * rsh[(Q + q) * 128 + m_];
+  }
+  // d l, d var: fixed-order block reduction
+  __syncthreads();
+  double* red = rsh;
+#pragma unroll 1
+  for (int k = 0; k <= Q; ++k) {
+    if (k < Q && k >= pq) continue;
+    double v = 0.0;
+    if (k == Q) {
+      v = dv_acc;
+    } else {
+#pragma unroll
+      for (int j = 0; j < NQS; ++j)
+        if (ch + 4 * j == k) v = dl_acc[j];
+    }
+    red[tid] = v;
+    __syncthreads();
+    for (int w = NT / 2; w > 0; w >>= 1) {
+      if (tid < w) red[tid] += red[tid + w];
+      __syncthreads();
+    }
+    if (tid == 0) rowp[k < Q ? 1 + k : 0] = red[0];
+    __syncthreads();
+  }
+  if (warp == 0) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, TCOLS);
+  }
+}
+
 PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled fn = [] {
     void* p = nullptr;
@@ -721,11 +1098,56 @@ int launch_fwd(const PsiConst& P, double* part, int64_t pstride, int rows, int* 
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
+// 2D tensor map of a column-major fp64 matrix [n rows x cols] with a box of `box_rows` rows
+// (rows past n zero-filled); false when the base / leading dimension is not 16-byte aligned
+bool encode_rows(CUtensorMap* map, const double* base, int64_t ld, int64_t n, int cols, int box_rows) {
+  auto encode = tensor_map_encoder();
+  if (!encode || reinterpret_cast<uintptr_t>(base) % 16 != 0 || ld % 2 != 0) return false;
+  cuuint64_t dims[2] = {cuuint64_t(n), cuuint64_t(cols)};
+  cuuint64_t strides[1] = {cuuint64_t(ld) * 8};
+  cuuint32_t box[2] = {cuuint32_t(box_rows), cuuint32_t(cols)};
+  cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool env_bwd_old() {
+  const char* e = getenv("SGPX_PSI1_BWD");
+  return e && !strcmp(e, "old");
+}
+
+// The pipelined backward where it applies (Q <= 12, tiles within 227 KB, TMA-able rows); 1 = not taken
+template <int Q>
+int launch_bwd_pipe(const PsiConst& P, const BwdConst& B, double* part, int64_t pstride, int rows, cudaStream_t st) {
+  if constexpr (Q > 12) {
+    return 1;
+  } else {
+    if (env_bwd_old() || P.d > 64 || P.m > 128) return 1;
+    const Bwd2Smem L = bwd2_smem(Q, P.d, P.m);
+    if (L.total > 227 * 1024) return 1;
+    CUtensorMap tm[3];
+    std::memset(tm, 0, sizeof(tm));
+    if (!encode_rows(&tm[0], P.mu, P.ld_mu, P.n, P.q, 128) ||
+        (P.expected && !encode_rows(&tm[1], P.s, P.ld_s, P.n, P.q, 128)) ||
+        !encode_rows(&tm[2], P.y, P.ld_y, P.n, P.d, 128))
+      return 1;
+    auto kern = psi1_bwd_pipe_kernel<Q>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess) return 3;
+    const int64_t nchunks = (P.n + 127) / 128;
+    kern<<<rows, kB2Threads, L.total, st>>>(P, B, nchunks, part, pstride, tm[0], tm[1], tm[2]);
+    g_tc_launches.fetch_add(1);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  }
+}
+
 template <int Q>
 int launch_bwd(const PsiConst& P, const BwdConst& B, double* part, int64_t pstride, int rows, cudaStream_t st) {
   const BwdSmem L = bwd_smem(Q, P.d, P.m);
   const int64_t nchunks = (P.n + kBwdN - 1) / kBwdN;
   if (rows <= 0) return 0;
+  const int rc = launch_bwd_pipe<Q>(P, B, part, pstride, rows, st);
+  if (rc != 1) return rc;
   auto kern = psi1_bwd_tc_kernel<Q>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess) return 3;
   kern<<<rows, kBwdThreads, L.total, st>>>(P, B, nchunks, part, pstride);

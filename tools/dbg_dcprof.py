@@ -3,6 +3,7 @@ sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
 from paper_1410_4984_b200 import sgp, synthetic, _lib
 w = synthetic.make(True, 100000, 10, 50, 100, seed=0, device="cuda")
 os.environ["SGPX_GRAPH"] = "0"
+os.environ.setdefault("SGPX_DEVICE_COORD", "1")
 e = sgp.Engine(sgp.ModelKind.latent, w.mu, w.s, w.y)
 e.broadcast(w.kernel, w.beta, w.z)
 for _ in range(3):

@@ -41,9 +41,20 @@ for _ in range(3):
     eng.broadcast(kern, w.beta, z, mu_np, s_np)
     eng.evaluate(True)
 torch.cuda.synchronize()
+resident = bool(os.environ.get("RESIDENT"))
+if resident:  # device-resident rows (the bench's `value` path)
+    eng = sgp.Engine(sgp.ModelKind.latent, mu, s, y, ctx=ctx)
+    for _ in range(3):
+        eng.broadcast(kern, w.beta, z)
+        eng.evaluate(True, local_to_host=False)
+    torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
-    eng.broadcast(kern, w.beta, z, mu_np, s_np)
-    r = eng.evaluate(True)
+    if resident:
+        eng.broadcast(kern, w.beta, z)
+        r = eng.evaluate(True, local_to_host=False)
+    else:
+        eng.broadcast(kern, w.beta, z, mu_np, s_np)
+        r = eng.evaluate(True)
     torch.cuda.synchronize()
 events = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
 t0 = min(e.time_range.start for e in events)
@@ -52,3 +63,9 @@ for st, en, name in rows:
     if en - st >= 20 or "Memcpy" in name:
         print(f"{st / 1e3:8.3f} - {en / 1e3:8.3f} ms  {(en - st) / 1e3:7.3f}  {name[:80]}")
 print(f"span {max(r[1] for r in rows) / 1e3:.3f} ms over {len(rows)} device events")
+if os.environ.get("CPU_EVENTS"):
+    cpu = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CPU and e.name.startswith("cu")]
+    c0 = min(e.time_range.start for e in cpu)
+    print(f"--- runtime API calls (CPU clock, first at {c0}; device clock first event at {t0})")
+    for e in sorted(cpu, key=lambda e: e.time_range.start):
+        print(f"{(e.time_range.start - c0) / 1e3:8.3f} ms  {(e.time_range.end - e.time_range.start) / 1e3:7.3f}  {e.name[:60]}")
