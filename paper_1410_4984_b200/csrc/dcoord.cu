@@ -299,48 +299,60 @@ __device__ void trinv_warp_smem(const double* L, double* S, int m) {
 
 // C = A B with a(i, p), b(p, j) element accessors: 4 x 4 register tiles, one per thread, p ascending
 // (each element a single fma chain in a fixed order); c(i, j, value) stores.
-// A warp owns a 128 x 4 tile: lane l the rows i0 + l + 32 u (u < 4, consecutive lanes read consecutive
-// a(i, p): no bank conflicts on column-major operands), the four columns j0 .. j0 + 3 shared by the
-// warp (b(p, j) reads are broadcasts).
-template <class FA, class FB, class FC>
-__device__ void tile_gemm(int m, int n, int k, FA a, FB b, FC c) {
+// C = A B on the fp64 tensor cores (mma.sync m8n8k4 .f64: the same 64 FMA/clk/SM as DFMA, one
+// instruction per 256 FMAs instead of 32 -- the small-M coordinator is instruction-bound, not
+// FMA-bound).  Strided operands A(i, p) = a[i ai + p ap], B(p, j) = b[p bp + j bj] (shared or global
+// memory); a warp per 16 x 16 tile of C (2 x 2 mma tiles), k ascending in steps of 4 (fixed order:
+// deterministic); c(i, j, value) stores.  Fragments (PTX m8n8k4 f64): A row = lane / 4, col = lane % 4;
+// B row = lane % 4, col = lane / 4; C row = lane / 4, cols 2 (lane % 4) + {0, 1}.
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+template <class FC>
+__device__ void mma_gemm(int m, int n, int k, const double* __restrict__ a, int ai, int ap, const double* __restrict__ b,
+                         int bp, int bj, FC c) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int tm = (m + 127) / 128, tn = (n + 3) / 4;
-  for (int t = warp; t < tm * tn; t += nw) {
-    const int ib = (t % tm) * 128, j0 = (t / tm) * 4;
-    double acc[4][4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
-    for (int p = 0; p < k; ++p) {
-      double av[4], bv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = ib + lane + 32 * u;
-        av[u] = i < m ? a(i, p) : 0.0;
-        bv[u] = j0 + u < n ? b(p, j0 + u) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+  const int g = lane >> 2, t = lane & 3;
+  const int tm = (m + 15) / 16, tn = (n + 15) / 16;
+  for (int tile = warp; tile < tm * tn; tile += nw) {
+    const int i0 = (tile % tm) * 16, j0 = (tile / tm) * 16;
+    double acc[2][2][2] = {};
+    const int ia0 = i0 + g, ia1 = i0 + 8 + g, jb0 = j0 + g, jb1 = j0 + 8 + g;
+    const bool ra0 = ia0 < m, ra1 = ia1 < m, cb0 = jb0 < n, cb1 = jb1 < n;
+    const double* pa0 = a + int64_t(ra0 ? ia0 : 0) * ai;
+    const double* pa1 = a + int64_t(ra1 ? ia1 : 0) * ai;
+    const double* pb0 = b + int64_t(cb0 ? jb0 : 0) * bj;
+    const double* pb1 = b + int64_t(cb1 ? jb1 : 0) * bj;
+    for (int p0 = 0; p0 < k; p0 += 4) {
+      const int pp = p0 + t;
+      const bool kp = pp < k;
+      const int64_t oa = int64_t(kp ? pp : 0) * ap, ob = int64_t(kp ? pp : 0) * bp;
+      const double a0 = (kp && ra0) ? pa0[oa] : 0.0, a1 = (kp && ra1) ? pa1[oa] : 0.0;
+      const double b0 = (kp && cb0) ? pb0[ob] : 0.0, b1 = (kp && cb1) ? pb1[ob] : 0.0;
+      dmma(acc[0][0], a0, b0);
+      dmma(acc[0][1], a0, b1);
+      dmma(acc[1][0], a1, b0);
+      dmma(acc[1][1], a1, b1);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int r = 0; r < 2; ++r)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int i = ib + lane + 32 * u;
-        if (i < m && j0 + v < n) c(i, j0 + v, acc[u][v]);
-      }
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = i0 + 8 * r + g, j = j0 + 8 * q + 2 * t + h;
+          if (i < m && j < n) c(i, j, acc[r][q][h]);
+        }
   }
 }
 
 // X = W^T W from the row-major S (W lower triangular: the terms below the diagonal range are exact
 // zeros; both triangles from the same products in the same order) -> out (and out2 if given)
 __device__ void wtw_smem(const double* S, int m, double* out, double* out2 = nullptr) {
-  tile_gemm(
-      m, m, m, [&](int i, int p) { return S[p * m + i]; }, [&](int p, int j) { return S[p * m + j]; },
+  mma_gemm(
+      m, m, m, S, 1, m, S, m, 1,
       [&](int i, int j, double v) {
         out[i + j * m] = v;
         if (out2) out2[i + j * m] = v;
@@ -480,17 +492,16 @@ __global__ void __launch_bounds__(1024) bound_small_kernel(DcArgs A, float* __re
   // G = A^-1 Psi (M x D): A^-1 from shared memory, Psi through the read-only path; G into shared memory
   // over W when it fits (M D <= M^2), else global only
   double* gs = d <= m ? W : nullptr;
-  tile_gemm(
-      m, d, m, [&](int i, int p) { return L[i + p * m]; }, [&](int p, int j) { return __ldg(psi + int64_t(j) * m + p); },
+  mma_gemm(
+      m, d, m, L, 1, m, psi, 1, m,
       [&](int i, int j, double v) {
         A.g[i + int64_t(j) * m] = v;
         if (gs) gs[i + j * m] = v;
       });
   __syncthreads();
   const double* gg = gs ? gs : A.g;
-  tile_gemm(
-      m, m, d, [&](int i, int p) { return gg[i + int64_t(p) * m]; }, [&](int p, int j) { return gg[j + int64_t(p) * m]; },
-      [&](int i, int j, double v) { A.ggt[i + j * m] = v; });
+  mma_gemm(
+      m, m, d, gg, 1, m, gg, m, 1, [&](int i, int j, double v) { A.ggt[i + j * m] = v; });
   __syncthreads();
   DC_STAMP(4);
   // reductions and the bound terms (bound.hpp:108-116)
@@ -550,6 +561,337 @@ __global__ void __launch_bounds__(1024) bound_small_kernel(DcArgs A, float* __re
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Split small-M coordinator: the backward's psi1 kernel needs only d Psi = beta^2 G, so
+//   K1 (bound_g_small_kernel, on the evaluation's stream): A = Kmm + jitter + beta Phi, factor_spd
+//       escalation, log|A|, G = A^-1 Psi by two triangular solves, d Psi, <Psi, G>;
+//   K2 (bound_u_small_kernel, on a side stream, concurrent with the psi1 backward): L^-1, A^-1, G G^T,
+//       the bound terms and d Phi (= U, the psi2 backward's operand); then deferred_small_kernel.
+// K1's Cholesky is column-cyclic and dataflow-ordered: warp w owns columns w, w + 32, ... in registers
+// (lane l rows l + 32 u); column k is finalised (sqrt, scale) by its owner right after its last update
+// and published through shared memory with an mbarrier per column, so the critical path is one
+// update + one finalisation per column, with no block-wide barrier.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void mb_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(b))));
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(b)))
+               : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, "
+        "0, p;\n\t}"
+        : "=r"(done)
+        : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(b))), "r"(parity)
+        : "memory");
+}
+template <int N>
+__device__ __forceinline__ double pick(const double (&v)[N], int u) {
+  double r = v[0];
+#pragma unroll
+  for (int t = 1; t < N; ++t)
+    if (u == t) r = v[t];
+  return r;
+}
+template <int N>
+__device__ __forceinline__ void put(double (&v)[N], int u, double x) {
+#pragma unroll
+  for (int t = 0; t < N; ++t)
+    if (u == t) v[t] = x;
+}
+
+__global__ void __launch_bounds__(1024) bound_g_small_kernel(DcArgs A, float* __restrict__ dpsi,
+                                                             double* __restrict__ dpsi64) {
+  extern __shared__ double sm[];
+  __shared__ uint64_t ready[128];
+  __shared__ double red[1024];
+  __shared__ double invd[128], logd[128];
+  __shared__ volatile int s_fail;
+  const int m = A.m, d = A.d, mv = A.mv;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lrs = m | 1;    // odd row stride: conflict-free column writes / row reads of Lr
+  double* L = sm;           // column-major factor, zero above the diagonal
+  double* Lr = sm + m * m;  // Lr[k lrs + i] = L(k, i) (rows of L, for the transposed solve)
+  const double* packed = A.packed;
+  const double* psi = packed + 4 + int64_t(m) * (m + 1) / 2;
+  const double beta = A.beta, jit = A.sc[kScJitterFactor] * A.var;
+  auto phi_at = [&](int i, int j) {
+    const int lo = min(i, j), hi = max(i, j);
+    return packed[4 + int64_t(lo) * m - int64_t(lo) * (lo - 1) / 2 + (hi - lo)];
+  };
+  DC_STAMP(0);
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    A.phi[e] = phi_at(e % m, e / m);  // dense Phi (K2, deferred)
+    L[e] = 0.0;                       // the factor's upper triangle
+  }
+  double f = 0.0, scale = 0.0;  // factor_spd escalation (bound.hpp:52-62): shift f * max |a_ii|
+  bool ok = false;
+  for (int attempt = 0; attempt < 32; ++attempt) {
+    if (attempt == 1) {  // the matrix's own scale, needed from the first retry on
+      double mx = 0.0;
+      for (int i = threadIdx.x; i < m; i += blockDim.x) mx = fmax(mx, fabs(A.kmm[i + i * m] + jit + beta * phi_at(i, i)));
+      red[threadIdx.x] = mx;
+      __syncthreads();
+      for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+        __syncthreads();
+      }
+      scale = red[0];
+      __syncthreads();
+    }
+    const double shift = f * scale;
+    if (attempt == 0 && threadIdx.x < m) mb_init(&ready[threadIdx.x]);  // each attempt completes every barrier once
+    if (threadIdx.x == 0) s_fail = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    const uint32_t par = uint32_t(attempt & 1);
+    // this warp's columns c = warp + 32 cc in registers (rows lane + 32 u)
+    double x[4][4];
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = warp + 32 * cc, i = lane + 32 * u;
+        x[cc][u] = (c < m && i < m) ? A.kmm[i + int64_t(c) * m] + beta * phi_at(i, c) + (i == c ? jit + shift : 0.0)
+                                    : 0.0;
+      }
+    // finalise column k (slot cc of this warp): l_kk = sqrt(a_kk), scale below, publish
+    auto finalise = [&](int k, double (&v)[4]) {
+      const double dkk = __shfl_sync(0xffffffffu, pick(v, k >> 5), k & 31);
+      const bool bad = !(dkk > 0.0);
+      const double lkk = bad ? 1.0 : sqrt(dkk), inv = 1.0 / lkk;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (32 * u + 31 < k) continue;  // rows above the diagonal stay zero (warp-uniform)
+        const int i = lane + 32 * u;
+        v[u] = i > k ? v[u] * inv : (i == k ? lkk : 0.0);
+        if (i < m && i >= k) {
+          L[i + k * m] = v[u];
+          Lr[i * lrs + k] = v[u];
+        }
+      }
+      if (lane == 0) {
+        invd[k] = inv;
+        logd[k] = lkk;  // log taken after the factorisation (off the critical path)
+        if (bad) s_fail = 1;
+      }
+      __syncwarp();
+      if (lane == 0) mb_arrive(&ready[k]);
+    };
+    DC_STAMP(1);
+    if (warp == 0) finalise(0, x[0]);
+    const int last = warp < m ? warp + 32 * ((m - 1 - warp) / 32) : -1;  // this warp's last column
+    for (int k = 0; k + 1 < m && k < last; ++k) {
+      mb_wait(&ready[k], par);  // column k published (a no-op wait for its owner)
+      const int k1 = k + 1;
+      if (s_fail) {  // a pivot failed: the owners still publish every later column (no waiter is left behind)
+        if ((k1 & 31) == warp && lane == 0) mb_arrive(&ready[k1]);
+        continue;
+      }
+      // the owner of column k + 1 applies column k to it first, then finalises and publishes it
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int c = warp + 32 * cc;
+        if (c == k1) {
+          const double lck = L[c + k * m];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (32 * u + 31 < c) continue;
+            const int i = lane + 32 * u;
+            if (i >= c && i < m) x[cc][u] -= L[i + k * m] * lck;
+          }
+          finalise(k1, x[cc]);
+        }
+      }
+      // column k into this warp's later columns
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int c = warp + 32 * cc;
+        if (c > k1 && c < m) {
+          const double lck = L[c + k * m];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (32 * u + 31 < c) continue;
+            const int i = lane + 32 * u;
+            if (i >= c && i < m) x[cc][u] -= L[i + k * m] * lck;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    ok = !s_fail;
+    __syncthreads();
+    if (ok) break;
+    f = f == 0.0 ? 1e-10 : f * 10.0;
+    if (!(f <= 1e-2)) break;
+  }
+  DC_STAMP(2);
+  // log |A| (fixed-order tree, the same as factor_smem's)
+  double s = 0.0;
+  if (ok)
+    for (int i = threadIdx.x; i < m; i += blockDim.x) s += log(logd[i]);
+  s = block_sum_s(s, red);
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) A.la[e] = L[e];  // K2 (L^-1) and prediction
+  // G = L^-T L^-1 Psi: a warp per right-hand side (two at a time), column-oriented substitutions
+  for (int j0 = 2 * warp; j0 < d; j0 += 2 * (blockDim.x >> 5)) {
+    const int nj = min(2, d - j0);
+    double xv[2][4];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = lane + 32 * u;
+        xv[r][u] = (r < nj && i < m) ? psi[i + int64_t(j0 + r) * m] : 0.0;
+      }
+    if (ok) {
+      for (int k = 0; k < m; ++k) {  // L y = psi
+        const double ik = invd[k];
+        double yk[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          yk[r] = __shfl_sync(0xffffffffu, pick(xv[r], k >> 5), k & 31) * ik;
+          if (lane == (k & 31)) put(xv[r], k >> 5, yk[r]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (32 * u + 31 <= k) continue;
+          const int i = lane + 32 * u;
+          if (i > k && i < m) {
+            const double l = L[i + k * m];
+            xv[0][u] -= l * yk[0];
+            xv[1][u] -= l * yk[1];
+          }
+        }
+      }
+      for (int k = m - 1; k >= 0; --k) {  // L^T g = y
+        const double ik = invd[k];
+        double gk[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          gk[r] = __shfl_sync(0xffffffffu, pick(xv[r], k >> 5), k & 31) * ik;
+          if (lane == (k & 31)) put(xv[r], k >> 5, gk[r]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (32 * u >= k) continue;
+          const int i = lane + 32 * u;
+          if (i < k) {
+            const double l = Lr[k * lrs + i];
+            xv[0][u] -= l * gk[0];
+            xv[1][u] -= l * gk[1];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      if (r >= nj) break;
+      const int j = j0 + r;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = lane + 32 * u;
+        if (i < m) A.g[i + int64_t(j) * m] = xv[r][u];
+        if (i < mv) {
+          const double v = i < m ? beta * beta * xv[r][u] : 0.0;
+          dpsi[int64_t(j) * mv + i] = float(v);
+          dpsi64[int64_t(j) * mv + i] = v;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  DC_STAMP(3);
+  double pg = 0.0;  // <Psi, G> (bound.hpp:108-116), fixed-order tree
+  for (int64_t e = threadIdx.x; e < int64_t(m) * d; e += blockDim.x) pg += psi[e] * A.g[e];
+  pg = block_sum_s(pg, red);
+  if (threadIdx.x == 0) {
+    A.sc[kScLogDetA] = 2.0 * s;
+    A.sc[kScShiftA] = f;
+    A.sc[kScPg] = pg;
+    A.sc[kScStatus] = double(int(A.sc[kScStatusK]) | (ok ? 0 : kStAFailed));
+  }
+  DC_STAMP(4);
+}
+
+// K2: L^-1, A^-1 = W^T W, G G^T, the bound terms and status, d Phi (U) as the psi2 backward's operands.
+__global__ void __launch_bounds__(1024) bound_u_small_kernel(DcArgs A, float* __restrict__ u,
+                                                             double* __restrict__ u64) {
+  extern __shared__ double sm[];
+  __shared__ double red[1024];
+  const int m = A.m, d = A.d, mv = A.mv;
+  double* L = sm;
+  double* W = sm + m * m;
+  const double* packed = A.packed;
+  const double beta = A.beta;
+  const bool ok = !(int(A.sc[kScStatus]) & kStAFailed);
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) L[e] = A.la[e];
+  __syncthreads();
+  if (ok) {
+    trinv_warp_smem(L, W, m);
+    __syncthreads();
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) A.wa[e] = W[(e % m) * m + e / m];  // L_a^-1 (prediction)
+    __syncthreads();
+    wtw_smem(W, m, L, A.ainv);  // A^-1 into shared memory (over L) and global
+  }
+  __syncthreads();
+  // G G^T with G (K1's output) staged over W when it fits
+  double* gs = d <= m ? W : nullptr;
+  if (gs)
+    for (int e = threadIdx.x; e < m * d; e += blockDim.x) gs[e] = A.g[e];
+  __syncthreads();
+  const double* gg = gs ? gs : A.g;
+  mma_gemm(
+      m, m, d, gg, 1, m, gg, m, 1, [&](int i, int j, double v) { A.ggt[i + j * m] = v; });
+  __syncthreads();
+  double kp = 0.0, ap = 0.0;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const double ph = A.phi[e];
+    kp += A.kinv[e] * ph;
+    ap += L[e] * ph;
+  }
+  kp = block_sum_s(kp, red);
+  ap = block_sum_s(ap, red);
+  if (threadIdx.x == 0) {
+    double* sc = A.sc;
+    int st = int(sc[kScStatus]);
+    const double nd = double(A.n), dd = double(d);
+    const double phi0 = packed[0], yy = packed[1], nc = packed[2], kl = packed[3];
+    if (!(nc == nd)) st |= kStBadCount;
+    if (!(phi0 >= 0.0 && yy >= 0.0)) st |= kStBadStats;
+    double* bd = sc + kScBound;
+    const double pg = sc[kScPg];
+    bd[1] = dd * (0.5 * nd * log(beta) + 0.5 * sc[kScLogDetK] - 0.5 * nd * kLog2Pi - 0.5 * sc[kScLogDetA]);
+    bd[2] = -0.5 * beta * yy;
+    bd[3] = 0.5 * beta * beta * pg;
+    bd[4] = -0.5 * beta * dd * phi0;
+    bd[5] = 0.5 * beta * dd * kp;
+    bd[6] = A.latent ? -kl : 0.0;
+    bd[0] = bd[1] + bd[2] + bd[3] + bd[4] + bd[5] + bd[6];
+    if (!isfinite(bd[0])) st |= kStNonFinite;
+    sc[kScKp] = kp;
+    sc[kScAp] = ap;
+    sc[kScDPhi] = -0.5 * beta * dd;
+    sc[kScStatus] = double(st);
+  }
+  __syncthreads();
+  const double dd = double(d);
+  for (int e = threadIdx.x; e < mv * mv; e += blockDim.x) {  // bound.hpp:203-210
+    const int i = e % mv, j = e / mv;
+    double v = 0.0;
+    if (i < m && j < m) {
+      const int k = i + j * m;
+      v = -0.5 * beta * dd * L[k] - 0.5 * beta * beta * beta * A.ggt[k] + 0.5 * beta * dd * A.kinv[k];
+    }
+    u[e] = float(v);
+    u64[e] = v;
+  }
+}
+
 __global__ void dc_prof_kernel(long long* out) {
   if (threadIdx.x < 16) out[threadIdx.x] = g_dc_prof[threadIdx.x];
 }
@@ -565,25 +907,79 @@ __global__ void __launch_bounds__(1024) deferred_small_kernel(DcArgs A) {
     T[e] = A.phi[e];
   }
   __syncthreads();
-  tile_gemm(  // Phi G
-      m, d, m, [&](int i, int p) { return T[i + p * m]; }, [&](int p, int j) { return __ldg(A.g + int64_t(j) * m + p); },
-      [&](int i, int j, double v) { A.phig[i + int64_t(j) * m] = v; });
-  tile_gemm(  // tmp = Kmm^-1 Phi
-      m, m, m, [&](int i, int p) { return K[i + p * m]; }, [&](int p, int j) { return T[p + j * m]; },
-      [&](int i, int j, double v) { A.tmp[i + j * m] = v; });
+  mma_gemm(  // Phi G
+      m, d, m, T, 1, m, A.g, 1, m, [&](int i, int j, double v) { A.phig[i + int64_t(j) * m] = v; });
+  mma_gemm(  // tmp = Kmm^-1 Phi
+      m, m, m, K, 1, m, T, 1, m, [&](int i, int j, double v) { A.tmp[i + j * m] = v; });
   __syncthreads();
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) T[e] = A.tmp[e];
   __syncthreads();
-  tile_gemm(  // kpk = tmp Kmm^-1
-      m, m, m, [&](int i, int p) { return T[i + p * m]; }, [&](int p, int j) { return K[p + j * m]; },
-      [&](int i, int j, double v) { A.kpk[i + j * m] = v; });
+  mma_gemm(  // kpk = tmp Kmm^-1
+      m, m, m, T, 1, m, K, 1, m, [&](int i, int j, double v) { A.kpk[i + j * m] = v; });
   __syncthreads();
   const double beta = A.beta, dd = double(d);
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
     const int i = e % m, j = e / m;
     const double kpk = 0.5 * (A.kpk[e] + A.kpk[j + i * m]);
-    A.dkmm[e] = 0.5 * dd * A.kinv[e] - 0.5 * dd * A.ainv[e] - 0.5 * beta * beta * A.ggt[e] - 0.5 * beta * dd * kpk;
+    const double dk =
+        0.5 * dd * A.kinv[e] - 0.5 * dd * A.ainv[e] - 0.5 * beta * beta * A.ggt[e] - 0.5 * beta * dd * kpk;
+    A.dkmm[e] = dk;
+    K[e] = dk * A.kmm[e];  // W = d Kmm o K (kern_grads(Z, Z, d Kmm), kernels.hpp:124-164)
   }
+  __syncthreads();
+  // everything of the assembly (parallel.hpp:414-421) that does not depend on the backward's
+  // statistics, into A.result; finish_add_kernel adds the psi gradients
+  __shared__ double red[1024];
+  const int q = A.q, mq = m * q;
+  double* rs = A.rs;
+  for (int a = threadIdx.x; a < m; a += blockDim.x) {  // row sums of W, ascending b
+    double r = 0.0;
+    for (int b = 0; b < m; ++b) r += K[a + b * m];
+    rs[a] = r;
+  }
+  mma_gemm(m, q, m, K, 1, m, A.z, 1, m, [&](int i, int j, double v) { A.wz[i + j * m] = v; });  // W Z
+  __syncthreads();
+  double tg = 0.0;  // tr(G^T Phi G)
+  for (int64_t e = threadIdx.x; e < int64_t(m) * d; e += blockDim.x) tg += A.g[e] * A.phig[e];
+  tg = block_sum(tg, red);
+  double tot = 0.0, tr = 0.0;  // sum W, trace of d Kmm
+  for (int a = threadIdx.x; a < m; a += blockDim.x) {
+    tot += rs[a];
+    tr += A.dkmm[a + a * m];
+  }
+  tot = block_sum(tot, red);
+  tr = block_sum(tr, red);
+  double* res = A.result;  // [d var, d l (Q), d Z (M Q), d beta]
+  for (int e = threadIdx.x; e < mq; e += blockDim.x) {
+    const int a = e % m, j = e / m;
+    const double il2 = 1.0 / (A.ls[j] * A.ls[j]);
+    res[1 + q + e] = 2.0 * (A.wz[e] - rs[a] * A.z[e]) * il2;
+  }
+  // sum_ab W_ab (z_a - z_b)^2 = 2 (sum_a rs_a z_a^2 - z^T W z) per dimension (a warp per q, fixed tree)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = warp; j < q; j += blockDim.x >> 5) {
+    double s2 = 0.0, cross = 0.0;
+    for (int a = lane; a < m; a += 32) {
+      const double za = A.z[a + j * m];
+      s2 += rs[a] * za * za;
+      cross += za * A.wz[a + j * m];
+    }
+    s2 = dev_warp_sum(s2);
+    cross = dev_warp_sum(cross);
+    if (lane == 0) res[1 + j] = 2.0 * (s2 - cross) / (A.ls[j] * A.ls[j] * A.ls[j]);
+  }
+  if (threadIdx.x == 0) {
+    const double* sc = A.sc;
+    const double nd = double(A.n), yy = A.packed[1], phi0 = A.packed[0];
+    res[0] = tot / A.var + sc[kScJitterFactor] * tr;
+    res[1 + q + mq] = 0.5 * dd * nd / beta - 0.5 * dd * sc[kScAp] - 0.5 * yy + beta * sc[kScPg] -
+                      0.5 * beta * beta * tg - 0.5 * dd * phi0 + 0.5 * dd * sc[kScKp];
+  }
+}
+
+// final gradient vector = the coordinator's terms (deferred_small_kernel) + the psi gradients
+__global__ void finish_add_kernel(double* __restrict__ res, const double* __restrict__ pgrads, int count) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < count; e += gridDim.x * blockDim.x) res[e] += pgrads[e];
 }
 
 __global__ void init_status_kernel(double* sc, const int* info_k) {
@@ -639,6 +1035,7 @@ void dc_bind(DcArgs& A, double* ws) {
 }
 
 size_t small_smem(int m) { return sizeof(double) * 2 * size_t(m) * m; }
+size_t g_small_smem(int m) { return sizeof(double) * (size_t(m) * m + size_t(m) * size_t(m | 1)); }
 
 int dc_prefactor(const DcArgs& A, cudaStream_t st) {
   const int m = A.m;
@@ -689,6 +1086,30 @@ int dc_bound(const DcArgs& A, float* u, float* dpsi, double* u64, double* dpsi64
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
+int dc_bound_split(const DcArgs& A, float* u, float* dpsi, double* u64, double* dpsi64, cudaStream_t st,
+                   cudaStream_t side, cudaEvent_t ev_g, cudaEvent_t ev_u) {
+  const int m = A.m;
+  if (m > kSmallM || !side) {  // one stream: the whole coordinator before the backward
+    if (int rc = dc_bound(A, u, dpsi, u64, dpsi64, st)) return rc;
+    if (int rc = dc_deferred(A, st)) return rc;
+    if (cudaEventRecord(ev_g, st) != cudaSuccess || cudaEventRecord(ev_u, st) != cudaSuccess) return 3;
+    return 0;
+  }
+  const int smax = int(small_smem(kSmallM));
+  if (cudaFuncSetAttribute(bound_g_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(g_small_smem(kSmallM))) != cudaSuccess ||
+      cudaFuncSetAttribute(bound_u_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smax) != cudaSuccess ||
+      cudaFuncSetAttribute(deferred_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smax) != cudaSuccess)
+    return 3;
+  bound_g_small_kernel<<<1, 1024, g_small_smem(m), st>>>(A, dpsi, dpsi64);
+  if (cudaEventRecord(ev_g, st) != cudaSuccess || cudaStreamWaitEvent(side, ev_g, 0) != cudaSuccess) return 3;
+  bound_u_small_kernel<<<1, 1024, small_smem(m), side>>>(A, u, u64);
+  deferred_small_kernel<<<1, 1024, small_smem(m), side>>>(A);
+  if (cudaEventRecord(ev_u, side) != cudaSuccess) return 3;
+  g_tc_launches.fetch_add(3);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
 int dc_deferred(const DcArgs& A, cudaStream_t st) {
   const int m = A.m, d = A.d;
   if (m <= kSmallM) {
@@ -709,6 +1130,11 @@ int dc_deferred(const DcArgs& A, cudaStream_t st) {
 
 int dc_finish(const DcArgs& A, const double* pgrads, cudaStream_t st) {
   const int m = A.m;
+  if (m <= kSmallM) {  // deferred_small_kernel formed the rest of the assembly
+    finish_add_kernel<<<1, 256, 0, st>>>(A.result, pgrads, 1 + A.q + m * A.q);
+    g_tc_launches.fetch_add(1);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  }
   w_kernel<<<blocks_for(int64_t(m) * m), 256, 0, st>>>(A);
   rowsum_kernel<<<(m + 127) / 128, 128, 0, st>>>(A);
   g_tc_launches.fetch_add(2);

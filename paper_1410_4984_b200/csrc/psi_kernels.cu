@@ -245,8 +245,10 @@ int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, 
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
+bool psi_backward_phased(const PsiConst& P) { return !is_syrk(P) && !is_direct(P); }
+
 int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
-                 LaunchGeom* geom, void* ev_begin, void* ev_end) {
+                 LaunchGeom* geom, void* ev_begin, void* ev_end, int phase) {
   if (!B.fwd_rt) return 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   LaunchGeom g{};
@@ -267,11 +269,14 @@ int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* pac
   }
   const int64_t pstride = bwd_part_count(P.m, P.q);
   const int r1 = P.n > 0 ? psi1_bwd_rows(P, num_sms) : 0, rows = r1 + 1;
-  if (cudaMemsetAsync(part, 0, sizeof(double) * pstride * rows, st) != cudaSuccess) return 3;
-  if (ev_begin) record_event(ev_begin, st);
-  // psi1 first: it writes d_mu / d_s (psi1 + KL parts); the psi2 kernel accumulates into them
-  if (r1 > 0) {
-    if (int rc = psi1_backward(P, B, part, pstride, r1, stream)) return rc;
+  if (phase != 2) {
+    if (cudaMemsetAsync(part, 0, sizeof(double) * pstride * rows, st) != cudaSuccess) return 3;
+    if (ev_begin) record_event(ev_begin, st);
+    // psi1 first: it writes d_mu / d_s (psi1 + KL parts); the psi2 kernel accumulates into them
+    if (r1 > 0) {
+      if (int rc = psi1_backward(P, B, part, pstride, r1, stream)) return rc;
+    }
+    if (phase == 1) return cudaGetLastError() == cudaSuccess ? 0 : 3;
   }
   if (int rc = rt_backward(P, B, part + int64_t(rows) * pstride, part + int64_t(r1) * pstride, num_sms, stream))
     return rc;

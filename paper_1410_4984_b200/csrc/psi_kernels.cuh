@@ -115,8 +115,12 @@ int plan_backward(const PsiConst& P, int num_sms, LaunchGeom* geom);
 // recorded around the psi kernels so callers can time them alone (roofline evidence).
 int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, int num_sms,
                 void* stream, LaunchGeom* geom, void* ev_begin = nullptr, void* ev_end = nullptr);
+// phase (row-tile path only): 0 the whole pass, 1 the psi1 kernel alone (it needs d Psi, not d Phi),
+// 2 the rest (psi2 kernels, reduction) -- so a caller can overlap the coordinator's d Phi with phase 1.
 int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
-                 LaunchGeom* geom, void* ev_begin = nullptr, void* ev_end = nullptr);
+                 LaunchGeom* geom, void* ev_begin = nullptr, void* ev_end = nullptr, int phase = 0);
+// true when psi_backward can run in two phases for P (the row-tile path)
+bool psi_backward_phased(const PsiConst& P);
 // Where the forward left the region the backward reads (BwdConst::fwd_rt), and the per-pair sums
 // inside it: sub-shard forwards add theirs into the first sub-shard's before the gradient pass.
 const double* fwd_region(const PsiConst& P, const double* fwd_part, int num_sms);

@@ -361,6 +361,12 @@ struct sgpx_engine {
   DcArgs dc{};
   HostBuf h_dc;
   cudaEvent_t ev_c[2] = {};
+  // split device coordinator (dc_bound_split): d Psi first on the stream, d Phi / d Kmm on a side stream
+  // concurrently with the psi1 backward; split_join = the stream still has to wait for ev_split[1]
+  bool coord_split = true;
+  bool split = false, split_join = false;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_split[2] = {};
   // one evaluation (device-resident shard, device coordinator) as a CUDA graph, replayed while its
   // launch arguments are unchanged (graph_key)
   bool use_graph = true;
@@ -375,6 +381,9 @@ struct sgpx_engine {
       if (e) cudaEventDestroy(e);
     for (auto& e : ev_c)
       if (e) cudaEventDestroy(e);
+    for (auto& e : ev_split)
+      if (e) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
     if (graph) cudaGraphExecDestroy(graph);
     for (auto e : ev_in) cudaEventDestroy(e);
     for (auto e : ev_out) cudaEventDestroy(e);
@@ -565,16 +574,27 @@ void engine_coordinate(sgpx_engine* e, bool with_grads) {
     e->u64.ensure(sizeof(double) * e->P.mv * e->P.mv);
     e->dpsi64.ensure(sizeof(double) * std::max(1, e->P.d) * e->P.mv);
     CUDA_OK(record_event(e->ev_c[0], ctx->stream));
-    if (dc_bound(e->dc, e->u.get<float>(), e->dpsi.get<float>(), e->u64.get<double>(), e->dpsi64.get<double>(),
-                 ctx->stream))
+    e->split = e->coord_split && e->cfg.m <= 112;
+    if (e->split) {
+      if (!e->side) CUDA_OK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+      for (auto& ev : e->ev_split)
+        if (!ev) CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      if (dc_bound_split(e->dc, e->u.get<float>(), e->dpsi.get<float>(), e->u64.get<double>(), e->dpsi64.get<double>(),
+                         ctx->stream, e->side, e->ev_split[0], e->ev_split[1]))
+        throw CudaError("coordinator launch");
+      e->split_join = true;
+    } else if (dc_bound(e->dc, e->u.get<float>(), e->dpsi.get<float>(), e->u64.get<double>(), e->dpsi64.get<double>(),
+                        ctx->stream)) {
       throw CudaError("coordinator launch");
-    CUDA_OK(record_event(e->ev_c[1], ctx->stream));
+    }
+    CUDA_OK(record_event(e->ev_c[1], ctx->stream));  // the coordinator's critical path (d Psi when split)
     e->res.adj.d_phi = -0.5 * e->beta * double(e->cfg.d);  // adjoints_from_core (bound.hpp:203)
     e->with_grads = with_grads;
     e->coordinated = true;
     return;
   }
   sgpx_ctx* ctx = e->ctx;
+  e->split = e->split_join = false;
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t count = sgpx_packed_stats_count(e->cfg.m, e->cfg.d);
   e->h_stats.ensure(sizeof(double) * count);
@@ -617,12 +637,24 @@ void engine_grad_pass(sgpx_engine* e) {
   e->dmu.ensure(sizeof(double) * std::max<int64_t>(1, e->in.n * e->cfg.q));
   e->ds.ensure(sizeof(double) * std::max<int64_t>(1, e->in.n * e->cfg.q));
   CUDA_OK(record_event(e->ev[2], ctx->stream));
+  auto join = [&] {  // d Phi / d Kmm of the split coordinator (side stream) before their consumers
+    if (e->split_join) {
+      CUDA_OK(cudaStreamWaitEvent(ctx->stream, e->ev_split[1], 0));
+      e->split_join = false;
+    }
+  };
   if (e->in.n > 0) {
     const int k = int(e->subs.size());
+    // split coordinator: every psi1 kernel (it needs d Psi only) first, on all SMs but the one the side
+    // stream's coordinator kernel occupies, then d Phi is joined and the psi2 kernels run
+    bool phased = e->split_join;
+    for (auto& sub : e->subs) phased = phased && psi_backward_phased(sub.P);
+    const int nsm = phased ? std::max(1, ctx->num_sms - 1) : ctx->num_sms;
+    if (!phased) join();
     int64_t boff = 0;
     for (auto& sub : e->subs) {
       LaunchGeom g{};
-      if (plan_backward(sub.P, ctx->num_sms, &g)) throw CudaError("psi backward: launch planning failed");
+      if (plan_backward(sub.P, nsm, &g)) throw CudaError("psi backward: launch planning failed");
       sub.boff = boff;
       boff += bwd_part_count(sub.P.m, sub.P.q) * std::max(1, g.grid);
     }
@@ -649,8 +681,7 @@ void engine_grad_pass(sgpx_engine* e) {
       CUDA_OK(cudaGetLastError());
     }
     const bool stream_out = e->has_gout && e->latent;
-    for (int j = 0; j < k; ++j) {
-      auto& sub = e->subs[j];
+    auto bconst = [&](const sgpx_engine::Sub& sub, int j) {
       BwdConst B{};
       B.u = e->u.get<float>();
       B.dpsi = e->dpsi.get<float>();
@@ -664,11 +695,26 @@ void engine_grad_pass(sgpx_engine* e) {
       B.ld_g = e->in.n;
       B.fwd_rt = fwd_region(sub.P, e->fpart.get<double>() + sub.foff, ctx->num_sms);
       B.skip_pair_terms = (fold && j > 0) ? 1 : 0;
-      double* out = k > 1 ? e->pgrads_sub.get<double>() + int64_t(j) * count : e->pgrads.get<double>();
+      return B;
+    };
+    auto out_of = [&](int j) {
+      return k > 1 ? e->pgrads_sub.get<double>() + int64_t(j) * count : e->pgrads.get<double>();
+    };
+    if (phased) {
+      for (int j = 0; j < k; ++j) {
+        auto& sub = e->subs[j];
+        if (psi_backward(sub.P, bconst(sub, j), e->bpart.get<double>() + sub.boff, out_of(j), nsm, ctx->stream, &e->gb,
+                         j == 0 ? e->ev[6] : nullptr, nullptr, 1))
+          throw CudaError(std::string("psi backward launch: ") + cudaGetErrorString(cudaGetLastError()));
+      }
+      join();
+    }
+    for (int j = 0; j < k; ++j) {
+      auto& sub = e->subs[j];
       sub.P.ev_psi2[0] = j == 0 ? e->ev[10] : nullptr;
       sub.P.ev_psi2[1] = j == 0 ? e->ev[11] : nullptr;
-      if (psi_backward(sub.P, B, e->bpart.get<double>() + sub.boff, out, ctx->num_sms, ctx->stream, &e->gb,
-                       j == 0 ? e->ev[6] : nullptr, j == k - 1 ? e->ev[7] : nullptr))
+      if (psi_backward(sub.P, bconst(sub, j), e->bpart.get<double>() + sub.boff, out_of(j), nsm, ctx->stream, &e->gb,
+                       (j == 0 && !phased) ? e->ev[6] : nullptr, j == k - 1 ? e->ev[7] : nullptr, phased ? 2 : 0))
         throw CudaError(std::string("psi backward launch: ") + cudaGetErrorString(cudaGetLastError()));
       if (stream_out) {  // d mu / d S of this sub-shard are final: copy them out while the next runs
         const int64_t q = e->cfg.q, n = e->cfg.n_local;
@@ -687,11 +733,12 @@ void engine_grad_pass(sgpx_engine* e) {
       CUDA_OK(cudaGetLastError());
     }
   } else {
+    join();
     CUDA_OK(cudaMemsetAsync(e->pgrads.p, 0, sizeof(double) * count, ctx->stream));
   }
   CUDA_OK(record_event(e->ev[3], ctx->stream));
   if (e->dev_coord) {  // d Kmm, Phi G for the assembly, behind the gradient kernels on the stream
-    if (dc_deferred(e->dc, ctx->stream)) throw CudaError("coordinator launch");
+    if (!e->split && dc_deferred(e->dc, ctx->stream)) throw CudaError("coordinator launch");
     return;
   }
   // host-only adjoints, overlapping the kernels just enqueued
@@ -704,6 +751,10 @@ void engine_grad_pass(sgpx_engine* e) {
 // stream part: the assembly kernel and the read-back copies (captured into the evaluation's graph)
 void engine_finish_enqueue(sgpx_engine* e) {
   sgpx_ctx* ctx = e->ctx;
+  if (e->split_join) {  // bound-only evaluation: the side stream's bound terms
+    CUDA_OK(cudaStreamWaitEvent(ctx->stream, e->ev_split[1], 0));
+    e->split_join = false;
+  }
   const int64_t m = e->cfg.m, q = e->cfg.q, d = e->cfg.d;
   const DcArgs& dc = e->dc;
   if (e->with_grads && dc_finish(dc, e->pgrads.get<double>(), ctx->stream)) throw CudaError("coordinator launch");
@@ -1231,6 +1282,7 @@ int sgpx_engine_create(sgpx_ctx* ctx, const sgpx_engine_config* cfg, sgpx_engine
     // above it the host's O(M^3) algebra grows past the device's blocked kernels (M = 500: 19 ms vs 3 ms)
     e->dev_coord = cfg->m > 112;
     if (const char* dc = getenv("SGPX_DEVICE_COORD")) e->dev_coord = atoi(dc) != 0;  // A/B
+    if (const char* sp = getenv("SGPX_COORD_SPLIT")) e->coord_split = atoi(sp) != 0;  // A/B
     if (const char* gr = getenv("SGPX_GRAPH")) e->use_graph = atoi(gr) != 0;       // A/B: per-call launches
     *out = e.release();
   });
