@@ -564,59 +564,33 @@ __global__ void __launch_bounds__(1024) bound_small_kernel(DcArgs A, float* __re
 // ---------------------------------------------------------------------------------------------
 // Split small-M coordinator: the backward's psi1 kernel needs only d Psi = beta^2 G, so
 //   K1 (bound_g_small_kernel, on the evaluation's stream): A = Kmm + jitter + beta Phi, factor_spd
-//       escalation, log|A|, G = A^-1 Psi by two triangular solves, d Psi, <Psi, G>;
+//       escalation, log|A|, G = A^-1 Psi, d Psi, <Psi, G>;
 //   K2 (bound_u_small_kernel, on a side stream, concurrent with the psi1 backward): L^-1, A^-1, G G^T,
 //       the bound terms and d Phi (= U, the psi2 backward's operand); then deferred_small_kernel.
-// K1's Cholesky is column-cyclic and dataflow-ordered: warp w owns columns w, w + 32, ... in registers
-// (lane l rows l + 32 u); column k is finalised (sqrt, scale) by its owner right after its last update
-// and published through shared memory with an mbarrier per column, so the critical path is one
-// update + one finalisation per column, with no block-wide barrier.
+// K1 is a blocked right-looking Cholesky with 32-column panels: one warp factors the diagonal block,
+// the 32 warps invert it (a warp per column), and the panel below (TRSM, as A_21 D^-T), the trailing
+// update (SYRK) and both triangular solves for G are fp64 tensor-core GEMMs -- a block-wide barrier
+// per phase instead of one per column, and ~8x fewer instructions than per-element updates.
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ void mb_init(uint64_t* b) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(b))));
-}
-__device__ __forceinline__ void mb_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(b)))
-               : "memory");
-}
-__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done)
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, "
-        "0, p;\n\t}"
-        : "=r"(done)
-        : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(b))), "r"(parity)
-        : "memory");
-}
-template <int N>
-__device__ __forceinline__ double pick(const double (&v)[N], int u) {
-  double r = v[0];
-#pragma unroll
-  for (int t = 1; t < N; ++t)
-    if (u == t) r = v[t];
-  return r;
-}
-template <int N>
-__device__ __forceinline__ void put(double (&v)[N], int u, double x) {
-#pragma unroll
-  for (int t = 0; t < N; ++t)
-    if (u == t) v[t] = x;
+constexpr int kG1Rhs = 64;      // right-hand-side columns per solve chunk
+constexpr int kG1Threads = 512;  // 128 registers: the diagonal block lives in one warp's registers
+size_t g_small_smem(int m) {  // L (m x m), D^-1 blocks (4 x 32 x 32), X (m x kG1Rhs), Tmp (max(m, 64) x 32)
+  return sizeof(double) * (size_t(m) * m + 4 * 32 * 32 + size_t(m) * kG1Rhs + size_t(std::max(m, 64)) * 32);
 }
 
-__global__ void __launch_bounds__(1024) bound_g_small_kernel(DcArgs A, float* __restrict__ dpsi,
+__global__ void __launch_bounds__(kG1Threads) bound_g_small_kernel(DcArgs A, float* __restrict__ dpsi,
                                                              double* __restrict__ dpsi64) {
   extern __shared__ double sm[];
-  __shared__ uint64_t ready[128];
   __shared__ double red[1024];
-  __shared__ double invd[128], logd[128];
-  __shared__ volatile int s_fail;
+  __shared__ double invd[128], diag[128];
+  __shared__ int s_fail;
   const int m = A.m, d = A.d, mv = A.mv;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int lrs = m | 1;    // odd row stride: conflict-free column writes / row reads of Lr
-  double* L = sm;           // column-major factor, zero above the diagonal
-  double* Lr = sm + m * m;  // Lr[k lrs + i] = L(k, i) (rows of L, for the transposed solve)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nt = blockDim.x;
+  const int nb = (m + 31) / 32;
+  double* L = sm;                  // A, factored in place (lower triangle)
+  double* Wd = L + m * m;          // inverse of diagonal block b at Wd + 1024 b (32 x 32, column-major, lower)
+  double* X = Wd + 4 * 1024;       // m x kG1Rhs right-hand sides (leading dimension m)
+  double* Tmp = X + m * kG1Rhs;    // m x 32 scratch
   const double* packed = A.packed;
   const double* psi = packed + 4 + int64_t(m) * (m + 1) / 2;
   const double beta = A.beta, jit = A.sc[kScJitterFactor] * A.var;
@@ -625,19 +599,16 @@ __global__ void __launch_bounds__(1024) bound_g_small_kernel(DcArgs A, float* __
     return packed[4 + int64_t(lo) * m - int64_t(lo) * (lo - 1) / 2 + (hi - lo)];
   };
   DC_STAMP(0);
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    A.phi[e] = phi_at(e % m, e / m);  // dense Phi (K2, deferred)
-    L[e] = 0.0;                       // the factor's upper triangle
-  }
+  for (int e = threadIdx.x; e < m * m; e += nt) A.phi[e] = phi_at(e % m, e / m);  // dense Phi (K2, deferred)
   double f = 0.0, scale = 0.0;  // factor_spd escalation (bound.hpp:52-62): shift f * max |a_ii|
   bool ok = false;
   for (int attempt = 0; attempt < 32; ++attempt) {
     if (attempt == 1) {  // the matrix's own scale, needed from the first retry on
       double mx = 0.0;
-      for (int i = threadIdx.x; i < m; i += blockDim.x) mx = fmax(mx, fabs(A.kmm[i + i * m] + jit + beta * phi_at(i, i)));
+      for (int i = threadIdx.x; i < m; i += nt) mx = fmax(mx, fabs(A.kmm[i + i * m] + jit + beta * phi_at(i, i)));
       red[threadIdx.x] = mx;
       __syncthreads();
-      for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+      for (int w = nt / 2; w > 0; w >>= 1) {
         if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
         __syncthreads();
       }
@@ -645,82 +616,82 @@ __global__ void __launch_bounds__(1024) bound_g_small_kernel(DcArgs A, float* __
       __syncthreads();
     }
     const double shift = f * scale;
-    if (attempt == 0 && threadIdx.x < m) mb_init(&ready[threadIdx.x]);  // each attempt completes every barrier once
+    for (int e = threadIdx.x; e < m * m; e += nt) {
+      const int i = e % m, j = e / m;
+      L[e] = A.kmm[e] + beta * phi_at(i, j) + (i == j ? jit + shift : 0.0);
+    }
+    for (int e = threadIdx.x; e < 4 * 1024; e += nt) Wd[e] = 0.0;
     if (threadIdx.x == 0) s_fail = 0;
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
-    const uint32_t par = uint32_t(attempt & 1);
-    // this warp's columns c = warp + 32 cc in registers (rows lane + 32 u)
-    double x[4][4];
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc)
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int c = warp + 32 * cc, i = lane + 32 * u;
-        x[cc][u] = (c < m && i < m) ? A.kmm[i + int64_t(c) * m] + beta * phi_at(i, c) + (i == c ? jit + shift : 0.0)
-                                    : 0.0;
-      }
-    // finalise column k (slot cc of this warp): l_kk = sqrt(a_kk), scale below, publish
-    auto finalise = [&](int k, double (&v)[4]) {
-      const double dkk = __shfl_sync(0xffffffffu, pick(v, k >> 5), k & 31);
-      const bool bad = !(dkk > 0.0);
-      const double lkk = bad ? 1.0 : sqrt(dkk), inv = 1.0 / lkk;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (32 * u + 31 < k) continue;  // rows above the diagonal stay zero (warp-uniform)
-        const int i = lane + 32 * u;
-        v[u] = i > k ? v[u] * inv : (i == k ? lkk : 0.0);
-        if (i < m && i >= k) {
-          L[i + k * m] = v[u];
-          Lr[i * lrs + k] = v[u];
-        }
-      }
-      if (lane == 0) {
-        invd[k] = inv;
-        logd[k] = lkk;  // log taken after the factorisation (off the critical path)
-        if (bad) s_fail = 1;
-      }
-      __syncwarp();
-      if (lane == 0) mb_arrive(&ready[k]);
-    };
     DC_STAMP(1);
-    if (warp == 0) finalise(0, x[0]);
-    const int last = warp < m ? warp + 32 * ((m - 1 - warp) / 32) : -1;  // this warp's last column
-    for (int k = 0; k + 1 < m && k < last; ++k) {
-      mb_wait(&ready[k], par);  // column k published (a no-op wait for its owner)
-      const int k1 = k + 1;
-      if (s_fail) {  // a pivot failed: the owners still publish every later column (no waiter is left behind)
-        if ((k1 & 31) == warp && lane == 0) mb_arrive(&ready[k1]);
-        continue;
-      }
-      // the owner of column k + 1 applies column k to it first, then finalises and publishes it
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        const int c = warp + 32 * cc;
-        if (c == k1) {
-          const double lck = L[c + k * m];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (32 * u + 31 < c) continue;
-            const int i = lane + 32 * u;
-            if (i >= c && i < m) x[cc][u] -= L[i + k * m] * lck;
+    for (int b = 0; b < nb; ++b) {
+      const int j0 = 32 * b, jb = min(32, m - j0), mr = m - j0 - jb;
+      double* Lp = L + j0 + j0 * m;  // the diagonal block
+      if (warp == 0) {  // (1) factor the diagonal block: right-looking inside one warp (lane = row, in place)
+        const int r = lane;
+        for (int k = 0; k < jb; ++k) {
+          const double dkk = Lp[k + k * m];
+          const bool bad = !(dkk > 0.0);
+          const double lkk = bad ? 1.0 : sqrt(dkk), inv = 1.0 / lkk;
+          double lrk = 0.0;
+          if (r > k && r < jb) {
+            lrk = Lp[r + k * m] * inv;
+            Lp[r + k * m] = lrk;
           }
-          finalise(k1, x[cc]);
+          if (r == k) {
+            Lp[k + k * m] = lkk;
+            invd[j0 + k] = inv;
+            diag[j0 + k] = lkk;
+            if (bad) s_fail = 1;
+          }
+          __syncwarp();
+          // row r, columns k + 1 .. r: four at a time, every load before its stores (independent updates)
+          if (r > k && r < jb) {
+            int c = k + 1;
+            for (; c + 3 <= r; c += 4) {
+              const double l0 = Lp[c + k * m], l1 = Lp[c + 1 + k * m], l2 = Lp[c + 2 + k * m], l3 = Lp[c + 3 + k * m];
+              const double a0 = Lp[r + c * m], a1 = Lp[r + (c + 1) * m], a2 = Lp[r + (c + 2) * m], a3 = Lp[r + (c + 3) * m];
+              Lp[r + c * m] = fma(-lrk, l0, a0);
+              Lp[r + (c + 1) * m] = fma(-lrk, l1, a1);
+              Lp[r + (c + 2) * m] = fma(-lrk, l2, a2);
+              Lp[r + (c + 3) * m] = fma(-lrk, l3, a3);
+            }
+            for (; c <= r; ++c) Lp[r + c * m] = fma(-lrk, Lp[c + k * m], Lp[r + c * m]);
+          }
+          __syncwarp();
         }
       }
-      // column k into this warp's later columns
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        const int c = warp + 32 * cc;
-        if (c > k1 && c < m) {
-          const double lck = L[c + k * m];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (32 * u + 31 < c) continue;
-            const int i = lane + 32 * u;
-            if (i >= c && i < m) x[cc][u] -= L[i + k * m] * lck;
-          }
+      __syncthreads();
+      if (b == 0) DC_STAMP(5);
+      if (s_fail) break;
+      // (2) D^-1: a warp per column c, the block's 32 rows one per lane
+      double* W = Wd + 1024 * b;
+      for (int c = warp; c < jb; c += nt / 32) {
+        double x = lane == c ? 1.0 : 0.0;
+        for (int k = c; k < jb; ++k) {
+          const double xk = __shfl_sync(0xffffffffu, x, k) * invd[j0 + k];
+          if (lane == k) x = xk;
+          if (lane > k && lane < jb) x -= Lp[lane + k * m] * xk;
         }
+        W[lane + 32 * c] = (lane >= c && lane < jb) ? x : 0.0;
+      }
+      __syncthreads();
+      if (b == 0) DC_STAMP(6);
+      if (mr > 0) {
+        // (3) panel below: L_21 = A_21 D^-T  (Tmp, mr x jb)
+        double* A21 = L + (j0 + jb) + j0 * m;
+        mma_gemm(mr, jb, jb, A21, 1, m, W, 32, 1, [&](int i, int j, double v) { Tmp[i + j * mr] = v; });
+        __syncthreads();
+        for (int e = threadIdx.x; e < mr * jb; e += nt) A21[(e % mr) + (e / mr) * m] = Tmp[e];
+        __syncthreads();
+        if (b == 0) DC_STAMP(7);
+        // (4) trailing update A_22 -= L_21 L_21^T (lower triangle)
+        double* A22 = L + (j0 + jb) + (j0 + jb) * m;
+        mma_gemm(mr, mr, jb, A21, 1, m, A21, m, 1, [&](int i, int j, double v) {
+          if (i >= j) A22[i + j * m] -= v;
+        });
+        __syncthreads();
+        if (b == 0) DC_STAMP(8);
       }
     }
     __syncthreads();
@@ -731,83 +702,60 @@ __global__ void __launch_bounds__(1024) bound_g_small_kernel(DcArgs A, float* __
     if (!(f <= 1e-2)) break;
   }
   DC_STAMP(2);
-  // log |A| (fixed-order tree, the same as factor_smem's)
+  // log |A| (fixed-order tree over log l_ii)
   double s = 0.0;
   if (ok)
-    for (int i = threadIdx.x; i < m; i += blockDim.x) s += log(logd[i]);
+    for (int i = threadIdx.x; i < m; i += nt) s += log(diag[i]);
   s = block_sum_s(s, red);
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) A.la[e] = L[e];  // K2 (L^-1) and prediction
-  // G = L^-T L^-1 Psi: a warp per right-hand side (two at a time), column-oriented substitutions
-  for (int j0 = 2 * warp; j0 < d; j0 += 2 * (blockDim.x >> 5)) {
-    const int nj = min(2, d - j0);
-    double xv[2][4];
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = lane + 32 * u;
-        xv[r][u] = (r < nj && i < m) ? psi[i + int64_t(j0 + r) * m] : 0.0;
-      }
-    if (ok) {
-      for (int k = 0; k < m; ++k) {  // L y = psi
-        const double ik = invd[k];
-        double yk[2];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          yk[r] = __shfl_sync(0xffffffffu, pick(xv[r], k >> 5), k & 31) * ik;
-          if (lane == (k & 31)) put(xv[r], k >> 5, yk[r]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (32 * u + 31 <= k) continue;
-          const int i = lane + 32 * u;
-          if (i > k && i < m) {
-            const double l = L[i + k * m];
-            xv[0][u] -= l * yk[0];
-            xv[1][u] -= l * yk[1];
-          }
-        }
-      }
-      for (int k = m - 1; k >= 0; --k) {  // L^T g = y
-        const double ik = invd[k];
-        double gk[2];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          gk[r] = __shfl_sync(0xffffffffu, pick(xv[r], k >> 5), k & 31) * ik;
-          if (lane == (k & 31)) put(xv[r], k >> 5, gk[r]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (32 * u >= k) continue;
-          const int i = lane + 32 * u;
-          if (i < k) {
-            const double l = Lr[k * lrs + i];
-            xv[0][u] -= l * gk[0];
-            xv[1][u] -= l * gk[1];
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      if (r >= nj) break;
-      const int j = j0 + r;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = lane + 32 * u;
-        if (i < m) A.g[i + int64_t(j) * m] = xv[r][u];
-        if (i < mv) {
-          const double v = i < m ? beta * beta * xv[r][u] : 0.0;
-          dpsi[int64_t(j) * mv + i] = float(v);
-          dpsi64[int64_t(j) * mv + i] = v;
-        }
-      }
-    }
+  for (int e = threadIdx.x; e < m * m; e += nt) {  // the factor (zero upper triangle): K2 (L^-1), prediction
+    const int i = e % m, j = e / m;
+    A.la[e] = i >= j ? L[e] : 0.0;
   }
-  __syncthreads();
+  // G = L^-T L^-1 Psi in chunks of kG1Rhs columns: blocked substitutions with the D^-1 blocks
+  for (int c0 = 0; c0 < d; c0 += kG1Rhs) {
+    const int nc = min(kG1Rhs, d - c0);
+    for (int e = threadIdx.x; e < m * nc; e += nt) X[e] = psi[int64_t(c0) * m + e];
+    __syncthreads();
+    if (ok) {
+      for (int b = 0; b < nb; ++b) {  // forward: L y = psi
+        const int j0 = 32 * b, jb = min(32, m - j0), mr = m - j0 - jb;
+        const double* W = Wd + 1024 * b;
+        mma_gemm(jb, nc, jb, W, 1, 32, X + j0, 1, m, [&](int i, int j, double v) { Tmp[i + j * 32] = v; });
+        __syncthreads();
+        for (int e = threadIdx.x; e < jb * nc; e += nt) X[j0 + (e % jb) + (e / jb) * m] = Tmp[(e % jb) + (e / jb) * 32];
+        __syncthreads();
+        if (mr > 0) {
+          mma_gemm(mr, nc, jb, L + (j0 + jb) + j0 * m, 1, m, X + j0, 1, m,
+                   [&](int i, int j, double v) { X[(j0 + jb + i) + j * m] -= v; });
+          __syncthreads();
+        }
+      }
+      for (int b = nb - 1; b >= 0; --b) {  // backward: L^T g = y
+        const int j0 = 32 * b, jb = min(32, m - j0), mr = m - j0 - jb;
+        const double* W = Wd + 1024 * b;
+        if (mr > 0) {
+          mma_gemm(jb, nc, mr, L + (j0 + jb) + j0 * m, m, 1, X + j0 + jb, 1, m,
+                   [&](int i, int j, double v) { X[(j0 + i) + j * m] -= v; });
+          __syncthreads();
+        }
+        mma_gemm(jb, nc, jb, W, 32, 1, X + j0, 1, m, [&](int i, int j, double v) { Tmp[i + j * 32] = v; });
+        __syncthreads();
+        for (int e = threadIdx.x; e < jb * nc; e += nt) X[j0 + (e % jb) + (e / jb) * m] = Tmp[(e % jb) + (e / jb) * 32];
+        __syncthreads();
+      }
+    }
+    for (int e = threadIdx.x; e < m * nc; e += nt) A.g[int64_t(c0) * m + e] = X[e];
+    for (int e = threadIdx.x; e < mv * nc; e += nt) {
+      const int i = e % mv, j = c0 + e / mv;
+      const double v = i < m ? beta * beta * X[i + (j - c0) * m] : 0.0;
+      dpsi[int64_t(j) * mv + i] = float(v);
+      dpsi64[int64_t(j) * mv + i] = v;
+    }
+    __syncthreads();
+  }
   DC_STAMP(3);
   double pg = 0.0;  // <Psi, G> (bound.hpp:108-116), fixed-order tree
-  for (int64_t e = threadIdx.x; e < int64_t(m) * d; e += blockDim.x) pg += psi[e] * A.g[e];
+  for (int64_t e = threadIdx.x; e < int64_t(m) * d; e += nt) pg += psi[e] * A.g[e];
   pg = block_sum_s(pg, red);
   if (threadIdx.x == 0) {
     A.sc[kScLogDetA] = 2.0 * s;
@@ -1035,7 +983,24 @@ void dc_bind(DcArgs& A, double* ws) {
 }
 
 size_t small_smem(int m) { return sizeof(double) * 2 * size_t(m) * m; }
-size_t g_small_smem(int m) { return sizeof(double) * (size_t(m) * m + size_t(m) * size_t(m | 1)); }
+
+namespace {
+struct LsArg {
+  double v[64];
+};
+__global__ void upload_ls_kernel(double* __restrict__ dst, int q, const LsArg ls) {
+  if (threadIdx.x < q) dst[threadIdx.x] = ls.v[threadIdx.x];
+}
+}  // namespace
+
+int dc_upload_ls(const DcArgs& A, const double* ls, cudaStream_t st) {
+  if (A.q > 64) return 1;
+  LsArg a{};
+  for (int i = 0; i < A.q; ++i) a.v[i] = ls[i];
+  upload_ls_kernel<<<1, 64, 0, st>>>(const_cast<double*>(A.ls), A.q, a);
+  g_tc_launches.fetch_add(1);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
 
 int dc_prefactor(const DcArgs& A, cudaStream_t st) {
   const int m = A.m;
@@ -1101,7 +1066,7 @@ int dc_bound_split(const DcArgs& A, float* u, float* dpsi, double* u64, double* 
       cudaFuncSetAttribute(bound_u_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smax) != cudaSuccess ||
       cudaFuncSetAttribute(deferred_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smax) != cudaSuccess)
     return 3;
-  bound_g_small_kernel<<<1, 1024, g_small_smem(m), st>>>(A, dpsi, dpsi64);
+  bound_g_small_kernel<<<1, kG1Threads, g_small_smem(m), st>>>(A, dpsi, dpsi64);
   if (cudaEventRecord(ev_g, st) != cudaSuccess || cudaStreamWaitEvent(side, ev_g, 0) != cudaSuccess) return 3;
   bound_u_small_kernel<<<1, 1024, small_smem(m), side>>>(A, u, u64);
   deferred_small_kernel<<<1, 1024, small_smem(m), side>>>(A);

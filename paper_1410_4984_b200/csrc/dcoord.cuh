@@ -42,6 +42,7 @@ int64_t dc_workspace_doubles(int m, int q, int d);
 // Point every array of `A` into `ws` (dc_workspace_doubles long); the int slots follow the doubles.
 void dc_bind(DcArgs& A, double* ws);
 
+int dc_upload_ls(const DcArgs& A, const double* ls, cudaStream_t st);  // A.ls <- ls (by value, Q <= 64)
 int dc_prefactor(const DcArgs& A, cudaStream_t st);                 // per broadcast
 // after allreduce #1: the bound terms and the backward's adjoint operands (fp32 + fp64)
 int dc_bound(const DcArgs& A, float* u, float* dpsi, double* u64, double* dpsi64, cudaStream_t st);

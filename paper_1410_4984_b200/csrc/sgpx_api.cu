@@ -367,6 +367,8 @@ struct sgpx_engine {
   bool split = false, split_join = false;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_split[2] = {};
+  cudaEvent_t ev_pre[2] = {};  // the per-broadcast prefactor on the side stream (dc_setup)
+  bool pre_pending = false;
   // one evaluation (device-resident shard, device coordinator) as a CUDA graph, replayed while its
   // launch arguments are unchanged (graph_key)
   bool use_graph = true;
@@ -382,6 +384,8 @@ struct sgpx_engine {
     for (auto& e : ev_c)
       if (e) cudaEventDestroy(e);
     for (auto& e : ev_split)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : ev_pre)
       if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
     if (graph) cudaGraphExecDestroy(graph);
@@ -556,13 +560,29 @@ void dc_setup(sgpx_engine* e) {
   dc_bind(dc, e->dcw.get<double>());
   e->pstats.ensure(sizeof(double) * sgpx_packed_stats_count(e->cfg.m, e->cfg.d));
   dc.packed = e->pstats.get<double>();
-  e->h_stage.ensure(sizeof(double) * dc.q);
-  std::copy(e->kernel_ls.begin(), e->kernel_ls.end(), e->h_stage.get<double>());
-  CUDA_OK(cudaMemcpyAsync(const_cast<double*>(dc.ls), e->h_stage.p, sizeof(double) * dc.q, cudaMemcpyHostToDevice,
-                            e->ctx->stream));
-  if (dc_prefactor(dc, e->ctx->stream)) throw CudaError("coordinator launch");
-  CUDA_OK(cudaStreamSynchronize(e->ctx->stream));  // the staging buffer is reused
+  // the per-broadcast half (Kmm, its factor and inverse) runs on the side stream, overlapping the
+  // forward kernels; the evaluation joins it right before the coordinator (dc_join_prefactor).  The
+  // lengthscales travel as a kernel argument (no staging buffer to keep alive).
+  cudaStream_t st = e->ctx->stream;
+  if (!e->side) CUDA_OK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+  if (!e->ev_pre[0]) {
+    CUDA_OK(cudaEventCreateWithFlags(&e->ev_pre[0], cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&e->ev_pre[1], cudaEventDisableTiming));
+  }
+  CUDA_OK(cudaEventRecord(e->ev_pre[0], st));  // after every earlier user of the workspace
+  CUDA_OK(cudaStreamWaitEvent(e->side, e->ev_pre[0], 0));
+  if (dc_upload_ls(dc, e->kernel_ls.data(), e->side)) throw CudaError("coordinator launch");
+  if (dc_prefactor(dc, e->side)) throw CudaError("coordinator launch");
+  CUDA_OK(cudaEventRecord(e->ev_pre[1], e->side));
+  e->pre_pending = true;
   e->dc_ready = true;
+}
+
+// the stream waits for the per-broadcast prefactor (before the first coordinator kernel)
+void dc_join_prefactor(sgpx_engine* e) {
+  if (!e->pre_pending) return;
+  CUDA_OK(cudaStreamWaitEvent(e->ctx->stream, e->ev_pre[1], 0));
+  e->pre_pending = false;
 }
 
 void engine_coordinate(sgpx_engine* e, bool with_grads) {
@@ -573,6 +593,7 @@ void engine_coordinate(sgpx_engine* e, bool with_grads) {
     e->dpsi.ensure(sizeof(float) * std::max(1, e->P.d) * e->P.mv);
     e->u64.ensure(sizeof(double) * e->P.mv * e->P.mv);
     e->dpsi64.ensure(sizeof(double) * std::max(1, e->P.d) * e->P.mv);
+    dc_join_prefactor(e);
     CUDA_OK(record_event(e->ev_c[0], ctx->stream));
     e->split = e->coord_split && e->cfg.m <= 112;
     if (e->split) {
@@ -700,8 +721,12 @@ void engine_grad_pass(sgpx_engine* e) {
     auto out_of = [&](int j) {
       return k > 1 ? e->pgrads_sub.get<double>() + int64_t(j) * count : e->pgrads.get<double>();
     };
+    // with streamed-out d mu / d S only the first sub-shards run their psi1 kernels ahead (enough to
+    // cover the side stream's coordinator); the rest keep psi1 -> psi2 -> copy-out per sub-shard so the
+    // device-to-host copies start early
+    const int kp = phased ? (stream_out ? std::max(1, k / 3) : k) : 0;
     if (phased) {
-      for (int j = 0; j < k; ++j) {
+      for (int j = 0; j < kp; ++j) {
         auto& sub = e->subs[j];
         if (psi_backward(sub.P, bconst(sub, j), e->bpart.get<double>() + sub.boff, out_of(j), nsm, ctx->stream, &e->gb,
                          j == 0 ? e->ev[6] : nullptr, nullptr, 1))
@@ -714,7 +739,7 @@ void engine_grad_pass(sgpx_engine* e) {
       sub.P.ev_psi2[0] = j == 0 ? e->ev[10] : nullptr;
       sub.P.ev_psi2[1] = j == 0 ? e->ev[11] : nullptr;
       if (psi_backward(sub.P, bconst(sub, j), e->bpart.get<double>() + sub.boff, out_of(j), nsm, ctx->stream, &e->gb,
-                       (j == 0 && !phased) ? e->ev[6] : nullptr, j == k - 1 ? e->ev[7] : nullptr, phased ? 2 : 0))
+                       (j == 0 && !phased) ? e->ev[6] : nullptr, j == k - 1 ? e->ev[7] : nullptr, j < kp ? 2 : 0))
         throw CudaError(std::string("psi backward launch: ") + cudaGetErrorString(cudaGetLastError()));
       if (stream_out) {  // d mu / d S of this sub-shard are final: copy them out while the next runs
         const int64_t q = e->cfg.q, n = e->cfg.n_local;
@@ -1278,9 +1303,11 @@ int sgpx_engine_create(sgpx_ctx* ctx, const sgpx_engine_config* cfg, sgpx_engine
     e->latent = cfg->kind == 1;
     for (auto& ev : e->ev) CUDA_OK(cudaEventCreate(&ev));
     for (auto& ev : e->ev_c) CUDA_OK(cudaEventCreate(&ev));
-    // host coordinator up to the single-CTA shared-memory size (the two are within 0.1 ms there);
-    // above it the host's O(M^3) algebra grows past the device's blocked kernels (M = 500: 19 ms vs 3 ms)
-    e->dev_coord = cfg->m > 112;
+    // device coordinator by default: stream-ordered (no host round trip between the passes), split so
+    // that only the factorisation and G = A^-1 Psi sit between the passes (C3: 5.78 vs 6.08 ms per
+    // evaluation, end to end 7.98 vs 8.23 ms; profiles/r02/coord_split_ab.txt); the host coordinator
+    // (SGPX_DEVICE_COORD=0) remains for A/B
+    e->dev_coord = true;
     if (const char* dc = getenv("SGPX_DEVICE_COORD")) e->dev_coord = atoi(dc) != 0;  // A/B
     if (const char* sp = getenv("SGPX_COORD_SPLIT")) e->coord_split = atoi(sp) != 0;  // A/B
     if (const char* gr = getenv("SGPX_GRAPH")) e->use_graph = atoi(gr) != 0;       // A/B: per-call launches
@@ -1453,6 +1480,7 @@ int sgpx_engine_evaluate(sgpx_engine* e, int with_grads, sgpx_eval_result* out) 
       const int flags[2] = {with_grads ? 1 : 0, e->ctx->device};
       std::memcpy(p + sizeof(PsiConst) + sizeof(DcArgs), flags, sizeof(flags));
       cudaStream_t st = e->ctx->stream;
+      dc_join_prefactor(e);  // outside the capture (the prefactor's event is not part of the graph)
       if (!e->graph || key != e->graph_key) {
         if (e->graph) {
           cudaGraphExecDestroy(e->graph);
@@ -1506,6 +1534,7 @@ int sgpx_engine_predict(sgpx_engine* e, sgpx_cmat x_star, int observation, sgpx_
     if (!e->dev_coord) {  // host-coordinated engine: rebuild the factors on the device from the last statistics
       CUDA_OK(cudaSetDevice(e->ctx->device));
       if (!e->dc_ready) dc_setup(e);
+      dc_join_prefactor(e);
       e->u.ensure(sizeof(float) * e->P.mv * e->P.mv);
       e->dpsi.ensure(sizeof(float) * std::max(1, e->P.d) * e->P.mv);
       e->u64.ensure(sizeof(double) * e->P.mv * e->P.mv);

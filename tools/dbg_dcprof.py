@@ -10,4 +10,4 @@ for _ in range(3):
     r = e.evaluate(True, local_to_host=False)
 a = (C.c_longlong * 16)()
 _lib.load().sgpx_debug_dc_profile(a)
-print("phase cycles:", [a[i + 1] - a[i] for i in range(5)], "attempts", a[10], a[11], "ok", a[12], a[13], "coord", r.timing.coordinator_s)
+print("phase cycles:", [a[i + 1] - a[i] for i in range(5)], "panel0:", [a[5] - a[1], a[6] - a[5], a[7] - a[6], a[8] - a[7]], "attempts", a[10], a[11], "ok", a[12], a[13], "coord", r.timing.coordinator_s)
