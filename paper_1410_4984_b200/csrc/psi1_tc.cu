@@ -72,7 +72,7 @@ constexpr int kRaw = 4;  // raw-row buffers: copies run kRaw - 1 chunks ahead of
 struct FwdSmem {  // byte offsets
   int g, y, raw, pd, bar, total;
   int raw_stride;  // bytes per raw buffer: mu [q][kFwdK], S [q][kFwdK], Y [d][kFwdK] doubles
-  int pd_stride;   // bytes per stage of per-datapoint floats: mu - c, d1, 1/2 log2(d1 l^2) [3][q][kFwdK]
+  int pd_stride;   // bytes per stage of per-datapoint floats: a, -b, 1/2 log2(d1 l^2) [3][q][kFwdK], b1 [kFwdK]
 };
 __host__ __device__ inline FwdSmem fwd_smem(int q, int d) {
   FwdSmem L{};
@@ -81,7 +81,7 @@ __host__ __device__ inline FwdSmem fwd_smem(int q, int d) {
   L.y = L.g + 2 * 2 * 128 * kFwdK * 4;         // [stage][piece][dp x kFwdK] floats
   L.raw_stride = (2 * q + d) * kFwdK * 8;
   L.raw = L.y + 2 * 2 * dp * kFwdK * 4;        // [kRaw] raw rows
-  L.pd_stride = 3 * q * kFwdK * 4;
+  L.pd_stride = (3 * q + 1) * kFwdK * 4;
   L.pd = L.raw + kRaw * L.raw_stride;          // [stage]
   L.bar = (L.pd + 2 * L.pd_stride + 15) / 16 * 16;  // stage_full[2], mma_done[2], raw_full[kRaw], TMEM slot
   L.total = L.bar + 8 * (4 + kRaw) + 16;
@@ -193,7 +193,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       for (int i = pt; i < kFwdK * Q; i += kFwdProd) {  // psi_stats.hpp:144-159, validation, KL partial
         const int nl = i % kFwdK, q = i / kFwdK;
         const int64_t n = n0 + nl;
-        float mu = 0.f, d1 = 0.f, cl = (q == 0 && n >= P.n) ? -CUDART_INF_F : 0.f;
+        // log2 v1 = b1 - sum_q (a - b z)^2 with b = sqrt(log2e d1 / 2), a = b (mu - c): the direct
+        // difference d1 (mu - z)^2 log2e / 2 as one FFMA per term (see psi1_bwd_pipe_kernel)
+        float a = 0.f, nb = 0.f, cl = 0.f;
         if (q < P.q && n < P.n) {
           const double md = raw[q * kFwdK + nl];
           const double sd = P.expected ? raw[(Q + q) * kFwdK + nl] : 0.0;
@@ -202,13 +204,23 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             bad |= (sd > 0.0 && isfinite(sd)) ? 0 : 4;
             kl_acc += 0.5 * (sd + md * md - log(sd) - 1.0);  // parallel.hpp:148-149
           }
-          mu = float(md - P.center[q]);
-          d1 = 1.f / (float(sd) + P.l2[q]);
+          const float mu = float(md - P.center[q]);
+          const float d1 = 1.f / (float(sd) + P.l2[q]);
+          const float bq = sqrtf(0.5f * kLog2e * d1);
+          a = bq * mu;
+          nb = -bq;
           cl = 0.5f * log2f(d1 * P.l2[q]);
         }
-        pd[q * kFwdK + nl] = mu;
-        pd[(Q + q) * kFwdK + nl] = d1;
+        pd[q * kFwdK + nl] = a;
+        pd[(Q + q) * kFwdK + nl] = nb;
         pd[(2 * Q + q) * kFwdK + nl] = cl;
+      }
+      tc::named_sync(1, kFwdProd);  // every (datapoint, q) constant written
+      for (int nl = pt; nl < kFwdK; nl += kFwdProd) {  // b1 = log2 var + sum_q 1/2 log2(d1 l^2) (q ascending)
+        float b1 = P.log2_var;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) b1 += pd[(2 * Q + q) * kFwdK + nl];
+        pd[3 * Q * kFwdK + nl] = n0 + nl < P.n ? b1 : -CUDART_INF_F;
       }
       float* yb = ysm + st * 2 * dp * kFwdK;  // the Y chunk as tf32 pieces: rows = output dims, K = datapoints
 #pragma unroll 4
@@ -270,33 +282,43 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       float* gb = gsm + st * 2 * 128 * kFwdK;
       {
         float b[8], e[2][8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          b[u] = P.log2_var;
-          e[0][u] = e[1][u] = 0.f;
+        {
+          const float4 b0 = *reinterpret_cast<const float4*>(pd + 3 * Q * kFwdK + 8 * gj);
+          const float4 b4 = *reinterpret_cast<const float4*>(pd + 3 * Q * kFwdK + 8 * gj + 4);
+          b[0] = b0.x, b[1] = b0.y, b[2] = b0.z, b[3] = b0.w, b[4] = b4.x, b[5] = b4.y, b[6] = b4.z, b[7] = b4.w;
         }
+        float2 e2[2][4];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) e2[i][u] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-          float mv[8], dv[8], cv[8];
+          float2 av[4], nv[4];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const float4 m4 = *reinterpret_cast<const float4*>(pd + q * kFwdK + 8 * gj + 4 * h);
-            const float4 d4 = *reinterpret_cast<const float4*>(pd + (Q + q) * kFwdK + 8 * gj + 4 * h);
-            const float4 c4 = *reinterpret_cast<const float4*>(pd + (2 * Q + q) * kFwdK + 8 * gj + 4 * h);
-            mv[4 * h] = m4.x, mv[4 * h + 1] = m4.y, mv[4 * h + 2] = m4.z, mv[4 * h + 3] = m4.w;
-            dv[4 * h] = d4.x, dv[4 * h + 1] = d4.y, dv[4 * h + 2] = d4.z, dv[4 * h + 3] = d4.w;
-            cv[4 * h] = c4.x, cv[4 * h + 1] = c4.y, cv[4 * h + 2] = c4.z, cv[4 * h + 3] = c4.w;
+            const float4 a4 = *reinterpret_cast<const float4*>(pd + q * kFwdK + 8 * gj + 4 * h);
+            const float4 n4 = *reinterpret_cast<const float4*>(pd + (Q + q) * kFwdK + 8 * gj + 4 * h);
+            av[2 * h] = make_float2(a4.x, a4.y), av[2 * h + 1] = make_float2(a4.z, a4.w);
+            nv[2 * h] = make_float2(n4.x, n4.y), nv[2 * h + 1] = make_float2(n4.z, n4.w);
           }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            b[u] += cv[u];
+          for (int i = 0; i < 2; ++i) {
+            const float2 zz = make_float2(z[i][q], z[i][q]);
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const float f = mv[u] - z[i][q];
-              e[i][u] = fmaf(f * f, dv[u], e[i][u]);
+            for (int u = 0; u < 4; ++u) {
+              const float2 t = __ffma2_rn(nv[u], zz, av[u]);
+              e2[i][u] = __ffma2_rn(t, t, e2[i][u]);
             }
           }
         }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            e[i][2 * u] = e2[i][u].x;
+            e[i][2 * u + 1] = e2[i][u].y;
+          }
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int mm = gm + 64 * i;
@@ -305,7 +327,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             float hv[4], lv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const float g = mm < m ? ex2(fmaf(-0.5f * kLog2e, e[i][4 * h + u], b[4 * h + u])) : 0.f;
+              const float g = mm < m ? ex2(b[4 * h + u] - e[i][4 * h + u]) : 0.f;
               hv[u] = tc::tf32_hi(g);
               lv[u] = g - hv[u];
             }
