@@ -325,16 +325,25 @@ __device__ void mma_gemm(int m, int n, int k, const double* __restrict__ a, int 
     const double* pa1 = a + int64_t(ra1 ? ia1 : 0) * ai;
     const double* pb0 = b + int64_t(cb0 ? jb0 : 0) * bj;
     const double* pb1 = b + int64_t(cb1 ? jb1 : 0) * bj;
-    for (int p0 = 0; p0 < k; p0 += 4) {
+    auto fetch = [&](int p0, double& a0, double& a1, double& b0, double& b1) {
       const int pp = p0 + t;
       const bool kp = pp < k;
       const int64_t oa = int64_t(kp ? pp : 0) * ap, ob = int64_t(kp ? pp : 0) * bp;
-      const double a0 = (kp && ra0) ? pa0[oa] : 0.0, a1 = (kp && ra1) ? pa1[oa] : 0.0;
-      const double b0 = (kp && cb0) ? pb0[ob] : 0.0, b1 = (kp && cb1) ? pb1[ob] : 0.0;
+      a0 = (kp && ra0) ? pa0[oa] : 0.0;
+      a1 = (kp && ra1) ? pa1[oa] : 0.0;
+      b0 = (kp && cb0) ? pb0[ob] : 0.0;
+      b1 = (kp && cb1) ? pb1[ob] : 0.0;
+    };
+    double a0, a1, b0, b1;
+    fetch(0, a0, a1, b0, b1);
+    for (int p0 = 0; p0 < k; p0 += 4) {  // the next k-step's operands load under this step's MMAs
+      double na0 = 0.0, na1 = 0.0, nb0 = 0.0, nb1 = 0.0;
+      if (p0 + 4 < k) fetch(p0 + 4, na0, na1, nb0, nb1);
       dmma(acc[0][0], a0, b0);
       dmma(acc[0][1], a0, b1);
       dmma(acc[1][0], a1, b0);
       dmma(acc[1][1], a1, b1);
+      a0 = na0, a1 = na1, b0 = nb0, b1 = nb1;
     }
 #pragma unroll
     for (int r = 0; r < 2; ++r)
@@ -599,7 +608,6 @@ __global__ void __launch_bounds__(kG1Threads) bound_g_small_kernel(DcArgs A, flo
     return packed[4 + int64_t(lo) * m - int64_t(lo) * (lo - 1) / 2 + (hi - lo)];
   };
   DC_STAMP(0);
-  for (int e = threadIdx.x; e < m * m; e += nt) A.phi[e] = phi_at(e % m, e / m);  // dense Phi (K2, deferred)
   double f = 0.0, scale = 0.0;  // factor_spd escalation (bound.hpp:52-62): shift f * max |a_ii|
   bool ok = false;
   for (int attempt = 0; attempt < 32; ++attempt) {
@@ -618,7 +626,9 @@ __global__ void __launch_bounds__(kG1Threads) bound_g_small_kernel(DcArgs A, flo
     const double shift = f * scale;
     for (int e = threadIdx.x; e < m * m; e += nt) {
       const int i = e % m, j = e / m;
-      L[e] = A.kmm[e] + beta * phi_at(i, j) + (i == j ? jit + shift : 0.0);
+      const double ph = phi_at(i, j);
+      if (attempt == 0) A.phi[e] = ph;  // dense Phi (K2, deferred)
+      L[e] = A.kmm[e] + beta * ph + (i == j ? jit + shift : 0.0);
     }
     for (int e = threadIdx.x; e < 4 * 1024; e += nt) Wd[e] = 0.0;
     if (threadIdx.x == 0) s_fail = 0;
@@ -632,7 +642,7 @@ __global__ void __launch_bounds__(kG1Threads) bound_g_small_kernel(DcArgs A, flo
         for (int k = 0; k < jb; ++k) {
           const double dkk = Lp[k + k * m];
           const bool bad = !(dkk > 0.0);
-          const double lkk = bad ? 1.0 : sqrt(dkk), inv = 1.0 / lkk;
+          const double inv = bad ? 1.0 : rsqrt(dkk), lkk = bad ? 1.0 : dkk * inv;
           double lrk = 0.0;
           if (r > k && r < jb) {
             lrk = Lp[r + k * m] * inv;
@@ -707,47 +717,51 @@ __global__ void __launch_bounds__(kG1Threads) bound_g_small_kernel(DcArgs A, flo
   if (ok)
     for (int i = threadIdx.x; i < m; i += nt) s += log(diag[i]);
   s = block_sum_s(s, red);
-  for (int e = threadIdx.x; e < m * m; e += nt) {  // the factor (zero upper triangle): K2 (L^-1), prediction
+  for (int e = threadIdx.x; e < m * m; e += nt) {  // the factor (zero upper triangle): prediction
     const int i = e % m, j = e / m;
     A.la[e] = i >= j ? L[e] : 0.0;
+    if (i < j) L[e] = 0.0;  // (A's upper triangle is still there)
   }
-  // G = L^-T L^-1 Psi in chunks of kG1Rhs columns: blocked substitutions with the D^-1 blocks
-  for (int c0 = 0; c0 < d; c0 += kG1Rhs) {
-    const int nc = min(kG1Rhs, d - c0);
-    for (int e = threadIdx.x; e < m * nc; e += nt) X[e] = psi[int64_t(c0) * m + e];
-    __syncthreads();
-    if (ok) {
-      for (int b = 0; b < nb; ++b) {  // forward: L y = psi
-        const int j0 = 32 * b, jb = min(32, m - j0), mr = m - j0 - jb;
-        const double* W = Wd + 1024 * b;
-        mma_gemm(jb, nc, jb, W, 1, 32, X + j0, 1, m, [&](int i, int j, double v) { Tmp[i + j * 32] = v; });
+  __syncthreads();
+  if (ok) {
+    // W = L^-1 in place of L, block row by block row: W_ii = D_i^-1, W_i,<i = -D_i^-1 (L_i,<i W_<i,<i)
+    for (int bi = 0; bi < nb; ++bi) {
+      const int i0 = 32 * bi, ib = min(32, m - i0);
+      if (bi > 0) {
+        mma_gemm(ib, i0, i0, L + i0, 1, m, L, 1, m, [&](int r, int c, double v) { Tmp[r + c * 32] = v; });
         __syncthreads();
-        for (int e = threadIdx.x; e < jb * nc; e += nt) X[j0 + (e % jb) + (e / jb) * m] = Tmp[(e % jb) + (e / jb) * 32];
-        __syncthreads();
-        if (mr > 0) {
-          mma_gemm(mr, nc, jb, L + (j0 + jb) + j0 * m, 1, m, X + j0, 1, m,
-                   [&](int i, int j, double v) { X[(j0 + jb + i) + j * m] -= v; });
-          __syncthreads();
-        }
+        mma_gemm(ib, i0, ib, Wd + 1024 * bi, 1, 32, Tmp, 1, 32,
+                 [&](int r, int c, double v) { L[(i0 + r) + c * m] = -v; });
       }
-      for (int b = nb - 1; b >= 0; --b) {  // backward: L^T g = y
-        const int j0 = 32 * b, jb = min(32, m - j0), mr = m - j0 - jb;
-        const double* W = Wd + 1024 * b;
-        if (mr > 0) {
-          mma_gemm(jb, nc, mr, L + (j0 + jb) + j0 * m, m, 1, X + j0 + jb, 1, m,
-                   [&](int i, int j, double v) { X[(j0 + i) + j * m] -= v; });
-          __syncthreads();
-        }
-        mma_gemm(jb, nc, jb, W, 32, 1, X + j0, 1, m, [&](int i, int j, double v) { Tmp[i + j * 32] = v; });
-        __syncthreads();
-        for (int e = threadIdx.x; e < jb * nc; e += nt) X[j0 + (e % jb) + (e / jb) * m] = Tmp[(e % jb) + (e / jb) * 32];
-        __syncthreads();
+      for (int e = threadIdx.x; e < ib * ib; e += nt) {
+        const int r = e % ib, c = e / ib;
+        L[(i0 + r) + (i0 + c) * m] = r >= c ? Wd[1024 * bi + r + 32 * c] : 0.0;
       }
+      __syncthreads();
     }
-    for (int e = threadIdx.x; e < m * nc; e += nt) A.g[int64_t(c0) * m + e] = X[e];
+    for (int e = threadIdx.x; e < m * m; e += nt) {  // L_a^-1 (K2's A^-1, prediction), zero upper triangle
+      const int i = e % m, j = e / m;
+      A.wa[e] = i >= j ? L[e] : 0.0;
+      L[e] = i >= j ? L[e] : 0.0;
+    }
+    __syncthreads();
+  }
+  // G = W^T (W Psi) in chunks of 32 columns, Psi staged in shared memory
+  for (int c0 = 0; c0 < d; c0 += 32) {
+    const int nc = min(32, d - c0);
+    if (ok) {
+      for (int e = threadIdx.x; e < m * nc; e += nt) X[e] = psi[int64_t(c0) * m + e];
+      __syncthreads();
+      mma_gemm(m, nc, m, L, 1, m, X, 1, m, [&](int i, int j, double v) { Tmp[i + j * m] = v; });
+      __syncthreads();
+      mma_gemm(m, nc, m, L, m, 1, Tmp, 1, m, [&](int i, int j, double v) { A.g[int64_t(c0 + j) * m + i] = v; });
+    } else {
+      for (int e = threadIdx.x; e < m * nc; e += nt) A.g[int64_t(c0) * m + e] = psi[int64_t(c0) * m + e];
+    }
+    __syncthreads();
     for (int e = threadIdx.x; e < mv * nc; e += nt) {
       const int i = e % mv, j = c0 + e / mv;
-      const double v = i < m ? beta * beta * X[i + (j - c0) * m] : 0.0;
+      const double v = i < m ? beta * beta * A.g[i + int64_t(j) * m] : 0.0;
       dpsi[int64_t(j) * mv + i] = float(v);
       dpsi64[int64_t(j) * mv + i] = v;
     }
@@ -777,12 +791,8 @@ __global__ void __launch_bounds__(1024) bound_u_small_kernel(DcArgs A, float* __
   const double* packed = A.packed;
   const double beta = A.beta;
   const bool ok = !(int(A.sc[kScStatus]) & kStAFailed);
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) L[e] = A.la[e];
-  __syncthreads();
   if (ok) {
-    trinv_warp_smem(L, W, m);
-    __syncthreads();
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) A.wa[e] = W[(e % m) * m + e / m];  // L_a^-1 (prediction)
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) W[(e % m) * m + e / m] = A.wa[e];  // K1's L^-1, row-major
     __syncthreads();
     wtw_smem(W, m, L, A.ainv);  // A^-1 into shared memory (over L) and global
   }
@@ -845,25 +855,39 @@ __global__ void dc_prof_kernel(long long* out) {
 }
 
 // d Kmm (with Kmm^-1 Phi Kmm^-1), Phi G, d beta, kern_grads(Z, Z, d Kmm), the assembly: one CTA.
-__global__ void __launch_bounds__(1024) deferred_small_kernel(DcArgs A) {
+// part 1: Kmm^-1 Phi Kmm^-1 (needs only the statistics: runs concurrently with K1 in the split
+// coordinator); part 2: the rest (after K2); part 0: both.
+__global__ void __launch_bounds__(1024) deferred_small_kernel(DcArgs A, int part) {
   extern __shared__ double sm[];
   const int m = A.m, d = A.d;
   double* K = sm;          // Kmm^-1
   double* T = sm + m * m;  // Phi, then Kmm^-1 Phi
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    K[e] = A.kinv[e];
-    T[e] = A.phi[e];
+  if (part != 2) {
+    const double* packed = A.packed;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+      const int i = e % m, j = e / m, lo = min(i, j), hi = max(i, j);
+      K[e] = A.kinv[e];
+      T[e] = packed[4 + int64_t(lo) * m - int64_t(lo) * (lo - 1) / 2 + (hi - lo)];
+    }
+    __syncthreads();
+    mma_gemm(  // tmp = Kmm^-1 Phi
+        m, m, m, K, 1, m, T, 1, m, [&](int i, int j, double v) { A.tmp[i + j * m] = v; });
+    __syncthreads();
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) T[e] = A.tmp[e];
+    __syncthreads();
+    mma_gemm(  // kpk = tmp Kmm^-1
+        m, m, m, T, 1, m, K, 1, m, [&](int i, int j, double v) { A.kpk[i + j * m] = v; });
+    if (part == 1) return;
+    __syncthreads();
   }
-  __syncthreads();
-  mma_gemm(  // Phi G
-      m, d, m, T, 1, m, A.g, 1, m, [&](int i, int j, double v) { A.phig[i + int64_t(j) * m] = v; });
-  mma_gemm(  // tmp = Kmm^-1 Phi
-      m, m, m, K, 1, m, T, 1, m, [&](int i, int j, double v) { A.tmp[i + j * m] = v; });
-  __syncthreads();
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) T[e] = A.tmp[e];
-  __syncthreads();
-  mma_gemm(  // kpk = tmp Kmm^-1
-      m, m, m, T, 1, m, K, 1, m, [&](int i, int j, double v) { A.kpk[i + j * m] = v; });
+  if (d <= m) {  // Phi G with both operands staged in shared memory (Phi dense from K1)
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) T[e] = A.phi[e];
+    for (int e = threadIdx.x; e < m * d; e += blockDim.x) K[e] = A.g[e];
+    __syncthreads();
+    mma_gemm(m, d, m, T, 1, m, K, 1, m, [&](int i, int j, double v) { A.phig[i + int64_t(j) * m] = v; });
+  } else {
+    mma_gemm(m, d, m, A.phi, 1, m, A.g, 1, m, [&](int i, int j, double v) { A.phig[i + int64_t(j) * m] = v; });
+  }
   __syncthreads();
   const double beta = A.beta, dd = double(d);
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
@@ -1052,12 +1076,12 @@ int dc_bound(const DcArgs& A, float* u, float* dpsi, double* u64, double* dpsi64
 }
 
 int dc_bound_split(const DcArgs& A, float* u, float* dpsi, double* u64, double* dpsi64, cudaStream_t st,
-                   cudaStream_t side, cudaEvent_t ev_g, cudaEvent_t ev_u) {
+                   cudaStream_t side, cudaStream_t side2, cudaEvent_t* ev) {
   const int m = A.m;
-  if (m > kSmallM || !side) {  // one stream: the whole coordinator before the backward
+  if (m > kSmallM || !side || !side2) {  // one stream: the whole coordinator before the backward
     if (int rc = dc_bound(A, u, dpsi, u64, dpsi64, st)) return rc;
     if (int rc = dc_deferred(A, st)) return rc;
-    if (cudaEventRecord(ev_g, st) != cudaSuccess || cudaEventRecord(ev_u, st) != cudaSuccess) return 3;
+    if (cudaEventRecord(ev[0], st) != cudaSuccess || cudaEventRecord(ev[1], st) != cudaSuccess) return 3;
     return 0;
   }
   const int smax = int(small_smem(kSmallM));
@@ -1066,12 +1090,17 @@ int dc_bound_split(const DcArgs& A, float* u, float* dpsi, double* u64, double* 
       cudaFuncSetAttribute(bound_u_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smax) != cudaSuccess ||
       cudaFuncSetAttribute(deferred_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smax) != cudaSuccess)
     return 3;
+  // side2: Kmm^-1 Phi Kmm^-1 from the statistics alone, concurrently with K1
+  if (cudaEventRecord(ev[2], st) != cudaSuccess || cudaStreamWaitEvent(side2, ev[2], 0) != cudaSuccess) return 3;
+  deferred_small_kernel<<<1, 1024, small_smem(m), side2>>>(A, 1);
+  if (cudaEventRecord(ev[3], side2) != cudaSuccess) return 3;
   bound_g_small_kernel<<<1, kG1Threads, g_small_smem(m), st>>>(A, dpsi, dpsi64);
-  if (cudaEventRecord(ev_g, st) != cudaSuccess || cudaStreamWaitEvent(side, ev_g, 0) != cudaSuccess) return 3;
+  if (cudaEventRecord(ev[0], st) != cudaSuccess || cudaStreamWaitEvent(side, ev[0], 0) != cudaSuccess) return 3;
   bound_u_small_kernel<<<1, 1024, small_smem(m), side>>>(A, u, u64);
-  deferred_small_kernel<<<1, 1024, small_smem(m), side>>>(A);
-  if (cudaEventRecord(ev_u, side) != cudaSuccess) return 3;
-  g_tc_launches.fetch_add(3);
+  if (cudaStreamWaitEvent(side, ev[3], 0) != cudaSuccess) return 3;
+  deferred_small_kernel<<<1, 1024, small_smem(m), side>>>(A, 2);
+  if (cudaEventRecord(ev[1], side) != cudaSuccess) return 3;
+  g_tc_launches.fetch_add(4);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
@@ -1081,7 +1110,7 @@ int dc_deferred(const DcArgs& A, cudaStream_t st) {
     if (cudaFuncSetAttribute(deferred_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(small_smem(kSmallM))) != cudaSuccess)
       return 3;
-    deferred_small_kernel<<<1, 1024, small_smem(m), st>>>(A);
+    deferred_small_kernel<<<1, 1024, small_smem(m), st>>>(A, 0);
     g_tc_launches.fetch_add(1);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
   }

@@ -47,12 +47,13 @@ int dc_prefactor(const DcArgs& A, cudaStream_t st);                 // per broad
 // after allreduce #1: the bound terms and the backward's adjoint operands (fp32 + fp64)
 int dc_bound(const DcArgs& A, float* u, float* dpsi, double* u64, double* dpsi64, cudaStream_t st);
 // dc_bound + dc_deferred with the backward's psi1 operand first: on `st` A's factorisation and
-// G = A^-1 Psi (d Psi ready when `ev_g` fires); on `side` (after ev_g) L^-1, A^-1, G G^T, the bound
-// terms, d Phi and the deferred d Kmm / Phi G, done when `ev_u` fires -- the caller runs the psi1
-// backward kernels in between and makes `st` wait for ev_u before the psi2 backward and the finish.
-// M > 112 (or no side stream): everything on `st`, both events recorded after it.
+// G = A^-1 Psi (d Psi ready when ev[0] fires); on `side2` (from ev[2], recorded on `st` first)
+// Kmm^-1 Phi Kmm^-1 (ev[3]); on `side` (after ev[0]) L^-1, A^-1, G G^T, the bound terms and d Phi,
+// then (after ev[3]) d Kmm, Phi G and the kern_grads terms, done when ev[1] fires -- the caller runs
+// the psi1 backward kernels in between and makes `st` wait for ev[1] before the psi2 backward and the
+// finish.  M > 112 (or no side streams): everything on `st`, ev[0] and ev[1] recorded after it.
 int dc_bound_split(const DcArgs& A, float* u, float* dpsi, double* u64, double* dpsi64, cudaStream_t st,
-                   cudaStream_t side, cudaEvent_t ev_g, cudaEvent_t ev_u);
+                   cudaStream_t side, cudaStream_t side2, cudaEvent_t* ev);
 int dc_deferred(const DcArgs& A, cudaStream_t st);                  // d Kmm, Phi G (before finish)
 int dc_finish(const DcArgs& A, const double* pgrads, cudaStream_t st);  // after allreduce #2
 

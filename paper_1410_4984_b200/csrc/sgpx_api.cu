@@ -365,8 +365,8 @@ struct sgpx_engine {
   // concurrently with the psi1 backward; split_join = the stream still has to wait for ev_split[1]
   bool coord_split = true;
   bool split = false, split_join = false;
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_split[2] = {};
+  cudaStream_t side = nullptr, side2 = nullptr;
+  cudaEvent_t ev_split[4] = {};
   cudaEvent_t ev_pre[2] = {};  // the per-broadcast prefactor on the side stream (dc_setup)
   bool pre_pending = false;
   // one evaluation (device-resident shard, device coordinator) as a CUDA graph, replayed while its
@@ -388,6 +388,7 @@ struct sgpx_engine {
     for (auto& e : ev_pre)
       if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
+    if (side2) cudaStreamDestroy(side2);
     if (graph) cudaGraphExecDestroy(graph);
     for (auto e : ev_in) cudaEventDestroy(e);
     for (auto e : ev_out) cudaEventDestroy(e);
@@ -598,10 +599,11 @@ void engine_coordinate(sgpx_engine* e, bool with_grads) {
     e->split = e->coord_split && e->cfg.m <= 112;
     if (e->split) {
       if (!e->side) CUDA_OK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+      if (!e->side2) CUDA_OK(cudaStreamCreateWithFlags(&e->side2, cudaStreamNonBlocking));
       for (auto& ev : e->ev_split)
         if (!ev) CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
       if (dc_bound_split(e->dc, e->u.get<float>(), e->dpsi.get<float>(), e->u64.get<double>(), e->dpsi64.get<double>(),
-                         ctx->stream, e->side, e->ev_split[0], e->ev_split[1]))
+                         ctx->stream, e->side, e->side2, e->ev_split))
         throw CudaError("coordinator launch");
       e->split_join = true;
     } else if (dc_bound(e->dc, e->u.get<float>(), e->dpsi.get<float>(), e->u64.get<double>(), e->dpsi64.get<double>(),
