@@ -72,7 +72,7 @@ constexpr int kRaw = 4;  // raw-row buffers: copies run kRaw - 1 chunks ahead of
 struct FwdSmem {  // byte offsets
   int g, y, raw, pd, bar, total;
   int raw_stride;  // bytes per raw buffer: mu [q][kFwdK], S [q][kFwdK], Y [d][kFwdK] doubles
-  int pd_stride;   // bytes per stage of per-datapoint floats: a, -b, 1/2 log2(d1 l^2) [3][q][kFwdK], b1 [kFwdK]
+  int pd_stride;   // bytes per stage of per-datapoint floats: a, -b, 1/2 log2(d1 l^2) [3][q][kFwdK]
 };
 __host__ __device__ inline FwdSmem fwd_smem(int q, int d) {
   FwdSmem L{};
@@ -81,7 +81,7 @@ __host__ __device__ inline FwdSmem fwd_smem(int q, int d) {
   L.y = L.g + 2 * 2 * 128 * kFwdK * 4;         // [stage][piece][dp x kFwdK] floats
   L.raw_stride = (2 * q + d) * kFwdK * 8;
   L.raw = L.y + 2 * 2 * dp * kFwdK * 4;        // [kRaw] raw rows
-  L.pd_stride = (3 * q + 1) * kFwdK * 4;
+  L.pd_stride = 3 * q * kFwdK * 4;
   L.pd = L.raw + kRaw * L.raw_stride;          // [stage]
   L.bar = (L.pd + 2 * L.pd_stride + 15) / 16 * 16;  // stage_full[2], mma_done[2], raw_full[kRaw], TMEM slot
   L.total = L.bar + 8 * (4 + kRaw) + 16;
@@ -215,16 +215,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         pd[(Q + q) * kFwdK + nl] = nb;
         pd[(2 * Q + q) * kFwdK + nl] = cl;
       }
-      tc::named_sync(1, kFwdProd);  // every (datapoint, q) constant written
-      for (int nl = pt; nl < kFwdK; nl += kFwdProd) {  // b1 = log2 var + sum_q 1/2 log2(d1 l^2) (q ascending)
-        float b1 = P.log2_var;
-#pragma unroll
-        for (int q = 0; q < Q; ++q) b1 += pd[(2 * Q + q) * kFwdK + nl];
-        pd[3 * Q * kFwdK + nl] = n0 + nl < P.n ? b1 : -CUDART_INF_F;
-      }
+
       float* yb = ysm + st * 2 * dp * kFwdK;  // the Y chunk as tf32 pieces: rows = output dims, K = datapoints
+      // rotated start: the producers that took a second (datapoint, q) item above get the fewest Y items
+      const int pr = (pt + kFwdProd - (kFwdK * Q) % kFwdProd) % kFwdProd;
 #pragma unroll 4
-      for (int i = pt; i < kFwdK * d; i += kFwdProd) {
+      for (int i = pr; i < kFwdK * d; i += kFwdProd) {
         const int nl = i % kFwdK, dd = i / kFwdK;
         const double y = n0 + nl < P.n ? raw[(2 * Q + dd) * kFwdK + nl] : 0.0;
         bad |= isfinite(y) ? 0 : 1;
@@ -282,10 +278,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       float* gb = gsm + st * 2 * 128 * kFwdK;
       {
         float b[8], e[2][8];
-        {
-          const float4 b0 = *reinterpret_cast<const float4*>(pd + 3 * Q * kFwdK + 8 * gj);
-          const float4 b4 = *reinterpret_cast<const float4*>(pd + 3 * Q * kFwdK + 8 * gj + 4);
-          b[0] = b0.x, b[1] = b0.y, b[2] = b0.z, b[3] = b0.w, b[4] = b4.x, b[5] = b4.y, b[6] = b4.z, b[7] = b4.w;
+        {  // b1 = log2 var + sum_q 1/2 log2(d1 l^2), q ascending (rows past N: -inf)
+          const int64_t n0 = chunk_of(l) * kFwdK;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) b[u] = P.log2_var;
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            const float4 c0 = *reinterpret_cast<const float4*>(pd + (2 * Q + q) * kFwdK + 8 * gj);
+            const float4 c4 = *reinterpret_cast<const float4*>(pd + (2 * Q + q) * kFwdK + 8 * gj + 4);
+            b[0] += c0.x, b[1] += c0.y, b[2] += c0.z, b[3] += c0.w, b[4] += c4.x, b[5] += c4.y, b[6] += c4.z,
+                b[7] += c4.w;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (n0 + 8 * gj + u >= P.n) b[u] = -CUDART_INF_F;
         }
         float2 e2[2][4];
 #pragma unroll
