@@ -209,6 +209,11 @@ double* fwd_pair_sums(const PsiConst& P, double* region, int num_sms, int64_t* c
   return rt_fwd_pair_sums(P, region, num_sms, count);
 }
 
+const float* fwd_pair_operand(const PsiConst& P, const double* region, int num_sms) {
+  if (is_syrk(P) || is_direct(P)) return nullptr;
+  return rt_fwd_pair_operand(P, region, num_sms);
+}
+
 int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, int num_sms, void* stream,
                 LaunchGeom* geom, void* ev_begin, void* ev_end) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);

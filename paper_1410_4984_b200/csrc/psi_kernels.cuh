@@ -60,6 +60,7 @@ struct PsiConst {
   unsigned long long* prof;   // optional per-phase cycle counters (SGPX_TC_PROFILE=1), else null
   int mode;                   // kModeFast / kModePrecise / kModeDirect (psi_select_mode)
   void* ev_psi2[2];           // optional cudaEvent_t pair recorded around the main psi2 kernel (roofline)
+  const float* rt_pairs_shared;  // row-tile forward: another sub-shard's pair operand (N-independent), else null
 };
 
 // Backward-only inputs.
@@ -76,6 +77,10 @@ struct BwdConst {
   int64_t ld_g;
   const double* fwd_rt;  // row-tile path: the forward's feature / pair-sum region (rt_fwd_region)
   int skip_pair_terms;   // sub-shard passes: the per-pair gradient terms are added by one call only
+  // row-tile backward: the N-independent pair operand (U-weighted pair features) and Y scales of an
+  // earlier sub-shard's call (inputs, null = compute them), and where this call's are (outputs, optional)
+  const float *rt_pre_shared, *rt_ys_shared;
+  const float **rt_pre_out, **rt_ys_out;
 };
 
 // Packed per-CTA partial layouts (fp64, CTA-private rows, single-writer per slot):
@@ -125,6 +130,9 @@ bool psi_backward_phased(const PsiConst& P);
 // inside it: sub-shard forwards add theirs into the first sub-shard's before the gradient pass.
 const double* fwd_region(const PsiConst& P, const double* fwd_part, int num_sms);
 double* fwd_pair_sums(const PsiConst& P, double* region, int num_sms, int64_t* count);
+// the row-tile forward's pair operand inside `region` (N-independent: later sub-shards reuse the
+// first one's through PsiConst::rt_pairs_shared); null off the row-tile path
+const float* fwd_pair_operand(const PsiConst& P, const double* region, int num_sms);
 
 // psi1 kernels paired with the row-tile psi2 (psi1_kernels.cu: any M; psi1_tile.cu: M <= 128).
 int psi1_fwd_rows(const PsiConst& P, int num_sms);
@@ -155,6 +163,7 @@ int64_t rt_bwd_doubles(const PsiConst& P, int num_sms);
 int rt_forward(const PsiConst& P, double* base, double* packed, int num_sms, void* stream);
 int rt_backward(const PsiConst& P, const BwdConst& B, double* bbase, double* prow, int num_sms, void* stream);
 double* rt_fwd_pair_sums(const PsiConst& P, double* region, int num_sms, int64_t* count);
+const float* rt_fwd_pair_operand(const PsiConst& P, const double* region, int num_sms);
 // Direct-difference kernels (psi_direct.cu): the complete forward (validation, yy, KL, Phi, Psi) and
 // backward (d mu, d S, d Z, d l, d var) with fp64 exponents.
 bool direct_supported(const PsiConst& P);

@@ -1144,7 +1144,7 @@ int rt_forward_q(const PsiConst& P, double* base, double* packed, int num_sms, c
   float* fl = floats_at(base, L.off_floats);
   const int np = rt_pieces(P);
   RowTileArgs R{};
-  R.a = fl + L.f_fs;
+  R.a = P.rt_pairs_shared ? P.rt_pairs_shared : fl + L.f_fs;  // the pair operand does not depend on the rows
   R.a_stride = L.p_pad * C::K1;
   R.pre = fl + L.f_pre;
   R.mode = 0;
@@ -1169,10 +1169,13 @@ int rt_forward_q(const PsiConst& P, double* base, double* packed, int num_sms, c
   auto run = [&](auto np_tag, auto bf_tag) -> int {
     constexpr int NP = decltype(np_tag)::value;
     constexpr bool BF = decltype(bf_tag)::value;
-    rt_pair_rows_kernel<Q, NP><<<blocks_p, 256, 0, st>>>(P, L.p_pad, fl + L.f_fs, L.p_pad * C::K1);
+    if (!P.rt_pairs_shared) {
+      rt_pair_rows_kernel<Q, NP><<<blocks_p, 256, 0, st>>>(P, L.p_pad, fl + L.f_fs, L.p_pad * C::K1);
+      g_tc_launches.fetch_add(1);
+    }
     rt_data_rows_kernel<Q, BF, false, NP><<<blocks_n, 256, 0, st>>>(P, L.n_pad, fl + L.f_hs, L.n_pad * C::K1,
                                                                     fl + L.f_pre, ys);
-    g_tc_launches.fetch_add(2);
+    g_tc_launches.fetch_add(1);
     return launch_rowtile<Q, BF, false, NP>(P, R, dim3(unsigned(R.ntiles), unsigned(L.ns)), st);
   };
   using T2 = std::integral_constant<int, 2>;
@@ -1199,22 +1202,31 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
   // the forward's piece count (same deterministic decision on the same inputs)
   const int np = rt_pieces(P);
   float* ys = reinterpret_cast<float*>(bbase + L.off_ys);
-  rt_yscale_kernel<Q><<<1, 256, 0, st>>>(P, B.u, ys);
-  if (np == 3) rt_pair_pre_kernel<Q, false, 3><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, ys, pre);
-  else rt_pair_pre_kernel<Q, false, 2><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, ys, pre);
-  g_tc_launches.fetch_add(2);
+  const float* pre_use = pre;
+  const float* ys_use = ys;
+  if (B.rt_pre_shared && B.rt_ys_shared) {  // an earlier sub-shard's (U-weighted pair features, Y scales)
+    pre_use = B.rt_pre_shared;
+    ys_use = B.rt_ys_shared;
+  } else {
+    rt_yscale_kernel<Q><<<1, 256, 0, st>>>(P, B.u, ys);
+    if (np == 3) rt_pair_pre_kernel<Q, false, 3><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, ys, pre);
+    else rt_pair_pre_kernel<Q, false, 2><<<blocks_p, 256, 0, st>>>(P, B.u, F.p_pad, ys, pre);
+    g_tc_launches.fetch_add(2);
+  }
+  if (B.rt_pre_out) *B.rt_pre_out = pre_use;
+  if (B.rt_ys_out) *B.rt_ys_out = ys_use;
   if (P.n > 0) {
     RowTileArgs R{};
     R.a = ff + F.f_hs;
     R.a_stride = F.n_pad * RT<Q, false>::K1;
-    R.pre = pre;
+    R.pre = pre_use;
     R.mode = 1;
     R.ntiles = L.ntiles;
     R.nchunks = L.pchunks;
     R.cps = L.pchunks;
     R.nrows_static = P.n;
     R.out = bbase + L.off_t;
-    R.yinv = ys + 64;
+    R.yinv = ys_use + 64;
     const int rc = np == 3 ? launch_rowtile<Q, false, false, 3>(P, R, dim3(unsigned(L.grid)), st)
                            : launch_rowtile<Q, false, false, 2>(P, R, dim3(unsigned(L.grid)), st);
     if (rc) return rc;
@@ -1262,6 +1274,10 @@ double* rt_fwd_pair_sums(const PsiConst& P, double* region, int num_sms, int64_t
   return region + L.off_sums;
 }
 int64_t rt_bwd_doubles(const PsiConst& P, int num_sms) { return bwd_layout(P, num_sms).doubles; }
+const float* rt_fwd_pair_operand(const PsiConst& P, const double* region, int num_sms) {
+  const FwdLayout L = fwd_layout(P, num_sms);
+  return floats_at(const_cast<double*>(region), L.off_floats) + L.f_fs;
+}
 
 int rt_forward(const PsiConst& P, double* base, double* packed, int num_sms, void* stream) {
   SGPX_RT_DISPATCH(rt_forward_q, P, base, packed, num_sms, static_cast<cudaStream_t>(stream))

@@ -524,8 +524,15 @@ void engine_stats_pass(sgpx_engine* e) {
       CUDA_OK(cudaEventRecord(e->ev_in[j], e->copy));
     }
   }
+  // the row-tile forward's pair operand does not depend on the rows: later sub-shards reuse the first's
+  const float* pairs0 =
+      k > 1 ? fwd_pair_operand(e->subs[0].P, fwd_region(e->subs[0].P, e->fpart.get<double>() + e->subs[0].foff,
+                                                        ctx->num_sms),
+                               ctx->num_sms)
+            : nullptr;
   for (int j = 0; j < k; ++j) {
     auto& sub = e->subs[j];
+    sub.P.rt_pairs_shared = j > 0 ? pairs0 : nullptr;
     if (e->pending_upload) CUDA_OK(cudaStreamWaitEvent(ctx->stream, e->ev_in[j], 0));
     double* out = k > 1 ? e->pstats_sub.get<double>() + int64_t(j) * count : e->pstats.get<double>();
     sub.P.ev_psi2[0] = j == 0 ? e->ev[8] : nullptr;  // the first sub-shard's main psi2 kernel (roofline)
@@ -704,6 +711,7 @@ void engine_grad_pass(sgpx_engine* e) {
       CUDA_OK(cudaGetLastError());
     }
     const bool stream_out = e->has_gout && e->latent;
+    const float *rt_pre0 = nullptr, *rt_ys0 = nullptr;
     auto bconst = [&](const sgpx_engine::Sub& sub, int j) {
       BwdConst B{};
       B.u = e->u.get<float>();
@@ -718,6 +726,14 @@ void engine_grad_pass(sgpx_engine* e) {
       B.ld_g = e->in.n;
       B.fwd_rt = fwd_region(sub.P, e->fpart.get<double>() + sub.foff, ctx->num_sms);
       B.skip_pair_terms = (fold && j > 0) ? 1 : 0;
+      // the U-weighted pair operand and Y scales of the psi2 backward do not depend on the rows
+      if (j == 0) {
+        B.rt_pre_out = &rt_pre0;
+        B.rt_ys_out = &rt_ys0;
+      } else {
+        B.rt_pre_shared = rt_pre0;
+        B.rt_ys_shared = rt_ys0;
+      }
       return B;
     };
     auto out_of = [&](int j) {
