@@ -325,6 +325,89 @@ def test_device_coordinator_matches_host(sgp, latent, m, monkeypatch):
         assert rel_err(a.grads.d_mu, b.grads.d_mu) < 1e-11
 
 
+@pytest.mark.parametrize("m", [1, 7, 32, 33, 64, 97, 112])
+def test_split_coordinator_small_m_edges(sgp, m, monkeypatch):
+    """The split device coordinator (dcoord.cu: bound_g_small_kernel's blocked Cholesky with a short last
+    32-column panel, D^-1 blocks, W = L^-1 in place, G = W^T W Psi; bound_u / deferred on the side
+    streams) against the host coordinator at the panel edges, with and without gradients."""
+    from paper_1410_4984_b200 import synthetic
+
+    w = synthetic.make(True, 6_000, 5, 3, m, seed=21 + m)
+    for with_grads in (True, False):
+        out = []
+        for dev in ("1", "0"):
+            monkeypatch.setenv("SGPX_DEVICE_COORD", dev)
+            eng = sgp.Engine(sgp.ModelKind.latent, w.mu, w.s, w.y, precision="direct")
+            eng.broadcast(w.kernel, w.beta, w.z)
+            out.append(eng.evaluate(with_grads))
+            eng.close()
+        a, b = out
+        assert rel_err(a.bound.total, b.bound.total) < 1e-12
+        for f in sgp.BOUND_FIELDS:
+            assert rel_err(getattr(a.bound, f), getattr(b.bound, f)) < 1e-11, (f, with_grads)
+        if with_grads:
+            for g in ("d_z", "d_lengthscales", "d_variance", "d_beta", "d_mu", "d_s"):
+                assert rel_err(getattr(a.grads, g), getattr(b.grads, g)) < 1e-9, g
+
+
+def test_split_coordinator_escalation(sgp, monkeypatch):
+    """A near-duplicate inducing point: Kmm is singular to working precision, so factor_gram's jitter
+    escalation runs (prefactor_small_kernel on the side stream during the forward, coordinator.cpp on the
+    host) and the split coordinator factors A = Kmm + jitter + beta Phi with it; both pick the same jitter
+    factor and agree."""
+    from paper_1410_4984_b200 import synthetic
+
+    w = synthetic.make(True, 4_000, 3, 2, 24, seed=5)
+    z = np.array(w.z, copy=True)
+    z[1] = z[0] + 1e-9  # Kmm singular to working precision: factor_gram's jitter, then A's shift
+    out = []
+    for dev in ("1", "0"):
+        monkeypatch.setenv("SGPX_DEVICE_COORD", dev)
+        eng = sgp.Engine(sgp.ModelKind.latent, w.mu, w.s, w.y, precision="direct")
+        eng.broadcast(w.kernel, w.beta, z)
+        out.append(eng.evaluate(True))
+        eng.close()
+    a, b = out
+    assert a.jitter_factor == b.jitter_factor and a.jitter_factor > 0.0
+    assert rel_err(a.bound.total, b.bound.total) < 1e-9
+    # cond(Kmm + jitter) ~ 1e12 here: the two fp64 summation orders differ at ~1e-5 in d mu (measured 8.5e-6)
+    assert rel_err(a.grads.d_mu, b.grads.d_mu) < 1e-4
+
+
+@pytest.mark.parametrize("n,q,d,m", [(50_000, 10, 50, 100), (20_011, 6, 17, 40), (9_000, 12, 64, 128)])
+def test_psi1_backward_pipeline_matches_first_version(sgp, orc, n, q, d, m, monkeypatch):
+    """psi1_bwd_pipe_kernel (TMA prefetch of the next chunk, T through TMEM, FFMA2) against the first
+    tcgen05 backward (SGPX_PSI1_BWD=old) and the oracle: the same statistics and gradients to the mixed
+    tolerance (the two sum T in a different fp32 order)."""
+    from paper_1410_4984_b200 import synthetic
+
+    w = synthetic.make(True, n, q, d, m, seed=31)
+    out = []
+    for old in ("0", "1"):
+        if old == "1":
+            monkeypatch.setenv("SGPX_PSI1_BWD", "old")
+        else:
+            monkeypatch.delenv("SGPX_PSI1_BWD", raising=False)
+        eng = sgp.Engine(sgp.ModelKind.latent, w.mu, w.s, w.y)
+        eng.broadcast(w.kernel, w.beta, w.z)
+        out.append(eng.evaluate(True))
+        eng.close()
+    a, b = out
+    for g in ("d_z", "d_lengthscales", "d_variance", "d_mu", "d_s"):
+        assert norm_rel_err(getattr(a.grads, g), getattr(b.grads, g)) < 2e-6, g
+    # against the oracle: no worse than the first version, entry by entry (the worst d Z entries are residues
+    # of cancelling sums, ~5e3 x below the block's largest, and carry the row-tile kernels' mixed-precision
+    # rounding in both: tools/dbg_dz_check.py) and within the suite's norm-wise tolerance
+    ref = orc.engine_evaluate(True, w.mu, w.s, w.y, w.z, w.variance, w.lengthscales, w.beta, workers=THREADS)
+    assert rel_err(a.bound.total, ref.bound["total"]) < STAT_TOL
+    for g in ("d_z", "d_lengthscales", "d_variance", "d_mu", "d_s"):
+        r = np.ravel(getattr(ref, g))
+        ea = np.max(np.abs(np.ravel(getattr(a.grads, g)) - r) / np.maximum(np.abs(r), 1e-300))
+        eb = np.max(np.abs(np.ravel(getattr(b.grads, g)) - r) / np.maximum(np.abs(r), 1e-300))
+        assert ea <= 1.1 * eb + 1e-9, (g, ea, eb)
+        assert norm_rel_err(getattr(a.grads, g), getattr(ref, g)) < GRAD_TOL, g
+
+
 @pytest.mark.parametrize("workers", [2, 3])
 @pytest.mark.parametrize("latent", [True, False])
 def test_multi_gpu_engine(sgp, orc, workers, latent):
