@@ -63,6 +63,15 @@ using pc::h2u;
 // stage; two D/G stages of 192 TMEM columns plus the concatenated accumulators fill the 512 columns
 // (psi2 kernels at C3 2.13 / 2.16 -> 1.90 / 1.89 ms, C5 290 -> 231 ms / evaluation).
 constexpr int kCH = SGPX_RT_CH;
+// Exponentials on the FMA pipe (ex2_poly) instead of MUFU.EX2, one in k per consumer (0: none): the
+// consumers are XU-bound: forward 1 in 16, backward 1 in 32 measured -1.6 % per C3 evaluation (profiles/r02/poly_ab.txt)
+#ifndef SGPX_RT_POLY_F
+#define SGPX_RT_POLY_F 16
+#endif
+#ifndef SGPX_RT_POLY_B
+#define SGPX_RT_POLY_B 32
+#endif
+constexpr int kRtPolyFwd = SGPX_RT_POLY_F, kRtPolyBwd = SGPX_RT_POLY_B;
 constexpr int kGroups = 3;              // consumer warps per TMEM lane quarter (32 columns each)
 constexpr int kCons = 128 * kGroups;    // consumer threads   (warps 0 .. 11)
 constexpr int kDrain = 128;             // accumulator drain threads (warps 12 .. 15)
@@ -789,7 +798,7 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
         tc::ld16(dcol, r0);
         tc::ld16(dcol + 16, r1);
         tc::ld_wait();
-        auto exps = [&](const uint32_t (&r)[16], int i, float (&v)[4]) {
+        auto exps = [&](const uint32_t (&r)[16], int i, float (&v)[4], int gbase) {
           if (R.dbg & 8) {  // timing experiment: TMEM traffic without the exp2 math
             v[0] = __uint_as_float(r[i]);
             v[1] = __uint_as_float(r[i + 1]);
@@ -798,18 +807,24 @@ __global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTil
             return;
           }
           // every exponential on MUFU.EX2 (the FMA-pipe polynomial of round 1 cost ~11 instructions
-          // where MUFU takes one; measured: one in four or one in eight on it is no faster)
+          // where MUFU takes one; measured at 96-row chunks: one in four or one in eight on it is no
+          // faster).  SGPX_RT_POLY = k > 0 (experiment builds): one in k on the FMA-pipe polynomial.
           v[0] = ex2(__uint_as_float(r[i]));
           v[1] = ex2(__uint_as_float(r[i + 1]));
           v[2] = ex2(__uint_as_float(r[i + 2]));
-          v[3] = ex2(__uint_as_float(r[i + 3]));
+          {
+            constexpr int kp = BF ? kRtPolyFwd : kRtPolyBwd;  // one in kp on the FMA pipe (0: none)
+            const int gi = gbase + i / 4;                     // group of 4 within the 32-datapoint block
+            v[3] = (kp > 0 && gi % (kp > 0 ? kp / 4 : 1) == 0) ? ex2_poly(__uint_as_float(r[i + 3]))
+                                                             : ex2(__uint_as_float(r[i + 3]));
+          }
         };
         uint32_t hi[16], lo[16];
         auto half = [&](const uint32_t (&r)[16], int base) {
 #pragma unroll
           for (int i = 0; i < 16; i += 4) {
             float v[4];
-            exps(r, i, v);
+            exps(r, i, v, base / 2);
 #pragma unroll
             for (int u = 0; u < 4; u += 2) {
               if (BF) {
