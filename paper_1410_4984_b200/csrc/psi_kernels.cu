@@ -288,7 +288,15 @@ int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* pac
   if (ev_end) record_event(ev_end, st);
   const int64_t rt_rows = (rt_bwd_doubles(P, num_sms) + pstride - 1) / pstride;
   double* tmp = part + (int64_t(rows) + rt_rows) * pstride;
-  if (int rc = bwd_reduce_rows(part, pstride, rows, packed, B.d_phi * double(P.n), tmp, stream)) return rc;
+  if (B.reduce_stream && B.reduce_event) {  // off the pass's stream: the next sub-shard's kernels do not wait
+    cudaStream_t rs = static_cast<cudaStream_t>(B.reduce_stream);
+    if (cudaEventRecord(static_cast<cudaEvent_t>(B.reduce_event), st) != cudaSuccess ||
+        cudaStreamWaitEvent(rs, static_cast<cudaEvent_t>(B.reduce_event), 0) != cudaSuccess)
+      return 3;
+    if (int rc = bwd_reduce_rows(part, pstride, rows, packed, B.d_phi * double(P.n), tmp, rs)) return rc;
+  } else if (int rc = bwd_reduce_rows(part, pstride, rows, packed, B.d_phi * double(P.n), tmp, stream)) {
+    return rc;
+  }
   if (geom) *geom = g;
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }

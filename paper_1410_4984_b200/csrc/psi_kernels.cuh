@@ -81,6 +81,9 @@ struct BwdConst {
   // earlier sub-shard's call (inputs, null = compute them), and where this call's are (outputs, optional)
   const float *rt_pre_shared, *rt_ys_shared;
   const float **rt_pre_out, **rt_ys_out;
+  // sub-shard passes: run the partial-row reduction on this stream (after reduce_event, recorded on the
+  // pass's stream) instead of the pass's stream; the caller joins it before using `packed`
+  void *reduce_stream, *reduce_event;
 };
 
 // Packed per-CTA partial layouts (fp64, CTA-private rows, single-writer per slot):

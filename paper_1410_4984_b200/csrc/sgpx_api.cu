@@ -368,6 +368,7 @@ struct sgpx_engine {
   cudaStream_t side = nullptr, side2 = nullptr;
   cudaEvent_t ev_split[4] = {};
   cudaEvent_t ev_pre[2] = {};  // the per-broadcast prefactor on the side stream (dc_setup)
+  cudaEvent_t ev_red[2] = {};  // sub-shard backward reductions on side2: fork (per sub-shard), join
   bool pre_pending = false;
   // one evaluation (device-resident shard, device coordinator) as a CUDA graph, replayed while its
   // launch arguments are unchanged (graph_key)
@@ -386,6 +387,8 @@ struct sgpx_engine {
     for (auto& e : ev_split)
       if (e) cudaEventDestroy(e);
     for (auto& e : ev_pre)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : ev_red)
       if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
     if (side2) cudaStreamDestroy(side2);
@@ -739,6 +742,14 @@ void engine_grad_pass(sgpx_engine* e) {
     auto out_of = [&](int j) {
       return k > 1 ? e->pgrads_sub.get<double>() + int64_t(j) * count : e->pgrads.get<double>();
     };
+    // sub-shards: each one's partial-row reduction on side2, joined before the sub-shard sum
+    const char* rs_env = getenv("SGPX_RED_SIDE");  // A/B
+    const bool red_side = k > 1 && !(rs_env && atoi(rs_env) == 0);
+    if (red_side) {
+      if (!e->side2) CUDA_OK(cudaStreamCreateWithFlags(&e->side2, cudaStreamNonBlocking));
+      for (auto& ev : e->ev_red)
+        if (!ev) CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
     // with streamed-out d mu / d S only the first sub-shards run their psi1 kernels ahead (enough to
     // cover the side stream's coordinator); the rest keep psi1 -> psi2 -> copy-out per sub-shard so the
     // device-to-host copies start early
@@ -756,7 +767,12 @@ void engine_grad_pass(sgpx_engine* e) {
       auto& sub = e->subs[j];
       sub.P.ev_psi2[0] = j == 0 ? e->ev[10] : nullptr;
       sub.P.ev_psi2[1] = j == 0 ? e->ev[11] : nullptr;
-      if (psi_backward(sub.P, bconst(sub, j), e->bpart.get<double>() + sub.boff, out_of(j), nsm, ctx->stream, &e->gb,
+      BwdConst Bj = bconst(sub, j);
+      if (red_side) {
+        Bj.reduce_stream = e->side2;
+        Bj.reduce_event = e->ev_red[0];
+      }
+      if (psi_backward(sub.P, Bj, e->bpart.get<double>() + sub.boff, out_of(j), nsm, ctx->stream, &e->gb,
                        (j == 0 && !phased) ? e->ev[6] : nullptr, j == k - 1 ? e->ev[7] : nullptr, j < kp ? 2 : 0))
         throw CudaError(std::string("psi backward launch: ") + cudaGetErrorString(cudaGetLastError()));
       if (stream_out) {  // d mu / d S of this sub-shard are final: copy them out while the next runs
@@ -771,6 +787,10 @@ void engine_grad_pass(sgpx_engine* e) {
       }
     }
     if (k > 1) {
+      if (red_side) {
+        CUDA_OK(cudaEventRecord(e->ev_red[1], e->side2));
+        CUDA_OK(cudaStreamWaitEvent(ctx->stream, e->ev_red[1], 0));
+      }
       sum_parts_kernel<<<int(std::min<int64_t>((count + 255) / 256, 1024)), 256, 0, ctx->stream>>>(
           e->pgrads_sub.get<double>(), k, count, e->pgrads.get<double>());
       CUDA_OK(cudaGetLastError());

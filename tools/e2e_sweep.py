@@ -1,7 +1,7 @@
 """End-to-end C3 evaluation time (pinned host mu/S uploaded by broadcast(), d_mu/d_S streamed back)
 for a list of sub-shard plans (SGPX_SUBS) and coordinator placements (SGPX_DEVICE_COORD).
 
-  python tools/e2e_sweep.py [steps] "plan1" "plan2" ...     plan = "<subs>|<devcoord 0/1>", e.g. "1,2,2|0"
+  python tools/e2e_sweep.py [steps] "plan1" "plan2" ...     plan = "<subs>|<devcoord 0/1>[|NAME=v,...]", e.g. "1,2,2|0"
 """
 import os
 import sys
@@ -26,7 +26,11 @@ mu_np, s_np = mu_p.numpy().T, s_p.numpy().T
 gmu_p = torch.empty(q, n, dtype=torch.float64, pin_memory=True)
 gs_p = torch.empty(q, n, dtype=torch.float64, pin_memory=True)
 for plan in plans:
-    subs, _, dc = plan.partition("|")
+    subs, _, rest = plan.partition("|")
+    dc, _, extra = rest.partition("|")  # optional third field: NAME=value set for this plan
+    for kv in filter(None, extra.split(",")):
+        name, _, val = kv.partition("=")
+        os.environ[name] = val
     if subs:
         os.environ["SGPX_SUBS"] = subs
     else:
