@@ -395,20 +395,27 @@ cublasHandle_t handle_for_device() {
 
 // Batched forward: C_i = A_i^T B_i for the nb sub-chunks of kSub rows (A_i = rows of the chunk matrix,
 // lda = nc), each the sum of the three split products; fp32 accumulation over kSub rows only.
+// The M x M block of C is only ever used symmetrised (syrk_pack_kernel: Phi = (C + C^T) / 2), and there
+// small^T big = (big^T small)^T, so it takes two passes: big^T big + 2 big^T small.  The M x D block
+// (Psi) keeps all three: big^T big + big^T small + small^T big.
 int gemm3_batched_t(cublasHandle_t h, cudaStream_t st, int m, int n, int nb, int nc, const float* big,
                     const float* small, float* c) {
   if (cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) return 3;
-  const float one = 1.f, zero = 0.f;
-  const float* as[3] = {big, big, small};
-  const float* bs[3] = {big, small, big};
-  for (int i = 0; i < 3; ++i) {
-    if (cublasGemmStridedBatchedEx(h, CUBLAS_OP_T, CUBLAS_OP_N, m, n, int(kSub), &one, as[i], CUDA_R_32F, nc, kSub,
-                                   bs[i], CUDA_R_32F, nc, kSub, i == 0 ? &zero : &one, c, CUDA_R_32F, m,
-                                   int64_t(m) * n, nb, CUBLAS_COMPUTE_32F_FAST_TF32,
-                                   CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
-      return 3;
+  const float one = 1.f, two = 2.f, zero = 0.f;
+  const int d = n - m;
+  const int64_t cs = int64_t(m) * n, yoff = int64_t(m) * nc;  // batch stride of C, the Y columns of [K | Y]
+  auto pass = [&](int cols, const float* a, const float* b, const float* alpha, const float* beta, float* cc) {
+    return cublasGemmStridedBatchedEx(h, CUBLAS_OP_T, CUBLAS_OP_N, m, cols, int(kSub), alpha, a, CUDA_R_32F, nc, kSub,
+                                      b, CUDA_R_32F, nc, kSub, beta, cc, CUDA_R_32F, m, cs, nb,
+                                      CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT) == CUBLAS_STATUS_SUCCESS;
+  };
+  if (!pass(n, big, big, &one, &zero, c)) return 3;              // big^T [big | big_Y]
+  if (!pass(m, big, small, &two, &one, c)) return 3;             // + 2 big^T small   (Phi block)
+  if (d > 0) {
+    if (!pass(d, big, small + yoff, &one, &one, c + int64_t(m) * m)) return 3;  // + big^T small_Y
+    if (!pass(d, small, big + yoff, &one, &one, c + int64_t(m) * m)) return 3;  // + small^T big_Y
   }
-  g_tc_launches.fetch_add(3);
+  g_tc_launches.fetch_add(d > 0 ? 4 : 2);
   return 0;
 }
 
