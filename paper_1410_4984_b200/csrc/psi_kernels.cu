@@ -253,7 +253,7 @@ int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, 
 bool psi_backward_phased(const PsiConst& P) { return !is_syrk(P) && !is_direct(P); }
 
 int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
-                 LaunchGeom* geom, void* ev_begin, void* ev_end, int phase) {
+                 LaunchGeom* geom, void* ev_begin, void* ev_end, int phase, void* reduce_stream, void* reduce_event) {
   if (!B.fwd_rt) return 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   LaunchGeom g{};
@@ -288,10 +288,10 @@ int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* pac
   if (ev_end) record_event(ev_end, st);
   const int64_t rt_rows = (rt_bwd_doubles(P, num_sms) + pstride - 1) / pstride;
   double* tmp = part + (int64_t(rows) + rt_rows) * pstride;
-  if (B.reduce_stream && B.reduce_event) {  // off the pass's stream: the next sub-shard's kernels do not wait
-    cudaStream_t rs = static_cast<cudaStream_t>(B.reduce_stream);
-    if (cudaEventRecord(static_cast<cudaEvent_t>(B.reduce_event), st) != cudaSuccess ||
-        cudaStreamWaitEvent(rs, static_cast<cudaEvent_t>(B.reduce_event), 0) != cudaSuccess)
+  if (reduce_stream && reduce_event) {  // off the pass's stream: the next sub-shard's kernels do not wait
+    cudaStream_t rs = static_cast<cudaStream_t>(reduce_stream);
+    if (cudaEventRecord(static_cast<cudaEvent_t>(reduce_event), st) != cudaSuccess ||
+        cudaStreamWaitEvent(rs, static_cast<cudaEvent_t>(reduce_event), 0) != cudaSuccess)
       return 3;
     if (int rc = bwd_reduce_rows(part, pstride, rows, packed, B.d_phi * double(P.n), tmp, rs)) return rc;
   } else if (int rc = bwd_reduce_rows(part, pstride, rows, packed, B.d_phi * double(P.n), tmp, stream)) {

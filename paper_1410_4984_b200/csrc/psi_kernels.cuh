@@ -81,9 +81,6 @@ struct BwdConst {
   // earlier sub-shard's call (inputs, null = compute them), and where this call's are (outputs, optional)
   const float *rt_pre_shared, *rt_ys_shared;
   const float **rt_pre_out, **rt_ys_out;
-  // sub-shard passes: run the partial-row reduction on this stream (after reduce_event, recorded on the
-  // pass's stream) instead of the pass's stream; the caller joins it before using `packed`
-  void *reduce_stream, *reduce_event;
 };
 
 // Packed per-CTA partial layouts (fp64, CTA-private rows, single-writer per slot):
@@ -125,8 +122,11 @@ int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, 
                 void* stream, LaunchGeom* geom, void* ev_begin = nullptr, void* ev_end = nullptr);
 // phase (row-tile path only): 0 the whole pass, 1 the psi1 kernel alone (it needs d Psi, not d Phi),
 // 2 the rest (psi2 kernels, reduction) -- so a caller can overlap the coordinator's d Phi with phase 1.
+// reduce_stream / reduce_event (sub-shard passes): the partial-row reduction runs on reduce_stream after
+// reduce_event (recorded on `stream`); the caller joins it before using `packed`.
 int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
-                 LaunchGeom* geom, void* ev_begin = nullptr, void* ev_end = nullptr, int phase = 0);
+                 LaunchGeom* geom, void* ev_begin = nullptr, void* ev_end = nullptr, int phase = 0,
+                 void* reduce_stream = nullptr, void* reduce_event = nullptr);
 // true when psi_backward can run in two phases for P (the row-tile path)
 bool psi_backward_phased(const PsiConst& P);
 // Where the forward left the region the backward reads (BwdConst::fwd_rt), and the per-pair sums

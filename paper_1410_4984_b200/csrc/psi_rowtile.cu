@@ -955,21 +955,29 @@ __global__ void __launch_bounds__(256) rt_bwd_epilogue_kernel(PsiConst P, BwdCon
   double dl[Q];
 #pragma unroll
   for (int q = 0; q < Q; ++q) dl[q] = 0.0;
+  // restrict-qualified views: the read-modify-writes of d mu / d S cannot alias t, mu or S, so the loads
+  // of a datapoint issue together (without it the code generation, and a memory-bound kernel's time,
+  // varied by 60 % between builds)
+  const double* __restrict__ tv = t;
+  const double* __restrict__ muv = P.mu;
+  const double* __restrict__ sv = P.s;
+  double* __restrict__ dmuv = B.d_mu;
+  double* __restrict__ dsv = B.d_s;
   for (int64_t n = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; n < P.n; n += int64_t(gridDim.x) * blockDim.x) {
-    const double* tn = t + n * NH;
+    const double* tn = tv + n * NH;
     const double t0 = tn[0];
 #pragma unroll
     for (int q = 0; q < Q; ++q)
       if (q < P.q) {
-        const double mu = P.mu[q * P.ld_mu + n] - P.center[q];
-        const double s = P.expected ? P.s[q * P.ld_s + n] : 0.0;
+        const double mu = muv[q * P.ld_mu + n] - P.center[q];
+        const double s = P.expected ? sv[q * P.ld_s + n] : 0.0;
         const double ls = P.ls[q];
         const double d2 = 1.0 / (2.0 * s + ls * ls);
         const double t1 = tn[1 + q], t2 = tn[1 + Q + q];
         const double quad = mu * mu * t0 - 2.0 * mu * t1 + t2;
         if (B.write_local) {
-          B.d_mu[q * B.ld_g + n] += -2.0 * d2 * (mu * t0 - t1);
-          if (P.expected) B.d_s[q * B.ld_g + n] += 2.0 * d2 * d2 * quad - d2 * t0;
+          dmuv[q * B.ld_g + n] += -2.0 * d2 * (mu * t0 - t1);
+          if (P.expected) dsv[q * B.ld_g + n] += 2.0 * d2 * d2 * quad - d2 * t0;
         }
         dl[q] += 2.0 * ls * d2 * d2 * quad + (2.0 * s * d2 / ls) * t0;
       }

@@ -767,13 +767,9 @@ void engine_grad_pass(sgpx_engine* e) {
       auto& sub = e->subs[j];
       sub.P.ev_psi2[0] = j == 0 ? e->ev[10] : nullptr;
       sub.P.ev_psi2[1] = j == 0 ? e->ev[11] : nullptr;
-      BwdConst Bj = bconst(sub, j);
-      if (red_side) {
-        Bj.reduce_stream = e->side2;
-        Bj.reduce_event = e->ev_red[0];
-      }
-      if (psi_backward(sub.P, Bj, e->bpart.get<double>() + sub.boff, out_of(j), nsm, ctx->stream, &e->gb,
-                       (j == 0 && !phased) ? e->ev[6] : nullptr, j == k - 1 ? e->ev[7] : nullptr, j < kp ? 2 : 0))
+      if (psi_backward(sub.P, bconst(sub, j), e->bpart.get<double>() + sub.boff, out_of(j), nsm, ctx->stream, &e->gb,
+                       (j == 0 && !phased) ? e->ev[6] : nullptr, j == k - 1 ? e->ev[7] : nullptr, j < kp ? 2 : 0,
+                       red_side ? e->side2 : nullptr, red_side ? e->ev_red[0] : nullptr))
         throw CudaError(std::string("psi backward launch: ") + cudaGetErrorString(cudaGetLastError()));
       if (stream_out) {  // d mu / d S of this sub-shard are final: copy them out while the next runs
         const int64_t q = e->cfg.q, n = e->cfg.n_local;
