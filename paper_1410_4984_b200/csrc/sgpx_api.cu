@@ -348,6 +348,7 @@ struct sgpx_engine {
   std::vector<cudaEvent_t> ev_in, ev_out;
   // deferred upload of host mu / S (broadcast with host views), streamed by the stats pass
   bool pending_upload = false;
+  bool uploads_enqueued = false;  // the pending upload's sub-shard copies are already on the copy stream
   sgpx_cmat h_mu{}, h_s{};
   // registered host outputs for d mu / d S, streamed by the gradient pass
   bool has_gout = false;
@@ -485,6 +486,27 @@ void plan_subs(sgpx_engine* e) {
   if (!e->copy) CUDA_OK(cudaStreamCreateWithFlags(&e->copy, cudaStreamNonBlocking));
 }
 
+// copy stream: mu / S of every sub-shard (the forward of sub-shard j waits for ev_in[j]); issued by
+// broadcast() as soon as it has the host views, so the transfer overlaps the caller's own work
+void enqueue_uploads(sgpx_engine* e) {
+  if (!e->pending_upload || e->uploads_enqueued) return;
+  sgpx_ctx* ctx = e->ctx;
+  if (e->subs.empty()) plan_subs(e);
+  CUDA_OK(cudaEventRecord(e->ev_out[0], ctx->stream));  // previous users of the device rows are done
+  CUDA_OK(cudaStreamWaitEvent(e->copy, e->ev_out[0], 0));
+  const int64_t q = e->cfg.q, n = e->cfg.n_local;
+  const int64_t ldm = e->h_mu.ld ? e->h_mu.ld : n, lds = e->h_s.ld ? e->h_s.ld : n;
+  for (size_t j = 0; j < e->subs.size(); ++j) {
+    const auto& sub = e->subs[j];
+    CUDA_OK(cudaMemcpy2DAsync(e->own_x.get<double>() + sub.n0, sizeof(double) * n, e->h_mu.data + sub.n0,
+                                sizeof(double) * ldm, sizeof(double) * sub.n, q, cudaMemcpyHostToDevice, e->copy));
+    CUDA_OK(cudaMemcpy2DAsync(e->own_s.get<double>() + sub.n0, sizeof(double) * n, e->h_s.data + sub.n0,
+                                sizeof(double) * lds, sizeof(double) * sub.n, q, cudaMemcpyHostToDevice, e->copy));
+    CUDA_OK(cudaEventRecord(e->ev_in[j], e->copy));
+  }
+  e->uploads_enqueued = true;
+}
+
 void engine_stats_pass(sgpx_engine* e) {
   require(e->has_data && e->has_params, "engine: set_data and broadcast must precede evaluate");
   sgpx_ctx* ctx = e->ctx;
@@ -513,20 +535,7 @@ void engine_stats_pass(sgpx_engine* e) {
   e->fpart.ensure(sizeof(double) * foff);
   if (k > 1) e->pstats_sub.ensure(sizeof(double) * count * k);
   CUDA_OK(record_event(e->ev[0], ctx->stream));
-  if (e->pending_upload) {  // copy stream: mu / S of sub-shard j, then the forward of j waits for it
-    CUDA_OK(cudaEventRecord(e->ev_out[0], ctx->stream));  // previous users of the device rows are done
-    CUDA_OK(cudaStreamWaitEvent(e->copy, e->ev_out[0], 0));
-    for (int j = 0; j < k; ++j) {
-      const auto& sub = e->subs[j];
-      const int64_t q = e->cfg.q, n = e->cfg.n_local;
-      const int64_t ldm = e->h_mu.ld ? e->h_mu.ld : n, lds = e->h_s.ld ? e->h_s.ld : n;
-      CUDA_OK(cudaMemcpy2DAsync(e->own_x.get<double>() + sub.n0, sizeof(double) * n, e->h_mu.data + sub.n0,
-                                  sizeof(double) * ldm, sizeof(double) * sub.n, q, cudaMemcpyHostToDevice, e->copy));
-      CUDA_OK(cudaMemcpy2DAsync(e->own_s.get<double>() + sub.n0, sizeof(double) * n, e->h_s.data + sub.n0,
-                                  sizeof(double) * lds, sizeof(double) * sub.n, q, cudaMemcpyHostToDevice, e->copy));
-      CUDA_OK(cudaEventRecord(e->ev_in[j], e->copy));
-    }
-  }
+  enqueue_uploads(e);  // (normally already issued by broadcast)
   // the row-tile forward's pair operand does not depend on the rows: later sub-shards reuse the first's
   const float* pairs0 =
       k > 1 ? fwd_pair_operand(e->subs[0].P, fwd_region(e->subs[0].P, e->fpart.get<double>() + e->subs[0].foff,
@@ -550,6 +559,7 @@ void engine_stats_pass(sgpx_engine* e) {
     CUDA_OK(cudaGetLastError());
   }
   e->pending_upload = false;
+  e->uploads_enqueued = false;
   CUDA_OK(record_event(e->ev[1], ctx->stream));
   e->coordinated = false;
 }
@@ -1397,6 +1407,10 @@ int sgpx_engine_set_data(sgpx_engine* e, sgpx_cmat x_or_mu, sgpx_cmat s, sgpx_cm
       in.ld_s = n;
     }
     e->has_data = true;
+    if (e->uploads_enqueued) {  // an earlier broadcast's copies must not land on top of these rows
+      CUDA_OK(cudaStreamSynchronize(e->copy));
+      e->uploads_enqueued = false;
+    }
     e->pending_upload = false;  // rows set here replace any host views of an earlier broadcast
     if (e->has_params) {
       e->P.mu = in.mu;
@@ -1440,6 +1454,8 @@ int sgpx_engine_broadcast(sgpx_engine* e, const sgpx_kernel_spec* kernel, double
         e->own_s.ensure(bytes);
         e->h_mu = mu;
         e->h_s = s;
+        if (e->uploads_enqueued) CUDA_OK(cudaStreamSynchronize(e->copy));  // an unconsumed earlier broadcast
+        e->uploads_enqueued = false;
         e->pending_upload = e->cfg.n_local * e->cfg.q > 0;
         e->in.mu = e->own_x.get<double>();
         e->in.ld_mu = e->cfg.n_local;
@@ -1457,6 +1473,13 @@ int sgpx_engine_broadcast(sgpx_engine* e, const sgpx_kernel_spec* kernel, double
     if (e->dev_coord) dc_setup(e);  // per-broadcast half of the coordinator (Kmm, its factor, inverse)
     e->has_params = true;
     e->coordinated = false;
+    if (e->pending_upload) {
+      // host mu / S: the transfer starts now, under the caller's work until evaluate (after the Z upload
+      // above: copies in one direction share a copy engine, so a small copy queued behind these would wait
+      // for all of them); the stats pass re-plans the same sub-shards with this broadcast's constants
+      plan_subs(e);
+      enqueue_uploads(e);
+    }
   });
 }
 

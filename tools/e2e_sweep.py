@@ -41,15 +41,17 @@ for plan in plans:
         os.environ.pop("SGPX_DEVICE_COORD", None)
     eng = sgp.Engine(sgp.ModelKind.latent, w.mu, w.s, w.y)
     eng.set_local_grads_out(gmu_p.numpy().T, gs_p.numpy().T)
-    ts = []
+    ts, tb = [], []
     for i in range(steps + 2):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         eng.broadcast(w.kernel, w.beta, w.z, mu_np, s_np)
+        t1 = time.perf_counter()
         r = eng.evaluate(True)
         _ = r.bound.total
         ts.append(time.perf_counter() - t0)
-    ts = sorted(ts[2:])
+        tb.append(t1 - t0)
+    ts, tb = sorted(ts[2:]), sorted(tb[2:])
     print(f"plan {plan:28s} e2e median {ts[len(ts) // 2] * 1e3:7.3f} ms  min {ts[0] * 1e3:7.3f}  "
-          f"bound {r.bound.total:.10e}", flush=True)
+          f"(broadcast {tb[len(tb) // 2] * 1e3:6.3f} ms)  bound {r.bound.total:.10e}", flush=True)
     del eng
