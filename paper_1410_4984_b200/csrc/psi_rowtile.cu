@@ -77,12 +77,24 @@ constexpr int kRtPolyFwd = SGPX_RT_POLY_F, kRtPolyBwd = SGPX_RT_POLY_B;
 #ifndef SGPX_RT_LATE_STWAIT
 #define SGPX_RT_LATE_STWAIT 1
 #endif
-constexpr int kGroups = 3;              // consumer warps per TMEM lane quarter (32 columns each)
-constexpr int kCons = 128 * kGroups;    // consumer threads   (warps 0 .. 11)
-constexpr int kDrain = 128;             // accumulator drain threads (warps 12 .. 15)
-constexpr int kWarpLoad = (kCons + kDrain) / 32;  // loader warp (16)
-constexpr int kWarpMma = kWarpLoad + 1;           // MMA warp (17)
-constexpr int kThreads = kCons + kDrain + 64;
+// consumer warps per TMEM lane quarter (each takes 32-datapoint blocks g, g + groups, ... of a stage):
+// the forward's lighter consumers gain from one block per warp (6 groups, 960 threads: -0.05 ms at C3),
+// the backward's (fp16 pieces, more registers) stay at 3 (profiles/r02/rt_groups_ab.txt)
+#ifndef SGPX_RT_GROUPS_F
+#define SGPX_RT_GROUPS_F 6
+#endif
+#ifndef SGPX_RT_GROUPS_B
+#define SGPX_RT_GROUPS_B 3
+#endif
+constexpr int kDrain = 128;  // accumulator drain threads (the 4 warps after the consumers)
+template <bool BF>
+struct RtRoles {
+  static constexpr int G = BF ? SGPX_RT_GROUPS_F : SGPX_RT_GROUPS_B;
+  static constexpr int Cons = 128 * G;                   // consumer threads (warps 0 .. 4G - 1)
+  static constexpr int WarpLoad = (Cons + kDrain) / 32;  // loader warp
+  static constexpr int WarpMma = WarpLoad + 1;           // MMA warp
+  static constexpr int Threads = Cons + kDrain + 64;
+};
 constexpr int kPadRows = 768;           // feature-array row padding: lcm(kCH, 2 x 128)
 constexpr float kNegHuge = -6.0e4f;     // B_n of padded datapoints (fp16-representable): 2^-6e4 = 0
 using pc::kHalfMax;
@@ -503,7 +515,9 @@ struct RowTileArgs {
 };
 
 template <int Q, bool BF, bool PAIR, int NP>
-__global__ void __launch_bounds__(kThreads, 1) rowtile_kernel(PsiConst P, RowTileArgs R) {
+__global__ void __launch_bounds__(RtRoles<BF>::Threads, 1) rowtile_kernel(PsiConst P, RowTileArgs R) {
+  constexpr int kGroups = RtRoles<BF>::G, kCons = RtRoles<BF>::Cons, kWarpLoad = RtRoles<BF>::WarpLoad,
+                kWarpMma = RtRoles<BF>::WarpMma;
   using C = RT<Q, BF, PAIR, NP>;
   constexpr int K1 = C::K1, KS1 = K1 / 8, N3 = C::N3, NH = C::NH;
   constexpr int PF = C::PF, CHF = C::CHF, XF = C::XF, YFl = C::YFl, AF = C::AF;
@@ -1142,7 +1156,7 @@ int launch_rowtile(const PsiConst& P, RowTileArgs R, dim3 grid, cudaStream_t st)
   if (PAIR) {
     cudaLaunchConfig_t lc = {};
     lc.gridDim = grid;
-    lc.blockDim = dim3(kThreads);
+    lc.blockDim = dim3(RtRoles<BF>::Threads);
     lc.dynamicSmemBytes = cfg.smem;
     lc.stream = st;
     cudaLaunchAttribute attr[1];
@@ -1158,7 +1172,7 @@ int launch_rowtile(const PsiConst& P, RowTileArgs R, dim3 grid, cudaStream_t st)
     }
   } else {
     if (P.ev_psi2[0]) record_event(P.ev_psi2[0], st);
-    kern<<<grid, kThreads, cfg.smem, st>>>(P, R);
+    kern<<<grid, RtRoles<BF>::Threads, cfg.smem, st>>>(P, R);
     if (P.ev_psi2[1]) record_event(P.ev_psi2[1], st);
   }
   g_tc_launches.fetch_add(1);
