@@ -763,7 +763,8 @@ void engine_grad_pass(sgpx_engine* e) {
     // with streamed-out d mu / d S only the first sub-shards run their psi1 kernels ahead (enough to
     // cover the side stream's coordinator); the rest keep psi1 -> psi2 -> copy-out per sub-shard so the
     // device-to-host copies start early
-    const int kp = phased ? (stream_out ? std::max(1, k / 3) : k) : 0;
+    int kp = phased ? (stream_out ? std::max(1, k / 3) : k) : 0;
+    if (const char* v = getenv("SGPX_KP"); v && phased) kp = std::min(k, std::max(1, atoi(v)));  // A/B
     if (phased) {
       for (int j = 0; j < kp; ++j) {
         auto& sub = e->subs[j];
