@@ -241,10 +241,10 @@ int sgpx_engine_destroy(sgpx_engine* eng);
 int sgpx_engine_set_data(sgpx_engine* eng, sgpx_cmat x_or_mu, sgpx_cmat s, sgpx_cmat y, int on_device);
 /* Engine::broadcast: global params (kernel, beta, Z: host memory, M x Q); mu/s (latent) optional
  * local slice, n_local x Q (data == NULL keeps the current; on_device != 0: device pointers, adopted).
- * Host mu / s are NOT copied here: the next stats pass streams them to the device in sub-shards,
- * overlapped with its kernels, so the caller keeps both host buffers alive and unchanged until that
- * pass (sgpx_engine_evaluate / sgpx_engine_stats_pass) has returned.  A later set_data cancels the
- * pending upload. */
+ * Host mu / s are copied asynchronously: broadcast starts their sub-shard uploads on the engine's copy
+ * stream and the next stats pass waits for each before its kernels, so the caller keeps both host
+ * buffers alive and unchanged until that pass (sgpx_engine_evaluate / sgpx_engine_stats_pass) has
+ * returned.  A later set_data waits for and supersedes the pending upload. */
 int sgpx_engine_broadcast(sgpx_engine* eng, const sgpx_kernel_spec* kernel, double beta, sgpx_cmat z, sgpx_cmat mu,
                           sgpx_cmat s, int on_device);
 /* Single-rank Engine::evaluate(with_grads): the whole pipeline, no collective. */
