@@ -717,7 +717,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // TMEM) -> S2 -> epilogue (d mu, d S, d l, d var) -> S3 -> (TMA mu / S c+1) -> R phase -> S4.
 constexpr int kB2Threads = 512;
 struct Bwd2Smem {  // byte offsets
-  int ya, pb, zs, hs, rawy, rawms, bar, total;
+  int ya, pb, zs, hs, cl, rawy, rawms, bar, total;
   int dk, mn, mz, gst, hst;
 };
 __host__ __device__ inline Bwd2Smem bwd2_smem(int q, int d, int m) {
@@ -735,7 +735,8 @@ __host__ __device__ inline Bwd2Smem bwd2_smem(int q, int d, int m) {
   L.pb = (big + 127) / 128 * 128;                // dPsi pieces [2][mn x dk]
   L.zs = L.pb + 2 * L.mn * L.dk * 4;             // z [q][mz], z^2 [q][mz]
   L.hs = L.zs + 2 * q * L.mz * 4;                // [128][hst]
-  L.rawy = (L.hs + 128 * L.hst * 4 + 127) / 128 * 128;  // TMA box: Y [d][128] doubles
+  L.cl = L.hs + 128 * L.hst * 4;                 // [4][128]: partial sums of 1/2 log2(d1 l^2) per datapoint
+  L.rawy = (L.cl + 4 * 128 * 4 + 127) / 128 * 128;  // TMA box: Y [d][128] doubles
   L.rawms = L.rawy + d * 128 * 8;                // TMA boxes: mu [q][128], S [q][128] doubles
   L.bar = L.rawms + 2 * q * 128 * 8;
   L.total = L.bar + 64;
@@ -770,6 +771,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
   float* pb = reinterpret_cast<float*>(smem + L.pb);
   float* zs = reinterpret_cast<float*>(smem + L.zs);
   float* hs = reinterpret_cast<float*>(smem + L.hs);
+  float* clp = reinterpret_cast<float*>(smem + L.cl);
   double* rawy = reinterpret_cast<double*>(smem + L.rawy);
   double* rawm = reinterpret_cast<double*>(smem + L.rawms);
   double* raws = rawm + Q * 128;
@@ -850,7 +852,10 @@ __global__ void __launch_bounds__(kB2Threads, 1)
       ya[o] = hi;
       ya[128 * dk + o] = f - hi;
     }
-    // per-datapoint rows (rows past N arrive zero-filled: finite constants, Y = 0 so G = 0)
+    // per-datapoint rows (rows past N arrive zero-filled: finite constants, Y = 0 so G = 0); thread tid
+    // always takes datapoint tid & 127 (latent dims tid >> 7, + 4, ...) and leaves its part of
+    // b1 - log2 var = sum_q 1/2 log2(d1 l^2) in clp[tid >> 7]
+    float clsum = 0.f;
     for (int i = tid; i < 128 * Q4; i += NT) {
       const int nl = i & 127, q = i >> 7;
       float mu = 0.f, d1 = 0.f;
@@ -858,6 +863,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
         const double sd = P.expected ? raws[q * 128 + nl] : 0.0;
         mu = float(rawm[q * 128 + nl] - P.center[q]);
         d1 = 1.f / (float(sd) + P.l2[q]);
+        clsum += 0.5f * log2f(d1 * P.l2[q]);
       }
       const float bq = sqrtf(0.5f * kLog2e * d1);
       float* h = hs + nl * hst;
@@ -866,6 +872,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
       h[2 * Q4 + q] = bq * mu;
       h[3 * Q4 + q] = bq;
     }
+    clp[tid] = clsum;  // [tid >> 7][tid & 127]  (NT = 512 = 4 x 128)
     tc::fence_async_smem();
     tc::fence_before();
     __syncthreads();  // S1: Y pieces and rows ready; raw Y consumed
@@ -884,20 +891,15 @@ __global__ void __launch_bounds__(kB2Threads, 1)
     }
     // G phase constants while the MMAs run
     float av[Q4], bv[Q4];
-    float b1 = P.log2_var;
+    const float b1 = P.log2_var + ((clp[cn] + clp[128 + cn]) + (clp[256 + cn] + clp[384 + cn]));
     {
       const float* h = hs + cn * hst;
 #pragma unroll
       for (int k4 = 0; k4 < Q4; k4 += 4) {
         const float4 x = *reinterpret_cast<const float4*>(h + 2 * Q4 + k4);
         const float4 y = *reinterpret_cast<const float4*>(h + 3 * Q4 + k4);
-        const float4 w = *reinterpret_cast<const float4*>(h + Q4 + k4);
         av[k4] = x.x, av[k4 + 1] = x.y, av[k4 + 2] = x.z, av[k4 + 3] = x.w;
         bv[k4] = y.x, bv[k4 + 1] = y.y, bv[k4 + 2] = y.z, bv[k4 + 3] = y.w;
-        const float wv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (k4 + u < Q && k4 + u < pq) b1 += 0.5f * log2f(wv[u] * P.l2[k4 + u]);
       }
     }
     tc::mbar_wait(&bar[2], ph);
