@@ -87,9 +87,9 @@ constexpr int kRtPolyFwd = SGPX_RT_POLY_F, kRtPolyBwd = SGPX_RT_POLY_B;
 #define SGPX_RT_GROUPS_B 3
 #endif
 constexpr int kDrain = 128;  // accumulator drain threads (the 4 warps after the consumers)
-template <bool BF>
-struct RtRoles {
-  static constexpr int G = BF ? SGPX_RT_GROUPS_F : SGPX_RT_GROUPS_B;
+template <int Q, bool BF>
+struct RtRoles {  // (at Q > 10 the forward's 960-thread register budget spills: 3 groups there too)
+  static constexpr int G = (BF && Q <= 10) ? SGPX_RT_GROUPS_F : SGPX_RT_GROUPS_B;
   static constexpr int Cons = 128 * G;                   // consumer threads (warps 0 .. 4G - 1)
   static constexpr int WarpLoad = (Cons + kDrain) / 32;  // loader warp
   static constexpr int WarpMma = WarpLoad + 1;           // MMA warp
@@ -515,9 +515,9 @@ struct RowTileArgs {
 };
 
 template <int Q, bool BF, bool PAIR, int NP>
-__global__ void __launch_bounds__(RtRoles<BF>::Threads, 1) rowtile_kernel(PsiConst P, RowTileArgs R) {
-  constexpr int kGroups = RtRoles<BF>::G, kCons = RtRoles<BF>::Cons, kWarpLoad = RtRoles<BF>::WarpLoad,
-                kWarpMma = RtRoles<BF>::WarpMma;
+__global__ void __launch_bounds__(RtRoles<Q, BF>::Threads, 1) rowtile_kernel(PsiConst P, RowTileArgs R) {
+  constexpr int kGroups = RtRoles<Q, BF>::G, kCons = RtRoles<Q, BF>::Cons, kWarpLoad = RtRoles<Q, BF>::WarpLoad,
+                kWarpMma = RtRoles<Q, BF>::WarpMma;
   using C = RT<Q, BF, PAIR, NP>;
   constexpr int K1 = C::K1, KS1 = K1 / 8, N3 = C::N3, NH = C::NH;
   constexpr int PF = C::PF, CHF = C::CHF, XF = C::XF, YFl = C::YFl, AF = C::AF;
@@ -1156,7 +1156,7 @@ int launch_rowtile(const PsiConst& P, RowTileArgs R, dim3 grid, cudaStream_t st)
   if (PAIR) {
     cudaLaunchConfig_t lc = {};
     lc.gridDim = grid;
-    lc.blockDim = dim3(RtRoles<BF>::Threads);
+    lc.blockDim = dim3(RtRoles<Q, BF>::Threads);
     lc.dynamicSmemBytes = cfg.smem;
     lc.stream = st;
     cudaLaunchAttribute attr[1];
@@ -1172,7 +1172,7 @@ int launch_rowtile(const PsiConst& P, RowTileArgs R, dim3 grid, cudaStream_t st)
     }
   } else {
     if (P.ev_psi2[0]) record_event(P.ev_psi2[0], st);
-    kern<<<grid, RtRoles<BF>::Threads, cfg.smem, st>>>(P, R);
+    kern<<<grid, RtRoles<Q, BF>::Threads, cfg.smem, st>>>(P, R);
     if (P.ev_psi2[1]) record_event(P.ev_psi2[1], st);
   }
   g_tc_launches.fetch_add(1);
