@@ -209,6 +209,11 @@ double* fwd_pair_sums(const PsiConst& P, double* region, int num_sms, int64_t* c
   return rt_fwd_pair_sums(P, region, num_sms, count);
 }
 
+double* bwd_rt_region(const PsiConst& P, double* part, int num_sms) {
+  const int rows = (P.n > 0 ? psi1_bwd_rows(P, num_sms) : 0) + 1;  // as psi_backward lays it out
+  return part + int64_t(rows) * bwd_part_count(P.m, P.q);
+}
+
 const float* fwd_pair_operand(const PsiConst& P, const double* region, int num_sms) {
   if (is_syrk(P) || is_direct(P)) return nullptr;
   return rt_fwd_pair_operand(P, region, num_sms);

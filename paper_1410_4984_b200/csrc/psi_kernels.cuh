@@ -167,6 +167,10 @@ int rt_forward(const PsiConst& P, double* base, double* packed, int num_sms, voi
 int rt_backward(const PsiConst& P, const BwdConst& B, double* bbase, double* prow, int num_sms, void* stream);
 double* rt_fwd_pair_sums(const PsiConst& P, double* region, int num_sms, int64_t* count);
 const float* rt_fwd_pair_operand(const PsiConst& P, const double* region, int num_sms);
+int rt_bwd_prepare(const PsiConst& P, const float* u, double* bbase, int num_sms, void* stream, const float** pre,
+                   const float** ys);
+// the row-tile backward's region inside psi_backward's partial buffer `part` (after the psi1 rows)
+double* bwd_rt_region(const PsiConst& P, double* part, int num_sms);
 // Direct-difference kernels (psi_direct.cu): the complete forward (validation, yy, KL, Phi, Psi) and
 // backward (d mu, d S, d Z, d l, d var) with fp64 exponents.
 bool direct_supported(const PsiConst& P);

@@ -1291,6 +1291,25 @@ int rt_backward_q(const PsiConst& P, const BwdConst& B, double* bbase, double* p
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
+// The backward's N-independent pair operand (U-weighted pair features) and Y scales of `bbase`'s
+// region, launched on `stream` (the engine runs them on the coordinator's side stream, right after U).
+template <int Q>
+int rt_bwd_prepare_q(const PsiConst& P, const float* u, double* bbase, int num_sms, cudaStream_t st, const float** pre_out,
+                     const float** ys_out) {
+  const FwdLayout F = fwd_layout(P, num_sms);
+  const BwdLayout L = bwd_layout(P, num_sms);
+  float* pre = floats_at(bbase, L.off_floats);
+  float* ys = reinterpret_cast<float*>(bbase + L.off_ys);
+  const int blocks_p = int(std::min<int64_t>((F.p_pad + 255) / 256, int64_t(num_sms) * 8));
+  rt_yscale_kernel<Q><<<1, 256, 0, st>>>(P, u, ys);
+  if (rt_pieces(P) == 3) rt_pair_pre_kernel<Q, false, 3><<<blocks_p, 256, 0, st>>>(P, u, F.p_pad, ys, pre);
+  else rt_pair_pre_kernel<Q, false, 2><<<blocks_p, 256, 0, st>>>(P, u, F.p_pad, ys, pre);
+  g_tc_launches.fetch_add(2);
+  *pre_out = pre;
+  *ys_out = ys;
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
 #define SGPX_RT_DISPATCH(fn, ...)              \
   switch (instantiated_q(P.q)) {              \
     case 1: return fn<1>(__VA_ARGS__);         \
@@ -1328,6 +1347,10 @@ const float* rt_fwd_pair_operand(const PsiConst& P, const double* region, int nu
 
 int rt_forward(const PsiConst& P, double* base, double* packed, int num_sms, void* stream) {
   SGPX_RT_DISPATCH(rt_forward_q, P, base, packed, num_sms, static_cast<cudaStream_t>(stream))
+}
+int rt_bwd_prepare(const PsiConst& P, const float* u, double* bbase, int num_sms, void* stream, const float** pre,
+                   const float** ys) {
+  SGPX_RT_DISPATCH(rt_bwd_prepare_q, P, u, bbase, num_sms, static_cast<cudaStream_t>(stream), pre, ys)
 }
 int rt_backward(const PsiConst& P, const BwdConst& B, double* bbase, double* prow, int num_sms, void* stream) {
   SGPX_RT_DISPATCH(rt_backward_q, P, B, bbase, prow, num_sms, static_cast<cudaStream_t>(stream))

@@ -725,6 +725,15 @@ void engine_grad_pass(sgpx_engine* e) {
     }
     const bool stream_out = e->has_gout && e->latent;
     const float *rt_pre0 = nullptr, *rt_ys0 = nullptr;
+    bool prepared = false;
+    if (phased) {  // the pair operand of the psi2 backward right after U, on the coordinator's side stream
+      const auto& s0 = e->subs[0];
+      if (rt_bwd_prepare(s0.P, e->u.get<float>(), bwd_rt_region(s0.P, e->bpart.get<double>() + s0.boff, nsm), nsm,
+                         e->side, &rt_pre0, &rt_ys0))
+        throw CudaError("psi backward prepare launch");
+      CUDA_OK(cudaEventRecord(e->ev_split[1], e->side));  // the join now also covers them
+      prepared = true;
+    }
     auto bconst = [&](const sgpx_engine::Sub& sub, int j) {
       BwdConst B{};
       B.u = e->u.get<float>();
@@ -740,7 +749,10 @@ void engine_grad_pass(sgpx_engine* e) {
       B.fwd_rt = fwd_region(sub.P, e->fpart.get<double>() + sub.foff, ctx->num_sms);
       B.skip_pair_terms = (fold && j > 0) ? 1 : 0;
       // the U-weighted pair operand and Y scales of the psi2 backward do not depend on the rows
-      if (j == 0) {
+      if (prepared) {
+        B.rt_pre_shared = rt_pre0;
+        B.rt_ys_shared = rt_ys0;
+      } else if (j == 0) {
         B.rt_pre_out = &rt_pre0;
         B.rt_ys_out = &rt_ys0;
       } else {
