@@ -370,7 +370,9 @@ struct sgpx_engine {
   cudaEvent_t ev_split[4] = {};
   cudaEvent_t ev_pre[2] = {};  // the per-broadcast prefactor on the side stream (dc_setup)
   cudaEvent_t ev_red[2] = {};  // sub-shard backward reductions on side2: fork (per sub-shard), join
-  bool pre_pending = false;
+  cudaEvent_t ev_copy_done = nullptr;  // the streamed d mu / d S read-backs, joined into the stream
+  bool pre_needed = false;   // a broadcast's prefactor not launched yet
+  bool pre_pending = false;  // launched, not joined yet
   // one evaluation (device-resident shard, device coordinator) as a CUDA graph, replayed while its
   // launch arguments are unchanged (graph_key)
   bool use_graph = true;
@@ -391,6 +393,7 @@ struct sgpx_engine {
       if (e) cudaEventDestroy(e);
     for (auto& e : ev_red)
       if (e) cudaEventDestroy(e);
+    if (ev_copy_done) cudaEventDestroy(ev_copy_done);
     if (side) cudaStreamDestroy(side);
     if (side2) cudaStreamDestroy(side2);
     if (graph) cudaGraphExecDestroy(graph);
@@ -507,6 +510,8 @@ void enqueue_uploads(sgpx_engine* e) {
   e->uploads_enqueued = true;
 }
 
+void dc_launch_prefactor(sgpx_engine* e);
+
 void engine_stats_pass(sgpx_engine* e) {
   require(e->has_data && e->has_params, "engine: set_data and broadcast must precede evaluate");
   sgpx_ctx* ctx = e->ctx;
@@ -523,6 +528,7 @@ void engine_stats_pass(sgpx_engine* e) {
     return;
   }
   plan_subs(e);
+  if (e->dev_coord) dc_launch_prefactor(e);  // side stream, under the forward
   const int k = int(e->subs.size());
   // partial-buffer layout: one region per sub-shard
   int64_t foff = 0;
@@ -581,9 +587,15 @@ void dc_setup(sgpx_engine* e) {
   dc_bind(dc, e->dcw.get<double>());
   e->pstats.ensure(sizeof(double) * sgpx_packed_stats_count(e->cfg.m, e->cfg.d));
   dc.packed = e->pstats.get<double>();
-  // the per-broadcast half (Kmm, its factor and inverse) runs on the side stream, overlapping the
-  // forward kernels; the evaluation joins it right before the coordinator (dc_join_prefactor).  The
-  // lengthscales travel as a kernel argument (no staging buffer to keep alive).
+  // the per-broadcast half (Kmm, its factor and inverse) is launched by the next statistics pass on the
+  // side stream (dc_launch_prefactor), overlapping the forward kernels (and inside the evaluation's
+  // graph when it is replayed), and joined right before the coordinator (dc_join_prefactor)
+  e->pre_needed = true;
+  e->dc_ready = true;
+}
+
+void dc_launch_prefactor(sgpx_engine* e) {
+  if (!e->pre_needed) return;
   cudaStream_t st = e->ctx->stream;
   if (!e->side) CUDA_OK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
   if (!e->ev_pre[0]) {
@@ -592,11 +604,12 @@ void dc_setup(sgpx_engine* e) {
   }
   CUDA_OK(cudaEventRecord(e->ev_pre[0], st));  // after every earlier user of the workspace
   CUDA_OK(cudaStreamWaitEvent(e->side, e->ev_pre[0], 0));
-  if (dc_upload_ls(dc, e->kernel_ls.data(), e->side)) throw CudaError("coordinator launch");
-  if (dc_prefactor(dc, e->side)) throw CudaError("coordinator launch");
+  // the lengthscales travel as a kernel argument (no staging buffer to keep alive)
+  if (dc_upload_ls(e->dc, e->kernel_ls.data(), e->side)) throw CudaError("coordinator launch");
+  if (dc_prefactor(e->dc, e->side)) throw CudaError("coordinator launch");
   CUDA_OK(cudaEventRecord(e->ev_pre[1], e->side));
+  e->pre_needed = false;
   e->pre_pending = true;
-  e->dc_ready = true;
 }
 
 // the stream waits for the per-broadcast prefactor (before the first coordinator kernel)
@@ -614,6 +627,7 @@ void engine_coordinate(sgpx_engine* e, bool with_grads) {
     e->dpsi.ensure(sizeof(float) * std::max(1, e->P.d) * e->P.mv);
     e->u64.ensure(sizeof(double) * e->P.mv * e->P.mv);
     e->dpsi64.ensure(sizeof(double) * std::max(1, e->P.d) * e->P.mv);
+    dc_launch_prefactor(e);  // (a no-op unless the statistics pass had no rows to launch it under)
     dc_join_prefactor(e);
     CUDA_OK(record_event(e->ev_c[0], ctx->stream));
     e->split = e->coord_split && e->cfg.m <= 112;
@@ -804,6 +818,11 @@ void engine_grad_pass(sgpx_engine* e) {
         CUDA_OK(cudaMemcpy2DAsync(e->g_s.data + sub.n0, sizeof(double) * lds, e->ds.get<double>() + sub.n0,
                                     sizeof(double) * n, sizeof(double) * sub.n, q, cudaMemcpyDeviceToHost, e->copy));
       }
+    }
+    if (stream_out) {  // the read-backs join the stream (a captured graph needs every fork joined)
+      if (!e->ev_copy_done) CUDA_OK(cudaEventCreateWithFlags(&e->ev_copy_done, cudaEventDisableTiming));
+      CUDA_OK(cudaEventRecord(e->ev_copy_done, e->copy));
+      CUDA_OK(cudaStreamWaitEvent(ctx->stream, e->ev_copy_done, 0));
     }
     if (k > 1) {
       if (red_side) {
@@ -1486,7 +1505,7 @@ int sgpx_engine_broadcast(sgpx_engine* e, const sgpx_kernel_spec* kernel, double
     if (e->dev_coord) dc_setup(e);  // per-broadcast half of the coordinator (Kmm, its factor, inverse)
     e->has_params = true;
     e->coordinated = false;
-    if (e->pending_upload) {
+    if (e->pending_upload && !(e->use_graph && e->dev_coord && e->ctx->stream != nullptr)) {
       // host mu / S: the transfer starts now, under the caller's work until evaluate (after the Z upload
       // above: copies in one direction share a copy engine, so a small copy queued behind these would wait
       // for all of them); the stats pass re-plans the same sub-shards with this broadcast's constants
@@ -1540,17 +1559,28 @@ int sgpx_engine_evaluate(sgpx_engine* e, int with_grads, sgpx_eval_result* out) 
     const auto t0 = std::chrono::steady_clock::now();
     // graph replay: device-resident rows (no host streaming) and the device coordinator
     // (the legacy default stream cannot be captured)
-    const bool graphable = e->use_graph && e->dev_coord && !e->pending_upload && !(e->has_gout && e->latent) &&
-                           e->in.n > 0 && e->has_data && e->has_params && e->ctx->stream != nullptr;
+    // (the host-buffer path too: the sub-shard uploads and read-backs are captured as copy nodes, the
+    // host views and output buffers are part of the key)
+    const bool graphable = e->use_graph && e->dev_coord && !e->uploads_enqueued && e->in.n > 0 && e->has_data &&
+                           e->has_params && e->ctx->stream != nullptr;
     if (graphable) {
-      std::vector<unsigned char> key(sizeof(PsiConst) + sizeof(DcArgs) + 2 * sizeof(int));
+      const bool host_io = e->pending_upload || (e->has_gout && e->latent);
+      std::vector<unsigned char> key(sizeof(PsiConst) + sizeof(DcArgs) + 4 * sizeof(int) + 4 * sizeof(sgpx_cmat));
       unsigned char* p = key.data();
       std::memcpy(p, &e->P, sizeof(PsiConst));
-      std::memcpy(p + sizeof(PsiConst), &e->dc, sizeof(DcArgs));
-      const int flags[2] = {with_grads ? 1 : 0, e->ctx->device};
-      std::memcpy(p + sizeof(PsiConst) + sizeof(DcArgs), flags, sizeof(flags));
+      p += sizeof(PsiConst);
+      std::memcpy(p, &e->dc, sizeof(DcArgs));
+      p += sizeof(DcArgs);
+      const int flags[4] = {with_grads ? 1 : 0, e->ctx->device,
+                            (e->pending_upload ? 1 : 0) | (e->pre_needed ? 2 : 0) | (e->pre_pending ? 4 : 0),
+                            (e->has_gout && e->latent) ? 1 : 0};
+      std::memcpy(p, flags, sizeof(flags));
+      p += sizeof(flags);
+      const sgpx_cmat views[4] = {e->pending_upload ? e->h_mu : sgpx_cmat{}, e->pending_upload ? e->h_s : sgpx_cmat{},
+                                  host_io ? sgpx_cmat{e->g_mu.data, e->g_mu.rows, e->g_mu.cols, e->g_mu.ld} : sgpx_cmat{},
+                                  host_io ? sgpx_cmat{e->g_s.data, e->g_s.rows, e->g_s.cols, e->g_s.ld} : sgpx_cmat{}};
+      std::memcpy(p, views, sizeof(views));
       cudaStream_t st = e->ctx->stream;
-      dc_join_prefactor(e);  // outside the capture (the prefactor's event is not part of the graph)
       if (!e->graph || key != e->graph_key) {
         if (e->graph) {
           cudaGraphExecDestroy(e->graph);
@@ -1580,6 +1610,8 @@ int sgpx_engine_evaluate(sgpx_engine* e, int with_grads, sgpx_eval_result* out) 
       } else {
         e->with_grads = with_grads != 0;
         e->coordinated = true;
+        e->pending_upload = false;  // (what the captured passes do on the host)
+        e->pre_needed = e->pre_pending = false;
       }
       CUDA_OK(cudaGraphLaunch(e->graph, st));
       launches_add(e->graph_launches);
@@ -1604,6 +1636,7 @@ int sgpx_engine_predict(sgpx_engine* e, sgpx_cmat x_star, int observation, sgpx_
     if (!e->dev_coord) {  // host-coordinated engine: rebuild the factors on the device from the last statistics
       CUDA_OK(cudaSetDevice(e->ctx->device));
       if (!e->dc_ready) dc_setup(e);
+      dc_launch_prefactor(e);
       dc_join_prefactor(e);
       e->u.ensure(sizeof(float) * e->P.mv * e->P.mv);
       e->dpsi.ensure(sizeof(float) * std::max(1, e->P.d) * e->P.mv);
