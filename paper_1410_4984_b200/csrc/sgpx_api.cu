@@ -443,7 +443,7 @@ std::vector<double> sub_weights(int64_t n, bool transfers) {
     for (double x : w) ok = ok && x > 0.0;
     if (ok) return w;
   }
-  if (n >= 1000000) return {1.0, 1.5, 2.0, 2.0, 1.5, 1.0};  // measured best at C3 (tools/e2e_timeline.py)
+  if (n >= 1000000) return {1.0, 1.5, 2.0, 2.0, 2.0, 1.5, 1.0};  // measured best at C3, graph-replayed (tools/e2e_sweep.py)
   if (n >= 500000) return {1.0, 1.0};
   return {1.0};
 }

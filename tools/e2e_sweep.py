@@ -39,7 +39,9 @@ for plan in plans:
         os.environ["SGPX_DEVICE_COORD"] = dc
     else:
         os.environ.pop("SGPX_DEVICE_COORD", None)
-    eng = sgp.Engine(sgp.ModelKind.latent, w.mu, w.s, w.y)
+    ctx = sgp.Context(0)  # an explicit stream, as bench.py (the graph-replayed path)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    eng = sgp.Engine(sgp.ModelKind.latent, w.mu, w.s, w.y, ctx=ctx)
     eng.set_local_grads_out(gmu_p.numpy().T, gs_p.numpy().T)
     ts, tb = [], []
     for i in range(steps + 2):
