@@ -60,7 +60,7 @@ events = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType
 t0 = min(e.time_range.start for e in events)
 rows = sorted((e.time_range.start - t0, e.time_range.end - t0, e.name) for e in events)
 for st, en, name in rows:
-    if en - st >= 20 or "Memcpy" in name:
+    if en - st >= float(os.environ.get("MIN_US", "20")) or "Memcpy" in name:
         print(f"{st / 1e3:8.3f} - {en / 1e3:8.3f} ms  {(en - st) / 1e3:7.3f}  {name[:80]}")
 print(f"span {max(r[1] for r in rows) / 1e3:.3f} ms over {len(rows)} device events")
 if os.environ.get("CPU_EVENTS"):
