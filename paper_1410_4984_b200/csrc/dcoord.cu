@@ -655,18 +655,25 @@ __global__ void __launch_bounds__(kG1Threads) bound_g_small_kernel(DcArgs A, flo
             if (bad) s_fail = 1;
           }
           __syncwarp();
-          // row r, columns k + 1 .. r: four at a time, every load before its stores (independent updates)
-          if (r > k && r < jb) {
-            int c = k + 1;
-            for (; c + 3 <= r; c += 4) {
-              const double l0 = Lp[c + k * m], l1 = Lp[c + 1 + k * m], l2 = Lp[c + 2 + k * m], l3 = Lp[c + 3 + k * m];
-              const double a0 = Lp[r + c * m], a1 = Lp[r + (c + 1) * m], a2 = Lp[r + (c + 2) * m], a3 = Lp[r + (c + 3) * m];
-              Lp[r + c * m] = fma(-lrk, l0, a0);
-              Lp[r + (c + 1) * m] = fma(-lrk, l1, a1);
-              Lp[r + (c + 2) * m] = fma(-lrk, l2, a2);
-              Lp[r + (c + 3) * m] = fma(-lrk, l3, a3);
+          // row r, columns k + 1 .. r: every candidate column's loads first (predicated, compile-time
+          // register indices in halves of 16), then the FMAs and stores (tools/microbench/diag_factor.cu)
+          const bool rowact = r > k && r < jb;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (16 * h + 15 <= k) continue;  // warp-uniform
+            double av[16], lv[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              const int c = 16 * h + u;
+              const bool act = rowact && c > k && c <= r;
+              av[u] = act ? Lp[r + c * m] : 0.0;
+              lv[u] = act ? Lp[c + k * m] : 0.0;
             }
-            for (; c <= r; ++c) Lp[r + c * m] = fma(-lrk, Lp[c + k * m], Lp[r + c * m]);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              const int c = 16 * h + u;
+              if (rowact && c > k && c <= r) Lp[r + c * m] = fma(-lrk, lv[u], av[u]);
+            }
           }
           __syncwarp();
         }
