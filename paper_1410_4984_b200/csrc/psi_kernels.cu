@@ -258,7 +258,8 @@ int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, 
 bool psi_backward_phased(const PsiConst& P) { return !is_syrk(P) && !is_direct(P); }
 
 int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
-                 LaunchGeom* geom, void* ev_begin, void* ev_end, int phase, void* reduce_stream, void* reduce_event) {
+                 LaunchGeom* geom, void* ev_begin, void* ev_end, int phase, void* reduce_stream, void* reduce_event,
+                 int psi1_grid_cap) {
   if (!B.fwd_rt) return 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   LaunchGeom g{};
@@ -284,7 +285,8 @@ int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* pac
     if (ev_begin) record_event(ev_begin, st);
     // psi1 first: it writes d_mu / d_s (psi1 + KL parts); the psi2 kernel accumulates into them
     if (r1 > 0) {
-      if (int rc = psi1_backward(P, B, part, pstride, r1, stream)) return rc;
+      const int g1 = psi1_grid_cap > 0 ? std::min(r1, psi1_grid_cap) : r1;
+      if (int rc = psi1_backward(P, B, part, pstride, g1, stream)) return rc;
     }
     if (phase == 1) return cudaGetLastError() == cudaSuccess ? 0 : 3;
   }

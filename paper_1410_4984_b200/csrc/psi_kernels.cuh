@@ -123,10 +123,12 @@ int psi_forward(const PsiConst& P, double* part, double* packed, int* err_flag, 
 // phase (row-tile path only): 0 the whole pass, 1 the psi1 kernel alone (it needs d Psi, not d Phi),
 // 2 the rest (psi2 kernels, reduction) -- so a caller can overlap the coordinator's d Phi with phase 1.
 // reduce_stream / reduce_event (sub-shard passes): the partial-row reduction runs on reduce_stream after
-// reduce_event (recorded on `stream`); the caller joins it before using `packed`.
+// reduce_event (recorded on `stream`); the caller joins it before using `packed`.  psi1_grid_cap > 0:
+// the psi1 kernel runs on at most that many CTAs (an SM left to a concurrent coordinator kernel); the
+// partial-row layout stays the one of num_sms (the rows of absent CTAs stay zero).
 int psi_backward(const PsiConst& P, const BwdConst& B, double* part, double* packed, int num_sms, void* stream,
                  LaunchGeom* geom, void* ev_begin = nullptr, void* ev_end = nullptr, int phase = 0,
-                 void* reduce_stream = nullptr, void* reduce_event = nullptr);
+                 void* reduce_stream = nullptr, void* reduce_event = nullptr, int psi1_grid_cap = 0);
 // true when psi_backward can run in two phases for P (the row-tile path)
 bool psi_backward_phased(const PsiConst& P);
 // Where the forward left the region the backward reads (BwdConst::fwd_rt), and the per-pair sums

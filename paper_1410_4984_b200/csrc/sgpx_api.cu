@@ -489,6 +489,16 @@ void plan_subs(sgpx_engine* e) {
   if (!e->copy) CUDA_OK(cudaStreamCreateWithFlags(&e->copy, cudaStreamNonBlocking));
 }
 
+bool is_pinned(const void* ptr) {  // page-locked host memory (copies from it can be graph-captured)
+  if (!ptr) return true;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 // copy stream: mu / S of every sub-shard (the forward of sub-shard j waits for ev_in[j]); issued by
 // broadcast() as soon as it has the host views, so the transfer overlaps the caller's own work
 void enqueue_uploads(sgpx_engine* e) {
@@ -706,7 +716,11 @@ void engine_grad_pass(sgpx_engine* e) {
     // stream's coordinator kernel occupies, then d Phi is joined and the psi2 kernels run
     bool phased = e->split_join;
     for (auto& sub : e->subs) phased = phased && psi_backward_phased(sub.P);
-    const int nsm = phased ? std::max(1, ctx->num_sms - 1) : ctx->num_sms;
+    if (const char* v = getenv("SGPX_PHASED"); v && atoi(v) == 0) phased = false;  // A/B
+    // the psi1 kernels of the phased pass leave one SM to the side stream's coordinator kernel; every
+    // layout (partial rows, the forward's regions) stays the one of the full SM count
+    const int nsm = ctx->num_sms;
+    const int psi1_cap = phased ? std::max(1, ctx->num_sms - 1) : 0;
     if (!phased) join();
     int64_t boff = 0;
     for (auto& sub : e->subs) {
@@ -740,7 +754,8 @@ void engine_grad_pass(sgpx_engine* e) {
     const bool stream_out = e->has_gout && e->latent;
     const float *rt_pre0 = nullptr, *rt_ys0 = nullptr;
     bool prepared = false;
-    if (phased) {  // the pair operand of the psi2 backward right after U, on the coordinator's side stream
+    const char* prep_env = getenv("SGPX_RT_PREP");  // A/B
+    if (phased && !(prep_env && atoi(prep_env) == 0)) {  // the psi2 backward's pair operand right after U, on the side stream
       const auto& s0 = e->subs[0];
       if (rt_bwd_prepare(s0.P, e->u.get<float>(), bwd_rt_region(s0.P, e->bpart.get<double>() + s0.boff, nsm), nsm,
                          e->side, &rt_pre0, &rt_ys0))
@@ -795,7 +810,7 @@ void engine_grad_pass(sgpx_engine* e) {
       for (int j = 0; j < kp; ++j) {
         auto& sub = e->subs[j];
         if (psi_backward(sub.P, bconst(sub, j), e->bpart.get<double>() + sub.boff, out_of(j), nsm, ctx->stream, &e->gb,
-                         j == 0 ? e->ev[6] : nullptr, nullptr, 1))
+                         j == 0 ? e->ev[6] : nullptr, nullptr, 1, nullptr, nullptr, psi1_cap))
           throw CudaError(std::string("psi backward launch: ") + cudaGetErrorString(cudaGetLastError()));
       }
       join();
@@ -1505,7 +1520,8 @@ int sgpx_engine_broadcast(sgpx_engine* e, const sgpx_kernel_spec* kernel, double
     if (e->dev_coord) dc_setup(e);  // per-broadcast half of the coordinator (Kmm, its factor, inverse)
     e->has_params = true;
     e->coordinated = false;
-    if (e->pending_upload && !(e->use_graph && e->dev_coord && e->ctx->stream != nullptr)) {
+    if (e->pending_upload && !(e->use_graph && e->dev_coord && e->ctx->stream != nullptr && is_pinned(mu.data) &&
+                               is_pinned(s.data))) {
       // host mu / S: the transfer starts now, under the caller's work until evaluate (after the Z upload
       // above: copies in one direction share a copy engine, so a small copy queued behind these would wait
       // for all of them); the stats pass re-plans the same sub-shards with this broadcast's constants
@@ -1561,8 +1577,12 @@ int sgpx_engine_evaluate(sgpx_engine* e, int with_grads, sgpx_eval_result* out) 
     // (the legacy default stream cannot be captured)
     // (the host-buffer path too: the sub-shard uploads and read-backs are captured as copy nodes, the
     // host views and output buffers are part of the key)
-    const bool graphable = e->use_graph && e->dev_coord && !e->uploads_enqueued && e->in.n > 0 && e->has_data &&
-                           e->has_params && e->ctx->stream != nullptr;
+    // (copies from pageable host memory cannot be captured: the host-buffer path is replayed only when
+    // every host view is page-locked)
+    const bool host_pinned = (!e->pending_upload || (is_pinned(e->h_mu.data) && is_pinned(e->h_s.data))) &&
+                             (!(e->has_gout && e->latent) || (is_pinned(e->g_mu.data) && is_pinned(e->g_s.data)));
+    const bool graphable = e->use_graph && e->dev_coord && !e->uploads_enqueued && host_pinned && e->in.n > 0 &&
+                           e->has_data && e->has_params && e->ctx->stream != nullptr;
     if (graphable) {
       const bool host_io = e->pending_upload || (e->has_gout && e->latent);
       std::vector<unsigned char> key(sizeof(PsiConst) + sizeof(DcArgs) + 4 * sizeof(int) + 4 * sizeof(sgpx_cmat));
