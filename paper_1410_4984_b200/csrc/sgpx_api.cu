@@ -443,8 +443,12 @@ std::vector<double> sub_weights(int64_t n, bool transfers) {
     for (double x : w) ok = ok && x > 0.0;
     if (ok) return w;
   }
-  if (n >= 1000000) return {1.0, 1.5, 2.0, 2.0, 2.0, 1.5, 1.0};  // measured best at C3, graph-replayed (tools/e2e_sweep.py)
-  if (n >= 500000) return {1.0, 1.0};
+  // measured best end to end at the C3 shape (Q=10 D=50 M=100) per row count, graph-replayed
+  // (tools/e2e_sweep.py, profiles/r02/subs_sweep.txt): 1M / 500k / 250k / 125k+100k rows
+  if (n >= 1000000) return {1.0, 1.5, 2.0, 2.0, 2.0, 1.5, 1.0};
+  if (n >= 400000) return {1.0, 1.5, 2.0, 2.0, 1.5, 1.0};
+  if (n >= 200000) return {1.0, 1.5, 2.0, 1.5, 1.0};
+  if (n >= 80000) return {1.0, 1.0};
   return {1.0};
 }
 

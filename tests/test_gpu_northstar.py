@@ -418,7 +418,7 @@ def test_end_to_end_graph_replay(sgp, pinned):
 
     from paper_1410_4984_b200 import synthetic
 
-    n, q, d, m = 600_000, 10, 8, 50  # >= 500k rows: two sub-shards
+    n, q, d, m = 600_000, 10, 8, 50  # >= 400k rows: six weighted sub-shards with host I/O
     w = synthetic.make(True, n, q, d, m, seed=41, device="cuda")
     stream = torch.cuda.Stream()
     ctx = sgp.Context(0)

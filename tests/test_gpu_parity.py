@@ -312,7 +312,7 @@ def test_engine_subshard_pipeline(sgp, spread, q):
     rounding instead of bitwise."""
     import torch
 
-    n, d, m = 600_000, 3, 24  # >= 500k rows: two sub-shards
+    n, d, m = 600_000, 3, 24  # >= 400k rows: six weighted sub-shards with host I/O
     mu, s, y, z, var, ls = problem(9, n, q, d, m)
     mu = mu * spread
     z = z * spread

@@ -1,7 +1,8 @@
 """End-to-end C3 evaluation time (pinned host mu/S uploaded by broadcast(), d_mu/d_S streamed back)
 for a list of sub-shard plans (SGPX_SUBS) and coordinator placements (SGPX_DEVICE_COORD).
 
-  python tools/e2e_sweep.py [steps] "plan1" "plan2" ...     plan = "<subs>|<devcoord 0/1>[|NAME=v,...]", e.g. "1,2,2|0"
+  [E2E_SHAPE=n,q,d,m] python tools/e2e_sweep.py [steps] "plan1" "plan2" ...
+  plan = "<subs>|<devcoord 0/1>[|NAME=v,...]", e.g. "1,2,2|0"
 """
 import os
 import sys
@@ -16,7 +17,7 @@ from paper_1410_4984_b200 import sgp, synthetic  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
 plans = sys.argv[2:] or ["|0", "|1"]
-n, q, d, m = 1_000_000, 10, 50, 100
+n, q, d, m = (int(x) for x in os.environ.get("E2E_SHAPE", "1000000,10,50,100").split(","))  # C3 by default
 w = synthetic.make(True, n, q, d, m, seed=0, device="cuda")
 mu_p = torch.empty(q, n, dtype=torch.float64, pin_memory=True)
 s_p = torch.empty(q, n, dtype=torch.float64, pin_memory=True)
