@@ -62,8 +62,8 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
 }
 
 // ---------------------------------------------------------------------------------------------
-// forward: warp-specialised.  Producer warps (kFwdProd) copy each chunk's raw fp64 rows one chunk
-// ahead (cp.async), convert them into a stage (per-datapoint mu - c, d1, 1/2 log2(d1 l^2); the Y
+// forward: warp-specialised.  Producer warps (kFwdProd) copy each chunk's raw fp64 rows kRaw - 1 chunks
+// ahead (2D TMA boxes, else 8-byte cp.async), convert them into a stage (per-datapoint mu - c, d1, 1/2 log2(d1 l^2); the Y
 // chunk as tf32 pieces), and arrive on stage_full; consumer warps (kFwdCons) build the G^T tile of
 // the chunk from the stage, and one of them issues the MMAs, whose commit (mma_done) frees the stage
 // and the G buffer.  Two stages, two G buffers, two TMEM accumulators.
