@@ -278,20 +278,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       float* gb = gsm + st * 2 * 128 * kFwdK;
       {
         float b[8], e[2][8];
-        {  // b1 = log2 var + sum_q 1/2 log2(d1 l^2), q ascending (rows past N: -inf)
+        {  // b1 = log2 var + sum_q 1/2 log2(d1 l^2) (rows past N: -inf), formed once per warp: every lane
+           // of a warp shares the 8 datapoints of gj; lane = (datapoint lane & 7, latent dims q = lane >> 3
+           // mod 4), two butterfly steps, then the 8 sums are broadcast
           const int64_t n0 = chunk_of(l) * kFwdK;
+          float bs = 0.f;
 #pragma unroll
-          for (int u = 0; u < 8; ++u) b[u] = P.log2_var;
+          for (int q = lane >> 3; q < Q; q += 4) bs += pd[(2 * Q + q) * kFwdK + 8 * gj + (lane & 7)];
+          bs += __shfl_xor_sync(0xffffffffu, bs, 8);
+          bs += __shfl_xor_sync(0xffffffffu, bs, 16);
 #pragma unroll
-          for (int q = 0; q < Q; ++q) {
-            const float4 c0 = *reinterpret_cast<const float4*>(pd + (2 * Q + q) * kFwdK + 8 * gj);
-            const float4 c4 = *reinterpret_cast<const float4*>(pd + (2 * Q + q) * kFwdK + 8 * gj + 4);
-            b[0] += c0.x, b[1] += c0.y, b[2] += c0.z, b[3] += c0.w, b[4] += c4.x, b[5] += c4.y, b[6] += c4.z,
-                b[7] += c4.w;
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
+          for (int u = 0; u < 8; ++u) {
+            b[u] = P.log2_var + __shfl_sync(0xffffffffu, bs, u);
             if (n0 + 8 * gj + u >= P.n) b[u] = -CUDART_INF_F;
+          }
         }
         float2 e2[2][4];
 #pragma unroll
